@@ -1,0 +1,132 @@
+"""Oracle backpropagation (test infrastructure only; see oracle/__init__.py).
+
+Plain definition of the adjoint gradient:
+  A_N = M/h^2 + Hess E_int(x_{i+1}) = A - dA
+  dA  = sum_e w_e G_e^T dz_e*/dx
+  u   = A_N^{-1} b,   b = dL/dx_{i+1} (+ dL/dv_{i+1}/h)           (eq:pre_adjoint)
+  dL/dx_i = (1/h^2)(dy/dx_i)^T M u  (+ direct -dL/dv_{i+1}/h)
+The oracle assembles A_N explicitly from the 9x9 projection Jacobians and solves
+it directly (scipy sparse LU) — the BASELINE.json "direct dense solve of the
+linearized adjoint" check, done sparsely.  The paper's fixed point / quasi-Newton
+iteration converges to the same u; the GPU path runs that iteration.
+
+Constrained DoFs (Dirichlet, and in contact steps the pinned normal DoFs of the
+frozen active set, "the same modified matrix") carry u = 0.
+Parameter gradients: implicit-function differentiation of eq:time_integration:
+  dL/dw  = -sum_e sum_q V <G_q u_e, F_q - R_q>        (w = E/(1+nu), reading §8c.2)
+  dL/dr  = w_m sum_q V n_hat_q^T (G_mq u_e)            (muscle)
+  dL/df_ext(step) = u.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from . import energy, fem
+
+
+def hessian_blocks(scene, x, w, act=None):
+    """Per-element 24x24 blocks of sum_q V [w G^T (I - dR/dF) G + w_m G_m^T (I - dp/dFm) G_m]."""
+    F = fem.deformation_gradients(x, scene.hex8, scene.dx)
+    J, R = energy.polar_jacobian(F)                                 # [m,8,9,9]
+    G = fem.G_matrices(scene.dx)
+    I9 = np.eye(9)
+    H = w * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - J, G)
+    if scene.muscle:
+        Fm = F @ np.asarray(scene.fiber)
+        r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
+        Jm, p, n_hat = energy.muscle_jacobian(Fm, r, scene.fiber)
+        Gm = fem.Gm_matrices(scene.dx, scene.fiber)
+        H = H + scene.w_muscle * scene.V * np.einsum("qka,mqkl,qlb->mab", Gm, np.eye(3) - Jm, Gm)
+    return H
+
+
+def assemble_AN(scene, x, w, act=None):
+    """A_N = M/h^2 + Hess E_int."""
+    K = fem.assemble_blocks(hessian_blocks(scene, x, w, act), scene.hex8, scene.n)
+    return (sp.diags(scene.mass / scene.h ** 2) + K).tocsr()
+
+
+def assemble_dA(scene, x, w, act=None):
+    """dA = A - A_N = sum w G^T dz*/dx G."""
+    return (scene.A(w) - assemble_AN(scene, x, w, act)).tocsr()
+
+
+def solve_adjoint(scene, x, w, act, b, cons_mask):
+    AN = assemble_AN(scene, x, w, act)
+    fr = ~cons_mask
+    u = np.zeros_like(b)
+    u[fr] = spla.spsolve(AN[fr][:, fr].tocsc(), b[fr])
+    return u
+
+
+def param_terms(scene, x, u, act=None):
+    """(dL/dw, dL/dr[m]) contributions of one step (chain rule)."""
+    F = fem.deformation_gradients(x, scene.hex8, scene.dx)
+    R, S, V, s = energy.polar_svd(F)
+    Gu = fem.deformation_gradients(u, scene.hex8, scene.dx)         # G_q u_e
+    dw = -scene.V * np.sum(Gu * (F - R))
+    dr = None
+    if scene.muscle:
+        Fm = F @ np.asarray(scene.fiber)
+        r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
+        p, n_hat, nrm = energy.muscle_project(Fm, r, scene.fiber)
+        Gmu = Gu @ np.asarray(scene.fiber)
+        dr = scene.w_muscle * scene.V * np.sum(n_hat * Gmu, axis=(-1, -2))
+    return dw, dr
+
+
+def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None):
+    """Reverse pass over a trajectory from oracle.pd.forward.
+
+    Returns dict(dq0, dv0, dfext (summed over steps), dE, dnu, dw, dact[T,m] or None)."""
+    h = scene.h
+    w = scene.w_of(youngs)
+    T = traj["q"].shape[0] - 1
+    ax = dL_dqT.copy()
+    av = dL_dvT.copy()
+    base = ~scene.free
+    cand = scene.normal_dofs(scene.contact_nodes) if len(scene.contact_nodes) else np.zeros(0, int)
+    dfext = np.zeros(scene.N)
+    dw_tot = 0.0
+    dact = np.zeros((T, scene.m)) if scene.muscle else None
+    for i in range(T - 1, -1, -1):
+        x1 = traj["q"][i + 1]
+        cons = base.copy()
+        if len(cand):
+            cons[cand[traj["active"][i]]] = True
+        b = ax + av / h                                    # v_{i+1} = (x_{i+1} - x_i)/h
+        b[cons] = 0.0
+        a_i = None if act is None else act[i]
+        u = solve_adjoint(scene, x1, w, a_i, b, cons)
+        dw, dr = param_terms(scene, x1, u, a_i)
+        dw_tot += dw
+        if dr is not None:
+            dact[i] = dr
+        dfext += u
+        ax = scene.mass / h ** 2 * u - av / h              # (1/h^2)(dy/dx_i)^T M u - a_v/h
+        av = scene.mass / h * u                            # dy/dv_i = h I
+        ax[base] = 0.0
+        av[base] = 0.0
+    dfext[base] = 0.0
+    nu = scene.poisson
+    return dict(dq0=ax, dv0=av, dfext=dfext, dw=dw_tot,
+                dE=dw_tot / (1.0 + nu), dnu=-dw_tot * youngs / (1.0 + nu) ** 2, dact=dact)
+
+
+def loss_and_grad(inp, b, q, v):
+    """Loss of SURVEY §8c.13 for sim b and its terminal gradients (dL/dq_T, dL/dv_T)."""
+    cfg = inp["cfg"]
+    if cfg.loss == "linear_q":
+        return float(inp["c_q"][b] @ q), inp["c_q"][b].copy(), np.zeros_like(v)
+    if cfg.loss == "linear_qv":
+        return (float(inp["c_q"][b] @ q + inp["c_v"][b] @ v), inp["c_q"][b].copy(),
+                inp["c_v"][b].copy())
+    if cfg.loss == "tip":
+        idx = (3 * inp["tip_nodes"][:, None] + np.arange(3)[None, :]).ravel()
+        diff = q[idx] - inp["tip_target"][b]
+        g = np.zeros_like(q)
+        g[idx] = 2.0 * diff
+        return float(diff @ diff), g, np.zeros_like(v)
+    raise ValueError(cfg.loss)

@@ -1,0 +1,284 @@
+"""Oracle PD forward simulation (test infrastructure only; see oracle/__init__.py).
+
+Implements, per simulation and per time step:
+  y = x_i + h v_i + h^2 M^{-1} f_ext
+  g(x) = 1/(2h^2) ||M^{1/2}(x - y)||^2 + E_int(x)             (P:150 eq:opt)
+  E_int = sum_e sum_q V_q [w/2 ||F - R||^2 + w_m/2 ||Fm - p||^2]
+  local step  z* = Proj_M(G x)                                (P:187 eq:pd_proj)
+  global step A x = (1/h^2) M y + sum_e w_e G_e^T z_e*         (P:197 eq:pd_global, with M:
+                                                               reading §8c.7)
+  contact: Alg. 1 with frictionless normal pins at the plane z = 0
+           (readings §8c.10, §8c.11), constrained solve eq:dirichlet/eq:complement
+            with the coupling term kept (reading §8c.9).
+  v_{i+1} = (x_{i+1} - x_i)/h                                  (eq:implicit_x)
+
+The constrained global solve is the plain definition (a direct sparse solve of
+the reduced system A_{CbarCbar} x_Cbar = d_Cbar - A_{Cbar C} xbar); the paper's
+Woodbury route (Alg. 2) reaches the same x exactly and is checked against this
+in tests.  c1 is an iteration (exactly `fixed_iter` PD iterations from x^0 = x_i,
+reading §8c.6); every other config is the minimiser of g reached by plain PD to
+a relative residual ||grad g_free|| / ||(M/h^2) y_free|| <= tol (reading §8c.8).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from . import energy, fem
+
+EPS_PHI_REL = 1e-6      # predictor penetration threshold eps_phi = 1e-6 dx (reading §8c.11)
+MAX_OUTER = 10          # Alg. 1 "maximum iteration" (reading §8c.11)
+
+
+@dataclasses.dataclass
+class Scene:
+    rest: np.ndarray
+    hex8: np.ndarray
+    dx: float
+    density: float
+    h: float
+    youngs: float
+    poisson: float
+    gravity: np.ndarray
+    fixed_dofs: np.ndarray
+    contact_nodes: np.ndarray
+    muscle: bool = False
+    fiber: tuple = (1.0, 0.0, 0.0)
+
+    def __post_init__(self):
+        self.n = self.rest.shape[0]
+        self.N = 3 * self.n
+        self.m = self.hex8.shape[0]
+        self.mass = fem.lumped_mass(self.hex8, self.n, self.dx, self.density)
+        self.V = self.dx ** 3 / 8.0
+        self.free = np.ones(self.N, bool)
+        self.free[self.fixed_dofs] = False
+        self.Kcorot = fem.assemble_blocks(fem.element_stiffness(self.dx, 1.0), self.hex8, self.n)
+        self.Kmus = (fem.assemble_blocks(fem.element_stiffness(self.dx, 0.0, 1.0, self.fiber),
+                                         self.hex8, self.n) if self.muscle else None)
+        self._factors = {}
+
+    # ---- material (reading §8c.2 / §8c.3) ----
+    def w_of(self, youngs):
+        """Corotated PD weight w = 2 mu = E/(1+nu) (SPEC lame_weights; reading §8c.2)."""
+        return youngs / (1.0 + self.poisson)
+
+    @property
+    def w_muscle(self):
+        """w_m = 2 mu at the nominal material, constant (reading §8c.3)."""
+        return self.youngs / (1.0 + self.poisson) if self.muscle else 0.0
+
+    def A(self, w):
+        """A = M/h^2 + sum w G^T G (+ w_m G_m^T G_m)."""
+        A = sp.diags(self.mass / self.h ** 2) + w * self.Kcorot
+        if self.muscle:
+            A = A + self.w_muscle * self.Kmus
+        return A.tocsr()
+
+    def factor(self, w, cons_mask):
+        """Sparse LU of A restricted to unconstrained DoFs (library solve step)."""
+        key = (float(w), cons_mask.tobytes())
+        if key not in self._factors:
+            A = self.A(w)
+            fr = ~cons_mask
+            Aff = A[fr][:, fr].tocsc()
+            self._factors = {k: v for k, v in list(self._factors.items())[-4:]}
+            self._factors[key] = (spla.splu(Aff), A[fr][:, cons_mask].tocsr())
+        return self._factors[key]
+
+    # ---- per-step quantities ----
+    def y(self, x, v, f_ext):
+        """y = x + h v + h^2 M^{-1} f_ext, gravity included in f_ext."""
+        g = np.tile(self.gravity, self.n)
+        return x + self.h * v + self.h ** 2 * (g + f_ext / self.mass)
+
+    def local_step(self, x, act=None):
+        """z* = Proj_M(G x) per quad point: R (SO(3)) and p (muscle sphere)."""
+        F = fem.deformation_gradients(x, self.hex8, self.dx)     # [m,8,3,3]
+        R, S, V, s = energy.polar_svd(F)
+        out = dict(F=F, R=R)
+        if self.muscle:
+            Fm = F @ np.asarray(self.fiber)
+            r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
+            p, n_hat, nrm = energy.muscle_project(Fm, r, self.fiber)
+            out.update(Fm=Fm, p=p)
+        return out
+
+    def elastic_terms(self, z, w):
+        """Element sums: E_int and grad E_int = sum w V G^T (F - R) (+ muscle)."""
+        F, R = z["F"], z["R"]
+        D = F - R
+        E = 0.5 * w * self.V * np.sum(D * D)
+        P = w * self.V * D
+        if self.muscle:
+            Dm = z["Fm"] - z["p"]
+            E += 0.5 * self.w_muscle * self.V * np.sum(Dm * Dm)
+            P = P + self.w_muscle * self.V * Dm[..., :, None] * np.asarray(self.fiber)[None, None, None, :]
+        grad = fem.scatter_element_forces(P, self.hex8, self.dx, self.n)
+        return E, grad
+
+    def rhs_d(self, y, z, w):
+        """d = (1/h^2) M y + sum_e w_e G_e^T z_e*  (eq:pd_global, reading §8c.7)."""
+        P = w * self.V * z["R"]
+        if self.muscle:
+            P = P + self.w_muscle * self.V * z["p"][..., :, None] * np.asarray(self.fiber)[None, None, None, :]
+        return self.mass / self.h ** 2 * y + fem.scatter_element_forces(P, self.hex8, self.dx, self.n)
+
+    def objective(self, x, y, w, act=None):
+        """g(x) (eq:opt) and grad g(x) = M/h^2 (x - y) + grad E_int (eq:time_integration)."""
+        z = self.local_step(x, act)
+        E, gE = self.elastic_terms(z, w)
+        dxy = x - y
+        g = 0.5 / self.h ** 2 * np.dot(self.mass * dxy, dxy) + E
+        return g, self.mass / self.h ** 2 * dxy + gE
+
+    def rel_residual(self, x, y, w, act, cons_mask):
+        _, gg = self.objective(x, y, w, act)
+        fr = ~cons_mask
+        return np.linalg.norm(gg[fr]) / np.linalg.norm((self.mass / self.h ** 2 * y)[fr]), gg
+
+    def pd_iteration(self, x, y, w, act, cons_mask):
+        """One local-global iteration with DoFs in cons_mask held at their values in x."""
+        z = self.local_step(x, act)
+        d = self.rhs_d(y, z, w)
+        lu, Afc = self.factor(w, cons_mask)
+        fr = ~cons_mask
+        xn = x.copy()
+        xn[fr] = lu.solve(d[fr] - Afc @ x[cons_mask])
+        return xn
+
+    def pd_solve(self, x0, y, w, act, cons_mask, tol, fixed_iter=0, max_iter=20000):
+        """Literal PD local-global iterations from x^0 to tol, or exactly
+        fixed_iter iterations (c1).  Returns (x, iters, res).
+
+        Stagnation exit (reading §8c.8): stop if the residual has not halved in 200 its."""
+        x = x0.copy()
+        if fixed_iter:
+            for _ in range(fixed_iter):
+                x = self.pd_iteration(x, y, w, act, cons_mask)
+            res, _ = self.rel_residual(x, y, w, act, cons_mask)
+            return x, fixed_iter, res
+        hist = []
+        for it in range(max_iter + 1):
+            res, _ = self.rel_residual(x, y, w, act, cons_mask)
+            hist.append(res)
+            if res <= tol:
+                return x, it, res
+            if len(hist) > 200 and res > 0.5 * hist[-201]:
+                return x, it, res
+            x = self.pd_iteration(x, y, w, act, cons_mask)
+        return x, max_iter, res
+
+    def newton_solve(self, x0, y, w, act, cons_mask, tol, max_iter=200):
+        """Minimiser of g (eq:opt) with DoFs in cons_mask held, by Newton's method with
+        A_N = M/h^2 + Hess E_int and backtracking line search; falls back to
+        the PD direction -A^{-1} grad g when the Newton direction is not a descent
+        direction.  Reaches the same point PD converges to (tests check this)."""
+        from . import adjoint
+        x = x0.copy()
+        fr = ~cons_mask
+        scale = np.linalg.norm((self.mass / self.h ** 2 * y)[fr])
+        g, gg = self.objective(x, y, w, act)
+        res = np.linalg.norm(gg[fr]) / scale
+        for it in range(max_iter + 1):
+            if res <= tol:
+                return x, it, res
+            AN = adjoint.assemble_AN(self, x, w, act)
+            d = np.zeros_like(x)
+            try:
+                d[fr] = -spla.spsolve(AN[fr][:, fr].tocsc(), gg[fr])
+                ok = np.all(np.isfinite(d)) and gg[fr] @ d[fr] < 0
+            except Exception:
+                ok = False
+            if not ok:
+                lu, _ = self.factor(w, cons_mask)
+                d[fr] = -lu.solve(gg[fr])
+            slope = gg[fr] @ d[fr]
+            t = 1.0
+            for _ in range(60):
+                gn, ggn = self.objective(x + t * d, y, w, act)
+                resn = np.linalg.norm(ggn[fr]) / scale
+                # Armijo on g; near the minimiser g stops resolving the decrease in
+                # fp64, so a decrease of ||grad g|| is accepted there instead.
+                if gn <= g + 1e-4 * t * slope or (res < 1e-6 and resn < res):
+                    break
+                t *= 0.5
+            x = x + t * d
+            g, gg, res = gn, ggn, resn
+        return x, max_iter, res
+
+    def solve_step(self, x0, y, w, act, cons_mask, tol, fixed_iter=0, method="newton"):
+        if fixed_iter or method == "pd":
+            return self.pd_solve(x0, y, w, act, cons_mask, tol, fixed_iter)
+        return self.newton_solve(x0, y, w, act, cons_mask, tol)
+
+    # ---- contact (Alg. 1, frictionless normal pins on z = 0) ----
+    def normal_dofs(self, nodes):
+        return 3 * np.asarray(nodes, np.int64) + 2
+
+    def step(self, x, v, f_ext, w, act, tol, fixed_iter=0, method="newton"):
+        """One implicit step (Alg. 1 when contact candidates exist).
+
+        Returns dict(x, v, active[|V|] bool, iters, outer, res, flag)."""
+        y = self.y(x, v, f_ext)
+        base = ~self.free
+        if len(self.contact_nodes) == 0:
+            xn, it, res = self.solve_step(x, y, w, act, base, tol, fixed_iter, method)
+            return dict(x=xn, v=(xn - x) / self.h, active=np.zeros(0, bool), iters=it,
+                        outer=0, res=res, flag=bool(res > tol and not fixed_iter), y=y)
+        cand = self.normal_dofs(self.contact_nodes)
+        eps_phi = EPS_PHI_REL * self.dx
+        active = np.zeros(len(cand), bool)                     # V_i = empty
+        total_it = 0
+        flag = True
+        margins = []
+        for outer in range(1, MAX_OUTER + 1):
+            cons = base.copy()
+            cons[cand[active]] = True
+            x0 = x.copy()                                       # x_{i+1} = x_i
+            x0[cand[active]] = 0.0                               # pinned at the plane
+            xn, it, res = self.solve_step(x0, y, w, act, cons, tol, fixed_iter, method)
+            total_it += it
+            _, gg = self.objective(xn, y, w, act)
+            lam = np.where(active, gg[cand], 0.0)              # lambda_j = 0 if j not in V_i
+            phi = xn[cand]                                      # phi = z for the plane z = 0
+            new = (phi < -eps_phi) | (lam > 0)
+            margins.append((np.min(np.abs(phi + eps_phi)), np.min(np.abs(lam[active])) if active.any() else np.inf))
+            if np.array_equal(new, active):
+                flag = False
+                break
+            if outer == MAX_OUTER:
+                break
+            active = new
+        return dict(x=xn, v=(xn - x) / self.h, active=active, iters=total_it, outer=outer,
+                    res=res, flag=flag or bool(res > tol and not fixed_iter), y=y, lam=lam,
+                    margins=margins)
+
+
+def scene_from_inputs(inp, youngs=None):
+    cfg = inp["cfg"]
+    return Scene(rest=inp["rest"], hex8=inp["hex8"], dx=cfg.dx, density=cfg.density, h=cfg.h,
+                 youngs=cfg.youngs if youngs is None else youngs, poisson=cfg.poisson,
+                 gravity=np.asarray(cfg.gravity, float), fixed_dofs=inp["fixed_dofs"],
+                 contact_nodes=inp["contact_nodes"], muscle=cfg.muscle)
+
+
+def forward(scene, q0, v0, f_ext, youngs, act=None, steps=1, tol=1e-12, fixed_iter=0,
+            method="newton"):
+    """Trajectory of one simulation: returns dict(q[T+1,3n], v[T+1,3n], active[T,|V|], stats)."""
+    w = scene.w_of(youngs)
+    q = [q0.copy()]
+    vv = [v0.copy()]
+    actives, stats = [], []
+    for i in range(steps):
+        a = None if act is None else act[i]
+        r = scene.step(q[-1], vv[-1], f_ext, w, a, tol, fixed_iter, method)
+        q.append(r["x"])
+        vv.append(r["v"])
+        actives.append(r["active"])
+        stats.append({k: r[k] for k in ("iters", "outer", "res", "flag")})
+    return dict(q=np.array(q), v=np.array(vv), active=np.array(actives), stats=stats)

@@ -1,0 +1,107 @@
+"""Pins for oracle/adjoint.py: Hessian, direct adjoint, and full-trajectory gradients vs FD."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from oracle import adjoint, pd
+from pd_inputs import get_config, make_inputs
+
+
+def _scene(name, **kw):
+    cfg = get_config(name, **kw)
+    inp = make_inputs(cfg)
+    return pd.scene_from_inputs(inp), inp
+
+
+def test_AN_is_jacobian_of_grad_g():
+    # A_N = M/h^2 + Hess E_int: central FD of grad g along random directions.
+    for name in ("c1", "c5s"):
+        sc, inp = _scene(name)
+        rng = np.random.default_rng(0)
+        x = inp["q0"][0] + 5e-4 * rng.standard_normal(sc.N)
+        act = None if inp["act"] is None else inp["act"][0, 0]
+        y = sc.y(x, np.zeros(sc.N), np.zeros(sc.N))
+        w = sc.w_of(1e5)
+        AN = adjoint.assemble_AN(sc, x, w, act)
+        d = rng.standard_normal(sc.N)
+        eps = 1e-6
+        _, gp = sc.objective(x + eps * d, y, w, act)
+        _, gm = sc.objective(x - eps * d, y, w, act)
+        fd = (gp - gm) / (2 * eps)
+        np.testing.assert_allclose(AN @ d, fd, rtol=0, atol=1e-6 * np.abs(fd).max())
+        np.testing.assert_allclose(AN.toarray(), AN.toarray().T, atol=1e-8 * abs(AN).max())
+
+
+def test_dA_split_and_spectral_radius_at_rest():
+    # A_N = A - dA; at rest R = I and dR/dF maps skew->skew, sym->0, so
+    # dA = sum w G^T P_skew G and rho(A^{-1} dA) < 1 (the fixed point converges).
+    sc, inp = _scene("c1")
+    x = inp["rest"].ravel()
+    w = sc.w_of(1e5)
+    dA = adjoint.assemble_dA(sc, x, w).toarray()
+    A = sc.A(w).toarray()
+    fr = sc.free
+    ev = np.linalg.eigvals(np.linalg.solve(A[fr][:, fr], dA[fr][:, fr]))
+    rho = np.abs(ev).max()
+    assert 0.3 < rho < 1.0
+
+
+def test_zero_stiffness_closed_form():
+    # SPEC backprop_step example: pure mass system, L = c^T x_1 ->
+    # dL/dx_0 = c, dL/dv_0 = h c, dL/df_ext = h^2 M^{-1} c.
+    sc, inp = _scene("c1", dirichlet="none")
+    c = np.random.default_rng(1).standard_normal(sc.N)
+    tr = pd.forward(sc, inp["q0"][0], inp["v0"][0], np.zeros(sc.N), 0.0, steps=1, tol=1e-14)
+    g = adjoint.backward(sc, tr, 0.0, c, np.zeros(sc.N))
+    np.testing.assert_allclose(g["dq0"], c, rtol=1e-12)
+    np.testing.assert_allclose(g["dv0"], sc.h * c, rtol=1e-12)
+    np.testing.assert_allclose(g["dfext"], sc.h ** 2 / sc.mass * c, rtol=1e-12)
+
+
+def _fd_check(name, steps, params, rel, kw=None):
+    sc, inp = _scene(name, **(kw or {}))
+    b = 0
+    act = None if inp["act"] is None else inp["act"][b, :steps].copy()
+    base = dict(q0=inp["q0"][b].copy(), v0=inp["v0"][b].copy(), f=inp["f_ext"][b].copy(),
+                E=float(inp["youngs"][b]), act=act)
+
+    def run(p, sc=sc):
+        s = sc if p.get("nu") is None else dataclasses.replace(sc, poisson=p["nu"])
+        tr = pd.forward(s, p["q0"], p["v0"], p["f"], p["E"], p["act"], steps=steps, tol=1e-14)
+        L, gq, gv = adjoint.loss_and_grad(inp, b, tr["q"][-1], tr["v"][-1])
+        return L, tr, gq, gv, s
+
+    L, tr, gq, gv, s = run(base)
+    g = adjoint.backward(s, tr, base["E"], gq, gv, act)
+    rng = np.random.default_rng(7)
+    for key in params:
+        if key in ("q0", "v0", "f"):
+            d = rng.standard_normal(sc.N)
+            d[~sc.free] = 0
+            eps = {"q0": 1e-6, "v0": 1e-5, "f": 1e-5}[key]
+            an = {"q0": g["dq0"], "v0": g["dv0"], "f": g["dfext"]}[key] @ d
+        elif key == "E":
+            d, eps, an = 1.0, 10.0, g["dE"]
+        elif key == "nu":
+            d, eps, an = 1.0, 1e-5, g["dnu"]
+        elif key == "act":
+            d = rng.standard_normal(base["act"].shape)
+            eps, an = 1e-5, np.sum(g["dact"] * d)
+        pp, pm = dict(base), dict(base)
+        if key == "nu":
+            pp["nu"], pm["nu"] = sc.poisson + eps, sc.poisson - eps
+        else:
+            pp[key] = base[key] + eps * d
+            pm[key] = base[key] - eps * d
+        fd = (run(pp)[0] - run(pm)[0]) / (2 * eps)
+        assert abs(an - fd) <= rel * max(abs(fd), 1e-12), (key, an, fd)
+
+
+def test_gradients_vs_central_fd_cantilever():
+    # BASELINE.json self-check: central finite differences on tiny meshes, converged forwards.
+    _fd_check("c1", 3, ["q0", "v0", "f", "E", "nu"], 1e-5, kw=dict(loss="linear_qv"))
+
+
+def test_gradients_vs_central_fd_muscle():
+    _fd_check("c5s", 2, ["q0", "v0", "act", "E"], 1e-5, kw=dict(contact=False))
