@@ -1,0 +1,166 @@
+/*
+ * diffpd_b200.h — C-ABI of the B200-native DiffPD hot path (arXiv 2101.05917).
+ *
+ * One opaque handle per (mesh, material, h, Dirichlet set, contact set).  The
+ * library owns every device allocation it makes (factor, caches, workspaces,
+ * trajectory store); every array ARGUMENT is caller-owned.  Unless stated
+ * otherwise array arguments are fp64 DEVICE pointers (e.g. a contiguous torch
+ * CUDA tensor's data_ptr()) in the layout [B][3n], DoF index = 3*node + axis
+ * ("the floor(i/3) convention").  Mesh/material/option structs and
+ * their pointers are HOST memory.  Work is enqueued on `cuda_stream` (a
+ * cudaStream_t, NULL = legacy default stream); every call returns after the
+ * work completed (results are host-visible on return).  No allocation happens
+ * inside pd_forward / pd_backward.  A handle is not re-entrant; separate handles
+ * may be used concurrently from separate threads/streams.
+ *
+ * Errors: every entry point returns a pd_status; the message of the last
+ * failure is available from pd_last_error(handle) (or pd_last_error(NULL) for
+ * a failed pd_create).  Non-convergence of an iteration is NOT an error: the
+ * call returns PD_OK with the per-step flags/counters in pd_stats.
+ */
+#ifndef DIFFPD_B200_H
+#define DIFFPD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pd_sim pd_sim;
+
+typedef enum {
+  PD_OK = 0,
+  PD_ERR_INVALID_ARGUMENT = 1, /* bad sizes, non-voxel mesh, nu outside (-1, .5), h <= 0, ... */
+  PD_ERR_NUMERICAL = 2,        /* A not SPD at setup; singular contact capacitance matrix     */
+  PD_ERR_CUDA = 3,             /* a CUDA runtime call failed (message has the CUDA error)     */
+  PD_ERR_STATE = 4             /* e.g. pd_backward without a preceding pd_forward             */
+} pd_status;
+
+/* Hexahedral voxel mesh ("FEM-discretization", P:189 G_e).
+ * rest_xyz: host [n_nodes][3] rest positions (m).  hex8: host [n_elems][8]
+ * node indices, corner a = di + 2 dj + 4 dk (x-fastest).  Every element must be
+ * an axis-aligned cube of edge dx (checked; otherwise INVALID_ARGUMENT): all
+ * elements then share one constant G stencil (8-point Gauss). */
+typedef struct {
+  int32_t n_nodes, n_elems;
+  const double* rest_xyz;
+  const int32_t* hex8;
+  double dx;
+} pd_mesh;
+
+/* Material.  Corotated PD weight w = E/(1+nu) (= 2 mu, the
+ * reading of DESIGN.md §2.2).  muscle_w > 0 enables the muscle-fiber energy
+ * (w_m/2)||Fm - p||^2, p = r Fm/||Fm|| with the
+ * uniform unit fiber direction `fiber`; actuation r is given per (sim, step,
+ * element) to pd_forward.  gravity (m/s^2) enters f_ext as M g. */
+typedef struct {
+  double youngs, poisson, density;
+  double muscle_w;
+  double gravity[3];
+  double fiber[3];
+} pd_material;
+
+/* Solver options.  Tolerances are on the relative residual
+ * ||grad g(x)||_2 / ||(M/h^2) y||_2 over unconstrained DoFs (forward, P:527 and
+ * DESIGN.md §2.8) and ||A_N u - b|| / ||b|| (adjoint). */
+typedef struct {
+  double tol_fwd, tol_adj;
+  int32_t max_iter_fwd, max_iter_adj;
+  int32_t fixed_iter;     /* > 0: exactly this many plain local-global iterations per step
+                             from x^0 = x_i, no convergence test (config c1)               */
+  int32_t accel_fwd;      /* 0: plain PD x <- A^{-1} d(x); 1: L-BFGS with
+                             H0 = A^{-1} and line search (the quasi-Newton PD of P:79/P:254) */
+  int32_t accel_adj;      /* 0: fixed point u <- A^{-1}(b + dA u);
+                             1: its quasi-Newton acceleration, run as
+                             A-preconditioned CG — BFGS with exact line search on a(u)   */
+  int32_t check_every;    /* host polls convergence flags every k iterations (>= 1)        */
+  int32_t max_batch;      /* largest B passed to pd_forward                                */
+  int32_t max_steps;      /* largest `steps` passed to pd_forward (trajectory store size)  */
+  double youngs_ref;      /* Young's modulus of the ONE factorised A (0 = material.youngs).
+                             Sims with other E use the majorising step of DESIGN.md §2.12  */
+  /* Frictionless node-plane contact (Alg. 1):
+   * candidate nodes V (host, node indices), plane z = 0 with normal +z.        */
+  const int32_t* contact_nodes;
+  int32_t n_contact;
+  int32_t max_outer;      /* Alg. 1 "maximum iteration" (default 10)                     */
+  double eps_phi;         /* predictor penetration threshold (m), default 1e-6 dx          */
+} pd_options;
+
+/* Per-step statistics, caller-owned HOST arrays of length B*steps (index
+ * b*steps + i) or NULL each; filled by pd_forward / pd_backward. */
+typedef struct {
+  int32_t* iters_fwd;
+  int32_t* iters_adj;
+  int32_t* contact_outer;
+  double* final_res_fwd;
+  double* final_res_adj;
+  int32_t n_nonconverged; /* output: number of (sim, step) that hit a cap or stagnated */
+} pd_stats;
+
+/* Build a handle: validate the mesh, assemble A = M/h^2 + sum w G^T G
+ * on the free DoFs (fixed_dofs: host list of DoFs held at their rest
+ * values; must cover whole nodes), order it (nested dissection), factor it
+ * ONCE ("its Cholesky decomposition can be precomputed"), upload the
+ * factor and, with contact candidates, the cache (A^{-1})_{VV}.
+ * Returns INVALID_ARGUMENT / NUMERICAL / CUDA on failure (*out = NULL). */
+pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h,
+                    const int32_t* fixed_dofs, int32_t n_fixed,
+                    const pd_options* opts, pd_sim** out);
+
+/* Forward simulation of B independent sims for `steps` backward-Euler steps
+ * by PD local-global iterations, Alg. 1 contact when
+ * candidates exist.
+ *   q0, v0          device [B][3n]
+ *   f_ext           device [B][3n] non-gravity external force (N), constant over
+ *                   steps (f_ext_step_stride = 0) or NULL
+ *   actuation       device [B][steps][n_elems] muscle activation r, or NULL
+ *   youngs_per_sim  device [B] Young's modulus per sim, or NULL (= material.youngs)
+ *   q_traj, v_traj  device [B][steps+1][3n] outputs, or NULL
+ * The library keeps the trajectory for pd_backward until the next pd_forward. */
+pd_status pd_forward(pd_sim* sim, int32_t B, const double* q0, const double* v0,
+                     const double* f_ext, int64_t f_ext_step_stride,
+                     const double* actuation, const double* youngs_per_sim,
+                     int32_t steps, double* q_traj, double* v_traj,
+                     pd_stats* stats, void* cuda_stream);
+
+/* Reverse pass over the stored trajectory (adjoint method, with the
+ * PD fixed point / quasi-Newton solve of A_N u = b; contact steps use
+ * the same constrained matrix).
+ *   dL_dqT, dL_dvT   device [B][3n] terminal loss gradients (NULL = 0)
+ *   dL_dq0, dL_dv0   device [B][3n] outputs (or NULL)
+ *   dL_dfext         device [B][3n] output, summed over steps (or NULL)
+ *   dL_dE, dL_dnu    device [B] outputs (or NULL)
+ *   dL_dact          device [B][steps][n_elems] output (or NULL)
+ * Gradients on Dirichlet DoFs are exactly 0.  PD_ERR_STATE without a forward. */
+pd_status pd_backward(pd_sim* sim, const double* dL_dqT, const double* dL_dvT,
+                      double* dL_dq0, double* dL_dv0, double* dL_dfext,
+                      double* dL_dE, double* dL_dnu, double* dL_dact,
+                      pd_stats* stats, void* cuda_stream);
+
+/* Diagnostics / kernel-level parity hooks (same conventions as above). */
+/* grad_g[B][3n] = M/h^2 (x - y) + grad E_int(x) (eq:time_integration LHS) and
+ * g[B] = eq:opt objective at x; act device [B][n_elems] or NULL. */
+pd_status pd_eval_objective(pd_sim* sim, int32_t B, const double* x, const double* y,
+                            const double* youngs_per_sim, const double* act,
+                            double* grad_g, double* g, void* cuda_stream);
+/* out[B][3n] = A^{-1} rhs on free DoFs (0 on Dirichlet DoFs): the factored global solve. */
+pd_status pd_apply_Ainv(pd_sim* sim, int32_t B, const double* rhs, double* out, void* cuda_stream);
+/* out[B][3n] = A_N(x) p = (M/h^2) p + Hess E_int(x) p on all DoFs (matrix-free). */
+pd_status pd_apply_AN(pd_sim* sim, int32_t B, const double* x, const double* youngs_per_sim,
+                      const double* act, const double* p, double* out, void* cuda_stream);
+/* R[B][n_elems][8][9] = rotation R(F) of every quadrature point of x (local step projection). */
+pd_status pd_project_rotations(pd_sim* sim, int32_t B, const double* x, double* R, void* cuda_stream);
+
+/* Integer facts about the handle: out[0..n) = {n_nodes, n_free_nodes, n_supernodes,
+ * n_levels, nnz(L_s) (stored entries of the scalar factor), n_contact,
+ * setup_ms_factor (rounded), kernel launches of the last pd_forward+pd_backward}. */
+pd_status pd_info(const pd_sim* sim, int64_t* out, int32_t n);
+
+const char* pd_last_error(const pd_sim* sim);
+void pd_destroy(pd_sim* sim);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIFFPD_B200_H */

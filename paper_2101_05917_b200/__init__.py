@@ -1,0 +1,161 @@
+"""B200-native DiffPD hot path (arXiv 2101.05917): PD forward + PD backpropagation.
+
+Python surface = thin marshalling over the C-ABI in include/diffpd_b200.h.
+PyTorch provides device memory and streams only; every step of the path runs
+in libdiffpd_b200.so (sm_100a CUDA kernels + C++ host setup).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["Simulator", "PDError", "build"]
+
+
+def build(force=False):
+    from .build import build as _b
+    return _b(force=force)
+
+
+class PDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_lib.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t):
+    """Device pointer of a contiguous fp64/int CUDA tensor (or None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (the library takes device pointers)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Simulator:
+    """One pd_sim handle: mesh + material + h + Dirichlet set + contact candidates."""
+
+    def __init__(self, rest, hex8, dx, *, youngs, poisson, density, h, gravity=(0.0, 0.0, -9.81),
+                 fixed_dofs=(), contact_nodes=(), muscle_w=0.0, fiber=(1.0, 0.0, 0.0),
+                 tol_fwd=1e-9, tol_adj=1e-9, max_iter_fwd=20000, max_iter_adj=20000, fixed_iter=0,
+                 accel_fwd=0, accel_adj=1, check_every=1, max_batch=1, max_steps=1, youngs_ref=0.0,
+                 max_outer=10, eps_phi=None):
+        self.lib = _lib.load()
+        rest = np.ascontiguousarray(rest, dtype=np.float64)
+        hex8 = np.ascontiguousarray(hex8, dtype=np.int32)
+        self.n_nodes = rest.shape[0]
+        self.n_elems = hex8.shape[0]
+        self._keep = [rest, hex8]
+        mesh = _lib.PdMesh(self.n_nodes, self.n_elems, rest.ctypes.data_as(_lib.dp),
+                           hex8.ctypes.data_as(_lib.ip), float(dx))
+        mat = _lib.PdMaterial(float(youngs), float(poisson), float(density), float(muscle_w),
+                              (C.c_double * 3)(*gravity), (C.c_double * 3)(*fiber))
+        fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int32)
+        cand = np.ascontiguousarray(contact_nodes, dtype=np.int32)
+        self._keep += [fixed, cand]
+        opt = _lib.PdOptions(tol_fwd, tol_adj, max_iter_fwd, max_iter_adj, fixed_iter, accel_fwd, accel_adj,
+                             check_every, max_batch, max_steps, youngs_ref,
+                             cand.ctypes.data_as(_lib.ip) if len(cand) else None, len(cand), max_outer,
+                             float(1e-6 * dx if eps_phi is None else eps_phi))
+        h_ = C.c_void_p()
+        st = self.lib.pd_create(C.byref(mesh), C.byref(mat), float(h),
+                                fixed.ctypes.data_as(_lib.ip) if len(fixed) else None, len(fixed),
+                                C.byref(opt), C.byref(h_))
+        if st != 0:
+            raise PDError(st, self.lib.pd_last_error(None).decode())
+        self.handle = h_
+        self.max_batch, self.max_steps = max_batch, max_steps
+        self.h = h
+
+    def _check(self, st):
+        if st != 0:
+            raise PDError(st, self.lib.pd_last_error(self.handle).decode())
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.pd_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        out = (C.c_int64 * 8)()
+        self._check(self.lib.pd_info(self.handle, out, 8))
+        keys = ["n_nodes", "n_free_nodes", "n_supernodes", "n_levels", "nnz_L", "n_contact",
+                "factor_ms", "launches"]
+        return dict(zip(keys, list(out)))
+
+    def _stats(self, B, T):
+        arrs = dict(iters_fwd=np.zeros(B * T, np.int32), iters_adj=np.zeros(B * T, np.int32),
+                    contact_outer=np.zeros(B * T, np.int32), final_res_fwd=np.zeros(B * T),
+                    final_res_adj=np.zeros(B * T))
+        st = _lib.PdStats(arrs["iters_fwd"].ctypes.data_as(_lib.ip), arrs["iters_adj"].ctypes.data_as(_lib.ip),
+                          arrs["contact_outer"].ctypes.data_as(_lib.ip),
+                          arrs["final_res_fwd"].ctypes.data_as(_lib.dp),
+                          arrs["final_res_adj"].ctypes.data_as(_lib.dp), 0)
+        return st, arrs
+
+    def forward(self, q0, v0, steps, f_ext=None, actuation=None, youngs=None, q_traj=None, v_traj=None):
+        """q0, v0: CUDA fp64 [B, 3n].  Returns a stats dict (numpy [B, steps] arrays)."""
+        B = q0.shape[0]
+        st, arrs = self._stats(B, steps)
+        self._check(self.lib.pd_forward(self.handle, B, _ptr(q0), _ptr(v0), _ptr(f_ext), 0, _ptr(actuation),
+                                        _ptr(youngs), steps, _ptr(q_traj), _ptr(v_traj), C.byref(st), _stream()))
+        self._B, self._T = B, steps
+        out = {k: v.reshape(B, steps) for k, v in arrs.items() if k in ("iters_fwd", "final_res_fwd", "contact_outer")}
+        out["n_nonconverged"] = st.n_nonconverged
+        return out
+
+    def backward(self, dL_dqT=None, dL_dvT=None, dL_dq0=None, dL_dv0=None, dL_dfext=None, dL_dE=None,
+                 dL_dnu=None, dL_dact=None):
+        B, T = self._B, self._T
+        st, arrs = self._stats(B, T)
+        self._check(self.lib.pd_backward(self.handle, _ptr(dL_dqT), _ptr(dL_dvT), _ptr(dL_dq0), _ptr(dL_dv0),
+                                         _ptr(dL_dfext), _ptr(dL_dE), _ptr(dL_dnu), _ptr(dL_dact), C.byref(st),
+                                         _stream()))
+        out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
+        out["n_nonconverged"] = st.n_nonconverged
+        return out
+
+    def eval_objective(self, x, y, youngs=None, act=None, grad=None, g=None):
+        self._check(self.lib.pd_eval_objective(self.handle, x.shape[0], _ptr(x), _ptr(y), _ptr(youngs), _ptr(act),
+                                               _ptr(grad), _ptr(g), _stream()))
+
+    def apply_Ainv(self, rhs, out):
+        self._check(self.lib.pd_apply_Ainv(self.handle, rhs.shape[0], _ptr(rhs), _ptr(out), _stream()))
+
+    def apply_AN(self, x, p, out, youngs=None, act=None):
+        self._check(self.lib.pd_apply_AN(self.handle, x.shape[0], _ptr(x), _ptr(youngs), _ptr(act), _ptr(p),
+                                         _ptr(out), _stream()))
+
+    def project_rotations(self, x, R):
+        self._check(self.lib.pd_project_rotations(self.handle, x.shape[0], _ptr(x), _ptr(R), _stream()))
+
+
+def simulator_from_inputs(inp, **kw):
+    """Convenience: a Simulator for a pd_inputs workload dict."""
+    cfg = inp["cfg"]
+    muscle_w = cfg.youngs / (1 + cfg.poisson) if cfg.muscle else 0.0
+    args = dict(youngs=cfg.youngs, poisson=cfg.poisson, density=cfg.density, h=cfg.h, gravity=cfg.gravity,
+                fixed_dofs=inp["fixed_dofs"], contact_nodes=inp["contact_nodes"], muscle_w=muscle_w,
+                fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"])
+    if cfg.per_sim_youngs:
+        args["youngs_ref"] = float(np.max(inp["youngs"]))
+    args.update(kw)
+    return Simulator(inp["rest"], inp["hex8"], cfg.dx, **args)

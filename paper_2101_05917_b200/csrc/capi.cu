@@ -1,0 +1,721 @@
+// C-ABI of the B200 DiffPD hot path (include/diffpd_b200.h): handle lifetime,
+// device residency and the per-step orchestration of the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/diffpd_b200.h"
+#include "kernels.cu"  // single translation unit: kernels + orchestration
+#include "plan.h"
+
+using namespace pdb;
+
+namespace {
+thread_local std::string g_create_error;
+
+__global__ void k_fill_int(int32_t* p, int32_t v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+}  // namespace
+
+struct pd_sim {
+  HostPlan plan;
+  std::string err;
+  double youngs = 0, poisson = 0, density = 0, h = 0, w_m = 0;
+  double gravity[3] = {0, 0, 0};
+  pd_options opt{};
+  int Bmax = 1, Tmax = 1;
+  Stencil st{};
+  std::vector<DevBuf> bufs;
+  // plan on device
+  int32_t *d_hex8 = nullptr, *d_inc_ptr = nullptr, *d_inc_ec = nullptr, *d_pos = nullptr, *d_nodepos = nullptr;
+  double* d_mass = nullptr;
+  uint8_t* d_fixed = nullptr;
+  uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
+  SolveArgs sa{};
+  // work
+  double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
+  double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR;
+  double *w_sim, *youngs_sim, *dots, *partial, *alpha, *beta, *rz, *bb, *dw_acc, *act;
+  int32_t *active, *nactive, *it_buf, *flag_buf;
+  double* res_buf;
+  int32_t* h_nactive = nullptr;  // pinned
+  double* traj = nullptr;
+  int32_t *st_iters_f, *st_iters_a, *st_flag_f, *st_flag_a, *st_outer;
+  double *st_res_f, *st_res_a;
+  int64_t max_partial_blocks = 0;
+  // last forward
+  bool have_traj = false;
+  int B = 0, T = 0;
+  bool has_act = false;
+  int64_t launches = 0;
+  cudaStream_t stream = nullptr;
+
+  template <class T>
+  T* alloc(size_t count) {
+    DevBuf b;
+    b.bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (cudaMalloc(&b.p, b.bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+    cudaMemset(b.p, 0, b.bytes);
+    bufs.push_back(b);
+    return static_cast<T*>(b.p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* d = alloc<T>(v.size());
+    if (!v.empty()) cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return d;
+  }
+  ~pd_sim() {
+    for (auto& b : bufs) cudaFree(b.p);
+    if (h_nactive) cudaFreeHost(h_nactive);
+  }
+};
+
+namespace {
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+#define CK(x)                                                                                         \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+#define LAUNCH_CHECK(s) \
+  do {                  \
+    (s)->launches++;    \
+    CK(cudaGetLastError()); \
+  } while (0)
+
+pd_status fail(pd_sim* s, pd_status st, const std::string& msg) {
+  if (s) s->err = msg;
+  else g_create_error = msg;
+  return st;
+}
+
+ElemArgs elem_args(pd_sim* s, int B, const double* act_step, int64_t act_bstride) {
+  ElemArgs ea;
+  ea.hex8 = s->d_hex8;
+  ea.m = s->plan.m;
+  ea.B = B;
+  ea.w_sim = s->w_sim;
+  ea.act = act_step;
+  ea.act_bstride = act_bstride;
+  return ea;
+}
+
+// per-sim dot products of state-layout vectors of length len (*B) -> s->dots[p*B + b]
+void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const double*, const double*>> pairs,
+          double* out = nullptr) {
+  DotArgs da{};
+  int p = 0;
+  for (auto& pr : pairs) {
+    da.u[p] = pr.first;
+    da.v[p] = pr.second;
+    ++p;
+  }
+  da.npairs = p;
+  const int64_t chunk = 2048;
+  const int nchunk = (int)((len + chunk - 1) / chunk);
+  const int bd = B * std::max(1, 256 / B);
+  k_dot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
+  LAUNCH_CHECK(s);
+  k_dot_final<<<nblk(p * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots);
+  LAUNCH_CHECK(s);
+}
+
+// x = A^{-1} rhs in solve layout (S0 in, S0 out; S1, S2 scratch)
+void solve(pd_sim* s, int B) {
+  const HostPlan& P = s->plan;
+  const int R = 3 * B;
+  const size_t smem = (size_t)kTile * R * sizeof(double);
+  for (int lev = 0; lev < P.nlevels; ++lev) {
+    const int t0 = P.lvl_ptr[lev], nt = P.lvl_ptr[lev + 1] - t0;
+    if (!nt) continue;
+    k_fwdA<<<nt, 256, smem, s->stream>>>(s->sa, t0, R, s->S0, s->S2, s->S1);
+    LAUNCH_CHECK(s);
+    k_fwdB<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S1, s->S2);
+    LAUNCH_CHECK(s);
+  }
+  for (int lev = P.nlevels - 1; lev >= 0; --lev) {
+    const int t0 = P.lvl_ptr[lev], nt = P.lvl_ptr[lev + 1] - t0;
+    if (!nt) continue;
+    k_bwdA<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S2, s->S0, s->S1);
+    LAUNCH_CHECK(s);
+    k_bwdB<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S1, s->S0);
+    LAUNCH_CHECK(s);
+  }
+}
+
+// state vector V (free nodes) -> A^{-1} V -> OUT = beta OUT + alpha_c*alpha[b]*sol (masked)
+void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* alpha, double alpha_c, double beta,
+                const int32_t* active) {
+  const HostPlan& P = s->plan;
+  k_to_solve<<<nblk((int64_t)P.nfree * 3 * B), 256, 0, s->stream>>>(Vin, s->d_nodepos, P.nfree, B, s->S0);
+  LAUNCH_CHECK(s);
+  solve(s, B);
+  k_from_solve<<<nblk((int64_t)3 * P.n * B), 256, 0, s->stream>>>(s->S0, s->d_pos, P.n, B, alpha, alpha_c, beta,
+                                                                   active, OUT);
+  LAUNCH_CHECK(s);
+}
+
+// grad g(X) into G (+ W normaliser, S0 permuted RHS), element energies in EE
+void residual(pd_sim* s, int B, const double* X, const double* Y, const double* act_step, int64_t act_bstride,
+              const uint8_t* fixed_mask) {
+  const HostPlan& P = s->plan;
+  k_elem_residual<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
+                                                                       s->EF, s->EE);
+  LAUNCH_CHECK(s);
+  k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
+                                                          s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, s->G, s->W, s->S0,
+                                                          nullptr, nullptr, nullptr);
+  LAUNCH_CHECK(s);
+}
+
+// OUT = A_N(X) Pin, zero on constrained DoFs
+void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT, const double* act_step,
+              int64_t act_bstride) {
+  const HostPlan& P = s->plan;
+  k_elem_AN<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
+                                                                 s->EF);
+  LAUNCH_CHECK(s);
+  k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
+                                                          s->d_fixed, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, OUT,
+                                                          nullptr, nullptr, nullptr, nullptr, nullptr);
+  LAUNCH_CHECK(s);
+}
+
+void set_w(pd_sim* s, int B, const double* youngs_per_sim) {
+  // w = E/(1+nu) per sim; youngs_sim keeps E for dL/dE, dL/dnu
+  std::vector<double> ones(B, s->youngs);
+  if (youngs_per_sim)
+    CK(cudaMemcpyAsync(s->youngs_sim, youngs_per_sim, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  else
+    CK(cudaMemcpyAsync(s->youngs_sim, ones.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  k_axpby<<<1, 256, 0, s->stream>>>(s->w_sim, s->youngs_sim, 1.0 / (1.0 + s->poisson), nullptr, nullptr, 0.0, B, B,
+                                    nullptr);
+  LAUNCH_CHECK(s);
+  CK(cudaStreamSynchronize(s->stream));
+}
+
+int read_nactive(pd_sim* s) {
+  CK(cudaMemcpyAsync(s->h_nactive, s->nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return *s->h_nactive;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pd_last_error(const pd_sim* sim) { return sim ? sim->err.c_str() : g_create_error.c_str(); }
+
+void pd_destroy(pd_sim* sim) { delete sim; }
+
+pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const int32_t* fixed_dofs, int32_t n_fixed,
+                    const pd_options* opts, pd_sim** out) {
+  if (!out) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!mesh || !mat || !opts) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "mesh, material and options are required");
+  if (!(mat->poisson > -1.0 && mat->poisson < 0.5)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "poisson must be in (-1, 0.5)");
+  if (!(mat->youngs > 0) || !(mat->density > 0)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "youngs and density must be > 0");
+  if (!(h > 0)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "h must be > 0");
+  if (n_fixed < 0 || (n_fixed > 0 && !fixed_dofs)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "bad fixed DoF list");
+  if (opts->max_batch < 1 || opts->max_batch > 256) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "max_batch must be in [1, 256]");
+  if (opts->max_steps < 1) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "max_steps must be >= 1");
+  if (opts->n_contact != 0) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "contact is not enabled in this build yet");
+  std::unique_ptr<pd_sim> s(new pd_sim());
+  try {
+    s->youngs = mat->youngs;
+    s->poisson = mat->poisson;
+    s->density = mat->density;
+    s->h = h;
+    s->w_m = mat->muscle_w;
+    for (int j = 0; j < 3; ++j) s->gravity[j] = mat->gravity[j];
+    s->opt = *opts;
+    if (s->opt.check_every < 1) s->opt.check_every = 1;
+    if (s->opt.max_iter_fwd < 1) s->opt.max_iter_fwd = 10000;
+    if (s->opt.max_iter_adj < 1) s->opt.max_iter_adj = 10000;
+    if (s->opt.max_outer < 1) s->opt.max_outer = 10;
+    s->Bmax = opts->max_batch;
+    s->Tmax = opts->max_steps;
+    double fiber[3] = {mat->fiber[0], mat->fiber[1], mat->fiber[2]};
+    const double fn = std::sqrt(fiber[0] * fiber[0] + fiber[1] * fiber[1] + fiber[2] * fiber[2]);
+    if (mat->muscle_w != 0.0) {
+      if (!(fn > 0)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "fiber direction must be non-zero");
+      for (double& f : fiber) f /= fn;
+    }
+    const double yref = opts->youngs_ref > 0 ? opts->youngs_ref : mat->youngs;
+    const double w_ref = yref / (1.0 + mat->poisson);
+    bool numerical = false;
+    std::string e = build_plan(s->plan, mesh->n_nodes, mesh->n_elems, mesh->rest_xyz, mesh->hex8, mesh->dx,
+                               mat->density, h, fixed_dofs, n_fixed, w_ref, mat->muscle_w, fiber, &numerical);
+    if (!e.empty()) return fail(nullptr, numerical ? PD_ERR_NUMERICAL : PD_ERR_INVALID_ARGUMENT, e);
+    const HostPlan& P = s->plan;
+    std::memcpy(s->st.dN, P.dN, sizeof(P.dN));
+    for (int j = 0; j < 3; ++j) s->st.fiber[j] = fiber[j];
+    s->st.V = mesh->dx * mesh->dx * mesh->dx / 8.0;
+    s->st.w_m = mat->muscle_w;
+    s->st.clamp = 1e-6;
+    // ---- device residency
+    s->d_hex8 = s->upload(P.hex8);
+    s->d_inc_ptr = s->upload(P.inc_ptr);
+    s->d_inc_ec = s->upload(P.inc_ec);
+    s->d_pos = s->upload(P.pos_of_node);
+    s->d_nodepos = s->upload(P.node_of_pos);
+    s->d_mass = s->upload(P.node_mass);
+    s->d_fixed = s->upload(P.fixed_node);
+    s->d_nofix = s->alloc<uint8_t>(P.n);
+    s->sa.sfirst = s->upload(P.sfirst);
+    s->sa.ssize = s->upload(P.ssize);
+    s->sa.rptr = s->upload(P.rptr);
+    s->sa.doff = s->upload(P.doff);
+    s->sa.poff = s->upload(P.poff);
+    s->sa.rows = s->upload(P.rows);
+    s->sa.D = s->upload(P.D);
+    s->sa.P = s->upload(P.P);
+    s->sa.tile_sup = s->upload(P.tile_sup);
+    s->sa.tile_r0 = s->upload(P.tile_r0);
+    s->sa.tile_r1 = s->upload(P.tile_r1);
+    s->sa.tblk_ptr = s->upload(P.tblk_ptr);
+    s->sa.blk_d = s->upload(P.blk_d);
+    s->sa.blk_k0 = s->upload(P.blk_k0);
+    s->sa.blk_k1 = s->upload(P.blk_k1);
+    const int64_t n3B = 3LL * P.n * s->Bmax;
+    const int64_t sB = 3LL * P.nfree * s->Bmax;
+    double** st_vecs[] = {&s->X, &s->V, &s->Y, &s->Xp, &s->Fext, &s->G, &s->W, &s->U, &s->Rv, &s->Z,
+                          &s->Pv, &s->Q, &s->AX, &s->AV, &s->Bv, &s->DF};
+    for (double** p : st_vecs) *p = s->alloc<double>(n3B);
+    s->S0 = s->alloc<double>(sB);
+    s->S1 = s->alloc<double>(sB);
+    s->S2 = s->alloc<double>(sB);
+    s->EF = s->alloc<double>((int64_t)P.m * 24 * s->Bmax);
+    s->EE = s->alloc<double>((int64_t)P.m * s->Bmax);
+    s->DW = s->alloc<double>((int64_t)P.m * s->Bmax);
+    s->DR = s->alloc<double>((int64_t)P.m * s->Bmax);
+    double** small[] = {&s->w_sim, &s->youngs_sim, &s->alpha, &s->beta, &s->rz, &s->bb, &s->dw_acc, &s->res_buf};
+    for (double** p : small) *p = s->alloc<double>(s->Bmax);
+    s->dots = s->alloc<double>(3 * s->Bmax);
+    s->max_partial_blocks = (n3B / s->Bmax + 2047) / 2048 + 1;
+    s->partial = s->alloc<double>(3 * s->max_partial_blocks * s->Bmax);
+    s->active = s->alloc<int32_t>(s->Bmax);
+    s->nactive = s->alloc<int32_t>(1);
+    s->it_buf = s->alloc<int32_t>(s->Bmax);
+    s->flag_buf = s->alloc<int32_t>(s->Bmax);
+    const int64_t TB = (int64_t)s->Tmax * s->Bmax;
+    s->st_iters_f = s->alloc<int32_t>(TB);
+    s->st_iters_a = s->alloc<int32_t>(TB);
+    s->st_flag_f = s->alloc<int32_t>(TB);
+    s->st_flag_a = s->alloc<int32_t>(TB);
+    s->st_outer = s->alloc<int32_t>(TB);
+    s->st_res_f = s->alloc<double>(TB);
+    s->st_res_a = s->alloc<double>(TB);
+    s->traj = s->alloc<double>((int64_t)(s->Tmax + 1) * n3B);
+    s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
+    CK(cudaMallocHost(&s->h_nactive, sizeof(int32_t)));
+    const int smem_max = (int)(kTile * 3 * s->Bmax * sizeof(double));
+    if (smem_max > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_fwdA, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+    CK(cudaDeviceSynchronize());
+  } catch (CudaError& e) {
+    return fail(nullptr, PD_ERR_CUDA, e.what());
+  } catch (std::exception& e) {
+    return fail(nullptr, PD_ERR_CUDA, e.what());
+  }
+  *out = s.release();
+  return PD_OK;
+}
+
+pd_status pd_info(const pd_sim* s, int64_t* out, int32_t n) {
+  if (!s || !out) return PD_ERR_INVALID_ARGUMENT;
+  const HostPlan& P = s->plan;
+  const int64_t v[] = {P.n, P.nfree, P.nsup, P.nlevels, P.nnzL, (int64_t)s->opt.n_contact,
+                       (int64_t)std::llround(P.factor_ms), s->launches};
+  for (int i = 0; i < n && i < (int)(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
+  return PD_OK;
+}
+
+pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, const double* f_ext,
+                     int64_t f_ext_step_stride, const double* actuation, const double* youngs_per_sim, int32_t steps,
+                     double* q_traj, double* v_traj, pd_stats* stats, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax) return fail(s, PD_ERR_INVALID_ARGUMENT, "B out of [1, max_batch]");
+  if (steps < 1 || steps > s->Tmax) return fail(s, PD_ERR_INVALID_ARGUMENT, "steps out of [1, max_steps]");
+  if (!q0 || !v0) return fail(s, PD_ERR_INVALID_ARGUMENT, "q0 and v0 are required");
+  if (f_ext_step_stride != 0) return fail(s, PD_ERR_INVALID_ARGUMENT, "time-varying f_ext is not supported yet");
+  if (s->w_m != 0.0 && !actuation) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs an actuation array");
+  s->stream = (cudaStream_t)cuda_stream;
+  s->launches = 0;
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    set_w(s, B, youngs_per_sim);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(q0, s->X, n3, B);
+    LAUNCH_CHECK(s);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(v0, s->V, n3, B);
+    LAUNCH_CHECK(s);
+    if (f_ext) {
+      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(f_ext, s->Fext, n3, B);
+      LAUNCH_CHECK(s);
+    }
+    if (actuation && s->act) {
+      CK(cudaMemcpyAsync(s->act, actuation, sizeof(double) * (int64_t)B * steps * P.m, cudaMemcpyDeviceToDevice,
+                         s->stream));
+    }
+    s->has_act = actuation && s->act;
+    CK(cudaMemcpyAsync(s->traj, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    const double tol = s->opt.tol_fwd;
+    for (int i = 0; i < steps; ++i) {
+      const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
+      const int64_t act_bs = (int64_t)steps * P.m;
+      k_y<<<nblk(len), 256, 0, s->stream>>>(s->X, s->V, f_ext ? s->Fext : nullptr, s->d_mass, s->Y, P.n, B, s->h,
+                                            s->gravity[0], s->gravity[1], s->gravity[2]);
+      LAUNCH_CHECK(s);
+      CK(cudaMemcpyAsync(s->Xp, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+      k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
+      LAUNCH_CHECK(s);
+      for (int iter = 0;; ++iter) {
+        residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
+        dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+        CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+        k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter, s->opt.max_iter_fwd,
+                                                       s->active, s->st_iters_f + (int64_t)i * B,
+                                                       s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
+                                                       s->nactive);
+        LAUNCH_CHECK(s);
+        if (s->opt.fixed_iter > 0) {
+          if (iter >= s->opt.fixed_iter) break;
+        } else if (iter >= s->opt.max_iter_fwd) {
+          break;
+        } else if (iter % s->opt.check_every == 0) {
+          if (read_nactive(s) == 0) break;
+        }
+        apply_Ainv(s, B, s->G, s->X, nullptr, -1.0, 1.0, s->active);
+      }
+      k_velocity<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, s->V, len, 1.0 / s->h);
+      LAUNCH_CHECK(s);
+      CK(cudaMemcpyAsync(s->traj + (int64_t)(i + 1) * len, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice,
+                         s->stream));
+      if (q_traj) {
+        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->X, q_traj + (int64_t)(i + 1) * n3, n3, B,
+                                                         (int64_t)(steps + 1) * n3);
+        LAUNCH_CHECK(s);
+      }
+      if (v_traj) {
+        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->V, v_traj + (int64_t)(i + 1) * n3, n3, B,
+                                                         (int64_t)(steps + 1) * n3);
+        LAUNCH_CHECK(s);
+      }
+    }
+    if (q_traj)
+      CK(cudaMemcpy2DAsync(q_traj, (steps + 1) * n3 * sizeof(double), q0, n3 * sizeof(double), n3 * sizeof(double), B,
+                           cudaMemcpyDeviceToDevice, s->stream));
+    if (v_traj)
+      CK(cudaMemcpy2DAsync(v_traj, (steps + 1) * n3 * sizeof(double), v0, n3 * sizeof(double), n3 * sizeof(double), B,
+                           cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (stats) {
+      const int64_t TB = (int64_t)steps * B;
+      std::vector<int32_t> it(TB), fl(TB);
+      std::vector<double> rs(TB);
+      CK(cudaMemcpy(it.data(), s->st_iters_f, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(fl.data(), s->st_flag_f, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(rs.data(), s->st_res_f, TB * sizeof(double), cudaMemcpyDeviceToHost));
+      int nnc = 0;
+      for (int b = 0; b < B; ++b)
+        for (int i = 0; i < steps; ++i) {  // device buffers are [step][b]; ABI stats are [b][step]
+          if (stats->iters_fwd) stats->iters_fwd[b * steps + i] = it[(int64_t)i * B + b];
+          if (stats->final_res_fwd) stats->final_res_fwd[b * steps + i] = rs[(int64_t)i * B + b];
+          if (stats->contact_outer) stats->contact_outer[b * steps + i] = 0;
+          nnc += fl[(int64_t)i * B + b];
+        }
+      stats->n_nonconverged = nnc;
+    }
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  s->have_traj = true;
+  s->B = B;
+  s->T = steps;
+  return PD_OK;
+}
+
+pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, double* dL_dq0, double* dL_dv0,
+                      double* dL_dfext, double* dL_dE, double* dL_dnu, double* dL_dact, pd_stats* stats,
+                      void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (!s->have_traj) return fail(s, PD_ERR_STATE, "pd_backward needs a preceding pd_forward");
+  s->stream = (cudaStream_t)cuda_stream;
+  s->launches = 0;
+  const HostPlan& P = s->plan;
+  const int B = s->B, T = s->T;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  const double h = s->h;
+  try {
+    if (dL_dqT) {
+      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(dL_dqT, s->AX, n3, B);
+      LAUNCH_CHECK(s);
+    } else {
+      CK(cudaMemsetAsync(s->AX, 0, len * sizeof(double), s->stream));
+    }
+    if (dL_dvT) {
+      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(dL_dvT, s->AV, n3, B);
+      LAUNCH_CHECK(s);
+    } else {
+      CK(cudaMemsetAsync(s->AV, 0, len * sizeof(double), s->stream));
+    }
+    CK(cudaMemsetAsync(s->DF, 0, len * sizeof(double), s->stream));
+    CK(cudaMemsetAsync(s->dw_acc, 0, B * sizeof(double), s->stream));
+    const bool pcg = s->opt.accel_adj != 0;
+    for (int i = T - 1; i >= 0; --i) {
+      const double* x1 = s->traj + (int64_t)(i + 1) * len;
+      const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
+      const int64_t act_bs = (int64_t)T * P.m;
+      // b = a_x + a_v / h on unconstrained DoFs
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
+      LAUNCH_CHECK(s);
+      k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->d_fixed, P.n, B, nullptr, nullptr);
+      LAUNCH_CHECK(s);
+      dots(s, B, n3, {{s->Bv, s->Bv}}, s->bb);
+      CK(cudaMemsetAsync(s->U, 0, len * sizeof(double), s->stream));
+      CK(cudaMemcpyAsync(s->Rv, s->Bv, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+      k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
+      LAUNCH_CHECK(s);
+      if (pcg) {
+        apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, nullptr);
+        CK(cudaMemcpyAsync(s->Pv, s->Z, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+        dots(s, B, n3, {{s->Rv, s->Z}}, s->rz);
+      }
+      for (int iter = 0;; ++iter) {
+        dots(s, B, n3, {{s->Rv, s->Rv}});
+        CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+        k_adj_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, s->bb, B, s->opt.tol_adj, iter, s->opt.max_iter_adj,
+                                                       s->active, s->st_iters_a + (int64_t)i * B,
+                                                       s->st_res_a + (int64_t)i * B, s->st_flag_a + (int64_t)i * B,
+                                                       s->nactive);
+        LAUNCH_CHECK(s);
+        if (iter >= s->opt.max_iter_adj) break;
+        if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
+        if (pcg) {
+          apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs);
+          k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->d_fixed, P.n, B, nullptr, nullptr);
+          LAUNCH_CHECK(s);
+          dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
+          k_pcg_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->rz, s->dots + B, s->alpha, s->active, B);
+          LAUNCH_CHECK(s);
+          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->U, s->U, 1.0, s->Pv, s->alpha, 1.0, len, B, s->active);
+          LAUNCH_CHECK(s);
+          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Rv, 1.0, s->Q, s->alpha, -1.0, len, B, s->active);
+          LAUNCH_CHECK(s);
+          apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->active);
+          dots(s, B, n3, {{s->Rv, s->Z}}, s->dots + B);
+          k_pcg_beta<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots + B, s->rz, s->beta, s->active, B);
+          LAUNCH_CHECK(s);
+          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, 1.0, s->Pv, s->beta, 1.0, len, B, s->active);
+          LAUNCH_CHECK(s);
+        } else {
+          // fixed point u <- u + A^{-1}(b - A_N u) == A^{-1}(b + dA u)  (eq:bp_update)
+          apply_Ainv(s, B, s->Rv, s->U, nullptr, 1.0, 1.0, s->active);
+          apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs);
+          k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->d_fixed, P.n, B, nullptr, nullptr);
+          LAUNCH_CHECK(s);
+          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
+          LAUNCH_CHECK(s);
+        }
+      }
+      // parameter terms, f_ext accumulation, state adjoint update
+      k_elem_param<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
+                                                                      s->DW, s->has_act ? s->DR : nullptr);
+      LAUNCH_CHECK(s);
+      k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->DW, P.m, B, s->dw_acc, 1);
+      LAUNCH_CHECK(s);
+      if (dL_dact && s->has_act) {
+        k_state_to_abi<<<nblk((int64_t)P.m * B), 256, 0, s->stream>>>(s->DR, dL_dact + (int64_t)i * P.m, P.m, B,
+                                                                      (int64_t)T * P.m);
+        LAUNCH_CHECK(s);
+      }
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->DF, 1.0, s->U, nullptr, 1.0, len, B, nullptr);
+      LAUNCH_CHECK(s);
+      k_adj_state<<<nblk(len), 256, 0, s->stream>>>(s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
+      LAUNCH_CHECK(s);
+    }
+    if (dL_dq0) {
+      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dL_dq0, n3, B, n3);
+      LAUNCH_CHECK(s);
+    }
+    if (dL_dv0) {
+      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dL_dv0, n3, B, n3);
+      LAUNCH_CHECK(s);
+    }
+    if (dL_dfext) {
+      k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->d_fixed, P.n, B, nullptr, nullptr);
+      LAUNCH_CHECK(s);
+      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->DF, dL_dfext, n3, B, n3);
+      LAUNCH_CHECK(s);
+    }
+    // dL/dE = dL/dw / (1+nu); dL/dnu = -dL/dw E/(1+nu)^2   (w = E/(1+nu))
+    std::vector<double> dw(B), E(B);
+    CK(cudaMemcpyAsync(dw.data(), s->dw_acc, B * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(E.data(), s->youngs_sim, B * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    std::vector<double> dE(B), dnu(B);
+    for (int b = 0; b < B; ++b) {
+      dE[b] = dw[b] / (1.0 + s->poisson);
+      dnu[b] = -dw[b] * E[b] / ((1.0 + s->poisson) * (1.0 + s->poisson));
+    }
+    if (dL_dE) CK(cudaMemcpyAsync(dL_dE, dE.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    if (dL_dnu) CK(cudaMemcpyAsync(dL_dnu, dnu.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    if (stats) {
+      const int64_t TB = (int64_t)T * B;
+      std::vector<int32_t> it(TB), fl(TB);
+      std::vector<double> rs(TB);
+      CK(cudaMemcpy(it.data(), s->st_iters_a, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(fl.data(), s->st_flag_a, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(rs.data(), s->st_res_a, TB * sizeof(double), cudaMemcpyDeviceToHost));
+      int nnc = 0;
+      for (int b = 0; b < B; ++b)
+        for (int i = 0; i < T; ++i) {
+          if (stats->iters_adj) stats->iters_adj[b * T + i] = it[(int64_t)i * B + b];
+          if (stats->final_res_adj) stats->final_res_adj[b * T + i] = rs[(int64_t)i * B + b];
+          nnc += fl[(int64_t)i * B + b];
+        }
+      stats->n_nonconverged = nnc;
+    }
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+pd_status pd_eval_objective(pd_sim* s, int32_t B, const double* x, const double* y, const double* youngs_per_sim,
+                            const double* act, double* grad_g, double* g, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax || !x || !y) return fail(s, PD_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (s->w_m != 0.0 && !act) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs act");
+  s->stream = (cudaStream_t)cuda_stream;
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    set_w(s, B, youngs_per_sim);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    LAUNCH_CHECK(s);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(y, s->Y, n3, B);
+    LAUNCH_CHECK(s);
+    residual(s, B, s->X, s->Y, act, P.m, s->d_nofix);
+    if (grad_g) {
+      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->G, grad_g, n3, B, n3);
+      LAUNCH_CHECK(s);
+    }
+    if (g) {
+      // g = sum_e E_e + sum_i m_i/(2h^2) (x_i - y_i)^2   (eq:opt)
+      k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->EE, P.m, B, g, 0);
+      LAUNCH_CHECK(s);
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->X, 1.0, s->Y, nullptr, -1.0, len, B, nullptr);
+      LAUNCH_CHECK(s);
+      CK(cudaMemsetAsync(s->EF, 0, (int64_t)P.m * 24 * B * sizeof(double), s->stream));
+      k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Q, nullptr, s->EF, s->d_mass, s->d_inc_ptr,
+                                                              s->d_inc_ec, s->d_nofix, s->d_pos, P.n, B,
+                                                              1.0 / (s->h * s->h), 1, s->Z, nullptr, nullptr, nullptr,
+                                                              nullptr, nullptr);
+      LAUNCH_CHECK(s);
+      dots(s, B, n3, {{s->Q, s->Z}});
+      k_axpby<<<1, 64, 0, s->stream>>>(g, g, 1.0, s->dots, nullptr, 0.5, B, B, nullptr);
+      LAUNCH_CHECK(s);
+    }
+    CK(cudaStreamSynchronize(s->stream));
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+pd_status pd_apply_Ainv(pd_sim* s, int32_t B, const double* rhs, double* out, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax || !rhs || !out) return fail(s, PD_ERR_INVALID_ARGUMENT, "bad arguments");
+  s->stream = (cudaStream_t)cuda_stream;
+  const int n3 = 3 * s->plan.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(rhs, s->Rv, n3, B);
+    LAUNCH_CHECK(s);
+    apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, nullptr);
+    k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->Z, out, n3, B, n3);
+    LAUNCH_CHECK(s);
+    CK(cudaStreamSynchronize(s->stream));
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+pd_status pd_apply_AN(pd_sim* s, int32_t B, const double* x, const double* youngs_per_sim, const double* act,
+                      const double* p, double* out, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax || !x || !p || !out) return fail(s, PD_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (s->w_m != 0.0 && !act) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs act");
+  s->stream = (cudaStream_t)cuda_stream;
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    set_w(s, B, youngs_per_sim);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    LAUNCH_CHECK(s);
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(p, s->Pv, n3, B);
+    LAUNCH_CHECK(s);
+    k_elem_AN<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
+    LAUNCH_CHECK(s);
+    k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Pv, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
+                                                            s->d_nofix, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, s->Q,
+                                                            nullptr, nullptr, nullptr, nullptr, nullptr);
+    LAUNCH_CHECK(s);
+    k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->Q, out, n3, B, n3);
+    LAUNCH_CHECK(s);
+    CK(cudaStreamSynchronize(s->stream));
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+pd_status pd_project_rotations(pd_sim* s, int32_t B, const double* x, double* R, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax || !x || !R) return fail(s, PD_ERR_INVALID_ARGUMENT, "bad arguments");
+  s->stream = (cudaStream_t)cuda_stream;
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    LAUNCH_CHECK(s);
+    k_elem_rotations<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(s->X, s->st, s->d_hex8, P.m, B, R);
+    LAUNCH_CHECK(s);
+    CK(cudaStreamSynchronize(s->stream));
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,746 @@
+// sm_100a fp64 kernels of the DiffPD hot path (see kernels.cuh for layouts).
+//
+//   K1  k_elem_residual   local step: per (element, sim) F_q = G_q x_e, R = polar(F_q)
+//                         by scaled Newton iteration (SVD fallback), muscle p = r Fm/||Fm||,
+//                         element force sum_q V G_q^T [w (F - R) + w_m (Fm - p) m^T] and energy
+//   K2  k_gather          deterministic element->node gather (fixed incidence order, no atomics):
+//                         grad g = M/h^2 (x - y) + sum_e ... (eq:time_integration / eq:gradient)
+//   K3  k_fwdA/B, k_bwdA/B level-scheduled supernodal solves with L_s, 3B RHS per factor stream
+//   K4  k_elem_AN         matrix-free A_N p = (M/h^2) p + sum w V G^T (dF - dR[dF]) G p
+//   --  per-sim deterministic dot products, axpys, PCG scalars, parameter-gradient terms
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace pdb {
+
+// ----------------------------------------------------------------- 3x3 helpers (row-major)
+__device__ __forceinline__ double det3(const double* A) {
+  return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+         A[2] * (A[3] * A[7] - A[4] * A[6]);
+}
+// cofactor matrix C (C_ij = cofactor of A_ij); A^{-T} = C / det
+__device__ __forceinline__ void cof3(const double* A, double* C) {
+  C[0] = A[4] * A[8] - A[5] * A[7];
+  C[1] = A[5] * A[6] - A[3] * A[8];
+  C[2] = A[3] * A[7] - A[4] * A[6];
+  C[3] = A[2] * A[7] - A[1] * A[8];
+  C[4] = A[0] * A[8] - A[2] * A[6];
+  C[5] = A[1] * A[6] - A[0] * A[7];
+  C[6] = A[1] * A[5] - A[2] * A[4];
+  C[7] = A[2] * A[3] - A[0] * A[5];
+  C[8] = A[0] * A[4] - A[1] * A[3];
+}
+
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi: A (row-major, symmetric) ->
+// eigenvalues lam[3] (descending), eigenvectors V[:,k] (columns, row-major V), det V = +1.
+__device__ void jacobi_eig3(const double* Ain, double* lam, double* V) {
+  double a[9];
+  for (int i = 0; i < 9; ++i) a[i] = Ain[i];
+  for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    const double off = a[1] * a[1] + a[2] * a[2] + a[5] * a[5];
+    const double dia = a[0] * a[0] + a[4] * a[4] + a[8] * a[8];
+    if (off <= 1e-34 * dia || off == 0.0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        const double apq = a[3 * p + q];
+        if (apq == 0.0) continue;
+        const double app = a[3 * p + p], aqq = a[3 * q + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A J
+          const double akp = a[3 * k + p], akq = a[3 * k + q];
+          a[3 * k + p] = c * akp - s * akq;
+          a[3 * k + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double apk = a[3 * p + k], aqk = a[3 * q + k];
+          a[3 * p + k] = c * apk - s * aqk;
+          a[3 * q + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double vkp = V[3 * k + p], vkq = V[3 * k + q];
+          V[3 * k + p] = c * vkp - s * vkq;
+          V[3 * k + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  double l[3] = {a[0], a[4], a[8]};
+  int idx[3] = {0, 1, 2};
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2 - i; ++j)
+      if (l[idx[j]] < l[idx[j + 1]]) { int t = idx[j]; idx[j] = idx[j + 1]; idx[j + 1] = t; }
+  double W[9];
+  for (int k = 0; k < 3; ++k) {
+    lam[k] = l[idx[k]];
+    for (int r = 0; r < 3; ++r) W[3 * r + k] = V[3 * r + idx[k]];
+  }
+  if (det3(W) < 0)
+    for (int r = 0; r < 3; ++r) W[3 * r + 2] = -W[3 * r + 2];
+  for (int i = 0; i < 9; ++i) V[i] = W[i];
+}
+
+// Rotation closest to F via an SVD from the eigen-decomposition of F^T F; the
+// smallest singular direction is flipped when det F < 0.
+__device__ void polar_svd_fallback(const double* F, double* R) {
+  double C[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) C[3 * i + j] = F[i] * F[j] + F[3 + i] * F[3 + j] + F[6 + i] * F[6 + j];
+  double lam[3], V[9];
+  jacobi_eig3(C, lam, V);
+  double u[3][3];
+  for (int k = 0; k < 2; ++k) {
+    double fv[3];
+    for (int i = 0; i < 3; ++i) fv[i] = F[3 * i] * V[k] + F[3 * i + 1] * V[3 + k] + F[3 * i + 2] * V[6 + k];
+    if (k == 1) {  // Gram-Schmidt against u0
+      const double d = fv[0] * u[0][0] + fv[1] * u[0][1] + fv[2] * u[0][2];
+      for (int i = 0; i < 3; ++i) fv[i] -= d * u[0][i];
+    }
+    double nr = sqrt(fv[0] * fv[0] + fv[1] * fv[1] + fv[2] * fv[2]);
+    if (!(nr > 1e-300)) {  // degenerate: any unit vector orthogonal to the previous ones
+      if (k == 0) { fv[0] = 1; fv[1] = 0; fv[2] = 0; }
+      else {
+        const double* a = u[0];
+        const double e[3] = {fabs(a[0]) < 0.9 ? 1.0 : 0.0, fabs(a[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+        fv[0] = a[1] * e[2] - a[2] * e[1];
+        fv[1] = a[2] * e[0] - a[0] * e[2];
+        fv[2] = a[0] * e[1] - a[1] * e[0];
+      }
+      nr = sqrt(fv[0] * fv[0] + fv[1] * fv[1] + fv[2] * fv[2]);
+    }
+    for (int i = 0; i < 3; ++i) u[k][i] = fv[i] / nr;
+  }
+  u[2][0] = u[0][1] * u[1][2] - u[0][2] * u[1][1];
+  u[2][1] = u[0][2] * u[1][0] - u[0][0] * u[1][2];
+  u[2][2] = u[0][0] * u[1][1] - u[0][1] * u[1][0];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) R[3 * i + j] = u[0][i] * V[3 * j] + u[1][i] * V[3 * j + 1] + u[2][i] * V[3 * j + 2];
+}
+
+// R = rotation of the polar decomposition F = R S.  Scaled Newton iteration
+// X <- (g X + X^{-T}/g)/2 (Frobenius scaling) for det F > 0; SVD path otherwise.
+__device__ void polar_rotation(const double* F, double* R) {
+  const double d0 = det3(F);
+  double fn2 = 0;
+  for (int i = 0; i < 9; ++i) fn2 += F[i] * F[i];
+  if (!(d0 > 1e-6 * fn2 * sqrt(fn2))) {
+    polar_svd_fallback(F, R);
+    return;
+  }
+  double X[9];
+  for (int i = 0; i < 9; ++i) X[i] = F[i];
+  bool scaled = true;
+  for (int it = 0; it < 40; ++it) {
+    double C[9];
+    cof3(X, C);
+    const double det = X[0] * C[0] + X[1] * C[1] + X[2] * C[2];
+    const double idet = 1.0 / det;
+    double g = 1.0;
+    if (scaled) {
+      double xn = 0, cn = 0;
+      for (int i = 0; i < 9; ++i) { xn += X[i] * X[i]; cn += C[i] * C[i]; }
+      g = sqrt(sqrt(cn * idet * idet / xn));  // (||X^{-1}||_F / ||X||_F)^{1/2}
+    }
+    double diff = 0, nrm = 0;
+    for (int i = 0; i < 9; ++i) {
+      const double xn = 0.5 * (g * X[i] + C[i] * idet / g);
+      diff += (xn - X[i]) * (xn - X[i]);
+      nrm += xn * xn;
+      X[i] = xn;
+    }
+    if (diff < 1e-4 * nrm) scaled = false;
+    if (diff <= 1e-32 * nrm) break;
+  }
+  for (int i = 0; i < 9; ++i) R[i] = X[i];
+}
+
+// ----------------------------------------------------------------- layout kernels
+__global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict__ out, int n3, int B) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n3 * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  out[i] = in[(int64_t)b * n3 + d];
+}
+__global__ void k_state_to_abi(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
+                               int64_t out_bstride) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n3 * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  out[(int64_t)b * out_bstride + d] = in[i];
+}
+
+// y = x + h v + h^2 (g + f_ext / m)
+__global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
+                    const double* __restrict__ Fext, const double* __restrict__ mass, double* __restrict__ Y,
+                    int n, int B, double h, double g0, double g1, double g2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int64_t d = i / B;
+  const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
+  const double g = ax == 0 ? g0 : (ax == 1 ? g1 : g2);
+  const double f = Fext ? Fext[i] / mass[node] : 0.0;
+  Y[i] = X[i] + h * V[i] + h * h * (g + f);
+}
+
+// ----------------------------------------------------------------- K1: local step
+// One thread per (element, sim).  Writes EF[e][a][axis][b] and EE[e][b].
+__global__ void __launch_bounds__(128) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
+                                                       double* __restrict__ EF, double* __restrict__ EE) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  if (tid >= (int64_t)ea.m * B) return;
+  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
+  double xe[8][3];
+  for (int a = 0; a < 8; ++a) {
+    const int node = ea.hex8[8 * (int64_t)e + a];
+    for (int i = 0; i < 3; ++i) xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
+  }
+  const double w = ea.w_sim[b];
+  const double r_act = (st.w_m != 0.0 && ea.act) ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
+  double f[8][3];
+  for (int a = 0; a < 8; ++a) f[a][0] = f[a][1] = f[a][2] = 0.0;
+  double energy = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    double F[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0;
+        for (int a = 0; a < 8; ++a) s += xe[a][i] * st.dN[q][a][j];
+        F[3 * i + j] = s;
+      }
+    double R[9];
+    polar_rotation(F, R);
+    double Pm[9];
+    double en = 0;
+    for (int k = 0; k < 9; ++k) {
+      const double dk = F[k] - R[k];
+      en += dk * dk;
+      Pm[k] = w * st.V * dk;
+    }
+    energy += 0.5 * w * st.V * en;
+    if (st.w_m != 0.0) {
+      double Fm[3], nr = 0;
+      for (int i = 0; i < 3; ++i) {
+        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+        nr += Fm[i] * Fm[i];
+      }
+      nr = sqrt(nr);
+      double dm[3], em = 0;
+      for (int i = 0; i < 3; ++i) {
+        const double p = nr > 0 ? r_act * Fm[i] / nr : r_act * st.fiber[i];
+        dm[i] = Fm[i] - p;
+        em += dm[i] * dm[i];
+      }
+      energy += 0.5 * st.w_m * st.V * em;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
+    }
+    for (int a = 0; a < 8; ++a)
+      for (int i = 0; i < 3; ++i)
+        f[a][i] += Pm[3 * i] * st.dN[q][a][0] + Pm[3 * i + 1] * st.dN[q][a][1] + Pm[3 * i + 2] * st.dN[q][a][2];
+  }
+  for (int a = 0; a < 8; ++a)
+    for (int i = 0; i < 3; ++i) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = f[a][i];
+  if (EE) EE[(int64_t)e * B + b] = energy;
+}
+
+// Rotations of every quad point (diagnostic / parity hook).
+__global__ void k_elem_rotations(const double* __restrict__ X, Stencil st, const int32_t* __restrict__ hex8,
+                                 int m, int B, double* __restrict__ Rout) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)m * B) return;
+  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
+  double xe[8][3];
+  for (int a = 0; a < 8; ++a) {
+    const int node = hex8[8 * (int64_t)e + a];
+    for (int i = 0; i < 3; ++i) xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
+  }
+  for (int q = 0; q < 8; ++q) {
+    double F[9], R[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0;
+        for (int a = 0; a < 8; ++a) s += xe[a][i] * st.dN[q][a][j];
+        F[3 * i + j] = s;
+      }
+    polar_rotation(F, R);
+    for (int k = 0; k < 9; ++k) Rout[(((int64_t)b * m + e) * 8 + q) * 9 + k] = R[k];
+  }
+}
+
+// ----------------------------------------------------------------- K4: A_N p (matrix-free)
+// dR[dF] = R [w]x with (tr S I - S) w = vee(R^T dF - dF^T R), eigenvalues floored at
+// clamp * max|eig S|; muscle dp = (r/||Fm||)(I - n n^T) dFm.
+__device__ void solve_rot_derivative(const double* S, const double* rhs, double clamp, double* om) {
+  double tr = S[0] + S[4] + S[8];
+  double M[9];
+  for (int i = 0; i < 9; ++i) M[i] = -S[i];
+  M[0] += tr; M[4] += tr; M[8] += tr;
+  double sn = 0;
+  for (int i = 0; i < 9; ++i) sn += S[i] * S[i];
+  const double fub = clamp * sqrt(sn);  // >= clamp * max|eig S|
+  // fast path: Cholesky of M - fub I succeeds => no eigenvalue below the floor
+  const double a00 = M[0] - fub, a11 = M[4] - fub, a22 = M[8] - fub;
+  bool fast = a00 > 0;
+  double l10 = 0, l20 = 0, l11 = 0, l21 = 0, l22 = 0;
+  if (fast) {
+    const double l00 = sqrt(a00);
+    l10 = M[3] / l00; l20 = M[6] / l00;
+    const double t11 = a11 - l10 * l10;
+    fast = t11 > 0;
+    if (fast) {
+      l11 = sqrt(t11);
+      l21 = (M[7] - l20 * l10) / l11;
+      fast = a22 - l20 * l20 - l21 * l21 > 0;
+    }
+  }
+  if (fast) {
+    double C[9];
+    cof3(M, C);  // M symmetric: M^{-1} = C^T / det = C / det
+    const double idet = 1.0 / (M[0] * C[0] + M[1] * C[1] + M[2] * C[2]);
+    for (int i = 0; i < 3; ++i) om[i] = (C[3 * i] * rhs[0] + C[3 * i + 1] * rhs[1] + C[3 * i + 2] * rhs[2]) * idet;
+    return;
+  }
+  double lam[3], V[9];
+  jacobi_eig3(S, lam, V);
+  const double mx = fmax(fabs(lam[0]), fmax(fabs(lam[1]), fabs(lam[2])));
+  const double floor_ = clamp * mx;
+  double t[3];
+  for (int k = 0; k < 3; ++k) t[k] = V[k] * rhs[0] + V[3 + k] * rhs[1] + V[6 + k] * rhs[2];
+  for (int k = 0; k < 3; ++k) {
+    const double ev = fmax(tr - lam[k], floor_);
+    t[k] /= ev;
+  }
+  for (int i = 0; i < 3; ++i) om[i] = V[3 * i] * t[0] + V[3 * i + 1] * t[1] + V[3 * i + 2] * t[2];
+}
+
+__global__ void __launch_bounds__(128) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
+                                                 Stencil st, ElemArgs ea, double* __restrict__ EF) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  if (tid >= (int64_t)ea.m * B) return;
+  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
+  double xe[8][3], pe[8][3];
+  for (int a = 0; a < 8; ++a) {
+    const int node = ea.hex8[8 * (int64_t)e + a];
+    for (int i = 0; i < 3; ++i) {
+      xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
+      pe[a][i] = Pv[(3 * (int64_t)node + i) * B + b];
+    }
+  }
+  const double w = ea.w_sim[b];
+  const double r_act = (st.w_m != 0.0 && ea.act) ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
+  double f[8][3];
+  for (int a = 0; a < 8; ++a) f[a][0] = f[a][1] = f[a][2] = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    double F[9], dF[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0, t = 0;
+        for (int a = 0; a < 8; ++a) {
+          s += xe[a][i] * st.dN[q][a][j];
+          t += pe[a][i] * st.dN[q][a][j];
+        }
+        F[3 * i + j] = s;
+        dF[3 * i + j] = t;
+      }
+    double R[9];
+    polar_rotation(F, R);
+    double S[9];  // S = R^T F, symmetrised
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) S[3 * i + j] = R[i] * F[j] + R[3 + i] * F[3 + j] + R[6 + i] * F[6 + j];
+    for (int i = 0; i < 3; ++i)
+      for (int j = i + 1; j < 3; ++j) {
+        const double avg = 0.5 * (S[3 * i + j] + S[3 * j + i]);
+        S[3 * i + j] = S[3 * j + i] = avg;
+      }
+    double Wm[9];  // R^T dF
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Wm[3 * i + j] = R[i] * dF[j] + R[3 + i] * dF[3 + j] + R[6 + i] * dF[6 + j];
+    // vee(W - W^T) = (W21 - W12, W02 - W20, W10 - W01)
+    const double rhs[3] = {Wm[7] - Wm[5], Wm[2] - Wm[6], Wm[3] - Wm[1]};
+    double om[3];
+    solve_rot_derivative(S, rhs, st.clamp, om);
+    // dR = R [om]x ; [om]x = [[0,-o2,o1],[o2,0,-o0],[-o1,o0,0]]
+    double Pm[9];
+    for (int i = 0; i < 3; ++i) {
+      const double r0 = R[3 * i], r1 = R[3 * i + 1], r2 = R[3 * i + 2];
+      const double dR0 = r1 * om[2] - r2 * om[1];
+      const double dR1 = -r0 * om[2] + r2 * om[0];
+      const double dR2 = r0 * om[1] - r1 * om[0];
+      Pm[3 * i] = w * st.V * (dF[3 * i] - dR0);
+      Pm[3 * i + 1] = w * st.V * (dF[3 * i + 1] - dR1);
+      Pm[3 * i + 2] = w * st.V * (dF[3 * i + 2] - dR2);
+    }
+    if (st.w_m != 0.0) {
+      double Fm[3], dFm[3], nr = 0;
+      for (int i = 0; i < 3; ++i) {
+        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+        dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+        nr += Fm[i] * Fm[i];
+      }
+      nr = sqrt(nr);
+      double jd[3] = {0, 0, 0};
+      if (nr > 0) {
+        const double nd = (Fm[0] * dFm[0] + Fm[1] * dFm[1] + Fm[2] * dFm[2]) / nr;
+        for (int i = 0; i < 3; ++i) jd[i] = r_act / nr * (dFm[i] - nd * Fm[i] / nr);
+      }
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * (dFm[i] - jd[i]) * st.fiber[j];
+    }
+    for (int a = 0; a < 8; ++a)
+      for (int i = 0; i < 3; ++i)
+        f[a][i] += Pm[3 * i] * st.dN[q][a][0] + Pm[3 * i + 1] * st.dN[q][a][1] + Pm[3 * i + 2] * st.dN[q][a][2];
+  }
+  for (int a = 0; a < 8; ++a)
+    for (int i = 0; i < 3; ++i) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = f[a][i];
+}
+
+// Parameter-gradient terms at x_{i+1} for adjoint u (chain rule):
+//   DW[e][b] = -sum_q V <G_q u_e, F_q - R_q>,  DR[e][b] = w_m sum_q V n_hat^T (G_q u_e) m
+__global__ void __launch_bounds__(128) k_elem_param(const double* __restrict__ X, const double* __restrict__ U,
+                                                    Stencil st, ElemArgs ea, double* __restrict__ DW,
+                                                    double* __restrict__ DR) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  if (tid >= (int64_t)ea.m * B) return;
+  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
+  double xe[8][3], ue[8][3];
+  for (int a = 0; a < 8; ++a) {
+    const int node = ea.hex8[8 * (int64_t)e + a];
+    for (int i = 0; i < 3; ++i) {
+      xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
+      ue[a][i] = U[(3 * (int64_t)node + i) * B + b];
+    }
+  }
+  double dw = 0, dr = 0;
+  for (int q = 0; q < 8; ++q) {
+    double F[9], dF[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0, t = 0;
+        for (int a = 0; a < 8; ++a) {
+          s += xe[a][i] * st.dN[q][a][j];
+          t += ue[a][i] * st.dN[q][a][j];
+        }
+        F[3 * i + j] = s;
+        dF[3 * i + j] = t;
+      }
+    double R[9];
+    polar_rotation(F, R);
+    double acc = 0;
+    for (int k = 0; k < 9; ++k) acc += dF[k] * (F[k] - R[k]);
+    dw -= st.V * acc;
+    if (st.w_m != 0.0 && DR) {
+      double Fm[3], dFm[3], nr = 0;
+      for (int i = 0; i < 3; ++i) {
+        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+        dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+        nr += Fm[i] * Fm[i];
+      }
+      nr = sqrt(nr);
+      double nh[3];
+      for (int i = 0; i < 3; ++i) nh[i] = nr > 0 ? Fm[i] / nr : st.fiber[i];
+      dr += st.w_m * st.V * (nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2]);
+    }
+  }
+  DW[(int64_t)e * B + b] = dw;
+  if (DR) DR[(int64_t)e * B + b] = dr;
+}
+
+// ----------------------------------------------------------------- K2: deterministic gather
+// mode 0: G = M/h^2 (X - Y) + sum EF   (grad g)       W = M/h^2 Y  (residual normaliser)
+// mode 1: G = M/h^2 X + sum EF         (A_N p, X = p)  W unused
+// Constrained DoFs (fixed nodes; pinned z DoFs when PIN != null) get G = 0, W = 0; the raw
+// value of a pinned DoF is stored in LAM[j*B + b] (contact multiplier).
+__global__ void k_gather(const double* __restrict__ X, const double* __restrict__ Y, const double* __restrict__ EF,
+                         const double* __restrict__ mass, const int32_t* __restrict__ inc_ptr,
+                         const int32_t* __restrict__ inc_ec, const uint8_t* __restrict__ fixed,
+                         const int32_t* __restrict__ pos_of_node, int n, int B, double inv_h2, int mode,
+                         double* __restrict__ G, double* __restrict__ W, double* __restrict__ RHS,
+                         const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
+                         double* __restrict__ LAM) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)n * B) return;
+  const int node = (int)(tid / B), b = (int)(tid - (int64_t)node * B);
+  const int R = 3 * B;
+  const double mh = mass[node] * inv_h2;
+  const int k0 = inc_ptr[node], k1 = inc_ptr[node + 1];
+  const bool fx = fixed[node] != 0;
+  const int pos = pos_of_node[node];
+  const int cj = cand_of_node ? cand_of_node[node] : -1;
+  for (int ax = 0; ax < 3; ++ax) {
+    const int64_t i = (3 * (int64_t)node + ax) * B + b;
+    double s = 0;
+    for (int k = k0; k < k1; ++k) s += EF[((int64_t)inc_ec[k] * 3 + ax) * B + b];
+    double g = mode == 0 ? mh * (X[i] - Y[i]) + s : mh * X[i] + s;
+    double wv = mode == 0 ? mh * Y[i] : 0.0;
+    bool pinned = false;
+    if (ax == 2 && cj >= 0 && PIN) {
+      pinned = PIN[(int64_t)cj * B + b] != 0;
+      if (LAM) LAM[(int64_t)cj * B + b] = pinned ? g : 0.0;
+    }
+    if (fx || pinned) { g = 0.0; wv = 0.0; }
+    G[i] = g;
+    if (W && mode == 0) W[i] = wv;
+    if (RHS && pos >= 0) RHS[(int64_t)pos * R + ax * B + b] = g;
+  }
+}
+
+// state (free nodes) -> permuted solve vector
+__global__ void k_to_solve(const double* __restrict__ Xs, const int32_t* __restrict__ node_of_pos, int nfree, int B,
+                           double* __restrict__ S) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int R = 3 * B;
+  if (i >= (int64_t)nfree * R) return;
+  const int64_t pos = i / R;
+  const int rr = (int)(i - pos * R);
+  S[i] = Xs[3 * (int64_t)node_of_pos[pos] * B + rr];
+}
+// permuted solve vector -> state: OUT = beta*OUT + alpha[b]*S on free nodes (fixed: OUT = beta*OUT)
+// masked by ACTIVE[b] (inactive sims untouched).
+__global__ void k_from_solve(const double* __restrict__ S, const int32_t* __restrict__ pos_of_node, int n, int B,
+                             const double* __restrict__ alpha, double alpha_c, double beta,
+                             const int32_t* __restrict__ active, double* __restrict__ OUT) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  if (active && !active[b]) return;
+  const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
+  const int pos = pos_of_node[node];
+  const double a = alpha ? alpha[b] * alpha_c : alpha_c;
+  const double base = beta == 0.0 ? 0.0 : beta * OUT[i];
+  OUT[i] = pos >= 0 ? base + a * S[(int64_t)pos * 3 * B + ax * B + b] : base;
+}
+
+// ----------------------------------------------------------------- K3: supernodal solves
+// Forward L y = b: phase A  t[J_s] = b[J_s] - sum_d L[J_s, J_d] y[J_d]  (pull, fixed d order)
+__global__ void k_fwdA(SolveArgs sa, int tile0, int R, const double* __restrict__ rhs, const double* __restrict__ y,
+                       double* __restrict__ t) {
+  extern __shared__ double acc[];
+  const int tile = tile0 + blockIdx.x;
+  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
+  const int nt = r1 - r0, f = sa.sfirst[s];
+  const int64_t base = (int64_t)(f + r0) * R;
+  for (int i = threadIdx.x; i < nt * R; i += blockDim.x) acc[i] = rhs[base + i];
+  __syncthreads();
+  for (int bk = sa.tblk_ptr[tile]; bk < sa.tblk_ptr[tile + 1]; ++bk) {
+    const int d = sa.blk_d[bk], k0 = sa.blk_k0[bk], k1 = sa.blk_k1[bk];
+    const int nd = sa.ssize[d];
+    const double* Pd = sa.P + sa.poff[d];
+    const int32_t* Rd = sa.rows + sa.rptr[d];
+    const double* yd = y + (int64_t)sa.sfirst[d] * R;
+    for (int idx = threadIdx.x; idx < (k1 - k0) * R; idx += blockDim.x) {
+      const int kk = idx / R, r = idx - kk * R, k = k0 + kk;
+      const double* prow = Pd + (int64_t)k * nd;
+      double sum = 0;
+      for (int j = 0; j < nd; ++j) sum += prow[j] * yd[(int64_t)j * R + r];
+      acc[(Rd[k] - f - r0) * R + r] -= sum;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nt * R; i += blockDim.x) t[base + i] = acc[i];
+}
+// Forward phase B: y[J_s] = D_s t[J_s]   (D_s = L_ss^{-1}, packed lower)
+__global__ void k_fwdB(SolveArgs sa, int tile0, int R, const double* __restrict__ t, double* __restrict__ y) {
+  const int tile = tile0 + blockIdx.x;
+  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
+  const int f = sa.sfirst[s];
+  const double* D = sa.D + sa.doff[s];
+  const double* ts = t + (int64_t)f * R;
+  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
+    const int ii = idx / R, r = idx - ii * R, i = r0 + ii;
+    const double* drow = D + (int64_t)i * (i + 1) / 2;
+    double sum = 0;
+    for (int j = 0; j <= i; ++j) sum += drow[j] * ts[(int64_t)j * R + r];
+    y[(int64_t)(f + i) * R + r] = sum;
+  }
+}
+// Backward L^T x = y: phase A  t[J_s] = y[J_s] - L[R_s, J_s]^T x[R_s]
+__global__ void k_bwdA(SolveArgs sa, int tile0, int R, const double* __restrict__ y, const double* __restrict__ x,
+                       double* __restrict__ t) {
+  const int tile = tile0 + blockIdx.x;
+  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
+  const int f = sa.sfirst[s], ns = sa.ssize[s];
+  const int nr = (int)(sa.rptr[s + 1] - sa.rptr[s]);
+  const double* Ps = sa.P + sa.poff[s];
+  const int32_t* Rs = sa.rows + sa.rptr[s];
+  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
+    const int cc = idx / R, r = idx - cc * R, c = r0 + cc;
+    double sum = y[(int64_t)(f + c) * R + r];
+    for (int k = 0; k < nr; ++k) sum -= Ps[(int64_t)k * ns + c] * x[(int64_t)Rs[k] * R + r];
+    t[(int64_t)(f + c) * R + r] = sum;
+  }
+}
+// Backward phase B: x[J_s] = D_s^T t[J_s]
+__global__ void k_bwdB(SolveArgs sa, int tile0, int R, const double* __restrict__ t, double* __restrict__ x) {
+  const int tile = tile0 + blockIdx.x;
+  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
+  const int f = sa.sfirst[s], ns = sa.ssize[s];
+  const double* D = sa.D + sa.doff[s];
+  const double* ts = t + (int64_t)f * R;
+  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
+    const int cc = idx / R, r = idx - cc * R, c = r0 + cc;
+    double sum = 0;
+    for (int i = c; i < ns; ++i) sum += D[(int64_t)i * (i + 1) / 2 + c] * ts[(int64_t)i * R + r];
+    x[(int64_t)(f + c) * R + r] = sum;
+  }
+}
+
+// ----------------------------------------------------------------- per-sim reductions
+// partial[c][b] = sum over chunk c of u*v (up to 3 pairs); blockDim % B == 0 so that each
+// thread keeps one sim; fixed-order tree inside the block, fixed-order sum over chunks.
+__global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, double* __restrict__ partial) {
+  extern __shared__ double red[];
+  const int nb = blockDim.x;
+  const int b = threadIdx.x % B;
+  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
+  double acc[3] = {0, 0, 0};
+  for (int64_t i = beg + threadIdx.x; i < end; i += nb)
+    for (int p = 0; p < da.npairs; ++p) acc[p] += da.u[p][i] * da.v[p][i];
+  for (int p = 0; p < da.npairs; ++p) {
+    red[threadIdx.x] = acc[p];
+    __syncthreads();
+    // threads with the same b: t = b + B*j, j < nb/B; pairwise tree over j
+    const int J = nb / B;
+    for (int step = 1; step < J; step <<= 1) {
+      const int j = threadIdx.x / B;
+      if ((j % (2 * step)) == 0 && j + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
+      __syncthreads();
+    }
+    if (threadIdx.x < B) partial[((int64_t)p * gridDim.x + blockIdx.x) * B + threadIdx.x] = red[threadIdx.x];
+    __syncthreads();
+  }
+}
+__global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npairs * B) return;
+  const int p = i / B, b = i - p * B;
+  double s = 0;
+  for (int c = 0; c < nchunk; ++c) s += partial[((int64_t)p * nchunk + c) * B + b];
+  out[i] = s;
+}
+// sum over elements of E[e][b] (deterministic) -> out[b] (+= if accumulate)
+__global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* __restrict__ out, int accumulate) {
+  extern __shared__ double red[];
+  const int b = blockIdx.x;
+  double s = 0;
+  for (int e = threadIdx.x; e < m; e += blockDim.x) s += E[(int64_t)e * B + b];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[b] = accumulate ? out[b] + red[0] : red[0];
+}
+
+// ----------------------------------------------------------------- iteration control
+// Forward convergence: res = sqrt(res2/den2); active[b] for the NEXT update.
+__global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, int iter, int fixed_iter,
+                            int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
+                            double* __restrict__ res_out, int32_t* __restrict__ flag_out,
+                            int32_t* __restrict__ nactive) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (!active[b]) return;
+  const double den = dots[B + b];
+  const double res = den > 0 ? sqrt(dots[b] / den) : sqrt(dots[b]);
+  bool go;
+  if (fixed_iter > 0) go = iter < fixed_iter;
+  else go = res > tol && iter < max_iter;
+  res_out[b] = res;
+  iters_out[b] = iter;
+  if (!go) {
+    active[b] = 0;
+    flag_out[b] = (fixed_iter == 0 && res > tol) ? 1 : 0;
+  } else {
+    atomicAdd(nactive, 1);  // integer count only (no effect on arithmetic)
+  }
+}
+
+// v = (x - xprev)/h
+__global__ void k_velocity(const double* __restrict__ X, const double* __restrict__ Xp, double* __restrict__ V,
+                           int64_t len, double inv_h) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < len) V[i] = (X[i] - Xp[i]) * inv_h;
+}
+
+// generic per-sim axpy on state vectors: Y[i] = a*X[i] + c[b]*cs*Z[i] (+ masks)
+__global__ void k_axpby(double* __restrict__ Y, const double* __restrict__ X, double a, const double* __restrict__ Z,
+                        const double* __restrict__ c, double cs, int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (active && !active[b]) return;
+  double v = X ? a * X[i] : 0.0;
+  if (Z) v += (c ? c[b] : 1.0) * cs * Z[i];
+  Y[i] = v;
+}
+// zero fixed nodes (and pinned z DoFs) of a state vector
+__global__ void k_zero_constrained(double* __restrict__ Y, const uint8_t* __restrict__ fixed, int n, int B,
+                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
+  bool z = fixed[node] != 0;
+  if (!z && ax == 2 && PIN && cand_of_node[node] >= 0) z = PIN[(int64_t)cand_of_node[node] * B + b] != 0;
+  if (z) Y[i] = 0.0;
+}
+
+// Adjoint PCG scalars.  dots layout: [0:B) first pair, [B:2B) second ...
+// alpha = rz / pq ; converged check on rr / bb.
+__global__ void k_pcg_alpha(const double* __restrict__ rz, const double* __restrict__ pq, double* __restrict__ alpha,
+                            const int32_t* __restrict__ active, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  const double d = pq[b];
+  alpha[b] = d != 0.0 ? rz[b] / d : 0.0;
+}
+__global__ void k_pcg_beta(const double* __restrict__ rz_new, double* __restrict__ rz, double* __restrict__ beta,
+                           const int32_t* __restrict__ active, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  beta[b] = rz[b] != 0.0 ? rz_new[b] / rz[b] : 0.0;
+  rz[b] = rz_new[b];
+}
+__global__ void k_adj_check(const double* __restrict__ rr, const double* __restrict__ bb, int B, double tol, int iter,
+                            int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
+                            double* __restrict__ res_out, int32_t* __restrict__ flag_out, int32_t* __restrict__ nactive) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  const double res = bb[b] > 0 ? sqrt(rr[b] / bb[b]) : 0.0;
+  res_out[b] = res;
+  iters_out[b] = iter;
+  const bool go = res > tol && iter < max_iter;
+  if (!go) {
+    active[b] = 0;
+    flag_out[b] = res > tol ? 1 : 0;
+  } else {
+    atomicAdd(nactive, 1);
+  }
+}
+
+// a_x = (M/h^2) u - a_v/h ; a_v = (M/h) u ; zero on fixed nodes  (eq:pre_adjoint)
+__global__ void k_adj_state(const double* __restrict__ U, const double* __restrict__ mass, const uint8_t* __restrict__ fixed,
+                            double* __restrict__ AX, double* __restrict__ AV, int n, int B, double h) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int node = (int)(i / B / 3);
+  if (fixed[node]) { AX[i] = 0.0; AV[i] = 0.0; return; }
+  const double u = U[i], mm = mass[node];
+  const double av = AV[i];
+  AX[i] = mm / (h * h) * u - av / h;
+  AV[i] = mm / h * u;
+}
+
+}  // namespace pdb

@@ -1,0 +1,42 @@
+// sm_100a fp64 device kernels of the DiffPD hot path.
+//
+// Layouts:
+//   state   [n][3][B]      index (3*node + axis)*B + b       (sims fastest: coalesced over b)
+//   solve   [nfree][R]     index pos*R + axis*B + b, R = 3B  (A = A_s (x) I_3: 3B RHS per row)
+//   elemF   [m][8][3][B]   per-element nodal force contributions (deterministic gather input)
+#pragma once
+#include <cstdint>
+
+namespace pdb {
+
+struct Stencil {
+  double dN[8][8][3];  // dN[q][a][j]
+  double fiber[3];
+  double V;            // quadrature weight dx^3/8
+  double w_m;          // muscle weight (0 = off)
+  double clamp;        // eigenvalue floor factor of the polar derivative (1e-6)
+};
+
+struct ElemArgs {
+  const int32_t* hex8;
+  int m, B;
+  const double* w_sim;     // [B] corotated weight per sim
+  const double* act;       // actuation base for this step: act[b*act_bstride + e], or null
+  int64_t act_bstride;
+};
+
+struct SolveArgs {
+  const int32_t *sfirst, *ssize;
+  const int64_t *rptr, *doff, *poff;
+  const int32_t* rows;
+  const double *D, *P;
+  const int32_t *tile_sup, *tile_r0, *tile_r1, *tblk_ptr, *blk_d, *blk_k0, *blk_k1;
+};
+
+struct DotArgs {
+  const double* u[3];
+  const double* v[3];
+  int npairs;
+};
+
+}  // namespace pdb

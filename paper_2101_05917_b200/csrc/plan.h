@@ -1,0 +1,59 @@
+// Internal host-side plan of a pd_sim: mesh stencil, ordering, supernodal factor
+// of the scalar PD matrix A_s (A = A_s (x) I_3) and the level
+// schedule of the batched triangular solves.  Host-only (no CUDA types).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace pdb {
+
+constexpr int kTile = 32;  // rows per triangular-solve tile
+
+struct HostPlan {
+  // ---- mesh ----
+  int n = 0, m = 0;
+  double dx = 0, h = 0;
+  std::vector<double> rest;         // [n][3]
+  std::vector<int32_t> hex8;        // [m][8]
+  std::vector<double> node_mass;    // [n] lumped
+  std::vector<uint8_t> fixed_node;  // [n]
+  double dN[8][8][3];               // dN[q][a][j] = dN_a/dX_j at Gauss point q
+  double Kc[8][8];                  // sum_q V dN_a . dN_b            (corotated, unit w)
+  double Km[8][8];                  // sum_q V (dN_a.m)(dN_b.m)       (muscle, unit w_m)
+  double w_ref = 0, w_m = 0;        // weights of the factorised A
+  // node -> incident (element, corner) CSR sorted by element (deterministic gather)
+  std::vector<int32_t> inc_ptr, inc_ec;  // ec = 8*e + a
+  // ---- ordering ----
+  int nfree = 0;
+  std::vector<int32_t> pos_of_node;  // [n] solver position or -1 (fixed)
+  std::vector<int32_t> node_of_pos;  // [nfree]
+  // ---- scalar A_s over free nodes in solver order (CSR, full symmetric) ----
+  std::vector<int64_t> a_ptr;
+  std::vector<int32_t> a_col;
+  std::vector<double> a_val;
+  // ---- supernodes (ND tree; children precede parents) ----
+  int nsup = 0;
+  std::vector<int32_t> sfirst, ssize, parent, height;
+  std::vector<int64_t> rptr;         // [nsup+1] into rows
+  std::vector<int32_t> rows;         // below-block row positions (sorted, > last col)
+  std::vector<int64_t> doff, poff;   // offsets of D_s (packed lower, = L_ss^{-1}) and P_s
+  std::vector<double> D, P;          // P_s = L[R_s, J_s] row-major (nr x ns)
+  int64_t nnzL = 0;                  // stored entries of L_s (diag blocks packed + panels)
+  double factor_flops = 0, factor_ms = 0;
+  // ---- solve schedule ----
+  int nlevels = 0;
+  std::vector<int32_t> lvl_ptr;      // [nlevels+1] into tiles (tiles grouped by height)
+  std::vector<int32_t> tile_sup, tile_r0, tile_r1;
+  std::vector<int32_t> tblk_ptr;     // [ntiles+1] forward update blocks per tile
+  std::vector<int32_t> blk_d, blk_k0, blk_k1;
+};
+
+// Build everything host-side.  Returns "" on success, else an error message;
+// *numerical is set when the failure is a non-SPD pivot.
+std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
+                       double dx, double density, double h, const int32_t* fixed_dofs,
+                       int n_fixed, double w_ref, double w_m, const double fiber[3],
+                       bool* numerical);
+
+}  // namespace pdb

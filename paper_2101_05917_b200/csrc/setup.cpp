@@ -1,0 +1,531 @@
+// Host setup of the B200 DiffPD path (timed separately from the hot path).
+//
+//  * voxel-mesh validation, 8-point Gauss stencil of the trilinear hex (reading
+//    DESIGN.md §2.1), lumped mass;
+//  * the scalar PD matrix A_s = M_s/h^2 + sum_e sum_q V (w dN_a.dN_b + w_m (dN_a.m)(dN_b.m)):
+//    since G maps every coordinate axis identically for the corotated and the
+//    muscle energies, A = M/h^2 + sum w G^T G equals A_s (x) I_3
+//    exactly, and its Cholesky factor is L_s (x) I_3;
+//  * geometric nested dissection on the voxel lattice, ND-tree supernodes,
+//    multifrontal numeric Cholesky computed ONCE, diagonal blocks
+//    stored inverted (D_s = L_ss^{-1}) so the per-iteration solves are products;
+//  * the level schedule (tiles + forward update blocks) of the batched solves.
+#include "plan.h"
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <omp.h>
+
+namespace pdb {
+namespace {
+
+constexpr int kLeaf = 48;  // max nodes in an ND leaf
+
+struct NDNode {
+  std::vector<int32_t> nodes;  // mesh node ids in final order
+  int left = -1, right = -1;
+};
+
+}  // namespace
+
+static void stencil(HostPlan& P, const double fiber[3]) {
+  const double g = 1.0 / std::sqrt(3.0);
+  for (int q = 0; q < 8; ++q) {
+    const double xi[3] = {(2 * (q & 1) - 1) * g, (2 * ((q >> 1) & 1) - 1) * g,
+                          (2 * ((q >> 2) & 1) - 1) * g};
+    for (int a = 0; a < 8; ++a) {
+      const double s[3] = {double(2 * (a & 1) - 1), double(2 * ((a >> 1) & 1) - 1),
+                           double(2 * ((a >> 2) & 1) - 1)};
+      for (int j = 0; j < 3; ++j) {
+        double v = s[j] / 8.0;
+        for (int k = 0; k < 3; ++k)
+          if (k != j) v *= (1.0 + s[k] * xi[k]);
+        P.dN[q][a][j] = v * 2.0 / P.dx;
+      }
+    }
+  }
+  const double V = P.dx * P.dx * P.dx / 8.0;
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) {
+      double kc = 0, km = 0;
+      for (int q = 0; q < 8; ++q) {
+        double dd = 0, ma = 0, mb = 0;
+        for (int j = 0; j < 3; ++j) {
+          dd += P.dN[q][a][j] * P.dN[q][b][j];
+          ma += P.dN[q][a][j] * fiber[j];
+          mb += P.dN[q][b][j] * fiber[j];
+        }
+        kc += V * dd;
+        km += V * ma * mb;
+      }
+      P.Kc[a][b] = kc;
+      P.Km[a][b] = km;
+    }
+}
+
+// ---------------------------------------------------------------- dense kernels
+// Front F is row-major f x f (lower triangle used).
+static bool potrf_lower(double* F, int f, int ns, bool par) {
+  // Right-looking column Cholesky of the leading ns x ns block, rows ns.. get L21.
+  for (int j = 0; j < ns; ++j) {
+    double d = F[(int64_t)j * f + j];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    d = std::sqrt(d);
+    F[(int64_t)j * f + j] = d;
+    const double inv = 1.0 / d;
+    for (int i = j + 1; i < f; ++i) F[(int64_t)i * f + j] *= inv;
+    // update columns j+1..ns-1 of all rows below (within the first ns columns)
+#pragma omp parallel for schedule(dynamic, 16) if (par && (f - j) > 256)
+    for (int i = j + 1; i < f; ++i) {
+      const double lij = F[(int64_t)i * f + j];
+      if (lij == 0.0) continue;
+      double* Fi = F + (int64_t)i * f;
+      const int kmax = std::min(i, ns - 1);
+      for (int k = j + 1; k <= kmax; ++k) Fi[k] -= lij * F[(int64_t)k * f + j];
+    }
+  }
+  return true;
+}
+
+// Blocked variant for large fronts: factor panels of nb columns, then update.
+static bool partial_cholesky(double* F, int f, int ns, bool par) {
+  const int nb = 64;
+  if (ns <= nb || f < 512) return potrf_lower(F, f, ns, par);
+  for (int j0 = 0; j0 < ns; j0 += nb) {
+    const int j1 = std::min(ns, j0 + nb);
+    // factor the panel columns j0..j1 (unblocked, only within the panel)
+    for (int j = j0; j < j1; ++j) {
+      double d = F[(int64_t)j * f + j];
+      if (!(d > 0.0) || !std::isfinite(d)) return false;
+      d = std::sqrt(d);
+      F[(int64_t)j * f + j] = d;
+      const double inv = 1.0 / d;
+      for (int i = j + 1; i < f; ++i) F[(int64_t)i * f + j] *= inv;
+#pragma omp parallel for schedule(static) if (par && (f - j) > 1024)
+      for (int i = j + 1; i < f; ++i) {
+        double* Fi = F + (int64_t)i * f;
+        const double lij = Fi[j];
+        const int kmax = std::min(i, j1 - 1);
+        for (int k = j + 1; k <= kmax; ++k) Fi[k] -= lij * F[(int64_t)k * f + j];
+      }
+    }
+    // trailing update of columns j1..ns-1 (rows >= j1): F[i][k] -= sum_{j in panel} L[i][j] L[k][j]
+#pragma omp parallel for schedule(dynamic, 8) if (par)
+    for (int i = j1; i < f; ++i) {
+      double* Fi = F + (int64_t)i * f;
+      const int kmax = std::min(i, ns - 1);
+      for (int k = j1; k <= kmax; ++k) {
+        const double* Fk = F + (int64_t)k * f;
+        double s = 0;
+        for (int j = j0; j < j1; ++j) s += Fi[j] * Fk[j];
+        Fi[k] -= s;
+      }
+    }
+  }
+  return true;
+}
+
+// U = F22 - L21 L21^T (lower), F22 = F[ns.., ns..], L21 = F[ns.., 0..ns)
+static void schur_update(double* F, int f, int ns, bool par) {
+  const int nr = f - ns;
+  if (nr <= 0) return;
+  const int bs = 48;
+#pragma omp parallel for schedule(dynamic, 1) if (par && nr > 64)
+  for (int ib = 0; ib < nr; ib += bs) {
+    const int ie = std::min(nr, ib + bs);
+    for (int kb = 0; kb <= ib; kb += bs) {
+      const int ke = std::min(nr, kb + bs);
+      for (int jb = 0; jb < ns; jb += 256) {
+        const int je = std::min(ns, jb + 256);
+        for (int i = ib; i < ie; ++i) {
+          double* Fi = F + (int64_t)(ns + i) * f;
+          const int kk = std::min(ke - 1, i);
+          for (int k = kb; k <= kk; ++k) {
+            const double* Fk = F + (int64_t)(ns + k) * f;
+            double s = 0;
+            for (int j = jb; j < je; ++j) s += Fi[j] * Fk[j];
+            Fi[ns + k] -= s;
+          }
+        }
+      }
+    }
+  }
+}
+
+// D = L11^{-1} packed lower (row i at i(i+1)/2), from the ns x ns block of F.
+static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
+#pragma omp parallel for schedule(dynamic, 4) if (par && ns > 128)
+  for (int c = 0; c < ns; ++c) {
+    // column c of X: X[c][c] = 1/L[c][c]; X[i][c] = -(sum_{k=c}^{i-1} L[i][k] X[k][c]) / L[i][i]
+    D[(int64_t)c * (c + 1) / 2 + c] = 1.0 / F[(int64_t)c * f + c];
+    for (int i = c + 1; i < ns; ++i) {
+      const double* Fi = F + (int64_t)i * f;
+      double s = 0;
+      for (int k = c; k < i; ++k) s += Fi[k] * D[(int64_t)k * (k + 1) / 2 + c];
+      D[(int64_t)i * (i + 1) / 2 + c] = -s / Fi[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- build
+std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
+                       double dx, double density, double h, const int32_t* fixed_dofs,
+                       int n_fixed, double w_ref, double w_m, const double fiber[3],
+                       bool* numerical) {
+  *numerical = false;
+  if (n <= 0 || m <= 0 || !rest || !hex8) return "empty mesh";
+  if (!(dx > 0) || !(h > 0)) return "dx and h must be > 0";
+  P.n = n;
+  P.m = m;
+  P.dx = dx;
+  P.h = h;
+  P.w_ref = w_ref;
+  P.w_m = w_m;
+  P.rest.assign(rest, rest + 3 * (int64_t)n);
+  P.hex8.assign(hex8, hex8 + 8 * (int64_t)m);
+  // voxel check: corner a of element e sits at corner0 + dx (di, dj, dk)
+  for (int e = 0; e < m; ++e) {
+    const int32_t* c = hex8 + 8 * (int64_t)e;
+    for (int a = 0; a < 8; ++a)
+      if (c[a] < 0 || c[a] >= n) return "element " + std::to_string(e) + " has an out-of-range node";
+    for (int a = 0; a < 8; ++a)
+      for (int b = a + 1; b < 8; ++b)
+        if (c[a] == c[b]) return "element " + std::to_string(e) + " repeats a node";
+    const double* x0 = rest + 3 * (int64_t)c[0];
+    for (int a = 1; a < 8; ++a) {
+      const double off[3] = {double(a & 1), double((a >> 1) & 1), double((a >> 2) & 1)};
+      for (int j = 0; j < 3; ++j)
+        if (std::fabs(rest[3 * (int64_t)c[a] + j] - x0[j] - dx * off[j]) > 1e-9 * dx)
+          return "element " + std::to_string(e) + " is not an axis-aligned voxel of edge dx";
+    }
+  }
+  stencil(P, fiber);
+  P.node_mass.assign(n, 0.0);
+  for (int e = 0; e < m; ++e)
+    for (int a = 0; a < 8; ++a) P.node_mass[hex8[8 * (int64_t)e + a]] += density * dx * dx * dx / 8.0;
+  for (int i = 0; i < n; ++i)
+    if (!(P.node_mass[i] > 0)) return "node " + std::to_string(i) + " belongs to no element";
+  // fixed DoFs must cover whole nodes (A = A_s (x) I_3)
+  P.fixed_node.assign(n, 0);
+  {
+    std::vector<uint8_t> fd(3 * (int64_t)n, 0);
+    for (int k = 0; k < n_fixed; ++k) {
+      if (fixed_dofs[k] < 0 || fixed_dofs[k] >= 3 * n) return "fixed DoF out of range";
+      fd[fixed_dofs[k]] = 1;
+    }
+    for (int i = 0; i < n; ++i) {
+      const int s = fd[3 * i] + fd[3 * i + 1] + fd[3 * i + 2];
+      if (s != 0 && s != 3) return "fixed DoFs must fix all three axes of a node";
+      P.fixed_node[i] = s == 3;
+    }
+  }
+  // incidence (sorted by element id: the deterministic summation order of the gather)
+  P.inc_ptr.assign(n + 1, 0);
+  for (int e = 0; e < m; ++e)
+    for (int a = 0; a < 8; ++a) P.inc_ptr[hex8[8 * (int64_t)e + a] + 1]++;
+  for (int i = 0; i < n; ++i) P.inc_ptr[i + 1] += P.inc_ptr[i];
+  P.inc_ec.assign(P.inc_ptr[n], 0);
+  {
+    std::vector<int32_t> fill(P.inc_ptr.begin(), P.inc_ptr.end() - 1);
+    for (int e = 0; e < m; ++e)
+      for (int a = 0; a < 8; ++a) P.inc_ec[fill[hex8[8 * (int64_t)e + a]]++] = 8 * e + a;
+  }
+
+  // ---------------- nested dissection on the lattice of free nodes
+  double mn[3] = {1e300, 1e300, 1e300};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 3; ++j) mn[j] = std::min(mn[j], rest[3 * (int64_t)i + j]);
+  std::vector<int32_t> lat(3 * (int64_t)n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 3; ++j) lat[3 * (int64_t)i + j] = (int32_t)std::llround((rest[3 * (int64_t)i + j] - mn[j]) / dx);
+  std::vector<int32_t> freeNodes;
+  for (int i = 0; i < n; ++i)
+    if (!P.fixed_node[i]) freeNodes.push_back(i);
+  P.nfree = (int)freeNodes.size();
+  if (P.nfree == 0) return "every node is fixed";
+
+  std::vector<std::vector<int32_t>> supNodes;  // in creation (post) order
+  std::vector<int32_t> supParent;
+  auto lexless = [&](int32_t a, int32_t b) {
+    for (int j = 2; j >= 0; --j)
+      if (lat[3 * (int64_t)a + j] != lat[3 * (int64_t)b + j]) return lat[3 * (int64_t)a + j] < lat[3 * (int64_t)b + j];
+    return a < b;
+  };
+  std::function<int(std::vector<int32_t>&)> nd = [&](std::vector<int32_t>& nodes) -> int {
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int v : nodes)
+      for (int j = 0; j < 3; ++j) {
+        lo[j] = std::min(lo[j], lat[3 * (int64_t)v + j]);
+        hi[j] = std::max(hi[j], lat[3 * (int64_t)v + j]);
+      }
+    int ax = 0;
+    for (int j = 1; j < 3; ++j)
+      if (hi[j] - lo[j] > hi[ax] - lo[ax]) ax = j;
+    if ((int)nodes.size() <= kLeaf || hi[ax] - lo[ax] < 2) {
+      std::sort(nodes.begin(), nodes.end(), lexless);
+      supNodes.push_back(nodes);
+      supParent.push_back(-1);
+      return (int)supNodes.size() - 1;
+    }
+    // cut plane: the populated lattice coordinate strictly inside (lo, hi) closest to the middle
+    std::vector<int> hist(hi[ax] - lo[ax] + 1, 0);
+    for (int v : nodes) hist[lat[3 * (int64_t)v + ax] - lo[ax]]++;
+    int c = INT32_MIN;
+    const int mid = (lo[ax] + hi[ax]) / 2;
+    for (int off = 0; off <= hi[ax] - lo[ax] && c == INT32_MIN; ++off)
+      for (int sgn : {0, 1}) {
+        const int cc = sgn ? mid + off : mid - off;
+        if (cc > lo[ax] && cc < hi[ax] && hist[cc - lo[ax]] > 0) { c = cc; break; }
+      }
+    if (c == INT32_MIN) {  // cannot cut: dense leaf
+      std::sort(nodes.begin(), nodes.end(), lexless);
+      supNodes.push_back(nodes);
+      supParent.push_back(-1);
+      return (int)supNodes.size() - 1;
+    }
+    std::vector<int32_t> L, S, R;
+    for (int v : nodes) {
+      const int x = lat[3 * (int64_t)v + ax];
+      (x < c ? L : (x == c ? S : R)).push_back(v);
+    }
+    std::vector<int32_t>().swap(nodes);
+    std::vector<int> kids;
+    if (!L.empty()) kids.push_back(nd(L));
+    if (!R.empty()) kids.push_back(nd(R));
+    std::sort(S.begin(), S.end(), lexless);
+    supNodes.push_back(S);
+    supParent.push_back(-1);
+    const int s = (int)supNodes.size() - 1;
+    for (int k : kids) supParent[k] = s;
+    return s;
+  };
+  nd(freeNodes);
+  P.nsup = (int)supNodes.size();
+  P.sfirst.resize(P.nsup);
+  P.ssize.resize(P.nsup);
+  P.parent = supParent;
+  P.pos_of_node.assign(n, -1);
+  P.node_of_pos.resize(P.nfree);
+  {
+    int pos = 0;
+    for (int s = 0; s < P.nsup; ++s) {
+      P.sfirst[s] = pos;
+      P.ssize[s] = (int)supNodes[s].size();
+      for (int v : supNodes[s]) {
+        P.pos_of_node[v] = pos;
+        P.node_of_pos[pos] = v;
+        ++pos;
+      }
+    }
+  }
+  std::vector<int32_t> sup_of_pos(P.nfree);
+  for (int s = 0; s < P.nsup; ++s)
+    for (int k = 0; k < P.ssize[s]; ++k) sup_of_pos[P.sfirst[s] + k] = s;
+  for (int s = 0; s < P.nsup; ++s)
+    if (P.parent[s] >= 0 && P.parent[s] <= s) return "internal: ND tree not in postorder";
+
+  // ---------------- scalar A_s in solver order (CSR)
+  {
+    std::vector<std::vector<std::pair<int32_t, double>>> rowsA(P.nfree);
+    for (int e = 0; e < m; ++e) {
+      const int32_t* c = hex8 + 8 * (int64_t)e;
+      for (int a = 0; a < 8; ++a) {
+        const int pa = P.pos_of_node[c[a]];
+        if (pa < 0) continue;
+        for (int b = 0; b < 8; ++b) {
+          const int pb = P.pos_of_node[c[b]];
+          if (pb < 0) continue;
+          rowsA[pa].push_back({pb, w_ref * P.Kc[a][b] + w_m * P.Km[a][b]});
+        }
+      }
+    }
+    P.a_ptr.assign(P.nfree + 1, 0);
+    P.a_col.clear();
+    P.a_val.clear();
+    for (int p = 0; p < P.nfree; ++p) {
+      auto& r = rowsA[p];
+      r.push_back({p, P.node_mass[P.node_of_pos[p]] / (h * h)});
+      std::stable_sort(r.begin(), r.end(), [](auto& x, auto& y) { return x.first < y.first; });
+      for (size_t k = 0; k < r.size();) {
+        size_t k2 = k;
+        double s = 0;
+        while (k2 < r.size() && r[k2].first == r[k].first) s += r[k2++].second;
+        P.a_col.push_back(r[k].first);
+        P.a_val.push_back(s);
+        k = k2;
+      }
+      P.a_ptr[p + 1] = (int64_t)P.a_col.size();
+      std::vector<std::pair<int32_t, double>>().swap(r);
+    }
+  }
+
+  // ---------------- symbolic: rows(s) = (adj(J_s) U rows(children)) beyond J_s
+  std::vector<std::vector<int32_t>> kids(P.nsup);
+  for (int s = 0; s < P.nsup; ++s)
+    if (P.parent[s] >= 0) kids[P.parent[s]].push_back(s);
+  std::vector<std::vector<int32_t>> srows(P.nsup);
+  P.height.assign(P.nsup, 0);
+  for (int s = 0; s < P.nsup; ++s) {
+    const int last = P.sfirst[s] + P.ssize[s] - 1;
+    std::vector<int32_t> r;
+    for (int p = P.sfirst[s]; p <= last; ++p)
+      for (int64_t k = P.a_ptr[p]; k < P.a_ptr[p + 1]; ++k)
+        if (P.a_col[k] > last) r.push_back(P.a_col[k]);
+    for (int c : kids[s]) {
+      for (int q : srows[c])
+        if (q > last) r.push_back(q);
+      P.height[s] = std::max(P.height[s], P.height[c] + 1);
+    }
+    std::sort(r.begin(), r.end());
+    r.erase(std::unique(r.begin(), r.end()), r.end());
+    srows[s].swap(r);
+  }
+  for (int s = 0; s < P.nsup; ++s)
+    if (P.parent[s] < 0 && !srows[s].empty()) return "internal: ND root with off-diagonal rows";
+  P.rptr.assign(P.nsup + 1, 0);
+  for (int s = 0; s < P.nsup; ++s) P.rptr[s + 1] = P.rptr[s] + (int64_t)srows[s].size();
+  P.rows.resize(P.rptr[P.nsup]);
+  for (int s = 0; s < P.nsup; ++s) std::copy(srows[s].begin(), srows[s].end(), P.rows.begin() + P.rptr[s]);
+  P.doff.assign(P.nsup + 1, 0);
+  P.poff.assign(P.nsup + 1, 0);
+  for (int s = 0; s < P.nsup; ++s) {
+    const int64_t ns = P.ssize[s], nr = (int64_t)srows[s].size();
+    P.doff[s + 1] = P.doff[s] + ns * (ns + 1) / 2;
+    P.poff[s + 1] = P.poff[s] + nr * ns;
+    P.factor_flops += ns * ns * ns / 3.0 + nr * ns * ns + (double)nr * nr * ns;
+  }
+  P.nnzL = P.doff[P.nsup] + P.poff[P.nsup];
+  P.D.assign(P.doff[P.nsup], 0.0);
+  P.P.assign(P.poff[P.nsup], 0.0);
+
+  // ---------------- numeric multifrontal factorisation, level-synchronous
+  auto t0 = std::chrono::steady_clock::now();
+  int H = 0;
+  for (int s = 0; s < P.nsup; ++s) H = std::max(H, P.height[s]);
+  std::vector<std::vector<int32_t>> byh(H + 1);
+  for (int s = 0; s < P.nsup; ++s) byh[P.height[s]].push_back(s);
+  std::vector<std::vector<double>> U(P.nsup);  // update matrices (nr x nr row-major lower)
+  const int nthreads = omp_get_max_threads();
+  bool ok = true;
+  for (int lev = 0; lev <= H && ok; ++lev) {
+    const auto& list = byh[lev];
+    const bool outer = (int)list.size() >= 2 * nthreads;
+    auto work = [&](int s, bool inner_par, std::vector<int32_t>& loc) {
+      const int ns = P.ssize[s];
+      const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+      const int f = ns + nr;
+      const int32_t* R = P.rows.data() + P.rptr[s];
+      std::vector<double> F((int64_t)f * f, 0.0);
+      for (int k = 0; k < ns; ++k) loc[P.sfirst[s] + k] = k;
+      for (int k = 0; k < nr; ++k) loc[R[k]] = ns + k;
+      for (int k = 0; k < ns; ++k) {
+        const int p = P.sfirst[s] + k;
+        for (int64_t t = P.a_ptr[p]; t < P.a_ptr[p + 1]; ++t) {
+          const int q = P.a_col[t];
+          if (q < p) continue;
+          F[(int64_t)loc[q] * f + k] += P.a_val[t];
+        }
+      }
+      for (int c : kids[s]) {
+        const int nrc = (int)(P.rptr[c + 1] - P.rptr[c]);
+        const int32_t* Rc = P.rows.data() + P.rptr[c];
+        const double* Uc = U[c].data();
+        for (int i = 0; i < nrc; ++i) {
+          const int li = loc[Rc[i]];
+          for (int j = 0; j <= i; ++j) F[(int64_t)li * f + loc[Rc[j]]] += Uc[(int64_t)i * nrc + j];
+        }
+        std::vector<double>().swap(U[c]);
+      }
+      if (!partial_cholesky(F.data(), f, ns, inner_par)) return false;
+      schur_update(F.data(), f, ns, inner_par);
+      tri_inverse(F.data(), f, ns, P.D.data() + P.doff[s], inner_par);
+      double* Ps = P.P.data() + P.poff[s];
+      for (int i = 0; i < nr; ++i)
+        std::memcpy(Ps + (int64_t)i * ns, F.data() + (int64_t)(ns + i) * f, sizeof(double) * ns);
+      if (P.parent[s] >= 0 && nr > 0) {
+        U[s].assign((int64_t)nr * nr, 0.0);
+        for (int i = 0; i < nr; ++i)
+          std::memcpy(U[s].data() + (int64_t)i * nr, F.data() + (int64_t)(ns + i) * f + ns, sizeof(double) * (i + 1));
+      }
+      return true;
+    };
+    if (outer) {
+      int bad = 0;
+#pragma omp parallel
+      {
+        std::vector<int32_t> loc(P.nfree, -1);
+#pragma omp for schedule(dynamic, 1) reduction(+ : bad)
+        for (int k = 0; k < (int)list.size(); ++k)
+          if (!work(list[k], false, loc)) bad++;
+      }
+      ok = bad == 0;
+    } else {
+      std::vector<int32_t> loc(P.nfree, -1);
+      for (int s : list)
+        if (!work(s, true, loc)) { ok = false; break; }
+    }
+  }
+  P.factor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (!ok) {
+    *numerical = true;
+    return "A is not symmetric positive definite (non-positive pivot in the Cholesky factorisation)";
+  }
+
+  // ---------------- solve schedule: tiles by height; forward update blocks per tile
+  // blocks (s <- d): rows R_d[k0:k1) that fall into J_s (contiguous since R_d sorted)
+  std::vector<std::vector<std::array<int32_t, 3>>> into(P.nsup);
+  for (int d = 0; d < P.nsup; ++d) {
+    const int64_t b = P.rptr[d], e = P.rptr[d + 1];
+    for (int64_t k = b; k < e;) {
+      const int s = sup_of_pos[P.rows[k]];
+      int64_t k2 = k;
+      while (k2 < e && sup_of_pos[P.rows[k2]] == s) ++k2;
+      into[s].push_back({d, (int32_t)(k - b), (int32_t)(k2 - b)});
+      k = k2;
+    }
+  }
+  P.nlevels = H + 1;
+  P.lvl_ptr.assign(P.nlevels + 1, 0);
+  P.tile_sup.clear();
+  P.tile_r0.clear();
+  P.tile_r1.clear();
+  P.tblk_ptr.assign(1, 0);
+  P.blk_d.clear();
+  P.blk_k0.clear();
+  P.blk_k1.clear();
+  for (int lev = 0; lev <= H; ++lev) {
+    for (int s : byh[lev]) {
+      const int ns = P.ssize[s];
+      for (int r0 = 0; r0 < ns; r0 += kTile) {
+        const int r1 = std::min(ns, r0 + kTile);
+        P.tile_sup.push_back(s);
+        P.tile_r0.push_back(r0);
+        P.tile_r1.push_back(r1);
+        for (auto& blk : into[s]) {
+          const int d = blk[0];
+          const int32_t* Rd = P.rows.data() + P.rptr[d];
+          int k0 = blk[1], k1 = blk[2];
+          while (k0 < k1 && Rd[k0] - P.sfirst[s] < r0) ++k0;
+          int k1b = k0;
+          while (k1b < k1 && Rd[k1b] - P.sfirst[s] < r1) ++k1b;
+          if (k1b > k0) {
+            P.blk_d.push_back(d);
+            P.blk_k0.push_back(k0);
+            P.blk_k1.push_back(k1b);
+          }
+        }
+        P.tblk_ptr.push_back((int32_t)P.blk_d.size());
+      }
+    }
+    P.lvl_ptr[lev + 1] = (int32_t)P.tile_sup.size();
+  }
+  return "";
+}
+
+}  // namespace pdb

@@ -1,0 +1,88 @@
+// Native check of the host plan (no GPU): solves A_s x = A_s v with the stored
+// supernodal factor (D_s = L_ss^{-1}, panels P_s) by plain substitution and
+// reports max |x - v| / max |v|.  Build: see tests/test_native_plan.py.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+#include "../../paper_2101_05917_b200/csrc/plan.h"
+using namespace pdb;
+int main(int argc, char** argv) {
+  int nx = atoi(argv[1]), ny = atoi(argv[2]), nz = atoi(argv[3]);
+  int fix = argc > 4 ? atoi(argv[4]) : 1;
+  double dx = 0.01;
+  std::vector<double> rest; std::vector<int32_t> hex;
+  auto nid = [&](int i, int j, int k) { return i + (nx + 1) * (j + (ny + 1) * k); };
+  for (int k = 0; k <= nz; ++k) for (int j = 0; j <= ny; ++j) for (int i = 0; i <= nx; ++i) {
+    rest.push_back(i * dx); rest.push_back(j * dx); rest.push_back(k * dx); }
+  for (int k = 0; k < nz; ++k) for (int j = 0; j < ny; ++j) for (int i = 0; i < nx; ++i)
+    for (int c = 0; c < 8; ++c) hex.push_back(nid(i + (c & 1), j + ((c >> 1) & 1), k + ((c >> 2) & 1)));
+  std::vector<int32_t> fixed;
+  if (fix) for (int k = 0; k <= nz; ++k) for (int j = 0; j <= ny; ++j) for (int a = 0; a < 3; ++a) fixed.push_back(3 * nid(0, j, k) + a);
+  int n = (int)rest.size() / 3, m = (int)hex.size() / 8;
+  HostPlan P; bool num; double fib[3] = {1, 0, 0};
+  std::string e = build_plan(P, n, m, rest.data(), hex.data(), dx, 1e3, 0.01, fixed.data(), (int)fixed.size(),
+                             1e5 / 1.45, 1e5 / 1.45, fib, &num);
+  if (!e.empty()) { printf("ERROR %s\n", e.c_str()); return 1; }
+  int N = P.nfree;
+  std::mt19937 rng(1); std::normal_distribution<double> nd;
+  std::vector<double> v(N), b(N, 0.0);
+  for (auto& x : v) x = nd(rng);
+  for (int p = 0; p < N; ++p) for (int64_t k = P.a_ptr[p]; k < P.a_ptr[p + 1]; ++k) b[p] += P.a_val[k] * v[P.a_col[k]];
+  // forward L y = b (left-looking pull as on the GPU: blocks)
+  std::vector<double> y(N), t(N);
+  for (int lev = 0; lev < P.nlevels; ++lev)
+    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
+      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
+      for (int i = r0; i < r1; ++i) t[f + i] = b[f + i];
+      for (int bk = P.tblk_ptr[tl]; bk < P.tblk_ptr[tl + 1]; ++bk) {
+        int d = P.blk_d[bk], nd_ = P.ssize[d];
+        for (int k = P.blk_k0[bk]; k < P.blk_k1[bk]; ++k) {
+          double sum = 0;
+          for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * y[P.sfirst[d] + j];
+          t[P.rows[P.rptr[d] + k]] -= sum;
+        }
+      }
+    }
+    // (tiles of a level finish before phase B in this serial emulation)
+  // redo properly level by level: phase A then B
+  std::fill(y.begin(), y.end(), 0.0);
+  for (int lev = 0; lev < P.nlevels; ++lev) {
+    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
+      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
+      for (int i = r0; i < r1; ++i) t[f + i] = b[f + i];
+      for (int bk = P.tblk_ptr[tl]; bk < P.tblk_ptr[tl + 1]; ++bk) {
+        int d = P.blk_d[bk], nd_ = P.ssize[d];
+        for (int k = P.blk_k0[bk]; k < P.blk_k1[bk]; ++k) {
+          double sum = 0;
+          for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * y[P.sfirst[d] + j];
+          t[P.rows[P.rptr[d] + k]] -= sum;
+        }
+      }
+    }
+    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
+      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
+      for (int i = r0; i < r1; ++i) { double sum = 0; for (int j = 0; j <= i; ++j) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + j] * t[f + j]; y[f + i] = sum; }
+    }
+  }
+  std::vector<double> x(N), tt(N);
+  for (int lev = P.nlevels - 1; lev >= 0; --lev) {
+    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
+      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s], ns = P.ssize[s];
+      int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+      for (int c = r0; c < r1; ++c) { double sum = y[f + c]; for (int k = 0; k < nr; ++k) sum -= P.P[P.poff[s] + (int64_t)k * ns + c] * x[P.rows[P.rptr[s] + k]]; tt[f + c] = sum; }
+    }
+    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
+      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s], ns = P.ssize[s];
+      for (int c = r0; c < r1; ++c) { double sum = 0; for (int i = c; i < ns; ++i) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + c] * tt[f + i]; x[f + c] = sum; }
+    }
+  }
+  double err = 0, mx = 0;
+  for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
+  int64_t nnzA = P.a_ptr[N];
+  printf("n=%d nfree=%d nsup=%d levels=%d tiles=%zu blocks=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
+         n, N, P.nsup, P.nlevels, P.tile_sup.size(), P.blk_d.size(), (long long)nnzA, (long long)P.nnzL, P.factor_flops,
+         P.factor_ms, err / mx);
+  return err / mx < 1e-10 ? 0 : 2;
+}

@@ -1,0 +1,205 @@
+"""CUDA path (C-ABI, sm_100a) vs the CPU oracle — element by element on seeded inputs.
+
+Bars (BASELINE.json north_star): positions/velocities rel. 2-norm error <= 1e-9 per (sim, step),
+gradients <= 1e-6 per output array per sim, all fp64; kernel-level hooks at 1e-12.
+"""
+import numpy as np
+import pytest
+
+from gpu_common import GRAD_TOL, POS_TOL, TOL_PAR_ADJ, TOL_PAR_FWD, oracle_run, rel, to_dev
+from pd_inputs import get_config, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2101_05917_b200 as pdb
+    pdb.build()
+    return torch
+
+
+def _sim(inp, **kw):
+    import paper_2101_05917_b200 as pdb
+    base = dict(tol_fwd=TOL_PAR_FWD, tol_adj=TOL_PAR_ADJ)
+    base.update(kw)
+    return pdb.simulator_from_inputs(inp, **base)
+
+
+def _rand_states(inp, B, scale, seed):
+    rng = np.random.default_rng(seed)
+    x = np.repeat(inp["rest"].ravel()[None], B, 0) + scale * rng.standard_normal((B, 3 * inp["n_nodes"]))
+    return x
+
+
+# ----------------------------------------------------------------- kernel-level hooks
+def test_rotations_match_oracle_polar(torch):
+    from oracle import energy, fem
+    inp = make_inputs(get_config("c5s"))
+    sim = _sim(inp)
+    for scale in (1e-3, 5e-3, 2e-2):          # 2e-2 (2 dx) inverts many elements: SVD fallback path
+        x = _rand_states(inp, 2, scale, 0)
+        R = torch.zeros((2, inp["n_elems"], 8, 9), dtype=torch.float64, device="cuda")
+        sim.project_rotations(to_dev(x), R)
+        R = R.cpu().numpy()
+        for b in range(2):
+            F = fem.deformation_gradients(x[b], inp["hex8"], 0.01)
+            Ro, S, V, s = energy.polar_svd(F)
+            ok = np.abs(s).min(-1) > 1e-6 * np.abs(s).max(-1)   # skip near-singular F (R not unique)
+            gap = np.minimum(np.abs(s[..., 1] - s[..., 2]), np.abs(s[..., 0] - s[..., 2]))
+            ok &= (np.abs(s[..., 1] + s[..., 2]) > 1e-6)
+            d = np.abs(R[b].reshape(Ro.shape[:2] + (3, 3)) - Ro).max(axis=(-1, -2))
+            assert d[ok].max() < 1e-11, (scale, d[ok].max())
+
+
+@pytest.mark.parametrize("name", ["c1", "c3s", "c5s"])
+def test_objective_and_gradient(torch, name):
+    from oracle import pd
+    inp = make_inputs(get_config(name))
+    B = inp["B"]
+    sim = _sim(inp)
+    x = _rand_states(inp, B, 1e-3, 1)
+    rng = np.random.default_rng(2)
+    y = x + 1e-3 * rng.standard_normal(x.shape)
+    act = None if inp["act"] is None else np.ascontiguousarray(inp["act"][:, 0])
+    grad = torch.zeros((B, 3 * inp["n_nodes"]), dtype=torch.float64, device="cuda")
+    g = torch.zeros(B, dtype=torch.float64, device="cuda")
+    sim.eval_objective(to_dev(x), to_dev(y), youngs=to_dev(inp["youngs"]),
+                       act=None if act is None else to_dev(act), grad=grad, g=g)
+    grad, g = grad.cpu().numpy(), g.cpu().numpy()
+    for b in range(B):
+        sc = pd.scene_from_inputs(inp)
+        go, ggo = sc.objective(x[b], y[b], sc.w_of(inp["youngs"][b]), None if act is None else act[b])
+        assert abs(g[b] - go) <= 1e-12 * abs(go)
+        assert rel(grad[b], ggo) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c2s", "c3s", "c5s"])
+def test_global_solve_matches_direct(torch, name):
+    # The prefactorised global step A^{-1} against a direct sparse solve of A on free DoFs.
+    import scipy.sparse.linalg as spla
+    from oracle import pd
+    inp = make_inputs(get_config(name))
+    B = inp["B"]
+    sim = _sim(inp)
+    rng = np.random.default_rng(3)
+    rhs = rng.standard_normal((B, 3 * inp["n_nodes"]))
+    out = torch.zeros_like(to_dev(rhs))
+    sim.apply_Ainv(to_dev(rhs), out)
+    out = out.cpu().numpy()
+    sc = pd.scene_from_inputs(inp)
+    w_ref = (np.max(inp["youngs"]) if inp["cfg"].per_sim_youngs else inp["cfg"].youngs) / (1 + sc.poisson)
+    A = sc.A(w_ref)
+    fr = sc.free
+    for b in range(B):
+        ref = np.zeros(sc.N)
+        ref[fr] = spla.spsolve(A[fr][:, fr].tocsc(), rhs[b][fr])
+        assert rel(out[b], ref) <= 1e-12
+        assert np.all(out[b][~fr] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c5s"])
+def test_AN_product_matches_assembled_hessian(torch, name):
+    # Matrix-free A_N p vs the oracle's assembled A_N = A - dA.
+    from oracle import adjoint, pd
+    inp = make_inputs(get_config(name))
+    B = inp["B"]
+    sim = _sim(inp)
+    x = _rand_states(inp, B, 1e-3, 4)
+    p = np.random.default_rng(5).standard_normal(x.shape)
+    act = None if inp["act"] is None else np.ascontiguousarray(inp["act"][:, 0])
+    out = torch.zeros_like(to_dev(p))
+    sim.apply_AN(to_dev(x), to_dev(p), out, youngs=to_dev(inp["youngs"]), act=None if act is None else to_dev(act))
+    out = out.cpu().numpy()
+    sc = pd.scene_from_inputs(inp)
+    for b in range(B):
+        AN = adjoint.assemble_AN(sc, x[b], sc.w_of(inp["youngs"][b]), None if act is None else act[b])
+        assert rel(out[b], AN @ p[b]) <= 1e-12
+
+
+# ----------------------------------------------------------------- end to end
+def _run_gpu(torch, inp, sim):
+    B, T, N = inp["B"], inp["T"], 3 * inp["n_nodes"]
+    qt = torch.zeros((B, T + 1, N), dtype=torch.float64, device="cuda")
+    vt = torch.zeros_like(qt)
+    act = None if inp["act"] is None else to_dev(inp["act"][:, :T])
+    st = sim.forward(to_dev(inp["q0"]), to_dev(inp["v0"]), T, f_ext=to_dev(inp["f_ext"]), actuation=act,
+                     youngs=to_dev(inp["youngs"]), q_traj=qt, v_traj=vt)
+    from oracle import adjoint
+    q, v = qt.cpu().numpy(), vt.cpu().numpy()
+    gq = np.zeros((B, N))
+    gv = np.zeros((B, N))
+    for b in range(B):
+        _, gq[b], gv[b] = adjoint.loss_and_grad(inp, b, q[b, -1], v[b, -1])
+    outs = {k: torch.zeros((B, N), dtype=torch.float64, device="cuda") for k in ("dq0", "dv0", "dfext")}
+    dE = torch.zeros(B, dtype=torch.float64, device="cuda")
+    dnu = torch.zeros(B, dtype=torch.float64, device="cuda")
+    dact = None if act is None else torch.zeros_like(act)
+    sb = sim.backward(to_dev(gq), to_dev(gv), outs["dq0"], outs["dv0"], outs["dfext"], dE, dnu, dact)
+    res = dict(q=q, v=v, st=st, sb=sb, dE=dE.cpu().numpy(), dnu=dnu.cpu().numpy(),
+               dact=None if dact is None else dact.cpu().numpy())
+    res.update({k: t.cpu().numpy() for k, t in outs.items()})
+    return res
+
+
+def _compare(inp, gpu, sims):
+    for b in sims:
+        tr, g, _, _ = oracle_run(inp, b)
+        for i in range(1, inp["T"] + 1):
+            assert rel(gpu["q"][b, i], tr["q"][i]) <= POS_TOL, ("q", b, i, rel(gpu["q"][b, i], tr["q"][i]))
+            vo = tr["v"][i]
+            if np.linalg.norm(vo) > 0:
+                assert rel(gpu["v"][b, i], vo) <= POS_TOL, ("v", b, i, rel(gpu["v"][b, i], vo))
+            else:
+                assert np.abs(gpu["v"][b, i]).max() <= 1e-12
+        assert rel(gpu["dq0"][b], g["dq0"]) <= GRAD_TOL, ("dq0", rel(gpu["dq0"][b], g["dq0"]))
+        assert rel(gpu["dv0"][b], g["dv0"]) <= GRAD_TOL, ("dv0", rel(gpu["dv0"][b], g["dv0"]))
+        assert rel(gpu["dfext"][b], g["dfext"]) <= GRAD_TOL, ("dfext", rel(gpu["dfext"][b], g["dfext"]))
+        assert abs(gpu["dE"][b] - g["dE"]) <= GRAD_TOL * abs(g["dE"]), ("dE", gpu["dE"][b], g["dE"])
+        assert abs(gpu["dnu"][b] - g["dnu"]) <= GRAD_TOL * abs(g["dnu"]), ("dnu", gpu["dnu"][b], g["dnu"])
+        if g["dact"] is not None:
+            assert rel(gpu["dact"][b], g["dact"]) <= GRAD_TOL, ("dact", rel(gpu["dact"][b], g["dact"]))
+
+
+def test_c1_fixed_iterations_parity(torch):
+    # BASELINE.json configs[0]: exactly 10 local-global iterations per step (algorithmic parity).
+    inp = make_inputs(get_config("c1"))
+    gpu = _run_gpu(torch, inp, _sim(inp))
+    assert np.all(gpu["st"]["iters_fwd"] == 10)
+    _compare(inp, gpu, [0])
+
+
+@pytest.mark.parametrize("accel_adj", [1, 0])
+def test_c2s_converged_parity(torch, accel_adj):
+    inp = make_inputs(get_config("c2s"))
+    gpu = _run_gpu(torch, inp, _sim(inp, accel_adj=accel_adj))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    _compare(inp, gpu, [0])
+
+
+def test_c3s_batched_shared_factor_parity(torch):
+    # Per-sim E with ONE factor of A_ref; the oracle uses each sim's exact A_s.
+    inp = make_inputs(get_config("c3s"))
+    gpu = _run_gpu(torch, inp, _sim(inp))
+    assert gpu["st"]["n_nonconverged"] == 0
+    _compare(inp, gpu, range(inp["B"]))
+
+
+def test_c5s_muscle_no_contact_parity(torch):
+    inp = make_inputs(get_config("c5s", contact=False))
+    gpu = _run_gpu(torch, inp, _sim(inp))
+    assert gpu["st"]["n_nonconverged"] == 0
+    _compare(inp, gpu, range(inp["B"]))
+
+
+def test_bitwise_determinism(torch):
+    # No float atomics anywhere: two runs are bitwise identical.
+    inp = make_inputs(get_config("c3s"))
+    sim = _sim(inp)
+    a = _run_gpu(torch, inp, sim)
+    b = _run_gpu(torch, inp, sim)
+    for k in ("q", "v", "dq0", "dv0", "dfext", "dE", "dnu"):
+        assert np.array_equal(a[k], b[k]), k
