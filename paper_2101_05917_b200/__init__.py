@@ -18,7 +18,7 @@ __all__ = ["Simulator", "PDError", "build"]
 
 
 def build(force=False):
-    from .build import build as _b
+    from .buildlib import build as _b
     return _b(force=force)
 
 

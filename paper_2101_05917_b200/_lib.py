@@ -55,7 +55,7 @@ def load():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2101_05917_b200.build` "
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2101_05917_b200.buildlib` "
                            "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     vp = C.c_void_p

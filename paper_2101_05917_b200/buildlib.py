@@ -1,6 +1,6 @@
 """In-tree build of libdiffpd_b200.so (sm_100a) — nvcc + g++, no JIT cache.
 
-    python -m paper_2101_05917_b200.build
+    python -m paper_2101_05917_b200.buildlib
 """
 from __future__ import annotations
 

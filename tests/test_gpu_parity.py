@@ -24,7 +24,7 @@ def torch():
 
 def _sim(inp, **kw):
     import paper_2101_05917_b200 as pdb
-    base = dict(tol_fwd=TOL_PAR_FWD, tol_adj=TOL_PAR_ADJ)
+    base = dict(tol_fwd=TOL_PAR_FWD, tol_adj=TOL_PAR_ADJ, contact_nodes=())
     base.update(kw)
     return pdb.simulator_from_inputs(inp, **base)
 
