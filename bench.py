@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py — B200 DiffPD hot path: PD forward + PD backward throughput.
+
+One bench "step" = one pass of the whole hot path over one batch: pd_forward over the
+config's T time steps for its B sims (y, local step K1, gather K2, global solve K3, [contact
+K5]) followed by pd_backward (adjoint PCG with K4 + K3, parameter terms) — SURVEY §8(a).
+metric = (sims x time steps x DoF) / second (BASELINE.json "PD sim-steps/sec (forward+backward)
+x DoF per B200"), DoF = 3 n (all nodal DoFs, as the configs quote them).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+N > 1 (torchrun): each rank runs its own B sims (weak scaling, no data-path collective;
+DESIGN.md §6); the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from pd_inputs import get_config, make_inputs  # noqa: E402
+
+METRIC = "PD sim-steps/sec (forward+backward) x DoF per B200"
+UNIT = "DoF*steps/s"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 64 DFMA/clk/SM x 148 SMs x 1.965 GHz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--horizon", type=int, default=0, help="override T (time steps per trajectory)")
+    ap.add_argument("--tol", type=float, default=0.0, help="override forward/adjoint tolerance")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    ap.add_argument("--set", action="append", default=[], help="config override key=value (e.g. contact=False)")
+    return ap.parse_args()
+
+
+def make_cfg(args):
+    ov = {}
+    for kv in args.set:
+        k, v = kv.split("=", 1)
+        ov[k] = eval(v, {}, {})
+    if args.tol:
+        ov["tol"] = args.tol
+    return get_config(args.config, **ov)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample(cfg, sample_steps, sims=1):
+    """Time the oracle as it stands (forward + backward) on a bounded sample of the workload."""
+    import resource
+    from oracle import adjoint, pd
+    inp = make_inputs(cfg, batch=sims, steps=sample_steps)
+    r0 = resource.getrusage(resource.RUSAGE_SELF)
+    t0 = time.perf_counter()
+    for b in range(sims):
+        sc = pd.scene_from_inputs(inp)
+        act = None if inp["act"] is None else inp["act"][b]
+        tr = pd.forward(sc, inp["q0"][b], inp["v0"][b], inp["f_ext"][b], inp["youngs"][b], act,
+                        steps=sample_steps, tol=cfg.tol, fixed_iter=cfg.fixed_iter)
+        L, gq, gv = adjoint.loss_and_grad(inp, b, tr["q"][-1], tr["v"][-1])
+        adjoint.backward(sc, tr, inp["youngs"][b], gq, gv, act)
+    wall = time.perf_counter() - t0
+    r1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu = (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
+    units = sims * sample_steps * 3 * inp["n_nodes"]
+    return dict(value=units / wall, unit=UNIT, cores=max(1, round(cpu / wall)), kind="oracle",
+                sample=f"{sims} sim x {sample_steps} time steps of {cfg.name} (forward+backward, tol {cfg.tol:g})",
+                wall_s=wall)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = make_cfg(args)
+    walls = []
+    res = None
+    for _ in range(args.steps):
+        res = oracle_sample(cfg, args.cpu_sample_steps)
+        walls.append(res["wall_s"])
+    units = 3 * cfg.n_nodes * args.cpu_sample_steps
+    value = units * len(walls) / sum(walls)
+    line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+                ms_per_step=1e3 * sum(walls) / len(walls), higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+                config=dict(workload=cfg.name, sample=res["sample"]),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=res["cores"], kind="oracle", sample=res["sample"]),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+            except ValueError:
+                continue
+            for k, v in zip(names, r[2:]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(k)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return dict(sm_mhz=statistics.median(loaded), sm_max_mhz=mx, reasons=sorted(reasons), samples=len(sm))
+
+
+# ----------------------------------------------------------------------------- ours
+def main_ours(args):
+    import torch
+    import paper_2101_05917_b200 as pdb
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = make_cfg(args)
+    T = args.horizon or cfg.steps
+    # weak scaling: every rank simulates its own batch of B sims (seeded per rank)
+    if rank:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, seed=cfg.seed * 1000 + rank)
+    inp = make_inputs(cfg, steps=T)
+    B, N = inp["B"], 3 * inp["n_nodes"]
+    t_setup = time.perf_counter()
+    sim = pdb.simulator_from_inputs(inp, tol_fwd=cfg.tol, tol_adj=cfg.tol, max_steps=T, profile=1,
+                                    check_every=1)
+    setup_s = time.perf_counter() - t_setup
+    info = sim.info()
+    D = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
+    q0, v0, fext, E = D(inp["q0"]), D(inp["v0"]), D(inp["f_ext"]), D(inp["youngs"])
+    act = None if inp["act"] is None else D(inp["act"])
+    cq, cv = D(inp["c_q"]), D(inp["c_v"])
+    tip = torch.as_tensor((3 * inp["tip_nodes"][:, None] + np.arange(3)[None]).ravel(), device=dev)
+    target = D(inp["tip_target"])
+    qt = torch.zeros((B, T + 1, N), dtype=torch.float64, device=dev)
+    vt = torch.zeros_like(qt)
+    g = {k: torch.zeros((B, N), dtype=torch.float64, device=dev) for k in ("dq0", "dv0", "dfext")}
+    dE = torch.zeros(B, dtype=torch.float64, device=dev)
+    dnu = torch.zeros(B, dtype=torch.float64, device=dev)
+    dact = None if act is None else torch.zeros_like(act)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # > 126 MB L2
+
+    def loss_grad(qT, vT):
+        # user-side loss: linear in (q_T, v_T), or the c3 tip error
+        if cfg.loss == "tip":
+            gq = torch.zeros_like(qT)
+            diff = qT[:, tip] - target
+            gq[:, tip] = 2.0 * diff
+            return (diff * diff).sum(1), gq, None
+        L = (cq * qT).sum(1) + ((cv * vT).sum(1) if cfg.loss == "linear_qv" else 0.0)
+        return L, cq, (cv if cfg.loss == "linear_qv" else None)
+
+    stats = {}
+
+    def one_step(q0_, v0_, fext_, E_, act_):
+        st_f = sim.forward(q0_, v0_, T, f_ext=fext_, actuation=act_, youngs=E_, q_traj=qt, v_traj=vt)
+        launches = sim.info()["launches"]
+        L, gq, gv = loss_grad(qt[:, -1].contiguous(), vt[:, -1].contiguous())
+        st_b = sim.backward(gq.contiguous(), None if gv is None else gv.contiguous(), g["dq0"], g["dv0"],
+                            g["dfext"], dE, dnu, dact)
+        launches += sim.info()["launches"]
+        stats.update(fwd=st_f, bwd=st_b)
+        return L, launches
+
+    for _ in range(max(3, args.warmup)):
+        one_step(q0, v0, fext, E, act)
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed region (inputs resident in HBM)
+    clocks = Clocks(local)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    total_ms, launches, prof = 0.0, 0, {}
+    for _ in range(args.steps):
+        flush.fill_(1.0)                           # L2 flush between timed iterations
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, nl = one_step(q0, v0, fext, E, act)
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        launches += nl
+        for k, (ms, c) in sim.profile().items():
+            a, b = prof.get(k, (0.0, 0))
+            prof[k] = (a + ms, b + c)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    units = ws * B * T * N
+    value = units / (ms_per_step / 1e3)
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        H = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64).pin_memory()
+        host_in = [H(inp["q0"]), H(inp["v0"]), H(inp["f_ext"]), H(inp["youngs"])]
+        if act is not None:
+            host_in.append(H(inp["act"]))
+        out_loss = torch.zeros(B, dtype=torch.float64).pin_memory()
+        out_dE = torch.zeros(B, dtype=torch.float64).pin_memory()
+        out_dq0 = torch.zeros((B, N), dtype=torch.float64).pin_memory()
+        h2d = sum(t.numel() * 8 for t in host_in)
+        d2h = (out_loss.numel() + out_dE.numel() + out_dq0.numel()) * 8
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e2e_ms = 0.0
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dv = [t.to(dev, non_blocking=True) for t in host_in]
+            L, _ = one_step(dv[0], dv[1], dv[2], dv[3], dv[4] if act is not None else None)
+            out_loss.copy_(L, non_blocking=True)
+            out_dE.copy_(dE, non_blocking=True)
+            out_dq0.copy_(g["dq0"], non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = dict(value=units / (e2e_ms / args.steps / 1e3), unit=UNIT, h2d_bytes_per_step=h2d,
+                   d2h_bytes_per_step=d2h)
+
+    # ---------------- roofline of the dominant kernel family (live CUDA events)
+    fam = max(prof, key=lambda k: prof[k][0])
+    ms_tot, cnt = prof[fam]
+    avg_s = ms_tot / max(cnt, 1) / 1e3
+    nfree = info["n_free_nodes"]
+    R = 3 * B
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(cfg.name, {}).get(fam)
+    except Exception:
+        pass
+    if fam == "solve_K3":
+        # factor read twice (L then L^T) + solve vectors (rhs, y, t, x) + permutation in/out
+        alg_bytes = 2 * info["nnz_L"] * 8 + 4 * nfree * R * 8 + 2 * N * B * 8
+        roof = dict(bound="hbm", achieved=alg_bytes / avg_s / 1e9, peak=hbm_peak, unit="GB/s",
+                    frac=alg_bytes / avg_s / 1e9 / hbm_peak, traffic=traffic, kernel=fam,
+                    algorithmic_bytes_per_launch=alg_bytes, avg_launch_ms=avg_s * 1e3,
+                    peak_source="MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback")
+    else:
+        # K1/K4: per-quad-point algorithmic fp64 flops
+        per_qp = {"local_K1": 1500, "AN_K4": 1900, "gather_K2": 0, "param": 1300}.get(fam, 0)
+        flops = per_qp * 8 * inp["n_elems"] * B
+        ach = flops / avg_s / 1e12
+        roof = dict(bound="alu", achieved=ach, peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=ach / FP64_PEAK_TFLOPS,
+                    traffic=traffic, kernel=fam, avg_launch_ms=avg_s * 1e3,
+                    peak_source="derived fp64 FMA-pipe peak (DESIGN.md §5)")
+    share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
+
+    line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=max(3, args.warmup),
+                ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic",
+                config=dict(workload=cfg.name, batch_per_gpu=B, time_steps=T, dof=N, tol=cfg.tol,
+                            grid=list(cfg.counts), l2="flushed (256 MB write) before every timed iteration",
+                            parallelism=f"batch-sharded x{ws} (weak)"),
+                e2e=e2e, gpu_launches=launches, roofline=roof,
+                kernel_share=share,
+                iters=dict(fwd_mean=float(np.mean(stats["fwd"]["iters_fwd"])),
+                           adj_mean=float(np.mean(stats["bwd"]["iters_adj"])),
+                           nonconverged=int(stats["fwd"]["n_nonconverged"] + stats["bwd"]["n_nonconverged"])),
+                setup=dict(seconds=setup_s, factor_ms=info["factor_ms"], nnz_L=info["nnz_L"],
+                           supernodes=info["n_supernodes"], levels=info["n_levels"]),
+                clocks=clk)
+    if rank == 0:
+        line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_sample_steps).items() if k != "wall_s"}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        main_ours(a)

@@ -85,6 +85,7 @@ typedef struct {
   int32_t n_contact;
   int32_t max_outer;      /* Alg. 1 "maximum iteration" (default 10)                     */
   double eps_phi;         /* predictor penetration threshold (m), default 1e-6 dx          */
+  int32_t profile;        /* 1: bracket each kernel family with CUDA events (pd_profile)   */
 } pd_options;
 
 /* Per-step statistics, caller-owned HOST arrays of length B*steps (index
@@ -156,6 +157,13 @@ pd_status pd_project_rotations(pd_sim* sim, int32_t B, const double* x, double* 
  * n_levels, nnz(L_s) (stored entries of the scalar factor), n_contact,
  * setup_ms_factor (rounded), kernel launches of the last pd_forward+pd_backward}. */
 pd_status pd_info(const pd_sim* sim, int64_t* out, int32_t n);
+
+/* Per-kernel-family device time (CUDA events on the work stream) accumulated since the
+ * start of the last pd_forward (forward + backward), when opts.profile = 1.
+ * Families: 0 local step K1, 1 gather K2, 2 global solve K3 (one A^{-1} application),
+ * 3 A_N product K4 (element pass + gather), 4 contact K5, 5 parameter terms.
+ * ms[k] = total milliseconds, count[k] = number of timed regions. */
+pd_status pd_profile(const pd_sim* sim, double* ms, int64_t* count, int32_t n);
 
 const char* pd_last_error(const pd_sim* sim);
 void pd_destroy(pd_sim* sim);

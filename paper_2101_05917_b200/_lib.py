@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "PD_OK", 1: "PD_ERR_INVALID_ARGUMENT", 2: "PD_ERR_NUMERICAL",
 
 # every symbol include/diffpd_b200.h declares
 EXPORTS = ["pd_create", "pd_forward", "pd_backward", "pd_eval_objective", "pd_apply_Ainv", "pd_apply_AN",
-           "pd_project_rotations", "pd_info", "pd_last_error", "pd_destroy"]
+           "pd_project_rotations", "pd_info", "pd_profile", "pd_last_error", "pd_destroy"]
 
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int32)
@@ -38,7 +38,8 @@ class PdOptions(C.Structure):
                 ("max_iter_adj", C.c_int32), ("fixed_iter", C.c_int32), ("accel_fwd", C.c_int32),
                 ("accel_adj", C.c_int32), ("check_every", C.c_int32), ("max_batch", C.c_int32),
                 ("max_steps", C.c_int32), ("youngs_ref", C.c_double), ("contact_nodes", ip),
-                ("n_contact", C.c_int32), ("max_outer", C.c_int32), ("eps_phi", C.c_double)]
+                ("n_contact", C.c_int32), ("max_outer", C.c_int32), ("eps_phi", C.c_double),
+                ("profile", C.c_int32)]
 
 
 class PdStats(C.Structure):
@@ -69,6 +70,7 @@ def load():
     lib.pd_apply_AN.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
     lib.pd_project_rotations.argtypes = [vp, C.c_int32, vp, vp, vp]
     lib.pd_info.argtypes = [vp, C.POINTER(C.c_int64), C.c_int32]
+    lib.pd_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]
     lib.pd_last_error.argtypes = [vp]
     lib.pd_last_error.restype = C.c_char_p
     lib.pd_destroy.argtypes = [vp]

@@ -64,6 +64,12 @@ struct pd_sim {
   bool has_act = false;
   int64_t launches = 0;
   cudaStream_t stream = nullptr;
+  // profiler (opts.profile): event pairs per kernel family, resolved at host sync points
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_open;  // (family, index of start event)
+  int ev_next = 0;
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  int64_t prof_cnt[6] = {0, 0, 0, 0, 0, 0};
 
   template <class T>
   T* alloc(size_t count) {
@@ -81,6 +87,7 @@ struct pd_sim {
     return d;
   }
   ~pd_sim() {
+    for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& b : bufs) cudaFree(b.p);
     if (h_nactive) cudaFreeHost(h_nactive);
   }
@@ -108,6 +115,39 @@ pd_status fail(pd_sim* s, pd_status st, const std::string& msg) {
   if (s) s->err = msg;
   else g_create_error = msg;
   return st;
+}
+
+cudaEvent_t prof_event(pd_sim* s) {
+  if (s->ev_next == (int)s->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    s->ev_pool.push_back(e);
+  }
+  return s->ev_pool[s->ev_next++];
+}
+struct ProfScope {
+  pd_sim* s;
+  int fam;
+  ProfScope(pd_sim* s_, int f) : s(s_), fam(f) {
+    if (!s->opt.profile) return;
+    s->ev_open.push_back({fam, s->ev_next});
+    CK(cudaEventRecord(prof_event(s), s->stream));
+  }
+  ~ProfScope() {
+    if (s->opt.profile) cudaEventRecord(prof_event(s), s->stream);
+  }
+};
+// resolve recorded pairs (the stream must have been synchronised)
+void prof_flush(pd_sim* s) {
+  if (!s->opt.profile) return;
+  for (auto& pr : s->ev_open) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, s->ev_pool[pr.second], s->ev_pool[pr.second + 1]));
+    s->prof_ms[pr.first] += ms;
+    s->prof_cnt[pr.first] += 1;
+  }
+  s->ev_open.clear();
+  s->ev_next = 0;
 }
 
 ElemArgs elem_args(pd_sim* s, int B, const double* act_step, int64_t act_bstride) {
@@ -168,6 +208,7 @@ void solve(pd_sim* s, int B) {
 void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* alpha, double alpha_c, double beta,
                 const int32_t* active) {
   const HostPlan& P = s->plan;
+  ProfScope ps(s, 2);
   k_to_solve<<<nblk((int64_t)P.nfree * 3 * B), 256, 0, s->stream>>>(Vin, s->d_nodepos, P.nfree, B, s->S0);
   LAUNCH_CHECK(s);
   solve(s, B);
@@ -180,9 +221,13 @@ void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* 
 void residual(pd_sim* s, int B, const double* X, const double* Y, const double* act_step, int64_t act_bstride,
               const uint8_t* fixed_mask) {
   const HostPlan& P = s->plan;
-  k_elem_residual<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
-                                                                       s->EF, s->EE);
-  LAUNCH_CHECK(s);
+  {
+    ProfScope ps(s, 0);
+    k_elem_residual<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
+                                                                         s->EF, s->EE);
+    LAUNCH_CHECK(s);
+  }
+  ProfScope ps(s, 1);
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
                                                           s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, s->G, s->W, s->S0,
                                                           nullptr, nullptr, nullptr);
@@ -193,6 +238,7 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
 void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT, const double* act_step,
               int64_t act_bstride) {
   const HostPlan& P = s->plan;
+  ProfScope ps(s, 3);
   k_elem_AN<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
                                                                  s->EF);
   LAUNCH_CHECK(s);
@@ -218,6 +264,7 @@ void set_w(pd_sim* s, int B, const double* youngs_per_sim) {
 int read_nactive(pd_sim* s) {
   CK(cudaMemcpyAsync(s->h_nactive, s->nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
+  prof_flush(s);
   return *s->h_nactive;
 }
 
@@ -343,6 +390,15 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
   return PD_OK;
 }
 
+pd_status pd_profile(const pd_sim* s, double* ms, int64_t* count, int32_t n) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  for (int k = 0; k < n && k < 6; ++k) {
+    if (ms) ms[k] = s->prof_ms[k];
+    if (count) count[k] = s->prof_cnt[k];
+  }
+  return PD_OK;
+}
+
 pd_status pd_info(const pd_sim* s, int64_t* out, int32_t n) {
   if (!s || !out) return PD_ERR_INVALID_ARGUMENT;
   const HostPlan& P = s->plan;
@@ -363,6 +419,9 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   if (s->w_m != 0.0 && !actuation) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs an actuation array");
   s->stream = (cudaStream_t)cuda_stream;
   s->launches = 0;
+  for (int k = 0; k < 6; ++k) { s->prof_ms[k] = 0; s->prof_cnt[k] = 0; }
+  s->ev_open.clear();
+  s->ev_next = 0;
   const HostPlan& P = s->plan;
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
@@ -432,6 +491,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       CK(cudaMemcpy2DAsync(v_traj, (steps + 1) * n3 * sizeof(double), v0, n3 * sizeof(double), n3 * sizeof(double), B,
                            cudaMemcpyDeviceToDevice, s->stream));
     CK(cudaStreamSynchronize(s->stream));
+    prof_flush(s);
     if (stats) {
       const int64_t TB = (int64_t)steps * B;
       std::vector<int32_t> it(TB), fl(TB);
@@ -543,6 +603,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
         }
       }
       // parameter terms, f_ext accumulation, state adjoint update
+      ProfScope ps_param(s, 5);
       k_elem_param<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
                                                                       s->DW, s->has_act ? s->DR : nullptr);
       LAUNCH_CHECK(s);
@@ -585,6 +646,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
     if (dL_dE) CK(cudaMemcpyAsync(dL_dE, dE.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     if (dL_dnu) CK(cudaMemcpyAsync(dL_dnu, dnu.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CK(cudaStreamSynchronize(s->stream));
+    prof_flush(s);
     if (stats) {
       const int64_t TB = (int64_t)T * B;
       std::vector<int32_t> it(TB), fl(TB);
