@@ -181,27 +181,30 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   LAUNCH_CHECK(s);
 }
 
-// x = A^{-1} rhs in solve layout (S0 in, S0 out; S1, S2 scratch)
-void solve(pd_sim* s, int B) {
+// x = A^{-1} rhs in solve layout: S0 = rhs (consumed as the working z), S2 = y, S0 = x out
+template <int RC>
+void solve_rc(pd_sim* s, int B) {
   const HostPlan& P = s->plan;
   const int R = 3 * B;
-  const size_t smem = (size_t)kTile * R * sizeof(double);
+  const unsigned gy = (unsigned)((R + RC - 1) / RC);
   for (int lev = 0; lev < P.nlevels; ++lev) {
-    const int t0 = P.lvl_ptr[lev], nt = P.lvl_ptr[lev + 1] - t0;
+    const int t0 = P.flvl_ptr[lev], nt = P.flvl_ptr[lev + 1] - t0;
     if (!nt) continue;
-    k_fwdA<<<nt, 256, smem, s->stream>>>(s->sa, t0, R, s->S0, s->S2, s->S1);
-    LAUNCH_CHECK(s);
-    k_fwdB<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S1, s->S2);
+    k_fwd_level<RC><<<dim3(nt, gy), kNT, 0, s->stream>>>(s->sa, t0, R, s->S0, s->S2);
     LAUNCH_CHECK(s);
   }
   for (int lev = P.nlevels - 1; lev >= 0; --lev) {
-    const int t0 = P.lvl_ptr[lev], nt = P.lvl_ptr[lev + 1] - t0;
+    const int t0 = P.blvl_ptr[lev], nt = P.blvl_ptr[lev + 1] - t0;
     if (!nt) continue;
-    k_bwdA<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S2, s->S0, s->S1);
-    LAUNCH_CHECK(s);
-    k_bwdB<<<nt, 256, 0, s->stream>>>(s->sa, t0, R, s->S1, s->S0);
+    k_bwd_level<RC><<<dim3(nt, gy), kNT, 0, s->stream>>>(s->sa, t0, R, s->S2, s->S0);
     LAUNCH_CHECK(s);
   }
+}
+void solve(pd_sim* s, int B) {
+  const int R = 3 * B;
+  if (R <= 8) solve_rc<8>(s, B);
+  else if (R <= 24) solve_rc<24>(s, B);
+  else solve_rc<48>(s, B);
 }
 
 // state vector V (free nodes) -> A^{-1} V -> OUT = beta OUT + alpha_c*alpha[b]*sol (masked)
@@ -337,14 +340,18 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->sa.poff = s->upload(P.poff);
     s->sa.rows = s->upload(P.rows);
     s->sa.D = s->upload(P.D);
-    s->sa.P = s->upload(P.P);
-    s->sa.tile_sup = s->upload(P.tile_sup);
-    s->sa.tile_r0 = s->upload(P.tile_r0);
-    s->sa.tile_r1 = s->upload(P.tile_r1);
-    s->sa.tblk_ptr = s->upload(P.tblk_ptr);
-    s->sa.blk_d = s->upload(P.blk_d);
-    s->sa.blk_k0 = s->upload(P.blk_k0);
-    s->sa.blk_k1 = s->upload(P.blk_k1);
+    s->sa.W = s->upload(P.P);
+    s->sa.ft_type = s->upload(P.ft_type);
+    s->sa.ft_sup = s->upload(P.ft_sup);
+    s->sa.ft_r0 = s->upload(P.ft_r0);
+    s->sa.ft_r1 = s->upload(P.ft_r1);
+    s->sa.ft_bptr = s->upload(P.ft_bptr);
+    s->sa.fb_s = s->upload(P.fb_s);
+    s->sa.fb_k0 = s->upload(P.fb_k0);
+    s->sa.fb_k1 = s->upload(P.fb_k1);
+    s->sa.bt_sup = s->upload(P.bt_sup);
+    s->sa.bt_c0 = s->upload(P.bt_c0);
+    s->sa.bt_c1 = s->upload(P.bt_c1);
     const int64_t n3B = 3LL * P.n * s->Bmax;
     const int64_t sB = 3LL * P.nfree * s->Bmax;
     double** st_vecs[] = {&s->X, &s->V, &s->Y, &s->Xp, &s->Fext, &s->G, &s->W, &s->U, &s->Rv, &s->Z,
@@ -377,9 +384,6 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->traj = s->alloc<double>((int64_t)(s->Tmax + 1) * n3B);
     s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
     CK(cudaMallocHost(&s->h_nactive, sizeof(int32_t)));
-    const int smem_max = (int)(kTile * 3 * s->Bmax * sizeof(double));
-    if (smem_max > 48 * 1024)
-      CK(cudaFuncSetAttribute(k_fwdA, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
     CK(cudaDeviceSynchronize());
   } catch (CudaError& e) {
     return fail(nullptr, PD_ERR_CUDA, e.what());

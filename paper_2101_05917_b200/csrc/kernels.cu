@@ -521,76 +521,174 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 }
 
 // ----------------------------------------------------------------- K3: supernodal solves
-// Forward L y = b: phase A  t[J_s] = b[J_s] - sum_d L[J_s, J_d] y[J_d]  (pull, fixed d order)
-__global__ void k_fwdA(SolveArgs sa, int tile0, int R, const double* __restrict__ rhs, const double* __restrict__ y,
-                       double* __restrict__ t) {
-  extern __shared__ double acc[];
-  const int tile = tile0 + blockIdx.x;
-  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
-  const int nt = r1 - r0, f = sa.sfirst[s];
-  const int64_t base = (int64_t)(f + r0) * R;
-  for (int i = threadIdx.x; i < nt * R; i += blockDim.x) acc[i] = rhs[base + i];
+// One kernel per ND-tree level and direction.  Storage: D_s = L_ss^{-1}
+// (packed lower), W_s = L[R_s,J_s] D_s (row-major).  Forward level l (reads only values final
+// before the level):   y[J_s] = D_s z[J_s]   and   z[anc] -= W_s z[J_s]   (s in level l).
+// Backward level l:    x[J_s] = D_s^T y[J_s] - W_s^T x[R_s].
+// A CTA owns a 32-row (or 32-column) output tile and a chunk of RC right-hand sides; blocks are
+// accumulated in a fixed order (deterministic, no atomics).  Operands are staged through shared
+// memory in 32-wide K chunks; each thread keeps a 2 x RC/8 register micro-tile.
+constexpr int kTR = 32, kKC = 32, kNT = 128;
+
+template <int RC>
+__device__ __forceinline__ void micro_tile(double (&acc)[2][RC / 8], const double (*Vc)[kKC + 1],
+                                           const double (*Zc)[RC], int ti, int tr) {
+#pragma unroll 4
+  for (int j = 0; j < kKC; ++j) {
+    const double a0 = Vc[ti][j], a1 = Vc[ti + 16][j];
+#pragma unroll
+    for (int q = 0; q < RC / 8; ++q) {
+      const double zz = Zc[j][tr + 8 * q];
+      acc[0][q] = fma(a0, zz, acc[0][q]);
+      acc[1][q] = fma(a1, zz, acc[1][q]);
+    }
+  }
+}
+
+template <int RC>
+__global__ void __launch_bounds__(kNT) k_fwd_level(SolveArgs sa, int task0, int R, double* __restrict__ z,
+                                                    double* __restrict__ y) {
+  constexpr int NQ = RC / 8;
+  __shared__ double Zc[kKC][RC];
+  __shared__ double Vc[kTR][kKC + 1];
+  __shared__ double Acc[kTR][RC];
+  const int task = task0 + blockIdx.x;
+  const int rc0 = blockIdx.y * RC;
+  const int rcn = min(RC, R - rc0);
+  const int type = sa.ft_type[task], s = sa.ft_sup[task], r0 = sa.ft_r0[task], r1 = sa.ft_r1[task];
+  const int f = sa.sfirst[s];
+  const int t = threadIdx.x, ti = t >> 3, tr = t & 7;
+  double acc[2][NQ];
+  if (type == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
+    const double* Dp = sa.D + sa.doff[s];
+    const int nrow = r1 - r0;
+    for (int j0 = 0; j0 < r1; j0 += kKC) {
+      const int nj = min(kKC, r1 - j0);
+      for (int idx = t; idx < kKC * RC; idx += kNT) {
+        const int j = idx / RC, r = idx - j * RC;
+        Zc[j][r] = (j < nj && r < rcn) ? z[(int64_t)(f + j0 + j) * R + rc0 + r] : 0.0;
+      }
+      for (int idx = t; idx < kTR * kKC; idx += kNT) {
+        const int i = idx / kKC, j = idx - i * kKC;
+        const int row = r0 + i, col = j0 + j;
+        Vc[i][j] = (i < nrow && j < nj && col <= row) ? Dp[(int64_t)row * (row + 1) / 2 + col] : 0.0;
+      }
+      __syncthreads();
+      micro_tile<RC>(acc, Vc, Zc, ti, tr);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = ti + 16 * q;
+      if (i < nrow)
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq) {
+          const int r = tr + 8 * qq;
+          if (r < rcn) y[(int64_t)(f + r0 + i) * R + rc0 + r] = acc[q][qq];
+        }
+    }
+    return;
+  }
+  for (int idx = t; idx < kTR * RC; idx += kNT) Acc[idx / RC][idx % RC] = 0.0;
   __syncthreads();
-  for (int bk = sa.tblk_ptr[tile]; bk < sa.tblk_ptr[tile + 1]; ++bk) {
-    const int d = sa.blk_d[bk], k0 = sa.blk_k0[bk], k1 = sa.blk_k1[bk];
-    const int nd = sa.ssize[d];
-    const double* Pd = sa.P + sa.poff[d];
-    const int32_t* Rd = sa.rows + sa.rptr[d];
-    const double* yd = y + (int64_t)sa.sfirst[d] * R;
-    for (int idx = threadIdx.x; idx < (k1 - k0) * R; idx += blockDim.x) {
-      const int kk = idx / R, r = idx - kk * R, k = k0 + kk;
-      const double* prow = Pd + (int64_t)k * nd;
-      double sum = 0;
-      for (int j = 0; j < nd; ++j) sum += prow[j] * yd[(int64_t)j * R + r];
-      acc[(Rd[k] - f - r0) * R + r] -= sum;
+  for (int bk = sa.ft_bptr[task]; bk < sa.ft_bptr[task + 1]; ++bk) {
+    const int d = sa.fb_s[bk], k0 = sa.fb_k0[bk], nb = sa.fb_k1[bk] - k0;
+    const int nd = sa.ssize[d], fd = sa.sfirst[d];
+    const double* Wd = sa.W + sa.poff[d] + (int64_t)k0 * nd;
+    const int32_t* Rd = sa.rows + sa.rptr[d] + k0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
+    for (int j0 = 0; j0 < nd; j0 += kKC) {
+      const int nj = min(kKC, nd - j0);
+      for (int idx = t; idx < kKC * RC; idx += kNT) {
+        const int j = idx / RC, r = idx - j * RC;
+        Zc[j][r] = (j < nj && r < rcn) ? z[(int64_t)(fd + j0 + j) * R + rc0 + r] : 0.0;
+      }
+      for (int idx = t; idx < kTR * kKC; idx += kNT) {
+        const int i = idx / kKC, j = idx - i * kKC;
+        Vc[i][j] = (i < nb && j < nj) ? Wd[(int64_t)i * nd + j0 + j] : 0.0;
+      }
+      __syncthreads();
+      micro_tile<RC>(acc, Vc, Zc, ti, tr);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = ti + 16 * q;
+      if (i < nb) {
+        const int rel = Rd[i] - f - r0;
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq) Acc[rel][tr + 8 * qq] += acc[q][qq];
+      }
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < nt * R; i += blockDim.x) t[base + i] = acc[i];
-}
-// Forward phase B: y[J_s] = D_s t[J_s]   (D_s = L_ss^{-1}, packed lower)
-__global__ void k_fwdB(SolveArgs sa, int tile0, int R, const double* __restrict__ t, double* __restrict__ y) {
-  const int tile = tile0 + blockIdx.x;
-  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
-  const int f = sa.sfirst[s];
-  const double* D = sa.D + sa.doff[s];
-  const double* ts = t + (int64_t)f * R;
-  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
-    const int ii = idx / R, r = idx - ii * R, i = r0 + ii;
-    const double* drow = D + (int64_t)i * (i + 1) / 2;
-    double sum = 0;
-    for (int j = 0; j <= i; ++j) sum += drow[j] * ts[(int64_t)j * R + r];
-    y[(int64_t)(f + i) * R + r] = sum;
+  for (int idx = t; idx < (r1 - r0) * RC; idx += kNT) {
+    const int i = idx / RC, r = idx - i * RC;
+    if (r < rcn) z[(int64_t)(f + r0 + i) * R + rc0 + r] -= Acc[i][r];
   }
 }
-// Backward L^T x = y: phase A  t[J_s] = y[J_s] - L[R_s, J_s]^T x[R_s]
-__global__ void k_bwdA(SolveArgs sa, int tile0, int R, const double* __restrict__ y, const double* __restrict__ x,
-                       double* __restrict__ t) {
-  const int tile = tile0 + blockIdx.x;
-  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
+
+template <int RC>
+__global__ void __launch_bounds__(kNT) k_bwd_level(SolveArgs sa, int task0, int R, const double* __restrict__ y,
+                                                    double* __restrict__ x) {
+  constexpr int NQ = RC / 8;
+  __shared__ double Zc[kKC][RC];
+  __shared__ double Vc[kTR][kKC + 1];
+  const int task = task0 + blockIdx.x;
+  const int rc0 = blockIdx.y * RC;
+  const int rcn = min(RC, R - rc0);
+  const int s = sa.bt_sup[task], c0 = sa.bt_c0[task], c1 = sa.bt_c1[task];
   const int f = sa.sfirst[s], ns = sa.ssize[s];
   const int nr = (int)(sa.rptr[s + 1] - sa.rptr[s]);
-  const double* Ps = sa.P + sa.poff[s];
+  const int ncol = c1 - c0;
+  const double* Dp = sa.D + sa.doff[s];
+  const double* Ws = sa.W + sa.poff[s];
   const int32_t* Rs = sa.rows + sa.rptr[s];
-  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
-    const int cc = idx / R, r = idx - cc * R, c = r0 + cc;
-    double sum = y[(int64_t)(f + c) * R + r];
-    for (int k = 0; k < nr; ++k) sum -= Ps[(int64_t)k * ns + c] * x[(int64_t)Rs[k] * R + r];
-    t[(int64_t)(f + c) * R + r] = sum;
+  const int t = threadIdx.x, ti = t >> 3, tr = t & 7;
+  double acc[2][NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
+  for (int i0 = c0; i0 < ns; i0 += kKC) {  // D_s^T y[J_s]: rows i >= column c
+    const int ni = min(kKC, ns - i0);
+    for (int idx = t; idx < kKC * RC; idx += kNT) {
+      const int k = idx / RC, r = idx - k * RC;
+      Zc[k][r] = (k < ni && r < rcn) ? y[(int64_t)(f + i0 + k) * R + rc0 + r] : 0.0;
+    }
+    for (int idx = t; idx < kTR * kKC; idx += kNT) {
+      const int k = idx / kTR, c = idx - k * kTR;
+      const int row = i0 + k, col = c0 + c;
+      Vc[c][k] = (c < ncol && k < ni && row >= col) ? Dp[(int64_t)row * (row + 1) / 2 + col] : 0.0;
+    }
+    __syncthreads();
+    micro_tile<RC>(acc, Vc, Zc, ti, tr);
+    __syncthreads();
   }
-}
-// Backward phase B: x[J_s] = D_s^T t[J_s]
-__global__ void k_bwdB(SolveArgs sa, int tile0, int R, const double* __restrict__ t, double* __restrict__ x) {
-  const int tile = tile0 + blockIdx.x;
-  const int s = sa.tile_sup[tile], r0 = sa.tile_r0[tile], r1 = sa.tile_r1[tile];
-  const int f = sa.sfirst[s], ns = sa.ssize[s];
-  const double* D = sa.D + sa.doff[s];
-  const double* ts = t + (int64_t)f * R;
-  for (int idx = threadIdx.x; idx < (r1 - r0) * R; idx += blockDim.x) {
-    const int cc = idx / R, r = idx - cc * R, c = r0 + cc;
-    double sum = 0;
-    for (int i = c; i < ns; ++i) sum += D[(int64_t)i * (i + 1) / 2 + c] * ts[(int64_t)i * R + r];
-    x[(int64_t)(f + c) * R + r] = sum;
+  for (int k0 = 0; k0 < nr; k0 += kKC) {  // - W_s^T x[R_s]
+    const int nk = min(kKC, nr - k0);
+    for (int idx = t; idx < kKC * RC; idx += kNT) {
+      const int k = idx / RC, r = idx - k * RC;
+      Zc[k][r] = (k < nk && r < rcn) ? x[(int64_t)Rs[k0 + k] * R + rc0 + r] : 0.0;
+    }
+    for (int idx = t; idx < kTR * kKC; idx += kNT) {
+      const int k = idx / kTR, c = idx - k * kTR;
+      Vc[c][k] = (c < ncol && k < nk) ? -Ws[(int64_t)(k0 + k) * ns + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    micro_tile<RC>(acc, Vc, Zc, ti, tr);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int c = ti + 16 * q;
+    if (c < ncol)
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        const int r = tr + 8 * qq;
+        if (r < rcn) x[(int64_t)(f + c0 + c) * R + rc0 + r] = acc[q][qq];
+      }
   }
 }
 

@@ -29,8 +29,9 @@ struct SolveArgs {
   const int32_t *sfirst, *ssize;
   const int64_t *rptr, *doff, *poff;
   const int32_t* rows;
-  const double *D, *P;
-  const int32_t *tile_sup, *tile_r0, *tile_r1, *tblk_ptr, *blk_d, *blk_k0, *blk_k1;
+  const double *D, *W;
+  const int32_t *ft_type, *ft_sup, *ft_r0, *ft_r1, *ft_bptr, *fb_s, *fb_k0, *fb_k1;
+  const int32_t *bt_sup, *bt_c0, *bt_c1;
 };
 
 struct DotArgs {

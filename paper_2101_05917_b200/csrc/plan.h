@@ -37,16 +37,19 @@ struct HostPlan {
   std::vector<int32_t> sfirst, ssize, parent, height;
   std::vector<int64_t> rptr;         // [nsup+1] into rows
   std::vector<int32_t> rows;         // below-block row positions (sorted, > last col)
-  std::vector<int64_t> doff, poff;   // offsets of D_s (packed lower, = L_ss^{-1}) and P_s
-  std::vector<double> D, P;          // P_s = L[R_s, J_s] row-major (nr x ns)
+  std::vector<int64_t> doff, poff;   // offsets of D_s (packed lower, = L_ss^{-1}) and W_s
+  std::vector<double> D, P;          // P holds W_s = L[R_s, J_s] L_ss^{-1} row-major (nr x ns)
   int64_t nnzL = 0;                  // stored entries of L_s (diag blocks packed + panels)
   double factor_flops = 0, factor_ms = 0;
-  // ---- solve schedule ----
+  // ---- solve schedule (one kernel per tree level and direction) ----
   int nlevels = 0;
-  std::vector<int32_t> lvl_ptr;      // [nlevels+1] into tiles (tiles grouped by height)
-  std::vector<int32_t> tile_sup, tile_r0, tile_r1;
-  std::vector<int32_t> tblk_ptr;     // [ntiles+1] forward update blocks per tile
-  std::vector<int32_t> blk_d, blk_k0, blk_k1;
+  // forward level l: tasks [flvl_ptr[l], flvl_ptr[l+1]).  type 0 (D task): y[J_s rows r0..r1) =
+  // D_s z[J_s]; type 1 (W task): z[J_a rows r0..r1) -= sum_blocks W_s[k0..k1) z[J_s].
+  std::vector<int32_t> flvl_ptr, ft_type, ft_sup, ft_r0, ft_r1, ft_bptr;
+  std::vector<int32_t> fb_s, fb_k0, fb_k1;
+  // backward level l: column tiles [blvl_ptr[l], blvl_ptr[l+1]) of level-l supernodes:
+  // x[J_s cols c0..c1) = D_s^T y[J_s] - W_s^T x[R_s].
+  std::vector<int32_t> blvl_ptr, bt_sup, bt_c0, bt_c1;
 };
 
 // Build everything host-side.  Returns "" on success, else an error message;

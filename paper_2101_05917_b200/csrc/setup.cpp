@@ -445,9 +445,19 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
       if (!partial_cholesky(F.data(), f, ns, inner_par)) return false;
       schur_update(F.data(), f, ns, inner_par);
       tri_inverse(F.data(), f, ns, P.D.data() + P.doff[s], inner_par);
-      double* Ps = P.P.data() + P.poff[s];
-      for (int i = 0; i < nr; ++i)
-        std::memcpy(Ps + (int64_t)i * ns, F.data() + (int64_t)(ns + i) * f, sizeof(double) * ns);
+      // W_s = L21 L11^{-1} (row-major nr x ns): the per-level solve operator
+      double* Ws = P.P.data() + P.poff[s];
+      const double* Ds = P.D.data() + P.doff[s];
+#pragma omp parallel for schedule(static) if (inner_par && nr > 64)
+      for (int i = 0; i < nr; ++i) {
+        const double* Li = F.data() + (int64_t)(ns + i) * f;
+        double* Wi = Ws + (int64_t)i * ns;
+        for (int c = 0; c < ns; ++c) {
+          double acc = 0;
+          for (int j = c; j < ns; ++j) acc += Li[j] * Ds[(int64_t)j * (j + 1) / 2 + c];
+          Wi[c] = acc;
+        }
+      }
       if (P.parent[s] >= 0 && nr > 0) {
         U[s].assign((int64_t)nr * nr, 0.0);
         for (int i = 0; i < nr; ++i)
@@ -477,53 +487,61 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
     return "A is not symmetric positive definite (non-positive pivot in the Cholesky factorisation)";
   }
 
-  // ---------------- solve schedule: tiles by height; forward update blocks per tile
-  // blocks (s <- d): rows R_d[k0:k1) that fall into J_s (contiguous since R_d sorted)
-  std::vector<std::vector<std::array<int32_t, 3>>> into(P.nsup);
-  for (int d = 0; d < P.nsup; ++d) {
-    const int64_t b = P.rptr[d], e = P.rptr[d + 1];
-    for (int64_t k = b; k < e;) {
-      const int s = sup_of_pos[P.rows[k]];
-      int64_t k2 = k;
-      while (k2 < e && sup_of_pos[P.rows[k2]] == s) ++k2;
-      into[s].push_back({d, (int32_t)(k - b), (int32_t)(k2 - b)});
-      k = k2;
-    }
-  }
+  // ---------------- solve schedule: one forward and one backward kernel per tree level
   P.nlevels = H + 1;
-  P.lvl_ptr.assign(P.nlevels + 1, 0);
-  P.tile_sup.clear();
-  P.tile_r0.clear();
-  P.tile_r1.clear();
-  P.tblk_ptr.assign(1, 0);
-  P.blk_d.clear();
-  P.blk_k0.clear();
-  P.blk_k1.clear();
+  P.flvl_ptr.assign(1, 0);
+  P.blvl_ptr.assign(1, 0);
+  P.ft_type.clear(); P.ft_sup.clear(); P.ft_r0.clear(); P.ft_r1.clear(); P.ft_bptr.assign(1, 0);
+  P.fb_s.clear(); P.fb_k0.clear(); P.fb_k1.clear();
+  P.bt_sup.clear(); P.bt_c0.clear(); P.bt_c1.clear();
   for (int lev = 0; lev <= H; ++lev) {
+    // D tasks: row tiles of every level-l supernode
+    for (int s : byh[lev])
+      for (int r0 = 0; r0 < P.ssize[s]; r0 += kTile) {
+        P.ft_type.push_back(0);
+        P.ft_sup.push_back(s);
+        P.ft_r0.push_back(r0);
+        P.ft_r1.push_back(std::min(P.ssize[s], r0 + kTile));
+        P.ft_bptr.push_back((int32_t)P.fb_s.size());
+      }
+    // W tasks: ancestor row tiles touched by level-l panels; blocks in increasing s (fixed order)
+    std::vector<std::array<int32_t, 5>> blks;  // (anc, tile, s, k0, k1)
     for (int s : byh[lev]) {
-      const int ns = P.ssize[s];
-      for (int r0 = 0; r0 < ns; r0 += kTile) {
-        const int r1 = std::min(ns, r0 + kTile);
-        P.tile_sup.push_back(s);
-        P.tile_r0.push_back(r0);
-        P.tile_r1.push_back(r1);
-        for (auto& blk : into[s]) {
-          const int d = blk[0];
-          const int32_t* Rd = P.rows.data() + P.rptr[d];
-          int k0 = blk[1], k1 = blk[2];
-          while (k0 < k1 && Rd[k0] - P.sfirst[s] < r0) ++k0;
-          int k1b = k0;
-          while (k1b < k1 && Rd[k1b] - P.sfirst[s] < r1) ++k1b;
-          if (k1b > k0) {
-            P.blk_d.push_back(d);
-            P.blk_k0.push_back(k0);
-            P.blk_k1.push_back(k1b);
-          }
-        }
-        P.tblk_ptr.push_back((int32_t)P.blk_d.size());
+      const int64_t b = P.rptr[s], e = P.rptr[s + 1];
+      for (int64_t k = b; k < e;) {
+        const int a = sup_of_pos[P.rows[k]];
+        const int tile = (P.rows[k] - P.sfirst[a]) / kTile;
+        int64_t k2 = k;
+        while (k2 < e && sup_of_pos[P.rows[k2]] == a && (P.rows[k2] - P.sfirst[a]) / kTile == tile) ++k2;
+        blks.push_back({a, tile, s, (int32_t)(k - b), (int32_t)(k2 - b)});
+        k = k2;
       }
     }
-    P.lvl_ptr[lev + 1] = (int32_t)P.tile_sup.size();
+    std::sort(blks.begin(), blks.end());
+    for (size_t i = 0; i < blks.size();) {
+      size_t j = i;
+      const int a = blks[i][0], tile = blks[i][1];
+      while (j < blks.size() && blks[j][0] == a && blks[j][1] == tile) {
+        P.fb_s.push_back(blks[j][2]);
+        P.fb_k0.push_back(blks[j][3]);
+        P.fb_k1.push_back(blks[j][4]);
+        ++j;
+      }
+      P.ft_type.push_back(1);
+      P.ft_sup.push_back(a);
+      P.ft_r0.push_back(tile * kTile);
+      P.ft_r1.push_back(std::min(P.ssize[a], (tile + 1) * kTile));
+      P.ft_bptr.push_back((int32_t)P.fb_s.size());
+      i = j;
+    }
+    P.flvl_ptr.push_back((int32_t)P.ft_type.size());
+    for (int s : byh[lev])
+      for (int c0 = 0; c0 < P.ssize[s]; c0 += kTile) {
+        P.bt_sup.push_back(s);
+        P.bt_c0.push_back(c0);
+        P.bt_c1.push_back(std::min(P.ssize[s], c0 + kTile));
+      }
+    P.blvl_ptr.push_back((int32_t)P.bt_sup.size());
   }
   return "";
 }

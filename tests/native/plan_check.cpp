@@ -30,59 +30,45 @@ int main(int argc, char** argv) {
   std::vector<double> v(N), b(N, 0.0);
   for (auto& x : v) x = nd(rng);
   for (int p = 0; p < N; ++p) for (int64_t k = P.a_ptr[p]; k < P.a_ptr[p + 1]; ++k) b[p] += P.a_val[k] * v[P.a_col[k]];
-  // forward L y = b (left-looking pull as on the GPU: blocks)
-  std::vector<double> y(N), t(N);
-  for (int lev = 0; lev < P.nlevels; ++lev)
-    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
-      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
-      for (int i = r0; i < r1; ++i) t[f + i] = b[f + i];
-      for (int bk = P.tblk_ptr[tl]; bk < P.tblk_ptr[tl + 1]; ++bk) {
-        int d = P.blk_d[bk], nd_ = P.ssize[d];
-        for (int k = P.blk_k0[bk]; k < P.blk_k1[bk]; ++k) {
-          double sum = 0;
-          for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * y[P.sfirst[d] + j];
-          t[P.rows[P.rptr[d] + k]] -= sum;
-        }
-      }
-    }
-    // (tiles of a level finish before phase B in this serial emulation)
-  // redo properly level by level: phase A then B
-  std::fill(y.begin(), y.end(), 0.0);
+  // forward: per level, D tasks y[J_s] = D_s z[J_s]; W tasks z[anc] -= W_s z_old[J_s]
+  std::vector<double> z(b), y(N, 0.0), x(N, 0.0);
   for (int lev = 0; lev < P.nlevels; ++lev) {
-    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
-      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
-      for (int i = r0; i < r1; ++i) t[f + i] = b[f + i];
-      for (int bk = P.tblk_ptr[tl]; bk < P.tblk_ptr[tl + 1]; ++bk) {
-        int d = P.blk_d[bk], nd_ = P.ssize[d];
-        for (int k = P.blk_k0[bk]; k < P.blk_k1[bk]; ++k) {
-          double sum = 0;
-          for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * y[P.sfirst[d] + j];
-          t[P.rows[P.rptr[d] + k]] -= sum;
+    std::vector<double> zold = z;
+    for (int t = P.flvl_ptr[lev]; t < P.flvl_ptr[lev + 1]; ++t) {
+      int s = P.ft_sup[t], r0 = P.ft_r0[t], r1 = P.ft_r1[t], f = P.sfirst[s];
+      if (P.ft_type[t] == 0) {
+        for (int i = r0; i < r1; ++i) { double sum = 0; for (int j = 0; j <= i; ++j) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + j] * zold[f + j]; y[f + i] = sum; }
+      } else {
+        for (int bk = P.ft_bptr[t]; bk < P.ft_bptr[t + 1]; ++bk) {
+          int d = P.fb_s[bk], nd_ = P.ssize[d];
+          for (int k = P.fb_k0[bk]; k < P.fb_k1[bk]; ++k) {
+            int r = P.rows[P.rptr[d] + k];
+            if (r < f + r0 || r >= f + r1) { printf("bad block row\n"); return 3; }
+            double sum = 0;
+            for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * zold[P.sfirst[d] + j];
+            z[r] -= sum;
+          }
         }
       }
-    }
-    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
-      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s];
-      for (int i = r0; i < r1; ++i) { double sum = 0; for (int j = 0; j <= i; ++j) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + j] * t[f + j]; y[f + i] = sum; }
     }
   }
-  std::vector<double> x(N), tt(N);
   for (int lev = P.nlevels - 1; lev >= 0; --lev) {
-    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
-      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s], ns = P.ssize[s];
+    for (int t = P.blvl_ptr[lev]; t < P.blvl_ptr[lev + 1]; ++t) {
+      int s = P.bt_sup[t], c0 = P.bt_c0[t], c1 = P.bt_c1[t], f = P.sfirst[s], ns = P.ssize[s];
       int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-      for (int c = r0; c < r1; ++c) { double sum = y[f + c]; for (int k = 0; k < nr; ++k) sum -= P.P[P.poff[s] + (int64_t)k * ns + c] * x[P.rows[P.rptr[s] + k]]; tt[f + c] = sum; }
-    }
-    for (int tl = P.lvl_ptr[lev]; tl < P.lvl_ptr[lev + 1]; ++tl) {
-      int s = P.tile_sup[tl], r0 = P.tile_r0[tl], r1 = P.tile_r1[tl], f = P.sfirst[s], ns = P.ssize[s];
-      for (int c = r0; c < r1; ++c) { double sum = 0; for (int i = c; i < ns; ++i) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + c] * tt[f + i]; x[f + c] = sum; }
+      for (int c = c0; c < c1; ++c) {
+        double sum = 0;
+        for (int i = c; i < ns; ++i) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + c] * y[f + i];
+        for (int k = 0; k < nr; ++k) sum -= P.P[P.poff[s] + (int64_t)k * ns + c] * x[P.rows[P.rptr[s] + k]];
+        x[f + c] = sum;
+      }
     }
   }
   double err = 0, mx = 0;
   for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
   int64_t nnzA = P.a_ptr[N];
-  printf("n=%d nfree=%d nsup=%d levels=%d tiles=%zu blocks=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
-         n, N, P.nsup, P.nlevels, P.tile_sup.size(), P.blk_d.size(), (long long)nnzA, (long long)P.nnzL, P.factor_flops,
+  printf("n=%d nfree=%d nsup=%d levels=%d ftasks=%zu fblocks=%zu btasks=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
+         n, N, P.nsup, P.nlevels, P.ft_type.size(), P.fb_s.size(), P.bt_sup.size(), (long long)nnzA, (long long)P.nnzL, P.factor_flops,
          P.factor_ms, err / mx);
   return err / mx < 1e-10 ? 0 : 2;
 }
