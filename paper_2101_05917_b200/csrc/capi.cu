@@ -226,7 +226,7 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   const HostPlan& P = s->plan;
   {
     ProfScope ps(s, 0);
-    k_elem_residual<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
+    k_elem_residual<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
                                                                          s->EF, s->EE);
     LAUNCH_CHECK(s);
   }
@@ -242,7 +242,7 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
               int64_t act_bstride) {
   const HostPlan& P = s->plan;
   ProfScope ps(s, 3);
-  k_elem_AN<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
+  k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
                                                                  s->EF);
   LAUNCH_CHECK(s);
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
@@ -608,7 +608,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       }
       // parameter terms, f_ext accumulation, state adjoint update
       ProfScope ps_param(s, 5);
-      k_elem_param<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
+      k_elem_param<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
                                                                       s->DW, s->has_act ? s->DR : nullptr);
       LAUNCH_CHECK(s);
       k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->DW, P.m, B, s->dw_acc, 1);
@@ -750,7 +750,7 @@ pd_status pd_apply_AN(pd_sim* s, int32_t B, const double* x, const double* young
     LAUNCH_CHECK(s);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(p, s->Pv, n3, B);
     LAUNCH_CHECK(s);
-    k_elem_AN<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
+    k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
     LAUNCH_CHECK(s);
     k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Pv, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                             s->d_nofix, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, s->Q,

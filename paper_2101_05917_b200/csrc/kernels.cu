@@ -133,7 +133,7 @@ __device__ void polar_rotation(const double* F, double* R) {
   }
   double X[9];
   for (int i = 0; i < 9; ++i) X[i] = F[i];
-  bool scaled = true;
+  bool scaled = true, last = false;
   for (int it = 0; it < 40; ++it) {
     double C[9];
     cof3(X, C);
@@ -153,7 +153,10 @@ __device__ void polar_rotation(const double* F, double* R) {
       X[i] = xn;
     }
     if (diff < 1e-4 * nrm) scaled = false;
-    if (diff <= 1e-32 * nrm) break;
+    // quadratic convergence: once the (unscaled) step is below 1e-9 the next one is below
+    // fp64 resolution — take exactly one more step and stop.
+    if (last) break;
+    if (!scaled && diff < 1e-18 * nrm) last = true;
   }
   for (int i = 0; i < 9; ++i) R[i] = X[i];
 }
@@ -189,65 +192,99 @@ __global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
 }
 
 // ----------------------------------------------------------------- K1: local step
-// One thread per (element, sim).  Writes EF[e][a][axis][b] and EE[e][b].
-__global__ void __launch_bounds__(128) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
+// One thread per (element, sim, quad point), q fastest: the 8 quadrature points of an
+// (element, sim) pair are 8 consecutive lanes; their 24 nodal force contributions are summed by a
+// 3-stage xor butterfly (identical bits in all 8 lanes: fixed pairing, commutative adds), then lane q
+// stores components 3q..3q+2.  No atomics; deterministic.
+__device__ __forceinline__ double qsum8(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  return v;
+}
+
+// Deformation gradient F (and, if P != null, dF = G_q p_e) at quad point q of element e, sim b.
+__device__ __forceinline__ void load_F(const double* __restrict__ X, const int32_t* __restrict__ hex8,
+                                       const Stencil& st, int e, int b, int q, int B, double* F) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) F[k] = 0.0;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int node = __ldg(hex8 + 8 * (int64_t)e + a);
+    const double d0 = st.dN[q][a][0], d1 = st.dN[q][a][1], d2 = st.dN[q][a][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double xv = X[(3 * (int64_t)node + i) * B + b];
+      F[3 * i] = fma(xv, d0, F[3 * i]);
+      F[3 * i + 1] = fma(xv, d1, F[3 * i + 1]);
+      F[3 * i + 2] = fma(xv, d2, F[3 * i + 2]);
+    }
+  }
+}
+
+// G_q^T P summed over the 8 lanes of the (e, b) group, written to EF[e][a][i][b].
+__device__ __forceinline__ void store_force(const double* Pm, const Stencil& st, int e, int b, int q, int B,
+                                            double* __restrict__ EF) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const double d0 = st.dN[q][a][0], d1 = st.dN[q][a][1], d2 = st.dN[q][a][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double v = qsum8(Pm[3 * i] * d0 + Pm[3 * i + 1] * d1 + Pm[3 * i + 2] * d2);
+      if (EF && 3 * a + i >= 3 * q && 3 * a + i < 3 * q + 3) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                        double* __restrict__ EF, double* __restrict__ EE) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
-  if (tid >= (int64_t)ea.m * B) return;
-  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
-  double xe[8][3];
-  for (int a = 0; a < 8; ++a) {
-    const int node = ea.hex8[8 * (int64_t)e + a];
-    for (int i = 0; i < 3; ++i) xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
-  }
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  // dead lanes (past the end) compute on pair 0 and store nothing: every shuffle sees a full warp
+  const bool live = pair < (int64_t)ea.m * B;
+  const int64_t pr = live ? pair : 0;
+  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   const double w = ea.w_sim[b];
-  const double r_act = (st.w_m != 0.0 && ea.act) ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
-  double f[8][3];
-  for (int a = 0; a < 8; ++a) f[a][0] = f[a][1] = f[a][2] = 0.0;
-  double energy = 0.0;
-  for (int q = 0; q < 8; ++q) {
-    double F[9];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        double s = 0;
-        for (int a = 0; a < 8; ++a) s += xe[a][i] * st.dN[q][a][j];
-        F[3 * i + j] = s;
-      }
-    double R[9];
-    polar_rotation(F, R);
-    double Pm[9];
-    double en = 0;
-    for (int k = 0; k < 9; ++k) {
-      const double dk = F[k] - R[k];
-      en += dk * dk;
-      Pm[k] = w * st.V * dk;
-    }
-    energy += 0.5 * w * st.V * en;
-    if (st.w_m != 0.0) {
-      double Fm[3], nr = 0;
-      for (int i = 0; i < 3; ++i) {
-        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-        nr += Fm[i] * Fm[i];
-      }
-      nr = sqrt(nr);
-      double dm[3], em = 0;
-      for (int i = 0; i < 3; ++i) {
-        const double p = nr > 0 ? r_act * Fm[i] / nr : r_act * st.fiber[i];
-        dm[i] = Fm[i] - p;
-        em += dm[i] * dm[i];
-      }
-      energy += 0.5 * st.w_m * st.V * em;
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
-    }
-    for (int a = 0; a < 8; ++a)
-      for (int i = 0; i < 3; ++i)
-        f[a][i] += Pm[3 * i] * st.dN[q][a][0] + Pm[3 * i + 1] * st.dN[q][a][1] + Pm[3 * i + 2] * st.dN[q][a][2];
+  double F[9];
+  load_F(X, ea.hex8, st, e, b, q, B, F);
+  double R[9];
+  polar_rotation(F, R);
+  double Pm[9];
+  double en = 0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const double dk = F[k] - R[k];
+    en += dk * dk;
+    Pm[k] = w * st.V * dk;
   }
-  for (int a = 0; a < 8; ++a)
-    for (int i = 0; i < 3; ++i) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = f[a][i];
-  if (EE) EE[(int64_t)e * B + b] = energy;
+  double energy = 0.5 * w * st.V * en;
+  if (st.w_m != 0.0) {
+    const double r_act = ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
+    double Fm[3], nr = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+      nr += Fm[i] * Fm[i];
+    }
+    nr = sqrt(nr);
+    double dm[3], em = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double p = nr > 0 ? r_act * Fm[i] / nr : r_act * st.fiber[i];
+      dm[i] = Fm[i] - p;
+      em += dm[i] * dm[i];
+    }
+    energy += 0.5 * st.w_m * st.V * em;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
+  }
+  store_force(Pm, st, e, b, q, B, live ? EF : nullptr);
+  energy = qsum8(energy);
+  if (live && EE && q == 0) EE[(int64_t)e * B + b] = energy;
 }
 
 // Rotations of every quad point (diagnostic / parity hook).
@@ -320,138 +357,119 @@ __device__ void solve_rot_derivative(const double* S, const double* rhs, double 
   for (int i = 0; i < 3; ++i) om[i] = V[3 * i] * t[0] + V[3 * i + 1] * t[1] + V[3 * i + 2] * t[2];
 }
 
-__global__ void __launch_bounds__(128) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
+__global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
                                                  Stencil st, ElemArgs ea, double* __restrict__ EF) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
-  if (tid >= (int64_t)ea.m * B) return;
-  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
-  double xe[8][3], pe[8][3];
-  for (int a = 0; a < 8; ++a) {
-    const int node = ea.hex8[8 * (int64_t)e + a];
-    for (int i = 0; i < 3; ++i) {
-      xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
-      pe[a][i] = Pv[(3 * (int64_t)node + i) * B + b];
-    }
-  }
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const bool live = pair < (int64_t)ea.m * B;
+  const int64_t pr = live ? pair : 0;
+  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   const double w = ea.w_sim[b];
-  const double r_act = (st.w_m != 0.0 && ea.act) ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
-  double f[8][3];
-  for (int a = 0; a < 8; ++a) f[a][0] = f[a][1] = f[a][2] = 0.0;
-  for (int q = 0; q < 8; ++q) {
-    double F[9], dF[9];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        double s = 0, t = 0;
-        for (int a = 0; a < 8; ++a) {
-          s += xe[a][i] * st.dN[q][a][j];
-          t += pe[a][i] * st.dN[q][a][j];
-        }
-        F[3 * i + j] = s;
-        dF[3 * i + j] = t;
-      }
-    double R[9];
-    polar_rotation(F, R);
-    double S[9];  // S = R^T F, symmetrised
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) S[3 * i + j] = R[i] * F[j] + R[3 + i] * F[3 + j] + R[6 + i] * F[6 + j];
-    for (int i = 0; i < 3; ++i)
-      for (int j = i + 1; j < 3; ++j) {
-        const double avg = 0.5 * (S[3 * i + j] + S[3 * j + i]);
-        S[3 * i + j] = S[3 * j + i] = avg;
-      }
-    double Wm[9];  // R^T dF
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) Wm[3 * i + j] = R[i] * dF[j] + R[3 + i] * dF[3 + j] + R[6 + i] * dF[6 + j];
-    // vee(W - W^T) = (W21 - W12, W02 - W20, W10 - W01)
-    const double rhs[3] = {Wm[7] - Wm[5], Wm[2] - Wm[6], Wm[3] - Wm[1]};
-    double om[3];
-    solve_rot_derivative(S, rhs, st.clamp, om);
-    // dR = R [om]x ; [om]x = [[0,-o2,o1],[o2,0,-o0],[-o1,o0,0]]
-    double Pm[9];
-    for (int i = 0; i < 3; ++i) {
-      const double r0 = R[3 * i], r1 = R[3 * i + 1], r2 = R[3 * i + 2];
-      const double dR0 = r1 * om[2] - r2 * om[1];
-      const double dR1 = -r0 * om[2] + r2 * om[0];
-      const double dR2 = r0 * om[1] - r1 * om[0];
-      Pm[3 * i] = w * st.V * (dF[3 * i] - dR0);
-      Pm[3 * i + 1] = w * st.V * (dF[3 * i + 1] - dR1);
-      Pm[3 * i + 2] = w * st.V * (dF[3 * i + 2] - dR2);
+  double F[9], dF[9];
+  load_F(X, ea.hex8, st, e, b, q, B, F);
+  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
+  double R[9];
+  polar_rotation(F, R);
+  double S[9];  // S = R^T F, symmetrised
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[3 * i + j] = R[i] * F[j] + R[3 + i] * F[3 + j] + R[6 + i] * F[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 3; ++j) {
+      const double avg = 0.5 * (S[3 * i + j] + S[3 * j + i]);
+      S[3 * i + j] = S[3 * j + i] = avg;
     }
-    if (st.w_m != 0.0) {
-      double Fm[3], dFm[3], nr = 0;
-      for (int i = 0; i < 3; ++i) {
-        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-        dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
-        nr += Fm[i] * Fm[i];
-      }
-      nr = sqrt(nr);
-      double jd[3] = {0, 0, 0};
-      if (nr > 0) {
-        const double nd = (Fm[0] * dFm[0] + Fm[1] * dFm[1] + Fm[2] * dFm[2]) / nr;
-        for (int i = 0; i < 3; ++i) jd[i] = r_act / nr * (dFm[i] - nd * Fm[i] / nr);
-      }
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * (dFm[i] - jd[i]) * st.fiber[j];
-    }
-    for (int a = 0; a < 8; ++a)
-      for (int i = 0; i < 3; ++i)
-        f[a][i] += Pm[3 * i] * st.dN[q][a][0] + Pm[3 * i + 1] * st.dN[q][a][1] + Pm[3 * i + 2] * st.dN[q][a][2];
+  double Wm[9];  // R^T dF
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Wm[3 * i + j] = R[i] * dF[j] + R[3 + i] * dF[3 + j] + R[6 + i] * dF[6 + j];
+  // vee(W - W^T) = (W21 - W12, W02 - W20, W10 - W01)
+  const double rhs[3] = {Wm[7] - Wm[5], Wm[2] - Wm[6], Wm[3] - Wm[1]};
+  double om[3];
+  solve_rot_derivative(S, rhs, st.clamp, om);
+  // dR = R [om]x ; [om]x = [[0,-o2,o1],[o2,0,-o0],[-o1,o0,0]]
+  double Pm[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double r0 = R[3 * i], r1 = R[3 * i + 1], r2 = R[3 * i + 2];
+    const double dR0 = r1 * om[2] - r2 * om[1];
+    const double dR1 = -r0 * om[2] + r2 * om[0];
+    const double dR2 = r0 * om[1] - r1 * om[0];
+    Pm[3 * i] = w * st.V * (dF[3 * i] - dR0);
+    Pm[3 * i + 1] = w * st.V * (dF[3 * i + 1] - dR1);
+    Pm[3 * i + 2] = w * st.V * (dF[3 * i + 2] - dR2);
   }
-  for (int a = 0; a < 8; ++a)
-    for (int i = 0; i < 3; ++i) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = f[a][i];
+  if (st.w_m != 0.0) {
+    const double r_act = ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
+    double Fm[3], dFm[3], nr = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+      dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+      nr += Fm[i] * Fm[i];
+    }
+    nr = sqrt(nr);
+    double jd[3] = {0, 0, 0};
+    if (nr > 0) {
+      const double nd = (Fm[0] * dFm[0] + Fm[1] * dFm[1] + Fm[2] * dFm[2]) / nr;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) jd[i] = r_act / nr * (dFm[i] - nd * Fm[i] / nr);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * (dFm[i] - jd[i]) * st.fiber[j];
+  }
+  store_force(Pm, st, e, b, q, B, live ? EF : nullptr);
 }
 
 // Parameter-gradient terms at x_{i+1} for adjoint u (chain rule):
 //   DW[e][b] = -sum_q V <G_q u_e, F_q - R_q>,  DR[e][b] = w_m sum_q V n_hat^T (G_q u_e) m
-__global__ void __launch_bounds__(128) k_elem_param(const double* __restrict__ X, const double* __restrict__ U,
+__global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X, const double* __restrict__ U,
                                                     Stencil st, ElemArgs ea, double* __restrict__ DW,
                                                     double* __restrict__ DR) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
-  if (tid >= (int64_t)ea.m * B) return;
-  const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
-  double xe[8][3], ue[8][3];
-  for (int a = 0; a < 8; ++a) {
-    const int node = ea.hex8[8 * (int64_t)e + a];
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const bool live = pair < (int64_t)ea.m * B;
+  const int64_t pr = live ? pair : 0;
+  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
+  double F[9], dF[9];
+  load_F(X, ea.hex8, st, e, b, q, B, F);
+  load_F(U, ea.hex8, st, e, b, q, B, dF);
+  double R[9];
+  polar_rotation(F, R);
+  double acc = 0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc += dF[k] * (F[k] - R[k]);
+  double dw = -st.V * acc, dr = 0;
+  if (st.w_m != 0.0 && DR) {
+    double Fm[3], dFm[3], nr = 0;
+#pragma unroll
     for (int i = 0; i < 3; ++i) {
-      xe[a][i] = X[(3 * (int64_t)node + i) * B + b];
-      ue[a][i] = U[(3 * (int64_t)node + i) * B + b];
+      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+      dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+      nr += Fm[i] * Fm[i];
     }
+    nr = sqrt(nr);
+    double nh[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) nh[i] = nr > 0 ? Fm[i] / nr : st.fiber[i];
+    dr = st.w_m * st.V * (nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2]);
   }
-  double dw = 0, dr = 0;
-  for (int q = 0; q < 8; ++q) {
-    double F[9], dF[9];
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        double s = 0, t = 0;
-        for (int a = 0; a < 8; ++a) {
-          s += xe[a][i] * st.dN[q][a][j];
-          t += ue[a][i] * st.dN[q][a][j];
-        }
-        F[3 * i + j] = s;
-        dF[3 * i + j] = t;
-      }
-    double R[9];
-    polar_rotation(F, R);
-    double acc = 0;
-    for (int k = 0; k < 9; ++k) acc += dF[k] * (F[k] - R[k]);
-    dw -= st.V * acc;
-    if (st.w_m != 0.0 && DR) {
-      double Fm[3], dFm[3], nr = 0;
-      for (int i = 0; i < 3; ++i) {
-        Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-        dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
-        nr += Fm[i] * Fm[i];
-      }
-      nr = sqrt(nr);
-      double nh[3];
-      for (int i = 0; i < 3; ++i) nh[i] = nr > 0 ? Fm[i] / nr : st.fiber[i];
-      dr += st.w_m * st.V * (nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2]);
-    }
+  dw = qsum8(dw);
+  dr = qsum8(dr);
+  if (live && q == 0) {
+    DW[(int64_t)e * B + b] = dw;
+    if (DR) DR[(int64_t)e * B + b] = dr;
   }
-  DW[(int64_t)e * B + b] = dw;
-  if (DR) DR[(int64_t)e * B + b] = dr;
 }
 
 // ----------------------------------------------------------------- K2: deterministic gather
