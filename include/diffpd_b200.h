@@ -165,6 +165,11 @@ pd_status pd_info(const pd_sim* sim, int64_t* out, int32_t n);
  * ms[k] = total milliseconds, count[k] = number of timed regions. */
 pd_status pd_profile(const pd_sim* sim, double* ms, int64_t* count, int32_t n);
 
+/* Final active set of Alg. 1 for every (sim, step) of the last pd_forward:
+ * out = HOST uint8 [B][steps][n_contact], 1 = normal DoF of candidate j pinned at the plane
+ * (candidate order = opts.contact_nodes).  PD_ERR_STATE without a forward or without contact. */
+pd_status pd_contact_sets(const pd_sim* sim, uint8_t* out);
+
 const char* pd_last_error(const pd_sim* sim);
 void pd_destroy(pd_sim* sim);
 

@@ -76,6 +76,7 @@ class Simulator:
         if st != 0:
             raise PDError(st, self.lib.pd_last_error(None).decode())
         self.handle = h_
+        self.n_contact = len(cand)
         self.max_batch, self.max_steps = max_batch, max_steps
         self.h = h
 
@@ -141,6 +142,12 @@ class Simulator:
         out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
         out["n_nonconverged"] = st.n_nonconverged
         return out
+
+    def contact_sets(self):
+        """Final Alg. 1 active set per (sim, step) of the last forward: bool [B, T, n_contact]."""
+        out = np.zeros((self._B, self._T, self.n_contact), np.uint8)
+        self._check(self.lib.pd_contact_sets(self.handle, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out.astype(bool)
 
     def eval_objective(self, x, y, youngs=None, act=None, grad=None, g=None):
         self._check(self.lib.pd_eval_objective(self.handle, x.shape[0], _ptr(x), _ptr(y), _ptr(youngs), _ptr(act),

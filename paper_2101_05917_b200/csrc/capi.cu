@@ -54,6 +54,16 @@ struct pd_sim {
   int32_t *active, *nactive, *it_buf, *flag_buf;
   double* res_buf;
   int32_t* h_nactive = nullptr;  // pinned
+  // contact K5
+  int nc = 0, csup_first = 0;
+  bool pins_live = false;          // the solve applies the constrained root block
+  int32_t *d_cand_node = nullptr, *d_cand_of_node = nullptr, *d_cand_of_loc = nullptr;
+  double *d_S = nullptr, *LAM = nullptr, *Qc = nullptr, *PIc = nullptr, *Cb = nullptr, *Mb = nullptr, *Rb = nullptr,
+         *Rsave = nullptr;
+  uint8_t *PIN = nullptr, *NEWPIN = nullptr, *traj_pin = nullptr;
+  int32_t *flist = nullptr, *fpos = nullptr, *kcount = nullptr, *need = nullptr, *oact = nullptr, *onext = nullptr,
+          *changed = nullptr, *it_base = nullptr;
+  int32_t* h_small = nullptr;      // pinned [2*Bmax]
   double* traj = nullptr;
   int32_t *st_iters_f, *st_iters_a, *st_flag_f, *st_flag_a, *st_outer;
   double *st_res_f, *st_res_a;
@@ -90,6 +100,7 @@ struct pd_sim {
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& b : bufs) cudaFree(b.p);
     if (h_nactive) cudaFreeHost(h_nactive);
+    if (h_small) cudaFreeHost(h_small);
   }
 };
 
@@ -183,7 +194,7 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
 
 // x = A^{-1} rhs in solve layout: S0 = rhs (consumed as the working z), S2 = y, S0 = x out
 template <int RC>
-void solve_rc(pd_sim* s, int B) {
+void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->pins_live)
   const HostPlan& P = s->plan;
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
@@ -196,8 +207,17 @@ void solve_rc(pd_sim* s, int B) {
   for (int lev = P.nlevels - 1; lev >= 0; --lev) {
     const int t0 = P.blvl_ptr[lev], nt = P.blvl_ptr[lev + 1] - t0;
     if (!nt) continue;
+    const bool fix = s->pins_live && lev == P.nlevels - 1;  // the root level = the candidate block
+    double* root = s->S0 + (int64_t)s->csup_first * R;
+    if (fix) CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
     k_bwd_level<RC><<<dim3(nt, gy), kNT, 0, s->stream>>>(s->sa, t0, R, s->S2, s->S0);
     LAUNCH_CHECK(s);
+    if (fix) {
+      ProfScope ps(s, 4);
+      k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist,
+                                                                     s->fpos, s->Qc, root);
+      LAUNCH_CHECK(s);
+    }
   }
 }
 void solve(pd_sim* s, int B) {
@@ -231,9 +251,11 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
     LAUNCH_CHECK(s);
   }
   ProfScope ps(s, 1);
+  const bool pin = s->pins_live;
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
                                                           s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, s->G, s->W, s->S0,
-                                                          nullptr, nullptr, nullptr);
+                                                          pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr,
+                                                          pin ? s->LAM : nullptr);
   LAUNCH_CHECK(s);
 }
 
@@ -245,9 +267,11 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
   k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
                                                                  s->EF);
   LAUNCH_CHECK(s);
+  const bool pin = s->pins_live;
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                           s->d_fixed, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, OUT,
-                                                          nullptr, nullptr, nullptr, nullptr, nullptr);
+                                                          nullptr, nullptr, pin ? s->d_cand_of_node : nullptr,
+                                                          pin ? s->PIN : nullptr, nullptr);
   LAUNCH_CHECK(s);
 }
 
@@ -271,6 +295,49 @@ int read_nactive(pd_sim* s) {
   return *s->h_nactive;
 }
 
+// zero Dirichlet nodes and (when pins are live) the pinned z DoFs of a state vector
+void zero_constrained(pd_sim* s, double* Y, int B) {
+  const bool pin = s->pins_live;
+  k_zero_constrained<<<nblk((int64_t)3 * s->plan.n * B), 256, 0, s->stream>>>(
+      Y, s->d_fixed, s->plan.n, B, pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr);
+  LAUNCH_CHECK(s);
+}
+
+// Q_b = (S_ff)^{-1} for the current PIN of the sims in sel (device [B] or null = all): free list,
+// gather, blocked Gauss-Jordan.  One host sync (kcount) per call.
+void build_Q(pd_sim* s, int B, const int32_t* sel) {
+  ProfScope ps(s, 4);
+  const int c = s->nc;
+  k_contact_flist<<<B, 1024, 0, s->stream>>>(s->PIN, s->d_cand_of_loc, c, B, sel, s->flist, s->fpos, s->kcount);
+  LAUNCH_CHECK(s);
+  std::vector<int32_t> selh(B, 1);
+  if (sel) CK(cudaMemcpyAsync(s->h_small + B, sel, B * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaMemcpyAsync(s->h_small, s->kcount, B * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  int kmax = 0;
+  for (int b = 0; b < B; ++b) {
+    const int k = s->h_small[b];
+    const bool want = (!sel || s->h_small[B + b]) && k > 0 && k < c;
+    selh[b] = want ? 1 : 0;
+    if (want) kmax = std::max(kmax, k);
+  }
+  if (kmax == 0) return;
+  CK(cudaMemcpyAsync(s->need, selh.data(), B * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
+  const int nt = (kmax + 31) / 32;
+  k_contact_gather_S<<<dim3(nt, (kmax + 7) / 8, B), dim3(32, 8), 0, s->stream>>>(s->d_S, c, s->need, s->flist,
+                                                                                 s->kcount, s->Qc);
+  LAUNCH_CHECK(s);
+  for (int kb = 0; kb < nt; ++kb) {
+    k_gj_pivot<<<B, 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc);
+    LAUNCH_CHECK(s);
+    k_gj_panel<<<dim3((kmax + 63) / 64, B), 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Cb,
+                                                                 s->Mb, s->Rb);
+    LAUNCH_CHECK(s);
+    k_gj_update<<<dim3(nt, nt, B), 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Mb, s->Rb);
+    LAUNCH_CHECK(s);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -290,7 +357,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
   if (n_fixed < 0 || (n_fixed > 0 && !fixed_dofs)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "bad fixed DoF list");
   if (opts->max_batch < 1 || opts->max_batch > 256) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "max_batch must be in [1, 256]");
   if (opts->max_steps < 1) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "max_steps must be >= 1");
-  if (opts->n_contact != 0) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "contact is not enabled in this build yet");
+  if (opts->n_contact < 0 || (opts->n_contact > 0 && !opts->contact_nodes))
+    return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "bad contact candidate list");
   std::unique_ptr<pd_sim> s(new pd_sim());
   try {
     s->youngs = mat->youngs;
@@ -304,6 +372,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     if (s->opt.max_iter_fwd < 1) s->opt.max_iter_fwd = 10000;
     if (s->opt.max_iter_adj < 1) s->opt.max_iter_adj = 10000;
     if (s->opt.max_outer < 1) s->opt.max_outer = 10;
+    if (!(s->opt.eps_phi > 0)) s->opt.eps_phi = 1e-6 * mesh->dx;
     s->Bmax = opts->max_batch;
     s->Tmax = opts->max_steps;
     double fiber[3] = {mat->fiber[0], mat->fiber[1], mat->fiber[2]};
@@ -316,7 +385,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     const double w_ref = yref / (1.0 + mat->poisson);
     bool numerical = false;
     std::string e = build_plan(s->plan, mesh->n_nodes, mesh->n_elems, mesh->rest_xyz, mesh->hex8, mesh->dx,
-                               mat->density, h, fixed_dofs, n_fixed, w_ref, mat->muscle_w, fiber, &numerical);
+                               mat->density, h, fixed_dofs, n_fixed, w_ref, mat->muscle_w, fiber, opts->contact_nodes,
+                               opts->n_contact, &numerical);
     if (!e.empty()) return fail(nullptr, numerical ? PD_ERR_NUMERICAL : PD_ERR_INVALID_ARGUMENT, e);
     const HostPlan& P = s->plan;
     std::memcpy(s->st.dN, P.dN, sizeof(P.dN));
@@ -384,6 +454,31 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->traj = s->alloc<double>((int64_t)(s->Tmax + 1) * n3B);
     s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
     CK(cudaMallocHost(&s->h_nactive, sizeof(int32_t)));
+    CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
+    if (P.nc > 0) {
+      const int c = P.nc;
+      const int64_t cB = (int64_t)c * s->Bmax;
+      s->nc = c;
+      s->csup_first = P.sfirst[P.csup];
+      s->d_cand_node = s->upload(P.cand_node);
+      s->d_cand_of_node = s->upload(P.cand_of_node);
+      s->d_cand_of_loc = s->upload(P.cand_of_loc);
+      s->d_S = s->upload(P.Scc);
+      s->LAM = s->alloc<double>(cB);
+      s->PIN = s->alloc<uint8_t>(cB);
+      s->NEWPIN = s->alloc<uint8_t>(cB);
+      s->traj_pin = s->alloc<uint8_t>(cB * s->Tmax);
+      s->flist = s->alloc<int32_t>(cB);
+      s->fpos = s->alloc<int32_t>(cB);
+      s->Qc = s->alloc<double>(cB * c);
+      s->PIc = s->alloc<double>((int64_t)s->Bmax * 32 * 32);
+      s->Cb = s->alloc<double>(cB * 32);
+      s->Mb = s->alloc<double>(cB * 32);
+      s->Rb = s->alloc<double>(cB * 32);
+      s->Rsave = s->alloc<double>((int64_t)c * 3 * s->Bmax);
+      int32_t** small_i[] = {&s->kcount, &s->need, &s->oact, &s->onext, &s->changed, &s->it_base};
+      for (int32_t** p : small_i) *p = s->alloc<int32_t>(s->Bmax);
+    }
     CK(cudaDeviceSynchronize());
   } catch (CudaError& e) {
     return fail(nullptr, PD_ERR_CUDA, e.what());
@@ -400,6 +495,18 @@ pd_status pd_profile(const pd_sim* s, double* ms, int64_t* count, int32_t n) {
     if (ms) ms[k] = s->prof_ms[k];
     if (count) count[k] = s->prof_cnt[k];
   }
+  return PD_OK;
+}
+
+pd_status pd_contact_sets(const pd_sim* s, uint8_t* out) {
+  if (!s || !out) return PD_ERR_INVALID_ARGUMENT;
+  if (!s->have_traj || s->nc == 0) return PD_ERR_STATE;
+  const int B = s->B, T = s->T, c = s->nc;
+  std::vector<uint8_t> h((int64_t)T * c * B);  // device layout [step][j][b]
+  if (cudaMemcpy(h.data(), s->traj_pin, h.size(), cudaMemcpyDeviceToHost) != cudaSuccess) return PD_ERR_CUDA;
+  for (int b = 0; b < B; ++b)
+    for (int i = 0; i < T; ++i)
+      for (int j = 0; j < c; ++j) out[((int64_t)b * T + i) * c + j] = h[((int64_t)i * c + j) * B + b];
   return PD_OK;
 }
 
@@ -423,6 +530,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   if (s->w_m != 0.0 && !actuation) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs an actuation array");
   s->stream = (cudaStream_t)cuda_stream;
   s->launches = 0;
+  s->pins_live = false;
   for (int k = 0; k < 6; ++k) { s->prof_ms[k] = 0; s->prof_cnt[k] = 0; }
   s->ev_open.clear();
   s->ev_next = 0;
@@ -453,25 +561,71 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
                                             s->gravity[0], s->gravity[1], s->gravity[2]);
       LAUNCH_CHECK(s);
       CK(cudaMemcpyAsync(s->Xp, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
-      k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
-      LAUNCH_CHECK(s);
-      for (int iter = 0;; ++iter) {
-        residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
-        dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
-        CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-        k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter, s->opt.max_iter_fwd,
-                                                       s->active, s->st_iters_f + (int64_t)i * B,
-                                                       s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
-                                                       s->nactive);
+      const bool contact = s->nc > 0;
+      const int64_t cB = (int64_t)s->nc * B;
+      if (contact) {  // Alg. 1: V_i = empty
+        CK(cudaMemsetAsync(s->PIN, 0, cB, s->stream));
+        k_fill_int<<<1, 256, 0, s->stream>>>(s->oact, 1, B);
         LAUNCH_CHECK(s);
-        if (s->opt.fixed_iter > 0) {
-          if (iter >= s->opt.fixed_iter) break;
-        } else if (iter >= s->opt.max_iter_fwd) {
-          break;
-        } else if (iter % s->opt.check_every == 0) {
-          if (read_nactive(s) == 0) break;
+        k_fill_int<<<1, 256, 0, s->stream>>>(s->kcount, s->nc, B);  // no pins: unconstrained root block
+        LAUNCH_CHECK(s);
+        CK(cudaMemsetAsync(s->it_base, 0, B * sizeof(int32_t), s->stream));
+        s->pins_live = true;
+      }
+      for (int outer = 1; outer <= (contact ? s->opt.max_outer : 1); ++outer) {
+        if (contact) {
+          k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact);
+          LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
+          if (outer > 1) build_Q(s, B, s->oact);
+          CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
+        } else {
+          k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
+          LAUNCH_CHECK(s);
         }
-        apply_Ainv(s, B, s->G, s->X, nullptr, -1.0, 1.0, s->active);
+        for (int iter = 0;; ++iter) {
+          residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
+          dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+          CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+          k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter, s->opt.max_iter_fwd,
+                                                         s->active, s->st_iters_f + (int64_t)i * B,
+                                                         s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
+                                                         s->nactive, contact ? s->it_base : nullptr);
+          LAUNCH_CHECK(s);
+          if (s->opt.fixed_iter > 0) {
+            if (iter >= s->opt.fixed_iter) break;
+          } else if (iter >= s->opt.max_iter_fwd) {
+            break;
+          } else if (iter % s->opt.check_every == 0) {
+            if (read_nactive(s) == 0) break;
+          }
+          apply_Ainv(s, B, s->G, s->X, nullptr, -1.0, 1.0, s->active);
+        }
+        if (!contact) break;
+        // predictor on the converged x; stop when the set is unchanged
+        CK(cudaMemcpyAsync(s->it_base, s->st_iters_f + (int64_t)i * B, B * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                           s->stream));
+        CK(cudaMemsetAsync(s->changed, 0, B * sizeof(int32_t), s->stream));
+        {
+          ProfScope ps(s, 4);
+          k_contact_predict<<<nblk(cB), 256, 0, s->stream>>>(s->X, s->LAM, s->d_cand_node, s->nc, B, s->opt.eps_phi,
+                                                             s->PIN, s->oact, s->NEWPIN, s->changed);
+          LAUNCH_CHECK(s);
+          k_contact_outer<<<nblk(cB), 256, 0, s->stream>>>(s->oact, s->changed, s->NEWPIN, s->PIN, s->nc, B, outer,
+                                                           s->opt.max_outer, s->onext, s->st_outer + (int64_t)i * B,
+                                                           s->st_flag_f + (int64_t)i * B);
+          LAUNCH_CHECK(s);
+        }
+        CK(cudaMemcpyAsync(s->oact, s->onext, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
+        CK(cudaMemcpyAsync(s->h_small, s->onext, B * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        prof_flush(s);
+        int going = 0;
+        for (int b = 0; b < B; ++b) going += s->h_small[b];
+        if (!going) break;
+      }
+      if (contact) {
+        CK(cudaMemcpyAsync(s->traj_pin + (int64_t)i * cB, s->PIN, cB, cudaMemcpyDeviceToDevice, s->stream));
+        s->pins_live = false;
       }
       k_velocity<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, s->V, len, 1.0 / s->h);
       LAUNCH_CHECK(s);
@@ -498,8 +652,9 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
     prof_flush(s);
     if (stats) {
       const int64_t TB = (int64_t)steps * B;
-      std::vector<int32_t> it(TB), fl(TB);
+      std::vector<int32_t> it(TB), fl(TB), ou(TB);
       std::vector<double> rs(TB);
+      CK(cudaMemcpy(ou.data(), s->st_outer, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(it.data(), s->st_iters_f, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(fl.data(), s->st_flag_f, TB * sizeof(int32_t), cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(rs.data(), s->st_res_f, TB * sizeof(double), cudaMemcpyDeviceToHost));
@@ -508,12 +663,13 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
         for (int i = 0; i < steps; ++i) {  // device buffers are [step][b]; ABI stats are [b][step]
           if (stats->iters_fwd) stats->iters_fwd[b * steps + i] = it[(int64_t)i * B + b];
           if (stats->final_res_fwd) stats->final_res_fwd[b * steps + i] = rs[(int64_t)i * B + b];
-          if (stats->contact_outer) stats->contact_outer[b * steps + i] = 0;
+          if (stats->contact_outer) stats->contact_outer[b * steps + i] = s->nc > 0 ? ou[(int64_t)i * B + b] : 0;
           nnc += fl[(int64_t)i * B + b];
         }
       stats->n_nonconverged = nnc;
     }
   } catch (CudaError& e) {
+    s->pins_live = false;
     return fail(s, PD_ERR_CUDA, e.what());
   }
   s->have_traj = true;
@@ -529,6 +685,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
   if (!s->have_traj) return fail(s, PD_ERR_STATE, "pd_backward needs a preceding pd_forward");
   s->stream = (cudaStream_t)cuda_stream;
   s->launches = 0;
+  s->pins_live = false;
   const HostPlan& P = s->plan;
   const int B = s->B, T = s->T;
   const int n3 = 3 * P.n;
@@ -555,10 +712,15 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
       const int64_t act_bs = (int64_t)T * P.m;
       // b = a_x + a_v / h on unconstrained DoFs
+      if (s->nc > 0) {  // the step's final active set, frozen ("the same modified matrix")
+        CK(cudaMemcpyAsync(s->PIN, s->traj_pin + (int64_t)i * s->nc * B, (int64_t)s->nc * B, cudaMemcpyDeviceToDevice,
+                           s->stream));
+        s->pins_live = true;
+        build_Q(s, B, nullptr);
+      }
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
       LAUNCH_CHECK(s);
-      k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->d_fixed, P.n, B, nullptr, nullptr);
-      LAUNCH_CHECK(s);
+      zero_constrained(s, s->Bv, B);
       dots(s, B, n3, {{s->Bv, s->Bv}}, s->bb);
       CK(cudaMemsetAsync(s->U, 0, len * sizeof(double), s->stream));
       CK(cudaMemcpyAsync(s->Rv, s->Bv, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
@@ -581,8 +743,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
         if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
         if (pcg) {
           apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs);
-          k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->d_fixed, P.n, B, nullptr, nullptr);
-          LAUNCH_CHECK(s);
+          zero_constrained(s, s->Q, B);
           dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
           k_pcg_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->rz, s->dots + B, s->alpha, s->active, B);
           LAUNCH_CHECK(s);
@@ -600,8 +761,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
           // fixed point u <- u + A^{-1}(b - A_N u) == A^{-1}(b + dA u)  (eq:bp_update)
           apply_Ainv(s, B, s->Rv, s->U, nullptr, 1.0, 1.0, s->active);
           apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs);
-          k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->d_fixed, P.n, B, nullptr, nullptr);
-          LAUNCH_CHECK(s);
+          zero_constrained(s, s->Q, B);
           k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
           LAUNCH_CHECK(s);
         }
@@ -622,6 +782,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       LAUNCH_CHECK(s);
       k_adj_state<<<nblk(len), 256, 0, s->stream>>>(s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
       LAUNCH_CHECK(s);
+      s->pins_live = false;
     }
     if (dL_dq0) {
       k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dL_dq0, n3, B, n3);
@@ -668,6 +829,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       stats->n_nonconverged = nnc;
     }
   } catch (CudaError& e) {
+    s->pins_live = false;
     return fail(s, PD_ERR_CUDA, e.what());
   }
   return PD_OK;

@@ -710,6 +710,268 @@ __global__ void __launch_bounds__(kNT) k_bwd_level(SolveArgs sa, int task0, int 
   }
 }
 
+// ----------------------------------------------------------------- K5: contact
+// The candidate nodes V are ordered last: their rows form the root supernode, whose assembled
+// front is the Schur complement S = S_CC of A_s onto V.  For the z-column of sim b with pinned
+// set a_b (x_a = xbar = 0, P:380-383 eq:dirichlet/eq:complement, reading §2.9-2.10) the root
+// block of the constrained solve is x_f = (S_ff)^{-1} r_f, x_a = 0, where r = z[J_root] after
+// the forward sweep; every other level is unchanged.  Q_b = (S_ff)^{-1} is rebuilt (gather +
+// blocked Gauss-Jordan) only when the active set changes.
+constexpr int kGJ = 32;  // Gauss-Jordan pivot block
+
+// flist[b][0..k) = root-local indices of UNPINNED candidates (ascending), fpos[b][loc] = index or -1,
+// kcount[b] = k.  One CTA per selected sim; deterministic block scan.
+__global__ void __launch_bounds__(1024) k_contact_flist(const uint8_t* __restrict__ PIN, const int32_t* __restrict__ cand_of_loc,
+                                                        int c, int B, const int32_t* __restrict__ sel,
+                                                        int32_t* __restrict__ flist, int32_t* __restrict__ fpos,
+                                                        int32_t* __restrict__ kcount) {
+  const int b = blockIdx.x;
+  if (sel && !sel[b]) return;
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int l0 = 0; l0 < c; l0 += blockDim.x) {
+    const int loc = l0 + threadIdx.x;
+    const int fr = (loc < c && !PIN[(int64_t)cand_of_loc[loc] * B + b]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, fr);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int off = base;
+    for (int w = 0; w < wid; ++w) off += warp_tot[w];
+    if (loc < c) {
+      const int idx = off + pre;
+      fpos[(int64_t)b * c + loc] = fr ? idx : -1;
+      if (fr) flist[(int64_t)b * c + idx] = loc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) kcount[b] = base;
+}
+
+// Q_b[i][j] = S[flist_i][flist_j]   (leading dimension c)
+__global__ void k_contact_gather_S(const double* __restrict__ S, int c, const int32_t* __restrict__ sel,
+                                   const int32_t* __restrict__ flist, const int32_t* __restrict__ kcount,
+                                   double* __restrict__ Q) {
+  const int b = blockIdx.z;
+  if (sel && !sel[b]) return;
+  const int k = kcount[b];
+  const int i = blockIdx.y * 8 + threadIdx.y, j = blockIdx.x * 32 + threadIdx.x;
+  if (i >= k || j >= k) return;
+  const int32_t* fl = flist + (int64_t)b * c;
+  Q[((int64_t)b * c + i) * c + j] = S[(int64_t)fl[i] * c + fl[j]];
+}
+
+// Block Gauss-Jordan step kb, part 1: Pinv = (Q_KK)^{-1} (SPD, in shared memory, no pivoting),
+// C = Q[:, K] copied to Cb (k x kGJ), M = C Pinv into Mb, Rw = Q[K, :] copied to Rb (kGJ x k).
+__global__ void __launch_bounds__(256) k_gj_pivot(double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
+                                                  const int32_t* __restrict__ kcount, double* __restrict__ PI) {
+  const int b = blockIdx.x;
+  if (sel && !sel[b]) return;
+  const int k = kcount[b];
+  const int k0 = kb * kGJ;
+  if (k0 >= k) return;
+  const int nbk = min(kGJ, k - k0);
+  __shared__ double P[kGJ][kGJ + 1];
+  const double* Qb = Q + (int64_t)b * c * c;
+  for (int idx = threadIdx.x; idx < kGJ * kGJ; idx += blockDim.x) {
+    const int i = idx / kGJ, j = idx % kGJ;
+    P[i][j] = (i < nbk && j < nbk) ? Qb[(int64_t)(k0 + i) * c + k0 + j] : (i == j ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  // in-place Gauss-Jordan inversion of the kGJ x kGJ block (padding = identity)
+  for (int p = 0; p < kGJ; ++p) {
+    const double piv = P[p][p];
+    double rowp = 0, colp = 0;
+    const int i = threadIdx.x / kGJ, j = threadIdx.x % kGJ;  // 256 threads: 8 rows per pass
+    __syncthreads();
+    // snapshot of row p and column p
+    __shared__ double rp[kGJ], cp[kGJ];
+    if (threadIdx.x < kGJ) { rp[threadIdx.x] = P[p][threadIdx.x]; cp[threadIdx.x] = P[threadIdx.x][p]; }
+    __syncthreads();
+    const double ipiv = 1.0 / piv;
+    for (int ii = i; ii < kGJ; ii += blockDim.x / kGJ) {
+      double v;
+      if (ii == p && j == p) v = ipiv;
+      else if (ii == p) v = rp[j] * ipiv;
+      else if (j == p) v = -cp[ii] * ipiv;
+      else v = P[ii][j] - cp[ii] * rp[j] * ipiv;
+      P[ii][j] = v;
+    }
+    (void)rowp; (void)colp;
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < kGJ * kGJ; idx += blockDim.x)
+    PI[(int64_t)b * kGJ * kGJ + idx] = P[idx / kGJ][idx % kGJ];
+}
+
+// part 2 (grid: row tiles x sims): Cb[i][t] = Q[i][k0+t], Mb[i][:] = Cb[i] Pinv, Rb[t][i] = Q[k0+t][i]
+__global__ void __launch_bounds__(256) k_gj_panel(const double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
+                                                  const int32_t* __restrict__ kcount, const double* __restrict__ PI,
+                                                  double* __restrict__ Cb, double* __restrict__ Mb, double* __restrict__ Rb) {
+  const int b = blockIdx.y;
+  if (sel && !sel[b]) return;
+  const int k = kcount[b];
+  const int k0 = kb * kGJ;
+  if (k0 >= k) return;
+  const int nbk = min(kGJ, k - k0);
+  __shared__ double Pi[kGJ][kGJ + 1];
+  __shared__ double Ct[8][kGJ];
+  for (int idx = threadIdx.x; idx < kGJ * kGJ; idx += blockDim.x) Pi[idx / kGJ][idx % kGJ] = PI[(int64_t)b * kGJ * kGJ + idx];
+  const double* Qb = Q + (int64_t)b * c * c;
+  const int t = threadIdx.x % kGJ, r = threadIdx.x / kGJ;  // 8 rows x 32 cols per pass
+  for (int i0 = blockIdx.x * 64; i0 < min(k, (int)(blockIdx.x + 1) * 64); i0 += 8) {
+    const int i = i0 + r;
+    __syncthreads();
+    const double cv = (i < k && t < nbk) ? Qb[(int64_t)i * c + k0 + t] : 0.0;
+    Ct[r][t] = cv;
+    if (i < k) {
+      Cb[((int64_t)b * c + i) * kGJ + t] = cv;
+      Rb[((int64_t)b * kGJ + t) * c + i] = t < nbk ? Qb[(int64_t)(k0 + t) * c + i] : 0.0;
+    }
+    __syncthreads();
+    if (i < k) {
+      double acc = 0;
+#pragma unroll 8
+      for (int u = 0; u < kGJ; ++u) acc = fma(Ct[r][u], Pi[u][t], acc);
+      Mb[((int64_t)b * c + i) * kGJ + t] = acc;
+    }
+  }
+}
+
+// part 3 (grid: 32x32 tiles of Q x sims):  Q_KK = Pinv, Q_KO = Pinv Rw, Q_OK = -M, Q_OO -= M Rw.
+__global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
+                                                   const int32_t* __restrict__ kcount, const double* __restrict__ PI,
+                                                   const double* __restrict__ Mb, const double* __restrict__ Rb) {
+  const int b = blockIdx.z;
+  if (sel && !sel[b]) return;
+  const int k = kcount[b];
+  const int k0 = kb * kGJ;
+  if (k0 >= k) return;
+  const int nbk = min(kGJ, k - k0);
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  if (i0 >= k || j0 >= k) return;
+  __shared__ double Ms[32][kGJ + 1];   // M rows i0.. (or Pinv rows when the tile is in the pivot rows)
+  __shared__ double Rs[kGJ][32 + 1];   // Rw columns j0..
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  const bool iK = (i0 == k0), jK = (j0 == k0);             // tiles align with pivot blocks (kGJ = 32)
+  for (int idx = threadIdx.x; idx < 32 * kGJ; idx += blockDim.x) {
+    const int a = idx / kGJ, u = idx % kGJ;
+    const int i = i0 + a, j = j0 + a;
+    Ms[a][u] = iK ? PI[(int64_t)b * kGJ * kGJ + a * kGJ + u] : (i < k ? Mb[((int64_t)b * c + i) * kGJ + u] : 0.0);
+    Rs[u][a] = j < k ? Rb[((int64_t)b * kGJ + u) * c + j] : 0.0;
+  }
+  __syncthreads();
+  double* Qb = Q + (int64_t)b * c * c;
+  for (int a = ty; a < 32; a += 8) {
+    const int i = i0 + a, j = j0 + tx;
+    if (i >= k || j >= k) continue;
+    double v;
+    if (iK && jK) {
+      v = (a < nbk && tx < nbk) ? Ms[a][tx] : 0.0;
+    } else if (iK) {        // Q_KO = Pinv Rw
+      double acc = 0;
+#pragma unroll 8
+      for (int u = 0; u < kGJ; ++u) acc = fma(Ms[a][u], Rs[u][tx], acc);
+      v = acc;
+    } else if (jK) {        // Q_OK = -M
+      v = -Ms[a][tx];
+    } else {                // Q_OO -= M Rw
+      double acc = 0;
+#pragma unroll 8
+      for (int u = 0; u < nbk; ++u) acc = fma(Ms[a][u], Rs[u][tx], acc);
+      v = Qb[(int64_t)i * c + j] - acc;
+    }
+    Qb[(int64_t)i * c + j] = v;
+  }
+}
+
+// Constrained root block of the solve for the z-columns (col = 2B + b) of sims with pins:
+// x_loc = 0 if pinned, else sum_l Q_b[fpos(loc)][l] r[flist_l].  One warp per output row,
+// lanes stride the dot product, fixed-order shuffle reduction (deterministic).
+__global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ Rsave, int c, int R, int B,
+                                                     const int32_t* __restrict__ kcount, const int32_t* __restrict__ flist,
+                                                     const int32_t* __restrict__ fpos, const double* __restrict__ Q,
+                                                     double* __restrict__ Xroot) {
+  const int b = blockIdx.y;
+  const int k = kcount[b];
+  if (k == c) return;  // no pins: the unconstrained root solve stands
+  const int lane = threadIdx.x & 31;
+  const int loc = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (loc >= c) return;
+  const int col = 2 * B + b;
+  const int fi = fpos[(int64_t)b * c + loc];
+  double acc = 0;
+  if (fi >= 0) {
+    const double* Qr = Q + ((int64_t)b * c + fi) * c;
+    const int32_t* fl = flist + (int64_t)b * c;
+    for (int l = lane; l < k; l += 32) acc = fma(Qr[l], Rsave[(int64_t)fl[l] * R + col], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  }
+  if (lane == 0) Xroot[(int64_t)loc * R + col] = acc;
+}
+
+// x^0 of an outer iteration (Alg. 1): X = Xp for outer-active sims, pinned z DoFs at the plane.
+__global__ void k_contact_restart(double* __restrict__ X, const double* __restrict__ Xp, int n, int B,
+                                  const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
+                                  const int32_t* __restrict__ oact) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  if (!oact[b]) return;
+  const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
+  const int cj = cand_of_node[node];
+  X[i] = (ax == 2 && cj >= 0 && PIN[(int64_t)cj * B + b]) ? 0.0 : Xp[i];
+}
+
+// Predictor (Alg. 1, reading §2.11): active' = (phi < -eps_phi) or (lambda > 0), phi = z
+// (plane z = 0), lambda = (A x - d)_j for pinned j (LAM, from the gather), 0 otherwise.
+__global__ void k_contact_predict(const double* __restrict__ X, const double* __restrict__ LAM,
+                                  const int32_t* __restrict__ cand_node, int c, int B, double eps_phi,
+                                  const uint8_t* __restrict__ PIN, const int32_t* __restrict__ oact,
+                                  uint8_t* __restrict__ NEWPIN, int32_t* __restrict__ changed) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)c * B) return;
+  const int j = (int)(i / B), b = (int)(i - (int64_t)j * B);
+  if (!oact[b]) return;
+  const double phi = X[(3 * (int64_t)cand_node[j] + 2) * B + b];
+  const double lam = PIN[i] ? LAM[i] : 0.0;
+  const uint8_t nw = (phi < -eps_phi || lam > 0.0) ? 1 : 0;
+  NEWPIN[i] = nw;
+  if (nw != PIN[i]) changed[b] = 1;  // integer flag, value independent of thread order
+}
+
+// Outer-loop bookkeeping: continue with the new set if it changed and the cap is not reached.
+__global__ void k_contact_outer(const int32_t* __restrict__ oact, const int32_t* __restrict__ changed,
+                                const uint8_t* __restrict__ NEWPIN, uint8_t* __restrict__ PIN, int c, int B,
+                                int outer, int max_outer, int32_t* __restrict__ onext,
+                                int32_t* __restrict__ outer_out, int32_t* __restrict__ flag_out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)c * B) return;
+  const int j = (int)(i / B), b = (int)(i - (int64_t)j * B);
+  if (!oact[b]) {
+    if (j == 0) onext[b] = 0;
+    return;
+  }
+  const bool go = changed[b] && outer < max_outer;
+  if (go) PIN[i] = NEWPIN[i];
+  if (j == 0) {
+    onext[b] = go ? 1 : 0;
+    outer_out[b] = outer;
+    if (changed[b] && !go) flag_out[b] = 1;  // hit the outer cap
+  }
+}
+
 // ----------------------------------------------------------------- per-sim reductions
 // partial[c][b] = sum over chunk c of u*v (up to 3 pairs); blockDim % B == 0 so that each
 // thread keeps one sim; fixed-order tree inside the block, fixed-order sum over chunks.
@@ -763,7 +1025,7 @@ __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* 
 __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, int iter, int fixed_iter,
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out,
-                            int32_t* __restrict__ nactive) {
+                            int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   if (!active[b]) return;
@@ -773,7 +1035,7 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
   if (fixed_iter > 0) go = iter < fixed_iter;
   else go = res > tol && iter < max_iter;
   res_out[b] = res;
-  iters_out[b] = iter;
+  iters_out[b] = iter + (iter_base ? iter_base[b] : 0);
   if (!go) {
     active[b] = 0;
     flag_out[b] = (fixed_iter == 0 && res > tol) ? 1 : 0;

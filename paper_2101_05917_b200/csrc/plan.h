@@ -50,6 +50,14 @@ struct HostPlan {
   // backward level l: column tiles [blvl_ptr[l], blvl_ptr[l+1]) of level-l supernodes:
   // x[J_s cols c0..c1) = D_s^T y[J_s] - W_s^T x[R_s].
   std::vector<int32_t> blvl_ptr, bt_sup, bt_c0, bt_c1;
+  // ---- contact candidates: ordered LAST as one root supernode ----
+  int nc = 0;                        // number of candidate nodes (0 = no contact)
+  int csup = -1;                     // index of the candidate supernode (= nsup - 1)
+  std::vector<int32_t> cand_node;    // [nc] node of candidate j (caller order)
+  std::vector<int32_t> cand_loc;     // [nc] local row of candidate j inside the root block
+  std::vector<int32_t> cand_of_loc;  // [nc] inverse of cand_loc
+  std::vector<int32_t> cand_of_node; // [n]  j or -1
+  std::vector<double> Scc;           // [nc][nc] Schur complement of A_s onto the candidates (local order)
 };
 
 // Build everything host-side.  Returns "" on success, else an error message;
@@ -57,6 +65,6 @@ struct HostPlan {
 std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
                        double dx, double density, double h, const int32_t* fixed_dofs,
                        int n_fixed, double w_ref, double w_m, const double fiber[3],
-                       bool* numerical);
+                       const int32_t* contact_nodes, int n_contact, bool* numerical);
 
 }  // namespace pdb

@@ -177,7 +177,7 @@ static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
 std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
                        double dx, double density, double h, const int32_t* fixed_dofs,
                        int n_fixed, double w_ref, double w_m, const double fiber[3],
-                       bool* numerical) {
+                       const int32_t* contact_nodes, int n_contact, bool* numerical) {
   *numerical = false;
   if (n <= 0 || m <= 0 || !rest || !hex8) return "empty mesh";
   if (!(dx > 0) || !(h > 0)) return "dx and h must be > 0";
@@ -244,10 +244,21 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
   std::vector<int32_t> lat(3 * (int64_t)n);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < 3; ++j) lat[3 * (int64_t)i + j] = (int32_t)std::llround((rest[3 * (int64_t)i + j] - mn[j]) / dx);
+  // contact candidates (P:278 the node set V): free nodes, no repeats; ordered LAST
+  P.nc = n_contact;
+  P.cand_of_node.assign(n, -1);
+  P.cand_node.assign(contact_nodes, contact_nodes + n_contact);
+  for (int j = 0; j < n_contact; ++j) {
+    const int v = contact_nodes[j];
+    if (v < 0 || v >= n) return "contact node out of range";
+    if (P.fixed_node[v]) return "a contact candidate is a Dirichlet node";
+    if (P.cand_of_node[v] >= 0) return "repeated contact candidate";
+    P.cand_of_node[v] = j;
+  }
   std::vector<int32_t> freeNodes;
   for (int i = 0; i < n; ++i)
-    if (!P.fixed_node[i]) freeNodes.push_back(i);
-  P.nfree = (int)freeNodes.size();
+    if (!P.fixed_node[i] && P.cand_of_node[i] < 0) freeNodes.push_back(i);
+  P.nfree = (int)freeNodes.size() + n_contact;
   if (P.nfree == 0) return "every node is fixed";
 
   std::vector<std::vector<int32_t>> supNodes;  // in creation (post) order
@@ -305,7 +316,15 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
     for (int k : kids) supParent[k] = s;
     return s;
   };
-  nd(freeNodes);
+  const int ndroot = freeNodes.empty() ? -1 : nd(freeNodes);
+  if (n_contact > 0) {
+    std::vector<int32_t> cs(contact_nodes, contact_nodes + n_contact);
+    std::sort(cs.begin(), cs.end(), lexless);
+    supNodes.push_back(cs);
+    supParent.push_back(-1);
+    P.csup = (int)supNodes.size() - 1;
+    if (ndroot >= 0) supParent[ndroot] = P.csup;
+  }
   P.nsup = (int)supNodes.size();
   P.sfirst.resize(P.nsup);
   P.ssize.resize(P.nsup);
@@ -322,6 +341,14 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
         P.node_of_pos[pos] = v;
         ++pos;
       }
+    }
+  }
+  if (P.nc > 0) {
+    P.cand_loc.resize(P.nc);
+    P.cand_of_loc.resize(P.nc);
+    for (int j = 0; j < P.nc; ++j) {
+      P.cand_loc[j] = P.pos_of_node[P.cand_node[j]] - P.sfirst[P.csup];
+      P.cand_of_loc[P.cand_loc[j]] = j;
     }
   }
   std::vector<int32_t> sup_of_pos(P.nfree);
@@ -441,6 +468,12 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
           for (int j = 0; j <= i; ++j) F[(int64_t)li * f + loc[Rc[j]]] += Uc[(int64_t)i * nrc + j];
         }
         std::vector<double>().swap(U[c]);
+      }
+      if (s == P.csup) {  // the assembled root front IS the Schur complement S_CC
+        P.Scc.assign((int64_t)ns * ns, 0.0);
+        for (int i = 0; i < ns; ++i)
+          for (int j = 0; j <= i; ++j)
+            P.Scc[(int64_t)i * ns + j] = P.Scc[(int64_t)j * ns + i] = F[(int64_t)i * f + j];
       }
       if (!partial_cholesky(F.data(), f, ns, inner_par)) return false;
       schur_update(F.data(), f, ns, inner_par);

@@ -21,9 +21,26 @@ int main(int argc, char** argv) {
   std::vector<int32_t> fixed;
   if (fix) for (int k = 0; k <= nz; ++k) for (int j = 0; j <= ny; ++j) for (int a = 0; a < 3; ++a) fixed.push_back(3 * nid(0, j, k) + a);
   int n = (int)rest.size() / 3, m = (int)hex.size() / 8;
+  // optional 5th arg = 1: bottom-face nodes (z = 0) are contact candidates, ordered last
+  int contact = argc > 5 ? atoi(argv[5]) : 0;
+  std::vector<int32_t> cand;
+  if (contact) for (int j = 0; j <= ny; ++j) for (int i = 0; i <= nx; ++i) if (!fix || i > 0) cand.push_back(nid(i, j, 0));
   HostPlan P; bool num; double fib[3] = {1, 0, 0};
   std::string e = build_plan(P, n, m, rest.data(), hex.data(), dx, 1e3, 0.01, fixed.data(), (int)fixed.size(),
-                             1e5 / 1.45, 1e5 / 1.45, fib, &num);
+                             1e5 / 1.45, 1e5 / 1.45, fib, cand.data(), (int)cand.size(), &num);
+  if (contact) {  // the candidate block is the last supernode and Scc = L_cc L_cc^T
+    if (P.csup != P.nsup - 1 || P.ssize[P.csup] != (int)cand.size()) { printf("bad candidate supernode\n"); return 4; }
+    const int c = P.nc; const double* D = P.D.data() + P.doff[P.csup];
+    // Scc^{-1} = D^T D: check Scc (D^T D e_k) = e_k for a few k
+    double worst = 0;
+    for (int k = 0; k < c; k += std::max(1, c / 7)) {
+      std::vector<double> t(c, 0.0), u(c, 0.0);
+      for (int i = k; i < c; ++i) t[i] = D[(int64_t)i * (i + 1) / 2 + k];
+      for (int j = 0; j < c; ++j) { double s = 0; for (int i = j; i < c; ++i) s += D[(int64_t)i * (i + 1) / 2 + j] * t[i]; u[j] = s; }
+      for (int i = 0; i < c; ++i) { double s = 0; for (int j = 0; j < c; ++j) s += P.Scc[(int64_t)i * c + j] * u[j]; worst = std::max(worst, std::fabs(s - (i == k))); }
+    }
+    if (worst > 1e-9) { printf("Scc check failed %.3e\n", worst); return 5; }
+  }
   if (!e.empty()) { printf("ERROR %s\n", e.c_str()); return 1; }
   int N = P.nfree;
   std::mt19937 rng(1); std::normal_distribution<double> nd;

@@ -203,3 +203,46 @@ def test_bitwise_determinism(torch):
     b = _run_gpu(torch, inp, sim)
     for k in ("q", "v", "dq0", "dv0", "dfext", "dE", "dnu"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ----------------------------------------------------------------- contact (K5, Alg. 1)
+def _contact_parity(torch, name, **over):
+    inp = make_inputs(get_config(name, **over))
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"])
+    gpu = _run_gpu(torch, inp, sim)
+    sets = sim.contact_sets()
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    cand = 3 * inp["contact_nodes"] + 2
+    n_active = 0
+    for b in range(inp["B"]):
+        tr, _, _, _ = oracle_run(inp, b)
+        # bit-exact contact-set selection (BASELINE.json north_star) and identical Alg. 1 outer counts
+        assert np.array_equal(sets[b], tr["active"]), ("active set", b)
+        assert list(gpu["st"]["contact_outer"][b]) == [s["outer"] for s in tr["stats"]], b
+        for i in range(inp["T"]):
+            # pinned normal DoFs sit exactly on the plane z = 0 (eq:dirichlet with xbar = 0)
+            assert np.all(gpu["q"][b, i + 1][cand[sets[b, i]]] == 0.0)
+        n_active += int(sets[b].sum())
+    assert n_active > 0, "the workload never touched the plane"
+    _compare(inp, gpu, range(inp["B"]))
+
+
+def test_c4s_contact_drop_parity(torch):
+    # BASELINE.json configs[3] recipe at oracle size: tilted plate dropped on z = 0, frictionless LCP.
+    _contact_parity(torch, "c4s")
+
+
+def test_c5s_contact_muscle_parity(torch):
+    # configs[4] recipe at oracle size: muscle actuation + bottom-face contact, B = 2.
+    _contact_parity(torch, "c5s")
+
+
+def test_contact_deterministic(torch):
+    inp = make_inputs(get_config("c4s"))
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"])
+    a = _run_gpu(torch, inp, sim)
+    sa = sim.contact_sets()
+    b = _run_gpu(torch, inp, sim)
+    assert np.array_equal(sa, sim.contact_sets())
+    for k in ("q", "v", "dq0", "dv0", "dfext", "dE", "dnu"):
+        assert np.array_equal(a[k], b[k]), k

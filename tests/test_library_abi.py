@@ -51,6 +51,7 @@ def test_native_plan_factorisation():
     subprocess.run(["g++", "-O2", "-std=c++17", "-fopenmp", "-o", exe,
                     os.path.join(ROOT, "tests", "native", "plan_check.cpp"),
                     os.path.join(ROOT, "paper_2101_05917_b200", "csrc", "setup.cpp")], check=True)
-    for args in (["4", "2", "2"], ["8", "4", "4"], ["20", "20", "4", "0"], ["24", "12", "12", "0"]):
+    for args in (["4", "2", "2"], ["8", "4", "4"], ["20", "20", "4", "0"], ["24", "12", "12", "0"],
+                 ["20", "20", "4", "0", "1"], ["6", "4", "3", "0", "1"], ["8", "4", "4", "1", "1"]):
         r = subprocess.run([exe] + args, capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
