@@ -64,6 +64,12 @@ struct pd_sim {
   int32_t *flist = nullptr, *fpos = nullptr, *kcount = nullptr, *need = nullptr, *oact = nullptr, *onext = nullptr,
           *changed = nullptr, *it_base = nullptr;
   int32_t* h_small = nullptr;      // pinned [2*Bmax]
+  // forward L-BFGS (accel_fwd = 1)
+  int nhist = 0;
+  double *LS = nullptr, *LY = nullptr, *Dv = nullptr, *Xn = nullptr, *Gn = nullptr, *rho_h = nullptr, *aj_h = nullptr;
+  double *fcur = nullptr, *fnew = nullptr, *alpha_ls = nullptr, *gtd = nullptr, *g2 = nullptr, *gn2 = nullptr,
+         *inert = nullptr, *esum = nullptr, *dtmp = nullptr;
+  int32_t *ls_act = nullptr, *ls_flag = nullptr;
   double* traj = nullptr;
   int32_t *st_iters_f, *st_iters_a, *st_flag_f, *st_flag_a, *st_outer;
   double *st_res_f, *st_res_a;
@@ -242,7 +248,7 @@ void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* 
 
 // grad g(X) into G (+ W normaliser, S0 permuted RHS), element energies in EE
 void residual(pd_sim* s, int B, const double* X, const double* Y, const double* act_step, int64_t act_bstride,
-              const uint8_t* fixed_mask) {
+              const uint8_t* fixed_mask, double* Gout = nullptr) {
   const HostPlan& P = s->plan;
   {
     ProfScope ps(s, 0);
@@ -253,7 +259,8 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   ProfScope ps(s, 1);
   const bool pin = s->pins_live;
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
-                                                          s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, s->G, s->W, s->S0,
+                                                          s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, Gout ? Gout : s->G,
+                                                          s->W, s->S0,
                                                           pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr,
                                                           pin ? s->LAM : nullptr);
   LAUNCH_CHECK(s);
@@ -295,6 +302,25 @@ int read_nactive(pd_sim* s) {
   return *s->h_nactive;
 }
 
+// objective g (eq:opt) and its gradient at X: Gout = grad g (constrained rows 0), fout[b] = g
+void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const double* act_step, int64_t act_bs) {
+  const HostPlan& P = s->plan;
+  residual(s, B, X, s->Y, act_step, act_bs, s->d_fixed, Gout);
+  const int64_t chunk = 2048;
+  const int64_t n3 = 3LL * P.n;
+  const int nchunk = (int)((n3 + chunk - 1) / chunk);
+  const int bd = B * std::max(1, 256 / B);
+  k_inertia_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B,
+                                                                    chunk, s->partial);
+  LAUNCH_CHECK(s);
+  k_dot_final<<<nblk(B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, 1, s->inert);
+  LAUNCH_CHECK(s);
+  k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->EE, P.m, B, s->esum, 0);
+  LAUNCH_CHECK(s);
+  k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
+  LAUNCH_CHECK(s);
+}
+
 // zero Dirichlet nodes and (when pins are live) the pinned z DoFs of a state vector
 void zero_constrained(pd_sim* s, double* Y, int B) {
   const bool pin = s->pins_live;
@@ -334,6 +360,83 @@ void build_Q(pd_sim* s, int B, const int32_t* sel) {
                                                                  s->Mb, s->Rb);
     LAUNCH_CHECK(s);
     k_gj_update<<<dim3(nt, nt, B), 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Mb, s->Rb);
+    LAUNCH_CHECK(s);
+  }
+}
+
+// Forward quasi-Newton PD (P:79, P:254-271 applied to eq:opt): L-BFGS on g with H0 = A^{-1} (the
+// constrained prefactorised solve) and Armijo backtracking; per-sim masks; history slots shared by index.
+void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base) {
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  const int m = s->nhist;
+  const int max_trial = 30;
+  auto LSs = [&](int k) { return s->LS + (int64_t)k * len; };
+  auto LYs = [&](int k) { return s->LY + (int64_t)k * len; };
+  CK(cudaMemcpyAsync(s->Xn, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  eval_f(s, B, s->X, s->G, s->fcur, act_i, act_bs);
+  int hist = 0;
+  for (int iter = 0;; ++iter) {
+    dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+    CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+    k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
+                                                   s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
+                                                   s->st_flag_f + (int64_t)i * B, s->nactive, it_base);
+    LAUNCH_CHECK(s);
+    if (iter >= s->opt.max_iter_fwd) break;
+    if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
+    CK(cudaMemcpyAsync(s->g2, s->dots, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    // two-loop recursion: D = -H grad g
+    CK(cudaMemcpyAsync(s->Dv, s->G, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    for (int k = 0; k < hist; ++k) {
+      const int slot = ((iter - 1 - k) % m + m) % m;
+      dots(s, B, n3, {{LSs(slot), s->Dv}}, s->dtmp);
+      k_lbfgs_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, LYs(slot), s->rho_h + (int64_t)slot * B, s->dtmp,
+                                                     s->aj_h + (int64_t)slot * B, 0, len, B, s->active);
+      LAUNCH_CHECK(s);
+    }
+    apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);
+    for (int k = hist - 1; k >= 0; --k) {
+      const int slot = ((iter - 1 - k) % m + m) % m;
+      dots(s, B, n3, {{LYs(slot), s->Dv}}, s->dtmp);
+      k_lbfgs_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, LSs(slot), s->rho_h + (int64_t)slot * B, s->dtmp,
+                                                     s->aj_h + (int64_t)slot * B, 1, len, B, s->active);
+      LAUNCH_CHECK(s);
+    }
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
+    LAUNCH_CHECK(s);
+    dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
+    // Armijo backtracking from alpha = 1
+    k_axpby<<<1, 256, 0, s->stream>>>(s->alpha_ls, nullptr, 0.0, nullptr, nullptr, 1.0, B, B, nullptr);  // alpha = 1
+    LAUNCH_CHECK(s);
+    CK(cudaMemcpyAsync(s->ls_act, s->active, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
+    for (int trial = 0;; ++trial) {
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
+      LAUNCH_CHECK(s);
+      eval_f(s, B, s->Xn, s->Gn, s->fnew, act_i, act_bs);
+      dots(s, B, n3, {{s->Gn, s->Gn}}, s->gn2);
+      CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+      k_ls_accept<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->gtd, s->g2, s->gn2, s->alpha_ls, s->ls_act,
+                                                     trial, max_trial, s->nactive, s->ls_flag, B);
+      LAUNCH_CHECK(s);
+      if (read_nactive(s) == 0) break;
+    }
+    // curvature pair (s, y) into slot iter % m; commit x, grad g, g
+    const int slot = iter % m;
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(LSs(slot), s->Xn, 1.0, s->X, nullptr, -1.0, len, B, s->active);
+    LAUNCH_CHECK(s);
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(LYs(slot), s->Gn, 1.0, s->G, nullptr, -1.0, len, B, s->active);
+    LAUNCH_CHECK(s);
+    dots(s, B, n3, {{LSs(slot), LYs(slot)}}, s->dtmp);
+    k_lbfgs_rho<<<nblk(B, 64), 64, 0, s->stream>>>(s->dtmp, s->rho_h + (int64_t)slot * B, s->active, B);
+    LAUNCH_CHECK(s);
+    hist = std::min(hist + 1, m);
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
+    LAUNCH_CHECK(s);
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->G, s->Gn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
+    LAUNCH_CHECK(s);
+    k_copy_masked<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->active, B);
     LAUNCH_CHECK(s);
   }
 }
@@ -455,6 +558,20 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
     CK(cudaMallocHost(&s->h_nactive, sizeof(int32_t)));
     CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
+    if (s->opt.accel_fwd) {
+      s->nhist = 8;
+      s->LS = s->alloc<double>(s->nhist * n3B);
+      s->LY = s->alloc<double>(s->nhist * n3B);
+      s->Dv = s->alloc<double>(n3B);
+      s->Xn = s->alloc<double>(n3B);
+      s->Gn = s->alloc<double>(n3B);
+      s->rho_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
+      s->aj_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
+      double** sc[] = {&s->fcur, &s->fnew, &s->alpha_ls, &s->gtd, &s->g2, &s->gn2, &s->inert, &s->esum, &s->dtmp};
+      for (double** p : sc) *p = s->alloc<double>(s->Bmax);
+      s->ls_act = s->alloc<int32_t>(s->Bmax);
+      s->ls_flag = s->alloc<int32_t>(s->Bmax);
+    }
     if (P.nc > 0) {
       const int c = P.nc;
       const int64_t cB = (int64_t)c * s->Bmax;
@@ -582,23 +699,27 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
           LAUNCH_CHECK(s);
         }
-        for (int iter = 0;; ++iter) {
-          residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
-          dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
-          CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-          k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter, s->opt.max_iter_fwd,
-                                                         s->active, s->st_iters_f + (int64_t)i * B,
-                                                         s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
-                                                         s->nactive, contact ? s->it_base : nullptr);
-          LAUNCH_CHECK(s);
-          if (s->opt.fixed_iter > 0) {
-            if (iter >= s->opt.fixed_iter) break;
-          } else if (iter >= s->opt.max_iter_fwd) {
-            break;
-          } else if (iter % s->opt.check_every == 0) {
-            if (read_nactive(s) == 0) break;
+        if (s->opt.accel_fwd && s->opt.fixed_iter <= 0) {
+          inner_lbfgs(s, B, i, act_i, act_bs, contact ? s->it_base : nullptr);
+        } else {
+          for (int iter = 0;; ++iter) {
+            residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
+            dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+            CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
+            k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter,
+                                                           s->opt.max_iter_fwd, s->active, s->st_iters_f + (int64_t)i * B,
+                                                           s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
+                                                           s->nactive, contact ? s->it_base : nullptr);
+            LAUNCH_CHECK(s);
+            if (s->opt.fixed_iter > 0) {
+              if (iter >= s->opt.fixed_iter) break;
+            } else if (iter >= s->opt.max_iter_fwd) {
+              break;
+            } else if (iter % s->opt.check_every == 0) {
+              if (read_nactive(s) == 0) break;
+            }
+            apply_Ainv(s, B, s->G, s->X, nullptr, -1.0, 1.0, s->active);  // x <- A^{-1} d(x)  (eq:pd_global)
           }
-          apply_Ainv(s, B, s->G, s->X, nullptr, -1.0, 1.0, s->active);
         }
         if (!contact) break;
         // predictor on the converged x; stop when the set is unchanged

@@ -1020,6 +1020,95 @@ __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* 
   if (threadIdx.x == 0) out[b] = accumulate ? out[b] + red[0] : red[0];
 }
 
+// ----------------------------------------------------------------- forward quasi-Newton (L-BFGS, H0 = A^{-1})
+// The quasi-Newton PD of P:79/P:254 (Liu et al.): minimise g (eq:opt) with L-BFGS whose initial inverse
+// Hessian is the prefactorised A^{-1}; Armijo backtracking on g.  Same minimiser as plain PD.
+
+// partial[c][b] = sum over chunk c of (m_node/h^2) (X - Y)^2   (fixed-order, like k_dot_partial)
+__global__ void k_inertia_partial(const double* __restrict__ X, const double* __restrict__ Y,
+                                  const double* __restrict__ mass, double inv_h2, int64_t len, int B, int64_t chunk,
+                                  double* __restrict__ partial) {
+  extern __shared__ double red[];
+  const int nb = blockDim.x;
+  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
+  double acc = 0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
+    const double d = X[i] - Y[i];
+    acc += mass[i / B / 3] * inv_h2 * d * d;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  const int J = nb / B;
+  for (int step = 1; step < J; step <<= 1) {
+    const int j = threadIdx.x / B;
+    if ((j % (2 * step)) == 0 && j + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
+    __syncthreads();
+  }
+  if (threadIdx.x < B) partial[(int64_t)blockIdx.x * B + threadIdx.x] = red[threadIdx.x];
+}
+
+// f[b] = 0.5 * inert[b] + esum[b]
+__global__ void k_obj_combine(const double* __restrict__ inert, const double* __restrict__ esum, double* __restrict__ f,
+                              int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) f[b] = 0.5 * inert[b] + esum[b];
+}
+
+// two-loop recursion steps, per sim coefficient from a dot product:
+//   mode 0: a = rho*dot; aj[b] = a; Y -= a V          (newest -> oldest)
+//   mode 1: beta = rho*dot; Y += (aj - beta) V        (oldest -> newest)
+__global__ void k_lbfgs_axpy(double* __restrict__ Y, const double* __restrict__ V, const double* __restrict__ rho,
+                             const double* __restrict__ dot, double* __restrict__ aj, int mode, int64_t len, int B,
+                             const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (active && !active[b]) return;
+  const double t = rho[b] * dot[b];
+  if (mode == 0) {
+    if (i < B) aj[b] = t;
+    Y[i] -= t * V[i];
+  } else {
+    Y[i] += (aj[b] - t) * V[i];
+  }
+}
+
+// Armijo backtracking decision per sim.  Near the minimiser g no longer resolves the decrease in fp64;
+// there a step that leaves g unchanged to 1e-13 relative and lowers ||grad g|| is accepted (the oracle's
+// Newton uses the same rule).  After max_trial halvings the step is taken anyway and flagged.
+__global__ void k_ls_accept(const double* __restrict__ f, const double* __restrict__ fn, const double* __restrict__ gtd,
+                            const double* __restrict__ g2, const double* __restrict__ gn2, double* __restrict__ alpha,
+                            int32_t* __restrict__ ls_active, int trial, int max_trial, int32_t* __restrict__ nactive,
+                            int32_t* __restrict__ ls_flag, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !ls_active[b]) return;
+  const double a = alpha[b];
+  const bool armijo = fn[b] <= f[b] + 1e-4 * a * gtd[b];
+  const bool flat = fabs(fn[b] - f[b]) <= 1e-13 * fabs(f[b]) && gn2[b] < g2[b];
+  if (armijo || flat || trial >= max_trial) {
+    ls_active[b] = 0;
+    if (!(armijo || flat)) ls_flag[b] = 1;
+  } else {
+    alpha[b] = 0.5 * a;
+    atomicAdd(nactive, 1);
+  }
+}
+
+// rho = 1/(s^T y) if the curvature pair is positive, else 0 (pair ignored)
+__global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ rho, const int32_t* __restrict__ active,
+                            int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  rho[b] = sy[b] > 0.0 ? 1.0 / sy[b] : 0.0;
+}
+
+// masked copy of per-sim scalars
+__global__ void k_copy_masked(double* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ active,
+                              int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && (!active || active[b])) dst[b] = src[b];
+}
+
 // ----------------------------------------------------------------- iteration control
 // Forward convergence: res = sqrt(res2/den2); active[b] for the NEXT update.
 __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, int iter, int fixed_iter,

@@ -172,18 +172,20 @@ def test_c1_fixed_iterations_parity(torch):
     _compare(inp, gpu, [0])
 
 
-@pytest.mark.parametrize("accel_adj", [1, 0])
-def test_c2s_converged_parity(torch, accel_adj):
+@pytest.mark.parametrize("accel_fwd,accel_adj", [(0, 1), (0, 0), (1, 1)])
+def test_c2s_converged_parity(torch, accel_fwd, accel_adj):
+    # plain PD / quasi-Newton forward; PD fixed point (eq:bp_update) / accelerated adjoint
     inp = make_inputs(get_config("c2s"))
-    gpu = _run_gpu(torch, inp, _sim(inp, accel_adj=accel_adj))
+    gpu = _run_gpu(torch, inp, _sim(inp, accel_fwd=accel_fwd, accel_adj=accel_adj))
     assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
     _compare(inp, gpu, [0])
 
 
-def test_c3s_batched_shared_factor_parity(torch):
+@pytest.mark.parametrize("accel_fwd", [0, 1])
+def test_c3s_batched_shared_factor_parity(torch, accel_fwd):
     # Per-sim E with ONE factor of A_ref; the oracle uses each sim's exact A_s.
     inp = make_inputs(get_config("c3s"))
-    gpu = _run_gpu(torch, inp, _sim(inp))
+    gpu = _run_gpu(torch, inp, _sim(inp, accel_fwd=accel_fwd))
     assert gpu["st"]["n_nonconverged"] == 0
     _compare(inp, gpu, range(inp["B"]))
 
@@ -206,9 +208,9 @@ def test_bitwise_determinism(torch):
 
 
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
-def _contact_parity(torch, name, **over):
+def _contact_parity(torch, name, accel_fwd=0, **over):
     inp = make_inputs(get_config(name, **over))
-    sim = _sim(inp, contact_nodes=inp["contact_nodes"])
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd)
     gpu = _run_gpu(torch, inp, sim)
     sets = sim.contact_sets()
     assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
@@ -227,14 +229,16 @@ def _contact_parity(torch, name, **over):
     _compare(inp, gpu, range(inp["B"]))
 
 
-def test_c4s_contact_drop_parity(torch):
+@pytest.mark.parametrize("accel_fwd", [0, 1])
+def test_c4s_contact_drop_parity(torch, accel_fwd):
     # BASELINE.json configs[3] recipe at oracle size: tilted plate dropped on z = 0, frictionless LCP.
-    _contact_parity(torch, "c4s")
+    _contact_parity(torch, "c4s", accel_fwd)
 
 
-def test_c5s_contact_muscle_parity(torch):
+@pytest.mark.parametrize("accel_fwd", [0, 1])
+def test_c5s_contact_muscle_parity(torch, accel_fwd):
     # configs[4] recipe at oracle size: muscle actuation + bottom-face contact, B = 2.
-    _contact_parity(torch, "c5s")
+    _contact_parity(torch, "c5s", accel_fwd)
 
 
 def test_contact_deterministic(torch):
