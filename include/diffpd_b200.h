@@ -86,6 +86,9 @@ typedef struct {
   int32_t max_outer;      /* Alg. 1 "maximum iteration" (default 10)                     */
   double eps_phi;         /* predictor penetration threshold (m), default 1e-6 dx          */
   int32_t profile;        /* 1: bracket each kernel family with CUDA events (pd_profile)   */
+  int32_t outer_warm;     /* 1: outer iterations k > 1 of Alg. 1 start from iteration k-1's x
+                             (pinned DoFs moved to the plane) instead of x_i; the converged x
+                             of each corrector solve is the same            */
 } pd_options;
 
 /* Per-step statistics, caller-owned HOST arrays of length B*steps (index

@@ -408,7 +408,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     LAUNCH_CHECK(s);
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
     // Armijo backtracking from alpha = 1
-    k_axpby<<<1, 256, 0, s->stream>>>(s->alpha_ls, nullptr, 0.0, nullptr, nullptr, 1.0, B, B, nullptr);  // alpha = 1
+    k_fill_double<<<nblk(B, 64), 64, 0, s->stream>>>(s->alpha_ls, 1.0, B);  // alpha = 1
     LAUNCH_CHECK(s);
     CK(cudaMemcpyAsync(s->ls_act, s->active, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
     for (int trial = 0;; ++trial) {
@@ -691,7 +691,8 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       }
       for (int outer = 1; outer <= (contact ? s->opt.max_outer : 1); ++outer) {
         if (contact) {
-          k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact);
+          k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact,
+                                                              s->opt.outer_warm && outer > 1);
           LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
           if (outer > 1) build_Q(s, B, s->oact);
           CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));

@@ -921,9 +921,11 @@ __global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ 
 }
 
 // x^0 of an outer iteration (Alg. 1): X = Xp for outer-active sims, pinned z DoFs at the plane.
+// warm = 1: start from the previous outer iteration's converged x instead (the inner
+// solve's converged point does not depend on its start; only the iteration count does).
 __global__ void k_contact_restart(double* __restrict__ X, const double* __restrict__ Xp, int n, int B,
                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
-                                  const int32_t* __restrict__ oact) {
+                                  const int32_t* __restrict__ oact, int warm) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -931,7 +933,7 @@ __global__ void k_contact_restart(double* __restrict__ X, const double* __restri
   if (!oact[b]) return;
   const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
   const int cj = cand_of_node[node];
-  X[i] = (ax == 2 && cj >= 0 && PIN[(int64_t)cj * B + b]) ? 0.0 : Xp[i];
+  X[i] = (ax == 2 && cj >= 0 && PIN[(int64_t)cj * B + b]) ? 0.0 : (warm ? X[i] : Xp[i]);
 }
 
 // Predictor (Alg. 1, reading §2.11): active' = (phi < -eps_phi) or (lambda > 0), phi = z
@@ -1100,6 +1102,12 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
   rho[b] = sy[b] > 0.0 ? 1.0 / sy[b] : 0.0;
+}
+
+// v[b] = c (per-sim scalar fill)
+__global__ void k_fill_double(double* __restrict__ v, double c, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) v[b] = c;
 }
 
 // masked copy of per-sim scalars
