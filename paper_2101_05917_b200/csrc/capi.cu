@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -46,7 +47,9 @@ struct pd_sim {
   double* d_mass = nullptr;
   uint8_t* d_fixed = nullptr;
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
-  SolveArgs sa{};
+  SweepDev swf{}, swb{};
+  int32_t* d_rows = nullptr;
+  double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
   double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
   double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR;
@@ -102,7 +105,11 @@ struct pd_sim {
     if (!v.empty()) cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
     return d;
   }
+  std::map<int, std::pair<cudaGraphExec_t, int64_t>> solve_graphs;  // (B, fixup) -> graph, kernels in it
+  cudaStream_t cap_stream = nullptr;
   ~pd_sim() {
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (auto& g : solve_graphs) cudaGraphExecDestroy(g.second.first);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (auto& b : bufs) cudaFree(b.p);
     if (h_nactive) cudaFreeHost(h_nactive);
@@ -113,6 +120,9 @@ struct pd_sim {
 namespace {
 
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+// DoFs per reduction block: ~4096 (DoF, sim) elements per block whatever B is (fixed partition =
+// deterministic sums).
+inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 4096 / B); }
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -180,7 +190,7 @@ ElemArgs elem_args(pd_sim* s, int B, const double* act_step, int64_t act_bstride
 
 // per-sim dot products of state-layout vectors of length len (*B) -> s->dots[p*B + b]
 void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const double*, const double*>> pairs,
-          double* out = nullptr) {
+          double* out = nullptr, int accumulate = 0) {
   DotArgs da{};
   int p = 0;
   for (auto& pr : pairs) {
@@ -189,48 +199,86 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
     ++p;
   }
   da.npairs = p;
-  const int64_t chunk = 2048;
+  const int64_t chunk = dot_chunk(B);
   const int nchunk = (int)((len + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
   k_dot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk(p * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots);
+  k_dot_final<<<nblk(p * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
 }
 
 // x = A^{-1} rhs in solve layout: S0 = rhs (consumed as the working z), S2 = y, S0 = x out
-template <int RC>
+template <int RC, bool VEC>
 void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->pins_live)
   const HostPlan& P = s->plan;
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
-  for (int lev = 0; lev < P.nlevels; ++lev) {
-    const int t0 = P.flvl_ptr[lev], nt = P.flvl_ptr[lev + 1] - t0;
-    if (!nt) continue;
-    k_fwd_level<RC><<<dim3(nt, gy), kNT, 0, s->stream>>>(s->sa, t0, R, s->S0, s->S2);
-    LAUNCH_CHECK(s);
-  }
-  for (int lev = P.nlevels - 1; lev >= 0; --lev) {
-    const int t0 = P.blvl_ptr[lev], nt = P.blvl_ptr[lev + 1] - t0;
-    if (!nt) continue;
-    const bool fix = s->pins_live && lev == P.nlevels - 1;  // the root level = the candidate block
-    double* root = s->S0 + (int64_t)s->csup_first * R;
-    if (fix) CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
-    k_bwd_level<RC><<<dim3(nt, gy), kNT, 0, s->stream>>>(s->sa, t0, R, s->S2, s->S0);
-    LAUNCH_CHECK(s);
-    if (fix) {
-      ProfScope ps(s, 4);
-      k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist,
-                                                                     s->fpos, s->Qc, root);
-      LAUNCH_CHECK(s);
+  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd) {
+    for (int j = 0; j < P.nlevels; ++j) {
+      const int t0 = S.lvl_item[j], nt = S.lvl_item[j + 1] - t0;
+      const bool fix = !fwd && s->pins_live && j == 0;  // backward level 0 = the root = the candidate block
+      double* root = s->S0 + (int64_t)s->csup_first * R;
+      if (fix)
+        CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
+      if (nt) {
+        // forward: sources z (S0), direct y (S2); backward: D part y (S2), W part x (S0), direct x (S0)
+        k_sweep_items<RC, VEC><<<dim3((nt + 3) / 4, gy), 128, 0, s->stream>>>(
+            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->Spart);
+        LAUNCH_CHECK(s);
+      }
+      const int r0 = S.lvl_red[j], nr = S.lvl_red[j + 1] - r0;
+      if (nr) {
+        k_sweep_reduce<<<nblk((int64_t)nr * R), 256, 0, s->stream>>>(d, r0, nr, R, s->Spart, fwd ? s->S2 : s->S0,
+                                                                      s->S0);
+        LAUNCH_CHECK(s);
+      }
+      if (fix) {
+        k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist,
+                                                                       s->fpos, s->Qc, root);
+        LAUNCH_CHECK(s);
+      }
     }
-  }
+  };
+  sweep(P.fw, s->swf, true);
+  sweep(P.bw, s->swb, false);
 }
-void solve(pd_sim* s, int B) {
+void solve_launch(pd_sim* s, int B) {
   const int R = 3 * B;
-  if (R <= 8) solve_rc<8>(s, B);
-  else if (R <= 24) solve_rc<24>(s, B);
-  else solve_rc<48>(s, B);
+  if (R <= 4) solve_rc<4, false>(s, B);
+  else if (R <= 8) (R % 2 == 0) ? solve_rc<8, true>(s, B) : solve_rc<8, false>(s, B);
+  else if (R <= 24) (R % 2 == 0) ? solve_rc<24, true>(s, B) : solve_rc<24, false>(s, B);
+  else (R % 2 == 0) ? solve_rc<48, true>(s, B) : solve_rc<48, false>(s, B);
+}
+// The whole two-sweep solve (≈ 2 x levels kernels) is captured once per (B, contact fixup) as a CUDA
+// graph and replayed: one launch per A^{-1} application.
+void solve(pd_sim* s, int B) {
+  const int key = 2 * B + (s->pins_live ? 1 : 0);
+  auto it = s->solve_graphs.find(key);
+  if (it == s->solve_graphs.end()) {
+    cudaGraph_t g;
+    const int64_t l0 = s->launches;
+    if (!s->cap_stream) CK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = s->stream;
+    s->stream = s->cap_stream;  // capture on a private stream (the caller's may be the legacy stream)
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      solve_launch(s, B);
+    } catch (...) {
+      cudaStreamEndCapture(s->stream, &g);
+      s->stream = user;
+      throw;
+    }
+    s->stream = user;
+    CK(cudaStreamEndCapture(s->cap_stream, &g));
+    cudaGraphExec_t ge;
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphDestroy(g));
+    it = s->solve_graphs.emplace(key, std::make_pair(ge, s->launches - l0)).first;
+    s->launches = l0;
+  }
+  CK(cudaGraphLaunch(it->second.first, s->stream));
+  s->launches += it->second.second;
 }
 
 // state vector V (free nodes) -> A^{-1} V -> OUT = beta OUT + alpha_c*alpha[b]*sol (masked)
@@ -306,8 +354,8 @@ int read_nactive(pd_sim* s) {
 void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const double* act_step, int64_t act_bs) {
   const HostPlan& P = s->plan;
   residual(s, B, X, s->Y, act_step, act_bs, s->d_fixed, Gout);
-  const int64_t chunk = 2048;
   const int64_t n3 = 3LL * P.n;
+  const int64_t chunk = dot_chunk(B);
   const int nchunk = (int)((n3 + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
   k_inertia_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B,
@@ -315,8 +363,7 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
   LAUNCH_CHECK(s);
   k_dot_final<<<nblk(B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, 1, s->inert);
   LAUNCH_CHECK(s);
-  k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->EE, P.m, B, s->esum, 0);
-  LAUNCH_CHECK(s);
+  dots(s, B, P.m, {{s->EE, nullptr}}, s->esum);
   k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
   LAUNCH_CHECK(s);
 }
@@ -506,25 +553,23 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->d_mass = s->upload(P.node_mass);
     s->d_fixed = s->upload(P.fixed_node);
     s->d_nofix = s->alloc<uint8_t>(P.n);
-    s->sa.sfirst = s->upload(P.sfirst);
-    s->sa.ssize = s->upload(P.ssize);
-    s->sa.rptr = s->upload(P.rptr);
-    s->sa.doff = s->upload(P.doff);
-    s->sa.poff = s->upload(P.poff);
-    s->sa.rows = s->upload(P.rows);
-    s->sa.D = s->upload(P.D);
-    s->sa.W = s->upload(P.P);
-    s->sa.ft_type = s->upload(P.ft_type);
-    s->sa.ft_sup = s->upload(P.ft_sup);
-    s->sa.ft_r0 = s->upload(P.ft_r0);
-    s->sa.ft_r1 = s->upload(P.ft_r1);
-    s->sa.ft_bptr = s->upload(P.ft_bptr);
-    s->sa.fb_s = s->upload(P.fb_s);
-    s->sa.fb_k0 = s->upload(P.fb_k0);
-    s->sa.fb_k1 = s->upload(P.fb_k1);
-    s->sa.bt_sup = s->upload(P.bt_sup);
-    s->sa.bt_c0 = s->upload(P.bt_c0);
-    s->sa.bt_c1 = s->upload(P.bt_c1);
+    s->d_rows = s->upload(P.rows);
+    auto up_sweep = [&](const HostPlan::Sweep& S, SweepDev& d) {
+      d.A = s->upload(S.A);
+      d.a_off = s->upload(S.a_off);
+      d.zidx = s->upload(S.zidx);
+      d.nk = s->upload(S.nk);
+      d.zrow = s->upload(S.zrow);
+      d.out = s->upload(S.out);
+      d.nvalid = s->upload(S.nvalid);
+      d.red_row = s->upload(S.red_row);
+      d.red_mode = s->upload(S.red_mode);
+      d.red_ptr = s->upload(S.red_ptr);
+      d.red_src = s->upload(S.red_src);
+    };
+    up_sweep(P.fw, s->swf);
+    up_sweep(P.bw, s->swb);
+    s->Spart = s->alloc<double>((std::max(P.fw.max_partial_rows, P.bw.max_partial_rows) + 32) * 3 * s->Bmax);
     const int64_t n3B = 3LL * P.n * s->Bmax;
     const int64_t sB = 3LL * P.nfree * s->Bmax;
     double** st_vecs[] = {&s->X, &s->V, &s->Y, &s->Xp, &s->Fext, &s->G, &s->W, &s->U, &s->Rv, &s->Z,
@@ -540,8 +585,9 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     double** small[] = {&s->w_sim, &s->youngs_sim, &s->alpha, &s->beta, &s->rz, &s->bb, &s->dw_acc, &s->res_buf};
     for (double** p : small) *p = s->alloc<double>(s->Bmax);
     s->dots = s->alloc<double>(3 * s->Bmax);
-    s->max_partial_blocks = (n3B / s->Bmax + 2047) / 2048 + 1;
-    s->partial = s->alloc<double>(3 * s->max_partial_blocks * s->Bmax);
+    for (int b = 1; b <= s->Bmax; ++b)
+      s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
+    s->partial = s->alloc<double>(3 * s->max_partial_blocks + 64);
     s->active = s->alloc<int32_t>(s->Bmax);
     s->nactive = s->alloc<int32_t>(1);
     s->it_buf = s->alloc<int32_t>(s->Bmax);
@@ -893,8 +939,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       k_elem_param<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
                                                                       s->DW, s->has_act ? s->DR : nullptr);
       LAUNCH_CHECK(s);
-      k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->DW, P.m, B, s->dw_acc, 1);
-      LAUNCH_CHECK(s);
+      dots(s, B, P.m, {{s->DW, nullptr}}, s->dw_acc, 1);
       if (dL_dact && s->has_act) {
         k_state_to_abi<<<nblk((int64_t)P.m * B), 256, 0, s->stream>>>(s->DR, dL_dact + (int64_t)i * P.m, P.m, B,
                                                                       (int64_t)T * P.m);
@@ -979,8 +1024,7 @@ pd_status pd_eval_objective(pd_sim* s, int32_t B, const double* x, const double*
     }
     if (g) {
       // g = sum_e E_e + sum_i m_i/(2h^2) (x_i - y_i)^2   (eq:opt)
-      k_sum_elems<<<B, 256, 256 * sizeof(double), s->stream>>>(s->EE, P.m, B, g, 0);
-      LAUNCH_CHECK(s);
+      dots(s, B, P.m, {{s->EE, nullptr}}, g);
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->X, 1.0, s->Y, nullptr, -1.0, len, B, nullptr);
       LAUNCH_CHECK(s);
       CK(cudaMemsetAsync(s->EF, 0, (int64_t)P.m * 24 * B * sizeof(double), s->stream));

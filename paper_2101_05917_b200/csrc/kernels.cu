@@ -538,176 +538,72 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
   OUT[i] = pos >= 0 ? base + a * S[(int64_t)pos * 3 * B + ax * B + b] : base;
 }
 
-// ----------------------------------------------------------------- K3: supernodal solves
-// One kernel per ND-tree level and direction.  Storage: D_s = L_ss^{-1}
-// (packed lower), W_s = L[R_s,J_s] D_s (row-major).  Forward level l (reads only values final
-// before the level):   y[J_s] = D_s z[J_s]   and   z[anc] -= W_s z[J_s]   (s in level l).
-// Backward level l:    x[J_s] = D_s^T y[J_s] - W_s^T x[R_s].
-// A CTA owns a 32-row (or 32-column) output tile and a chunk of RC right-hand sides; blocks are
-// accumulated in a fixed order (deterministic, no atomics).  Operands are staged through shared
-// memory in 32-wide K chunks; each thread keeps a 2 x RC/8 register micro-tile.
-constexpr int kTR = 32, kKC = 32, kNT = 128;
-
-template <int RC>
-__device__ __forceinline__ void micro_tile(double (&acc)[2][RC / 8], const double (*Vc)[kKC + 1],
-                                           const double (*Zc)[RC], int ti, int tr) {
+// ----------------------------------------------------------------- K3: supernodal solves (v3)
+// One kernel pair per ND-tree level and sweep.  Work item = one warp: lane = output
+// row (forward) or output column (backward) of a 32-wide chunk of one supernode, k-loop over at most
+// kc factor columns/rows stored k-major in the sweep's stream (A[k*32 + lane]: one coalesced 256 B
+// load per k, read once: streaming hint).  The right-hand-side rows (RC consecutive columns of the
+// [pos][R] solve layout) are warp-uniform broadcast loads.  Single-item chunks write their output row
+// directly; split chunks and every forward W item write partial rows that k_sweep_reduce sums in a
+// fixed order into y / x (assign) or into z of ancestors (subtract): deterministic, no atomics.
+template <int RC, bool VEC>
+__global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int nitems, int R,
+                                                     const double* __restrict__ zc, const double* __restrict__ zi,
+                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
+                                                     double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (t >= nitems) return;
+  const int it = t0 + t;
+  const int c0 = blockIdx.y * RC;
+  const int rcn = min(RC, R - c0);
+  const double* __restrict__ A = sw.A + sw.a_off[it] + lane;
+  const int nk = sw.nk[it];
+  const int zr = sw.zrow[it];
+  const int32_t* __restrict__ idx = rows + sw.zidx[it];
+  double acc[RC];
+#pragma unroll
+  for (int c = 0; c < RC; ++c) acc[c] = 0.0;
 #pragma unroll 4
-  for (int j = 0; j < kKC; ++j) {
-    const double a0 = Vc[ti][j], a1 = Vc[ti + 16][j];
+  for (int k = 0; k < nk; ++k) {
+    const double a = __ldcs(A + (int64_t)k * 32);
+    const int row = zr >= 0 ? zr + k : __ldg(idx + k);
+    const double* __restrict__ src = (zr >= 0 ? zc : zi) + (int64_t)row * R + c0;
+    if (VEC) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
-    for (int q = 0; q < RC / 8; ++q) {
-      const double zz = Zc[j][tr + 8 * q];
-      acc[0][q] = fma(a0, zz, acc[0][q]);
-      acc[1][q] = fma(a1, zz, acc[1][q]);
-    }
-  }
-}
-
-template <int RC>
-__global__ void __launch_bounds__(kNT) k_fwd_level(SolveArgs sa, int task0, int R, double* __restrict__ z,
-                                                    double* __restrict__ y) {
-  constexpr int NQ = RC / 8;
-  __shared__ double Zc[kKC][RC];
-  __shared__ double Vc[kTR][kKC + 1];
-  __shared__ double Acc[kTR][RC];
-  const int task = task0 + blockIdx.x;
-  const int rc0 = blockIdx.y * RC;
-  const int rcn = min(RC, R - rc0);
-  const int type = sa.ft_type[task], s = sa.ft_sup[task], r0 = sa.ft_r0[task], r1 = sa.ft_r1[task];
-  const int f = sa.sfirst[s];
-  const int t = threadIdx.x, ti = t >> 3, tr = t & 7;
-  double acc[2][NQ];
-  if (type == 0) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
-    const double* Dp = sa.D + sa.doff[s];
-    const int nrow = r1 - r0;
-    for (int j0 = 0; j0 < r1; j0 += kKC) {
-      const int nj = min(kKC, r1 - j0);
-      for (int idx = t; idx < kKC * RC; idx += kNT) {
-        const int j = idx / RC, r = idx - j * RC;
-        Zc[j][r] = (j < nj && r < rcn) ? z[(int64_t)(f + j0 + j) * R + rc0 + r] : 0.0;
-      }
-      for (int idx = t; idx < kTR * kKC; idx += kNT) {
-        const int i = idx / kKC, j = idx - i * kKC;
-        const int row = r0 + i, col = j0 + j;
-        Vc[i][j] = (i < nrow && j < nj && col <= row) ? Dp[(int64_t)row * (row + 1) / 2 + col] : 0.0;
-      }
-      __syncthreads();
-      micro_tile<RC>(acc, Vc, Zc, ti, tr);
-      __syncthreads();
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = ti + 16 * q;
-      if (i < nrow)
-#pragma unroll
-        for (int qq = 0; qq < NQ; ++qq) {
-          const int r = tr + 8 * qq;
-          if (r < rcn) y[(int64_t)(f + r0 + i) * R + rc0 + r] = acc[q][qq];
+      for (int c = 0; c < RC / 2; ++c) {
+        if (2 * c < rcn) {
+          const double2 v = __ldg(s2 + c);
+          acc[2 * c] = fma(a, v.x, acc[2 * c]);
+          acc[2 * c + 1] = fma(a, v.y, acc[2 * c + 1]);
         }
-    }
-    return;
-  }
-  for (int idx = t; idx < kTR * RC; idx += kNT) Acc[idx / RC][idx % RC] = 0.0;
-  __syncthreads();
-  for (int bk = sa.ft_bptr[task]; bk < sa.ft_bptr[task + 1]; ++bk) {
-    const int d = sa.fb_s[bk], k0 = sa.fb_k0[bk], nb = sa.fb_k1[bk] - k0;
-    const int nd = sa.ssize[d], fd = sa.sfirst[d];
-    const double* Wd = sa.W + sa.poff[d] + (int64_t)k0 * nd;
-    const int32_t* Rd = sa.rows + sa.rptr[d] + k0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
-    for (int j0 = 0; j0 < nd; j0 += kKC) {
-      const int nj = min(kKC, nd - j0);
-      for (int idx = t; idx < kKC * RC; idx += kNT) {
-        const int j = idx / RC, r = idx - j * RC;
-        Zc[j][r] = (j < nj && r < rcn) ? z[(int64_t)(fd + j0 + j) * R + rc0 + r] : 0.0;
       }
-      for (int idx = t; idx < kTR * kKC; idx += kNT) {
-        const int i = idx / kKC, j = idx - i * kKC;
-        Vc[i][j] = (i < nb && j < nj) ? Wd[(int64_t)i * nd + j0 + j] : 0.0;
-      }
-      __syncthreads();
-      micro_tile<RC>(acc, Vc, Zc, ti, tr);
-      __syncthreads();
-    }
+    } else {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = ti + 16 * q;
-      if (i < nb) {
-        const int rel = Rd[i] - f - r0;
-#pragma unroll
-        for (int qq = 0; qq < NQ; ++qq) Acc[rel][tr + 8 * qq] += acc[q][qq];
-      }
+      for (int c = 0; c < RC; ++c)
+        if (c < rcn) acc[c] = fma(a, __ldg(src + c), acc[c]);
     }
-    __syncthreads();
   }
-  for (int idx = t; idx < (r1 - r0) * RC; idx += kNT) {
-    const int i = idx / RC, r = idx - i * RC;
-    if (r < rcn) z[(int64_t)(f + r0 + i) * R + rc0 + r] -= Acc[i][r];
-  }
+  if (lane >= sw.nvalid[it]) return;
+  const int out = sw.out[it];
+  double* __restrict__ dst = out >= 0 ? direct + (int64_t)(out + lane) * R + c0
+                                      : partial + ((int64_t)(-out - 1) * 32 + lane) * R + c0;
+#pragma unroll
+  for (int c = 0; c < RC; ++c)
+    if (c < rcn) dst[c] = acc[c];
 }
 
-template <int RC>
-__global__ void __launch_bounds__(kNT) k_bwd_level(SolveArgs sa, int task0, int R, const double* __restrict__ y,
-                                                    double* __restrict__ x) {
-  constexpr int NQ = RC / 8;
-  __shared__ double Zc[kKC][RC];
-  __shared__ double Vc[kTR][kKC + 1];
-  const int task = task0 + blockIdx.x;
-  const int rc0 = blockIdx.y * RC;
-  const int rcn = min(RC, R - rc0);
-  const int s = sa.bt_sup[task], c0 = sa.bt_c0[task], c1 = sa.bt_c1[task];
-  const int f = sa.sfirst[s], ns = sa.ssize[s];
-  const int nr = (int)(sa.rptr[s + 1] - sa.rptr[s]);
-  const int ncol = c1 - c0;
-  const double* Dp = sa.D + sa.doff[s];
-  const double* Ws = sa.W + sa.poff[s];
-  const int32_t* Rs = sa.rows + sa.rptr[s];
-  const int t = threadIdx.x, ti = t >> 3, tr = t & 7;
-  double acc[2][NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[0][q] = acc[1][q] = 0.0;
-  for (int i0 = c0; i0 < ns; i0 += kKC) {  // D_s^T y[J_s]: rows i >= column c
-    const int ni = min(kKC, ns - i0);
-    for (int idx = t; idx < kKC * RC; idx += kNT) {
-      const int k = idx / RC, r = idx - k * RC;
-      Zc[k][r] = (k < ni && r < rcn) ? y[(int64_t)(f + i0 + k) * R + rc0 + r] : 0.0;
-    }
-    for (int idx = t; idx < kTR * kKC; idx += kNT) {
-      const int k = idx / kTR, c = idx - k * kTR;
-      const int row = i0 + k, col = c0 + c;
-      Vc[c][k] = (c < ncol && k < ni && row >= col) ? Dp[(int64_t)row * (row + 1) / 2 + col] : 0.0;
-    }
-    __syncthreads();
-    micro_tile<RC>(acc, Vc, Zc, ti, tr);
-    __syncthreads();
-  }
-  for (int k0 = 0; k0 < nr; k0 += kKC) {  // - W_s^T x[R_s]
-    const int nk = min(kKC, nr - k0);
-    for (int idx = t; idx < kKC * RC; idx += kNT) {
-      const int k = idx / RC, r = idx - k * RC;
-      Zc[k][r] = (k < nk && r < rcn) ? x[(int64_t)Rs[k0 + k] * R + rc0 + r] : 0.0;
-    }
-    for (int idx = t; idx < kTR * kKC; idx += kNT) {
-      const int k = idx / kTR, c = idx - k * kTR;
-      Vc[c][k] = (c < ncol && k < nk) ? -Ws[(int64_t)(k0 + k) * ns + c0 + c] : 0.0;
-    }
-    __syncthreads();
-    micro_tile<RC>(acc, Vc, Zc, ti, tr);
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int c = ti + 16 * q;
-    if (c < ncol)
-#pragma unroll
-      for (int qq = 0; qq < NQ; ++qq) {
-        const int r = tr + 8 * qq;
-        if (r < rcn) x[(int64_t)(f + c0 + c) * R + rc0 + r] = acc[q][qq];
-      }
-  }
+__global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
+                               double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)ntarget * R) return;
+  const int t = r0 + (int)(g / R), c = (int)(g % R);
+  double acc = 0;
+  for (int q = sw.red_ptr[t]; q < sw.red_ptr[t + 1]; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  const int64_t o = (int64_t)sw.red_row[t] * R + c;
+  if (sw.red_mode[t] == 0) dst_assign[o] = acc;
+  else dst_sub[o] -= acc;
 }
 
 // ----------------------------------------------------------------- K5: contact
@@ -984,7 +880,7 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, dou
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
   double acc[3] = {0, 0, 0};
   for (int64_t i = beg + threadIdx.x; i < end; i += nb)
-    for (int p = 0; p < da.npairs; ++p) acc[p] += da.u[p][i] * da.v[p][i];
+    for (int p = 0; p < da.npairs; ++p) acc[p] += da.v[p] ? da.u[p][i] * da.v[p][i] : da.u[p][i];
   for (int p = 0; p < da.npairs; ++p) {
     red[threadIdx.x] = acc[p];
     __syncthreads();
@@ -999,13 +895,14 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, dou
     __syncthreads();
   }
 }
-__global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out) {
+__global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out,
+                            int accumulate = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npairs * B) return;
   const int p = i / B, b = i - p * B;
   double s = 0;
   for (int c = 0; c < nchunk; ++c) s += partial[((int64_t)p * nchunk + c) * B + b];
-  out[i] = s;
+  out[i] = accumulate ? out[i] + s : s;
 }
 // sum over elements of E[e][b] (deterministic) -> out[b] (+= if accumulate)
 __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* __restrict__ out, int accumulate) {

@@ -25,13 +25,11 @@ struct ElemArgs {
   int64_t act_bstride;
 };
 
-struct SolveArgs {
-  const int32_t *sfirst, *ssize;
-  const int64_t *rptr, *doff, *poff;
-  const int32_t* rows;
-  const double *D, *W;
-  const int32_t *ft_type, *ft_sup, *ft_r0, *ft_r1, *ft_bptr, *fb_s, *fb_k0, *fb_k1;
-  const int32_t *bt_sup, *bt_c0, *bt_c1;
+struct SweepDev {  // device copy of HostPlan::Sweep
+  const double* A;
+  const int64_t *a_off, *zidx;
+  const int32_t *nk, *zrow, *out, *nvalid;
+  const int32_t *red_row, *red_mode, *red_ptr, *red_src;
 };
 
 struct DotArgs {

@@ -8,7 +8,6 @@
 
 namespace pdb {
 
-constexpr int kTile = 32;  // rows per triangular-solve tile
 
 struct HostPlan {
   // ---- mesh ----
@@ -41,15 +40,27 @@ struct HostPlan {
   std::vector<double> D, P;          // P holds W_s = L[R_s, J_s] L_ss^{-1} row-major (nr x ns)
   int64_t nnzL = 0;                  // stored entries of L_s (diag blocks packed + panels)
   double factor_flops = 0, factor_ms = 0;
-  // ---- solve schedule (one kernel per tree level and direction) ----
+  // ---- solve schedule (K3 v3): per level and sweep, warp work items over a
+  // k-major factor stream (element (k, lane) of item t at a_off[t] + (k - k0) * 32 + lane), then a
+  // deterministic reduction of partial rows into their targets.
   int nlevels = 0;
-  // forward level l: tasks [flvl_ptr[l], flvl_ptr[l+1]).  type 0 (D task): y[J_s rows r0..r1) =
-  // D_s z[J_s]; type 1 (W task): z[J_a rows r0..r1) -= sum_blocks W_s[k0..k1) z[J_s].
-  std::vector<int32_t> flvl_ptr, ft_type, ft_sup, ft_r0, ft_r1, ft_bptr;
-  std::vector<int32_t> fb_s, fb_k0, fb_k1;
-  // backward level l: column tiles [blvl_ptr[l], blvl_ptr[l+1]) of level-l supernodes:
-  // x[J_s cols c0..c1) = D_s^T y[J_s] - W_s^T x[R_s].
-  std::vector<int32_t> blvl_ptr, bt_sup, bt_c0, bt_c1;
+  struct Sweep {
+    std::vector<double> A;             // factor stream in item order (k-major 32-lane blocks)
+    std::vector<int32_t> lvl_item;     // [nlevels+1] items of level l: [lvl_item[l], lvl_item[l+1])
+    std::vector<int64_t> a_off;        // per item
+    std::vector<int32_t> nk;           // k-steps
+    std::vector<int32_t> zrow;         // >= 0: source rows zrow + k (contiguous); < 0: rows from zidx
+    std::vector<int64_t> zidx;         // offset into `rows` (indirect source rows R_s[k0 + k])
+    std::vector<int32_t> out;          // >= 0: direct output row out + lane; < 0: partial rows (-out-1)*32 + lane
+    std::vector<int32_t> nvalid;       // valid lanes
+    std::vector<int32_t> lvl_red;      // [nlevels+1] reduce targets of level l
+    std::vector<int32_t> red_row;      // target row (solve position)
+    std::vector<int32_t> red_mode;     // 0: dst[row] = sum (y or x), 1: z[row] -= sum
+    std::vector<int32_t> red_ptr;      // [ntargets+1] into red_src
+    std::vector<int32_t> red_src;      // partial row indices, summed in this order
+    int64_t max_partial_rows = 0;
+  } fw, bw;
+  int kc = 128;                        // max k-steps per item
   // ---- contact candidates: ordered LAST as one root supernode ----
   int nc = 0;                        // number of candidate nodes (0 = no contact)
   int csup = -1;                     // index of the candidate supernode (= nsup - 1)

@@ -173,6 +173,160 @@ static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
   }
 }
 
+// ---------------------------------------------------------------- solve schedule
+// Forward sweep, level l (children before parents), for every level-l supernode s (z[J_s] final):
+//   D items: y[J_s rows i0..i0+32) = D_s[rows, 0..min(i0+32, ns)) z[J_s]      (k-major, lane = row)
+//   W items: partial rows = W_s[rows i0..i0+32, :] z[J_s];  reduce: z[R_s[i]] -= partial row i
+// Backward sweep, level l (parents first), column chunk c0..c0+32 of s:
+//   x[J_s cols] = D_s^T y[J_s] - W_s^T x[R_s]     (D part k = c0..ns, W part k = 0..nr; lane = column)
+// Items hold <= kc k-steps; a chunk covered by one item writes its output directly, otherwise its
+// items write partial rows that the level's reduce sums in item order (deterministic).
+static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
+  const int L = 32, KC = P.kc;
+  auto init = [&](HostPlan::Sweep& S) {
+    S = HostPlan::Sweep();
+    S.lvl_item.assign(1, 0);
+    S.lvl_red.assign(1, 0);
+    S.red_ptr.assign(1, 0);
+  };
+  init(P.fw);
+  init(P.bw);
+  auto Dval = [&](int s, int i, int k) -> double {  // D_s[i][k], packed lower
+    return k <= i ? P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + k] : 0.0;
+  };
+  auto Wval = [&](int s, int i, int k) -> double {  // W_s[i][k], row-major nr x ns
+    return P.P[P.poff[s] + (int64_t)i * P.ssize[s] + k];
+  };
+  // ---- forward
+  {
+    HostPlan::Sweep& S = P.fw;
+    for (int lev = 0; lev < P.nlevels; ++lev) {
+      int64_t prow = 0;  // partial rows of this level
+      std::vector<std::pair<int32_t, int32_t>> contrib;  // (target row, partial row) in item order
+      std::vector<std::pair<int32_t, std::vector<int32_t>>> dsum;  // (y row, partial rows) multi-item D chunks
+      for (int s : byh[lev]) {
+        const int ns = P.ssize[s], f = P.sfirst[s];
+        const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        for (int i0 = 0; i0 < ns; i0 += L) {  // D items
+          const int kend = std::min(i0 + L, ns), nv = std::min(L, ns - i0);
+          const int nit = (kend + KC - 1) / KC;
+          std::vector<int32_t> rows_p;
+          for (int k0 = 0; k0 < kend; k0 += KC) {
+            const int k1 = std::min(kend, k0 + KC);
+            S.a_off.push_back((int64_t)S.A.size());
+            for (int k = k0; k < k1; ++k)
+              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? Dval(s, i0 + l, k) : 0.0);
+            S.nk.push_back(k1 - k0);
+            S.zrow.push_back(f + k0);
+            S.zidx.push_back(0);
+            S.nvalid.push_back(nv);
+            if (nit == 1) {
+              S.out.push_back(f + i0);
+            } else {
+              S.out.push_back(-(int32_t)(prow / L) - 1);
+              for (int l = 0; l < nv; ++l) rows_p.push_back((int32_t)(prow + l));
+              prow += L;
+            }
+          }
+          if (nit > 1)
+            for (int l = 0; l < nv; ++l) {
+              std::vector<int32_t> src;
+              for (int t = 0; t < nit; ++t) src.push_back(rows_p[t * nv + l]);
+              dsum.push_back({f + i0 + l, src});
+            }
+        }
+        for (int i0 = 0; i0 < nr; i0 += L) {  // W items
+          const int nv = std::min(L, nr - i0);
+          for (int k0 = 0; k0 < ns; k0 += KC) {
+            const int k1 = std::min(ns, k0 + KC);
+            S.a_off.push_back((int64_t)S.A.size());
+            for (int k = k0; k < k1; ++k)
+              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? Wval(s, i0 + l, k) : 0.0);
+            S.nk.push_back(k1 - k0);
+            S.zrow.push_back(f + k0);
+            S.zidx.push_back(0);
+            S.nvalid.push_back(nv);
+            S.out.push_back(-(int32_t)(prow / L) - 1);
+            for (int l = 0; l < nv; ++l) contrib.push_back({P.rows[P.rptr[s] + i0 + l], (int32_t)(prow + l)});
+            prow += L;
+          }
+        }
+      }
+      S.lvl_item.push_back((int32_t)S.a_off.size());
+      S.max_partial_rows = std::max(S.max_partial_rows, prow);
+      for (auto& d : dsum) {
+        S.red_row.push_back(d.first);
+        S.red_mode.push_back(0);
+        for (int32_t r : d.second) S.red_src.push_back(r);
+        S.red_ptr.push_back((int32_t)S.red_src.size());
+      }
+      std::stable_sort(contrib.begin(), contrib.end(),
+                       [](const std::pair<int32_t, int32_t>& x, const std::pair<int32_t, int32_t>& y) {
+                         return x.first < y.first;
+                       });
+      for (size_t i = 0; i < contrib.size();) {
+        size_t j = i;
+        S.red_row.push_back(contrib[i].first);
+        S.red_mode.push_back(1);
+        while (j < contrib.size() && contrib[j].first == contrib[i].first) S.red_src.push_back(contrib[j++].second);
+        S.red_ptr.push_back((int32_t)S.red_src.size());
+        i = j;
+      }
+      S.lvl_red.push_back((int32_t)S.red_row.size());
+    }
+  }
+  // ---- backward (levels top-down; stored in that execution order: level index = H - l)
+  {
+    HostPlan::Sweep& S = P.bw;
+    for (int lev = P.nlevels - 1; lev >= 0; --lev) {
+      int64_t prow = 0;
+      for (int s : byh[lev]) {
+        const int ns = P.ssize[s], f = P.sfirst[s];
+        const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        for (int c0 = 0; c0 < ns; c0 += L) {
+          const int nv = std::min(L, ns - c0);
+          const int nit = (ns - c0 + KC - 1) / KC + (nr + KC - 1) / KC;
+          std::vector<int32_t> rows_p;
+          auto emit = [&](int64_t zi, int zr, int nk, auto&& val) {
+            S.a_off.push_back((int64_t)S.A.size());
+            for (int k = 0; k < nk; ++k)
+              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, c0 + l) : 0.0);
+            S.nk.push_back(nk);
+            S.zrow.push_back(zr);
+            S.zidx.push_back(zi);
+            S.nvalid.push_back(nv);
+            if (nit == 1) {
+              S.out.push_back(f + c0);
+            } else {
+              S.out.push_back(-(int32_t)(prow / L) - 1);
+              for (int l = 0; l < nv; ++l) rows_p.push_back((int32_t)(prow + l));
+              prow += L;
+            }
+          };
+          for (int k0 = c0; k0 < ns; k0 += KC) {  // D_s^T y[J_s]: k = row of D_s, lane = column
+            const int k1 = std::min(ns, k0 + KC);
+            emit(0, f + k0, k1 - k0, [&](int k, int c) { return Dval(s, k0 + k, c); });
+          }
+          for (int k0 = 0; k0 < nr; k0 += KC) {  // - W_s^T x[R_s]
+            const int k1 = std::min(nr, k0 + KC);
+            emit(P.rptr[s] + k0, -1, k1 - k0, [&](int k, int c) { return -Wval(s, k0 + k, c); });
+          }
+          if (nit > 1)
+            for (int l = 0; l < nv; ++l) {
+              S.red_row.push_back(f + c0 + l);
+              S.red_mode.push_back(0);
+              for (int t = 0; t < nit; ++t) S.red_src.push_back(rows_p[t * nv + l]);
+              S.red_ptr.push_back((int32_t)S.red_src.size());
+            }
+        }
+      }
+      S.lvl_item.push_back((int32_t)S.a_off.size());
+      S.lvl_red.push_back((int32_t)S.red_row.size());
+      S.max_partial_rows = std::max(S.max_partial_rows, prow);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- build
 std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
                        double dx, double density, double h, const int32_t* fixed_dofs,
@@ -520,62 +674,9 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
     return "A is not symmetric positive definite (non-positive pivot in the Cholesky factorisation)";
   }
 
-  // ---------------- solve schedule: one forward and one backward kernel per tree level
+  // ---------------- solve schedule (K3 v3)
   P.nlevels = H + 1;
-  P.flvl_ptr.assign(1, 0);
-  P.blvl_ptr.assign(1, 0);
-  P.ft_type.clear(); P.ft_sup.clear(); P.ft_r0.clear(); P.ft_r1.clear(); P.ft_bptr.assign(1, 0);
-  P.fb_s.clear(); P.fb_k0.clear(); P.fb_k1.clear();
-  P.bt_sup.clear(); P.bt_c0.clear(); P.bt_c1.clear();
-  for (int lev = 0; lev <= H; ++lev) {
-    // D tasks: row tiles of every level-l supernode
-    for (int s : byh[lev])
-      for (int r0 = 0; r0 < P.ssize[s]; r0 += kTile) {
-        P.ft_type.push_back(0);
-        P.ft_sup.push_back(s);
-        P.ft_r0.push_back(r0);
-        P.ft_r1.push_back(std::min(P.ssize[s], r0 + kTile));
-        P.ft_bptr.push_back((int32_t)P.fb_s.size());
-      }
-    // W tasks: ancestor row tiles touched by level-l panels; blocks in increasing s (fixed order)
-    std::vector<std::array<int32_t, 5>> blks;  // (anc, tile, s, k0, k1)
-    for (int s : byh[lev]) {
-      const int64_t b = P.rptr[s], e = P.rptr[s + 1];
-      for (int64_t k = b; k < e;) {
-        const int a = sup_of_pos[P.rows[k]];
-        const int tile = (P.rows[k] - P.sfirst[a]) / kTile;
-        int64_t k2 = k;
-        while (k2 < e && sup_of_pos[P.rows[k2]] == a && (P.rows[k2] - P.sfirst[a]) / kTile == tile) ++k2;
-        blks.push_back({a, tile, s, (int32_t)(k - b), (int32_t)(k2 - b)});
-        k = k2;
-      }
-    }
-    std::sort(blks.begin(), blks.end());
-    for (size_t i = 0; i < blks.size();) {
-      size_t j = i;
-      const int a = blks[i][0], tile = blks[i][1];
-      while (j < blks.size() && blks[j][0] == a && blks[j][1] == tile) {
-        P.fb_s.push_back(blks[j][2]);
-        P.fb_k0.push_back(blks[j][3]);
-        P.fb_k1.push_back(blks[j][4]);
-        ++j;
-      }
-      P.ft_type.push_back(1);
-      P.ft_sup.push_back(a);
-      P.ft_r0.push_back(tile * kTile);
-      P.ft_r1.push_back(std::min(P.ssize[a], (tile + 1) * kTile));
-      P.ft_bptr.push_back((int32_t)P.fb_s.size());
-      i = j;
-    }
-    P.flvl_ptr.push_back((int32_t)P.ft_type.size());
-    for (int s : byh[lev])
-      for (int c0 = 0; c0 < P.ssize[s]; c0 += kTile) {
-        P.bt_sup.push_back(s);
-        P.bt_c0.push_back(c0);
-        P.bt_c1.push_back(std::min(P.ssize[s], c0 + kTile));
-      }
-    P.blvl_ptr.push_back((int32_t)P.bt_sup.size());
-  }
+  build_solve_schedule(P, byh);
   return "";
 }
 

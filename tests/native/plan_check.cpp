@@ -47,45 +47,39 @@ int main(int argc, char** argv) {
   std::vector<double> v(N), b(N, 0.0);
   for (auto& x : v) x = nd(rng);
   for (int p = 0; p < N; ++p) for (int64_t k = P.a_ptr[p]; k < P.a_ptr[p + 1]; ++k) b[p] += P.a_val[k] * v[P.a_col[k]];
-  // forward: per level, D tasks y[J_s] = D_s z[J_s]; W tasks z[anc] -= W_s z_old[J_s]
+  // Emulate the device schedule (K3 v3) exactly: per level, items (k-major 32-lane blocks) then the
+  // level's reduce; forward writes y (D) / partial rows, backward writes x / partial rows.
   std::vector<double> z(b), y(N, 0.0), x(N, 0.0);
-  for (int lev = 0; lev < P.nlevels; ++lev) {
-    std::vector<double> zold = z;
-    for (int t = P.flvl_ptr[lev]; t < P.flvl_ptr[lev + 1]; ++t) {
-      int s = P.ft_sup[t], r0 = P.ft_r0[t], r1 = P.ft_r1[t], f = P.sfirst[s];
-      if (P.ft_type[t] == 0) {
-        for (int i = r0; i < r1; ++i) { double sum = 0; for (int j = 0; j <= i; ++j) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + j] * zold[f + j]; y[f + i] = sum; }
-      } else {
-        for (int bk = P.ft_bptr[t]; bk < P.ft_bptr[t + 1]; ++bk) {
-          int d = P.fb_s[bk], nd_ = P.ssize[d];
-          for (int k = P.fb_k0[bk]; k < P.fb_k1[bk]; ++k) {
-            int r = P.rows[P.rptr[d] + k];
-            if (r < f + r0 || r >= f + r1) { printf("bad block row\n"); return 3; }
-            double sum = 0;
-            for (int j = 0; j < nd_; ++j) sum += P.P[P.poff[d] + (int64_t)k * nd_ + j] * zold[P.sfirst[d] + j];
-            z[r] -= sum;
+  auto run = [&](const HostPlan::Sweep& S, std::vector<double>& zsrc, std::vector<double>& direct,
+                 std::vector<double>* zsub, bool fwd) {
+    for (int lev = 0; lev < P.nlevels; ++lev) {
+      std::vector<double> part(S.max_partial_rows + 32, 0.0);
+      for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t) {
+        for (int l = 0; l < S.nvalid[t]; ++l) {
+          double acc = 0;
+          for (int k = 0; k < S.nk[t]; ++k) {
+            const int zr = S.zrow[t] >= 0 ? S.zrow[t] + k : P.rows[S.zidx[t] + k];
+            acc += S.A[S.a_off[t] + (int64_t)k * 32 + l] * (fwd ? zsrc[zr] : (S.zrow[t] >= 0 ? y[zr] : x[zr]));
           }
+          if (S.out[t] >= 0) direct[S.out[t] + l] = acc;
+          else part[(int64_t)(-S.out[t] - 1) * 32 + l] = acc;
         }
       }
-    }
-  }
-  for (int lev = P.nlevels - 1; lev >= 0; --lev) {
-    for (int t = P.blvl_ptr[lev]; t < P.blvl_ptr[lev + 1]; ++t) {
-      int s = P.bt_sup[t], c0 = P.bt_c0[t], c1 = P.bt_c1[t], f = P.sfirst[s], ns = P.ssize[s];
-      int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-      for (int c = c0; c < c1; ++c) {
-        double sum = 0;
-        for (int i = c; i < ns; ++i) sum += P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + c] * y[f + i];
-        for (int k = 0; k < nr; ++k) sum -= P.P[P.poff[s] + (int64_t)k * ns + c] * x[P.rows[P.rptr[s] + k]];
-        x[f + c] = sum;
+      for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) {
+        double acc = 0;
+        for (int q = S.red_ptr[r]; q < S.red_ptr[r + 1]; ++q) acc += part[S.red_src[q]];
+        if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
+        else (*zsub)[S.red_row[r]] -= acc;
       }
     }
-  }
+  };
+  run(P.fw, z, y, &z, true);
+  run(P.bw, y, x, nullptr, false);
   double err = 0, mx = 0;
   for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
   int64_t nnzA = P.a_ptr[N];
-  printf("n=%d nfree=%d nsup=%d levels=%d ftasks=%zu fblocks=%zu btasks=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
-         n, N, P.nsup, P.nlevels, P.ft_type.size(), P.fb_s.size(), P.bt_sup.size(), (long long)nnzA, (long long)P.nnzL, P.factor_flops,
-         P.factor_ms, err / mx);
+  printf("n=%d nfree=%d nsup=%d levels=%d fitems=%zu bitems=%zu fstream=%zu bstream=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
+         n, N, P.nsup, P.nlevels, P.fw.a_off.size(), P.bw.a_off.size(), P.fw.A.size(), P.bw.A.size(), (long long)nnzA,
+         (long long)P.nnzL, P.factor_flops, P.factor_ms, err / mx);
   return err / mx < 1e-10 ? 0 : 2;
 }
