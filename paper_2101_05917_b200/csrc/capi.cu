@@ -214,6 +214,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const HostPlan& P = s->plan;
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
+  CK(cudaFuncSetAttribute(k_sweep_items<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
   auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd) {
     for (int j = 0; j < P.nlevels; ++j) {
       const int t0 = S.lvl_item[j], nt = S.lvl_item[j + 1] - t0;
@@ -223,7 +224,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
         CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
       if (nt) {
         // forward: sources z (S0), direct y (S2); backward: D part y (S2), W part x (S0), direct x (S0)
-        k_sweep_items<RC, VEC><<<dim3((nt + 3) / 4, gy), 128, 0, s->stream>>>(
+        k_sweep_items<RC, VEC><<<dim3(nt, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
             d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->Spart);
         LAUNCH_CHECK(s);
       }
@@ -539,7 +540,12 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
                                opts->n_contact, &numerical);
     if (!e.empty()) return fail(nullptr, numerical ? PD_ERR_NUMERICAL : PD_ERR_INVALID_ARGUMENT, e);
     const HostPlan& P = s->plan;
-    std::memcpy(s->st.dN, P.dN, sizeof(P.dN));
+    {
+      const double g = 1.0 / std::sqrt(3.0), c = 1.0 / (4.0 * mesh->dx);
+      s->st.m3[0] = c * (1 - g) * (1 - g);
+      s->st.m3[1] = c * (1 - g) * (1 + g);
+      s->st.m3[2] = c * (1 + g) * (1 + g);
+    }
     for (int j = 0; j < 3; ++j) s->st.fiber[j] = fiber[j];
     s->st.V = mesh->dx * mesh->dx * mesh->dx / 8.0;
     s->st.w_m = mat->muscle_w;

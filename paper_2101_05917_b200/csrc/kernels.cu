@@ -203,7 +203,17 @@ __device__ __forceinline__ double qsum8(double v) {
   return v;
 }
 
-// Deformation gradient F (and, if P != null, dF = G_q p_e) at quad point q of element e, sim b.
+// Shape-function gradient of the voxel stencil at quad point q, corner a, axis j (reading §2.1):
+// dN_a/dX_j = s_j(a)/(4 dx) prod_{k != j} (1 + s_k(a) xi_k(q)); each factor is (1 + 1/sqrt3) when bit k
+// of a equals bit k of q, else (1 - 1/sqrt3) -> one of three magnitudes (st.m3), computed from bits so
+// that lanes with different q never diverge on a constant-bank index.
+__device__ __forceinline__ double dNf(const Stencil& st, int q, int a, int j) {
+  const int n = __popc(~(a ^ q) & 7 & ~(1 << j));
+  const double mag = n == 2 ? st.m3[2] : (n == 1 ? st.m3[1] : st.m3[0]);
+  return ((a >> j) & 1) ? mag : -mag;
+}
+
+// Deformation gradient F = G_q x_e at quad point q of element e, sim b (state layout [n][3][B]).
 __device__ __forceinline__ void load_F(const double* __restrict__ X, const int32_t* __restrict__ hex8,
                                        const Stencil& st, int e, int b, int q, int B, double* F) {
 #pragma unroll
@@ -211,10 +221,10 @@ __device__ __forceinline__ void load_F(const double* __restrict__ X, const int32
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int node = __ldg(hex8 + 8 * (int64_t)e + a);
-    const double d0 = st.dN[q][a][0], d1 = st.dN[q][a][1], d2 = st.dN[q][a][2];
+    const double d0 = dNf(st, q, a, 0), d1 = dNf(st, q, a, 1), d2 = dNf(st, q, a, 2);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double xv = X[(3 * (int64_t)node + i) * B + b];
+      const double xv = __ldg(X + (3 * (int64_t)node + i) * B + b);
       F[3 * i] = fma(xv, d0, F[3 * i]);
       F[3 * i + 1] = fma(xv, d1, F[3 * i + 1]);
       F[3 * i + 2] = fma(xv, d2, F[3 * i + 2]);
@@ -222,17 +232,30 @@ __device__ __forceinline__ void load_F(const double* __restrict__ X, const int32
   }
 }
 
-// G_q^T P summed over the 8 lanes of the (e, b) group, written to EF[e][a][i][b].
+// Element force sum_q G_q^T P_q of the (e, b) group (8 consecutive lanes, lane q holds P_q): the 8 P_q
+// go through shared memory (group-private, padded rows), then lane a forms the 3 components of corner
+// a in a fixed q order: EF[e][a][i][b].  Ps = this group's 73-double slot.
 __device__ __forceinline__ void store_force(const double* Pm, const Stencil& st, int e, int b, int q, int B,
-                                            double* __restrict__ EF) {
+                                            double* Ps, double* __restrict__ EF) {
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const double d0 = st.dN[q][a][0], d1 = st.dN[q][a][1], d2 = st.dN[q][a][2];
+  for (int k = 0; k < 9; ++k) Ps[9 * q + k] = Pm[k];
+  __syncwarp();
+  const int a = q;
+  double o0 = 0, o1 = 0, o2 = 0;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double v = qsum8(Pm[3 * i] * d0 + Pm[3 * i + 1] * d1 + Pm[3 * i + 2] * d2);
-      if (EF && 3 * a + i >= 3 * q && 3 * a + i < 3 * q + 3) EF[((8 * (int64_t)e + a) * 3 + i) * B + b] = v;
-    }
+  for (int qq = 0; qq < 8; ++qq) {
+    const double d0 = dNf(st, qq, a, 0), d1 = dNf(st, qq, a, 1), d2 = dNf(st, qq, a, 2);
+    const double* P = Ps + 9 * qq;
+    o0 = fma(P[0], d0, fma(P[1], d1, fma(P[2], d2, o0)));
+    o1 = fma(P[3], d0, fma(P[4], d1, fma(P[5], d2, o1)));
+    o2 = fma(P[6], d0, fma(P[7], d1, fma(P[8], d2, o2)));
+  }
+  __syncwarp();
+  if (EF) {
+    double* o = EF + ((8 * (int64_t)e + a) * 3) * B + b;
+    o[0] = o0;
+    o[B] = o1;
+    o[2 * B] = o2;
   }
 }
 
@@ -282,7 +305,8 @@ __global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict_
 #pragma unroll
       for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
   }
-  store_force(Pm, st, e, b, q, B, live ? EF : nullptr);
+  __shared__ double Psm[32][73];
+  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
   energy = qsum8(energy);
   if (live && EE && q == 0) EE[(int64_t)e * B + b] = energy;
 }
@@ -303,7 +327,7 @@ __global__ void k_elem_rotations(const double* __restrict__ X, Stencil st, const
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
         double s = 0;
-        for (int a = 0; a < 8; ++a) s += xe[a][i] * st.dN[q][a][j];
+        for (int a = 0; a < 8; ++a) s += xe[a][i] * dNf(st, q, a, j);
         F[3 * i + j] = s;
       }
     polar_rotation(F, R);
@@ -426,7 +450,8 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
 #pragma unroll
       for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * (dFm[i] - jd[i]) * st.fiber[j];
   }
-  store_force(Pm, st, e, b, q, B, live ? EF : nullptr);
+  __shared__ double Psm[32][73];
+  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
 
 // Parameter-gradient terms at x_{i+1} for adjoint u (chain rule):
@@ -539,53 +564,101 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 }
 
 // ----------------------------------------------------------------- K3: supernodal solves (v3)
-// One kernel pair per ND-tree level and sweep.  Work item = one warp: lane = output
-// row (forward) or output column (backward) of a 32-wide chunk of one supernode, k-loop over at most
-// kc factor columns/rows stored k-major in the sweep's stream (A[k*32 + lane]: one coalesced 256 B
-// load per k, read once: streaming hint).  The right-hand-side rows (RC consecutive columns of the
-// [pos][R] solve layout) are warp-uniform broadcast loads.  Single-item chunks write their output row
-// directly; split chunks and every forward W item write partial rows that k_sweep_reduce sums in a
-// fixed order into y / x (assign) or into z of ancestors (subtract): deterministic, no atomics.
+// One kernel pair per ND-tree level and sweep.  Work item = one CTA of 4 warps: lane
+// = output row (forward) or output column (backward) of a 32-wide chunk of one supernode; the item's
+// <= 256 k-steps are split into 4 warp ranges.  Each warp stages its factor block (k-major, 32
+// doubles per k, contiguous in the sweep's stream) and its right-hand-side rows (RC columns of the
+// [pos][R] solve layout) into shared memory with cp.async — everything in flight at once — then
+// accumulates RC columns per lane with broadcast shared loads; the 4 warp sums are added in warp
+// order.  Single-item chunks write their output rows directly; split chunks and every forward W
+// item write partial rows that k_sweep_reduce adds in a fixed order into y / x (assign) or into z of
+// ancestors (subtract): deterministic, no atomics.
+constexpr int kWK = 64;  // k-steps per warp
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int RC>
+constexpr int sweep_smem_bytes() { return 4 * (kWK * 32 + kWK * RC) * 8; }
+
 template <int RC, bool VEC>
 __global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int nitems, int R,
                                                      const double* __restrict__ zc, const double* __restrict__ zi,
                                                      const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                      double* __restrict__ partial) {
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (t >= nitems) return;
-  const int it = t0 + t;
+  extern __shared__ __align__(16) double sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it = t0 + blockIdx.x;
   const int c0 = blockIdx.y * RC;
   const int rcn = min(RC, R - c0);
-  const double* __restrict__ A = sw.A + sw.a_off[it] + lane;
   const int nk = sw.nk[it];
-  const int zr = sw.zrow[it];
-  const int32_t* __restrict__ idx = rows + sw.zidx[it];
+  const int per = (nk + 3) >> 2;
+  const int kw0 = min(nk, w * per), kw1 = min(nk, kw0 + per), nkw = kw1 - kw0;
+  double* As = sm + w * (kWK * 32 + kWK * RC);
+  double* Zs = As + kWK * 32;
+  {
+    const double* Ag = sw.A + sw.a_off[it] + (int64_t)kw0 * 32;
+    for (int i = lane; i < nkw * 16; i += 32) cp_async16(As + 2 * i, Ag + 2 * i);
+    const int zr = sw.zrow[it];
+    const double* zsrc = zr >= 0 ? zc : zi;
+    const int32_t* idx = rows + sw.zidx[it] + kw0;
+    if (VEC) {
+      constexpr int H = RC / 2;
+      for (int i = lane; i < nkw * H; i += 32) {
+        const int k = i / H, c = 2 * (i - k * H);
+        const int row = zr >= 0 ? zr + kw0 + k : __ldg(idx + k);
+        if (c < rcn) cp_async16(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+      }
+    } else {
+      for (int i = lane; i < nkw * RC; i += 32) {
+        const int k = i / RC, c = i - k * RC;
+        const int row = zr >= 0 ? zr + kw0 + k : __ldg(idx + k);
+        if (c < rcn) cp_async8(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+        else Zs[k * RC + c] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+  }
   double acc[RC];
 #pragma unroll
   for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < nk; ++k) {
-    const double a = __ldcs(A + (int64_t)k * 32);
-    const int row = zr >= 0 ? zr + k : __ldg(idx + k);
-    const double* __restrict__ src = (zr >= 0 ? zc : zi) + (int64_t)row * R + c0;
+  for (int k = 0; k < nkw; ++k) {
+    const double a = As[k * 32 + lane];
     if (VEC) {
-      const double2* s2 = reinterpret_cast<const double2*>(src);
+      const double2* z2 = reinterpret_cast<const double2*>(Zs + k * RC);
 #pragma unroll
       for (int c = 0; c < RC / 2; ++c) {
-        if (2 * c < rcn) {
-          const double2 v = __ldg(s2 + c);
-          acc[2 * c] = fma(a, v.x, acc[2 * c]);
-          acc[2 * c + 1] = fma(a, v.y, acc[2 * c + 1]);
-        }
+        const double2 v = z2[c];
+        acc[2 * c] = fma(a, v.x, acc[2 * c]);
+        acc[2 * c + 1] = fma(a, v.y, acc[2 * c + 1]);
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < RC; ++c)
-        if (c < rcn) acc[c] = fma(a, __ldg(src + c), acc[c]);
+      for (int c = 0; c < RC; ++c) acc[c] = fma(a, Zs[k * RC + c], acc[c]);
     }
   }
-  if (lane >= sw.nvalid[it]) return;
+  // fixed-order sum of the 4 warp partials (warp w's slot reuses its own A staging area)
+  __syncthreads();
+  double* red = sm + w * (kWK * 32 + kWK * RC);
+#pragma unroll
+  for (int c = 0; c < RC; ++c) red[c * 32 + lane] = acc[c];
+  __syncthreads();
+  if (w != 0 || lane >= sw.nvalid[it]) return;
+#pragma unroll
+  for (int c = 0; c < RC; ++c) {
+    double v = sm[c * 32 + lane];
+#pragma unroll
+    for (int ww = 1; ww < 4; ++ww) v += sm[ww * (kWK * 32 + kWK * RC) + c * 32 + lane];
+    acc[c] = v;
+  }
   const int out = sw.out[it];
   double* __restrict__ dst = out >= 0 ? direct + (int64_t)(out + lane) * R + c0
                                       : partial + ((int64_t)(-out - 1) * 32 + lane) * R + c0;

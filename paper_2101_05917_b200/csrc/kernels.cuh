@@ -10,7 +10,7 @@
 namespace pdb {
 
 struct Stencil {
-  double dN[8][8][3];  // dN[q][a][j]
+  double m3[3];        // the three |dN_a/dX_j| magnitudes of the voxel stencil (see dNf)
   double fiber[3];
   double V;            // quadrature weight dx^3/8
   double w_m;          // muscle weight (0 = off)

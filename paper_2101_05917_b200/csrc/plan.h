@@ -60,7 +60,7 @@ struct HostPlan {
     std::vector<int32_t> red_src;      // partial row indices, summed in this order
     int64_t max_partial_rows = 0;
   } fw, bw;
-  int kc = 128;                        // max k-steps per item
+  int kc = 256;                        // max k-steps per item (4 warps x 64)
   // ---- contact candidates: ordered LAST as one root supernode ----
   int nc = 0;                        // number of candidate nodes (0 = no contact)
   int csup = -1;                     // index of the candidate supernode (= nsup - 1)
