@@ -73,6 +73,7 @@ struct pd_sim {
   double *fcur = nullptr, *fnew = nullptr, *alpha_ls = nullptr, *gtd = nullptr, *g2 = nullptr, *gn2 = nullptr,
          *inert = nullptr, *esum = nullptr, *dtmp = nullptr;
   int32_t *ls_act = nullptr, *ls_flag = nullptr;
+  double *lb_sg = nullptr, *lb_yr = nullptr, *lb_beta = nullptr, *lb_da = nullptr, *lb_db = nullptr, *lb_G = nullptr;
   double* traj = nullptr;
   int32_t *st_iters_f, *st_iters_a, *st_flag_f, *st_flag_a, *st_outer;
   double *st_res_f, *st_res_a;
@@ -351,6 +352,18 @@ int read_nactive(pd_sim* s) {
   return *s->h_nactive;
 }
 
+// out[j*B + b] = <u_b, V_j,b> for j < nv, V_j = Vbase + j * (3n B)   (deterministic, 2 launches)
+void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double* out) {
+  const int64_t n3 = 3LL * s->plan.n;
+  const int64_t chunk = dot_chunk(B);
+  const int nchunk = (int)((n3 + chunk - 1) / chunk);
+  const int bd = B * std::max(1, 256 / B);
+  k_mdot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk, s->partial);
+  LAUNCH_CHECK(s);
+  k_dot_final<<<nblk(nv * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, nv, out);
+  LAUNCH_CHECK(s);
+}
+
 // objective g (eq:opt) and its gradient at X: Gout = grad g (constrained rows 0), fout[b] = g
 void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const double* act_step, int64_t act_bs) {
   const HostPlan& P = s->plan;
@@ -435,25 +448,30 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     if (iter >= s->opt.max_iter_fwd) break;
     if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
     CK(cudaMemcpyAsync(s->g2, s->dots, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
-    // two-loop recursion: D = -H grad g
-    CK(cudaMemcpyAsync(s->Dv, s->G, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
-    for (int k = 0; k < hist; ++k) {
-      const int slot = ((iter - 1 - k) % m + m) % m;
-      dots(s, B, n3, {{LSs(slot), s->Dv}}, s->dtmp);
-      k_lbfgs_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, LYs(slot), s->rho_h + (int64_t)slot * B, s->dtmp,
-                                                     s->aj_h + (int64_t)slot * B, 0, len, B, s->active);
+    // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
+    if (hist > 0) {
+      mdot(s, B, s->G, s->LS, hist, s->lb_sg);
+      k_lbfgs_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, iter, B, s->active);
+      LAUNCH_CHECK(s);
+      k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
+                                                     s->active);  // q = g - sum alpha_j y_j
+      LAUNCH_CHECK(s);
+    } else {
+      CK(cudaMemcpyAsync(s->Dv, s->G, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    }
+    apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);  // r0 = H0 q = A^{-1} q
+    if (hist > 0) {
+      mdot(s, B, s->Dv, s->LY, hist, s->lb_yr);
+      k_lbfgs_beta<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, iter, B,
+                                                      s->active);
+      LAUNCH_CHECK(s);
+      k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,
+                                                     B, s->active);  // d = -(r0 + sum (alpha_j - beta_j) s_j)
+      LAUNCH_CHECK(s);
+    } else {
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
       LAUNCH_CHECK(s);
     }
-    apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);
-    for (int k = hist - 1; k >= 0; --k) {
-      const int slot = ((iter - 1 - k) % m + m) % m;
-      dots(s, B, n3, {{LYs(slot), s->Dv}}, s->dtmp);
-      k_lbfgs_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, LSs(slot), s->rho_h + (int64_t)slot * B, s->dtmp,
-                                                     s->aj_h + (int64_t)slot * B, 1, len, B, s->active);
-      LAUNCH_CHECK(s);
-    }
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
-    LAUNCH_CHECK(s);
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
     // Armijo backtracking from alpha = 1
     k_fill_double<<<nblk(B, 64), 64, 0, s->stream>>>(s->alpha_ls, 1.0, B);  // alpha = 1
@@ -476,10 +494,12 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     LAUNCH_CHECK(s);
     k_axpby<<<nblk(len), 256, 0, s->stream>>>(LYs(slot), s->Gn, 1.0, s->G, nullptr, -1.0, len, B, s->active);
     LAUNCH_CHECK(s);
-    dots(s, B, n3, {{LSs(slot), LYs(slot)}}, s->dtmp);
-    k_lbfgs_rho<<<nblk(B, 64), 64, 0, s->stream>>>(s->dtmp, s->rho_h + (int64_t)slot * B, s->active, B);
+    const int nv = std::min(hist + 1, m);  // valid slots after this store are [0, nv)
+    mdot(s, B, LSs(slot), s->LY, nv, s->lb_da);  // s_new^T y_j
+    mdot(s, B, LYs(slot), s->LS, nv, s->lb_db);  // y_new^T s_j
+    k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_db, slot, m, nv, B, s->active);
     LAUNCH_CHECK(s);
-    hist = std::min(hist + 1, m);
+    hist = nv;
     k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
     LAUNCH_CHECK(s);
     k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->G, s->Gn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
@@ -593,7 +613,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->dots = s->alloc<double>(3 * s->Bmax);
     for (int b = 1; b <= s->Bmax; ++b)
       s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
-    s->partial = s->alloc<double>(3 * s->max_partial_blocks + 64);
+    s->partial = s->alloc<double>(8 * s->max_partial_blocks + 64);
     s->active = s->alloc<int32_t>(s->Bmax);
     s->nactive = s->alloc<int32_t>(1);
     s->it_buf = s->alloc<int32_t>(s->Bmax);
@@ -622,6 +642,9 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       double** sc[] = {&s->fcur, &s->fnew, &s->alpha_ls, &s->gtd, &s->g2, &s->gn2, &s->inert, &s->esum, &s->dtmp};
       for (double** p : sc) *p = s->alloc<double>(s->Bmax);
       s->ls_act = s->alloc<int32_t>(s->Bmax);
+      double** lb[] = {&s->lb_sg, &s->lb_yr, &s->lb_beta, &s->lb_da, &s->lb_db};
+      for (double** p : lb) *p = s->alloc<double>((int64_t)s->nhist * s->Bmax);
+      s->lb_G = s->alloc<double>((int64_t)s->nhist * s->nhist * s->Bmax);
       s->ls_flag = s->alloc<int32_t>(s->Bmax);
     }
     if (P.nc > 0) {

@@ -1074,6 +1074,107 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
   rho[b] = sy[b] > 0.0 ? 1.0 / sy[b] : 0.0;
 }
 
+// ---- compact two-loop recursion (same iterates as the textbook two-loop, fewer passes)
+// With the Gram matrix Gm[i][j] = s_i^T y_j kept per sim, every coefficient of the two-loop
+// recursion follows from m dots with g (first loop) and m dots with r0 = A^{-1} q (second loop):
+//   alpha_i = rho_i (s_i^T g - sum_{j newer} alpha_j Gm[i][j]),  q = g - sum alpha_j y_j,
+//   beta_i  = rho_i (y_i^T r0 + sum_{j older} (alpha_j - beta_j) Gm[j][i]),
+//   d = -(r0 + sum_j (alpha_j - beta_j) s_j).
+
+// partial[(j*nchunk + c)*B + b] = sum over chunk c of u * V_j  (V_j = Vbase + j*vstride), j < nv
+__global__ void k_mdot_partial(const double* __restrict__ u, const double* __restrict__ Vbase, int64_t vstride,
+                               int nv, int64_t len, int B, int64_t chunk, double* __restrict__ partial) {
+  extern __shared__ double red[];
+  const int nb = blockDim.x;
+  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
+    const double ui = u[i];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nv) acc[j] += ui * Vbase[j * vstride + i];
+  }
+  const int J = nb / B;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= nv) break;
+    red[threadIdx.x] = acc[j];
+    __syncthreads();
+    for (int step = 1; step < J; step <<= 1) {
+      const int jj = threadIdx.x / B;
+      if ((jj % (2 * step)) == 0 && jj + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
+      __syncthreads();
+    }
+    if (threadIdx.x < B) partial[((int64_t)j * gridDim.x + blockIdx.x) * B + threadIdx.x] = red[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// slot of the k-th newest pair at iteration `iter` (ring of m)
+__device__ __forceinline__ int lb_slot(int iter, int k, int m) { return ((iter - 1 - k) % m + m) % m; }
+
+__global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __restrict__ Gm, const double* __restrict__ rho,
+                              double* __restrict__ alpha, int m, int hist, int iter, int B,
+                              const int32_t* __restrict__ active) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  for (int k = 0; k < hist; ++k) {
+    const int i = lb_slot(iter, k, m);
+    double t = sg[i * B + b];
+    for (int kk = 0; kk < k; ++kk) {
+      const int j = lb_slot(iter, kk, m);
+      t -= alpha[j * B + b] * Gm[(i * m + j) * B + b];
+    }
+    alpha[i * B + b] = rho[i * B + b] * t;
+  }
+}
+
+__global__ void k_lbfgs_beta(const double* __restrict__ yr, const double* __restrict__ Gm, const double* __restrict__ rho,
+                             const double* __restrict__ alpha, double* __restrict__ beta, int m, int hist, int iter,
+                             int B, const int32_t* __restrict__ active) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  for (int k = hist - 1; k >= 0; --k) {
+    const int i = lb_slot(iter, k, m);
+    double t = yr[i * B + b];
+    for (int kk = hist - 1; kk > k; --kk) {
+      const int j = lb_slot(iter, kk, m);
+      t += (alpha[j * B + b] - beta[j * B + b]) * Gm[(j * m + i) * B + b];
+    }
+    beta[i * B + b] = rho[i * B + b] * t;
+  }
+}
+
+// Y = sgn * (X + csgn * sum_{j < nv} (c1_j - c2_j) V_j) per sim (c2 may be null), masked by active
+__global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ X, double sgn, double csgn,
+                             const double* __restrict__ Vbase, int64_t vstride, const double* __restrict__ c1,
+                             const double* __restrict__ c2, int nv, int64_t len, int B,
+                             const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (active && !active[b]) return;
+  double v = X[i];
+  for (int j = 0; j < nv; ++j) v += csgn * (c1[j * B + b] - (c2 ? c2[j * B + b] : 0.0)) * Vbase[j * vstride + i];
+  Y[i] = sgn * v;
+}
+
+// new pair in slot sl: Gm[sl][j] = s_sl^T y_j (da[j]), Gm[j][sl] = s_j^T y_sl (db[j]); rho_sl
+__global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, const double* __restrict__ da,
+                             const double* __restrict__ db, int sl, int m, int nv, int B,
+                             const int32_t* __restrict__ active) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  for (int j = 0; j < nv; ++j) {
+    Gm[(sl * m + j) * B + b] = da[j * B + b];
+    Gm[(j * m + sl) * B + b] = db[j * B + b];
+  }
+  const double sy = da[sl * B + b];
+  rho[sl * B + b] = sy > 0.0 ? 1.0 / sy : 0.0;
+}
+
 // v[b] = c (per-sim scalar fill)
 __global__ void k_fill_double(double* __restrict__ v, double c, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;

@@ -210,9 +210,10 @@ def test_bitwise_determinism(torch):
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
 def _contact_parity(torch, name, accel_fwd=0, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for
-    # position agreement at the fp64 floor; the forward therefore runs to 1e-13.
+    # position agreement near the fp64 floor of the residual metric (~1e-14); the forward therefore
+    # runs to 2e-14 here (measured: tools/contact_diag.py).
     inp = make_inputs(get_config(name, **over))
-    sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd, tol_fwd=1e-13, max_iter_fwd=4000)
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd, tol_fwd=2e-14, max_iter_fwd=4000)
     gpu = _run_gpu(torch, inp, sim)
     sets = sim.contact_sets()
     assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
