@@ -573,7 +573,8 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 // order.  Single-item chunks write their output rows directly; split chunks and every forward W
 // item write partial rows that k_sweep_reduce adds in a fixed order into y / x (assign) or into z of
 // ancestors (subtract): deterministic, no atomics.
-constexpr int kWK = 64;  // k-steps per warp
+constexpr int kKS = 8;   // k-steps per pipeline stage
+constexpr int kPS = 4;   // pipeline stages per warp
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -583,88 +584,120 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int RC>
-constexpr int sweep_smem_bytes() { return 4 * (kWK * 32 + kWK * RC) * 8; }
+__host__ __device__ constexpr int sweep_warp_doubles() { return kPS * kKS * (32 + RC); }
+template <int RC>
+__host__ __device__ constexpr int sweep_smem_bytes() { return 4 * sweep_warp_doubles<RC>() * 8; }
 
+// Item = CTA of 4 warps; warp w takes k-steps [w*per, (w+1)*per) of the item and streams them through a
+// kPS-stage cp.async ring (kKS k-steps per stage: 32 factor doubles + RC right-hand-side doubles per
+// k).  Lane (rg, cg) = (lane % 8, lane / 8) keeps a 4-row x RC/4-column register tile.  The 4 warp
+// tiles are summed in warp order (deterministic).
 template <int RC, bool VEC>
 __global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int nitems, int R,
                                                      const double* __restrict__ zc, const double* __restrict__ zi,
                                                      const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                      double* __restrict__ partial) {
+  constexpr int CW = RC / 4;
+  constexpr int WD = sweep_warp_doubles<RC>();
   extern __shared__ __align__(16) double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = lane & 7, cg = lane >> 3;
   const int it = t0 + blockIdx.x;
   const int c0 = blockIdx.y * RC;
   const int rcn = min(RC, R - c0);
   const int nk = sw.nk[it];
   const int per = (nk + 3) >> 2;
-  const int kw0 = min(nk, w * per), kw1 = min(nk, kw0 + per), nkw = kw1 - kw0;
-  double* As = sm + w * (kWK * 32 + kWK * RC);
-  double* Zs = As + kWK * 32;
-  {
-    const double* Ag = sw.A + sw.a_off[it] + (int64_t)kw0 * 32;
-    for (int i = lane; i < nkw * 16; i += 32) cp_async16(As + 2 * i, Ag + 2 * i);
-    const int zr = sw.zrow[it];
-    const double* zsrc = zr >= 0 ? zc : zi;
-    const int32_t* idx = rows + sw.zidx[it] + kw0;
-    if (VEC) {
-      constexpr int H = RC / 2;
-      for (int i = lane; i < nkw * H; i += 32) {
-        const int k = i / H, c = 2 * (i - k * H);
-        const int row = zr >= 0 ? zr + kw0 + k : __ldg(idx + k);
-        if (c < rcn) cp_async16(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
-      }
-    } else {
-      for (int i = lane; i < nkw * RC; i += 32) {
-        const int k = i / RC, c = i - k * RC;
-        const int row = zr >= 0 ? zr + kw0 + k : __ldg(idx + k);
-        if (c < rcn) cp_async8(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
-        else Zs[k * RC + c] = 0.0;
+  const int kw0 = min(nk, w * per), nkw = min(nk, kw0 + per) - kw0;
+  double* buf = sm + w * WD;
+  const double* Ag = sw.A + sw.a_off[it] + (int64_t)kw0 * 32;
+  const int zr = sw.zrow[it];
+  const double* zsrc = zr >= 0 ? zc : zi;
+  const int32_t* idx = rows + sw.zidx[it] + kw0;
+  const int nst = (nkw + kKS - 1) / kKS;
+  auto issue = [&](int st) {
+    if (st < nst) {
+      double* As = buf + (st % kPS) * kKS * (32 + RC);
+      double* Zs = As + kKS * 32;
+      const int k0 = st * kKS, kn = min(kKS, nkw - k0);
+      for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + (int64_t)k0 * 32 + 2 * i);
+      if (VEC) {
+        constexpr int H = RC / 2;
+        for (int i = lane; i < kn * H; i += 32) {
+          const int k = i / H, c = 2 * (i - k * H);
+          const int row = zr >= 0 ? zr + kw0 + k0 + k : __ldg(idx + k0 + k);
+          if (c < rcn) cp_async16(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+          else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
+        }
+      } else {
+        for (int i = lane; i < kn * RC; i += 32) {
+          const int k = i / RC, c = i - k * RC;
+          const int row = zr >= 0 ? zr + kw0 + k0 + k : __ldg(idx + k0 + k);
+          if (c < rcn) cp_async8(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+          else Zs[k * RC + c] = 0.0;
+        }
       }
     }
-    cp_async_wait_all();
+    cp_async_commit();
+  };
+  double acc[4][CW];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+#pragma unroll
+  for (int st = 0; st < kPS - 1; ++st) issue(st);
+  for (int st = 0; st < nst; ++st) {
+    issue(st + kPS - 1);
+    cp_async_wait_group<kPS - 1>();
+    __syncwarp();
+    const double* As = buf + (st % kPS) * kKS * (32 + RC);
+    const double* Zs = As + kKS * 32;
+    const int kn = min(kKS, nkw - st * kKS);
+    for (int k = 0; k < kn; ++k) {
+      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
+      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      double zv[CW];
+      if (CW % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < CW / 2; ++c) {
+          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
+          zv[2 * c] = t.x;
+          zv[2 * c + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+    }
     __syncwarp();
   }
-  double acc[RC];
-#pragma unroll
-  for (int c = 0; c < RC; ++c) acc[c] = 0.0;
-  for (int k = 0; k < nkw; ++k) {
-    const double a = As[k * 32 + lane];
-    if (VEC) {
-      const double2* z2 = reinterpret_cast<const double2*>(Zs + k * RC);
-#pragma unroll
-      for (int c = 0; c < RC / 2; ++c) {
-        const double2 v = z2[c];
-        acc[2 * c] = fma(a, v.x, acc[2 * c]);
-        acc[2 * c + 1] = fma(a, v.y, acc[2 * c + 1]);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < RC; ++c) acc[c] = fma(a, Zs[k * RC + c], acc[c]);
-    }
-  }
-  // fixed-order sum of the 4 warp partials (warp w's slot reuses its own A staging area)
+  cp_async_wait_group<0>();
   __syncthreads();
-  double* red = sm + w * (kWK * 32 + kWK * RC);
+  // warp tiles -> shared [w][32][RC]; then fixed-order sum over w and coalesced store
 #pragma unroll
-  for (int c = 0; c < RC; ++c) red[c * 32 + lane] = acc[c];
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < CW; ++c) buf[(4 * rg + r) * RC + cg * CW + c] = acc[r][c];
   __syncthreads();
-  if (w != 0 || lane >= sw.nvalid[it]) return;
-#pragma unroll
-  for (int c = 0; c < RC; ++c) {
-    double v = sm[c * 32 + lane];
-#pragma unroll
-    for (int ww = 1; ww < 4; ++ww) v += sm[ww * (kWK * 32 + kWK * RC) + c * 32 + lane];
-    acc[c] = v;
-  }
+  const int nv = sw.nvalid[it];
   const int out = sw.out[it];
-  double* __restrict__ dst = out >= 0 ? direct + (int64_t)(out + lane) * R + c0
-                                      : partial + ((int64_t)(-out - 1) * 32 + lane) * R + c0;
-#pragma unroll
-  for (int c = 0; c < RC; ++c)
-    if (c < rcn) dst[c] = acc[c];
+  double* __restrict__ dst = out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
+  for (int e = threadIdx.x; e < nv * RC; e += 128) {
+    const int r = e / RC, c = e - r * RC;
+    if (c >= rcn) continue;
+    const double v = ((sm[e] + sm[WD + e]) + sm[2 * WD + e]) + sm[3 * WD + e];
+    dst[(int64_t)r * R + c] = v;
+  }
 }
 
 __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
