@@ -172,7 +172,7 @@ def main_ours(args):
     B, N = inp["B"], 3 * inp["n_nodes"]
     t_setup = time.perf_counter()
     sim = pdb.simulator_from_inputs(inp, tol_fwd=cfg.tol, tol_adj=cfg.tol, max_steps=T, profile=1,
-                                    check_every=1)
+                                    check_every=1, accel_fwd=1, outer_warm=1)
     setup_s = time.perf_counter() - t_setup
     info = sim.info()
     D = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
@@ -278,10 +278,7 @@ def main_ours(args):
         e2e = dict(value=units / (e2e_ms / args.steps / 1e3), unit=UNIT, h2d_bytes_per_step=h2d,
                    d2h_bytes_per_step=d2h)
 
-    # ---------------- roofline of the dominant kernel family (live CUDA events)
-    fam = max(prof, key=lambda k: prof[k][0])
-    ms_tot, cnt = prof[fam]
-    avg_s = ms_tot / max(cnt, 1) / 1e3
+    # ---------------- rooflines (live CUDA events per kernel family, pd_profile)
     nfree = info["n_free_nodes"]
     R = 3 * B
     peaks = {}
@@ -290,27 +287,38 @@ def main_ours(args):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    ncu = {}
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(cfg.name, {}).get(fam)
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(cfg.name, {})
     except Exception:
         pass
-    if fam == "solve_K3":
-        # factor read twice (L then L^T) + solve vectors (rhs, y, t, x) + permutation in/out
-        alg_bytes = 2 * info["nnz_L"] * 8 + 4 * nfree * R * 8 + 2 * N * B * 8
-        roof = dict(bound="hbm", achieved=alg_bytes / avg_s / 1e9, peak=hbm_peak, unit="GB/s",
-                    frac=alg_bytes / avg_s / 1e9 / hbm_peak, traffic=traffic, kernel=fam,
-                    algorithmic_bytes_per_launch=alg_bytes, avg_launch_ms=avg_s * 1e3,
-                    peak_source="MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback")
-    else:
-        # K1/K4: per-quad-point algorithmic fp64 flops
-        per_qp = {"local_K1": 1500, "AN_K4": 1900, "gather_K2": 0, "param": 1300}.get(fam, 0)
+
+    def roof_of(fam):
+        ms_tot, cnt = prof.get(fam, (0.0, 0))
+        if not cnt:
+            return None
+        avg_s = ms_tot / cnt / 1e3
+        if fam == "solve_K3":
+            # the scalar factor L_s streamed once per sweep (2 nnz(L_s) 8 B) + the solve vectors
+            # (rhs in, y out+in, x out: 4 nfree R 8 B) + layout permutation in/out (2 3n B 8 B)
+            alg = 2 * info["nnz_L"] * 8 + 4 * nfree * R * 8 + 2 * N * B * 8
+            return dict(bound="hbm", achieved=alg / avg_s / 1e9, peak=hbm_peak, unit="GB/s",
+                        frac=alg / avg_s / 1e9 / hbm_peak, traffic=ncu.get("solve_K3_dram_bytes"), kernel=fam,
+                        algorithmic_bytes_per_launch=alg, avg_launch_ms=avg_s * 1e3,
+                        peak_source="MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650")
+        # element kernels: fp64 flops per quadrature point (DESIGN.md §5 operation count; ncu-measured when
+        # profiles/ncu_traffic.json has it)
+        per_qp = ncu.get(fam + "_flops_per_qp", {"local_K1": 950, "AN_K4": 420, "param": 700}.get(fam))
+        if per_qp is None:
+            return None
         flops = per_qp * 8 * inp["n_elems"] * B
         ach = flops / avg_s / 1e12
-        roof = dict(bound="alu", achieved=ach, peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=ach / FP64_PEAK_TFLOPS,
-                    traffic=traffic, kernel=fam, avg_launch_ms=avg_s * 1e3,
-                    peak_source="derived fp64 FMA-pipe peak (DESIGN.md §5)")
+        return dict(bound="alu", achieved=ach, peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=ach / FP64_PEAK_TFLOPS,
+                    traffic=ncu.get(fam + "_dram_bytes"), kernel=fam, flops_per_qp=per_qp, avg_launch_ms=avg_s * 1e3,
+                    peak_source="derived fp64 pipe peak: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §5)")
+
+    fam = max(prof, key=lambda k: prof[k][0])
+    roof = roof_of(fam) or roof_of("solve_K3")
     share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
 
     line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=max(3, args.warmup),
@@ -320,6 +328,7 @@ def main_ours(args):
                             grid=list(cfg.counts), l2="flushed (256 MB write) before every timed iteration",
                             parallelism=f"batch-sharded x{ws} (weak)"),
                 e2e=e2e, gpu_launches=launches, roofline=roof,
+                roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
                 kernel_share=share,
                 iters=dict(fwd_mean=float(np.mean(stats["fwd"]["iters_fwd"])),
                            adj_mean=float(np.mean(stats["bwd"]["iters_adj"])),

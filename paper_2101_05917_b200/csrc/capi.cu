@@ -48,11 +48,12 @@ struct pd_sim {
   uint8_t* d_fixed = nullptr;
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
+  int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
   double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
-  double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR;
+  double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR, *JC;
   double *w_sim, *youngs_sim, *dots, *partial, *alpha, *beta, *rz, *bb, *dw_acc, *act;
   int32_t *active, *nactive, *it_buf, *flag_buf;
   double* res_buf;
@@ -215,8 +216,15 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const HostPlan& P = s->plan;
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
-  CK(cudaFuncSetAttribute(k_sweep_items<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
-  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd) {
+  if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
+  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
+  // one resident wave: warps take items round-robin, so CTAs beyond residency would only add a tail
+  int per_sm = 0, nsm = 0, dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, sweep_smem_bytes<RC>()));
+  const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
+  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, int32_t* cnt, bool fwd) {
     for (int j = 0; j < P.nlevels; ++j) {
       const int t0 = S.lvl_item[j], nt = S.lvl_item[j + 1] - t0;
       const bool fix = !fwd && s->pins_live && j == 0;  // backward level 0 = the root = the candidate block
@@ -224,15 +232,11 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
       if (fix)
         CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
       if (nt) {
-        // forward: sources z (S0), direct y (S2); backward: D part y (S2), W part x (S0), direct x (S0)
-        k_sweep_items<RC, VEC><<<dim3(nt, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
-            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->Spart);
-        LAUNCH_CHECK(s);
-      }
-      const int r0 = S.lvl_red[j], nr = S.lvl_red[j + 1] - r0;
-      if (nr) {
-        k_sweep_reduce<<<nblk((int64_t)nr * R), 256, 0, s->stream>>>(d, r0, nr, R, s->Spart, fwd ? s->S2 : s->S0,
-                                                                      s->S0);
+        // forward: sources z (S0), direct y (S2), group subtract into z (S0);
+        // backward: D part y (S2), W part x (S0), direct x (S0)
+        const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
+        k_sweep_level<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
+            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, cnt);
         LAUNCH_CHECK(s);
       }
       if (fix) {
@@ -242,8 +246,8 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
       }
     }
   };
-  sweep(P.fw, s->swf, true);
-  sweep(P.bw, s->swb, false);
+  sweep(P.fw, s->swf, s->cnt_f, true);
+  sweep(P.bw, s->swb, s->cnt_b, false);
 }
 void solve_launch(pd_sim* s, int B) {
   const int R = 3 * B;
@@ -316,13 +320,17 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   LAUNCH_CHECK(s);
 }
 
-// OUT = A_N(X) Pin, zero on constrained DoFs
+// OUT = A_N(X) Pin, zero on constrained DoFs.  jc: per-step Jacobian cache of X (k_elem_jac) or null.
 void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT, const double* act_step,
-              int64_t act_bstride) {
+              int64_t act_bstride, const double* jc = nullptr) {
   const HostPlan& P = s->plan;
   ProfScope ps(s, 3);
-  k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st, elem_args(s, B, act_step, act_bstride),
-                                                                 s->EF);
+  if (jc)
+    k_elem_AN_cached<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(
+        Pin, s->st, elem_args(s, B, act_step, act_bstride), jc, s->EF);
+  else
+    k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st,
+                                                                   elem_args(s, B, act_step, act_bstride), s->EF);
   LAUNCH_CHECK(s);
   const bool pin = s->pins_live;
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
@@ -588,11 +596,24 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.zrow = s->upload(S.zrow);
       d.out = s->upload(S.out);
       d.nvalid = s->upload(S.nvalid);
+      d.ig_ptr = s->upload(S.ig_ptr);
+      d.ig = s->upload(S.ig);
+      d.g_tptr = s->upload(S.g_tptr);
+      d.g_cnt = s->upload(S.g_cnt);
       d.red_row = s->upload(S.red_row);
       d.red_mode = s->upload(S.red_mode);
       d.red_ptr = s->upload(S.red_ptr);
       d.red_src = s->upload(S.red_src);
     };
+    // group countdown counters, one slot per column chunk, armed with the group's item count
+    auto up_cnt = [&](const HostPlan::Sweep& S) {
+      std::vector<int32_t> c(S.g_cnt.size() * kGY);
+      for (size_t g = 0; g < S.g_cnt.size(); ++g)
+        for (int y = 0; y < kGY; ++y) c[g * kGY + y] = S.g_cnt[g];
+      return s->upload(c);
+    };
+    s->cnt_f = up_cnt(P.fw);
+    s->cnt_b = up_cnt(P.bw);
     up_sweep(P.fw, s->swf);
     up_sweep(P.bw, s->swb);
     s->Spart = s->alloc<double>((std::max(P.fw.max_partial_rows, P.bw.max_partial_rows) + 32) * 3 * s->Bmax);
@@ -605,6 +626,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->S1 = s->alloc<double>(sB);
     s->S2 = s->alloc<double>(sB);
     s->EF = s->alloc<double>((int64_t)P.m * 24 * s->Bmax);
+    s->JC = s->alloc<double>((int64_t)P.m * 8 * s->Bmax * (s->w_m != 0.0 ? kJC : 15));
     s->EE = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DW = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DR = s->alloc<double>((int64_t)P.m * s->Bmax);
@@ -915,6 +937,12 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
         s->pins_live = true;
         build_Q(s, B, nullptr);
       }
+      {  // per-step Jacobian data of the projections at x_{i+1}, reused by every K4 product
+        ProfScope ps(s, 3);
+        k_elem_jac<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->st, elem_args(s, B, act_i, act_bs),
+                                                                         s->JC);
+        LAUNCH_CHECK(s);
+      }
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
       LAUNCH_CHECK(s);
       zero_constrained(s, s->Bv, B);
@@ -939,7 +967,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
         if (iter >= s->opt.max_iter_adj) break;
         if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
         if (pcg) {
-          apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs);
+          apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs, s->JC);
           zero_constrained(s, s->Q, B);
           dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
           k_pcg_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->rz, s->dots + B, s->alpha, s->active, B);
@@ -957,7 +985,7 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
         } else {
           // fixed point u <- u + A^{-1}(b - A_N u) == A^{-1}(b + dA u)  (eq:bp_update)
           apply_Ainv(s, B, s->Rv, s->U, nullptr, 1.0, 1.0, s->active);
-          apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs);
+          apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs, s->JC);
           zero_constrained(s, s->Q, B);
           k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
           LAUNCH_CHECK(s);

@@ -121,16 +121,12 @@ __device__ void polar_svd_fallback(const double* F, double* R) {
     for (int j = 0; j < 3; ++j) R[3 * i + j] = u[0][i] * V[3 * j] + u[1][i] * V[3 * j + 1] + u[2][i] * V[3 * j + 2];
 }
 
-// R = rotation of the polar decomposition F = R S.  Scaled Newton iteration
-// X <- (g X + X^{-T}/g)/2 (Frobenius scaling) for det F > 0; SVD path otherwise.
-__device__ void polar_rotation(const double* F, double* R) {
-  const double d0 = det3(F);
-  double fn2 = 0;
-  for (int i = 0; i < 9; ++i) fn2 += F[i] * F[i];
-  if (!(d0 > 1e-6 * fn2 * sqrt(fn2))) {
-    polar_svd_fallback(F, R);
-    return;
-  }
+// R = rotation of the polar decomposition F = R S, det F > 0: Newton-Schulz iteration
+// X <- X (3I - X^T X)/2 on X0 = F sqrt(3)/||F||_F (all singular values in (0, sqrt3), quadratic
+// convergence, no divisions); stops after the step taken with ||X^T X - I||_F < 1e-8 (the next error is
+// below fp64 resolution).  Falls back to the scaled Newton iteration X <- (g X + X^{-T}/g)/2 if it is
+// slow (strongly anisotropic F), and to the SVD path for det F <= 1e-6 ||F||^3.
+__device__ void polar_newton(const double* F, double* R) {
   double X[9];
   for (int i = 0; i < 9; ++i) X[i] = F[i];
   bool scaled = true, last = false;
@@ -153,12 +149,52 @@ __device__ void polar_rotation(const double* F, double* R) {
       X[i] = xn;
     }
     if (diff < 1e-4 * nrm) scaled = false;
-    // quadratic convergence: once the (unscaled) step is below 1e-9 the next one is below
-    // fp64 resolution — take exactly one more step and stop.
     if (last) break;
     if (!scaled && diff < 1e-18 * nrm) last = true;
   }
   for (int i = 0; i < 9; ++i) R[i] = X[i];
+}
+
+__device__ void polar_rotation(const double* F, double* R) {
+  const double d0 = det3(F);
+  double fn2 = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) fn2 += F[i] * F[i];
+  if (!(d0 > 1e-6 * fn2 * sqrt(fn2))) {
+    polar_svd_fallback(F, R);
+    return;
+  }
+  const double c = sqrt(3.0 / fn2);
+  double X[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) X[i] = c * F[i];
+  for (int it = 0; it < 14; ++it) {
+    // C = X^T X (symmetric), delta = ||C - I||_F^2
+    const double c00 = X[0] * X[0] + X[3] * X[3] + X[6] * X[6];
+    const double c11 = X[1] * X[1] + X[4] * X[4] + X[7] * X[7];
+    const double c22 = X[2] * X[2] + X[5] * X[5] + X[8] * X[8];
+    const double c01 = X[0] * X[1] + X[3] * X[4] + X[6] * X[7];
+    const double c02 = X[0] * X[2] + X[3] * X[5] + X[6] * X[8];
+    const double c12 = X[1] * X[2] + X[4] * X[5] + X[7] * X[8];
+    const double d = (c00 - 1) * (c00 - 1) + (c11 - 1) * (c11 - 1) + (c22 - 1) * (c22 - 1) +
+                     2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
+    // Y = (3I - C)/2 ; X <- X Y
+    const double y00 = 1.5 - 0.5 * c00, y11 = 1.5 - 0.5 * c11, y22 = 1.5 - 0.5 * c22;
+    const double y01 = -0.5 * c01, y02 = -0.5 * c02, y12 = -0.5 * c12;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double a0 = X[3 * i], a1 = X[3 * i + 1], a2 = X[3 * i + 2];
+      X[3 * i] = a0 * y00 + a1 * y01 + a2 * y02;
+      X[3 * i + 1] = a0 * y01 + a1 * y11 + a2 * y12;
+      X[3 * i + 2] = a0 * y02 + a1 * y12 + a2 * y22;
+    }
+    if (d < 1e-16) {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = X[i];
+      return;
+    }
+  }
+  polar_newton(F, R);
 }
 
 // ----------------------------------------------------------------- layout kernels
@@ -338,7 +374,10 @@ __global__ void k_elem_rotations(const double* __restrict__ X, Stencil st, const
 // ----------------------------------------------------------------- K4: A_N p (matrix-free)
 // dR[dF] = R [w]x with (tr S I - S) w = vee(R^T dF - dF^T R), eigenvalues floored at
 // clamp * max|eig S|; muscle dp = (r/||Fm||)(I - n n^T) dFm.
-__device__ void solve_rot_derivative(const double* S, const double* rhs, double clamp, double* om) {
+// Mi = (tr S I - S)^{-1} (symmetric; stored xx, xy, xz, yy, yz, zz), eigenvalues floored at
+// clamp * max|eig S|.  Fast path: Cholesky positivity test of (M - floor I), then the
+// cofactor inverse; clamped path: Jacobi eigen-decomposition.
+__device__ void rot_derivative_matrix(const double* S, double clamp, double* Mi) {
   double tr = S[0] + S[4] + S[8];
   double M[9];
   for (int i = 0; i < 9; ++i) M[i] = -S[i];
@@ -346,10 +385,9 @@ __device__ void solve_rot_derivative(const double* S, const double* rhs, double 
   double sn = 0;
   for (int i = 0; i < 9; ++i) sn += S[i] * S[i];
   const double fub = clamp * sqrt(sn);  // >= clamp * max|eig S|
-  // fast path: Cholesky of M - fub I succeeds => no eigenvalue below the floor
   const double a00 = M[0] - fub, a11 = M[4] - fub, a22 = M[8] - fub;
   bool fast = a00 > 0;
-  double l10 = 0, l20 = 0, l11 = 0, l21 = 0, l22 = 0;
+  double l10 = 0, l20 = 0, l11 = 0, l21 = 0;
   if (fast) {
     const double l00 = sqrt(a00);
     l10 = M[3] / l00; l20 = M[6] / l00;
@@ -363,40 +401,27 @@ __device__ void solve_rot_derivative(const double* S, const double* rhs, double 
   }
   if (fast) {
     double C[9];
-    cof3(M, C);  // M symmetric: M^{-1} = C^T / det = C / det
+    cof3(M, C);  // M symmetric: M^{-1} = C / det
     const double idet = 1.0 / (M[0] * C[0] + M[1] * C[1] + M[2] * C[2]);
-    for (int i = 0; i < 3; ++i) om[i] = (C[3 * i] * rhs[0] + C[3 * i + 1] * rhs[1] + C[3 * i + 2] * rhs[2]) * idet;
+    Mi[0] = C[0] * idet; Mi[1] = C[1] * idet; Mi[2] = C[2] * idet;
+    Mi[3] = C[4] * idet; Mi[4] = C[5] * idet; Mi[5] = C[8] * idet;
     return;
   }
   double lam[3], V[9];
   jacobi_eig3(S, lam, V);
   const double mx = fmax(fabs(lam[0]), fmax(fabs(lam[1]), fabs(lam[2])));
   const double floor_ = clamp * mx;
-  double t[3];
-  for (int k = 0; k < 3; ++k) t[k] = V[k] * rhs[0] + V[3 + k] * rhs[1] + V[6 + k] * rhs[2];
-  for (int k = 0; k < 3; ++k) {
-    const double ev = fmax(tr - lam[k], floor_);
-    t[k] /= ev;
+  double iv[3];
+  for (int k = 0; k < 3; ++k) iv[k] = 1.0 / fmax(tr - lam[k], floor_);
+  const int pr[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  for (int t = 0; t < 6; ++t) {
+    const int i = pr[t][0], j = pr[t][1];
+    Mi[t] = V[3 * i] * iv[0] * V[3 * j] + V[3 * i + 1] * iv[1] * V[3 * j + 1] + V[3 * i + 2] * iv[2] * V[3 * j + 2];
   }
-  for (int i = 0; i < 3; ++i) om[i] = V[3 * i] * t[0] + V[3 * i + 1] * t[1] + V[3 * i + 2] * t[2];
 }
 
-__global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
-                                                 Stencil st, ElemArgs ea, double* __restrict__ EF) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int B = ea.B;
-  const int64_t pair = tid >> 3;
-  const int q = (int)(tid & 7);
-  const bool live = pair < (int64_t)ea.m * B;
-  const int64_t pr = live ? pair : 0;
-  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
-  const double w = ea.w_sim[b];
-  double F[9], dF[9];
-  load_F(X, ea.hex8, st, e, b, q, B, F);
-  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
-  double R[9];
-  polar_rotation(F, R);
-  double S[9];  // S = R^T F, symmetrised
+// S = sym(R^T F)
+__device__ __forceinline__ void sym_stretch(const double* R, const double* F, double* S) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -408,48 +433,143 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
       const double avg = 0.5 * (S[3 * i + j] + S[3 * j + i]);
       S[3 * i + j] = S[3 * j + i] = avg;
     }
+}
+
+// Pm = w V (dF - dR[dF]) (+ muscle w_m V (dFm - s (dFm - (n.dFm) n)) m^T): the projection-derivative
+// term of A_N p, dR = R [om]x, om = Mi vee(R^T dF - dF^T R).
+__device__ __forceinline__ void an_stress(const double* R, const double* Mi, const double* dF, double wv,
+                                          const Stencil& st, bool mus, const double* nh, double sc, double* Pm) {
   double Wm[9];  // R^T dF
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) Wm[3 * i + j] = R[i] * dF[j] + R[3 + i] * dF[3 + j] + R[6 + i] * dF[6 + j];
-  // vee(W - W^T) = (W21 - W12, W02 - W20, W10 - W01)
-  const double rhs[3] = {Wm[7] - Wm[5], Wm[2] - Wm[6], Wm[3] - Wm[1]};
-  double om[3];
-  solve_rot_derivative(S, rhs, st.clamp, om);
-  // dR = R [om]x ; [om]x = [[0,-o2,o1],[o2,0,-o0],[-o1,o0,0]]
-  double Pm[9];
+  const double r0 = Wm[7] - Wm[5], r1 = Wm[2] - Wm[6], r2 = Wm[3] - Wm[1];
+  const double om0 = Mi[0] * r0 + Mi[1] * r1 + Mi[2] * r2;
+  const double om1 = Mi[1] * r0 + Mi[3] * r1 + Mi[4] * r2;
+  const double om2 = Mi[2] * r0 + Mi[4] * r1 + Mi[5] * r2;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const double r0 = R[3 * i], r1 = R[3 * i + 1], r2 = R[3 * i + 2];
-    const double dR0 = r1 * om[2] - r2 * om[1];
-    const double dR1 = -r0 * om[2] + r2 * om[0];
-    const double dR2 = r0 * om[1] - r1 * om[0];
-    Pm[3 * i] = w * st.V * (dF[3 * i] - dR0);
-    Pm[3 * i + 1] = w * st.V * (dF[3 * i + 1] - dR1);
-    Pm[3 * i + 2] = w * st.V * (dF[3 * i + 2] - dR2);
+    const double a0 = R[3 * i], a1 = R[3 * i + 1], a2 = R[3 * i + 2];
+    Pm[3 * i] = wv * (dF[3 * i] - (a1 * om2 - a2 * om1));
+    Pm[3 * i + 1] = wv * (dF[3 * i + 1] - (-a0 * om2 + a2 * om0));
+    Pm[3 * i + 2] = wv * (dF[3 * i + 2] - (a0 * om1 - a1 * om0));
   }
-  if (st.w_m != 0.0) {
-    const double r_act = ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
-    double Fm[3], dFm[3], nr = 0;
+  if (mus) {
+    double dFm[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+    const double nd = nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2];
+    const double wm = st.w_m * st.V;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-      dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
-      nr += Fm[i] * Fm[i];
+      const double jd = sc * (dFm[i] - nd * nh[i]);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += wm * (dFm[i] - jd) * st.fiber[j];
     }
-    nr = sqrt(nr);
-    double jd[3] = {0, 0, 0};
-    if (nr > 0) {
-      const double nd = (Fm[0] * dFm[0] + Fm[1] * dFm[1] + Fm[2] * dFm[2]) / nr;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) jd[i] = r_act / nr * (dFm[i] - nd * Fm[i] / nr);
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * (dFm[i] - jd[i]) * st.fiber[j];
   }
+}
+
+// muscle data at F: n = Fm/||Fm||, sc = r/||Fm|| (0 if ||Fm|| = 0)
+__device__ __forceinline__ void muscle_dir(const double* F, const Stencil& st, double r_act, double* nh, double& sc) {
+  double Fm[3], nr = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+    nr += Fm[i] * Fm[i];
+  }
+  nr = sqrt(nr);
+  if (nr > 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) nh[i] = Fm[i] / nr;
+    sc = r_act / nr;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) nh[i] = st.fiber[i];
+    sc = 0.0;
+  }
+}
+
+constexpr int kJC = 19;  // cached doubles per quad point: R (9), Mi (6), n (3), sc (1)
+
+// Per-step Jacobian data at x_{i+1} ("needs to be done only once per time step"), SoA:
+// JC[k * nq + tid], tid = (e*B + b)*8 + q.
+__global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, Stencil st, ElemArgs ea,
+                                                  double* __restrict__ JC) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nq = (int64_t)ea.m * ea.B * 8;
+  if (tid >= nq) return;
+  const int B = ea.B;
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const int e = (int)(pair / B), b = (int)(pair - (int64_t)e * B);
+  double F[9], R[9], S[9], Mi[6];
+  load_F(X, ea.hex8, st, e, b, q, B, F);
+  polar_rotation(F, R);
+  sym_stretch(R, F, S);
+  rot_derivative_matrix(S, st.clamp, Mi);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) JC[k * nq + tid] = R[k];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) JC[(9 + k) * nq + tid] = Mi[k];
+  if (st.w_m != 0.0) {
+    double nh[3], sc;
+    muscle_dir(F, st, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) JC[(15 + k) * nq + tid] = nh[k];
+    JC[18 * nq + tid] = sc;
+  }
+}
+
+// K4 with cached Jacobian data: A_N p element term from dF = G_q p_e only (no polar per product).
+__global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict__ Pv, Stencil st, ElemArgs ea,
+                                                        const double* __restrict__ JC, double* __restrict__ EF) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  const int64_t nq = (int64_t)ea.m * B * 8;
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const bool live = pair < (int64_t)ea.m * B;
+  const int64_t pr = live ? pair : 0;
+  const int64_t t = live ? tid : q;
+  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
+  double dF[9], R[9], Mi[6], nh[3] = {0, 0, 0}, sc = 0;
+  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(JC + k * nq + t);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) Mi[k] = __ldg(JC + (9 + k) * nq + t);
+  const bool mus = st.w_m != 0.0;
+  if (mus) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nh[k] = __ldg(JC + (15 + k) * nq + t);
+    sc = __ldg(JC + 18 * nq + t);
+  }
+  double Pm[9];
+  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
+  __shared__ double Psm[32][73];
+  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
+}
+
+__global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
+                                                 Stencil st, ElemArgs ea, double* __restrict__ EF) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const bool live = pair < (int64_t)ea.m * B;
+  const int64_t pr = live ? pair : 0;
+  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
+  double F[9], dF[9], R[9], S[9], Mi[6], nh[3] = {0, 0, 0}, sc = 0;
+  load_F(X, ea.hex8, st, e, b, q, B, F);
+  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
+  polar_rotation(F, R);
+  sym_stretch(R, F, S);
+  rot_derivative_matrix(S, st.clamp, Mi);
+  const bool mus = st.w_m != 0.0;
+  if (mus) muscle_dir(F, st, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
+  double Pm[9];
+  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
   __shared__ double Psm[32][73];
   store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
@@ -571,7 +691,7 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 // [pos][R] solve layout) into shared memory with cp.async — everything in flight at once — then
 // accumulates RC columns per lane with broadcast shared loads; the 4 warp sums are added in warp
 // order.  Single-item chunks write their output rows directly; split chunks and every forward W
-// item write partial rows that k_sweep_reduce adds in a fixed order into y / x (assign) or into z of
+// item write partial rows that the group's last item adds in a fixed order into y / x (assign) or into z of
 // ancestors (subtract): deterministic, no atomics.
 constexpr int kKS = 8;   // k-steps per pipeline stage
 constexpr int kPS = 4;   // pipeline stages per warp
@@ -593,56 +713,67 @@ __host__ __device__ constexpr int sweep_warp_doubles() { return kPS * kKS * (32 
 template <int RC>
 __host__ __device__ constexpr int sweep_smem_bytes() { return 4 * sweep_warp_doubles<RC>() * 8; }
 
-// Item = CTA of 4 warps; warp w takes k-steps [w*per, (w+1)*per) of the item and streams them through a
-// kPS-stage cp.async ring (kKS k-steps per stage: 32 factor doubles + RC right-hand-side doubles per
-// k).  Lane (rg, cg) = (lane % 8, lane / 8) keeps a 4-row x RC/4-column register tile.  The 4 warp
-// tiles are summed in warp order (deterministic).
+// One launch per level (K3 v4).  Every warp walks its items gw, gw + W, gw + 2W, ... (W = warps in the
+// grid) through a kPS-stage cp.async ring that runs across item boundaries (kKS k-steps per stage: 32
+// factor doubles + RC right-hand-side doubles per k).  Lane (rg, cg) = (lane % 8, lane / 8) keeps a
+// 4-row x RC/4-column register tile.  A finished item writes its output rows directly or, for shared
+// outputs, partial rows; it then counts down each reduction group it feeds, and the warp that brings a
+// group to zero sums the group's partial rows in their fixed order into the targets (and re-arms the
+// counter).  Deterministic: the arithmetic of every item and every sum is independent of scheduling.
+constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group
+
 template <int RC, bool VEC>
-__global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int nitems, int R,
+__global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                      const double* __restrict__ zc, const double* __restrict__ zi,
                                                      const int32_t* __restrict__ rows, double* __restrict__ direct,
-                                                     double* __restrict__ partial) {
+                                                     double* __restrict__ zsub, double* __restrict__ partial,
+                                                     int32_t* __restrict__ cnt) {
   constexpr int CW = RC / 4;
-  constexpr int WD = sweep_warp_doubles<RC>();
+  constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = lane & 7, cg = lane >> 3;
-  const int it = t0 + blockIdx.x;
+  const int gw = blockIdx.x * 4 + w, W = gridDim.x * 4;
   const int c0 = blockIdx.y * RC;
   const int rcn = min(RC, R - c0);
-  const int nk = sw.nk[it];
-  const int per = (nk + 3) >> 2;
-  const int kw0 = min(nk, w * per), nkw = min(nk, kw0 + per) - kw0;
-  double* buf = sm + w * WD;
-  const double* Ag = sw.A + sw.a_off[it] + (int64_t)kw0 * 32;
-  const int zr = sw.zrow[it];
-  const double* zsrc = zr >= 0 ? zc : zi;
-  const int32_t* idx = rows + sw.zidx[it] + kw0;
-  const int nst = (nkw + kKS - 1) / kKS;
-  auto issue = [&](int st) {
-    if (st < nst) {
-      double* As = buf + (st % kPS) * kKS * (32 + RC);
+  double* buf = sm + w * kPS * SD;
+  int ij = gw, ik = 0, is = 0;  // issue cursor: item, k offset, stage count
+  auto issue = [&]() {
+    if (ij < nitems) {
+      const int it = t0 + ij;
+      const int nk = sw.nk[it];
+      const int kn = min(kKS, nk - ik);
+      double* As = buf + (is % kPS) * SD;
       double* Zs = As + kKS * 32;
-      const int k0 = st * kKS, kn = min(kKS, nkw - k0);
-      for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + (int64_t)k0 * 32 + 2 * i);
+      const double* Ag = sw.A + sw.a_off[it] + (int64_t)ik * 32;
+      for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + 2 * i);
+      const int zr = sw.zrow[it];
+      const double* zsrc = zr >= 0 ? zc : zi;
+      const int32_t* idx = rows + sw.zidx[it] + ik;
       if (VEC) {
         constexpr int H = RC / 2;
         for (int i = lane; i < kn * H; i += 32) {
           const int k = i / H, c = 2 * (i - k * H);
-          const int row = zr >= 0 ? zr + kw0 + k0 + k : __ldg(idx + k0 + k);
+          const int row = zr >= 0 ? zr + ik + k : __ldg(idx + k);
           if (c < rcn) cp_async16(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
           else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
         }
       } else {
         for (int i = lane; i < kn * RC; i += 32) {
           const int k = i / RC, c = i - k * RC;
-          const int row = zr >= 0 ? zr + kw0 + k0 + k : __ldg(idx + k0 + k);
+          const int row = zr >= 0 ? zr + ik + k : __ldg(idx + k);
           if (c < rcn) cp_async8(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
           else Zs[k * RC + c] = 0.0;
         }
       }
+      ik += kn;
+      if (ik >= nk) {
+        ij += W;
+        ik = 0;
+      }
     }
     cp_async_commit();
+    ++is;
   };
   double acc[4][CW];
 #pragma unroll
@@ -650,14 +781,17 @@ __global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int ni
 #pragma unroll
     for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
 #pragma unroll
-  for (int st = 0; st < kPS - 1; ++st) issue(st);
-  for (int st = 0; st < nst; ++st) {
-    issue(st + kPS - 1);
+  for (int p = 0; p < kPS - 1; ++p) issue();
+  int cj = gw, ck = 0, st = 0;
+  while (cj < nitems) {
+    issue();
     cp_async_wait_group<kPS - 1>();
     __syncwarp();
-    const double* As = buf + (st % kPS) * kKS * (32 + RC);
+    const int it = t0 + cj;
+    const int nk = sw.nk[it];
+    const int kn = min(kKS, nk - ck);
+    const double* As = buf + (st % kPS) * SD;
     const double* Zs = As + kKS * 32;
-    const int kn = min(kKS, nkw - st * kKS);
     for (int k = 0; k < kn; ++k) {
       const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
       const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
@@ -680,36 +814,48 @@ __global__ void __launch_bounds__(128) k_sweep_items(SweepDev sw, int t0, int ni
         for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
     }
     __syncwarp();
+    ++st;
+    ck += kn;
+    if (ck < nk) continue;
+    // ---- item done: output rows (direct) or partial rows + group countdown
+    const int out = sw.out[it];
+    const int nv = sw.nvalid[it];
+    double* __restrict__ dst =
+        out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        if (4 * rg + r < nv && cg * CW + c < rcn) dst[(int64_t)(4 * rg + r) * R + cg * CW + c] = acc[r][c];
+        acc[r][c] = 0.0;
+      }
+    if (out < 0) {
+      __threadfence();
+      __syncwarp();
+      for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
+        const int g = sw.ig[q];
+        int last = 0;
+        if (lane == 0) last = atomicSub(cnt + (int64_t)g * kGY + blockIdx.y, 1) == 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+        const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
+        for (int e = lane; e < nt * rcn; e += 32) {
+          const int t = tb + e / rcn, c = e % rcn;
+          double v = 0;
+          for (int u = sw.red_ptr[t]; u < sw.red_ptr[t + 1]; ++u)
+            v += __ldcg(partial + (int64_t)sw.red_src[u] * R + c0 + c);
+          double* o = (sw.red_mode[t] == 0 ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0 + c;
+          if (sw.red_mode[t] == 0) *o = v;
+          else *o = __ldcg(o) - v;
+        }
+        if (lane == 0) cnt[(int64_t)g * kGY + blockIdx.y] = sw.g_cnt[g];  // re-arm for the next solve
+      }
+    }
+    cj += W;
+    ck = 0;
   }
   cp_async_wait_group<0>();
-  __syncthreads();
-  // warp tiles -> shared [w][32][RC]; then fixed-order sum over w and coalesced store
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < CW; ++c) buf[(4 * rg + r) * RC + cg * CW + c] = acc[r][c];
-  __syncthreads();
-  const int nv = sw.nvalid[it];
-  const int out = sw.out[it];
-  double* __restrict__ dst = out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
-  for (int e = threadIdx.x; e < nv * RC; e += 128) {
-    const int r = e / RC, c = e - r * RC;
-    if (c >= rcn) continue;
-    const double v = ((sm[e] + sm[WD + e]) + sm[2 * WD + e]) + sm[3 * WD + e];
-    dst[(int64_t)r * R + c] = v;
-  }
-}
-
-__global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
-                               double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= (int64_t)ntarget * R) return;
-  const int t = r0 + (int)(g / R), c = (int)(g % R);
-  double acc = 0;
-  for (int q = sw.red_ptr[t]; q < sw.red_ptr[t + 1]; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
-  const int64_t o = (int64_t)sw.red_row[t] * R + c;
-  if (sw.red_mode[t] == 0) dst_assign[o] = acc;
-  else dst_sub[o] -= acc;
 }
 
 // ----------------------------------------------------------------- K5: contact

@@ -40,9 +40,11 @@ struct HostPlan {
   std::vector<double> D, P;          // P holds W_s = L[R_s, J_s] L_ss^{-1} row-major (nr x ns)
   int64_t nnzL = 0;                  // stored entries of L_s (diag blocks packed + panels)
   double factor_flops = 0, factor_ms = 0;
-  // ---- solve schedule (K3 v3): per level and sweep, warp work items over a
-  // k-major factor stream (element (k, lane) of item t at a_off[t] + (k - k0) * 32 + lane), then a
-  // deterministic reduction of partial rows into their targets.
+  // ---- solve schedule (K3 v4): per level and sweep, warp work items over a
+  // k-major factor stream (element (k, lane) of item t at a_off[t] + (k - k0) * 32 + lane).  Items that
+  // share an output (forward W rows of one ancestor tile, split chunks) write partial rows; the last
+  // item of each reduction group to finish (integer countdown) sums the group's partial rows in a fixed
+  // order into its targets — deterministic, one kernel per level.
   int nlevels = 0;
   struct Sweep {
     std::vector<double> A;             // factor stream in item order (k-major 32-lane blocks)
@@ -53,14 +55,17 @@ struct HostPlan {
     std::vector<int64_t> zidx;         // offset into `rows` (indirect source rows R_s[k0 + k])
     std::vector<int32_t> out;          // >= 0: direct output row out + lane; < 0: partial rows (-out-1)*32 + lane
     std::vector<int32_t> nvalid;       // valid lanes
-    std::vector<int32_t> lvl_red;      // [nlevels+1] reduce targets of level l
+    std::vector<int32_t> ig_ptr, ig;   // CSR item -> reduction groups it contributes to
+    std::vector<int32_t> lvl_grp;      // [nlevels+1] groups of level l
+    std::vector<int32_t> g_tptr;       // [ngroups+1] targets of group g: [g_tptr[g], g_tptr[g+1])
+    std::vector<int32_t> g_cnt;        // items contributing to group g (countdown start)
     std::vector<int32_t> red_row;      // target row (solve position)
     std::vector<int32_t> red_mode;     // 0: dst[row] = sum (y or x), 1: z[row] -= sum
     std::vector<int32_t> red_ptr;      // [ntargets+1] into red_src
     std::vector<int32_t> red_src;      // partial row indices, summed in this order
     int64_t max_partial_rows = 0;
   } fw, bw;
-  int kc = 256;                        // max k-steps per item (4 warps x 64)
+  int warps_target = 148 * 16;         // warps per level launch the item size is balanced for
   // ---- contact candidates: ordered LAST as one root supernode ----
   int nc = 0;                        // number of candidate nodes (0 = no contact)
   int csup = -1;                     // index of the candidate supernode (= nsup - 1)

@@ -176,152 +176,200 @@ static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
 // ---------------------------------------------------------------- solve schedule
 // Forward sweep, level l (children before parents), for every level-l supernode s (z[J_s] final):
 //   D items: y[J_s rows i0..i0+32) = D_s[rows, 0..min(i0+32, ns)) z[J_s]      (k-major, lane = row)
-//   W items: partial rows = W_s[rows i0..i0+32, :] z[J_s];  reduce: z[R_s[i]] -= partial row i
+//   W items: partial rows = W_s[rows i0..i0+32, :] z[J_s];  group of an ancestor tile: z[R_s[i]] -= sum
 // Backward sweep, level l (parents first), column chunk c0..c0+32 of s:
 //   x[J_s cols] = D_s^T y[J_s] - W_s^T x[R_s]     (D part k = c0..ns, W part k = 0..nr; lane = column)
-// Items hold <= kc k-steps; a chunk covered by one item writes its output directly, otherwise its
-// items write partial rows that the level's reduce sums in item order (deterministic).
+// Items hold <= kc_l k-steps (kc_l balances the level over warps_target warps); a chunk covered by one
+// item writes its output directly, otherwise its items write partial rows summed by the chunk's group.
 static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
-  const int L = 32, KC = P.kc;
+  const int L = 32;
   auto init = [&](HostPlan::Sweep& S) {
     S = HostPlan::Sweep();
     S.lvl_item.assign(1, 0);
-    S.lvl_red.assign(1, 0);
     S.red_ptr.assign(1, 0);
+    S.g_tptr.assign(1, 0);
+    S.ig_ptr.assign(1, 0);
+    S.lvl_grp.assign(1, 0);
   };
   init(P.fw);
   init(P.bw);
+  std::vector<int32_t> sup_of_pos(P.nfree);
+  for (int s = 0; s < P.nsup; ++s)
+    for (int k = 0; k < P.ssize[s]; ++k) sup_of_pos[P.sfirst[s] + k] = s;
   auto Dval = [&](int s, int i, int k) -> double {  // D_s[i][k], packed lower
     return k <= i ? P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + k] : 0.0;
   };
   auto Wval = [&](int s, int i, int k) -> double {  // W_s[i][k], row-major nr x ns
     return P.P[P.poff[s] + (int64_t)i * P.ssize[s] + k];
   };
+  auto kc_for = [&](int64_t ktot) {
+    int64_t kc = (ktot + P.warps_target - 1) / P.warps_target;
+    kc = (kc + 7) / 8 * 8;
+    return (int)std::max<int64_t>(16, std::min<int64_t>(256, kc));
+  };
+  // one item: k-major block rows/cols of `val(k, lane)`, k = 0..nk
+  auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val) {
+    S.a_off.push_back((int64_t)S.A.size());
+    for (int k = 0; k < nk; ++k)
+      for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, l) : 0.0);
+    S.nk.push_back(nk);
+    S.zrow.push_back(zr);
+    S.zidx.push_back(zi);
+    S.nvalid.push_back(nv);
+  };
+  // a level's reduction groups: targets (row, mode, contributions in order), contributing items
+  struct Target { int32_t row, mode; std::vector<int32_t> src; };
+  struct Group { std::vector<Target> t; std::vector<int32_t> items; };
+  auto flush_groups = [&](HostPlan::Sweep& S, std::vector<Group>& groups, int item_base) {
+    const int nitem = (int)S.a_off.size() - item_base;
+    std::vector<std::vector<int32_t>> of_item(nitem);
+    for (auto& g : groups) {
+      const int gid = (int)S.g_cnt.size();
+      for (auto& t : g.t) {
+        S.red_row.push_back(t.row);
+        S.red_mode.push_back(t.mode);
+        for (int32_t r : t.src) S.red_src.push_back(r);
+        S.red_ptr.push_back((int32_t)S.red_src.size());
+      }
+      S.g_tptr.push_back((int32_t)S.red_row.size());
+      std::sort(g.items.begin(), g.items.end());
+      g.items.erase(std::unique(g.items.begin(), g.items.end()), g.items.end());
+      S.g_cnt.push_back((int32_t)g.items.size());
+      for (int32_t it : g.items) of_item[it - item_base].push_back(gid);
+    }
+    for (auto& v : of_item) {
+      for (int32_t g : v) S.ig.push_back(g);
+      S.ig_ptr.push_back((int32_t)S.ig.size());
+    }
+    groups.clear();
+  };
   // ---- forward
   {
     HostPlan::Sweep& S = P.fw;
     for (int lev = 0; lev < P.nlevels; ++lev) {
-      int64_t prow = 0;  // partial rows of this level
-      std::vector<std::pair<int32_t, int32_t>> contrib;  // (target row, partial row) in item order
-      std::vector<std::pair<int32_t, std::vector<int32_t>>> dsum;  // (y row, partial rows) multi-item D chunks
+      int64_t ktot = 0;
+      for (int s : byh[lev]) {
+        const int ns = P.ssize[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        for (int i0 = 0; i0 < ns; i0 += L) ktot += std::min(i0 + L, ns);
+        ktot += (int64_t)((nr + L - 1) / L) * ns;
+      }
+      const int KC = kc_for(ktot);
+      const int item_base = (int)S.a_off.size();
+      int64_t prow = 0;
+      std::vector<Group> groups;
+      // W contributions: (target row, partial row, item) in emission order
+      std::vector<std::array<int32_t, 3>> contrib;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
         for (int i0 = 0; i0 < ns; i0 += L) {  // D items
           const int kend = std::min(i0 + L, ns), nv = std::min(L, ns - i0);
           const int nit = (kend + KC - 1) / KC;
-          std::vector<int32_t> rows_p;
+          Group g;
+          if (nit > 1)
+            for (int l = 0; l < nv; ++l) g.t.push_back({f + i0 + l, 0, {}});
           for (int k0 = 0; k0 < kend; k0 += KC) {
             const int k1 = std::min(kend, k0 + KC);
-            S.a_off.push_back((int64_t)S.A.size());
-            for (int k = k0; k < k1; ++k)
-              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? Dval(s, i0 + l, k) : 0.0);
-            S.nk.push_back(k1 - k0);
-            S.zrow.push_back(f + k0);
-            S.zidx.push_back(0);
-            S.nvalid.push_back(nv);
+            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Dval(s, i0 + l, k0 + k); });
             if (nit == 1) {
               S.out.push_back(f + i0);
             } else {
               S.out.push_back(-(int32_t)(prow / L) - 1);
-              for (int l = 0; l < nv; ++l) rows_p.push_back((int32_t)(prow + l));
+              for (int l = 0; l < nv; ++l) g.t[l].src.push_back((int32_t)(prow + l));
+              g.items.push_back((int32_t)S.a_off.size() - 1);
               prow += L;
             }
           }
-          if (nit > 1)
-            for (int l = 0; l < nv; ++l) {
-              std::vector<int32_t> src;
-              for (int t = 0; t < nit; ++t) src.push_back(rows_p[t * nv + l]);
-              dsum.push_back({f + i0 + l, src});
-            }
+          if (nit > 1) groups.push_back(std::move(g));
         }
         for (int i0 = 0; i0 < nr; i0 += L) {  // W items
           const int nv = std::min(L, nr - i0);
           for (int k0 = 0; k0 < ns; k0 += KC) {
             const int k1 = std::min(ns, k0 + KC);
-            S.a_off.push_back((int64_t)S.A.size());
-            for (int k = k0; k < k1; ++k)
-              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? Wval(s, i0 + l, k) : 0.0);
-            S.nk.push_back(k1 - k0);
-            S.zrow.push_back(f + k0);
-            S.zidx.push_back(0);
-            S.nvalid.push_back(nv);
+            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Wval(s, i0 + l, k0 + k); });
             S.out.push_back(-(int32_t)(prow / L) - 1);
-            for (int l = 0; l < nv; ++l) contrib.push_back({P.rows[P.rptr[s] + i0 + l], (int32_t)(prow + l)});
+            for (int l = 0; l < nv; ++l)
+              contrib.push_back({P.rows[P.rptr[s] + i0 + l], (int32_t)(prow + l), (int32_t)S.a_off.size() - 1});
             prow += L;
           }
         }
       }
-      S.lvl_item.push_back((int32_t)S.a_off.size());
-      S.max_partial_rows = std::max(S.max_partial_rows, prow);
-      for (auto& d : dsum) {
-        S.red_row.push_back(d.first);
-        S.red_mode.push_back(0);
-        for (int32_t r : d.second) S.red_src.push_back(r);
-        S.red_ptr.push_back((int32_t)S.red_src.size());
-      }
+      // W groups: one per 32-row tile of an ancestor supernode; per target row, contributions in order
       std::stable_sort(contrib.begin(), contrib.end(),
-                       [](const std::pair<int32_t, int32_t>& x, const std::pair<int32_t, int32_t>& y) {
-                         return x.first < y.first;
-                       });
+                       [](const std::array<int32_t, 3>& x, const std::array<int32_t, 3>& y) { return x[0] < y[0]; });
       for (size_t i = 0; i < contrib.size();) {
+        const int row = contrib[i][0];
+        const int a = sup_of_pos[row];
+        const int tile = (row - P.sfirst[a]) / L;
+        Group g;
         size_t j = i;
-        S.red_row.push_back(contrib[i].first);
-        S.red_mode.push_back(1);
-        while (j < contrib.size() && contrib[j].first == contrib[i].first) S.red_src.push_back(contrib[j++].second);
-        S.red_ptr.push_back((int32_t)S.red_src.size());
+        while (j < contrib.size() && sup_of_pos[contrib[j][0]] == a && (contrib[j][0] - P.sfirst[a]) / L == tile) {
+          const int r = contrib[j][0];
+          Target t{r, 1, {}};
+          while (j < contrib.size() && contrib[j][0] == r) {
+            t.src.push_back(contrib[j][1]);
+            g.items.push_back(contrib[j][2]);
+            ++j;
+          }
+          g.t.push_back(std::move(t));
+        }
+        groups.push_back(std::move(g));
         i = j;
       }
-      S.lvl_red.push_back((int32_t)S.red_row.size());
+      flush_groups(S, groups, item_base);
+      S.lvl_grp.push_back((int32_t)S.g_cnt.size());
+      S.lvl_item.push_back((int32_t)S.a_off.size());
+      S.max_partial_rows = std::max(S.max_partial_rows, prow);
     }
   }
   // ---- backward (levels top-down; stored in that execution order: level index = H - l)
   {
     HostPlan::Sweep& S = P.bw;
     for (int lev = P.nlevels - 1; lev >= 0; --lev) {
+      int64_t ktot = 0;
+      for (int s : byh[lev]) {
+        const int ns = P.ssize[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        for (int c0 = 0; c0 < ns; c0 += L) ktot += (ns - c0) + nr;
+      }
+      const int KC = kc_for(ktot);
+      const int item_base = (int)S.a_off.size();
       int64_t prow = 0;
+      std::vector<Group> groups;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
         for (int c0 = 0; c0 < ns; c0 += L) {
           const int nv = std::min(L, ns - c0);
           const int nit = (ns - c0 + KC - 1) / KC + (nr + KC - 1) / KC;
-          std::vector<int32_t> rows_p;
-          auto emit = [&](int64_t zi, int zr, int nk, auto&& val) {
-            S.a_off.push_back((int64_t)S.A.size());
-            for (int k = 0; k < nk; ++k)
-              for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, c0 + l) : 0.0);
-            S.nk.push_back(nk);
-            S.zrow.push_back(zr);
-            S.zidx.push_back(zi);
-            S.nvalid.push_back(nv);
+          Group g;
+          if (nit > 1)
+            for (int l = 0; l < nv; ++l) g.t.push_back({f + c0 + l, 0, {}});
+          auto out_of = [&]() {
             if (nit == 1) {
               S.out.push_back(f + c0);
             } else {
               S.out.push_back(-(int32_t)(prow / L) - 1);
-              for (int l = 0; l < nv; ++l) rows_p.push_back((int32_t)(prow + l));
+              for (int l = 0; l < nv; ++l) g.t[l].src.push_back((int32_t)(prow + l));
+              g.items.push_back((int32_t)S.a_off.size() - 1);
               prow += L;
             }
           };
           for (int k0 = c0; k0 < ns; k0 += KC) {  // D_s^T y[J_s]: k = row of D_s, lane = column
             const int k1 = std::min(ns, k0 + KC);
-            emit(0, f + k0, k1 - k0, [&](int k, int c) { return Dval(s, k0 + k, c); });
+            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Dval(s, k0 + k, c0 + l); });
+            out_of();
           }
           for (int k0 = 0; k0 < nr; k0 += KC) {  // - W_s^T x[R_s]
             const int k1 = std::min(nr, k0 + KC);
-            emit(P.rptr[s] + k0, -1, k1 - k0, [&](int k, int c) { return -Wval(s, k0 + k, c); });
+            emit_item(S, k1 - k0, nv, -1, P.rptr[s] + k0, [&](int k, int l) { return -Wval(s, k0 + k, c0 + l); });
+            out_of();
           }
-          if (nit > 1)
-            for (int l = 0; l < nv; ++l) {
-              S.red_row.push_back(f + c0 + l);
-              S.red_mode.push_back(0);
-              for (int t = 0; t < nit; ++t) S.red_src.push_back(rows_p[t * nv + l]);
-              S.red_ptr.push_back((int32_t)S.red_src.size());
-            }
+          if (nit > 1) groups.push_back(std::move(g));
         }
       }
+      flush_groups(S, groups, item_base);
+      S.lvl_grp.push_back((int32_t)S.g_cnt.size());
       S.lvl_item.push_back((int32_t)S.a_off.size());
-      S.lvl_red.push_back((int32_t)S.red_row.size());
       S.max_partial_rows = std::max(S.max_partial_rows, prow);
     }
   }

@@ -65,11 +65,18 @@ int main(int argc, char** argv) {
           else part[(int64_t)(-S.out[t] - 1) * 32 + l] = acc;
         }
       }
-      for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) {
-        double acc = 0;
-        for (int q = S.red_ptr[r]; q < S.red_ptr[r + 1]; ++q) acc += part[S.red_src[q]];
-        if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
-        else (*zsub)[S.red_row[r]] -= acc;
+      // every item lists each group it feeds exactly once, and each group counts its items
+      for (int g = S.lvl_grp[lev]; g < S.lvl_grp[lev + 1]; ++g) {
+        int cnt = 0;
+        for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t)
+          for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q) cnt += S.ig[q] == g;
+        if (cnt != S.g_cnt[g]) { printf("group %d count %d != %d\n", g, cnt, S.g_cnt[g]); exit(6); }
+        for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
+          double acc = 0;
+          for (int q = S.red_ptr[r]; q < S.red_ptr[r + 1]; ++q) acc += part[S.red_src[q]];
+          if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
+          else (*zsub)[S.red_row[r]] -= acc;
+        }
       }
     }
   };
