@@ -235,10 +235,8 @@ def main_ours(args):
             prof[k] = (a + ms, b + c)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    from paper_2101_05917_b200 import shard
+    total_ms = shard.max_over_ranks(total_ms, ws, dev)
     ms_per_step = total_ms / args.steps
     units = ws * B * T * N
     value = units / (ms_per_step / 1e3)
@@ -271,10 +269,10 @@ def main_ours(args):
             e1.record()
             torch.cuda.synchronize()
             e2e_ms += e0.elapsed_time(e1)
-        if ws > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = shard.max_over_ranks(e2e_ms, ws, dev)
+        # the one end-of-run collective of the sharded path: per-sim losses of every rank
+        all_loss = shard.gather_rows(out_loss.to(dev)[:, None], ws)
+        assert all_loss.shape[0] == ws * B
         e2e = dict(value=units / (e2e_ms / args.steps / 1e3), unit=UNIT, h2d_bytes_per_step=h2d,
                    d2h_bytes_per_step=d2h)
 

@@ -36,7 +36,7 @@ __device__ __forceinline__ void cof3(const double* A, double* C) {
 
 // Symmetric 3x3 eigen-decomposition by cyclic Jacobi: A (row-major, symmetric) ->
 // eigenvalues lam[3] (descending), eigenvectors V[:,k] (columns, row-major V), det V = +1.
-__device__ void jacobi_eig3(const double* Ain, double* lam, double* V) {
+__device__ __noinline__ void jacobi_eig3(const double* Ain, double* lam, double* V) {
   double a[9];
   for (int i = 0; i < 9; ++i) a[i] = Ain[i];
   for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
@@ -86,7 +86,7 @@ __device__ void jacobi_eig3(const double* Ain, double* lam, double* V) {
 
 // Rotation closest to F via an SVD from the eigen-decomposition of F^T F; the
 // smallest singular direction is flipped when det F < 0.
-__device__ void polar_svd_fallback(const double* F, double* R) {
+__device__ __noinline__ void polar_svd_fallback(const double* F, double* R) {
   double C[9];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) C[3 * i + j] = F[i] * F[j] + F[3 + i] * F[3 + j] + F[6 + i] * F[6 + j];
@@ -126,7 +126,7 @@ __device__ void polar_svd_fallback(const double* F, double* R) {
 // convergence, no divisions); stops after the step taken with ||X^T X - I||_F < 1e-8 (the next error is
 // below fp64 resolution).  Falls back to the scaled Newton iteration X <- (g X + X^{-T}/g)/2 if it is
 // slow (strongly anisotropic F), and to the SVD path for det F <= 1e-6 ||F||^3.
-__device__ void polar_newton(const double* F, double* R) {
+__device__ __noinline__ void polar_newton(const double* F, double* R) {
   double X[9];
   for (int i = 0; i < 9; ++i) X[i] = F[i];
   bool scaled = true, last = false;
