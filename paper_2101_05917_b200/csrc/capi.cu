@@ -49,6 +49,7 @@ struct pd_sim {
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
   int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
+  int32_t* grab = nullptr;                      // K3 per-level item counters
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
@@ -224,8 +225,11 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, sweep_smem_bytes<RC>()));
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
+  // per-level item counters of the dynamic schedule, zeroed at the start of every solve
+  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 2 * P.nlevels * kGY, s->stream));
   auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, int32_t* cnt, bool fwd) {
     for (int j = 0; j < P.nlevels; ++j) {
+      int32_t* grab = s->grab + ((fwd ? 0 : P.nlevels) + j) * kGY;
       const int t0 = S.lvl_item[j], nt = S.lvl_item[j + 1] - t0;
       const bool fix = !fwd && s->pins_live && j == 0;  // backward level 0 = the root = the candidate block
       double* root = s->S0 + (int64_t)s->csup_first * R;
@@ -236,7 +240,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
         // backward: D part y (S2), W part x (S0), direct x (S0)
         const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
         k_sweep_level<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
-            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, cnt);
+            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, cnt, grab);
         LAUNCH_CHECK(s);
       }
       if (fix) {
@@ -593,6 +597,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.a_off = s->upload(S.a_off);
       d.zidx = s->upload(S.zidx);
       d.nk = s->upload(S.nk);
+      d.nkd = s->upload(S.nkd);
       d.zrow = s->upload(S.zrow);
       d.out = s->upload(S.out);
       d.nvalid = s->upload(S.nvalid);
@@ -612,6 +617,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
         for (int y = 0; y < kGY; ++y) c[g * kGY + y] = S.g_cnt[g];
       return s->upload(c);
     };
+    s->grab = s->alloc<int32_t>(2 * P.nlevels * kGY);
     s->cnt_f = up_cnt(P.fw);
     s->cnt_b = up_cnt(P.bw);
     up_sweep(P.fw, s->swf);

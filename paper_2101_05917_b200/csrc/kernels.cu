@@ -713,63 +713,80 @@ __host__ __device__ constexpr int sweep_warp_doubles() { return kPS * kKS * (32 
 template <int RC>
 __host__ __device__ constexpr int sweep_smem_bytes() { return 4 * sweep_warp_doubles<RC>() * 8; }
 
-// One launch per level (K3 v4).  Every warp walks its items gw, gw + W, gw + 2W, ... (W = warps in the
-// grid) through a kPS-stage cp.async ring that runs across item boundaries (kKS k-steps per stage: 32
-// factor doubles + RC right-hand-side doubles per k).  Lane (rg, cg) = (lane % 8, lane / 8) keeps a
-// 4-row x RC/4-column register tile.  A finished item writes its output rows directly or, for shared
-// outputs, partial rows; it then counts down each reduction group it feeds, and the warp that brings a
-// group to zero sums the group's partial rows in their fixed order into the targets (and re-arms the
-// counter).  Deterministic: the arithmetic of every item and every sum is independent of scheduling.
+// One launch per level (K3 v4).  Warps take items dynamically (one integer atomicAdd per item on the
+// level's counter) and stream them through a kPS-stage cp.async ring that runs across item boundaries
+// (kKS k-steps per stage: 32 factor doubles + RC right-hand-side doubles per k); the grabbed item ids
+// wait in a small per-warp queue until the compute side reaches them.  Lane (rg, cg) = (lane % 8,
+// lane / 8) keeps a 4-row x RC/4-column register tile.  A finished item writes its output rows directly
+// or, for shared outputs, partial rows; it then counts down each reduction group it feeds, and the warp
+// that brings a group to zero sums the group's partial rows in their fixed order into the targets (and
+// re-arms the counter).  Deterministic: the arithmetic of every item and every sum is independent of
+// which warp runs it.
 constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group
+constexpr int kQ = 8;    // per-warp queue of grabbed items (>= kPS: one stage can hold at most one item)
 
 template <int RC, bool VEC>
 __global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                      const double* __restrict__ zc, const double* __restrict__ zi,
                                                      const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                      double* __restrict__ zsub, double* __restrict__ partial,
-                                                     int32_t* __restrict__ cnt) {
+                                                     int32_t* __restrict__ cnt, int32_t* __restrict__ grab) {
   constexpr int CW = RC / 4;
   constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
+  __shared__ int32_t qs[4][kQ];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = lane & 7, cg = lane >> 3;
-  const int gw = blockIdx.x * 4 + w, W = gridDim.x * 4;
   const int c0 = blockIdx.y * RC;
   const int rcn = min(RC, R - c0);
   double* buf = sm + w * kPS * SD;
-  int ij = gw, ik = 0, is = 0;  // issue cursor: item, k offset, stage count
+  int32_t* q = qs[w];
+  auto take = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(grab + blockIdx.y, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  int nq = 0;           // items grabbed so far (queue slots used cyclically)
+  int ij = take(), ik = 0, is = 0;  // issue cursor: item, k offset, stage count
+  if (lane == 0) q[0] = ij;
+  nq = 1;
   auto issue = [&]() {
     if (ij < nitems) {
       const int it = t0 + ij;
-      const int nk = sw.nk[it];
+      const int nk = sw.nk[it], nkd = sw.nkd[it];
       const int kn = min(kKS, nk - ik);
       double* As = buf + (is % kPS) * SD;
       double* Zs = As + kKS * 32;
       const double* Ag = sw.A + sw.a_off[it] + (int64_t)ik * 32;
       for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + 2 * i);
       const int zr = sw.zrow[it];
-      const double* zsrc = zr >= 0 ? zc : zi;
-      const int32_t* idx = rows + sw.zidx[it] + ik;
+      const int32_t* idx = rows + sw.zidx[it] - nkd;
       if (VEC) {
         constexpr int H = RC / 2;
         for (int i = lane; i < kn * H; i += 32) {
           const int k = i / H, c = 2 * (i - k * H);
-          const int row = zr >= 0 ? zr + ik + k : __ldg(idx + k);
-          if (c < rcn) cp_async16(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+          const int kk = ik + k;
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          if (c < rcn) cp_async16(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
           else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
         }
       } else {
         for (int i = lane; i < kn * RC; i += 32) {
           const int k = i / RC, c = i - k * RC;
-          const int row = zr >= 0 ? zr + ik + k : __ldg(idx + k);
-          if (c < rcn) cp_async8(Zs + k * RC + c, zsrc + (int64_t)row * R + c0 + c);
+          const int kk = ik + k;
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
           else Zs[k * RC + c] = 0.0;
         }
       }
       ik += kn;
       if (ik >= nk) {
-        ij += W;
+        ij = take();
         ik = 0;
+        if (lane == 0) q[nq % kQ] = ij;
+        ++nq;
       }
     }
     cp_async_commit();
@@ -782,7 +799,9 @@ __global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int ni
     for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
 #pragma unroll
   for (int p = 0; p < kPS - 1; ++p) issue();
-  int cj = gw, ck = 0, st = 0;
+  int cq = 0, ck = 0, st = 0;  // compute cursor: queue position, k offset
+  __syncwarp();
+  int cj = q[0];
   while (cj < nitems) {
     issue();
     cp_async_wait_group<kPS - 1>();
@@ -830,29 +849,54 @@ __global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int ni
         acc[r][c] = 0.0;
       }
     if (out < 0) {
-      __threadfence();
-      __syncwarp();
+      __syncwarp();  // the warp's partial-row stores happen-before lane 0's release fence (cumulativity)
       for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
         const int g = sw.ig[q];
         int last = 0;
-        if (lane == 0) last = atomicSub(cnt + (int64_t)g * kGY + blockIdx.y, 1) == 1;
+        if (lane == 0) {
+          __threadfence();
+          last = atomicSub(cnt + (int64_t)g * kGY + blockIdx.y, 1) == 1;
+        }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) continue;
         __threadfence();
+        // lane = target row (<= 32 per group); its RC columns accumulate in registers over the target's
+        // partial rows in their planned order
         const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
-        for (int e = lane; e < nt * rcn; e += 32) {
-          const int t = tb + e / rcn, c = e % rcn;
-          double v = 0;
-          for (int u = sw.red_ptr[t]; u < sw.red_ptr[t + 1]; ++u)
-            v += __ldcg(partial + (int64_t)sw.red_src[u] * R + c0 + c);
-          double* o = (sw.red_mode[t] == 0 ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0 + c;
-          if (sw.red_mode[t] == 0) *o = v;
-          else *o = __ldcg(o) - v;
+        if (lane < nt) {
+          const int t = tb + lane;
+          double v[RC];
+#pragma unroll
+          for (int c = 0; c < RC; ++c) v[c] = 0.0;
+          const int u0 = sw.red_ptr[t], u1 = sw.red_ptr[t + 1];
+          for (int u = u0; u < u1; ++u) {
+            const double* pr = partial + (int64_t)sw.red_src[u] * R + c0;
+            if (VEC) {
+#pragma unroll
+              for (int c = 0; c < RC / 2; ++c)
+                if (2 * c < rcn) {
+                  const double2 x = __ldcg(reinterpret_cast<const double2*>(pr) + c);
+                  v[2 * c] += x.x;
+                  v[2 * c + 1] += x.y;
+                }
+            } else {
+#pragma unroll
+              for (int c = 0; c < RC; ++c)
+                if (c < rcn) v[c] += __ldcg(pr + c);
+            }
+          }
+          const bool assign = sw.red_mode[t] == 0;
+          double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0;
+#pragma unroll
+          for (int c = 0; c < RC; ++c)
+            if (c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
         }
         if (lane == 0) cnt[(int64_t)g * kGY + blockIdx.y] = sw.g_cnt[g];  // re-arm for the next solve
       }
     }
-    cj += W;
+    ++cq;
+    __syncwarp();
+    cj = q[cq % kQ];
     ck = 0;
   }
   cp_async_wait_group<0>();

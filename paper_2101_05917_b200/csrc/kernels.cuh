@@ -28,7 +28,7 @@ struct ElemArgs {
 struct SweepDev {  // device copy of HostPlan::Sweep
   const double* A;
   const int64_t *a_off, *zidx;
-  const int32_t *nk, *zrow, *out, *nvalid;
+  const int32_t *nk, *nkd, *zrow, *out, *nvalid;
   const int32_t *ig_ptr, *ig, *g_tptr, *g_cnt;
   const int32_t *red_row, *red_mode, *red_ptr, *red_src;
 };

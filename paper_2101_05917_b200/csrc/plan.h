@@ -51,8 +51,9 @@ struct HostPlan {
     std::vector<int32_t> lvl_item;     // [nlevels+1] items of level l: [lvl_item[l], lvl_item[l+1])
     std::vector<int64_t> a_off;        // per item
     std::vector<int32_t> nk;           // k-steps
-    std::vector<int32_t> zrow;         // >= 0: source rows zrow + k (contiguous); < 0: rows from zidx
-    std::vector<int64_t> zidx;         // offset into `rows` (indirect source rows R_s[k0 + k])
+    std::vector<int32_t> nkd;          // k < nkd: source row zrow + k of the contiguous source
+    std::vector<int32_t> zrow;         //   (z forward, y backward); k >= nkd: row rows[zidx + k - nkd]
+    std::vector<int64_t> zidx;         //   of the indirect source (x backward: x[R_s])
     std::vector<int32_t> out;          // >= 0: direct output row out + lane; < 0: partial rows (-out-1)*32 + lane
     std::vector<int32_t> nvalid;       // valid lanes
     std::vector<int32_t> ig_ptr, ig;   // CSR item -> reduction groups it contributes to

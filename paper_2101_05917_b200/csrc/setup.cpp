@@ -205,14 +205,15 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   auto kc_for = [&](int64_t ktot) {
     int64_t kc = (ktot + P.warps_target - 1) / P.warps_target;
     kc = (kc + 7) / 8 * 8;
-    return (int)std::max<int64_t>(16, std::min<int64_t>(256, kc));
+    return (int)std::max<int64_t>(128, std::min<int64_t>(256, kc));  // >= 128: partial rows stay <= R/128 of the bytes
   };
   // one item: k-major block rows/cols of `val(k, lane)`, k = 0..nk
-  auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val) {
+  auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val, int nkd = -1) {
     S.a_off.push_back((int64_t)S.A.size());
     for (int k = 0; k < nk; ++k)
       for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, l) : 0.0);
     S.nk.push_back(nk);
+    S.nkd.push_back(nkd < 0 ? nk : nkd);
     S.zrow.push_back(zr);
     S.zidx.push_back(zi);
     S.nvalid.push_back(nv);
@@ -340,11 +341,21 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
         for (int c0 = 0; c0 < ns; c0 += L) {
           const int nv = std::min(L, ns - c0);
-          const int nit = (ns - c0 + KC - 1) / KC + (nr + KC - 1) / KC;
+          // k-sequence = [D part: rows c0..ns of D_s | W part: rows 0..nr of W_s], cut into items of <= KC
+          const int nd = ns - c0, ktot_c = nd + nr;
+          const int nit = (ktot_c + KC - 1) / KC;
           Group g;
           if (nit > 1)
             for (int l = 0; l < nv; ++l) g.t.push_back({f + c0 + l, 0, {}});
-          auto out_of = [&]() {
+          for (int p0 = 0; p0 < ktot_c; p0 += KC) {
+            const int nk = std::min(KC, ktot_c - p0);
+            const int nkd = std::max(0, std::min(nk, nd - p0));
+            emit_item(S, nk, nv, f + c0 + p0, P.rptr[s] + std::max(0, p0 - nd),
+                      [&](int k, int l) {
+                        const int q = p0 + k;
+                        return q < nd ? Dval(s, c0 + q, c0 + l) : -Wval(s, q - nd, c0 + l);
+                      },
+                      nkd);
             if (nit == 1) {
               S.out.push_back(f + c0);
             } else {
@@ -353,16 +364,6 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
               g.items.push_back((int32_t)S.a_off.size() - 1);
               prow += L;
             }
-          };
-          for (int k0 = c0; k0 < ns; k0 += KC) {  // D_s^T y[J_s]: k = row of D_s, lane = column
-            const int k1 = std::min(ns, k0 + KC);
-            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Dval(s, k0 + k, c0 + l); });
-            out_of();
-          }
-          for (int k0 = 0; k0 < nr; k0 += KC) {  // - W_s^T x[R_s]
-            const int k1 = std::min(nr, k0 + KC);
-            emit_item(S, k1 - k0, nv, -1, P.rptr[s] + k0, [&](int k, int l) { return -Wval(s, k0 + k, c0 + l); });
-            out_of();
           }
           if (nit > 1) groups.push_back(std::move(g));
         }
