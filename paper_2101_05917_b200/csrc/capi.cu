@@ -49,7 +49,8 @@ struct pd_sim {
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
   int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
-  int32_t* grab = nullptr;                      // K3 per-level item counters
+  int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
+  int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
@@ -218,40 +219,42 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
   if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
-  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
+  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
   // one resident wave: warps take items round-robin, so CTAs beyond residency would only add a tail
   int per_sm = 0, nsm = 0, dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, sweep_smem_bytes<RC>()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, sweep_smem_bytes<RC>()));
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
-  // per-level item counters of the dynamic schedule, zeroed at the start of every solve
-  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 2 * P.nlevels * kGY, s->stream));
-  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, int32_t* cnt, bool fwd) {
-    for (int j = 0; j < P.nlevels; ++j) {
-      int32_t* grab = s->grab + ((fwd ? 0 : P.nlevels) + j) * kGY;
-      const int t0 = S.lvl_item[j], nt = S.lvl_item[j + 1] - t0;
-      const bool fix = !fwd && s->pins_live && j == 0;  // backward level 0 = the root = the candidate block
-      double* root = s->S0 + (int64_t)s->csup_first * R;
-      if (fix)
-        CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
-      if (nt) {
-        // forward: sources z (S0), direct y (S2), group subtract into z (S0);
-        // backward: D part y (S2), W part x (S0), direct x (S0)
-        const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
-        k_sweep_level<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
-            d, t0, nt, R, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, cnt, grab);
-        LAUNCH_CHECK(s);
-      }
-      if (fix) {
-        k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist,
-                                                                       s->fpos, s->Qc, root);
-        LAUNCH_CHECK(s);
-      }
-    }
+  // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
+  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY, s->stream));
+  CK(cudaMemcpyAsync(s->cd_f, s->cd_f0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
+  CK(cudaMemcpyAsync(s->cd_b, s->cd_b0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
+  auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab) {
+    if (!nt) return;
+    // forward: sources z (S0), direct y (S2), group subtract into z (S0);
+    // backward: D part y (S2), W part x (S0), direct x (S0)
+    const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
+    k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
+        d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
+        cd, grab);
+    LAUNCH_CHECK(s);
   };
-  sweep(P.fw, s->swf, s->cnt_f, true);
-  sweep(P.bw, s->swb, s->cnt_b, false);
+  const HostPlan::Sweep& F = P.fw;
+  const HostPlan::Sweep& Bk = P.bw;
+  launch(s->swf, 0, F.lvl_item[P.nlevels], true, s->cnt_f, s->cd_f, s->grab);
+  if (s->pins_live) {
+    // the root (= candidate block) first, then its constrained fixup, then every other level
+    double* root = s->S0 + (int64_t)s->csup_first * R;
+    CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
+    launch(s->swb, 0, Bk.lvl_item[1], false, s->cnt_b, s->cd_b, s->grab + kGY);
+    k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos,
+                                                                   s->Qc, root);
+    LAUNCH_CHECK(s);
+    launch(s->swb, Bk.lvl_item[1], Bk.lvl_item[P.nlevels] - Bk.lvl_item[1], false, s->cnt_b, s->cd_b, s->grab + 2 * kGY);
+  } else {
+    launch(s->swb, 0, Bk.lvl_item[P.nlevels], false, s->cnt_b, s->cd_b, s->grab + kGY);
+  }
 }
 void solve_launch(pd_sim* s, int B) {
   const int R = 3 * B;
@@ -609,6 +612,11 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.red_mode = s->upload(S.red_mode);
       d.red_ptr = s->upload(S.red_ptr);
       d.red_src = s->upload(S.red_src);
+      d.sup = s->upload(S.sup);
+      d.sig = s->upload(S.sig);
+      d.g_sig = s->upload(S.g_sig);
+      d.wl_ptr = s->upload(S.wl_ptr);
+      d.wl = s->upload(S.wl);
     };
     // group countdown counters, one slot per column chunk, armed with the group's item count
     auto up_cnt = [&](const HostPlan::Sweep& S) {
@@ -617,7 +625,17 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
         for (int y = 0; y < kGY; ++y) c[g * kGY + y] = S.g_cnt[g];
       return s->upload(c);
     };
-    s->grab = s->alloc<int32_t>(2 * P.nlevels * kGY);
+    s->grab = s->alloc<int32_t>(4 * kGY);
+    auto up_cd = [&](const HostPlan::Sweep& S) {
+      std::vector<int32_t> c((size_t)P.nsup * kGY);
+      for (int u = 0; u < P.nsup; ++u)
+        for (int y = 0; y < kGY; ++y) c[(size_t)u * kGY + y] = S.cd_init[u];
+      return s->upload(c);
+    };
+    s->cd_f0 = up_cd(P.fw);
+    s->cd_b0 = up_cd(P.bw);
+    s->cd_f = s->alloc<int32_t>((int64_t)P.nsup * kGY);
+    s->cd_b = s->alloc<int32_t>((int64_t)P.nsup * kGY);
     s->cnt_f = up_cnt(P.fw);
     s->cnt_b = up_cnt(P.bw);
     up_sweep(P.fw, s->swf);

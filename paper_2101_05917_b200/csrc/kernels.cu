@@ -694,7 +694,7 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 // item write partial rows that the group's last item adds in a fixed order into y / x (assign) or into z of
 // ancestors (subtract): deterministic, no atomics.
 constexpr int kKS = 8;   // k-steps per pipeline stage
-constexpr int kPS = 4;   // pipeline stages per warp
+constexpr int kPS = 6;   // pipeline stages per warp
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -713,130 +713,149 @@ __host__ __device__ constexpr int sweep_warp_doubles() { return kPS * kKS * (32 
 template <int RC>
 __host__ __device__ constexpr int sweep_smem_bytes() { return 4 * sweep_warp_doubles<RC>() * 8; }
 
-// One launch per level (K3 v4).  Warps take items dynamically (one integer atomicAdd per item on the
-// level's counter) and stream them through a kPS-stage cp.async ring that runs across item boundaries
-// (kKS k-steps per stage: 32 factor doubles + RC right-hand-side doubles per k); the grabbed item ids
-// wait in a small per-warp queue until the compute side reaches them.  Lane (rg, cg) = (lane % 8,
-// lane / 8) keeps a 4-row x RC/4-column register tile.  A finished item writes its output rows directly
-// or, for shared outputs, partial rows; it then counts down each reduction group it feeds, and the warp
-// that brings a group to zero sums the group's partial rows in their fixed order into the targets (and
-// re-arms the counter).  Deterministic: the arithmetic of every item and every sum is independent of
-// which warp runs it.
-constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group
-constexpr int kQ = 8;    // per-warp queue of grabbed items (>= kPS: one stage can hold at most one item)
+// K3 v5: ONE launch per sweep (dataflow).  Items are taken in the planned order (levels in sweep order)
+// through one integer counter; before reading its right-hand-side rows an item waits until they are
+// final: forward, the countdown of its supernode (W groups of descendants that still have to subtract
+// into z[J_s]); backward, the countdowns of the supernodes owning R_s (their 32-column chunks of x).
+// Waits only ever point at earlier items, which are held by running warps, so the schedule cannot
+// deadlock.  Within an item the warp streams its k-range through a kPS-stage cp.async ring (kKS k-steps
+// per stage: 32 factor doubles + RC right-hand-side doubles per k); lane (rg, cg) = (lane % 8, lane / 8)
+// keeps a 4-row x RC/4-column register tile.  Output: direct rows, or partial rows + countdown of each
+// reduction group fed; the warp that brings a group to zero sums its partial rows in the planned order
+// (lane = target row), re-arms the group counter and decrements the group's supernode countdown.  All
+// atomics are integer; every floating-point sum has a fixed order -> bitwise reproducible.
+constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group / supernode
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <int RC, bool VEC>
-__global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
-                                                     const double* __restrict__ zc, const double* __restrict__ zi,
-                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
-                                                     double* __restrict__ zsub, double* __restrict__ partial,
-                                                     int32_t* __restrict__ cnt, int32_t* __restrict__ grab) {
+__global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
+                                                    const double* __restrict__ zc, const double* __restrict__ zi,
+                                                    const int32_t* __restrict__ rows, double* __restrict__ direct,
+                                                    double* __restrict__ zsub, double* __restrict__ partial,
+                                                    int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
+                                                    int32_t* __restrict__ grab) {
   constexpr int CW = RC / 4;
   constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
-  __shared__ int32_t qs[4][kQ];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = lane & 7, cg = lane >> 3;
-  const int c0 = blockIdx.y * RC;
+  const int y = blockIdx.y;
+  const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
   double* buf = sm + w * kPS * SD;
-  int32_t* q = qs[w];
   auto take = [&]() {
     int v = 0;
-    if (lane == 0) v = atomicAdd(grab + blockIdx.y, 1);
+    if (lane == 0) v = atomicAdd(grab + y, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  int nq = 0;           // items grabbed so far (queue slots used cyclically)
-  int ij = take(), ik = 0, is = 0;  // issue cursor: item, k offset, stage count
-  if (lane == 0) q[0] = ij;
-  nq = 1;
-  auto issue = [&]() {
-    if (ij < nitems) {
-      const int it = t0 + ij;
-      const int nk = sw.nk[it], nkd = sw.nkd[it];
-      const int kn = min(kKS, nk - ik);
-      double* As = buf + (is % kPS) * SD;
-      double* Zs = As + kKS * 32;
-      const double* Ag = sw.A + sw.a_off[it] + (int64_t)ik * 32;
-      for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + 2 * i);
-      const int zr = sw.zrow[it];
-      const int32_t* idx = rows + sw.zidx[it] - nkd;
-      if (VEC) {
-        constexpr int H = RC / 2;
-        for (int i = lane; i < kn * H; i += 32) {
-          const int k = i / H, c = 2 * (i - k * H);
-          const int kk = ik + k;
-          const bool ct = kk < nkd;
-          const int row = ct ? zr + kk : __ldg(idx + kk);
-          if (c < rcn) cp_async16(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-          else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
-        }
-      } else {
-        for (int i = lane; i < kn * RC; i += 32) {
-          const int k = i / RC, c = i - k * RC;
-          const int kk = ik + k;
-          const bool ct = kk < nkd;
-          const int row = ct ? zr + kk : __ldg(idx + kk);
-          if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-          else Zs[k * RC + c] = 0.0;
-        }
-      }
-      ik += kn;
-      if (ik >= nk) {
-        ij = take();
-        ik = 0;
-        if (lane == 0) q[nq % kQ] = ij;
-        ++nq;
-      }
+  auto signal = [&](int sup) {  // all lanes' prior stores -> release -> countdown
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicSub(cd + (int64_t)sup * kGY + y, 1);
     }
-    cp_async_commit();
-    ++is;
   };
-  double acc[4][CW];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-#pragma unroll
-  for (int p = 0; p < kPS - 1; ++p) issue();
-  int cq = 0, ck = 0, st = 0;  // compute cursor: queue position, k offset
-  __syncwarp();
-  int cj = q[0];
-  while (cj < nitems) {
-    issue();
-    cp_async_wait_group<kPS - 1>();
-    __syncwarp();
-    const int it = t0 + cj;
-    const int nk = sw.nk[it];
-    const int kn = min(kKS, nk - ck);
-    const double* As = buf + (st % kPS) * SD;
-    const double* Zs = As + kKS * 32;
-    for (int k = 0; k < kn; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
-      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
-      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-      double zv[CW];
-      if (CW % 2 == 0) {
-#pragma unroll
-        for (int c = 0; c < CW / 2; ++c) {
-          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
-          zv[2 * c] = t.x;
-          zv[2 * c + 1] = t.y;
+  int next = take();
+  while (next < nitems) {
+    const int it = t0 + next;
+    next = take();  // prefetch the next index (never waited on before this item is done)
+    const int nk = sw.nk[it], nkd = sw.nkd[it];
+    // ---- wait until the item's right-hand-side rows are final
+    if (lane == 0) {
+      // bounded spin: a schedule bug becomes a launch error (trap) instead of a hung GPU
+      const int su = sw.sup[it];
+      int64_t spins = 0;
+      auto wait0 = [&](const int32_t* c) {
+        while (ld_acquire(c) != 0) {
+          __nanosleep(64);
+          if (++spins > (int64_t)1 << 26) __trap();
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+      };
+      if (fwd) {
+        wait0(cd + (int64_t)su * kGY + y);
+      } else if (nkd < nk) {
+        for (int q = sw.wl_ptr[su]; q < sw.wl_ptr[su + 1]; ++q) wait0(cd + (int64_t)sw.wl[q] * kGY + y);
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
     }
     __syncwarp();
-    ++st;
-    ck += kn;
-    if (ck < nk) continue;
-    // ---- item done: output rows (direct) or partial rows + group countdown
+    const double* Ag = sw.A + sw.a_off[it];
+    const int zr = sw.zrow[it];
+    const int32_t* idx = rows + sw.zidx[it] - nkd;
+    const int nst = (nk + kKS - 1) / kKS;
+    auto issue = [&](int st) {
+      if (st < nst) {
+        double* As = buf + (st % kPS) * SD;
+        double* Zs = As + kKS * 32;
+        const int k0 = st * kKS, kn = min(kKS, nk - k0);
+        for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + (int64_t)k0 * 32 + 2 * i);
+        if (VEC) {
+          constexpr int H = RC / 2;
+          for (int i = lane; i < kn * H; i += 32) {
+            const int k = i / H, c = 2 * (i - k * H);
+            const int kk = k0 + k;
+            const bool ct = kk < nkd;
+            const int row = ct ? zr + kk : __ldg(idx + kk);
+            if (c < rcn) cp_async16(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
+            else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
+          }
+        } else {
+          for (int i = lane; i < kn * RC; i += 32) {
+            const int k = i / RC, c = i - k * RC;
+            const int kk = k0 + k;
+            const bool ct = kk < nkd;
+            const int row = ct ? zr + kk : __ldg(idx + kk);
+            if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
+            else Zs[k * RC + c] = 0.0;
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    double acc[4][CW];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+#pragma unroll
+    for (int st = 0; st < kPS - 1; ++st) issue(st);
+    for (int st = 0; st < nst; ++st) {
+      issue(st + kPS - 1);
+      cp_async_wait_group<kPS - 1>();
+      __syncwarp();
+      const double* As = buf + (st % kPS) * SD;
+      const double* Zs = As + kKS * 32;
+      const int kn = min(kKS, nk - st * kKS);
+      for (int k = 0; k < kn; ++k) {
+        const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
+        const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        double zv[CW];
+        if (CW % 2 == 0) {
+#pragma unroll
+          for (int c = 0; c < CW / 2; ++c) {
+            const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
+            zv[2 * c] = t.x;
+            zv[2 * c + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+      }
+      __syncwarp();
+    }
+    cp_async_wait_group<0>();
+    __syncwarp();
+    // ---- output
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];
     double* __restrict__ dst =
@@ -844,60 +863,54 @@ __global__ void __launch_bounds__(128) k_sweep_level(SweepDev sw, int t0, int ni
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int c = 0; c < CW; ++c) {
+      for (int c = 0; c < CW; ++c)
         if (4 * rg + r < nv && cg * CW + c < rcn) dst[(int64_t)(4 * rg + r) * R + cg * CW + c] = acc[r][c];
-        acc[r][c] = 0.0;
-      }
-    if (out < 0) {
-      __syncwarp();  // the warp's partial-row stores happen-before lane 0's release fence (cumulativity)
-      for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
-        const int g = sw.ig[q];
-        int last = 0;
-        if (lane == 0) {
-          __threadfence();
-          last = atomicSub(cnt + (int64_t)g * kGY + blockIdx.y, 1) == 1;
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (!last) continue;
-        __threadfence();
-        // lane = target row (<= 32 per group); its RC columns accumulate in registers over the target's
-        // partial rows in their planned order
-        const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
-        if (lane < nt) {
-          const int t = tb + lane;
-          double v[RC];
-#pragma unroll
-          for (int c = 0; c < RC; ++c) v[c] = 0.0;
-          const int u0 = sw.red_ptr[t], u1 = sw.red_ptr[t + 1];
-          for (int u = u0; u < u1; ++u) {
-            const double* pr = partial + (int64_t)sw.red_src[u] * R + c0;
-            if (VEC) {
-#pragma unroll
-              for (int c = 0; c < RC / 2; ++c)
-                if (2 * c < rcn) {
-                  const double2 x = __ldcg(reinterpret_cast<const double2*>(pr) + c);
-                  v[2 * c] += x.x;
-                  v[2 * c + 1] += x.y;
-                }
-            } else {
-#pragma unroll
-              for (int c = 0; c < RC; ++c)
-                if (c < rcn) v[c] += __ldcg(pr + c);
-            }
-          }
-          const bool assign = sw.red_mode[t] == 0;
-          double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0;
-#pragma unroll
-          for (int c = 0; c < RC; ++c)
-            if (c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
-        }
-        if (lane == 0) cnt[(int64_t)g * kGY + blockIdx.y] = sw.g_cnt[g];  // re-arm for the next solve
-      }
+    if (out >= 0) {
+      if (sw.sig[it] >= 0) signal(sw.sig[it]);
+      continue;
     }
-    ++cq;
     __syncwarp();
-    cj = q[cq % kQ];
-    ck = 0;
+    for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
+      const int g = sw.ig[q];
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        last = atomicSub(gcnt + (int64_t)g * kGY + y, 1) == 1;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last) continue;
+      __threadfence();
+      const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
+      if (lane < nt) {
+        const int t = tb + lane;
+        double v[RC];
+#pragma unroll
+        for (int c = 0; c < RC; ++c) v[c] = 0.0;
+        for (int u = sw.red_ptr[t]; u < sw.red_ptr[t + 1]; ++u) {
+          const double* pr = partial + (int64_t)sw.red_src[u] * R + c0;
+          if (VEC) {
+#pragma unroll
+            for (int c = 0; c < RC / 2; ++c)
+              if (2 * c < rcn) {
+                const double2 xv = __ldcg(reinterpret_cast<const double2*>(pr) + c);
+                v[2 * c] += xv.x;
+                v[2 * c + 1] += xv.y;
+              }
+          } else {
+#pragma unroll
+            for (int c = 0; c < RC; ++c)
+              if (c < rcn) v[c] += __ldcg(pr + c);
+          }
+        }
+        const bool assign = sw.red_mode[t] == 0;
+        double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0;
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          if (c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
+      }
+      if (lane == 0) gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
+      if (sw.g_sig[g] >= 0) signal(sw.g_sig[g]);
+    }
   }
   cp_async_wait_group<0>();
 }

@@ -64,7 +64,14 @@ struct HostPlan {
     std::vector<int32_t> red_mode;     // 0: dst[row] = sum (y or x), 1: z[row] -= sum
     std::vector<int32_t> red_ptr;      // [ntargets+1] into red_src
     std::vector<int32_t> red_src;      // partial row indices, summed in this order
-    int64_t max_partial_rows = 0;
+    // dataflow (one launch per sweep): an item waits until its inputs are final
+    std::vector<int32_t> sup;          // per item: its supernode
+    std::vector<int32_t> sig;          // per item: supernode whose countdown it decrements when done (-1)
+    std::vector<int32_t> g_sig;        // per group: supernode whose countdown the group decrements (-1)
+    std::vector<int32_t> cd_init;      // per supernode: countdown start (fwd: W groups into it;
+                                       //   bwd: its 32-column chunks)
+    std::vector<int32_t> wl_ptr, wl;   // per supernode: supernodes whose countdown must be 0 first
+    int64_t max_partial_rows = 0;      // partial rows are unique over the whole sweep
   } fw, bw;
   int warps_target = 148 * 16;         // warps per level launch the item size is balanced for
   // ---- contact candidates: ordered LAST as one root supernode ----

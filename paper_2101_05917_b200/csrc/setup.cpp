@@ -190,6 +190,8 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
     S.g_tptr.assign(1, 0);
     S.ig_ptr.assign(1, 0);
     S.lvl_grp.assign(1, 0);
+    S.cd_init.assign(P.nsup, 0);
+    S.wl_ptr.assign(1, 0);
   };
   init(P.fw);
   init(P.bw);
@@ -208,7 +210,9 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
     return (int)std::max<int64_t>(128, std::min<int64_t>(256, kc));  // >= 128: partial rows stay <= R/128 of the bytes
   };
   // one item: k-major block rows/cols of `val(k, lane)`, k = 0..nk
+  int cur_sup = -1;
   auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val, int nkd = -1) {
+    S.sup.push_back(cur_sup);
     S.a_off.push_back((int64_t)S.A.size());
     for (int k = 0; k < nk; ++k)
       for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, l) : 0.0);
@@ -220,7 +224,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   };
   // a level's reduction groups: targets (row, mode, contributions in order), contributing items
   struct Target { int32_t row, mode; std::vector<int32_t> src; };
-  struct Group { std::vector<Target> t; std::vector<int32_t> items; };
+  struct Group { std::vector<Target> t; std::vector<int32_t> items; int32_t sig = -1; };
   auto flush_groups = [&](HostPlan::Sweep& S, std::vector<Group>& groups, int item_base) {
     const int nitem = (int)S.a_off.size() - item_base;
     std::vector<std::vector<int32_t>> of_item(nitem);
@@ -236,6 +240,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       std::sort(g.items.begin(), g.items.end());
       g.items.erase(std::unique(g.items.begin(), g.items.end()), g.items.end());
       S.g_cnt.push_back((int32_t)g.items.size());
+      S.g_sig.push_back(g.sig);
       for (int32_t it : g.items) of_item[it - item_base].push_back(gid);
     }
     for (auto& v : of_item) {
@@ -247,6 +252,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   // ---- forward
   {
     HostPlan::Sweep& S = P.fw;
+    int64_t prow = 0;  // partial rows: unique over the sweep (one launch runs all levels)
     for (int lev = 0; lev < P.nlevels; ++lev) {
       int64_t ktot = 0;
       for (int s : byh[lev]) {
@@ -256,13 +262,13 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       }
       const int KC = kc_for(ktot);
       const int item_base = (int)S.a_off.size();
-      int64_t prow = 0;
       std::vector<Group> groups;
       // W contributions: (target row, partial row, item) in emission order
       std::vector<std::array<int32_t, 3>> contrib;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        cur_sup = s;
         for (int i0 = 0; i0 < ns; i0 += L) {  // D items
           const int kend = std::min(i0 + L, ns), nv = std::min(L, ns - i0);
           const int nit = (kend + KC - 1) / KC;
@@ -272,6 +278,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
           for (int k0 = 0; k0 < kend; k0 += KC) {
             const int k1 = std::min(kend, k0 + KC);
             emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Dval(s, i0 + l, k0 + k); });
+            S.sig.push_back(-1);
             if (nit == 1) {
               S.out.push_back(f + i0);
             } else {
@@ -288,6 +295,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
           for (int k0 = 0; k0 < ns; k0 += KC) {
             const int k1 = std::min(ns, k0 + KC);
             emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Wval(s, i0 + l, k0 + k); });
+            S.sig.push_back(-1);
             S.out.push_back(-(int32_t)(prow / L) - 1);
             for (int l = 0; l < nv; ++l)
               contrib.push_back({P.rows[P.rptr[s] + i0 + l], (int32_t)(prow + l), (int32_t)S.a_off.size() - 1});
@@ -303,6 +311,8 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
         const int a = sup_of_pos[row];
         const int tile = (row - P.sfirst[a]) / L;
         Group g;
+        g.sig = a;
+        S.cd_init[a]++;
         size_t j = i;
         while (j < contrib.size() && sup_of_pos[contrib[j][0]] == a && (contrib[j][0] - P.sfirst[a]) / L == tile) {
           const int r = contrib[j][0];
@@ -320,12 +330,14 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       flush_groups(S, groups, item_base);
       S.lvl_grp.push_back((int32_t)S.g_cnt.size());
       S.lvl_item.push_back((int32_t)S.a_off.size());
-      S.max_partial_rows = std::max(S.max_partial_rows, prow);
     }
+    S.max_partial_rows = prow;
+    for (int s2 = 0; s2 < P.nsup; ++s2) S.wl_ptr.push_back(0);  // forward waits on cd of its own supernode
   }
   // ---- backward (levels top-down; stored in that execution order: level index = H - l)
   {
     HostPlan::Sweep& S = P.bw;
+    int64_t prow = 0;
     for (int lev = P.nlevels - 1; lev >= 0; --lev) {
       int64_t ktot = 0;
       for (int s : byh[lev]) {
@@ -334,17 +346,19 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       }
       const int KC = kc_for(ktot);
       const int item_base = (int)S.a_off.size();
-      int64_t prow = 0;
       std::vector<Group> groups;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        cur_sup = s;
         for (int c0 = 0; c0 < ns; c0 += L) {
+          S.cd_init[s]++;
           const int nv = std::min(L, ns - c0);
           // k-sequence = [D part: rows c0..ns of D_s | W part: rows 0..nr of W_s], cut into items of <= KC
           const int nd = ns - c0, ktot_c = nd + nr;
           const int nit = (ktot_c + KC - 1) / KC;
           Group g;
+          g.sig = s;
           if (nit > 1)
             for (int l = 0; l < nv; ++l) g.t.push_back({f + c0 + l, 0, {}});
           for (int p0 = 0; p0 < ktot_c; p0 += KC) {
@@ -356,6 +370,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
                         return q < nd ? Dval(s, c0 + q, c0 + l) : -Wval(s, q - nd, c0 + l);
                       },
                       nkd);
+            S.sig.push_back(nit == 1 ? s : -1);
             if (nit == 1) {
               S.out.push_back(f + c0);
             } else {
@@ -371,7 +386,17 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       flush_groups(S, groups, item_base);
       S.lvl_grp.push_back((int32_t)S.g_cnt.size());
       S.lvl_item.push_back((int32_t)S.a_off.size());
-      S.max_partial_rows = std::max(S.max_partial_rows, prow);
+    }
+    S.max_partial_rows = prow;
+    // wait list of s: the supernodes owning rows of R_s (their x must be final before W_s^T x[R_s])
+    S.wl_ptr.assign(1, 0);
+    for (int s = 0; s < P.nsup; ++s) {
+      std::vector<int32_t> a;
+      for (int64_t k = P.rptr[s]; k < P.rptr[s + 1]; ++k) a.push_back(sup_of_pos[P.rows[k]]);
+      std::sort(a.begin(), a.end());
+      a.erase(std::unique(a.begin(), a.end()), a.end());
+      for (int32_t v : a) S.wl.push_back(v);
+      S.wl_ptr.push_back((int32_t)S.wl.size());
     }
   }
 }

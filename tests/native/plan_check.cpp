@@ -52,9 +52,22 @@ int main(int argc, char** argv) {
   std::vector<double> z(b), y(N, 0.0), x(N, 0.0);
   auto run = [&](const HostPlan::Sweep& S, std::vector<double>& zsrc, std::vector<double>& direct,
                  std::vector<double>* zsub, bool fwd) {
+    // dataflow invariants of the one-launch sweep: in item order every wait is already satisfied, and
+    // every countdown ends at exactly 0
+    std::vector<int> cd(S.cd_init.begin(), S.cd_init.end()), grem(S.g_cnt.begin(), S.g_cnt.end());
+    std::vector<double> part(S.max_partial_rows + 32, 0.0);
     for (int lev = 0; lev < P.nlevels; ++lev) {
-      std::vector<double> part(S.max_partial_rows + 32, 0.0);
       for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t) {
+        const int su = S.sup[t];
+        if (fwd) {
+          if (cd[su] != 0) { printf("fwd item %d of s=%d runs before its inputs are final\n", t, su); exit(7); }
+        } else if (S.nkd[t] < S.nk[t]) {
+          for (int q = S.wl_ptr[su]; q < S.wl_ptr[su + 1]; ++q)
+            if (cd[S.wl[q]] != 0) { printf("bwd item %d waits on s=%d\n", t, S.wl[q]); exit(8); }
+        }
+        if (S.sig[t] >= 0) cd[S.sig[t]]--;
+        for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q)
+          if (--grem[S.ig[q]] == 0 && S.g_sig[S.ig[q]] >= 0) cd[S.g_sig[S.ig[q]]]--;
         for (int l = 0; l < S.nvalid[t]; ++l) {
           double acc = 0;
           for (int k = 0; k < S.nk[t]; ++k) {
@@ -80,6 +93,8 @@ int main(int argc, char** argv) {
         }
       }
     }
+    for (size_t i = 0; i < cd.size(); ++i)
+      if (cd[i] != 0) { printf("countdown of s=%zu ends at %d\n", i, cd[i]); exit(9); }
   };
   run(P.fw, z, y, &z, true);
   run(P.bw, y, x, nullptr, false);
