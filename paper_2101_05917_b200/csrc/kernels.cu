@@ -704,7 +704,38 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+// ---- TMA bulk copies (cp.async.bulk, 1-D) completing on an mbarrier (tx-count)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded: a byte-count bug becomes a trap (launch error), never a hung GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  for (int64_t i = 0; !mbar_try_wait(bar, parity); ++i)
+    if (i > ((int64_t)1 << 24)) __trap();
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
@@ -748,6 +779,14 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
   double* buf = sm + w * kPS * SD;
+  __shared__ __align__(8) uint64_t mbs[4][kPS];
+  uint64_t* mb = mbs[w];
+  if (lane == 0) {
+    for (int i = 0; i < kPS; ++i) mbar_init(mb + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  unsigned gst = 0;  // stages issued by this warp so far (slot / parity bookkeeping)
   auto take = [&]() {
     int v = 0;
     if (lane == 0) v = atomicAdd(grab + y, 1);
@@ -787,47 +826,60 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
     const int zr = sw.zrow[it];
     const int32_t* idx = rows + sw.zidx[it] - nkd;
     const int nst = (nk + kKS - 1) / kKS;
+    // stage st of this item lives in slot (g0 + st) % kPS with mbarrier parity ((g0 + st) / kPS) & 1
+    const unsigned g0 = gst;
     auto issue = [&](int st) {
-      if (st < nst) {
-        double* As = buf + (st % kPS) * SD;
-        double* Zs = As + kKS * 32;
-        const int k0 = st * kKS, kn = min(kKS, nk - k0);
-        for (int i = lane; i < kn * 16; i += 32) cp_async16(As + 2 * i, Ag + (int64_t)k0 * 32 + 2 * i);
-        if (VEC) {
-          constexpr int H = RC / 2;
-          for (int i = lane; i < kn * H; i += 32) {
-            const int k = i / H, c = 2 * (i - k * H);
-            const int kk = k0 + k;
-            const bool ct = kk < nkd;
-            const int row = ct ? zr + kk : __ldg(idx + kk);
-            if (c < rcn) cp_async16(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-            else *reinterpret_cast<double2*>(Zs + k * RC + c) = make_double2(0.0, 0.0);
-          }
-        } else {
-          for (int i = lane; i < kn * RC; i += 32) {
-            const int k = i / RC, c = i - k * RC;
-            const int kk = k0 + k;
-            const bool ct = kk < nkd;
-            const int row = ct ? zr + kk : __ldg(idx + kk);
-            if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-            else Zs[k * RC + c] = 0.0;
-          }
+      const unsigned gs = g0 + st;
+      const int slot = gs % kPS;
+      double* As = buf + slot * SD;
+      double* Zs = As + kKS * 32;
+      uint64_t* bar = mb + slot;
+      const int k0 = st * kKS, kn = min(kKS, nk - k0);
+      fence_proxy_async();  // generic reads of this slot (previous use) before the async-proxy refill
+      if (VEC) {
+        const bool whole = rcn == RC && RC == R;  // contiguous rows, all columns: one copy
+        if (lane == 0) {
+          mbar_arrive_expect_tx(bar, (unsigned)(kn * 256 + kn * rcn * 8));
+          bulk_g2s(As, Ag + (int64_t)k0 * 32, (unsigned)(kn * 256), bar);
+          if (whole && k0 + kn <= nkd) bulk_g2s(Zs, zc + (int64_t)(zr + k0) * R, (unsigned)(kn * R * 8), bar);
         }
+        if (!(whole && k0 + kn <= nkd) && lane < kn) {
+          const int kk = k0 + lane;
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          bulk_g2s(Zs + lane * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), bar);
+        }
+      } else {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(bar, (unsigned)(kn * 256));
+          bulk_g2s(As, Ag + (int64_t)k0 * 32, (unsigned)(kn * 256), bar);
+        }
+        for (int i = lane; i < kn * RC; i += 32) {
+          const int k = i / RC, c = i - k * RC;
+          const int kk = k0 + k;
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
+          else Zs[k * RC + c] = 0.0;
+        }
+        cp_async_commit();
       }
-      cp_async_commit();
     };
     double acc[4][CW];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-#pragma unroll
-    for (int st = 0; st < kPS - 1; ++st) issue(st);
+    for (int st = 0; st < kPS - 1 && st < nst; ++st) issue(st);
     for (int st = 0; st < nst; ++st) {
-      issue(st + kPS - 1);
-      cp_async_wait_group<kPS - 1>();
-      __syncwarp();
-      const double* As = buf + (st % kPS) * SD;
+      if (st + kPS - 1 < nst) issue(st + kPS - 1);
+      const unsigned gs = g0 + st;
+      mbar_wait(mb + gs % kPS, (gs / kPS) & 1);
+      if (!VEC) {
+        cp_async_wait_all();
+        __syncwarp();
+      }
+      const double* As = buf + (gs % kPS) * SD;
       const double* Zs = As + kKS * 32;
       const int kn = min(kKS, nk - st * kKS);
       for (int k = 0; k < kn; ++k) {
@@ -853,8 +905,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       }
       __syncwarp();
     }
-    cp_async_wait_group<0>();
-    __syncwarp();
+    gst = g0 + nst;
     // ---- output
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];
