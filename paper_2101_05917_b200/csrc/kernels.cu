@@ -822,6 +822,8 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       }
     }
     __syncwarp();
+    // the acquired rows were written through the generic proxy; the TMA reads below use the async proxy
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
     const double* Ag = sw.A + sw.a_off[it];
     const int zr = sw.zrow[it];
     const int32_t* idx = rows + sw.zidx[it] - nkd;
