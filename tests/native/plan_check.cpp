@@ -56,6 +56,14 @@ int main(int argc, char** argv) {
     // every countdown ends at exactly 0
     std::vector<int> cd(S.cd_init.begin(), S.cd_init.end()), grem(S.g_cnt.begin(), S.g_cnt.end());
     std::vector<double> part(S.max_partial_rows + 32, 0.0);
+    {  // a row is the target of at most one group (no concurrent read-modify-write of the same row)
+      std::vector<int> hits(2 * N, 0);  // per destination vector (mode 0: y/x assign, mode 1: z subtract)
+      for (size_t r = 0; r < S.red_row.size(); ++r)
+        if (++hits[S.red_mode[r] * N + S.red_row[r]] > 1) {
+          printf("row %d is targeted by two groups\n", S.red_row[r]);
+          exit(10);
+        }
+    }
     for (int lev = 0; lev < P.nlevels; ++lev) {
       for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t) {
         const int su = S.sup[t];
@@ -65,9 +73,6 @@ int main(int argc, char** argv) {
           for (int q = S.wl_ptr[su]; q < S.wl_ptr[su + 1]; ++q)
             if (cd[S.wl[q]] != 0) { printf("bwd item %d waits on s=%d\n", t, S.wl[q]); exit(8); }
         }
-        if (S.sig[t] >= 0) cd[S.sig[t]]--;
-        for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q)
-          if (--grem[S.ig[q]] == 0 && S.g_sig[S.ig[q]] >= 0) cd[S.g_sig[S.ig[q]]]--;
         for (int l = 0; l < S.nvalid[t]; ++l) {
           double acc = 0;
           for (int k = 0; k < S.nk[t]; ++k) {
@@ -78,21 +83,23 @@ int main(int argc, char** argv) {
           if (S.out[t] >= 0) direct[S.out[t] + l] = acc;
           else part[(int64_t)(-S.out[t] - 1) * 32 + l] = acc;
         }
-      }
-      // every item lists each group it feeds exactly once, and each group counts its items
-      for (int g = S.lvl_grp[lev]; g < S.lvl_grp[lev + 1]; ++g) {
-        int cnt = 0;
-        for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t)
-          for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q) cnt += S.ig[q] == g;
-        if (cnt != S.g_cnt[g]) { printf("group %d count %d != %d\n", g, cnt, S.g_cnt[g]); exit(6); }
-        for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
-          double acc = 0;
-          for (int q = S.red_ptr[r]; q < S.red_ptr[r + 1]; ++q) acc += part[S.red_src[q]];
-          if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
-          else (*zsub)[S.red_row[r]] -= acc;
+        if (S.sig[t] >= 0) cd[S.sig[t]]--;
+        // device semantics: the item that brings a group to zero applies the group's sums, then signals
+        for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q) {
+          const int g = S.ig[q];
+          if (--grem[g] != 0) continue;
+          for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
+            double acc = 0;
+            for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
+            if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
+            else (*zsub)[S.red_row[r]] -= acc;
+          }
+          if (S.g_sig[g] >= 0) cd[S.g_sig[g]]--;
         }
       }
     }
+    for (size_t g = 0; g < grem.size(); ++g)
+      if (grem[g] != 0) { printf("group %zu never completes (%d left)\n", g, grem[g]); exit(6); }
     for (size_t i = 0; i < cd.size(); ++i)
       if (cd[i] != 0) { printf("countdown of s=%zu ends at %d\n", i, cd[i]); exit(9); }
   };
