@@ -50,6 +50,7 @@ struct pd_sim {
   SweepDev swf{}, swb{};
   int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
   int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
+  int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
   int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
@@ -228,6 +229,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
   // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
   CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY, s->stream));
+  CK(cudaMemsetAsync(s->turn, 0, sizeof(int32_t) * (size_t)std::max(1, P.fw.ntiles) * kGY, s->stream));
   CK(cudaMemcpyAsync(s->cd_f, s->cd_f0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
   CK(cudaMemcpyAsync(s->cd_b, s->cd_b0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
   auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab) {
@@ -237,7 +239,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
     k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
         d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-        cd, grab);
+        cd, grab, s->turn);
     LAUNCH_CHECK(s);
   };
   const HostPlan::Sweep& F = P.fw;
@@ -617,6 +619,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.g_sig = s->upload(S.g_sig);
       d.wl_ptr = s->upload(S.wl_ptr);
       d.wl = s->upload(S.wl);
+      d.g_tile = s->upload(S.g_tile);
+      d.g_turn = s->upload(S.g_turn);
     };
     // group countdown counters, one slot per column chunk, armed with the group's item count
     auto up_cnt = [&](const HostPlan::Sweep& S) {
@@ -626,6 +630,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       return s->upload(c);
     };
     s->grab = s->alloc<int32_t>(4 * kGY);
+    s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
     auto up_cd = [&](const HostPlan::Sweep& S) {
       std::vector<int32_t> c((size_t)P.nsup * kGY);
       for (int u = 0; u < P.nsup; ++u)

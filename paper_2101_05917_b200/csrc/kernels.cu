@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                     double* __restrict__ zsub, double* __restrict__ partial,
                                                     int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
-                                                    int32_t* __restrict__ grab) {
+                                                    int32_t* __restrict__ grab, int32_t* __restrict__ turn) {
   constexpr int CW = RC / 4;
   constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
@@ -932,6 +932,15 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (!last) continue;
+      const int tile = sw.g_tile[g];
+      if (tile >= 0 && lane == 0) {  // z-row tiles apply their per-level groups in level order
+        int64_t spins = 0;
+        while (ld_acquire(turn + (int64_t)tile * kGY + y) != sw.g_turn[g]) {
+          __nanosleep(32);
+          if (++spins > (int64_t)1 << 26) __trap();
+        }
+      }
+      __syncwarp();
       __threadfence();
       const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
       if (lane < nt) {
@@ -939,6 +948,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
         double v[RC];
 #pragma unroll
         for (int c = 0; c < RC; ++c) v[c] = 0.0;
+#pragma unroll 4
         for (int u = sw.red_ptr[t]; u < sw.red_ptr[t + 1]; ++u) {
           const double* pr = partial + (int64_t)sw.red_src[u] * R + c0;
           if (VEC) {
@@ -962,6 +972,13 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
           if (c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
       }
       if (lane == 0) gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
+      if (tile >= 0) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(turn + (int64_t)tile * kGY + y, 1);
+        }
+      }
       if (sw.g_sig[g] >= 0) signal(sw.g_sig[g]);
     }
   }

@@ -31,7 +31,7 @@ struct SweepDev {  // device copy of HostPlan::Sweep
   const int32_t *nk, *nkd, *zrow, *out, *nvalid;
   const int32_t *ig_ptr, *ig, *g_tptr, *g_cnt;
   const int32_t *red_row, *red_mode, *red_ptr, *red_src;
-  const int32_t *sup, *sig, *g_sig, *wl_ptr, *wl;
+  const int32_t *sup, *sig, *g_sig, *wl_ptr, *wl, *g_tile, *g_turn;
 };
 
 struct DotArgs {

@@ -68,6 +68,9 @@ struct HostPlan {
     std::vector<int32_t> sup;          // per item: its supernode
     std::vector<int32_t> sig;          // per item: supernode whose countdown it decrements when done (-1)
     std::vector<int32_t> g_sig;        // per group: supernode whose countdown the group decrements (-1)
+    std::vector<int32_t> g_tile;       // per group: z-row tile it subtracts into (-1: assign groups)
+    std::vector<int32_t> g_turn;       //   and its turn among that tile's groups (level order)
+    int32_t ntiles = 0;
     std::vector<int32_t> cd_init;      // per supernode: countdown start (fwd: W groups into it;
                                        //   bwd: its 32-column chunks)
     std::vector<int32_t> wl_ptr, wl;   // per supernode: supernodes whose countdown must be 0 first

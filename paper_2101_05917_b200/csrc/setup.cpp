@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <numeric>
 #include <omp.h>
 
@@ -224,7 +225,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   };
   // a level's reduction groups: targets (row, mode, contributions in order), contributing items
   struct Target { int32_t row, mode; std::vector<int32_t> src; };
-  struct Group { std::vector<Target> t; std::vector<int32_t> items; int32_t sig = -1; };
+  struct Group { std::vector<Target> t; std::vector<int32_t> items; int32_t sig = -1, tile = -1, turn = 0; };
   auto flush_groups = [&](HostPlan::Sweep& S, std::vector<Group>& groups, int item_base) {
     const int nitem = (int)S.a_off.size() - item_base;
     std::vector<std::vector<int32_t>> of_item(nitem);
@@ -241,6 +242,8 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
       g.items.erase(std::unique(g.items.begin(), g.items.end()), g.items.end());
       S.g_cnt.push_back((int32_t)g.items.size());
       S.g_sig.push_back(g.sig);
+      S.g_tile.push_back(g.tile);
+      S.g_turn.push_back(g.turn);
       for (int32_t it : g.items) of_item[it - item_base].push_back(gid);
     }
     for (auto& v : of_item) {
@@ -253,11 +256,9 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   {
     HostPlan::Sweep& S = P.fw;
     int64_t prow = 0;  // partial rows: unique over the sweep (one launch runs all levels)
-    std::vector<Group> groups;
-    // W contributions over ALL levels: (target row, partial row, item) in emission order.  One group per
-    // 32-row tile of an ancestor collects every level's contributions, so the read-modify-write of z
-    // rows happens exactly once per tile (no two groups ever update the same rows).
-    std::vector<std::array<int32_t, 3>> contrib;
+    // z-row tiles (32 rows of one supernode) receive one W group per level that touches them; the groups
+    // of a tile take turns in level order (deterministic order of the read-modify-writes of z)
+    std::map<std::pair<int, int>, std::pair<int, int>> tiles;  // (sup, tile) -> (tile id, groups so far)
     for (int lev = 0; lev < P.nlevels; ++lev) {
       int64_t ktot = 0;
       for (int s : byh[lev]) {
@@ -266,6 +267,9 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
         ktot += (int64_t)((nr + L - 1) / L) * ns;
       }
       const int KC = kc_for(ktot);
+      const int item_base = (int)S.a_off.size();
+      std::vector<Group> groups;
+      std::vector<std::array<int32_t, 3>> contrib;  // (target row, partial row, item), emission order
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
@@ -304,34 +308,37 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
           }
         }
       }
+      std::stable_sort(contrib.begin(), contrib.end(),
+                       [](const std::array<int32_t, 3>& x, const std::array<int32_t, 3>& y) { return x[0] < y[0]; });
+      for (size_t i = 0; i < contrib.size();) {
+        const int row = contrib[i][0];
+        const int a = sup_of_pos[row];
+        const int tile = (row - P.sfirst[a]) / L;
+        Group g;
+        g.sig = a;
+        S.cd_init[a]++;
+        auto ins = tiles.insert({{a, tile}, {(int)tiles.size(), 0}}).first;
+        g.tile = ins->second.first;
+        g.turn = ins->second.second++;
+        size_t j = i;
+        while (j < contrib.size() && sup_of_pos[contrib[j][0]] == a && (contrib[j][0] - P.sfirst[a]) / L == tile) {
+          const int r = contrib[j][0];
+          Target t{r, 1, {}};
+          while (j < contrib.size() && contrib[j][0] == r) {
+            t.src.push_back(contrib[j][1]);
+            g.items.push_back(contrib[j][2]);
+            ++j;
+          }
+          g.t.push_back(std::move(t));
+        }
+        groups.push_back(std::move(g));
+        i = j;
+      }
+      flush_groups(S, groups, item_base);
+      S.lvl_grp.push_back((int32_t)S.g_cnt.size());
       S.lvl_item.push_back((int32_t)S.a_off.size());
     }
-    std::stable_sort(contrib.begin(), contrib.end(),
-                     [](const std::array<int32_t, 3>& x, const std::array<int32_t, 3>& y) { return x[0] < y[0]; });
-    for (size_t i = 0; i < contrib.size();) {
-      const int row = contrib[i][0];
-      const int a = sup_of_pos[row];
-      const int tile = (row - P.sfirst[a]) / L;
-      Group g;
-      g.sig = a;
-      S.cd_init[a]++;
-      size_t j = i;
-      while (j < contrib.size() && sup_of_pos[contrib[j][0]] == a && (contrib[j][0] - P.sfirst[a]) / L == tile) {
-        const int r = contrib[j][0];
-        Target t{r, 1, {}};
-        while (j < contrib.size() && contrib[j][0] == r) {
-          t.src.push_back(contrib[j][1]);
-          g.items.push_back(contrib[j][2]);
-          ++j;
-        }
-        g.t.push_back(std::move(t));
-      }
-      groups.push_back(std::move(g));
-      i = j;
-    }
-    flush_groups(S, groups, 0);
-    S.lvl_grp.assign(P.nlevels + 1, (int32_t)S.g_cnt.size());  // groups span levels in the forward sweep
-    S.lvl_grp[0] = 0;
+    S.ntiles = (int32_t)tiles.size();
     S.max_partial_rows = prow;
     for (int s2 = 0; s2 < P.nsup; ++s2) S.wl_ptr.push_back(0);  // forward waits on cd of its own supernode
   }

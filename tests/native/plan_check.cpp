@@ -55,13 +55,24 @@ int main(int argc, char** argv) {
     // dataflow invariants of the one-launch sweep: in item order every wait is already satisfied, and
     // every countdown ends at exactly 0
     std::vector<int> cd(S.cd_init.begin(), S.cd_init.end()), grem(S.g_cnt.begin(), S.g_cnt.end());
+    std::vector<int> turn(S.ntiles, 0);
     std::vector<double> part(S.max_partial_rows + 32, 0.0);
     {  // a row is the target of at most one group (no concurrent read-modify-write of the same row)
-      std::vector<int> hits(2 * N, 0);  // per destination vector (mode 0: y/x assign, mode 1: z subtract)
-      for (size_t r = 0; r < S.red_row.size(); ++r)
-        if (++hits[S.red_mode[r] * N + S.red_row[r]] > 1) {
-          printf("row %d is targeted by two groups\n", S.red_row[r]);
-          exit(10);
+      // mode 0 (y/x assign): exactly one group per row; mode 1 (z subtract): every group of a row belongs
+      // to the same tile, whose groups are serialised by their turns
+      std::vector<int> hits(N, 0), tile_of(N, -1);
+      for (size_t g = 0; g < S.g_cnt.size(); ++g)
+        for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
+          const int row = S.red_row[r];
+          if (S.red_mode[r] == 0) {
+            if (++hits[row] > 1) { printf("row %d assigned by two groups\n", row); exit(10); }
+          } else {
+            if (S.g_tile[g] < 0 || (tile_of[row] >= 0 && tile_of[row] != S.g_tile[g])) {
+              printf("row %d updated by groups of different tiles\n", row);
+              exit(10);
+            }
+            tile_of[row] = S.g_tile[g];
+          }
         }
     }
     for (int lev = 0; lev < P.nlevels; ++lev) {
@@ -88,6 +99,7 @@ int main(int argc, char** argv) {
         for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q) {
           const int g = S.ig[q];
           if (--grem[g] != 0) continue;
+          if (S.g_tile[g] >= 0 && turn[S.g_tile[g]]++ != S.g_turn[g]) { printf("group %d out of turn\n", g); exit(11); }
           for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
             double acc = 0;
             for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
