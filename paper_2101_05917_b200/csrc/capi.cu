@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -51,6 +52,7 @@ struct pd_sim {
   int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
   int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
   int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
+  int64_t* trace = nullptr;                     // K3 per-item timeline (debug hook, pd_debug_trace)
   int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
@@ -239,7 +241,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
     k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
         d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-        cd, grab, s->turn);
+        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)6 * P.fw.a_off.size()) + (int64_t)6 * t0 : nullptr);
     LAUNCH_CHECK(s);
   };
   const HostPlan::Sweep& F = P.fw;
@@ -631,6 +633,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     };
     s->grab = s->alloc<int32_t>(4 * kGY);
     s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
+    if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(6 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
     auto up_cd = [&](const HostPlan::Sweep& S) {
       std::vector<int32_t> c((size_t)P.nsup * kGY);
       for (int u = 0; u < P.nsup; ++u)
@@ -738,6 +741,16 @@ pd_status pd_profile(const pd_sim* s, double* ms, int64_t* count, int32_t n) {
     if (ms) ms[k] = s->prof_ms[k];
     if (count) count[k] = s->prof_cnt[k];
   }
+  return PD_OK;
+}
+
+pd_status pd_debug_k3_trace(const pd_sim* s, int64_t* out, int64_t n, int64_t* count) {
+  if (!s || !count) return PD_ERR_INVALID_ARGUMENT;
+  if (!s->trace) return PD_ERR_STATE;
+  const int64_t tot = 6 * (int64_t)(s->plan.fw.a_off.size() + s->plan.bw.a_off.size());
+  *count = tot;
+  if (out && n > 0 && cudaMemcpy(out, s->trace, sizeof(int64_t) * std::min(n, tot), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return PD_ERR_CUDA;
   return PD_OK;
 }
 

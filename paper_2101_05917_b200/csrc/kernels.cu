@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                     double* __restrict__ zsub, double* __restrict__ partial,
                                                     int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
-                                                    int32_t* __restrict__ grab, int32_t* __restrict__ turn) {
+                                                    int32_t* __restrict__ grab, int32_t* __restrict__ turn,
+                                                    int64_t* __restrict__ trace) {
   constexpr int CW = RC / 4;
   constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
@@ -799,9 +800,16 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       atomicSub(cd + (int64_t)sup * kGY + y, 1);
     }
   };
+  auto gtime = []() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return (int64_t)t;
+  };
   int next = take();
   while (next < nitems) {
     const int it = t0 + next;
+    int64_t* tr = (trace && y == 0) ? trace + (int64_t)next * 6 : nullptr;  // [start, deps, data, end, smid, warp]
+    if (tr && lane == 0) tr[0] = gtime();
     next = take();  // prefetch the next index (never waited on before this item is done)
     const int nk = sw.nk[it], nkd = sw.nkd[it];
     // ---- wait until the item's right-hand-side rows are final
@@ -822,6 +830,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       }
     }
     __syncwarp();
+    if (tr && lane == 0) tr[1] = gtime();
     // the acquired rows were written through the generic proxy; the TMA reads below use the async proxy
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     const double* Ag = sw.A + sw.a_off[it];
@@ -908,6 +917,13 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       __syncwarp();
     }
     gst = g0 + nst;
+    if (tr && lane == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      tr[2] = gtime();
+      tr[4] = smid;
+      tr[5] = blockIdx.x * 4 + w;
+    }
     // ---- output
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];
@@ -920,6 +936,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
         if (4 * rg + r < nv && cg * CW + c < rcn) dst[(int64_t)(4 * rg + r) * R + cg * CW + c] = acc[r][c];
     if (out >= 0) {
       if (sw.sig[it] >= 0) signal(sw.sig[it]);
+      if (tr && lane == 0) tr[3] = gtime();
       continue;
     }
     __syncwarp();
@@ -981,6 +998,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
       }
       if (sw.g_sig[g] >= 0) signal(sw.g_sig[g]);
     }
+    if (tr && lane == 0) tr[3] = gtime();
   }
   cp_async_wait_group<0>();
 }

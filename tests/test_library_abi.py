@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "diffpd_b200.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(pd_[a-z_A-Z]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(pd_[a-z_A-Z0-9]+)\s*\(", src)))
 
 
 def test_library_builds_and_exports_header_symbols():

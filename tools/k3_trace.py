@@ -1,0 +1,39 @@
+"""Timeline of one K3 solve (PD_K3_TRACE=1): per level, span, time waiting for inputs, data, reductions."""
+import os
+import sys
+
+os.environ["PD_K3_TRACE"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+import paper_2101_05917_b200 as pdb
+from pd_inputs import get_config, make_inputs
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+inp = make_inputs(get_config(name), steps=1)
+sim = pdb.simulator_from_inputs(inp, contact_nodes=())
+B, N = inp["B"], 3 * inp["n_nodes"]
+rhs = torch.randn((B, N), dtype=torch.float64, device="cuda")
+out = torch.zeros_like(rhs)
+for _ in range(3):
+    sim.apply_Ainv(rhs, out)
+torch.cuda.synchronize()
+tr = sim.k3_trace()
+ok = tr[:, 0] > 0
+t0 = tr[ok, 0].min()
+tr = tr.astype(np.float64)
+tr[:, :4] = (tr[:, :4] - t0) / 1e3  # us
+nf = (tr.shape[0])
+print("items", tr.shape[0], "span us %.1f" % (tr[ok, 3].max()))
+wait = tr[ok, 1] - tr[ok, 0]
+data = tr[ok, 2] - tr[ok, 1]
+tail = tr[ok, 3] - tr[ok, 2]
+print("per item us: wait mean %.1f max %.1f | data+compute mean %.1f max %.1f | output/reduce mean %.1f max %.1f" % (
+    wait.mean(), wait.max(), data.mean(), data.max(), tail.mean(), tail.max()))
+# coarse timeline: items finished per 10 us bucket
+end = tr[ok, 3]
+hist, edges = np.histogram(end, bins=40)
+print("completions per bucket:", hist.tolist(), "bucket us %.1f" % (edges[1] - edges[0]))
+warps = np.unique(tr[ok, 5]).size
+print("warps used", warps, "SMs", np.unique(tr[ok, 4]).size)
