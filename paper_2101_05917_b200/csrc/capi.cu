@@ -222,12 +222,13 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
   if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
-  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
+  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC, sweep_wpc<RC>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
   // one resident wave: warps take items round-robin, so CTAs beyond residency would only add a tail
   int per_sm = 0, nsm = 0, dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, sweep_smem_bytes<RC>()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC, sweep_wpc<RC>()>, 32 * sweep_wpc<RC>(),
+                                                   sweep_smem_bytes<RC>()));
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
   // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
   CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY, s->stream));
@@ -238,8 +239,9 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     if (!nt) return;
     // forward: sources z (S0), direct y (S2), group subtract into z (S0);
     // backward: D part y (S2), W part x (S0), direct x (S0)
-    const unsigned gx = (unsigned)std::min<int64_t>((nt + 3) / 4, std::max<int64_t>(1, resident / gy));
-    k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
+    constexpr int wpc = sweep_wpc<RC>();
+    const unsigned gx = (unsigned)std::min<int64_t>((nt + wpc - 1) / wpc, std::max<int64_t>(1, resident / gy));
+    k_sweep_flow<RC, VEC, wpc><<<dim3(gx, gy), 32 * wpc, sweep_smem_bytes<RC>(), s->stream>>>(
         d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
         cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)6 * P.fw.a_off.size()) + (int64_t)6 * t0 : nullptr);
     LAUNCH_CHECK(s);

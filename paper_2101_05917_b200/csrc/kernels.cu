@@ -739,10 +739,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+constexpr int kItemK = 128;  // max k-steps per item (the planner's kc)
 template <int RC>
-__host__ __device__ constexpr int sweep_warp_doubles() { return kPS * kKS * (32 + RC); }
+__host__ __device__ constexpr int sweep_item_doubles() { return kItemK * (32 + RC); }
+// warps per CTA: as many whole-item buffers as fit in 227 KB of shared memory (at most 4)
 template <int RC>
-__host__ __device__ constexpr int sweep_smem_bytes() { return 4 * sweep_warp_doubles<RC>() * 8; }
+__host__ __device__ constexpr int sweep_wpc() {
+  return (232448 / (sweep_item_doubles<RC>() * 8)) >= 4 ? 4 : (232448 / (sweep_item_doubles<RC>() * 8));
+}
+template <int RC>
+__host__ __device__ constexpr int sweep_smem_bytes() { return sweep_wpc<RC>() * sweep_item_doubles<RC>() * 8; }
 
 // K3 v5: ONE launch per sweep (dataflow).  Items are taken in the planned order (levels in sweep order)
 // through one integer counter; before reading its right-hand-side rows an item waits until they are
@@ -763,8 +769,8 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-template <int RC, bool VEC>
-__global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
+template <int RC, bool VEC, int WPC>
+__global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
                                                     const double* __restrict__ zc, const double* __restrict__ zi,
                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                     double* __restrict__ zsub, double* __restrict__ partial,
@@ -772,22 +778,21 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
                                                     int32_t* __restrict__ grab, int32_t* __restrict__ turn,
                                                     int64_t* __restrict__ trace) {
   constexpr int CW = RC / 4;
-  constexpr int SD = kKS * (32 + RC);
   extern __shared__ __align__(16) double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rg = lane & 7, cg = lane >> 3;
   const int y = blockIdx.y;
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
-  double* buf = sm + w * kPS * SD;
-  __shared__ __align__(8) uint64_t mbs[4][kPS];
-  uint64_t* mb = mbs[w];
+  double* buf = sm + w * sweep_item_doubles<RC>();
+  __shared__ __align__(8) uint64_t mbs[WPC];
+  uint64_t* mb = mbs + w;
   if (lane == 0) {
-    for (int i = 0; i < kPS; ++i) mbar_init(mb + i, 1);
+    mbar_init(mb, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
-  unsigned gst = 0;  // stages issued by this warp so far (slot / parity bookkeeping)
+  unsigned gst = 0;  // items loaded by this warp so far (mbarrier parity)
   auto take = [&]() {
     int v = 0;
     if (lane == 0) v = atomicAdd(grab + y, 1);
@@ -836,93 +841,75 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
     const double* Ag = sw.A + sw.a_off[it];
     const int zr = sw.zrow[it];
     const int32_t* idx = rows + sw.zidx[it] - nkd;
-    const int nst = (nk + kKS - 1) / kKS;
-    // stage st of this item lives in slot (g0 + st) % kPS with mbarrier parity ((g0 + st) / kPS) & 1
-    const unsigned g0 = gst;
-    auto issue = [&](int st) {
-      const unsigned gs = g0 + st;
-      const int slot = gs % kPS;
-      double* As = buf + slot * SD;
-      double* Zs = As + kKS * 32;
-      uint64_t* bar = mb + slot;
-      const int k0 = st * kKS, kn = min(kKS, nk - k0);
-      fence_proxy_async();  // generic reads of this slot (previous use) before the async-proxy refill
-      if (VEC) {
-        const bool whole = rcn == RC && RC == R;  // contiguous rows, all columns: one copy
-        if (lane == 0) {
-          mbar_arrive_expect_tx(bar, (unsigned)(kn * 256 + kn * rcn * 8));
-          bulk_g2s(As, Ag + (int64_t)k0 * 32, (unsigned)(kn * 256), bar);
-          if (whole && k0 + kn <= nkd) bulk_g2s(Zs, zc + (int64_t)(zr + k0) * R, (unsigned)(kn * R * 8), bar);
-        }
-        if (!(whole && k0 + kn <= nkd) && lane < kn) {
-          const int kk = k0 + lane;
-          const bool ct = kk < nkd;
-          const int row = ct ? zr + kk : __ldg(idx + kk);
-          bulk_g2s(Zs + lane * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), bar);
-        }
-      } else {
-        if (lane == 0) {
-          mbar_arrive_expect_tx(bar, (unsigned)(kn * 256));
-          bulk_g2s(As, Ag + (int64_t)k0 * 32, (unsigned)(kn * 256), bar);
-        }
-        for (int i = lane; i < kn * RC; i += 32) {
-          const int k = i / RC, c = i - k * RC;
-          const int kk = k0 + k;
-          const bool ct = kk < nkd;
-          const int row = ct ? zr + kk : __ldg(idx + kk);
-          if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-          else Zs[k * RC + c] = 0.0;
-        }
-        cp_async_commit();
+    // ---- the whole item (<= kItemK k-steps: factor block + right-hand-side rows) in one TMA round
+    double* As = buf;
+    double* Zs = buf + kItemK * 32;
+    fence_proxy_async();  // generic reads of the previous item before the async-proxy refill
+    if (VEC) {
+      const bool whole = rcn == RC && RC == R && nkd == nk;  // contiguous rows, all columns: one copy
+      if (lane == 0) {
+        mbar_arrive_expect_tx(mb, (unsigned)(nk * 256 + nk * rcn * 8));
+        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
+        if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb);
       }
-    };
+      if (!whole)
+        for (int kk = lane; kk < nk; kk += 32) {
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          bulk_g2s(Zs + kk * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), mb);
+        }
+    } else {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(mb, (unsigned)(nk * 256));
+        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
+      }
+      for (int i = lane; i < nk * RC; i += 32) {
+        const int k = i / RC, c = i - k * RC;
+        const bool ct = k < nkd;
+        const int row = ct ? zr + k : __ldg(idx + k);
+        if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
+        else Zs[k * RC + c] = 0.0;
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+    }
     double acc[4][CW];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-    for (int st = 0; st < kPS - 1 && st < nst; ++st) issue(st);
-    for (int st = 0; st < nst; ++st) {
-      if (st + kPS - 1 < nst) issue(st + kPS - 1);
-      const unsigned gs = g0 + st;
-      mbar_wait(mb + gs % kPS, (gs / kPS) & 1);
-      if (!VEC) {
-        cp_async_wait_all();
-        __syncwarp();
-      }
-      const double* As = buf + (gs % kPS) * SD;
-      const double* Zs = As + kKS * 32;
-      const int kn = min(kKS, nk - st * kKS);
-      for (int k = 0; k < kn; ++k) {
-        const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
-        const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
-        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-        double zv[CW];
-        if (CW % 2 == 0) {
+    mbar_wait(mb, gst & 1);
+    __syncwarp();
+    if (tr && lane == 0) tr[2] = gtime();
+#pragma unroll 2
+    for (int k = 0; k < nk; ++k) {
+      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
+      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      double zv[CW];
+      if (CW % 2 == 0) {
 #pragma unroll
-          for (int c = 0; c < CW / 2; ++c) {
-            const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
-            zv[2 * c] = t.x;
-            zv[2 * c + 1] = t.y;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+        for (int c = 0; c < CW / 2; ++c) {
+          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
+          zv[2 * c] = t.x;
+          zv[2 * c + 1] = t.y;
         }
+      } else {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
       }
-      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
     }
-    gst = g0 + nst;
+    __syncwarp();
+    ++gst;
     if (tr && lane == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      tr[2] = gtime();
       tr[4] = smid;
-      tr[5] = blockIdx.x * 4 + w;
+      tr[5] = blockIdx.x * WPC + w;
     }
     // ---- output
     const int out = sw.out[it];

@@ -208,7 +208,8 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   auto kc_for = [&](int64_t ktot) {
     int64_t kc = (ktot + P.warps_target - 1) / P.warps_target;
     kc = (kc + 7) / 8 * 8;
-    return (int)std::max<int64_t>(128, std::min<int64_t>(256, kc));  // >= 128: partial rows stay <= R/128 of the bytes
+    (void)kc;
+    return 128;  // = kItemK: one item (32 x 128 factor block + 128 rhs rows) per warp buffer, one TMA round
   };
   // one item: k-major block rows/cols of `val(k, lane)`, k = 0..nk
   int cur_sup = -1;
