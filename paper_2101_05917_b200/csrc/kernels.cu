@@ -763,6 +763,14 @@ __host__ __device__ constexpr int sweep_smem_bytes() { return sweep_wpc<RC>() * 
 // atomics are integer; every floating-point sum has a fixed order -> bitwise reproducible.
 constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group / supernode
 
+__device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(int32_t* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -798,12 +806,9 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
     if (lane == 0) v = atomicAdd(grab + y, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
-  auto signal = [&](int sup) {  // all lanes' prior stores -> release -> countdown
+  auto signal = [&](int sup) {  // all lanes' prior stores (warp barrier, cumulativity) -> release countdown
     __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      atomicSub(cd + (int64_t)sup * kGY + y, 1);
-    }
+    if (lane == 0) red_add_release(cd + (int64_t)sup * kGY + y, -1);
   };
   auto gtime = []() {
     uint64_t t;
@@ -930,11 +935,8 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
     for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
       const int g = sw.ig[q];
       int last = 0;
-      if (lane == 0) {
-        __threadfence();
-        last = atomicSub(gcnt + (int64_t)g * kGY + y, 1) == 1;
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
+      if (lane == 0) last = atom_add_acq_rel(gcnt + (int64_t)g * kGY + y, -1) == 1;  // release partials,
+      last = __shfl_sync(0xffffffffu, last, 0);                                        // acquire the others'
       if (!last) continue;
       const int tile = sw.g_tile[g];
       if (tile >= 0 && lane == 0) {  // z-row tiles apply their per-level groups in level order
@@ -945,7 +947,6 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
         }
       }
       __syncwarp();
-      __threadfence();
       const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
       if (lane < nt) {
         const int t = tb + lane;
@@ -978,10 +979,7 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
       if (lane == 0) gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
       if (tile >= 0) {
         __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(turn + (int64_t)tile * kGY + y, 1);
-        }
+        if (lane == 0) red_add_release(turn + (int64_t)tile * kGY + y, 1);
       }
       if (sw.g_sig[g] >= 0) signal(sw.g_sig[g]);
     }

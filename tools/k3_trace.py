@@ -37,3 +37,12 @@ hist, edges = np.histogram(end, bins=40)
 print("completions per bucket:", hist.tolist(), "bucket us %.1f" % (edges[1] - edges[0]))
 warps = np.unique(tr[ok, 5]).size
 print("warps used", warps, "SMs", np.unique(tr[ok, 4]).size)
+
+# item-index windows (items are in level order: forward first, then backward)
+nwin = 16
+edges = np.linspace(0, tr.shape[0], nwin + 1).astype(int)
+for a, b in zip(edges[:-1], edges[1:]):
+    w = tr[a:b]
+    w = w[w[:, 0] > -1e9]
+    print("items %6d-%6d start %7.1f end %7.1f | wait %6.1f data %5.1f out %6.1f" % (
+        a, b, w[:, 0].min(), w[:, 3].max(), (w[:, 1] - w[:, 0]).mean(), (w[:, 2] - w[:, 1]).mean(), (w[:, 3] - w[:, 2]).mean()))
