@@ -222,13 +222,12 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
   if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
-  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC, sweep_wpc<RC>()>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
+  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
   // one resident wave: warps take items round-robin, so CTAs beyond residency would only add a tail
   int per_sm = 0, nsm = 0, dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC, sweep_wpc<RC>()>, 32 * sweep_wpc<RC>(),
-                                                   sweep_smem_bytes<RC>()));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, sweep_smem_bytes<RC>()));
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
   // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
   CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY, s->stream));
@@ -239,11 +238,10 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     if (!nt) return;
     // forward: sources z (S0), direct y (S2), group subtract into z (S0);
     // backward: D part y (S2), W part x (S0), direct x (S0)
-    constexpr int wpc = sweep_wpc<RC>();
-    const unsigned gx = (unsigned)std::min<int64_t>((nt + wpc - 1) / wpc, std::max<int64_t>(1, resident / gy));
-    k_sweep_flow<RC, VEC, wpc><<<dim3(gx, gy), 32 * wpc, sweep_smem_bytes<RC>(), s->stream>>>(
+    const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident / gy));
+    k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
         d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)6 * P.fw.a_off.size()) + (int64_t)6 * t0 : nullptr);
+        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : nullptr);
     LAUNCH_CHECK(s);
   };
   const HostPlan::Sweep& F = P.fw;
@@ -635,7 +633,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     };
     s->grab = s->alloc<int32_t>(4 * kGY);
     s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
-    if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(6 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
+    if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(8 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
     auto up_cd = [&](const HostPlan::Sweep& S) {
       std::vector<int32_t> c((size_t)P.nsup * kGY);
       for (int u = 0; u < P.nsup; ++u)
@@ -749,7 +747,7 @@ pd_status pd_profile(const pd_sim* s, double* ms, int64_t* count, int32_t n) {
 pd_status pd_debug_k3_trace(const pd_sim* s, int64_t* out, int64_t n, int64_t* count) {
   if (!s || !count) return PD_ERR_INVALID_ARGUMENT;
   if (!s->trace) return PD_ERR_STATE;
-  const int64_t tot = 6 * (int64_t)(s->plan.fw.a_off.size() + s->plan.bw.a_off.size());
+  const int64_t tot = 8 * (int64_t)(s->plan.fw.a_off.size() + s->plan.bw.a_off.size());
   *count = tot;
   if (out && n > 0 && cudaMemcpy(out, s->trace, sizeof(int64_t) * std::min(n, tot), cudaMemcpyDeviceToHost) != cudaSuccess)
     return PD_ERR_CUDA;

@@ -693,8 +693,6 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
 // order.  Single-item chunks write their output rows directly; split chunks and every forward W
 // item write partial rows that the group's last item adds in a fixed order into y / x (assign) or into z of
 // ancestors (subtract): deterministic, no atomics.
-constexpr int kKS = 8;   // k-steps per pipeline stage
-constexpr int kPS = 6;   // pipeline stages per warp
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -742,13 +740,8 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 constexpr int kItemK = 128;  // max k-steps per item (the planner's kc)
 template <int RC>
 __host__ __device__ constexpr int sweep_item_doubles() { return kItemK * (32 + RC); }
-// warps per CTA: as many whole-item buffers as fit in 227 KB of shared memory (at most 4)
 template <int RC>
-__host__ __device__ constexpr int sweep_wpc() {
-  return (232448 / (sweep_item_doubles<RC>() * 8)) >= 4 ? 4 : (232448 / (sweep_item_doubles<RC>() * 8));
-}
-template <int RC>
-__host__ __device__ constexpr int sweep_smem_bytes() { return sweep_wpc<RC>() * sweep_item_doubles<RC>() * 8; }
+__host__ __device__ constexpr int sweep_smem_bytes() { return sweep_item_doubles<RC>() * 8; }  // >= 4 x 32 x RC
 
 // K3 v5: ONE launch per sweep (dataflow).  Items are taken in the planned order (levels in sweep order)
 // through one integer counter; before reading its right-hand-side rows an item waits until they are
@@ -777,8 +770,8 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-template <int RC, bool VEC, int WPC>
-__global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
+template <int RC, bool VEC>
+__global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
                                                     const double* __restrict__ zc, const double* __restrict__ zi,
                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                     double* __restrict__ zsub, double* __restrict__ partial,
@@ -787,44 +780,36 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
                                                     int64_t* __restrict__ trace) {
   constexpr int CW = RC / 4;
   extern __shared__ __align__(16) double sm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int rg = lane & 7, cg = lane >> 3;
   const int y = blockIdx.y;
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
-  double* buf = sm + w * sweep_item_doubles<RC>();
-  __shared__ __align__(8) uint64_t mbs[WPC];
-  uint64_t* mb = mbs + w;
-  if (lane == 0) {
+  double* As = sm;                  // [kItemK][32]   factor block
+  double* Zs = sm + kItemK * 32;    // [kItemK][RC]   right-hand-side rows
+  __shared__ __align__(8) uint64_t mb[1];
+  __shared__ int s_next, s_flag;
+  if (tid == 0) {
     mbar_init(mb, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    s_next = atomicAdd(grab + y, 1);
   }
-  __syncwarp();
-  unsigned gst = 0;  // items loaded by this warp so far (mbarrier parity)
-  auto take = [&]() {
-    int v = 0;
-    if (lane == 0) v = atomicAdd(grab + y, 1);
-    return __shfl_sync(0xffffffffu, v, 0);
-  };
-  auto signal = [&](int sup) {  // all lanes' prior stores (warp barrier, cumulativity) -> release countdown
-    __syncwarp();
-    if (lane == 0) red_add_release(cd + (int64_t)sup * kGY + y, -1);
-  };
+  __syncthreads();
+  unsigned phase = 0;
   auto gtime = []() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return (int64_t)t;
   };
-  int next = take();
+  int next = s_next;
   while (next < nitems) {
     const int it = t0 + next;
-    int64_t* tr = (trace && y == 0) ? trace + (int64_t)next * 6 : nullptr;  // [start, deps, data, end, smid, warp]
-    if (tr && lane == 0) tr[0] = gtime();
-    next = take();  // prefetch the next index (never waited on before this item is done)
+    int64_t* tr = (trace && y == 0) ? trace + (int64_t)next * 8 : nullptr;  // [start, deps, data, end, smid, cta, written, counted]
+    if (tr && tid == 0) tr[0] = gtime();
     const int nk = sw.nk[it], nkd = sw.nkd[it];
-    // ---- wait until the item's right-hand-side rows are final
-    if (lane == 0) {
-      // bounded spin: a schedule bug becomes a launch error (trap) instead of a hung GPU
+    if (tid == 0) {
+      s_next = atomicAdd(grab + y, 1);  // prefetch the next index (never waited on before this item is done)
+      // wait until the item's right-hand-side rows are final (bounded: a schedule bug traps, never hangs)
       const int su = sw.sup[it];
       int64_t spins = 0;
       auto wait0 = [&](const int32_t* c) {
@@ -839,36 +824,34 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
         for (int q = sw.wl_ptr[su]; q < sw.wl_ptr[su + 1]; ++q) wait0(cd + (int64_t)sw.wl[q] * kGY + y);
       }
     }
-    __syncwarp();
-    if (tr && lane == 0) tr[1] = gtime();
-    // the acquired rows were written through the generic proxy; the TMA reads below use the async proxy
+    __syncthreads();
+    if (tr && tid == 0) tr[1] = gtime();
+    // acquired rows were written through the generic proxy; the TMA reads below use the async proxy
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
+    fence_proxy_async();  // generic reads of the previous item's buffer before the async-proxy refill
     const double* Ag = sw.A + sw.a_off[it];
     const int zr = sw.zrow[it];
     const int32_t* idx = rows + sw.zidx[it] - nkd;
     // ---- the whole item (<= kItemK k-steps: factor block + right-hand-side rows) in one TMA round
-    double* As = buf;
-    double* Zs = buf + kItemK * 32;
-    fence_proxy_async();  // generic reads of the previous item before the async-proxy refill
     if (VEC) {
       const bool whole = rcn == RC && RC == R && nkd == nk;  // contiguous rows, all columns: one copy
-      if (lane == 0) {
+      if (tid == 0) {
         mbar_arrive_expect_tx(mb, (unsigned)(nk * 256 + nk * rcn * 8));
         bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
         if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb);
       }
       if (!whole)
-        for (int kk = lane; kk < nk; kk += 32) {
+        for (int kk = tid; kk < nk; kk += 128) {
           const bool ct = kk < nkd;
           const int row = ct ? zr + kk : __ldg(idx + kk);
           bulk_g2s(Zs + kk * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), mb);
         }
     } else {
-      if (lane == 0) {
+      if (tid == 0) {
         mbar_arrive_expect_tx(mb, (unsigned)(nk * 256));
         bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
       }
-      for (int i = lane; i < nk * RC; i += 32) {
+      for (int i = tid; i < nk * RC; i += 128) {
         const int k = i / RC, c = i - k * RC;
         const bool ct = k < nkd;
         const int row = ct ? zr + k : __ldg(idx + k);
@@ -878,16 +861,20 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
       cp_async_commit();
       cp_async_wait_all();
     }
+    mbar_wait(mb, phase);
+    phase ^= 1;
+    __syncthreads();
+    if (tr && tid == 0) tr[2] = gtime();
+    // ---- 4 warps split the k-steps; lane (rg, cg) keeps a 4-row x RC/4-column register tile
     double acc[4][CW];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-    mbar_wait(mb, gst & 1);
-    __syncwarp();
-    if (tr && lane == 0) tr[2] = gtime();
+    const int per = (nk + 3) >> 2;
+    const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
 #pragma unroll 2
-    for (int k = 0; k < nk; ++k) {
+    for (int k = k0; k < k1; ++k) {
       const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
       const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
       const double av[4] = {a01.x, a01.y, a23.x, a23.y};
@@ -908,84 +895,93 @@ __global__ void __launch_bounds__(32 * WPC) k_sweep_flow(SweepDev sw, int t0, in
 #pragma unroll
         for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
     }
-    __syncwarp();
-    ++gst;
-    if (tr && lane == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      tr[4] = smid;
-      tr[5] = blockIdx.x * WPC + w;
-    }
-    // ---- output
+    __syncthreads();  // everyone is done with As/Zs: reuse the buffer for the 4 warp tiles
+    double* red = sm + w * 32 * RC;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) red[(4 * rg + r) * RC + cg * CW + c] = acc[r][c];
+    __syncthreads();
+    // ---- output rows: fixed-order sum of the 4 warp tiles, coalesced over columns
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];
     double* __restrict__ dst =
         out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < CW; ++c)
-        if (4 * rg + r < nv && cg * CW + c < rcn) dst[(int64_t)(4 * rg + r) * R + cg * CW + c] = acc[r][c];
-    if (out >= 0) {
-      if (sw.sig[it] >= 0) signal(sw.sig[it]);
-      if (tr && lane == 0) tr[3] = gtime();
-      continue;
+    for (int e = tid; e < nv * RC; e += 128) {
+      const int r = e / RC, c = e - r * RC;
+      if (c < rcn) dst[(int64_t)r * R + c] = ((sm[e] + sm[32 * RC + e]) + sm[64 * RC + e]) + sm[96 * RC + e];
     }
-    __syncwarp();
-    for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
-      const int g = sw.ig[q];
-      int last = 0;
-      if (lane == 0) last = atom_add_acq_rel(gcnt + (int64_t)g * kGY + y, -1) == 1;  // release partials,
-      last = __shfl_sync(0xffffffffu, last, 0);                                        // acquire the others'
-      if (!last) continue;
-      const int tile = sw.g_tile[g];
-      if (tile >= 0 && lane == 0) {  // z-row tiles apply their per-level groups in level order
-        int64_t spins = 0;
-        while (ld_acquire(turn + (int64_t)tile * kGY + y) != sw.g_turn[g]) {
-          __nanosleep(32);
-          if (++spins > (int64_t)1 << 26) __trap();
-        }
+    __syncthreads();
+    if (tr && tid == 0) tr[6] = gtime();
+    if (out >= 0) {
+      if (tid == 0) {
+        if (sw.sig[it] >= 0) red_add_release(cd + (int64_t)sw.sig[it] * kGY + y, -1);
+        if (tr) tr[3] = tr[7] = gtime();
       }
-      __syncwarp();
-      const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
-      if (lane < nt) {
-        const int t = tb + lane;
-        double v[RC];
-#pragma unroll
-        for (int c = 0; c < RC; ++c) v[c] = 0.0;
-#pragma unroll 4
-        for (int u = sw.red_ptr[t]; u < sw.red_ptr[t + 1]; ++u) {
-          const double* pr = partial + (int64_t)sw.red_src[u] * R + c0;
-          if (VEC) {
-#pragma unroll
-            for (int c = 0; c < RC / 2; ++c)
-              if (2 * c < rcn) {
-                const double2 xv = __ldcg(reinterpret_cast<const double2*>(pr) + c);
-                v[2 * c] += xv.x;
-                v[2 * c + 1] += xv.y;
-              }
-          } else {
-#pragma unroll
-            for (int c = 0; c < RC; ++c)
-              if (c < rcn) v[c] += __ldcg(pr + c);
+    } else {
+      int64_t t_counted = 0;
+      for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
+        const int g = sw.ig[q];
+        if (tid == 0) {
+          s_flag = atom_add_acq_rel(gcnt + (int64_t)g * kGY + y, -1) == 1;  // release ours, acquire the others'
+          if (tr && !t_counted) t_counted = gtime();
+          const int tile = sw.g_tile[g];
+          if (s_flag && tile >= 0) {  // z-row tiles apply their per-level groups in level order
+            int64_t spins = 0;
+            while (ld_acquire(turn + (int64_t)tile * kGY + y) != sw.g_turn[g]) {
+              __nanosleep(32);
+              if (++spins > (int64_t)1 << 26) __trap();
+            }
           }
         }
-        const bool assign = sw.red_mode[t] == 0;
-        double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[t] * R + c0;
+        __syncthreads();
+        const bool last = s_flag != 0;
+        if (last) {
+          // thread (target t, column quarter cq): its RC/4 columns accumulate over the target's partial
+          // rows in the planned order
+          const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
+          const int t = tid & 31, cq = tid >> 5;
+          if (t < nt) {
+            double v[CW];
 #pragma unroll
-        for (int c = 0; c < RC; ++c)
-          if (c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
+            for (int c = 0; c < CW; ++c) v[c] = 0.0;
+            const int u0 = sw.red_ptr[tb + t], u1 = sw.red_ptr[tb + t + 1];
+#pragma unroll 4
+            for (int u = u0; u < u1; ++u) {
+              const double* pr = partial + (int64_t)sw.red_src[u] * R + c0 + cq * CW;
+#pragma unroll
+              for (int c = 0; c < CW; ++c)
+                if (cq * CW + c < rcn) v[c] += __ldcg(pr + c);
+            }
+            const bool assign = sw.red_mode[tb + t] == 0;
+            double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[tb + t] * R + c0 + cq * CW;
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+              if (cq * CW + c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
+          }
+          __syncthreads();
+          if (tid == 0) {
+            gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
+            if (sw.g_tile[g] >= 0) red_add_release(turn + (int64_t)sw.g_tile[g] * kGY + y, 1);
+            if (sw.g_sig[g] >= 0) red_add_release(cd + (int64_t)sw.g_sig[g] * kGY + y, -1);
+          }
+        }
       }
-      if (lane == 0) gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
-      if (tile >= 0) {
-        __syncwarp();
-        if (lane == 0) red_add_release(turn + (int64_t)tile * kGY + y, 1);
+      if (tr && tid == 0) {
+        tr[3] = gtime();
+        tr[7] = t_counted ? t_counted : tr[3];
       }
-      if (sw.g_sig[g] >= 0) signal(sw.g_sig[g]);
     }
-    if (tr && lane == 0) tr[3] = gtime();
+    if (tr && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      tr[4] = smid;
+      tr[5] = blockIdx.x;
+    }
+    __syncthreads();
+    next = s_next;
+    __syncthreads();
   }
-  cp_async_wait_group<0>();
 }
 
 // ----------------------------------------------------------------- K5: contact

@@ -24,6 +24,7 @@ ok = tr[:, 0] > 0
 t0 = tr[ok, 0].min()
 tr = tr.astype(np.float64)
 tr[:, :4] = (tr[:, :4] - t0) / 1e3  # us
+tr[:, 6:8] = (tr[:, 6:8] - t0) / 1e3
 nf = (tr.shape[0])
 print("items", tr.shape[0], "span us %.1f" % (tr[ok, 3].max()))
 wait = tr[ok, 1] - tr[ok, 0]
@@ -46,3 +47,20 @@ for a, b in zip(edges[:-1], edges[1:]):
     w = w[w[:, 0] > -1e9]
     print("items %6d-%6d start %7.1f end %7.1f | wait %6.1f data %5.1f out %6.1f" % (
         a, b, w[:, 0].min(), w[:, 3].max(), (w[:, 1] - w[:, 0]).mean(), (w[:, 2] - w[:, 1]).mean(), (w[:, 3] - w[:, 2]).mean()))
+# per-warp occupancy: gaps between consecutive items of the same warp
+gaps, busy = [], []
+for wid in np.unique(tr[ok, 5]):
+    w = tr[ok & (tr[:, 5] == wid)]
+    w = w[np.argsort(w[:, 0])]
+    if len(w) > 1:
+        gaps.extend((w[1:, 0] - w[:-1, 3]).tolist())
+    busy.append(((w[:, 3] - w[:, 0]).sum(), len(w), w[:, 3].max() - w[:, 0].min()))
+gaps = np.array(gaps)
+busy = np.array(busy)
+print("gap between items of a warp: mean %.2f us, max %.1f; items per warp mean %.1f max %d; warp busy/lifetime %.2f" % (
+    gaps.mean(), gaps.max(), busy[:, 1].mean(), busy[:, 1].max(), busy[:, 0].sum() / busy[:, 2].sum()))
+
+wr = tr[ok, 6] - tr[ok, 2]
+cn = tr[ok, 7] - tr[ok, 6]
+rd = tr[ok, 3] - tr[ok, 7]
+print("out phase split: write %.2f  first-countdown %.2f  rest(reductions/signals) %.2f  (means, us)" % (wr.mean(), cn.mean(), rd.mean()))
