@@ -53,6 +53,7 @@ struct pd_sim {
   int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
   int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
   int64_t* trace = nullptr;                     // K3 per-item timeline (debug hook, pd_debug_trace)
+  int k3_levels = 1;                            // K3 launch per level (1) or one dataflow launch per sweep (0)
   int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
@@ -230,7 +231,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, sweep_smem_bytes<RC>()));
   const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
   // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
-  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY, s->stream));
+  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY * (P.nlevels + 1), s->stream));
   CK(cudaMemsetAsync(s->turn, 0, sizeof(int32_t) * (size_t)std::max(1, P.fw.ntiles) * kGY, s->stream));
   CK(cudaMemcpyAsync(s->cd_f, s->cd_f0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
   CK(cudaMemcpyAsync(s->cd_b, s->cd_b0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
@@ -246,18 +247,29 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   };
   const HostPlan::Sweep& F = P.fw;
   const HostPlan::Sweep& Bk = P.bw;
-  launch(s->swf, 0, F.lvl_item[P.nlevels], true, s->cnt_f, s->cd_f, s->grab);
+  // Launch granularity: one launch per tree level (s->k3_levels = 1, default; kernel boundaries order the
+  // levels, every wait inside is already satisfied) or one dataflow launch per sweep.
+  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab,
+                   int j0, int j1) {
+    if (s->k3_levels) {
+      for (int j = j0; j < j1; ++j)
+        launch(d, S.lvl_item[j], S.lvl_item[j + 1] - S.lvl_item[j], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j * 4 * kGY);
+    } else {
+      launch(d, S.lvl_item[j0], S.lvl_item[j1] - S.lvl_item[j0], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j0 * 4 * kGY);
+    }
+  };
+  sweep(F, s->swf, true, s->cnt_f, s->cd_f, s->grab, 0, P.nlevels);
   if (s->pins_live) {
     // the root (= candidate block) first, then its constrained fixup, then every other level
     double* root = s->S0 + (int64_t)s->csup_first * R;
     CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
-    launch(s->swb, 0, Bk.lvl_item[1], false, s->cnt_b, s->cd_b, s->grab + kGY);
+    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 0, 1);
     k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos,
                                                                    s->Qc, root);
     LAUNCH_CHECK(s);
-    launch(s->swb, Bk.lvl_item[1], Bk.lvl_item[P.nlevels] - Bk.lvl_item[1], false, s->cnt_b, s->cd_b, s->grab + 2 * kGY);
+    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 1, P.nlevels);
   } else {
-    launch(s->swb, 0, Bk.lvl_item[P.nlevels], false, s->cnt_b, s->cd_b, s->grab + kGY);
+    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 0, P.nlevels);
   }
 }
 void solve_launch(pd_sim* s, int B) {
@@ -631,7 +643,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
         for (int y = 0; y < kGY; ++y) c[g * kGY + y] = S.g_cnt[g];
       return s->upload(c);
     };
-    s->grab = s->alloc<int32_t>(4 * kGY);
+    s->grab = s->alloc<int32_t>(4 * kGY * (P.nlevels + 1));
+    s->k3_levels = std::getenv("PD_K3_DATAFLOW") ? 0 : 1;
     s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
     if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(8 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
     auto up_cd = [&](const HostPlan::Sweep& S) {
