@@ -242,7 +242,14 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident / gy));
     k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
         d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : nullptr);
+        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : nullptr,
+        s->k3_levels ? 0 : 1);
+    LAUNCH_CHECK(s);
+  };
+  auto reduce = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int j) {
+    const int r0 = S.g_tptr[S.lvl_grp[j]], nr = S.g_tptr[S.lvl_grp[j + 1]] - r0;
+    if (!nr) return;
+    k_sweep_reduce<<<nblk((int64_t)nr * R), 256, 0, s->stream>>>(d, r0, nr, R, s->Spart, fwd ? s->S2 : s->S0, s->S0);
     LAUNCH_CHECK(s);
   };
   const HostPlan::Sweep& F = P.fw;
@@ -252,8 +259,10 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab,
                    int j0, int j1) {
     if (s->k3_levels) {
-      for (int j = j0; j < j1; ++j)
+      for (int j = j0; j < j1; ++j) {
         launch(d, S.lvl_item[j], S.lvl_item[j + 1] - S.lvl_item[j], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j * 4 * kGY);
+        reduce(S, d, fwd, j);
+      }
     } else {
       launch(d, S.lvl_item[j0], S.lvl_item[j1] - S.lvl_item[j0], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j0 * 4 * kGY);
     }

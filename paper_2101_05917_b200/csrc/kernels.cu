@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
                                                     double* __restrict__ zsub, double* __restrict__ partial,
                                                     int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
                                                     int32_t* __restrict__ grab, int32_t* __restrict__ turn,
-                                                    int64_t* __restrict__ trace) {
+                                                    int64_t* __restrict__ trace, int groups_inline) {
   constexpr int CW = RC / 4;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -918,7 +918,7 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
         if (sw.sig[it] >= 0) red_add_release(cd + (int64_t)sw.sig[it] * kGY + y, -1);
         if (tr) tr[3] = tr[7] = gtime();
       }
-    } else {
+    } else if (groups_inline) {
       int64_t t_counted = 0;
       for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
         const int g = sw.ig[q];
@@ -982,6 +982,20 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
     next = s_next;
     __syncthreads();
   }
+}
+
+// Per-level launches: the level's reduction targets after all its items (thread per (target, column)),
+// each target's partial rows in the planned order.  Level groups hit disjoint rows (one group per tile).
+__global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
+                               double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)ntarget * R) return;
+  const int t = r0 + (int)(g / R), c = (int)(g % R);
+  double acc = 0;
+  for (int q = sw.red_ptr[t]; q < sw.red_ptr[t + 1]; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  const int64_t o = (int64_t)sw.red_row[t] * R + c;
+  if (sw.red_mode[t] == 0) dst_assign[o] = acc;
+  else dst_sub[o] -= acc;
 }
 
 // ----------------------------------------------------------------- K5: contact
