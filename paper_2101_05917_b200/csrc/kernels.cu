@@ -818,7 +818,9 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
           if (++spins > (int64_t)1 << 26) __trap();
         }
       };
-      if (fwd) {
+      if (!groups_inline) {
+        // per-level launches: kernel boundaries already order the levels
+      } else if (fwd) {
         wait0(cd + (int64_t)su * kGY + y);
       } else if (nkd < nk) {
         for (int q = sw.wl_ptr[su]; q < sw.wl_ptr[su + 1]; ++q) wait0(cd + (int64_t)sw.wl[q] * kGY + y);
