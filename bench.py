@@ -335,7 +335,12 @@ def main_ours(args):
                            supernodes=info["n_supernodes"], levels=info["n_levels"]),
                 clocks=clk)
     if rank == 0:
-        line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_sample_steps).items() if k != "wall_s"}
+        if args.cpu_sample_steps > 0:
+            line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_sample_steps).items() if k != "wall_s"}
+        else:
+            line["cpu_baseline"] = dict(value=None, unit=UNIT, cores=None, kind="oracle",
+                                        sample="not run (--cpu-sample-steps 0): one oracle sim-step of this "
+                                               "workload exceeds 50 min on the host")
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
