@@ -180,7 +180,12 @@ def simulator_from_inputs(inp, **kw):
     args = dict(youngs=cfg.youngs, poisson=cfg.poisson, density=cfg.density, h=cfg.h, gravity=cfg.gravity,
                 fixed_dofs=inp["fixed_dofs"], contact_nodes=inp["contact_nodes"], muscle_w=muscle_w,
                 fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"])
-    if cfg.per_sim_youngs:
-        args["youngs_ref"] = float(np.max(inp["youngs"]))
     args.update(kw)
+    if cfg.per_sim_youngs and "youngs_ref" not in kw:
+        # plain PD needs the majorising A_ref (largest E of the batch); the quasi-Newton
+        # forward/adjoint only use A_ref^{-1} as a preconditioner, where the geometric mean of the batch
+        # extremes halves the worst-case condition number
+        E = np.asarray(inp["youngs"], dtype=np.float64)
+        accel = args.get("accel_fwd", 1)
+        args["youngs_ref"] = float(np.max(E)) if not accel else float(np.sqrt(np.min(E) * np.max(E)))
     return Simulator(inp["rest"], inp["hex8"], cfg.dx, **args)
