@@ -130,7 +130,7 @@ namespace {
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 // DoFs per reduction block: ~4096 (DoF, sim) elements per block whatever B is (fixed partition =
 // deterministic sums).
-inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 4096 / B); }
+inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 1024 / B); }
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -212,7 +212,7 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   const int bd = B * std::max(1, 256 / B);
   k_dot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk(p * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
+  k_dot_final<<<nblk((int64_t)(p * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
 }
 
@@ -400,7 +400,7 @@ void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double
   const int bd = B * std::max(1, 256 / B);
   k_mdot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk(nv * B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, nv, out);
+  k_dot_final<<<nblk((int64_t)(nv * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, nv, out);
   LAUNCH_CHECK(s);
 }
 
@@ -415,7 +415,7 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
   k_inertia_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B,
                                                                     chunk, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk(B, 64), 64, 0, s->stream>>>(s->partial, nchunk, B, 1, s->inert);
+  k_dot_final<<<nblk((int64_t)(B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, 1, s->inert);
   LAUNCH_CHECK(s);
   dots(s, B, P.m, {{s->EE, nullptr}}, s->esum);
   k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
@@ -491,7 +491,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
-      k_lbfgs_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, iter, B, s->active);
+      k_lbfgs_alpha<<<B, 32, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, iter, B, s->active);
       LAUNCH_CHECK(s);
       k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
                                                      s->active);  // q = g - sum alpha_j y_j
@@ -502,7 +502,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);  // r0 = H0 q = A^{-1} q
     if (hist > 0) {
       mdot(s, B, s->Dv, s->LY, hist, s->lb_yr);
-      k_lbfgs_beta<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, iter, B,
+      k_lbfgs_beta<<<B, 32, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, iter, B,
                                                       s->active);
       LAUNCH_CHECK(s);
       k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,

@@ -1289,14 +1289,17 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, dou
     __syncthreads();
   }
 }
+// one warp per (pair, sim): lane l sums chunks l, l+32, ... in order, then a fixed xor tree (deterministic)
 __global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out,
                             int accumulate = 0) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= npairs * B) return;
   const int p = i / B, b = i - p * B;
   double s = 0;
-  for (int c = 0; c < nchunk; ++c) s += partial[((int64_t)p * nchunk + c) * B + b];
-  out[i] = accumulate ? out[i] + s : s;
+  for (int c = lane; c < nchunk; c += 32) s += partial[((int64_t)p * nchunk + c) * B + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[i] = accumulate ? out[i] + s : s;
 }
 // sum over elements of E[e][b] (deterministic) -> out[b] (+= if accumulate)
 __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* __restrict__ out, int accumulate) {
@@ -1436,35 +1439,63 @@ __global__ void k_mdot_partial(const double* __restrict__ u, const double* __res
 // slot of the k-th newest pair at iteration `iter` (ring of m)
 __device__ __forceinline__ int lb_slot(int iter, int k, int m) { return ((iter - 1 - k) % m + m) % m; }
 
+// one warp per sim: the per-sim Gram data staged in shared memory, the (tiny, sequential) recursion in lane 0
 __global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __restrict__ Gm, const double* __restrict__ rho,
                               double* __restrict__ alpha, int m, int hist, int iter, int B,
                               const int32_t* __restrict__ active) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !active[b]) return;
-  for (int k = 0; k < hist; ++k) {
-    const int i = lb_slot(iter, k, m);
-    double t = sg[i * B + b];
-    for (int kk = 0; kk < k; ++kk) {
-      const int j = lb_slot(iter, kk, m);
-      t -= alpha[j * B + b] * Gm[(i * m + j) * B + b];
+  __shared__ double g[64], sv[8], rv[8], av[8];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  if (!active[b]) return;
+  for (int i = lane; i < m * m; i += 32) g[i] = Gm[(int64_t)i * B + b];
+  if (lane < m) {
+    sv[lane] = sg[lane * B + b];
+    rv[lane] = rho[lane * B + b];
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int k = 0; k < hist; ++k) {
+      const int i = lb_slot(iter, k, m);
+      double t = sv[i];
+      for (int kk = 0; kk < k; ++kk) {
+        const int j = lb_slot(iter, kk, m);
+        t -= av[j] * g[i * m + j];
+      }
+      av[i] = rv[i] * t;
     }
-    alpha[i * B + b] = rho[i * B + b] * t;
+  __syncwarp();
+  if (lane < hist) {
+    const int i = lb_slot(iter, lane, m);
+    alpha[i * B + b] = av[i];
   }
 }
 
 __global__ void k_lbfgs_beta(const double* __restrict__ yr, const double* __restrict__ Gm, const double* __restrict__ rho,
                              const double* __restrict__ alpha, double* __restrict__ beta, int m, int hist, int iter,
                              int B, const int32_t* __restrict__ active) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !active[b]) return;
-  for (int k = hist - 1; k >= 0; --k) {
-    const int i = lb_slot(iter, k, m);
-    double t = yr[i * B + b];
-    for (int kk = hist - 1; kk > k; --kk) {
-      const int j = lb_slot(iter, kk, m);
-      t += (alpha[j * B + b] - beta[j * B + b]) * Gm[(j * m + i) * B + b];
+  __shared__ double g[64], yv[8], rv[8], av[8], bv[8];
+  const int b = blockIdx.x, lane = threadIdx.x;
+  if (!active[b]) return;
+  for (int i = lane; i < m * m; i += 32) g[i] = Gm[(int64_t)i * B + b];
+  if (lane < m) {
+    yv[lane] = yr[lane * B + b];
+    rv[lane] = rho[lane * B + b];
+    av[lane] = alpha[lane * B + b];
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int k = hist - 1; k >= 0; --k) {
+      const int i = lb_slot(iter, k, m);
+      double t = yv[i];
+      for (int kk = hist - 1; kk > k; --kk) {
+        const int j = lb_slot(iter, kk, m);
+        t += (av[j] - bv[j]) * g[j * m + i];
+      }
+      bv[i] = rv[i] * t;
     }
-    beta[i * B + b] = rho[i * B + b] * t;
+  __syncwarp();
+  if (lane < hist) {
+    const int i = lb_slot(iter, lane, m);
+    beta[i * B + b] = bv[i];
   }
 }
 
