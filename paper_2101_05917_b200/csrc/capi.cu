@@ -224,32 +224,55 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
   if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
   CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
-  // one resident wave: warps take items round-robin, so CTAs beyond residency would only add a tail
-  int per_sm = 0, nsm = 0, dev = 0;
+  int nsm = 0, dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, sweep_smem_bytes<RC>()));
-  const int64_t resident = std::max(1, per_sm) * (int64_t)nsm;
+  // shared memory of a launch = its largest item (and >= the 4 x 32 x RC warp-tile buffer); residency by size
+  auto smem_of = [&](int kmax) { return std::max(kmax * (32 + RC), 4 * 32 * RC) * 8; };
+  auto resident_of = [&](int bytes) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, bytes));
+    return std::max(1, per_sm) * (int64_t)nsm;
+  };
   // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
   CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY * (P.nlevels + 1), s->stream));
   CK(cudaMemsetAsync(s->turn, 0, sizeof(int32_t) * (size_t)std::max(1, P.fw.ntiles) * kGY, s->stream));
   CK(cudaMemcpyAsync(s->cd_f, s->cd_f0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
   CK(cudaMemcpyAsync(s->cd_b, s->cd_b0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
-  auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab) {
+  // programmatic dependent launch (PDL): a kernel's CTAs may be scheduled while its predecessor drains;
+  // they block in griddepcontrol.wait until the predecessor's writes are visible
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  auto cfg_of = [&](dim3 grid, dim3 block, size_t smem) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = grid;
+    c.blockDim = block;
+    c.dynamicSmemBytes = smem;
+    c.stream = s->stream;
+    c.attrs = pdl;
+    c.numAttrs = 1;
+    return c;
+  };
+  auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
     if (!nt) return;
     // forward: sources z (S0), direct y (S2), group subtract into z (S0);
     // backward: D part y (S2), W part x (S0), direct x (S0)
-    const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident / gy));
-    k_sweep_flow<RC, VEC><<<dim3(gx, gy), 128, sweep_smem_bytes<RC>(), s->stream>>>(
-        d, t0, nt, R, fwd ? 1 : 0, fwd ? s->S0 : s->S2, s->S0, s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-        cd, grab, s->turn, s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : nullptr,
-        s->k3_levels ? 0 : 1);
+    const int smem = smem_of(kmax);
+    const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_of(smem) / gy));
+    cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
+    CK(cudaLaunchKernelEx(&c, k_sweep_flow<RC, VEC>, d, t0, nt, R, fwd ? 1 : 0, (const double*)(fwd ? s->S0 : s->S2),
+                          (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
+                          cd, grab, s->turn,
+                          s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : (int64_t*)nullptr,
+                          s->k3_levels ? 0 : 1, kmax));
     LAUNCH_CHECK(s);
   };
   auto reduce = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int j) {
     const int r0 = S.g_tptr[S.lvl_grp[j]], nr = S.g_tptr[S.lvl_grp[j + 1]] - r0;
     if (!nr) return;
-    k_sweep_reduce<<<nblk((int64_t)nr * R), 256, 0, s->stream>>>(d, r0, nr, R, s->Spart, fwd ? s->S2 : s->S0, s->S0);
+    cudaLaunchConfig_t c = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
+    CK(cudaLaunchKernelEx(&c, k_sweep_reduce, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
     LAUNCH_CHECK(s);
   };
   const HostPlan::Sweep& F = P.fw;
@@ -260,11 +283,15 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
                    int j0, int j1) {
     if (s->k3_levels) {
       for (int j = j0; j < j1; ++j) {
-        launch(d, S.lvl_item[j], S.lvl_item[j + 1] - S.lvl_item[j], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j * 4 * kGY);
+        launch(d, S.lvl_item[j], S.lvl_item[j + 1] - S.lvl_item[j], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j * 4 * kGY,
+               S.lvl_kmax[j]);
         reduce(S, d, fwd, j);
       }
     } else {
-      launch(d, S.lvl_item[j0], S.lvl_item[j1] - S.lvl_item[j0], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j0 * 4 * kGY);
+      int km = 0;
+      for (int j = j0; j < j1; ++j) km = std::max(km, S.lvl_kmax[j]);
+      launch(d, S.lvl_item[j0], S.lvl_item[j1] - S.lvl_item[j0], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j0 * 4 * kGY,
+             km);
     }
   };
   sweep(F, s->swf, true, s->cnt_f, s->cd_f, s->grab, 0, P.nlevels);

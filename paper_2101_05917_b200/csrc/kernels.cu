@@ -771,13 +771,13 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 }
 
 template <int RC, bool VEC>
-__global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
+__global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
                                                     const double* __restrict__ zc, const double* __restrict__ zi,
                                                     const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                     double* __restrict__ zsub, double* __restrict__ partial,
                                                     int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
                                                     int32_t* __restrict__ grab, int32_t* __restrict__ turn,
-                                                    int64_t* __restrict__ trace, int groups_inline) {
+                                                    int64_t* __restrict__ trace, int groups_inline, int kmax) {
   constexpr int CW = RC / 4;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -785,8 +785,10 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
   const int y = blockIdx.y;
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
-  double* As = sm;                  // [kItemK][32]   factor block
-  double* Zs = sm + kItemK * 32;    // [kItemK][RC]   right-hand-side rows
+  // programmatic dependent launch: everything below may read what the previous kernel wrote
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  double* As = sm;                  // [kmax][32]   factor block (kmax = the level's largest item)
+  double* Zs = sm + kmax * 32;      // [kmax][RC]   right-hand-side rows
   __shared__ __align__(8) uint64_t mb[1];
   __shared__ int s_next, s_flag;
   if (tid == 0) {
@@ -984,12 +986,15 @@ __global__ void __launch_bounds__(128) k_sweep_flow(SweepDev sw, int t0, int nit
     next = s_next;
     __syncthreads();
   }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 // Per-level launches: the level's reduction targets after all its items (thread per (target, column)),
 // each target's partial rows in the planned order.  Level groups hit disjoint rows (one group per tile).
 __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
                                double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= (int64_t)ntarget * R) return;
   const int t = r0 + (int)(g / R), c = (int)(g % R);

@@ -49,6 +49,7 @@ struct HostPlan {
   struct Sweep {
     std::vector<double> A;             // factor stream in item order (k-major 32-lane blocks)
     std::vector<int32_t> lvl_item;     // [nlevels+1] items of level l: [lvl_item[l], lvl_item[l+1])
+    std::vector<int32_t> lvl_kmax;     // [nlevels] largest item (k-steps) of level l: its shared-memory size
     std::vector<int64_t> a_off;        // per item
     std::vector<int32_t> nk;           // k-steps
     std::vector<int32_t> nkd;          // k < nkd: source row zrow + k of the contiguous source

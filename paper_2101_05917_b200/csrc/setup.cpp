@@ -182,7 +182,16 @@ static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
 //   x[J_s cols] = D_s^T y[J_s] - W_s^T x[R_s]     (D part k = c0..ns, W part k = 0..nr; lane = column)
 // Items hold <= kc_l k-steps (kc_l balances the level over warps_target warps); a chunk covered by one
 // item writes its output directly, otherwise its items write partial rows summed by the chunk's group.
+static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vector<int32_t>>& byh);
 static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
+  build_solve_schedule_items(P, byh);
+  for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
+    S->lvl_kmax.assign(P.nlevels, 0);
+    for (int l = 0; l < P.nlevels; ++l)
+      for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) S->lvl_kmax[l] = std::max(S->lvl_kmax[l], S->nk[t]);
+  }
+}
+static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
   const int L = 32;
   auto init = [&](HostPlan::Sweep& S) {
     S = HostPlan::Sweep();
