@@ -866,6 +866,11 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
                                             s->gravity[0], s->gravity[1], s->gravity[2]);
       LAUNCH_CHECK(s);
       CK(cudaMemcpyAsync(s->Xp, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+      const bool predict = s->opt.x0_predict && s->opt.fixed_iter <= 0;
+      if (predict) {  // x^0 = x_i + h v_i (Dirichlet DoFs have v = 0 and stay at rest)
+        k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, 1.0, s->V, nullptr, s->h, len, B, nullptr);
+        LAUNCH_CHECK(s);
+      }
       const bool contact = s->nc > 0;
       const int64_t cB = (int64_t)s->nc * B;
       if (contact) {  // Alg. 1: V_i = empty
@@ -880,7 +885,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       for (int outer = 1; outer <= (contact ? s->opt.max_outer : 1); ++outer) {
         if (contact) {
           k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact,
-                                                              s->opt.outer_warm && outer > 1);
+                                                              (s->opt.outer_warm && outer > 1) || (predict && outer == 1));
           LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
           if (outer > 1) build_Q(s, B, s->oact);
           CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
