@@ -254,8 +254,23 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     c.numAttrs = 1;
     return c;
   };
+  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sweep_smem_bytes<RC>()));
+  auto resident_lvl = [&](int bytes) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, bytes));
+    return std::max(1, per_sm) * (int64_t)nsm;
+  };
   auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
     if (!nt) return;
+    if (s->k3_levels) {  // per-level mode: double-buffered items, static assignment
+      const int smem = 2 * smem_of(kmax);
+      const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
+      cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
+      CK(cudaLaunchKernelEx(&c, k_sweep_level<RC, VEC>, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
+                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kmax));
+      LAUNCH_CHECK(s);
+      return;
+    }
     // forward: sources z (S0), direct y (S2), group subtract into z (S0);
     // backward: D part y (S2), W part x (S0), direct x (S0)
     const int smem = smem_of(kmax);

@@ -989,6 +989,137 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
+// Per-level mode (default): items of ONE level, no dependency waits (kernel boundaries order the levels).
+// CTA c takes items c, c + G, c + 2G, ... (G = gridDim.x) and double-buffers them: the TMA round of the next
+// item is issued as soon as the current item's data has landed, so its latency hides behind the compute.
+template <int RC, bool VEC>
+__global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
+                                                        const double* __restrict__ zc, const double* __restrict__ zi,
+                                                        const int32_t* __restrict__ rows, double* __restrict__ direct,
+                                                        double* __restrict__ partial, int kmax) {
+  constexpr int CW = RC / 4;
+  extern __shared__ __align__(16) double sm[];
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int rg = lane & 7, cg = lane >> 3;
+  const int y = blockIdx.y;
+  const int c0 = y * RC;
+  const int rcn = min(RC, R - c0);
+  const int bufd = kmax * (32 + RC);  // doubles per buffer
+  __shared__ __align__(8) uint64_t mb[2];
+  __shared__ double red_s[1];  // (unused: keeps the static smem non-empty)
+  (void)red_s;
+  if (tid == 0) {
+    mbar_init(mb, 1);
+    mbar_init(mb + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto load = [&](int rel, int slot) {  // one TMA round for item t0 + rel into buffer `slot`
+    const int it = t0 + rel;
+    double* As = sm + slot * bufd;
+    double* Zs = As + kmax * 32;
+    const int nk = sw.nk[it], nkd = sw.nkd[it];
+    const double* Ag = sw.A + sw.a_off[it];
+    const int zr = sw.zrow[it];
+    const int32_t* idx = rows + sw.zidx[it] - nkd;
+    if (VEC) {
+      const bool whole = rcn == RC && RC == R && nkd == nk;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(mb + slot, (unsigned)(nk * 256 + nk * rcn * 8));
+        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb + slot);
+        if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb + slot);
+      }
+      if (!whole)
+        for (int kk = tid; kk < nk; kk += 128) {
+          const bool ct = kk < nkd;
+          const int row = ct ? zr + kk : __ldg(idx + kk);
+          bulk_g2s(Zs + kk * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), mb + slot);
+        }
+    } else {
+      if (tid == 0) {
+        mbar_arrive_expect_tx(mb + slot, (unsigned)(nk * 256));
+        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb + slot);
+      }
+      for (int i = tid; i < nk * RC; i += 128) {
+        const int k = i / RC, c = i - k * RC;
+        const bool ct = k < nkd;
+        const int row = ct ? zr + k : __ldg(idx + k);
+        if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
+        else Zs[k * RC + c] = 0.0;
+      }
+      cp_async_commit();
+    }
+  };
+  const int G = gridDim.x;
+  int rel = blockIdx.x, slot = 0;
+  unsigned ph[2] = {0, 0};
+  if (rel < nitems) load(rel, 0);
+  while (rel < nitems) {
+    const int it = t0 + rel;
+    const int nk = sw.nk[it];
+    if (!VEC) cp_async_wait_all();
+    mbar_wait(mb + slot, ph[slot]);
+    ph[slot] ^= 1;
+    __syncthreads();  // this item's data visible to all; the other buffer's previous readers are done
+    const int nrel = rel + G;
+    if (nrel < nitems) {
+      fence_proxy_async();
+      load(nrel, slot ^ 1);  // prefetch the next item while this one computes
+    }
+    const double* As = sm + slot * bufd;
+    const double* Zs = As + kmax * 32;
+    double acc[4][CW];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+    const int per = (nk + 3) >> 2;
+    const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
+      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      double zv[CW];
+      if (CW % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < CW / 2; ++c) {
+          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
+          zv[2 * c] = t.x;
+          zv[2 * c + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+    }
+    __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
+    double* redb = sm + slot * bufd;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < CW; ++c) redb[w * 32 * RC + (4 * rg + r) * RC + cg * CW + c] = acc[r][c];
+    __syncthreads();
+    const int out = sw.out[it];
+    const int nv = sw.nvalid[it];
+    double* __restrict__ dst =
+        out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
+    for (int e = tid; e < nv * RC; e += 128) {
+      const int r = e / RC, c = e - r * RC;
+      if (c < rcn) dst[(int64_t)r * R + c] = ((redb[e] + redb[32 * RC + e]) + redb[64 * RC + e]) + redb[96 * RC + e];
+    }
+    __syncthreads();  // buffer free before it is refilled two items from now
+    rel = nrel;
+    slot ^= 1;
+  }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // Per-level launches: the level's reduction targets after all its items (thread per (target, column)),
 // each target's partial rows in the planned order.  Level groups hit disjoint rows (one group per tile).
 __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
