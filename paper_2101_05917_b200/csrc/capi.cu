@@ -229,6 +229,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   // shared memory of a launch = its largest item (and >= the 4 x 32 x RC warp-tile buffer); residency by size
   auto smem_of = [&](int kmax) { return std::max(kmax * (32 + RC), 4 * 32 * RC) * 8; };
+  auto kpad_of = [&](int kmax) { return std::max(kmax, (4 * 32 * RC + 32 + RC - 1) / (32 + RC)); };  // buffer >= tiles
   auto resident_of = [&](int bytes) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, bytes));
@@ -254,7 +255,8 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     c.numAttrs = 1;
     return c;
   };
-  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sweep_smem_bytes<RC>()));
+  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          std::min(232448, 2 * sweep_smem_bytes<RC>())));
   auto resident_lvl = [&](int bytes) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, bytes));
@@ -263,11 +265,12 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
     if (!nt) return;
     if (s->k3_levels) {  // per-level mode: double-buffered items, static assignment
-      const int smem = 2 * smem_of(kmax);
+      const int kp = kpad_of(kmax);  // each of the 2 buffers also holds the 4 warp tiles
+      const int smem = 2 * kp * (32 + RC) * 8;
       const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
       CK(cudaLaunchKernelEx(&c, k_sweep_level<RC, VEC>, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
-                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kmax));
+                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp));
       LAUNCH_CHECK(s);
       return;
     }
