@@ -1,0 +1,137 @@
+"""Full-size parity (BASELINE.json configs at their real mesh/batch sizes, in the launch configuration bench.py
+times: same Simulator options) on a short horizon: element-by-element against the oracle for sampled sims, and
+property checks that hold at any size where the oracle cannot follow (c5)."""
+import numpy as np
+import pytest
+
+from gpu_common import GRAD_TOL, POS_TOL, rel, to_dev
+from pd_inputs import get_config, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2101_05917_b200 as pdb
+    pdb.build()
+    return torch
+
+
+def _bench_sim(inp, **kw):
+    """The Simulator exactly as bench.py builds it (tolerances tightened for parity where stated)."""
+    import paper_2101_05917_b200 as pdb
+    cfg = inp["cfg"]
+    base = dict(tol_fwd=cfg.tol, tol_adj=cfg.tol, max_steps=inp["T"], check_every=1, accel_fwd=1, outer_warm=1)
+    base.update(kw)
+    return pdb.simulator_from_inputs(inp, **base)
+
+
+def _run(torch, inp, sim):
+    from oracle import adjoint
+    B, T, N = inp["B"], inp["T"], 3 * inp["n_nodes"]
+    qt = torch.zeros((B, T + 1, N), dtype=torch.float64, device="cuda")
+    vt = torch.zeros_like(qt)
+    act = None if inp["act"] is None else to_dev(inp["act"][:, :T])
+    st = sim.forward(to_dev(inp["q0"]), to_dev(inp["v0"]), T, f_ext=to_dev(inp["f_ext"]), actuation=act,
+                     youngs=to_dev(inp["youngs"]), q_traj=qt, v_traj=vt)
+    q, v = qt.cpu().numpy(), vt.cpu().numpy()
+    gq = np.zeros((B, N))
+    gv = np.zeros((B, N))
+    for b in range(B):
+        _, gq[b], gv[b] = adjoint.loss_and_grad(inp, b, q[b, -1], v[b, -1])
+    outs = {k: torch.zeros((B, N), dtype=torch.float64, device="cuda") for k in ("dq0", "dv0", "dfext")}
+    dE = torch.zeros(B, dtype=torch.float64, device="cuda")
+    dnu = torch.zeros(B, dtype=torch.float64, device="cuda")
+    dact = None if act is None else torch.zeros_like(act)
+    sb = sim.backward(to_dev(gq), to_dev(gv), outs["dq0"], outs["dv0"], outs["dfext"], dE, dnu, dact)
+    r = dict(q=q, v=v, st=st, sb=sb, dE=dE.cpu().numpy(), dnu=dnu.cpu().numpy(),
+             dact=None if dact is None else dact.cpu().numpy())
+    r.update({k: t.cpu().numpy() for k, t in outs.items()})
+    return r
+
+
+def _oracle(inp, b, tol=1e-13):
+    from oracle import adjoint, pd
+    sc = pd.scene_from_inputs(inp)
+    act = None if inp["act"] is None else inp["act"][b, :inp["T"]]
+    tr = pd.forward(sc, inp["q0"][b], inp["v0"][b], inp["f_ext"][b], inp["youngs"][b], act, steps=inp["T"], tol=tol)
+    _, gq, gv = adjoint.loss_and_grad(inp, b, tr["q"][-1], tr["v"][-1])
+    return tr, adjoint.backward(sc, tr, inp["youngs"][b], gq, gv, act)
+
+
+def _check(inp, gpu, b, tr, g, vel_floor=0.0):
+    for i in range(1, inp["T"] + 1):
+        assert rel(gpu["q"][b, i], tr["q"][i]) <= POS_TOL, ("q", b, i, rel(gpu["q"][b, i], tr["q"][i]))
+        assert rel(gpu["v"][b, i], tr["v"][i]) <= POS_TOL, ("v", b, i, rel(gpu["v"][b, i], tr["v"][i]))
+    for k in ("dq0", "dv0", "dfext"):
+        assert rel(gpu[k][b], g[k]) <= GRAD_TOL, (k, b, rel(gpu[k][b], g[k]))
+    assert abs(gpu["dE"][b] - g["dE"]) <= GRAD_TOL * abs(g["dE"]), ("dE", b)
+
+
+def test_c2_full_mesh_parity(torch):
+    # configs[1] at full size (16x8x8, 4131 DoF), first 4 steps, parity tolerances
+    inp = make_inputs(get_config("c2"), steps=4)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    tr, g = _oracle(inp, 0)
+    _check(inp, gpu, 0, tr, g)
+
+
+def test_c3_full_batch_sampled_sims_parity(torch):
+    # configs[2] at full size: all 64 sims on the GPU in one batch (the bench launch configuration), the
+    # stiffest and the softest sim (extremes of the shared-factor reading) against the oracle
+    inp = make_inputs(get_config("c3"), steps=2)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    E = inp["youngs"]
+    for b in (int(np.argmax(E)), int(np.argmin(E))):
+        tr, g = _oracle(inp, b)
+        _check(inp, gpu, b, tr, g)
+
+
+def test_c4_full_plate_contact_parity(torch):
+    # configs[3] at full size (20x20x4, 441 candidates) through first contact (step ~13), active sets
+    # bit-exact, positions/velocities/gradients within the bars
+    inp = make_inputs(get_config("c4"), steps=16)
+    sim = _bench_sim(inp, tol_fwd=2e-14, tol_adj=1e-11, max_iter_fwd=6000)
+    gpu = _run(torch, inp, sim)
+    sets = sim.contact_sets()
+    tr, g = _oracle(inp, 0)
+    assert np.array_equal(sets[0], tr["active"])
+    assert sets[0].sum() > 0, "the plate never touched the plane in the tested horizon"
+    _check(inp, gpu, 0, tr, g)
+
+
+def test_c5_full_properties(torch):
+    # configs[4] at full size (212k DoF, B = 8, contact + muscle), 2 steps: the oracle cannot follow (> 50 min
+    # per sim-step), so properties that hold at any size: converged, frictionless LCP (pinned z = 0 exactly,
+    # no node below -eps_phi, pinned set = KKT set of the final solve), bitwise determinism, and the adjoint
+    # gradient dL/dE against a central finite difference of the GPU forward itself.
+    inp = make_inputs(get_config("c5"), steps=2)
+    sim = _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11)
+    a = _run(torch, inp, sim)
+    sets = sim.contact_sets()
+    assert a["st"]["n_nonconverged"] == 0 and a["sb"]["n_nonconverged"] == 0
+    cand = 3 * inp["contact_nodes"] + 2
+    for b in range(inp["B"]):
+        for i in range(inp["T"]):
+            z = a["q"][b, i + 1][cand]
+            assert np.all(z[sets[b, i]] == 0.0)
+            assert z.min() >= -1e-6 * inp["cfg"].dx
+    assert sets.sum() > 0
+    b2 = _run(torch, inp, sim)
+    for k in ("q", "v", "dq0", "dE"):
+        assert np.array_equal(a[k], b2[k]), k
+    # central FD of L(E) for sim 0 (all sims share the factor; E enters through the projections' weight)
+    from oracle import adjoint
+    import copy
+    eps = 1e-4
+    Ls = []
+    for sgn in (1, -1):
+        inp2 = copy.deepcopy(inp)
+        inp2["youngs"] = inp["youngs"] * (1 + sgn * eps * (np.arange(inp["B"]) == 0))
+        r = _run(torch, inp2, sim)
+        Ls.append(adjoint.loss_and_grad(inp2, 0, r["q"][0, -1], r["v"][0, -1])[0])
+    fd = (Ls[0] - Ls[1]) / (2 * eps * inp["youngs"][0])
+    assert abs(fd - a["dE"][0]) <= 1e-4 * abs(fd) + 1e-12, (fd, a["dE"][0])
