@@ -255,8 +255,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     c.numAttrs = 1;
     return c;
   };
-  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          std::min(232448, 2 * sweep_smem_bytes<RC>())));
+  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
   auto resident_lvl = [&](int bytes) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, bytes));
@@ -265,12 +264,15 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
     if (!nt) return;
     if (s->k3_levels) {  // per-level mode: double-buffered items, static assignment
-      const int kp = kpad_of(kmax);  // each of the 2 buffers also holds the 4 warp tiles
-      const int smem = 2 * kp * (32 + RC) * 8;
+      const int kp = kpad_of(kmax);  // each buffer also holds the 4 warp tiles
+      const int bufb = kp * (32 + RC) * 8;
+      // ring depth: as many item buffers as fit (<= 4); small-item levels also get several CTAs per SM
+      const int nbuf = std::max(2, std::min(4, 232448 / bufb));
+      const int smem = nbuf * bufb;
       const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
       CK(cudaLaunchKernelEx(&c, k_sweep_level<RC, VEC>, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
-                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp));
+                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf));
       LAUNCH_CHECK(s);
       return;
     }

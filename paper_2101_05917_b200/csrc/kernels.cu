@@ -990,13 +990,13 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
 }
 
 // Per-level mode (default): items of ONE level, no dependency waits (kernel boundaries order the levels).
-// CTA c takes items c, c + G, c + 2G, ... (G = gridDim.x) and double-buffers them: the TMA round of the next
-// item is issued as soon as the current item's data has landed, so its latency hides behind the compute.
+// CTA c takes items c, c + G, c + 2G, ... (G = gridDim.x) through a ring of nbuf item buffers: while item j
+// computes, the TMA rounds of items j+1 .. j+nbuf-1 are in flight.
 template <int RC, bool VEC>
 __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
-                                                        double* __restrict__ partial, int kmax) {
+                                                        double* __restrict__ partial, int kmax, int nbuf) {
   constexpr int CW = RC / 4;
   extern __shared__ __align__(16) double sm[];
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -1006,12 +1006,9 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
   const int bufd = kmax * (32 + RC);  // doubles per buffer
-  __shared__ __align__(8) uint64_t mb[2];
-  __shared__ double red_s[1];  // (unused: keeps the static smem non-empty)
-  (void)red_s;
+  __shared__ __align__(8) uint64_t mb[4];
   if (tid == 0) {
-    mbar_init(mb, 1);
-    mbar_init(mb + 1, 1);
+    for (int i = 0; i < nbuf; ++i) mbar_init(mb + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -1048,24 +1045,26 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
         if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
         else Zs[k * RC + c] = 0.0;
       }
-      cp_async_commit();
     }
+    if (!VEC) cp_async_commit();
   };
   const int G = gridDim.x;
-  int rel = blockIdx.x, slot = 0;
-  unsigned ph[2] = {0, 0};
-  if (rel < nitems) load(rel, 0);
-  while (rel < nitems) {
+  // item ordinal j of this CTA: rel = blockIdx.x + j G, buffer j % nbuf, mbarrier parity (j / nbuf) & 1
+  for (int p = 0; p < nbuf - 1; ++p)
+    if (blockIdx.x + p * G < nitems) load(blockIdx.x + p * G, p);
+  for (int j = 0;; ++j) {
+    const int rel = blockIdx.x + j * G;
+    if (rel >= nitems) break;
+    const int slot = j % nbuf;
     const int it = t0 + rel;
     const int nk = sw.nk[it];
     if (!VEC) cp_async_wait_all();
-    mbar_wait(mb + slot, ph[slot]);
-    ph[slot] ^= 1;
-    __syncthreads();  // this item's data visible to all; the other buffer's previous readers are done
-    const int nrel = rel + G;
-    if (nrel < nitems) {
+    mbar_wait(mb + slot, (j / nbuf) & 1);
+    __syncthreads();  // item j visible to all; the buffer refilled next was released at the end of item j-1
+    const int pre = blockIdx.x + (j + nbuf - 1) * G;
+    if (pre < nitems) {
       fence_proxy_async();
-      load(nrel, slot ^ 1);  // prefetch the next item while this one computes
+      load(pre, (j + nbuf - 1) % nbuf);
     }
     const double* As = sm + slot * bufd;
     const double* Zs = As + kmax * 32;
@@ -1113,9 +1112,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
       const int r = e / RC, c = e - r * RC;
       if (c < rcn) dst[(int64_t)r * R + c] = ((redb[e] + redb[32 * RC + e]) + redb[64 * RC + e]) + redb[96 * RC + e];
     }
-    __syncthreads();  // buffer free before it is refilled two items from now
-    rel = nrel;
-    slot ^= 1;
+    __syncthreads();  // buffer released: it is refilled at the top of item j+1
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
