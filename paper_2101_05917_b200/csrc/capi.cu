@@ -267,7 +267,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
       const int kp = kpad_of(kmax);  // each buffer also holds the 4 warp tiles
       const int bufb = kp * (32 + RC) * 8;
       // ring depth: as many item buffers as fit (<= 4); small-item levels also get several CTAs per SM
-      const int nbuf = std::max(2, std::min(4, (232448 - 1024) / bufb));
+      const int nbuf = 2;  // measured: 2 buffers x several CTAs/SM beats deeper rings with 1 CTA/SM
       const int smem = nbuf * bufb;
       const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
