@@ -77,18 +77,26 @@ def param_terms(scene, x, u, act=None):
     return dw, dr
 
 
-def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None):
+def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL_dv_steps=None):
     """Reverse pass over a trajectory from oracle.pd.forward.
 
-    Returns dict(dq0, dv0, dfext (summed over steps), dE, dnu, dw, dact[T,m] or None)."""
+    Per-step losses L = sum_i l_i(q_i, v_i) (the Plant task's "loss at each time step"): optional
+    dL_dq_steps, dL_dv_steps [T+1, 3n] are added to the adjoint of state i when the reverse pass reaches it.
+    Returns dict(dq0, dv0, dfext (summed over steps), dfext_steps [T, 3n] (= u_i, dL/df_ext of step i),
+    dE, dnu, dw, dact[T,m] or None)."""
     h = scene.h
     w = scene.w_of(youngs)
     T = traj["q"].shape[0] - 1
     ax = dL_dqT.copy()
     av = dL_dvT.copy()
+    if dL_dq_steps is not None:
+        ax = ax + dL_dq_steps[T]
+    if dL_dv_steps is not None:
+        av = av + dL_dv_steps[T]
     base = ~scene.free
     cand = scene.normal_dofs(scene.contact_nodes) if len(scene.contact_nodes) else np.zeros(0, int)
     dfext = np.zeros(scene.N)
+    dfext_steps = np.zeros((T, scene.N))
     dw_tot = 0.0
     dact = np.zeros((T, scene.m)) if scene.muscle else None
     for i in range(T - 1, -1, -1):
@@ -105,13 +113,19 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None):
         if dr is not None:
             dact[i] = dr
         dfext += u
+        dfext_steps[i] = u
         ax = scene.mass / h ** 2 * u - av / h              # (1/h^2)(dy/dx_i)^T M u - a_v/h
         av = scene.mass / h * u                            # dy/dv_i = h I
+        if dL_dq_steps is not None:
+            ax = ax + dL_dq_steps[i]
+        if dL_dv_steps is not None:
+            av = av + dL_dv_steps[i]
         ax[base] = 0.0
         av[base] = 0.0
     dfext[base] = 0.0
+    dfext_steps[:, base] = 0.0
     nu = scene.poisson
-    return dict(dq0=ax, dv0=av, dfext=dfext, dw=dw_tot,
+    return dict(dq0=ax, dv0=av, dfext=dfext, dfext_steps=dfext_steps, dw=dw_tot,
                 dE=dw_tot / (1.0 + nu), dnu=-dw_tot * youngs / (1.0 + nu) ** 2, dact=dact)
 
 

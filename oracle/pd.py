@@ -269,14 +269,18 @@ def scene_from_inputs(inp, youngs=None):
 
 def forward(scene, q0, v0, f_ext, youngs, act=None, steps=1, tol=1e-12, fixed_iter=0,
             method="newton"):
-    """Trajectory of one simulation: returns dict(q[T+1,3n], v[T+1,3n], active[T,|V|], stats)."""
+    """Trajectory of one simulation: returns dict(q[T+1,3n], v[T+1,3n], active[T,|V|], stats).
+
+    f_ext: [3n] constant or [T, 3n] per step."""
     w = scene.w_of(youngs)
     q = [q0.copy()]
     vv = [v0.copy()]
     actives, stats = [], []
+    f_ext = np.asarray(f_ext, dtype=np.float64)
     for i in range(steps):
         a = None if act is None else act[i]
-        r = scene.step(q[-1], vv[-1], f_ext, w, a, tol, fixed_iter, method)
+        fe = f_ext[i] if f_ext.ndim == 2 else f_ext          # time-varying f_ext [T, 3n] (P:161)
+        r = scene.step(q[-1], vv[-1], fe, w, a, tol, fixed_iter, method)
         q.append(r["x"])
         vv.append(r["v"])
         actives.append(r["active"])

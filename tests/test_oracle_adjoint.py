@@ -105,3 +105,40 @@ def test_gradients_vs_central_fd_cantilever():
 
 def test_gradients_vs_central_fd_muscle():
     _fd_check("c5s", 2, ["q0", "v0", "act", "E"], 1e-5, kw=dict(contact=False))
+
+
+def test_per_step_loss_and_time_varying_fext_vs_fd():
+    # L = sum_i c_i . q_i + e_i . v_i with a time-varying f_ext; gradients w.r.t. q0 and
+    # the per-step f_ext against central finite differences of the oracle forward (converged solves)
+    from oracle import adjoint, pd
+    from pd_inputs import get_config, make_inputs
+    inp = make_inputs(get_config("c1"), steps=3)
+    sc = pd.scene_from_inputs(inp)
+    T, N = 3, sc.N
+    rng = np.random.default_rng(7)
+    cq = rng.standard_normal((T + 1, N))
+    cv = rng.standard_normal((T + 1, N))
+    fext = rng.standard_normal((T, N)) * 0.05
+    fext[:, ~sc.free] = 0.0
+    E = inp["youngs"][0]
+
+    def L(q0, fe):
+        tr = pd.forward(sc, q0, inp["v0"][0], fe, E, steps=T, tol=1e-13)
+        return float(np.sum(cq * tr["q"]) + np.sum(cv * tr["v"])), tr
+
+    _, tr = L(inp["q0"][0], fext)
+    g = adjoint.backward(sc, tr, E, np.zeros(N), np.zeros(N), dL_dq_steps=cq, dL_dv_steps=cv)
+    eps = 1e-6
+    k = int(np.nonzero(sc.free)[0][7])
+    for which in ("q0", "f1"):
+        qp, qm = inp["q0"][0].copy(), inp["q0"][0].copy()
+        fp, fm = fext.copy(), fext.copy()
+        if which == "q0":
+            qp[k] += eps
+            qm[k] -= eps
+        else:
+            fp[1, k] += eps
+            fm[1, k] -= eps
+        fd = (L(qp, fp)[0] - L(qm, fm)[0]) / (2 * eps)
+        an = g["dq0"][k] if which == "q0" else g["dfext_steps"][1, k]
+        assert abs(fd - an) <= 1e-6 * max(1.0, abs(fd)), (which, fd, an)
