@@ -119,8 +119,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h,
  * by PD local-global iterations, Alg. 1 contact when
  * candidates exist.
  *   q0, v0          device [B][3n]
- *   f_ext           device [B][3n] non-gravity external force (N), constant over
- *                   steps (f_ext_step_stride = 0) or NULL
+ *   f_ext           device non-gravity external force (N): [B][3n] constant over steps
+ *                   (f_ext_step_stride = 0), [B][steps][3n] per step (f_ext_step_stride = 3n), or NULL
  *   actuation       device [B][steps][n_elems] muscle activation r, or NULL
  *   youngs_per_sim  device [B] Young's modulus per sim, or NULL (= material.youngs)
  *   q_traj, v_traj  device [B][steps+1][3n] outputs, or NULL
@@ -144,6 +144,16 @@ pd_status pd_backward(pd_sim* sim, const double* dL_dqT, const double* dL_dvT,
                       double* dL_dq0, double* dL_dv0, double* dL_dfext,
                       double* dL_dE, double* dL_dnu, double* dL_dact,
                       pd_stats* stats, void* cuda_stream);
+
+/* Reverse pass for per-step losses L = sum_i l_i(q_i, v_i) (the per-step losses of the paper's tasks, e.g.
+ * "loss at each time step"):
+ *   dL_dq_steps, dL_dv_steps  device [B][steps+1][3n] (dl_i/dq_i, dl_i/dv_i; NULL = 0)
+ *   dL_dfext_steps            device [B][steps][3n] output: dL/df_ext of each step (or NULL)
+ * other arguments as pd_backward.  Use f_ext_step_stride = 3n in pd_forward for per-step f_ext. */
+pd_status pd_backward_steps(pd_sim* sim, const double* dL_dq_steps, const double* dL_dv_steps,
+                            double* dL_dq0, double* dL_dv0, double* dL_dfext_steps,
+                            double* dL_dE, double* dL_dnu, double* dL_dact,
+                            pd_stats* stats, void* cuda_stream);
 
 /* Diagnostics / kernel-level parity hooks (same conventions as above). */
 /* grad_g[B][3n] = M/h^2 (x - y) + grad E_int(x) (eq:time_integration LHS) and

@@ -123,10 +123,12 @@ class Simulator:
         return st, arrs
 
     def forward(self, q0, v0, steps, f_ext=None, actuation=None, youngs=None, q_traj=None, v_traj=None):
-        """q0, v0: CUDA fp64 [B, 3n].  Returns a stats dict (numpy [B, steps] arrays)."""
+        """q0, v0: CUDA fp64 [B, 3n]; f_ext [B, 3n] (constant) or [B, steps, 3n] (per step).
+        Returns a stats dict (numpy [B, steps] arrays)."""
         B = q0.shape[0]
         st, arrs = self._stats(B, steps)
-        self._check(self.lib.pd_forward(self.handle, B, _ptr(q0), _ptr(v0), _ptr(f_ext), 0, _ptr(actuation),
+        stride = 0 if f_ext is None or f_ext.dim() == 2 else f_ext.shape[-1]
+        self._check(self.lib.pd_forward(self.handle, B, _ptr(q0), _ptr(v0), _ptr(f_ext), stride, _ptr(actuation),
                                         _ptr(youngs), steps, _ptr(q_traj), _ptr(v_traj), C.byref(st), _stream()))
         self._B, self._T = B, steps
         out = {k: v.reshape(B, steps) for k, v in arrs.items() if k in ("iters_fwd", "final_res_fwd", "contact_outer")}
@@ -140,6 +142,18 @@ class Simulator:
         self._check(self.lib.pd_backward(self.handle, _ptr(dL_dqT), _ptr(dL_dvT), _ptr(dL_dq0), _ptr(dL_dv0),
                                          _ptr(dL_dfext), _ptr(dL_dE), _ptr(dL_dnu), _ptr(dL_dact), C.byref(st),
                                          _stream()))
+        out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
+        out["n_nonconverged"] = st.n_nonconverged
+        return out
+
+    def backward_steps(self, dL_dq_steps=None, dL_dv_steps=None, dL_dq0=None, dL_dv0=None, dL_dfext_steps=None,
+                       dL_dE=None, dL_dnu=None, dL_dact=None):
+        """Per-step losses: dL_dq_steps / dL_dv_steps [B, T+1, 3n]; dL_dfext_steps output [B, T, 3n]."""
+        B, T = self._B, self._T
+        st, arrs = self._stats(B, T)
+        self._check(self.lib.pd_backward_steps(self.handle, _ptr(dL_dq_steps), _ptr(dL_dv_steps), _ptr(dL_dq0),
+                                               _ptr(dL_dv0), _ptr(dL_dfext_steps), _ptr(dL_dE), _ptr(dL_dnu),
+                                               _ptr(dL_dact), C.byref(st), _stream()))
         out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
         out["n_nonconverged"] = st.n_nonconverged
         return out

@@ -16,7 +16,7 @@ STATUS_NAMES = {0: "PD_OK", 1: "PD_ERR_INVALID_ARGUMENT", 2: "PD_ERR_NUMERICAL",
                 4: "PD_ERR_STATE"}
 
 # every symbol include/diffpd_b200.h declares
-EXPORTS = ["pd_create", "pd_forward", "pd_backward", "pd_eval_objective", "pd_apply_Ainv", "pd_apply_AN",
+EXPORTS = ["pd_create", "pd_forward", "pd_backward", "pd_backward_steps", "pd_eval_objective", "pd_apply_Ainv", "pd_apply_AN",
            "pd_project_rotations", "pd_info", "pd_profile", "pd_contact_sets", "pd_debug_k3_trace", "pd_last_error",
            "pd_destroy"]
 
@@ -66,6 +66,7 @@ def load():
     lib.pd_forward.argtypes = [vp, C.c_int32, vp, vp, vp, C.c_int64, vp, vp, C.c_int32, vp, vp,
                                C.POINTER(PdStats), vp]
     lib.pd_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(PdStats), vp]
+    lib.pd_backward_steps.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, C.POINTER(PdStats), vp]
     lib.pd_eval_objective.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp, vp]
     lib.pd_apply_Ainv.argtypes = [vp, C.c_int32, vp, vp, vp]
     lib.pd_apply_AN.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]

@@ -477,6 +477,13 @@ void zero_constrained(pd_sim* s, double* Y, int B) {
   LAUNCH_CHECK(s);
 }
 
+// zero Dirichlet nodes only
+void zero_constrained_fixed(pd_sim* s, double* Y, int B) {
+  k_zero_constrained<<<nblk((int64_t)3 * s->plan.n * B), 256, 0, s->stream>>>(Y, s->d_fixed, s->plan.n, B, nullptr,
+                                                                              nullptr);
+  LAUNCH_CHECK(s);
+}
+
 // Q_b = (S_ff)^{-1} for the current PIN of the sims in sel (device [B] or null = all): free list,
 // gather, blocked Gauss-Jordan.  One host sync (kcount) per call.
 void build_Q(pd_sim* s, int B, const int32_t* sel) {
@@ -851,7 +858,8 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   if (B < 1 || B > s->Bmax) return fail(s, PD_ERR_INVALID_ARGUMENT, "B out of [1, max_batch]");
   if (steps < 1 || steps > s->Tmax) return fail(s, PD_ERR_INVALID_ARGUMENT, "steps out of [1, max_steps]");
   if (!q0 || !v0) return fail(s, PD_ERR_INVALID_ARGUMENT, "q0 and v0 are required");
-  if (f_ext_step_stride != 0) return fail(s, PD_ERR_INVALID_ARGUMENT, "time-varying f_ext is not supported yet");
+  if (f_ext_step_stride != 0 && f_ext_step_stride != 3LL * s->plan.n)
+    return fail(s, PD_ERR_INVALID_ARGUMENT, "f_ext_step_stride must be 0 (constant) or 3n ([B][steps][3n])");
   if (s->w_m != 0.0 && !actuation) return fail(s, PD_ERR_INVALID_ARGUMENT, "muscle energy needs an actuation array");
   s->stream = (cudaStream_t)cuda_stream;
   s->launches = 0;
@@ -868,7 +876,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
     LAUNCH_CHECK(s);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(v0, s->V, n3, B);
     LAUNCH_CHECK(s);
-    if (f_ext) {
+    if (f_ext && !f_ext_step_stride) {
       k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(f_ext, s->Fext, n3, B);
       LAUNCH_CHECK(s);
     }
@@ -882,6 +890,10 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
     for (int i = 0; i < steps; ++i) {
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
       const int64_t act_bs = (int64_t)steps * P.m;
+      if (f_ext && f_ext_step_stride) {  // time-varying f_ext: this step's slice of [B][steps][3n]
+        k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(f_ext + (int64_t)i * n3, s->Fext, n3, B, (int64_t)steps * n3);
+        LAUNCH_CHECK(s);
+      }
       k_y<<<nblk(len), 256, 0, s->stream>>>(s->X, s->V, f_ext ? s->Fext : nullptr, s->d_mass, s->Y, P.n, B, s->h,
                                             s->gravity[0], s->gravity[1], s->gravity[2]);
       LAUNCH_CHECK(s);
@@ -1013,9 +1025,10 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   return PD_OK;
 }
 
-pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, double* dL_dq0, double* dL_dv0,
-                      double* dL_dfext, double* dL_dE, double* dL_dnu, double* dL_dact, pd_stats* stats,
-                      void* cuda_stream) {
+static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL_dvT, const double* dq_steps,
+                               const double* dv_steps, double* dL_dq0, double* dL_dv0, double* dL_dfext,
+                               double* dfext_steps, double* dL_dE, double* dL_dnu, double* dL_dact, pd_stats* stats,
+                               void* cuda_stream) {
   if (!s) return PD_ERR_INVALID_ARGUMENT;
   if (!s->have_traj) return fail(s, PD_ERR_STATE, "pd_backward needs a preceding pd_forward");
   s->stream = (cudaStream_t)cuda_stream;
@@ -1041,6 +1054,15 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
     }
     CK(cudaMemsetAsync(s->DF, 0, len * sizeof(double), s->stream));
     CK(cudaMemsetAsync(s->dw_acc, 0, B * sizeof(double), s->stream));
+    const int64_t sstride = (int64_t)(T + 1) * n3;  // batch stride of [B][T+1][3n] per-step loss arrays
+    if (dq_steps) {
+      k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)T * n3, n3, B, sstride, s->d_fixed);
+      LAUNCH_CHECK(s);
+    }
+    if (dv_steps) {
+      k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dv_steps + (int64_t)T * n3, n3, B, sstride, s->d_fixed);
+      LAUNCH_CHECK(s);
+    }
     const bool pcg = s->opt.accel_adj != 0;
     for (int i = T - 1; i >= 0; --i) {
       const double* x1 = s->traj + (int64_t)(i + 1) * len;
@@ -1120,8 +1142,21 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
       }
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->DF, 1.0, s->U, nullptr, 1.0, len, B, nullptr);
       LAUNCH_CHECK(s);
+      if (dfext_steps) {  // dL/df_ext of step i = u_i (0 on Dirichlet DoFs)
+        zero_constrained_fixed(s, s->U, B);
+        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->U, dfext_steps + (int64_t)i * n3, n3, B, (int64_t)T * n3);
+        LAUNCH_CHECK(s);
+      }
       k_adj_state<<<nblk(len), 256, 0, s->stream>>>(s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
       LAUNCH_CHECK(s);
+      if (dq_steps) {
+        k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)i * n3, n3, B, sstride, s->d_fixed);
+        LAUNCH_CHECK(s);
+      }
+      if (dv_steps) {
+        k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dv_steps + (int64_t)i * n3, n3, B, sstride, s->d_fixed);
+        LAUNCH_CHECK(s);
+      }
       s->pins_live = false;
     }
     if (dL_dq0) {
@@ -1173,6 +1208,20 @@ pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, dou
     return fail(s, PD_ERR_CUDA, e.what());
   }
   return PD_OK;
+}
+
+pd_status pd_backward(pd_sim* s, const double* dL_dqT, const double* dL_dvT, double* dL_dq0, double* dL_dv0,
+                      double* dL_dfext, double* dL_dE, double* dL_dnu, double* dL_dact, pd_stats* stats,
+                      void* cuda_stream) {
+  return backward_impl(s, dL_dqT, dL_dvT, nullptr, nullptr, dL_dq0, dL_dv0, dL_dfext, nullptr, dL_dE, dL_dnu, dL_dact,
+                       stats, cuda_stream);
+}
+
+pd_status pd_backward_steps(pd_sim* s, const double* dL_dq_steps, const double* dL_dv_steps, double* dL_dq0,
+                            double* dL_dv0, double* dL_dfext_steps, double* dL_dE, double* dL_dnu, double* dL_dact,
+                            pd_stats* stats, void* cuda_stream) {
+  return backward_impl(s, nullptr, nullptr, dL_dq_steps, dL_dv_steps, dL_dq0, dL_dv0, nullptr, dL_dfext_steps, dL_dE,
+                       dL_dnu, dL_dact, stats, cuda_stream);
 }
 
 pd_status pd_eval_objective(pd_sim* s, int32_t B, const double* x, const double* y, const double* youngs_per_sim,

@@ -198,12 +198,23 @@ __device__ void polar_rotation(const double* F, double* R) {
 }
 
 // ----------------------------------------------------------------- layout kernels
-__global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict__ out, int n3, int B) {
+__global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
+                               int64_t in_bstride = -1) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n3 * B) return;
   const int64_t d = i / B;
   const int b = (int)(i - d * B);
-  out[i] = in[(int64_t)b * n3 + d];
+  out[i] = in[(int64_t)b * (in_bstride < 0 ? n3 : in_bstride) + d];
+}
+// OUT[i] += in (ABI layout, batch stride in_bstride) on non-Dirichlet DoFs (per-step loss terms)
+__global__ void k_add_abi(double* __restrict__ out, const double* __restrict__ in, int n3, int B, int64_t in_bstride,
+                          const uint8_t* __restrict__ fixed) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n3 * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  if (fixed[d / 3]) return;
+  out[i] += in[(int64_t)b * in_bstride + d];
 }
 __global__ void k_state_to_abi(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
                                int64_t out_bstride) {

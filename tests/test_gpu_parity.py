@@ -256,3 +256,38 @@ def test_contact_deterministic(torch):
     assert np.array_equal(sa, sim.contact_sets())
     for k in ("q", "v", "dq0", "dv0", "dfext", "dE", "dnu"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ----------------------------------------------------------------- per-step losses, time-varying f_ext (8f.3)
+@pytest.mark.parametrize("name", ["c2s", "c4s"])
+def test_per_step_loss_time_varying_fext_parity(torch, name):
+    from oracle import adjoint, pd
+    inp = make_inputs(get_config(name))
+    B, T, N = inp["B"], inp["T"], 3 * inp["n_nodes"]
+    rng = np.random.default_rng(11)
+    free = np.ones(N, bool)
+    free[inp["fixed_dofs"]] = False
+    fext = 0.02 * rng.standard_normal((B, T, N))
+    fext[:, :, ~free] = 0.0
+    cq = rng.standard_normal((B, T + 1, N))
+    cv = rng.standard_normal((B, T + 1, N))
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"], tol_fwd=2e-14 if inp["cfg"].contact else 1e-12,
+               max_iter_fwd=4000)
+    qt = torch.zeros((B, T + 1, N), dtype=torch.float64, device="cuda")
+    vt = torch.zeros_like(qt)
+    st = sim.forward(to_dev(inp["q0"]), to_dev(inp["v0"]), T, f_ext=to_dev(fext), youngs=to_dev(inp["youngs"]),
+                     q_traj=qt, v_traj=vt)
+    assert st["n_nonconverged"] == 0
+    dq0 = torch.zeros((B, N), dtype=torch.float64, device="cuda")
+    dfs = torch.zeros((B, T, N), dtype=torch.float64, device="cuda")
+    dE = torch.zeros(B, dtype=torch.float64, device="cuda")
+    sim.backward_steps(to_dev(cq), to_dev(cv), dq0, None, dfs, dE)
+    q, dq0, dfs, dE = qt.cpu().numpy(), dq0.cpu().numpy(), dfs.cpu().numpy(), dE.cpu().numpy()
+    sc = pd.scene_from_inputs(inp)
+    tr = pd.forward(sc, inp["q0"][0], inp["v0"][0], fext[0], inp["youngs"][0], steps=T, tol=1e-13)
+    for i in range(1, T + 1):
+        assert rel(q[0, i], tr["q"][i]) <= POS_TOL
+    g = adjoint.backward(sc, tr, inp["youngs"][0], np.zeros(N), np.zeros(N), dL_dq_steps=cq[0], dL_dv_steps=cv[0])
+    assert rel(dq0[0], g["dq0"]) <= GRAD_TOL
+    assert rel(dfs[0], g["dfext_steps"]) <= GRAD_TOL
+    assert abs(dE[0] - g["dE"]) <= GRAD_TOL * abs(g["dE"])
