@@ -94,7 +94,8 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
     if dL_dv_steps is not None:
         av = av + dL_dv_steps[T]
     base = ~scene.free
-    cand = scene.normal_dofs(scene.contact_nodes) if len(scene.contact_nodes) else np.zeros(0, int)
+    sticky = getattr(scene, "contact_mode", "frictionless") == "sticky"
+    nodes = np.asarray(scene.contact_nodes)
     dfext = np.zeros(scene.N)
     dfext_steps = np.zeros((T, scene.N))
     dw_tot = 0.0
@@ -102,12 +103,19 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
     for i in range(T - 1, -1, -1):
         x1 = traj["q"][i + 1]
         cons = base.copy()
-        if len(cand):
-            cons[cand[traj["active"][i]]] = True
+        pins = scene.pinned_dofs(nodes[traj["active"][i]]) if len(nodes) else np.zeros(0, np.int64)
+        cons[pins] = True
         b = ax + av / h                                    # v_{i+1} = (x_{i+1} - x_i)/h
+        b_pin = b[pins].copy()
         b[cons] = 0.0
         a_i = None if act is None else act[i]
         u = solve_adjoint(scene, x1, w, a_i, b, cons)
+        extra = None
+        if sticky and len(pins):
+            # x_{i+1,a} = x_{i,a}: dL/dx_{i,a} += b_a - (A_N u)_a  (u_a = 0)
+            AN = assemble_AN(scene, x1, w, a_i)
+            extra = np.zeros_like(b)
+            extra[pins] = b_pin - (AN @ u)[pins]
         dw, dr = param_terms(scene, x1, u, a_i)
         dw_tot += dw
         if dr is not None:
@@ -115,6 +123,8 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
         dfext += u
         dfext_steps[i] = u
         ax = scene.mass / h ** 2 * u - av / h              # (1/h^2)(dy/dx_i)^T M u - a_v/h
+        if extra is not None:
+            ax = ax + extra
         av = scene.mass / h * u                            # dy/dv_i = h I
         if dL_dq_steps is not None:
             ax = ax + dL_dq_steps[i]

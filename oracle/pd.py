@@ -48,6 +48,7 @@ class Scene:
     contact_nodes: np.ndarray
     muscle: bool = False
     fiber: tuple = (1.0, 0.0, 0.0)
+    contact_mode: str = "frictionless"   # or "sticky": the paper's infinite-friction model
 
     def __post_init__(self):
         self.n = self.rest.shape[0]
@@ -220,6 +221,15 @@ class Scene:
     def normal_dofs(self, nodes):
         return 3 * np.asarray(nodes, np.int64) + 2
 
+    def pinned_dofs(self, nodes):
+        """DoFs held by an active contact node: the normal DoF at the plane (frictionless, reading §2.10) or
+        all three DoFs at the node's position x_i at the start of the step (sticky: "the contact node ... is
+        fixed", infinite friction, P:321 / Alg. 1 line "x_{i+1,j} = x_{i,j}", P:342-343)."""
+        nodes = np.asarray(nodes, np.int64)
+        if self.contact_mode == "sticky":
+            return (3 * nodes[:, None] + np.arange(3)[None, :]).ravel()
+        return 3 * nodes + 2
+
     def step(self, x, v, f_ext, w, act, tol, fixed_iter=0, method="newton"):
         """One implicit step (Alg. 1 when contact candidates exist).
 
@@ -236,11 +246,15 @@ class Scene:
         total_it = 0
         flag = True
         margins = []
+        sticky = self.contact_mode == "sticky"
         for outer in range(1, MAX_OUTER + 1):
             cons = base.copy()
-            cons[cand[active]] = True
+            pins = self.pinned_dofs(self.contact_nodes[active])
+            cons[pins] = True
             x0 = x.copy()                                       # x_{i+1} = x_i
-            x0[cand[active]] = 0.0                               # pinned at the plane
+            if not sticky:
+                x0[pins] = 0.0                                  # frictionless: pinned at the plane
+            # sticky: the pinned DoFs keep x_i, eq:complement with the coupling term (reading §2.9)
             xn, it, res = self.solve_step(x0, y, w, act, cons, tol, fixed_iter, method)
             total_it += it
             _, gg = self.objective(xn, y, w, act)
@@ -264,7 +278,8 @@ def scene_from_inputs(inp, youngs=None):
     return Scene(rest=inp["rest"], hex8=inp["hex8"], dx=cfg.dx, density=cfg.density, h=cfg.h,
                  youngs=cfg.youngs if youngs is None else youngs, poisson=cfg.poisson,
                  gravity=np.asarray(cfg.gravity, float), fixed_dofs=inp["fixed_dofs"],
-                 contact_nodes=inp["contact_nodes"], muscle=cfg.muscle)
+                 contact_nodes=inp["contact_nodes"], muscle=cfg.muscle,
+                 contact_mode=getattr(cfg, "contact_mode", "frictionless"))
 
 
 def forward(scene, q0, v0, f_ext, youngs, act=None, steps=1, tol=1e-12, fixed_iter=0,

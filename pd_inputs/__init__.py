@@ -42,6 +42,7 @@ class Config:
     fixed_iter: int = 0      # >0: run exactly this many plain PD iterations (c1)
     dirichlet: str = "none"  # "x0": all nodes on the x = 0 face fixed at rest
     contact: bool = False    # bottom-face nodes are contact candidates (plane z=0)
+    contact_mode: str = "frictionless"  # or "sticky" (the paper's infinite-friction nodes)
     muscle: bool = False     # per-element fiber actuation along +x
     loss: str = "linear_qv"  # "linear_q" | "linear_qv" | "tip"
     v0_std: float = 0.0      # N(0, v0_std) per free node component

@@ -105,3 +105,62 @@ def test_active_set_is_the_unique_kkt_point_by_enumeration():
     assert len(kkt) == 1
     np.testing.assert_array_equal(kkt[0][1], r["active"])
     assert r["active"].any()
+
+
+def _sticky_block():
+    """A 3x2x2 block standing on z = 0 under gravity, small horizontal push: every bottom node is active
+    (lambda > 0) at every step, so the active set is locally constant and finite differences are valid."""
+    from oracle import pd
+    from pd_inputs import grid_mesh
+    rest, hex8 = grid_mesh((3, 2, 2), 0.01)
+    cand = np.nonzero(rest[:, 2] == 0.0)[0]
+    sc = pd.Scene(rest=rest, hex8=hex8, dx=0.01, density=1e3, h=0.01, youngs=1e5, poisson=0.45,
+                  gravity=np.array([0.0, 0.0, -9.81]), fixed_dofs=np.zeros(0, np.int64), contact_nodes=cand,
+                  contact_mode="sticky")
+    rng = np.random.default_rng(3)
+    N = rest.size
+    f = 0.002 * rng.standard_normal(N)                    # small horizontal push
+    f[2::3] = 0.0
+    v0 = np.zeros(N)
+    return sc, rest.ravel().copy(), v0, f, rng
+
+
+def test_sticky_nodes_do_not_move():
+    # infinite friction (P:321): an active node keeps x_i in all three DoFs, its velocity is exactly 0
+    from oracle import pd
+    sc, q0, v0, f, _ = _sticky_block()
+    tr = pd.forward(sc, q0, v0, f, 1e5, steps=3, tol=1e-13)
+    cand = np.asarray(sc.contact_nodes)
+    for i in range(3):
+        act = cand[tr["active"][i]]
+        assert act.size == cand.size                      # the standing block presses every bottom node
+        pins = (3 * act[:, None] + np.arange(3)).ravel()
+        assert np.array_equal(tr["q"][i + 1][pins], tr["q"][i][pins])
+        assert np.all(tr["v"][i + 1][pins] == 0.0)
+
+
+def test_sticky_gradients_vs_central_fd():
+    # the adjoint with the pinned-value term dL/dx_{i,a} += b_a - (A_N u)_a against central FD, including a
+    # DoF of a pinned node (where only that term carries the gradient)
+    from oracle import adjoint, pd
+    sc, q0, v0, f, rng = _sticky_block()
+    N = q0.size
+    cq, cv = rng.standard_normal(N), rng.standard_normal(N)
+
+    def L(q, v):
+        tr = pd.forward(sc, q, v, f, 1e5, steps=2, tol=1e-13)
+        return float(cq @ tr["q"][-1] + cv @ tr["v"][-1]), tr
+
+    _, tr = L(q0, v0)
+    g = adjoint.backward(sc, tr, 1e5, cq, cv)
+    pinned_dof = 3 * int(sc.contact_nodes[1]) + 0
+    free_dof = 3 * int(np.nonzero(q0[2::3] > 0.015)[0][0]) + 1
+    eps = 1e-7
+    for k in (pinned_dof, free_dof):
+        qp, qm = q0.copy(), q0.copy()
+        qp[k] += eps
+        qm[k] -= eps
+        fd = (L(qp, v0)[0] - L(qm, v0)[0]) / (2 * eps)
+        assert abs(fd - g["dq0"][k]) <= 1e-5 * max(1.0, abs(fd)), (k, fd, g["dq0"][k])
+    # v0 of a pinned node has no effect (x_1 = x_0 there): its gradient is exactly (M/h) u_a = 0
+    assert g["dv0"][pinned_dof] == 0.0
