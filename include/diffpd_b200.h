@@ -89,6 +89,9 @@ typedef struct {
   int32_t outer_warm;     /* 1: outer iterations k > 1 of Alg. 1 start from iteration k-1's x
                              (pinned DoFs moved to the plane) instead of x_i; the converged x
                              of each corrector solve is the same            */
+  int32_t contact_mode;   /* 1 (or 0): frictionless — an active candidate's normal DoF is pinned on the
+                             plane (reading §2.10); 2: sticky — all three DoFs of an active candidate
+                             are held at x_i (the paper's infinite-friction nodes)  */
   int32_t x0_predict;     /* 1: start each step's solve from x_i + h v_i instead of x_i (converged
                              configurations only; fixed_iter keeps x^0 = x_i, reading §2.6).
                              Changes iteration counts, not the converged minimiser          */

@@ -67,6 +67,7 @@ struct pd_sim {
   // contact K5
   int nc = 0, csup_first = 0;
   bool pins_live = false;          // the solve applies the constrained root block
+  int sticky = 0;                  // contact_mode 2: active nodes hold all DoFs at x_i (infinite friction)
   int32_t *d_cand_node = nullptr, *d_cand_of_node = nullptr, *d_cand_of_loc = nullptr;
   double *d_S = nullptr, *LAM = nullptr, *Qc = nullptr, *PIc = nullptr, *Cb = nullptr, *Mb = nullptr, *Rb = nullptr,
          *Rsave = nullptr;
@@ -320,8 +321,8 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     double* root = s->S0 + (int64_t)s->csup_first * R;
     CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
     sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 0, 1);
-    k_contact_fix<<<dim3((s->nc + 7) / 8, B), 256, 0, s->stream>>>(s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos,
-                                                                   s->Qc, root);
+    k_contact_fix<<<dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, s->stream>>>(
+        s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos, s->Qc, root);
     LAUNCH_CHECK(s);
     sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 1, P.nlevels);
   } else {
@@ -395,7 +396,7 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
                                                           s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, Gout ? Gout : s->G,
                                                           s->W, s->S0,
                                                           pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr,
-                                                          pin ? s->LAM : nullptr);
+                                                          pin ? s->LAM : nullptr, s->sticky);
   LAUNCH_CHECK(s);
 }
 
@@ -415,7 +416,7 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                           s->d_fixed, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, OUT,
                                                           nullptr, nullptr, pin ? s->d_cand_of_node : nullptr,
-                                                          pin ? s->PIN : nullptr, nullptr);
+                                                          pin ? s->PIN : nullptr, nullptr, s->sticky);
   LAUNCH_CHECK(s);
 }
 
@@ -473,7 +474,7 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
 void zero_constrained(pd_sim* s, double* Y, int B) {
   const bool pin = s->pins_live;
   k_zero_constrained<<<nblk((int64_t)3 * s->plan.n * B), 256, 0, s->stream>>>(
-      Y, s->d_fixed, s->plan.n, B, pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr);
+      Y, s->d_fixed, s->plan.n, B, pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr, s->sticky);
   LAUNCH_CHECK(s);
 }
 
@@ -638,6 +639,10 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     if (s->opt.max_iter_adj < 1) s->opt.max_iter_adj = 10000;
     if (s->opt.max_outer < 1) s->opt.max_outer = 10;
     if (!(s->opt.eps_phi > 0)) s->opt.eps_phi = 1e-6 * mesh->dx;
+    if (s->opt.contact_mode == 0) s->opt.contact_mode = 1;
+    if (s->opt.contact_mode != 1 && s->opt.contact_mode != 2)
+      return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "contact_mode must be 1 (frictionless) or 2 (sticky)");
+    s->sticky = s->opt.contact_mode == 2 ? 1 : 0;
     s->Bmax = opts->max_batch;
     s->Tmax = opts->max_steps;
     double fiber[3] = {mat->fiber[0], mat->fiber[1], mat->fiber[2]};
@@ -917,7 +922,8 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       for (int outer = 1; outer <= (contact ? s->opt.max_outer : 1); ++outer) {
         if (contact) {
           k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact,
-                                                              (s->opt.outer_warm && outer > 1) || (predict && outer == 1));
+                                                              (s->opt.outer_warm && outer > 1) || (predict && outer == 1),
+                                                              s->sticky);
           LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
           if (outer > 1) build_Q(s, B, s->oact);
           CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
@@ -1147,8 +1153,21 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->U, dfext_steps + (int64_t)i * n3, n3, B, (int64_t)T * n3);
         LAUNCH_CHECK(s);
       }
+      const bool sticky_step = s->sticky && s->pins_live;
+      if (sticky_step) {  // pinned values x_{i+1,a} = x_{i,a}: EX = b_a - (A_N u)_a
+        s->pins_live = false;  // A_N u on every row, pinned rows included
+        apply_AN(s, B, x1, s->U, s->Z, act_i, act_bs, s->JC);
+        s->pins_live = true;
+        k_sticky_extra<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->AX, s->AV, s->Z, 1.0 / h, P.n, B, s->d_cand_of_node,
+                                                         s->PIN);
+        LAUNCH_CHECK(s);
+      }
       k_adj_state<<<nblk(len), 256, 0, s->stream>>>(s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
       LAUNCH_CHECK(s);
+      if (sticky_step) {
+        k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->AX, s->AX, 1.0, s->Pv, nullptr, 1.0, len, B, nullptr);
+        LAUNCH_CHECK(s);
+      }
       if (dq_steps) {
         k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)i * n3, n3, B, sstride, s->d_fixed);
         LAUNCH_CHECK(s);

@@ -639,7 +639,7 @@ __global__ void k_gather(const double* __restrict__ X, const double* __restrict_
                          const int32_t* __restrict__ pos_of_node, int n, int B, double inv_h2, int mode,
                          double* __restrict__ G, double* __restrict__ W, double* __restrict__ RHS,
                          const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
-                         double* __restrict__ LAM) {
+                         double* __restrict__ LAM, int pin_all = 0) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= (int64_t)n * B) return;
   const int node = (int)(tid / B), b = (int)(tid - (int64_t)node * B);
@@ -656,9 +656,9 @@ __global__ void k_gather(const double* __restrict__ X, const double* __restrict_
     double g = mode == 0 ? mh * (X[i] - Y[i]) + s : mh * X[i] + s;
     double wv = mode == 0 ? mh * Y[i] : 0.0;
     bool pinned = false;
-    if (ax == 2 && cj >= 0 && PIN) {
+    if ((ax == 2 || pin_all) && cj >= 0 && PIN) {  // pin_all: sticky contact holds all DoFs of the node
       pinned = PIN[(int64_t)cj * B + b] != 0;
-      if (LAM) LAM[(int64_t)cj * B + b] = pinned ? g : 0.0;
+      if (LAM && ax == 2) LAM[(int64_t)cj * B + b] = pinned ? g : 0.0;  // lambda = normal force
     }
     if (fx || pinned) { g = 0.0; wv = 0.0; }
     G[i] = g;
@@ -1335,13 +1335,15 @@ __global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ 
                                                      const int32_t* __restrict__ kcount, const int32_t* __restrict__ flist,
                                                      const int32_t* __restrict__ fpos, const double* __restrict__ Q,
                                                      double* __restrict__ Xroot) {
-  const int b = blockIdx.y;
+  // blockIdx.y = a*B + b over the pinned axes (frictionless: only z; sticky: x, y, z -> gridDim.y = 3B)
+  const int b = blockIdx.y % B;
+  const int ax = gridDim.y == (unsigned)B ? 2 : (int)(blockIdx.y / B);
   const int k = kcount[b];
   if (k == c) return;  // no pins: the unconstrained root solve stands
   const int lane = threadIdx.x & 31;
   const int loc = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (loc >= c) return;
-  const int col = 2 * B + b;
+  const int col = ax * B + b;
   const int fi = fpos[(int64_t)b * c + loc];
   double acc = 0;
   if (fi >= 0) {
@@ -1359,7 +1361,7 @@ __global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ 
 // solve's converged point does not depend on its start; only the iteration count does).
 __global__ void k_contact_restart(double* __restrict__ X, const double* __restrict__ Xp, int n, int B,
                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
-                                  const int32_t* __restrict__ oact, int warm) {
+                                  const int32_t* __restrict__ oact, int warm, int pin_all = 0) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -1367,7 +1369,9 @@ __global__ void k_contact_restart(double* __restrict__ X, const double* __restri
   if (!oact[b]) return;
   const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
   const int cj = cand_of_node[node];
-  X[i] = (ax == 2 && cj >= 0 && PIN[(int64_t)cj * B + b]) ? 0.0 : (warm ? X[i] : Xp[i]);
+  const bool pinned = (ax == 2 || pin_all) && cj >= 0 && PIN[(int64_t)cj * B + b];
+  // frictionless: the normal DoF on the plane z = 0; sticky: every DoF at x_i
+  X[i] = pinned ? (pin_all ? Xp[i] : 0.0) : (warm ? X[i] : Xp[i]);
 }
 
 // Predictor (Alg. 1, reading §2.11): active' = (phi < -eps_phi) or (lambda > 0), phi = z
@@ -1728,15 +1732,29 @@ __global__ void k_axpby(double* __restrict__ Y, const double* __restrict__ X, do
 }
 // zero fixed nodes (and pinned z DoFs) of a state vector
 __global__ void k_zero_constrained(double* __restrict__ Y, const uint8_t* __restrict__ fixed, int n, int B,
-                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN) {
+                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
+                                   int pin_all = 0) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
   const int b = (int)(i - d * B);
   const int node = (int)(d / 3), ax = (int)(d - 3 * (int64_t)node);
   bool z = fixed[node] != 0;
-  if (!z && ax == 2 && PIN && cand_of_node[node] >= 0) z = PIN[(int64_t)cand_of_node[node] * B + b] != 0;
+  if (!z && (ax == 2 || pin_all) && PIN && cand_of_node[node] >= 0) z = PIN[(int64_t)cand_of_node[node] * B + b] != 0;
   if (z) Y[i] = 0.0;
+}
+
+// Sticky contact adjoint (x_{i+1,a} = x_{i,a}): EX = (a_x + a_v/h - A_N u) on pinned DoFs, 0 elsewhere; added to
+// dL/dx_i after the state-adjoint update (oracle/adjoint.py).
+__global__ void k_sticky_extra(double* __restrict__ EX, const double* __restrict__ AX, const double* __restrict__ AV,
+                               const double* __restrict__ ANu, double inv_h, int n, int B,
+                               const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)3 * n * B) return;
+  const int64_t d = i / B;
+  const int b = (int)(i - d * B);
+  const int cj = cand_of_node[d / 3];
+  EX[i] = (cj >= 0 && PIN[(int64_t)cj * B + b]) ? AX[i] + AV[i] * inv_h - ANu[i] : 0.0;
 }
 
 // Adjoint PCG scalars.  dots layout: [0:B) first pair, [B:2B) second ...
