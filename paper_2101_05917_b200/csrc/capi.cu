@@ -133,7 +133,7 @@ namespace {
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 // DoFs per reduction block: ~4096 (DoF, sim) elements per block whatever B is (fixed partition =
 // deterministic sums).
-inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 1024 / B); }
+inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 2048 / B); }
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;

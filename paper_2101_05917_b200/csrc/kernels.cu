@@ -1471,8 +1471,18 @@ __global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int 
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= npairs * B) return;
   const int p = i / B, b = i - p * B;
-  double s = 0;
-  for (int c = lane; c < nchunk; c += 32) s += partial[((int64_t)p * nchunk + c) * B + b];
+  // 4 independent accumulators (loads in flight together), combined in a fixed order
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  const double* pp = partial + (int64_t)p * nchunk * B + b;
+  int c = lane;
+  for (; c + 96 < nchunk; c += 128) {
+    s0 += pp[(int64_t)c * B];
+    s1 += pp[(int64_t)(c + 32) * B];
+    s2 += pp[(int64_t)(c + 64) * B];
+    s3 += pp[(int64_t)(c + 96) * B];
+  }
+  for (; c < nchunk; c += 32) s0 += pp[(int64_t)c * B];
+  double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[i] = accumulate ? out[i] + s : s;
