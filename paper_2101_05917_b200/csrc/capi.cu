@@ -52,8 +52,6 @@ struct pd_sim {
   int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
   int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
   int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
-  int32_t* bar = nullptr;                       // K3 grid-barrier counters (one per level launch)
-  int bar_next = 0, pend_r0 = 0, pend_n = 0;    // K3: next barrier slot, deferred reduction of the last level
   int64_t* trace = nullptr;                     // K3 per-item timeline (debug hook, pd_debug_trace)
   int k3_levels = 1;                            // K3 launch per level (1) or one dataflow launch per sweep (0)
   int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
@@ -275,10 +273,8 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
       const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
       CK(cudaLaunchKernelEx(&c, k_sweep_level<RC, VEC>, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
-                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf,
-                            s->pend_r0, s->pend_n, fwd ? s->S2 : s->S0, s->S0, s->bar + s->bar_next++));
+                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf));
       LAUNCH_CHECK(s);
-      s->pend_n = 0;  // the previous level's reductions ran in this launch's phase A
       return;
     }
     // forward: sources z (S0), direct y (S2), group subtract into z (S0);
@@ -293,27 +289,9 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
                           s->k3_levels ? 0 : 1, kmax));
     LAUNCH_CHECK(s);
   };
-  // pending reduction of the last level launched: folded into the next level launch of the same sweep
-  // (phase A + grid barrier) or flushed by k_sweep_reduce at the end of the sweep
-  s->pend_n = 0;
-  s->bar_next = 0;
-  CK(cudaMemsetAsync(s->bar, 0, sizeof(int32_t) * 4 * (P.nlevels + 2), s->stream));
-  auto flush = [&](const SweepDev& d, bool fwd) {
-    if (!s->pend_n) return;
-    cudaLaunchConfig_t c = cfg_of(dim3(nblk((int64_t)s->pend_n * R)), dim3(256), 0);
-    CK(cudaLaunchKernelEx(&c, k_sweep_reduce, d, s->pend_r0, s->pend_n, R, (const double*)s->Spart, fwd ? s->S2 : s->S0,
-                          s->S0));
-    LAUNCH_CHECK(s);
-    s->pend_n = 0;
-  };
   auto reduce = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int j) {
     const int r0 = S.g_tptr[S.lvl_grp[j]], nr = S.g_tptr[S.lvl_grp[j + 1]] - r0;
     if (!nr) return;
-    if (s->k3_levels) {  // defer: the next level launch performs it before its items
-      s->pend_r0 = r0;
-      s->pend_n = nr;
-      return;
-    }
     cudaLaunchConfig_t c = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
     CK(cudaLaunchKernelEx(&c, k_sweep_reduce, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
     LAUNCH_CHECK(s);
@@ -330,7 +308,6 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
                S.lvl_kmax[j]);
         reduce(S, d, fwd, j);
       }
-      flush(d, fwd);
     } else {
       int km = 0;
       for (int j = j0; j < j1; ++j) km = std::max(km, S.lvl_kmax[j]);
@@ -737,7 +714,6 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->grab = s->alloc<int32_t>(4 * kGY * (P.nlevels + 1));
     s->k3_levels = std::getenv("PD_K3_DATAFLOW") ? 0 : 1;
     s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
-    s->bar = s->alloc<int32_t>(4 * (P.nlevels + 2));
     if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(8 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
     auto up_cd = [&](const HostPlan::Sweep& S) {
       std::vector<int32_t> c((size_t)P.nsup * kGY);

@@ -1007,39 +1007,11 @@ template <int RC, bool VEC>
 __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
-                                                        double* __restrict__ partial, int kmax, int nbuf,
-                                                        int red_r0, int red_n, double* __restrict__ red_assign,
-                                                        double* __restrict__ red_sub, int32_t* __restrict__ bar) {
+                                                        double* __restrict__ partial, int kmax, int nbuf) {
   constexpr int CW = RC / 4;
   extern __shared__ __align__(16) double sm[];
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  if (red_n > 0) {
-    // phase A: the previous level's reduction groups (its partial rows are complete: griddepcontrol.wait),
-    // thread per (target, column), partial rows in their planned order; then a grid-wide barrier (the grid is
-    // one resident wave) before any item reads the rows it produced
-    const int64_t nthr = (int64_t)gridDim.x * gridDim.y * 128;
-    for (int64_t g = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 128 + tid; g < (int64_t)red_n * R; g += nthr) {
-      const int t = red_r0 + (int)(g / R), c = (int)(g % R);
-      double acc = 0;
-      for (int q = sw.red_ptr[t]; q < sw.red_ptr[t + 1]; ++q) acc += __ldcg(partial + (int64_t)sw.red_src[q] * R + c);
-      const int64_t o = (int64_t)sw.red_row[t] * R + c;
-      if (sw.red_mode[t] == 0) red_assign[o] = acc;
-      else red_sub[o] = __ldcg(red_sub + o) - acc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const int total = (int)(gridDim.x * gridDim.y);
-      red_add_release(bar, 1);
-      int64_t spins = 0;
-      while (ld_acquire(bar) < total) {
-        __nanosleep(32);
-        if (++spins > (int64_t)1 << 26) __trap();
-      }
-    }
-    __syncthreads();
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic writes above -> TMA reads below
-  }
   const int rg = lane & 7, cg = lane >> 3;
   const int y = blockIdx.y;
   const int c0 = y * RC;
