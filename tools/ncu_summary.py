@@ -2,6 +2,7 @@
 the key metrics of --set full captures (.ncu-rep).  Usage:
     python tools/ncu_summary.py launches <launches.csv> > profiles/xxx.md
     python tools/ncu_summary.py full <report.ncu-rep> > profiles/yyy.md
+    python tools/ncu_summary.py seq <launches.csv> [first_id] [count]   (per-launch sequence, K3 level analysis)
 """
 import collections
 import csv
@@ -38,6 +39,30 @@ def launches(path):
         avg = v[0] / v[1]
         mb = v[2] / v[1]
         print(f"| {n} | {v[0] / 1e3:.3f} | {100 * v[0] / T:.1f}% | {v[1]} | {avg:.1f} | {mb:.2f} | {mb / avg * 1e3 if avg else 0:.0f} |")
+
+
+def seq(path, first=0, count=200):
+    rows = list(csv.reader(open(path)))
+    hdr, recs = None, collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        key = int(d["ID"])
+        m = recs.setdefault(key, {"name": d["Kernel Name"].split("(")[0].replace("void ", ""), "grid": d.get("Grid Size", "")})
+        v = d["Metric Value"].replace(",", "")
+        m[d["Metric Name"]] = float(v) if v not in ("", "n/a") else 0.0
+    print("| id | kernel | grid | us | DRAM MB | GB/s |")
+    print("|---|---|---|---|---|---|")
+    for i, (k, m) in enumerate(recs.items()):
+        if i < first or i >= first + count:
+            continue
+        t = m.get("gpu__time_duration.sum", 0.0) / 1e3
+        by = (m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)) / 1e6
+        print(f"| {k} | {m['name'][:40]} | {m['grid']} | {t:.1f} | {by:.2f} | {by / t * 1e3 if t else 0:.0f} |")
 
 
 WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throughput", "L2 Cache Throughput",
@@ -78,4 +103,7 @@ def full(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "seq":
+        seq(sys.argv[2], *[int(a) for a in sys.argv[3:5]])
+    else:
+        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
