@@ -54,6 +54,7 @@ struct pd_sim {
   int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
   int64_t* trace = nullptr;                     // K3 per-item timeline (debug hook, pd_debug_trace)
   int k3_levels = 1;                            // K3 launch per level (1) or one dataflow launch per sweep (0)
+  int k3_mma = 1;                               // per-level K3 products on the fp64 tensor cores (1) or FMA pipe (0)
   int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
@@ -256,10 +257,11 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     c.numAttrs = 1;
     return c;
   };
-  CK(cudaFuncSetAttribute(k_sweep_level<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));
+  auto* const level_fn = s->k3_mma ? k_sweep_level<RC, VEC, true> : k_sweep_level<RC, VEC, false>;
+  CK(cudaFuncSetAttribute(level_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024));
   auto resident_lvl = [&](int bytes) {
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_level<RC, VEC>, 128, bytes));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_fn, 128, bytes));
     return std::max(1, per_sm) * (int64_t)nsm;
   };
   auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
@@ -272,7 +274,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
       const int smem = nbuf * bufb;
       const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
-      CK(cudaLaunchKernelEx(&c, k_sweep_level<RC, VEC>, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
+      CK(cudaLaunchKernelEx(&c, level_fn, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
                             (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf));
       LAUNCH_CHECK(s);
       return;
@@ -713,6 +715,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     };
     s->grab = s->alloc<int32_t>(4 * kGY * (P.nlevels + 1));
     s->k3_levels = std::getenv("PD_K3_DATAFLOW") ? 0 : 1;
+    if (const char* e = std::getenv("PD_K3_MMA")) s->k3_mma = std::atoi(e) ? 1 : 0;
     s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
     if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(8 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
     auto up_cd = [&](const HostPlan::Sweep& S) {

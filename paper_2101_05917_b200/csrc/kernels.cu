@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
     const int it = t0 + next;
     int64_t* tr = (trace && y == 0) ? trace + (int64_t)next * 8 : nullptr;  // [start, deps, data, end, smid, cta, written, counted]
     if (tr && tid == 0) tr[0] = gtime();
-    const int nk = sw.nk[it], nkd = sw.nkd[it];
+    const int nk = sw.nk[it], nkd = sw.nkd[it], nkp = (nk + 3) & ~3;
     if (tid == 0) {
       s_next = atomicAdd(grab + y, 1);  // prefetch the next index (never waited on before this item is done)
       // wait until the item's right-hand-side rows are final (bounded: a schedule bug traps, never hangs)
@@ -851,8 +851,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
     if (VEC) {
       const bool whole = rcn == RC && RC == R && nkd == nk;  // contiguous rows, all columns: one copy
       if (tid == 0) {
-        mbar_arrive_expect_tx(mb, (unsigned)(nk * 256 + nk * rcn * 8));
-        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
+        mbar_arrive_expect_tx(mb, (unsigned)(nkp * 256 + nk * rcn * 8));
+        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb);
         if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb);
       }
       if (!whole)
@@ -863,8 +863,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
         }
     } else {
       if (tid == 0) {
-        mbar_arrive_expect_tx(mb, (unsigned)(nk * 256));
-        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb);
+        mbar_arrive_expect_tx(mb, (unsigned)(nkp * 256));
+        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb);
       }
       for (int i = tid; i < nk * RC; i += 128) {
         const int k = i / RC, c = i - k * RC;
@@ -890,8 +890,9 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
     const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
 #pragma unroll 2
     for (int k = k0; k < k1; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
-      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
+      // fragment layout (plan.h sweep_frag_pos): rows 4rg..4rg+3 of step k are two double2
+      const double2 a01 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2) * 32 + 4 * rg + (k & 3)) * 2);
+      const double2 a23 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2 + 1) * 32 + 4 * rg + (k & 3)) * 2);
       const double av[4] = {a01.x, a01.y, a23.x, a23.y};
       double zv[CW];
       if (CW % 2 == 0) {
@@ -1003,7 +1004,17 @@ __global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int 
 // Per-level mode (default): items of ONE level, no dependency waits (kernel boundaries order the levels).
 // CTA c takes items c, c + G, c + 2G, ... (G = gridDim.x) through a ring of nbuf item buffers: while item j
 // computes, the TMA rounds of items j+1 .. j+nbuf-1 are in flight.
-template <int RC, bool VEC>
+//
+// MMA = true: the item product runs on the fp64 tensor cores (mma.sync m8n8k4, DMMA): warp w takes k-groups
+// of 4 steps; per group one conflict-free double2 pair of A fragments (the stream's fragment layout) and RC/8
+// B fragments (right-hand-side columns), 4 x RC/8 MMAs into a 32 x RC accumulator tile held as fragments.
+// MMA = false: the same product on the fp64 FMA pipe, lane (rg, cg) = 4 rows x RC/4 columns.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+template <int RC, bool VEC, bool MMA>
 __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
@@ -1027,15 +1038,15 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
     const int it = t0 + rel;
     double* As = sm + slot * bufd;
     double* Zs = As + kmax * 32;
-    const int nk = sw.nk[it], nkd = sw.nkd[it];
+    const int nk = sw.nk[it], nkd = sw.nkd[it], nkp = (nk + 3) & ~3;
     const double* Ag = sw.A + sw.a_off[it];
     const int zr = sw.zrow[it];
     const int32_t* idx = rows + sw.zidx[it] - nkd;
     if (VEC) {
       const bool whole = rcn == RC && RC == R && nkd == nk;
       if (tid == 0) {
-        mbar_arrive_expect_tx(mb + slot, (unsigned)(nk * 256 + nk * rcn * 8));
-        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb + slot);
+        mbar_arrive_expect_tx(mb + slot, (unsigned)(nkp * 256 + nk * rcn * 8));
+        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb + slot);
         if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb + slot);
       }
       if (!whole)
@@ -1046,8 +1057,8 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
         }
     } else {
       if (tid == 0) {
-        mbar_arrive_expect_tx(mb + slot, (unsigned)(nk * 256));
-        bulk_g2s(As, Ag, (unsigned)(nk * 256), mb + slot);
+        mbar_arrive_expect_tx(mb + slot, (unsigned)(nkp * 256));
+        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb + slot);
       }
       for (int i = tid; i < nk * RC; i += 128) {
         const int k = i / RC, c = i - k * RC;
@@ -1079,41 +1090,85 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
     }
     const double* As = sm + slot * bufd;
     const double* Zs = As + kmax * 32;
-    double acc[4][CW];
+    double* redb = sm + slot * bufd;
+    if constexpr (MMA) {
+      constexpr int NT = (RC + 7) / 8;
+      const int g = lane >> 2, t = lane & 3;
+      double acc[4][NT][2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
-      for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-    const int per = (nk + 3) >> 2;
-    const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
+        for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      const int nq = (nk + 3) >> 2, per = (nq + 3) >> 2;
+      const int q0 = min(nq, w * per), q1 = min(nq, q0 + per);
+      const double2* A2 = reinterpret_cast<const double2*>(As);
 #pragma unroll 2
-    for (int k = k0; k < k1; ++k) {
-      const double2 a01 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg);
-      const double2 a23 = *reinterpret_cast<const double2*>(As + k * 32 + 4 * rg + 2);
-      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-      double zv[CW];
-      if (CW % 2 == 0) {
+      for (int q = q0; q < q1; ++q) {
+        const double2 a01 = A2[(q * 2) * 32 + lane];
+        const double2 a23 = A2[(q * 2 + 1) * 32 + lane];
+        const int k = 4 * q + t;
+        double b[NT];
 #pragma unroll
-        for (int c = 0; c < CW / 2; ++c) {
-          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
-          zv[2 * c] = t.x;
-          zv[2 * c + 1] = t.y;
+        for (int n = 0; n < NT; ++n) {  // padded k-steps read stale rows: their (zero) factor needs b = 0
+          const int col = 8 * n + g;
+          b[n] = (k < nk && col < RC) ? Zs[k * RC + col] : 0.0;
         }
-      } else {
 #pragma unroll
-        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+        for (int n = 0; n < NT; ++n) {
+          dmma_8x8x4(acc[0][n][0], acc[0][n][1], a01.x, b[n]);
+          dmma_8x8x4(acc[1][n][0], acc[1][n][1], a01.y, b[n]);
+          dmma_8x8x4(acc[2][n][0], acc[2][n][1], a23.x, b[n]);
+          dmma_8x8x4(acc[3][n][0], acc[3][n][1], a23.y, b[n]);
+        }
       }
+      __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
+      // fragment (m, n): rows 4g + m, columns 8n + 2t + {0, 1}
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int col = 8 * n + 2 * t + i;
+            if (col < RC) redb[w * 32 * RC + (4 * g + m) * RC + col] = acc[m][n][i];
+          }
+    } else {
+      double acc[4][CW];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+        for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+      const int per = (nk + 3) >> 2;
+      const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
+#pragma unroll 2
+      for (int k = k0; k < k1; ++k) {
+        // fragment layout (plan.h sweep_frag_pos): rows 4rg..4rg+3 of step k are two double2
+        const double2 a01 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2) * 32 + 4 * rg + (k & 3)) * 2);
+        const double2 a23 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2 + 1) * 32 + 4 * rg + (k & 3)) * 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        double zv[CW];
+        if (CW % 2 == 0) {
+#pragma unroll
+          for (int c = 0; c < CW / 2; ++c) {
+            const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
+            zv[2 * c] = t.x;
+            zv[2 * c + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+      }
+      __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) redb[w * 32 * RC + (4 * rg + r) * RC + cg * CW + c] = acc[r][c];
     }
-    __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
-    double* redb = sm + slot * bufd;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < CW; ++c) redb[w * 32 * RC + (4 * rg + r) * RC + cg * CW + c] = acc[r][c];
     __syncthreads();
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];

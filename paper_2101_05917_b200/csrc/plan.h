@@ -8,6 +8,15 @@
 
 namespace pdb {
 
+// Position of factor element (k, lane) inside a sweep item's block (k padded to a multiple of 4). The block
+// is stored in the fragment order of the fp64 MMA m8n8k4 with output row/col `lane` = 4 g + m (g = lane / 4
+// is the fragment's group, m = lane % 4 its M-tile): for k-group q = k / 4 and half h = m / 2, the 32 lanes
+// (g, t = k % 4) of a warp each read one contiguous double2 {m = 2h, 2h + 1} — one conflict-free 128-bit
+// shared-memory load per (q, h). The device kernels restate this index arithmetic (kernels.cu).
+inline int64_t sweep_frag_pos(int k, int lane) {
+  const int q = k >> 2, t = k & 3, g = lane >> 2, m = lane & 3;
+  return ((int64_t)(q * 2 + (m >> 1)) * 32 + g * 4 + t) * 2 + (m & 1);
+}
 
 struct HostPlan {
   // ---- mesh ----

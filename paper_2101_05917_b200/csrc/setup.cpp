@@ -188,7 +188,7 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
     S->lvl_kmax.assign(P.nlevels, 0);
     for (int l = 0; l < P.nlevels; ++l)
-      for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) S->lvl_kmax[l] = std::max(S->lvl_kmax[l], S->nk[t]);
+      for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) S->lvl_kmax[l] = std::max(S->lvl_kmax[l], (S->nk[t] + 3) & ~3);
   }
 }
 static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
@@ -220,13 +220,17 @@ static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vecto
     (void)kc;
     return 128;  // = kItemK: one item (32 x 128 factor block + 128 rhs rows) per warp buffer, one TMA round
   };
-  // one item: k-major block rows/cols of `val(k, lane)`, k = 0..nk
+  // one item: the block val(k, lane), k = 0..nk, lane = output row/col 0..31, in the fragment layout of the
+  // fp64 tensor-core MMA (m8n8k4; plan.h sweep_frag_pos): k padded with zeros to a multiple of 4
   int cur_sup = -1;
   auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val, int nkd = -1) {
     S.sup.push_back(cur_sup);
-    S.a_off.push_back((int64_t)S.A.size());
+    const int64_t base = (int64_t)S.A.size();
+    S.a_off.push_back(base);
+    const int nkp = (nk + 3) & ~3;
+    S.A.resize(base + (int64_t)nkp * L, 0.0);
     for (int k = 0; k < nk; ++k)
-      for (int l = 0; l < L; ++l) S.A.push_back(l < nv ? val(k, l) : 0.0);
+      for (int l = 0; l < nv; ++l) S.A[base + sweep_frag_pos(k, l)] = val(k, l);
     S.nk.push_back(nk);
     S.nkd.push_back(nkd < 0 ? nk : nkd);
     S.zrow.push_back(zr);

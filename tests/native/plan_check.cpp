@@ -89,7 +89,7 @@ int main(int argc, char** argv) {
           for (int k = 0; k < S.nk[t]; ++k) {
             const bool contig = k < S.nkd[t];
             const int zr = contig ? S.zrow[t] + k : P.rows[S.zidx[t] + k - S.nkd[t]];
-            acc += S.A[S.a_off[t] + (int64_t)k * 32 + l] * (fwd ? zsrc[zr] : (contig ? y[zr] : x[zr]));
+            acc += S.A[S.a_off[t] + sweep_frag_pos(k, l)] * (fwd ? zsrc[zr] : (contig ? y[zr] : x[zr]));
           }
           if (S.out[t] >= 0) direct[S.out[t] + l] = acc;
           else part[(int64_t)(-S.out[t] - 1) * 32 + l] = acc;
