@@ -212,7 +212,7 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   const int64_t chunk = dot_chunk(B);
   const int nchunk = (int)((len + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
-  k_dot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
+  k_dot_partial<<<nchunk, bd, p * bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
   LAUNCH_CHECK(s);
   k_dot_final<<<nblk((int64_t)(p * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
@@ -231,7 +231,9 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   // shared memory of a launch = its largest item (and >= the 4 x 32 x RC warp-tile buffer); residency by size
   auto smem_of = [&](int kmax) { return std::max(kmax * (32 + RC), 4 * 32 * RC) * 8; };
-  auto kpad_of = [&](int kmax) { return std::max(kmax, (4 * 32 * RC + 32 + RC - 1) / (32 + RC)); };  // buffer >= tiles
+  auto kpad_of = [&](int kmax) {  // buffer >= the 4 padded warp tiles
+    return std::max(kmax, (4 * 32 * tile_ld<RC>() + 32 + RC - 1) / (32 + RC));
+  };
   auto resident_of = [&](int bytes) {
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, bytes));
@@ -442,34 +444,45 @@ int read_nactive(pd_sim* s) {
   return *s->h_nactive;
 }
 
-// out[j*B + b] = <u_b, V_j,b> for j < nv, V_j = Vbase + j * (3n B)   (deterministic, 2 launches)
-void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double* out) {
+// out[j*B + b] = <u_b, V_j,b> for j < nv, V_j = Vbase + j * (3n B)   (deterministic, 2 launches);
+// with u2: out[(nv + j)*B + b] = <u2_b, V2_j,b> in the same pass
+void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double* out, const double* u2 = nullptr,
+          const double* V2base = nullptr) {
   const int64_t n3 = 3LL * s->plan.n;
   const int64_t chunk = dot_chunk(B);
   const int nchunk = (int)((n3 + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
-  k_mdot_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk, s->partial);
+  const int np = u2 ? 2 * nv : nv;
+  k_mdot_partial<<<nchunk, bd, np * bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk, s->partial,
+                                                                      u2, V2base);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk((int64_t)(nv * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, nv, out);
+  k_dot_final<<<nblk((int64_t)(np * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, np, out);
   LAUNCH_CHECK(s);
 }
 
-// objective g (eq:opt) and its gradient at X: Gout = grad g (constrained rows 0), fout[b] = g
-void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const double* act_step, int64_t act_bs) {
+// objective g (eq:opt) and its gradient at X: Gout = grad g (constrained rows 0), and either
+// fout[b] = g (with_f) or, for line-search trials, the parts inert[b] = sum m/h^2 |x - y|^2,
+// esum[b] = sum of element energies and inert[B + b] = |grad g|^2 (k_ls_accept forms g)
+void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const double* act_step, int64_t act_bs,
+            bool with_gn2 = false) {
   const HostPlan& P = s->plan;
   residual(s, B, X, s->Y, act_step, act_bs, s->d_fixed, Gout);
   const int64_t n3 = 3LL * P.n;
   const int64_t chunk = dot_chunk(B);
   const int nchunk = (int)((n3 + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
-  k_inertia_partial<<<nchunk, bd, bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B,
-                                                                    chunk, s->partial);
+  const int np = with_gn2 ? 2 : 1;
+  k_inertia_partial<<<nchunk, bd, np * bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3,
+                                                                         B, chunk, s->partial,
+                                                                         with_gn2 ? Gout : nullptr);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk((int64_t)(B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, 1, s->inert);
+  k_dot_final<<<nblk((int64_t)(np * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, np, s->inert);
   LAUNCH_CHECK(s);
   dots(s, B, P.m, {{s->EE, nullptr}}, s->esum);
-  k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
-  LAUNCH_CHECK(s);
+  if (fout) {
+    k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
+    LAUNCH_CHECK(s);
+  }
 }
 
 // zero Dirichlet nodes and (when pins are live) the pinned z DoFs of a state vector
@@ -534,17 +547,19 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
   auto LYs = [&](int k) { return s->LY + (int64_t)k * len; };
   CK(cudaMemcpyAsync(s->Xn, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
   eval_f(s, B, s->X, s->G, s->fcur, act_i, act_bs);
+  // dots[0:B] = |grad g|^2 (refreshed from each accepted trial by k_gram_store), dots[B:2B] = |W|^2 (W depends
+  // on y only: constant over the solve)
+  dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+  double* const gn2 = s->inert + B;  // |grad g(x_trial)|^2, from eval_f
   int hist = 0;
   for (int iter = 0;; ++iter) {
-    dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
-    CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-    k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
-                                                   s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
-                                                   s->st_flag_f + (int64_t)i * B, s->nactive, it_base);
+    // convergence check; also alpha = 1 and ls_act = active for the coming line search
+    k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
+                                          s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
+                                          s->st_flag_f + (int64_t)i * B, s->nactive, it_base, s->alpha_ls, s->ls_act);
     LAUNCH_CHECK(s);
     if (iter >= s->opt.max_iter_fwd) break;
     if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
-    CK(cudaMemcpyAsync(s->g2, s->dots, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
@@ -570,39 +585,27 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
       LAUNCH_CHECK(s);
     }
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
-    // Armijo backtracking from alpha = 1
-    k_fill_double<<<nblk(B, 64), 64, 0, s->stream>>>(s->alpha_ls, 1.0, B);  // alpha = 1
-    LAUNCH_CHECK(s);
-    CK(cudaMemcpyAsync(s->ls_act, s->active, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
+    // Armijo backtracking from alpha = 1 (set by k_fwd_check); g_new and the decision in k_ls_accept
     for (int trial = 0;; ++trial) {
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
       LAUNCH_CHECK(s);
-      eval_f(s, B, s->Xn, s->Gn, s->fnew, act_i, act_bs);
-      dots(s, B, n3, {{s->Gn, s->Gn}}, s->gn2);
-      CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-      k_ls_accept<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->gtd, s->g2, s->gn2, s->alpha_ls, s->ls_act,
-                                                     trial, max_trial, s->nactive, s->ls_flag, B);
+      eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
+      k_ls_accept<<<1, 256, 0, s->stream>>>(s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
+                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
       LAUNCH_CHECK(s);
       if (read_nactive(s) == 0) break;
     }
-    // curvature pair (s, y) into slot iter % m; commit x, grad g, g
+    // curvature pair (s, y) into slot iter % m and commit x, grad g (one pass); Gram row/column of the new
+    // pair (both multi-dots in one pass); f, |grad g|^2
     const int slot = iter % m;
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(LSs(slot), s->Xn, 1.0, s->X, nullptr, -1.0, len, B, s->active);
-    LAUNCH_CHECK(s);
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(LYs(slot), s->Gn, 1.0, s->G, nullptr, -1.0, len, B, s->active);
+    k_lbfgs_commit<<<nblk(len), 256, 0, s->stream>>>(LSs(slot), LYs(slot), s->X, s->G, s->Xn, s->Gn, len, B, s->active);
     LAUNCH_CHECK(s);
     const int nv = std::min(hist + 1, m);  // valid slots after this store are [0, nv)
-    mdot(s, B, LSs(slot), s->LY, nv, s->lb_da);  // s_new^T y_j
-    mdot(s, B, LYs(slot), s->LS, nv, s->lb_db);  // y_new^T s_j
-    k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_db, slot, m, nv, B, s->active);
+    mdot(s, B, LSs(slot), s->LY, nv, s->lb_da, LYs(slot), s->LS);  // s_new^T y_j | y_new^T s_j
+    k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)nv * B, slot, m, nv,
+                                                    B, s->active, s->fcur, s->fnew, s->dots, gn2);
     LAUNCH_CHECK(s);
     hist = nv;
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
-    LAUNCH_CHECK(s);
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->G, s->Gn, 1.0, nullptr, nullptr, 0.0, len, B, s->active);
-    LAUNCH_CHECK(s);
-    k_copy_masked<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->active, B);
-    LAUNCH_CHECK(s);
   }
 }
 
@@ -751,7 +754,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->dots = s->alloc<double>(3 * s->Bmax);
     for (int b = 1; b <= s->Bmax; ++b)
       s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
-    s->partial = s->alloc<double>(8 * s->max_partial_blocks + 64);
+    s->partial = s->alloc<double>(16 * s->max_partial_blocks + 64);  // up to 16 dot families (mdot pairs)
     s->active = s->alloc<int32_t>(s->Bmax);
     s->nactive = s->alloc<int32_t>(1);
     s->it_buf = s->alloc<int32_t>(s->Bmax);
@@ -778,10 +781,10 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       s->rho_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
       s->aj_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
       double** sc[] = {&s->fcur, &s->fnew, &s->alpha_ls, &s->gtd, &s->g2, &s->gn2, &s->inert, &s->esum, &s->dtmp};
-      for (double** p : sc) *p = s->alloc<double>(s->Bmax);
+      for (double** p : sc) *p = s->alloc<double>(2 * s->Bmax);  // inert: [inertia | |grad g|^2]
       s->ls_act = s->alloc<int32_t>(s->Bmax);
       double** lb[] = {&s->lb_sg, &s->lb_yr, &s->lb_beta, &s->lb_da, &s->lb_db};
-      for (double** p : lb) *p = s->alloc<double>((int64_t)s->nhist * s->Bmax);
+      for (double** p : lb) *p = s->alloc<double>((int64_t)2 * s->nhist * s->Bmax);  // lb_da: [da | db]
       s->lb_G = s->alloc<double>((int64_t)s->nhist * s->nhist * s->Bmax);
       s->ls_flag = s->alloc<int32_t>(s->Bmax);
     }
@@ -940,8 +943,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           for (int iter = 0;; ++iter) {
             residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
             dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
-            CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-            k_fwd_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter,
+            k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter,
                                                            s->opt.max_iter_fwd, s->active, s->st_iters_f + (int64_t)i * B,
                                                            s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
                                                            s->nactive, contact ? s->it_base : nullptr);
@@ -1104,36 +1106,32 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         dots(s, B, n3, {{s->Rv, s->Z}}, s->rz);
       }
       for (int iter = 0;; ++iter) {
-        dots(s, B, n3, {{s->Rv, s->Rv}});
-        CK(cudaMemsetAsync(s->nactive, 0, sizeof(int32_t), s->stream));
-        k_adj_check<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots, s->bb, B, s->opt.tol_adj, iter, s->opt.max_iter_adj,
-                                                       s->active, s->st_iters_a + (int64_t)i * B,
-                                                       s->st_res_a + (int64_t)i * B, s->st_flag_a + (int64_t)i * B,
-                                                       s->nactive);
+        // |r|^2: computed here on the first iteration (and by the fixed point), else by the fused dots at the
+        // end of the previous PCG iteration (dots[2B:3B]); k_adj_check also commits rz <- rz_new there
+        const bool fused_rr = pcg && iter > 0;
+        if (!fused_rr) dots(s, B, n3, {{s->Rv, s->Rv}});
+        k_adj_check<<<1, 256, 0, s->stream>>>(fused_rr ? s->dots + 2 * B : s->dots, s->bb, B, s->opt.tol_adj, iter,
+                                              s->opt.max_iter_adj, s->active, s->st_iters_a + (int64_t)i * B,
+                                              s->st_res_a + (int64_t)i * B, s->st_flag_a + (int64_t)i * B, s->nactive,
+                                              fused_rr ? s->rz : nullptr, s->dots + B);
         LAUNCH_CHECK(s);
         if (iter >= s->opt.max_iter_adj) break;
         if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
         if (pcg) {
-          apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs, s->JC);
-          zero_constrained(s, s->Q, B);
+          apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs, s->JC);  // (k_gather zeroes the constrained rows)
           dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
-          k_pcg_alpha<<<nblk(B, 64), 64, 0, s->stream>>>(s->rz, s->dots + B, s->alpha, s->active, B);
-          LAUNCH_CHECK(s);
-          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->U, s->U, 1.0, s->Pv, s->alpha, 1.0, len, B, s->active);
-          LAUNCH_CHECK(s);
-          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Rv, 1.0, s->Q, s->alpha, -1.0, len, B, s->active);
+          // u += alpha p, r -= alpha q, alpha = rz / pq (one pass)
+          k_pcg_update<<<nblk(len), 256, 0, s->stream>>>(s->U, s->Rv, s->Pv, s->Q, s->rz, s->dots + B, len, B, s->active);
           LAUNCH_CHECK(s);
           apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->active);
-          dots(s, B, n3, {{s->Rv, s->Z}}, s->dots + B);
-          k_pcg_beta<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots + B, s->rz, s->beta, s->active, B);
-          LAUNCH_CHECK(s);
-          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, 1.0, s->Pv, s->beta, 1.0, len, B, s->active);
+          dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + B);  // rz_new | |r|^2
+          // p = z + beta p, beta = rz_new / rz (rz itself is committed by the next k_adj_check)
+          k_pcg_dir<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, s->dots + B, s->rz, len, B, s->active);
           LAUNCH_CHECK(s);
         } else {
           // fixed point u <- u + A^{-1}(b - A_N u) == A^{-1}(b + dA u)  (eq:bp_update)
           apply_Ainv(s, B, s->Rv, s->U, nullptr, 1.0, 1.0, s->active);
-          apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs, s->JC);
-          zero_constrained(s, s->Q, B);
+          apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs, s->JC);  // (k_gather zeroes the constrained rows)
           k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
           LAUNCH_CHECK(s);
         }

@@ -749,6 +749,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int kItemK = 128;  // max k-steps per item (the planner's kc)
+// row stride (doubles) of the per-warp 32 x RC output tiles of k_sweep_level: RC rounded up so that a row is
+// an odd number of 16-byte units (conflict-free 16-byte fragment stores)
+template <int RC>
+__host__ __device__ constexpr int tile_ld() { return ((RC + 1) / 2 % 2 == 1) ? ((RC + 1) / 2) * 2 : ((RC + 1) / 2 + 1) * 2; }
 template <int RC>
 __host__ __device__ constexpr int sweep_item_doubles() { return kItemK * (32 + RC); }
 template <int RC>
@@ -1015,7 +1019,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
       : "d"(a), "d"(b));
 }
 template <int RC, bool VEC, bool MMA>
-__global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
+__global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                         double* __restrict__ partial, int kmax, int nbuf) {
@@ -1094,16 +1098,20 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
     if constexpr (MMA) {
       constexpr int NT = (RC + 7) / 8;
       const int g = lane >> 2, t = lane & 3;
-      double acc[4][NT][2];
+      // two accumulator sets (even / odd k-groups) when they fit in registers: twice the independent MMA
+      // chains in flight, summed once
+      constexpr int NU = NT <= 3 ? 2 : 1;
+      double acc[2][4][NT][2];
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) acc[u][m][n][0] = acc[u][m][n][1] = 0.0;
       const int nq = (nk + 3) >> 2, per = (nq + 3) >> 2;
       const int q0 = min(nq, w * per), q1 = min(nq, q0 + per);
       const double2* A2 = reinterpret_cast<const double2*>(As);
-#pragma unroll 2
-      for (int q = q0; q < q1; ++q) {
+      auto kstep = [&](int q, double (&ac)[4][NT][2]) {
         const double2 a01 = A2[(q * 2) * 32 + lane];
         const double2 a23 = A2[(q * 2 + 1) * 32 + lane];
         const int k = 4 * q + t;
@@ -1115,23 +1123,38 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
         }
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-          dmma_8x8x4(acc[0][n][0], acc[0][n][1], a01.x, b[n]);
-          dmma_8x8x4(acc[1][n][0], acc[1][n][1], a01.y, b[n]);
-          dmma_8x8x4(acc[2][n][0], acc[2][n][1], a23.x, b[n]);
-          dmma_8x8x4(acc[3][n][0], acc[3][n][1], a23.y, b[n]);
+          dmma_8x8x4(ac[0][n][0], ac[0][n][1], a01.x, b[n]);
+          dmma_8x8x4(ac[1][n][0], ac[1][n][1], a01.y, b[n]);
+          dmma_8x8x4(ac[2][n][0], ac[2][n][1], a23.x, b[n]);
+          dmma_8x8x4(ac[3][n][0], ac[3][n][1], a23.y, b[n]);
         }
+      };
+      int q = q0;
+      if (NU == 2) {
+        for (; q + 1 < q1; q += 2) {
+          kstep(q, acc[0]);
+          kstep(q + 1, acc[NU - 1]);
+        }
+      } else {
+#pragma unroll 2
+        for (; q + 1 < q1; ++q) kstep(q, acc[0]);
       }
+      if (q < q1) kstep(q, acc[0]);
       __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
-      // fragment (m, n): rows 4g + m, columns 8n + 2t + {0, 1}
+      // fragment (m, n): rows 4g + m, columns 8n + 2t + {0, 1}: one 16-byte store each; rows padded to
+      // kTileLd(RC) doubles (an odd number of 16-byte units: the 8 lanes of a store phase hit 8 distinct
+      // bank groups)
+      constexpr int LD = tile_ld<RC>();
 #pragma unroll
       for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int n = 0; n < NT; ++n)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int col = 8 * n + 2 * t + i;
-            if (col < RC) redb[w * 32 * RC + (4 * g + m) * RC + col] = acc[m][n][i];
-          }
+        for (int n = 0; n < NT; ++n) {
+          const int col = 8 * n + 2 * t;
+          if (col < RC)
+            *reinterpret_cast<double2*>(redb + w * 32 * LD + (4 * g + m) * LD + col) =
+                NU == 2 ? make_double2(acc[0][m][n][0] + acc[NU - 1][m][n][0], acc[0][m][n][1] + acc[NU - 1][m][n][1])
+                        : make_double2(acc[0][m][n][0], acc[0][m][n][1]);
+        }
     } else {
       double acc[4][CW];
 #pragma unroll
@@ -1167,16 +1190,18 @@ __global__ void __launch_bounds__(128, 4) k_sweep_level(SweepDev sw, int t0, int
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < CW; ++c) redb[w * 32 * RC + (4 * rg + r) * RC + cg * CW + c] = acc[r][c];
+        for (int c = 0; c < CW; ++c) redb[w * 32 * tile_ld<RC>() + (4 * rg + r) * tile_ld<RC>() + cg * CW + c] = acc[r][c];
     }
     __syncthreads();
     const int out = sw.out[it];
     const int nv = sw.nvalid[it];
     double* __restrict__ dst =
         out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
+    constexpr int LDT = tile_ld<RC>();
     for (int e = tid; e < nv * RC; e += 128) {
       const int r = e / RC, c = e - r * RC;
-      if (c < rcn) dst[(int64_t)r * R + c] = ((redb[e] + redb[32 * RC + e]) + redb[64 * RC + e]) + redb[96 * RC + e];
+      const double* rb = redb + r * LDT + c;
+      if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LDT]) + rb[64 * LDT]) + rb[96 * LDT];
     }
     __syncthreads();  // buffer released: it is refilled at the top of item j+1
   }
@@ -1468,29 +1493,41 @@ __global__ void k_contact_outer(const int32_t* __restrict__ oact, const int32_t*
 }
 
 // ----------------------------------------------------------------- per-sim reductions
+// Block-level per-sim sums: thread t holds acc for sim t % B; red = [np][nb] staged in shared memory, then
+// thread o < np*B adds the nb/B values of (pair o / B, sim o % B) in index order (two interleaved
+// accumulators, fixed combination) -> partial[(p*nchunk + blk)*B + b].  Deterministic.
+__device__ __forceinline__ void block_sim_sums(double* red, int np, int B, double* __restrict__ partial, int nchunk,
+                                               int blk) {
+  __syncthreads();
+  const int nb = blockDim.x, J = nb / B;
+  for (int o = threadIdx.x; o < np * B; o += nb) {
+    const int p = o / B, b = o - p * B;
+    const double* r = red + p * nb + b;
+    double s0 = 0.0, s1 = 0.0;
+    int j = 0;
+    for (; j + 1 < J; j += 2) {
+      s0 += r[j * B];
+      s1 += r[(j + 1) * B];
+    }
+    if (j < J) s0 += r[j * B];
+    partial[((int64_t)p * nchunk + blk) * B + b] = s0 + s1;
+  }
+}
 // partial[c][b] = sum over chunk c of u*v (up to 3 pairs); blockDim % B == 0 so that each
-// thread keeps one sim; fixed-order tree inside the block, fixed-order sum over chunks.
+// thread keeps one sim; fixed-order sum inside the block, fixed-order sum over chunks.
 __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, double* __restrict__ partial) {
   extern __shared__ double red[];
   const int nb = blockDim.x;
-  const int b = threadIdx.x % B;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
   double acc[3] = {0, 0, 0};
   for (int64_t i = beg + threadIdx.x; i < end; i += nb)
-    for (int p = 0; p < da.npairs; ++p) acc[p] += da.v[p] ? da.u[p][i] * da.v[p][i] : da.u[p][i];
-  for (int p = 0; p < da.npairs; ++p) {
-    red[threadIdx.x] = acc[p];
-    __syncthreads();
-    // threads with the same b: t = b + B*j, j < nb/B; pairwise tree over j
-    const int J = nb / B;
-    for (int step = 1; step < J; step <<= 1) {
-      const int j = threadIdx.x / B;
-      if ((j % (2 * step)) == 0 && j + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
-      __syncthreads();
-    }
-    if (threadIdx.x < B) partial[((int64_t)p * gridDim.x + blockIdx.x) * B + threadIdx.x] = red[threadIdx.x];
-    __syncthreads();
-  }
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+      if (p < da.npairs) acc[p] += da.v[p] ? da.u[p][i] * da.v[p][i] : da.u[p][i];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+    if (p < da.npairs) red[p * nb + threadIdx.x] = acc[p];
+  block_sim_sums(red, da.npairs, B, partial, gridDim.x, blockIdx.x);
 }
 // one warp per (pair, sim): lane l sums chunks l, l+32, ... in order, then a fixed xor tree (deterministic)
 __global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out,
@@ -1533,27 +1570,23 @@ __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* 
 // The quasi-Newton PD of P:79/P:254 (Liu et al.): minimise g (eq:opt) with L-BFGS whose initial inverse
 // Hessian is the prefactorised A^{-1}; Armijo backtracking on g.  Same minimiser as plain PD.
 
-// partial[c][b] = sum over chunk c of (m_node/h^2) (X - Y)^2   (fixed-order, like k_dot_partial)
+// partial[c][b] = sum over chunk c of (m_node/h^2) (X - Y)^2   (fixed-order, like k_dot_partial);
+// with G: a second pair, sum of G^2 (the gradient norm of the same evaluation)
 __global__ void k_inertia_partial(const double* __restrict__ X, const double* __restrict__ Y,
                                   const double* __restrict__ mass, double inv_h2, int64_t len, int B, int64_t chunk,
-                                  double* __restrict__ partial) {
+                                  double* __restrict__ partial, const double* __restrict__ G = nullptr) {
   extern __shared__ double red[];
   const int nb = blockDim.x;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
-  double acc = 0;
+  double acc = 0, acc2 = 0;
   for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
     const double d = X[i] - Y[i];
     acc += mass[i / B / 3] * inv_h2 * d * d;
+    if (G) acc2 += G[i] * G[i];
   }
   red[threadIdx.x] = acc;
-  __syncthreads();
-  const int J = nb / B;
-  for (int step = 1; step < J; step <<= 1) {
-    const int j = threadIdx.x / B;
-    if ((j % (2 * step)) == 0 && j + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
-    __syncthreads();
-  }
-  if (threadIdx.x < B) partial[(int64_t)blockIdx.x * B + threadIdx.x] = red[threadIdx.x];
+  if (G) red[nb + threadIdx.x] = acc2;
+  block_sim_sums(red, G ? 2 : 1, B, partial, gridDim.x, blockIdx.x);
 }
 
 // f[b] = 0.5 * inert[b] + esum[b]
@@ -1585,22 +1618,33 @@ __global__ void k_lbfgs_axpy(double* __restrict__ Y, const double* __restrict__ 
 // Armijo backtracking decision per sim.  Near the minimiser g no longer resolves the decrease in fp64;
 // there a step that leaves g unchanged to 1e-13 relative and lowers ||grad g|| is accepted (the oracle's
 // Newton uses the same rule).  After max_trial halvings the step is taken anyway and flagged.
-__global__ void k_ls_accept(const double* __restrict__ f, const double* __restrict__ fn, const double* __restrict__ gtd,
+// One block (loop over sims): the count of sims still searching is written to *nactive (no memset).
+// fn[b] = 0.5 inert[b] + esum[b] is formed here (the objective of the trial point, eq:opt).
+__global__ void k_ls_accept(const double* __restrict__ f, double* __restrict__ fn, const double* __restrict__ inert,
+                            const double* __restrict__ esum, const double* __restrict__ gtd,
                             const double* __restrict__ g2, const double* __restrict__ gn2, double* __restrict__ alpha,
                             int32_t* __restrict__ ls_active, int trial, int max_trial, int32_t* __restrict__ nactive,
                             int32_t* __restrict__ ls_flag, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !ls_active[b]) return;
-  const double a = alpha[b];
-  const bool armijo = fn[b] <= f[b] + 1e-4 * a * gtd[b];
-  const bool flat = fabs(fn[b] - f[b]) <= 1e-13 * fabs(f[b]) && gn2[b] < g2[b];
-  if (armijo || flat || trial >= max_trial) {
-    ls_active[b] = 0;
-    if (!(armijo || flat)) ls_flag[b] = 1;
-  } else {
-    alpha[b] = 0.5 * a;
-    atomicAdd(nactive, 1);
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (!ls_active[b]) continue;
+    const double fnb = 0.5 * inert[b] + esum[b];
+    fn[b] = fnb;
+    const double a = alpha[b];
+    const bool armijo = fnb <= f[b] + 1e-4 * a * gtd[b];
+    const bool flat = fabs(fnb - f[b]) <= 1e-13 * fabs(f[b]) && gn2[b] < g2[b];
+    if (armijo || flat || trial >= max_trial) {
+      ls_active[b] = 0;
+      if (!(armijo || flat)) ls_flag[b] = 1;
+    } else {
+      alpha[b] = 0.5 * a;
+      atomicAdd(&cnt, 1);
+    }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) *nactive = cnt;
 }
 
 // rho = 1/(s^T y) if the curvature pair is positive, else 0 (pair ignored)
@@ -1618,35 +1662,36 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
 //   beta_i  = rho_i (y_i^T r0 + sum_{j older} (alpha_j - beta_j) Gm[j][i]),
 //   d = -(r0 + sum_j (alpha_j - beta_j) s_j).
 
-// partial[(j*nchunk + c)*B + b] = sum over chunk c of u * V_j  (V_j = Vbase + j*vstride), j < nv
+// partial[(j*nchunk + c)*B + b] = sum over chunk c of u * V_j  (V_j = Vbase + j*vstride), j < nv; with u2:
+// pairs nv + j = u2 * V2_j as well (both families of the new curvature pair in one pass)
 __global__ void k_mdot_partial(const double* __restrict__ u, const double* __restrict__ Vbase, int64_t vstride,
-                               int nv, int64_t len, int B, int64_t chunk, double* __restrict__ partial) {
+                               int nv, int64_t len, int B, int64_t chunk, double* __restrict__ partial,
+                               const double* __restrict__ u2 = nullptr, const double* __restrict__ V2base = nullptr) {
   extern __shared__ double red[];
   const int nb = blockDim.x;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
-  double acc[8];
+  double acc[8], acc2[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  for (int j = 0; j < 8; ++j) acc[j] = acc2[j] = 0.0;
   for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
     const double ui = u[i];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (j < nv) acc[j] += ui * Vbase[j * vstride + i];
-  }
-  const int J = nb / B;
+    if (u2) {
+      const double wi = u2[i];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    if (j >= nv) break;
-    red[threadIdx.x] = acc[j];
-    __syncthreads();
-    for (int step = 1; step < J; step <<= 1) {
-      const int jj = threadIdx.x / B;
-      if ((jj % (2 * step)) == 0 && jj + step < J) red[threadIdx.x] += red[threadIdx.x + step * B];
-      __syncthreads();
+      for (int j = 0; j < 8; ++j)
+        if (j < nv) acc2[j] += wi * V2base[j * vstride + i];
     }
-    if (threadIdx.x < B) partial[((int64_t)j * gridDim.x + blockIdx.x) * B + threadIdx.x] = red[threadIdx.x];
-    __syncthreads();
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < nv) {
+      red[j * nb + threadIdx.x] = acc[j];
+      if (u2) red[(nv + j) * nb + threadIdx.x] = acc2[j];
+    }
+  block_sim_sums(red, u2 ? 2 * nv : nv, B, partial, gridDim.x, blockIdx.x);
 }
 
 // slot of the k-th newest pair at iteration `iter` (ring of m)
@@ -1726,10 +1771,13 @@ __global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ 
   Y[i] = sgn * v;
 }
 
-// new pair in slot sl: Gm[sl][j] = s_sl^T y_j (da[j]), Gm[j][sl] = s_j^T y_sl (db[j]); rho_sl
+// new pair in slot sl: Gm[sl][j] = s_sl^T y_j (da[j]), Gm[j][sl] = s_j^T y_sl (db[j]); rho_sl.
+// Also commits the accepted point's scalars: f = f_new, |grad g|^2 (gg[b], read by the next convergence
+// check) = |grad g_new|^2.
 __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, const double* __restrict__ da,
                              const double* __restrict__ db, int sl, int m, int nv, int B,
-                             const int32_t* __restrict__ active) {
+                             const int32_t* __restrict__ active, double* __restrict__ f, const double* __restrict__ fn,
+                             double* __restrict__ gg, const double* __restrict__ gn2) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
   for (int j = 0; j < nv; ++j) {
@@ -1738,6 +1786,23 @@ __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, 
   }
   const double sy = da[sl * B + b];
   rho[sl * B + b] = sy > 0.0 ? 1.0 / sy : 0.0;
+  f[b] = fn[b];
+  gg[b] = gn2[b];
+}
+
+// commit of an accepted L-BFGS step (one pass): S_sl = Xn - X, Y_sl = Gn - G, X = Xn, G = Gn (masked)
+__global__ void k_lbfgs_commit(double* __restrict__ S, double* __restrict__ Yv, double* __restrict__ X,
+                               double* __restrict__ G, const double* __restrict__ Xn, const double* __restrict__ Gn,
+                               int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (!active[b]) return;
+  const double xn = Xn[i], gn = Gn[i];
+  S[i] = xn - X[i];
+  Yv[i] = gn - G[i];
+  X[i] = xn;
+  G[i] = gn;
 }
 
 // v[b] = c (per-sim scalar fill)
@@ -1754,27 +1819,41 @@ __global__ void k_copy_masked(double* __restrict__ dst, const double* __restrict
 }
 
 // ----------------------------------------------------------------- iteration control
-// Forward convergence: res = sqrt(res2/den2); active[b] for the NEXT update.
+// Forward convergence: res = sqrt(res2/den2); active[b] for the NEXT update.  One block (loop over sims):
+// the active count is written to *nactive (no memset).  With alpha/ls_act: line-search state of the
+// coming iteration (alpha = 1, ls_act = active).
 __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, int iter, int fixed_iter,
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out,
-                            int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  if (!active[b]) return;
-  const double den = dots[B + b];
-  const double res = den > 0 ? sqrt(dots[b] / den) : sqrt(dots[b]);
-  bool go;
-  if (fixed_iter > 0) go = iter < fixed_iter;
-  else go = res > tol && iter < max_iter;
-  res_out[b] = res;
-  iters_out[b] = iter + (iter_base ? iter_base[b] : 0);
-  if (!go) {
-    active[b] = 0;
-    flag_out[b] = (fixed_iter == 0 && res > tol) ? 1 : 0;
-  } else {
-    atomicAdd(nactive, 1);  // integer count only (no effect on arithmetic)
+                            int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base,
+                            double* __restrict__ alpha = nullptr, int32_t* __restrict__ ls_act = nullptr) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    int act = active[b];
+    if (act) {
+      const double den = dots[B + b];
+      const double res = den > 0 ? sqrt(dots[b] / den) : sqrt(dots[b]);
+      bool go;
+      if (fixed_iter > 0) go = iter < fixed_iter;
+      else go = res > tol && iter < max_iter;
+      res_out[b] = res;
+      iters_out[b] = iter + (iter_base ? iter_base[b] : 0);
+      if (!go) {
+        active[b] = act = 0;
+        flag_out[b] = (fixed_iter == 0 && res > tol) ? 1 : 0;
+      } else {
+        atomicAdd(&cnt, 1);  // integer count only (no effect on arithmetic)
+      }
+    }
+    if (alpha) {
+      alpha[b] = 1.0;
+      ls_act[b] = act;
+    }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) *nactive = cnt;
 }
 
 // v = (x - xprev)/h
@@ -1824,35 +1903,55 @@ __global__ void k_sticky_extra(double* __restrict__ EX, const double* __restrict
 
 // Adjoint PCG scalars.  dots layout: [0:B) first pair, [B:2B) second ...
 // alpha = rz / pq ; converged check on rr / bb.
-__global__ void k_pcg_alpha(const double* __restrict__ rz, const double* __restrict__ pq, double* __restrict__ alpha,
-                            const int32_t* __restrict__ active, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !active[b]) return;
+// PCG (preconditioner A^{-1}) fused updates, per-sim coefficients formed per element:
+//   k_pcg_update: alpha = rz / pq; U += alpha P; R -= alpha Q
+//   k_pcg_dir:    beta = rz_new / rz; P = Z + beta P
+__global__ void k_pcg_update(double* __restrict__ U, double* __restrict__ Rv, const double* __restrict__ P,
+                             const double* __restrict__ Q, const double* __restrict__ rz, const double* __restrict__ pq,
+                             int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (!active[b]) return;
   const double d = pq[b];
-  alpha[b] = d != 0.0 ? rz[b] / d : 0.0;
+  const double alpha = d != 0.0 ? rz[b] / d : 0.0;
+  U[i] = U[i] + alpha * P[i];
+  Rv[i] = Rv[i] + (-alpha) * Q[i];
 }
-__global__ void k_pcg_beta(const double* __restrict__ rz_new, double* __restrict__ rz, double* __restrict__ beta,
-                           const int32_t* __restrict__ active, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !active[b]) return;
-  beta[b] = rz[b] != 0.0 ? rz_new[b] / rz[b] : 0.0;
-  rz[b] = rz_new[b];
+__global__ void k_pcg_dir(double* __restrict__ P, const double* __restrict__ Z, const double* __restrict__ rz_new,
+                          const double* __restrict__ rz, int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (!active[b]) return;
+  const double beta = rz[b] != 0.0 ? rz_new[b] / rz[b] : 0.0;
+  P[i] = Z[i] + beta * P[i];
 }
+// Adjoint convergence; one block (loop over sims), the active count written to *nactive (no memset).  With
+// rz: rz[b] = rz_new[b] for the sims that ran the previous PCG iteration.
 __global__ void k_adj_check(const double* __restrict__ rr, const double* __restrict__ bb, int B, double tol, int iter,
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
-                            double* __restrict__ res_out, int32_t* __restrict__ flag_out, int32_t* __restrict__ nactive) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B || !active[b]) return;
-  const double res = bb[b] > 0 ? sqrt(rr[b] / bb[b]) : 0.0;
-  res_out[b] = res;
-  iters_out[b] = iter;
-  const bool go = res > tol && iter < max_iter;
-  if (!go) {
-    active[b] = 0;
-    flag_out[b] = res > tol ? 1 : 0;
-  } else {
-    atomicAdd(nactive, 1);
+                            double* __restrict__ res_out, int32_t* __restrict__ flag_out, int32_t* __restrict__ nactive,
+                            double* __restrict__ rz = nullptr, const double* __restrict__ rz_new = nullptr) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (!active[b]) continue;
+    if (rz) rz[b] = rz_new[b];
+    const double res = bb[b] > 0 ? sqrt(rr[b] / bb[b]) : 0.0;
+    res_out[b] = res;
+    iters_out[b] = iter;
+    const bool go = res > tol && iter < max_iter;
+    if (!go) {
+      active[b] = 0;
+      flag_out[b] = res > tol ? 1 : 0;
+    } else {
+      atomicAdd(&cnt, 1);
+    }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) *nactive = cnt;
 }
 
 // a_x = (M/h^2) u - a_v/h ; a_v = (M/h) u ; zero on fixed nodes  (eq:pre_adjoint)

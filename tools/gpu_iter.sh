@@ -1,0 +1,5 @@
+# GPU iteration: full GPU tests, timelines, quick devrun timings
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+timeout 300 python tools/timeline.py c3 --horizon 2 > gpurun_out/tl_c3.txt 2>&1; head -24 gpurun_out/tl_c3.txt
+timeout 300 python tools/timeline.py c5 --horizon 1 > gpurun_out/tl_c5.txt 2>&1; head -24 gpurun_out/tl_c5.txt
