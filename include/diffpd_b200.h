@@ -189,12 +189,6 @@ pd_status pd_profile(const pd_sim* sim, double* ms, int64_t* count, int32_t n);
  * (candidate order = opts.contact_nodes).  PD_ERR_STATE without a forward or without contact. */
 pd_status pd_contact_sets(const pd_sim* sim, uint8_t* out);
 
-/* Developer timeline of the last triangular solve (K3), recorded only when the environment variable
- * PD_K3_TRACE is set at pd_create: for every work item (forward sweep items, then backward) eight int64
- * values [start ns, inputs-final ns, data-done ns, end ns, SM id, warp id, outputs-written ns,
- * first-countdown ns] into HOST `out` (capacity n values).  *count = values available.  PD_ERR_STATE when tracing is off. */
-pd_status pd_debug_k3_trace(const pd_sim* sim, int64_t* out, int64_t n, int64_t* count);
-
 const char* pd_last_error(const pd_sim* sim);
 void pd_destroy(pd_sim* sim);
 

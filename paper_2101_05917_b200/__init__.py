@@ -164,15 +164,6 @@ class Simulator:
         self._check(self.lib.pd_contact_sets(self.handle, out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out.astype(bool)
 
-    def k3_trace(self):
-        """Per-item K3 timeline of the last solve (needs PD_K3_TRACE set at creation): int64 [items, 8]."""
-        cnt = C.c_int64()
-        self._check(self.lib.pd_debug_k3_trace(self.handle, None, 0, C.byref(cnt)))
-        out = np.zeros(cnt.value, np.int64)
-        self._check(self.lib.pd_debug_k3_trace(self.handle, out.ctypes.data_as(C.POINTER(C.c_int64)), cnt.value,
-                                               C.byref(cnt)))
-        return out.reshape(-1, 8)
-
     def eval_objective(self, x, y, youngs=None, act=None, grad=None, g=None):
         self._check(self.lib.pd_eval_objective(self.handle, x.shape[0], _ptr(x), _ptr(y), _ptr(youngs), _ptr(act),
                                                _ptr(grad), _ptr(g), _stream()))

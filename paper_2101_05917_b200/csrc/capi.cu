@@ -49,13 +49,7 @@ struct pd_sim {
   uint8_t* d_fixed = nullptr;
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
-  int32_t *cnt_f = nullptr, *cnt_b = nullptr;  // K3 group countdown counters
-  int32_t* grab = nullptr;                      // K3 item counters (one per sweep launch and column chunk)
-  int32_t* turn = nullptr;                      // K3 per z-tile turn counters (forward)
-  int64_t* trace = nullptr;                     // K3 per-item timeline (debug hook, pd_debug_trace)
-  int k3_levels = 1;                            // K3 launch per level (1) or one dataflow launch per sweep (0)
-  int k3_mma = 1;                               // per-level K3 products on the fp64 tensor cores (1) or FMA pipe (0)
-  int32_t *cd_f = nullptr, *cd_b = nullptr, *cd_f0 = nullptr, *cd_b0 = nullptr;  // supernode countdowns
+  int k3_mma = 1;  // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
@@ -225,25 +219,11 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
   const int R = 3 * B;
   const unsigned gy = (unsigned)((R + RC - 1) / RC);
   if (gy > (unsigned)kGY) throw CudaError("batch too large for the solve's column chunking");
-  CK(cudaFuncSetAttribute(k_sweep_flow<RC, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem_bytes<RC>()));
   int nsm = 0, dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  // shared memory of a launch = its largest item (and >= the 4 x 32 x RC warp-tile buffer); residency by size
-  auto smem_of = [&](int kmax) { return std::max(kmax * (32 + RC), 4 * 32 * RC) * 8; };
-  auto kpad_of = [&](int kmax) {  // buffer >= the 4 padded warp tiles
-    return std::max(kmax, (4 * 32 * tile_ld<RC>() + 32 + RC - 1) / (32 + RC));
-  };
-  auto resident_of = [&](int bytes) {
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_flow<RC, VEC>, 128, bytes));
-    return std::max(1, per_sm) * (int64_t)nsm;
-  };
-  // dataflow counters: item counters zeroed, supernode countdowns re-armed, at the start of every solve
-  CK(cudaMemsetAsync(s->grab, 0, sizeof(int32_t) * 4 * kGY * (P.nlevels + 1), s->stream));
-  CK(cudaMemsetAsync(s->turn, 0, sizeof(int32_t) * (size_t)std::max(1, P.fw.ntiles) * kGY, s->stream));
-  CK(cudaMemcpyAsync(s->cd_f, s->cd_f0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
-  CK(cudaMemcpyAsync(s->cd_b, s->cd_b0, sizeof(int32_t) * (size_t)P.nsup * kGY, cudaMemcpyDeviceToDevice, s->stream));
+  // each item buffer also holds the 4 padded warp tiles of a chain's epilogue
+  auto kpad_of = [&](int kmax) { return std::max(kmax, (4 * 32 * tile_ld<RC>() + 32 + RC - 1) / (32 + RC)); };
   // programmatic dependent launch (PDL): a kernel's CTAs may be scheduled while its predecessor drains;
   // they block in griddepcontrol.wait until the predecessor's writes are visible
   cudaLaunchAttribute pdl[1];
@@ -266,71 +246,39 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_fn, 128, bytes));
     return std::max(1, per_sm) * (int64_t)nsm;
   };
-  auto launch = [&](const SweepDev& d, int t0, int nt, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab, int kmax) {
-    if (!nt) return;
-    if (s->k3_levels) {  // per-level mode: double-buffered items, static assignment
-      const int kp = kpad_of(kmax);  // each buffer also holds the 4 warp tiles
-      const int bufb = kp * (32 + RC) * 8;
-      // ring depth: as many item buffers as fit (<= 4); small-item levels also get several CTAs per SM
+  // forward: sources z (S0), direct y (S2), reduce: y (S2) / z -= (S0);
+  // backward: D part y (S2), W part x (S0), direct x (S0)
+  auto level = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int j) {
+    const int ch0 = S.lvl_chain[j], nch = S.lvl_chain[j + 1] - ch0;
+    if (nch > 0) {
+      const int kp = kpad_of(S.lvl_kmax[j]);
       const int nbuf = 2;  // measured: 2 buffers x several CTAs/SM beats deeper rings with 1 CTA/SM
-      const int smem = nbuf * bufb;
-      const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_lvl(smem) / gy));
+      const int smem = nbuf * kp * (32 + RC) * 8;
+      const unsigned gx = (unsigned)std::min<int64_t>(nch, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
-      CK(cudaLaunchKernelEx(&c, level_fn, d, t0, nt, R, (const double*)(fwd ? s->S0 : s->S2),
-                            (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf));
+      CK(cudaLaunchKernelEx(&c, level_fn, d, ch0, nch, R, (const double*)(fwd ? s->S0 : s->S2), (const double*)s->S0,
+                            (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->Spart, kp, nbuf));
       LAUNCH_CHECK(s);
-      return;
     }
-    // forward: sources z (S0), direct y (S2), group subtract into z (S0);
-    // backward: D part y (S2), W part x (S0), direct x (S0)
-    const int smem = smem_of(kmax);
-    const unsigned gx = (unsigned)std::min<int64_t>(nt, std::max<int64_t>(1, resident_of(smem) / gy));
-    cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
-    CK(cudaLaunchKernelEx(&c, k_sweep_flow<RC, VEC>, d, t0, nt, R, fwd ? 1 : 0, (const double*)(fwd ? s->S0 : s->S2),
-                          (const double*)s->S0, (const int32_t*)s->d_rows, fwd ? s->S2 : s->S0, s->S0, s->Spart, gcnt,
-                          cd, grab, s->turn,
-                          s->trace ? s->trace + (fwd ? 0 : (int64_t)8 * P.fw.a_off.size()) + (int64_t)8 * t0 : (int64_t*)nullptr,
-                          s->k3_levels ? 0 : 1, kmax));
-    LAUNCH_CHECK(s);
-  };
-  auto reduce = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int j) {
-    const int r0 = S.g_tptr[S.lvl_grp[j]], nr = S.g_tptr[S.lvl_grp[j + 1]] - r0;
-    if (!nr) return;
-    cudaLaunchConfig_t c = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
-    CK(cudaLaunchKernelEx(&c, k_sweep_reduce, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
-    LAUNCH_CHECK(s);
-  };
-  const HostPlan::Sweep& F = P.fw;
-  const HostPlan::Sweep& Bk = P.bw;
-  // Launch granularity: one launch per tree level (s->k3_levels = 1, default; kernel boundaries order the
-  // levels, every wait inside is already satisfied) or one dataflow launch per sweep.
-  auto sweep = [&](const HostPlan::Sweep& S, const SweepDev& d, bool fwd, int32_t* gcnt, int32_t* cd, int32_t* grab,
-                   int j0, int j1) {
-    if (s->k3_levels) {
-      for (int j = j0; j < j1; ++j) {
-        launch(d, S.lvl_item[j], S.lvl_item[j + 1] - S.lvl_item[j], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j * 4 * kGY,
-               S.lvl_kmax[j]);
-        reduce(S, d, fwd, j);
-      }
-    } else {
-      int km = 0;
-      for (int j = j0; j < j1; ++j) km = std::max(km, S.lvl_kmax[j]);
-      launch(d, S.lvl_item[j0], S.lvl_item[j1] - S.lvl_item[j0], fwd, gcnt, cd, grab + (fwd ? 0 : 2) * kGY + j0 * 4 * kGY,
-             km);
+    const int r0 = S.lvl_red[j], nr = S.lvl_red[j + 1] - r0;
+    if (nr > 0) {
+      cudaLaunchConfig_t c = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
+      CK(cudaLaunchKernelEx(&c, k_sweep_reduce, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
+      LAUNCH_CHECK(s);
     }
   };
-  sweep(F, s->swf, true, s->cnt_f, s->cd_f, s->grab, 0, P.nlevels);
+  for (int j = 0; j < P.nlevels; ++j) level(P.fw, s->swf, true, j);
   if (s->pins_live) {
     // the root (= candidate block) first, then its constrained fixup, then every other level
     double* root = s->S0 + (int64_t)s->csup_first * R;
     CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
-    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 0, 1);
+    level(P.bw, s->swb, false, 0);
     k_contact_fix<<<dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, s->stream>>>(
         s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos, s->Qc, root);
     LAUNCH_CHECK(s);
-    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 1, P.nlevels);
+    for (int j = 1; j < P.nlevels; ++j) level(P.bw, s->swb, false, j);
   } else {
-    sweep(Bk, s->swb, false, s->cnt_b, s->cd_b, s->grab, 0, P.nlevels);
+    for (int j = 0; j < P.nlevels; ++j) level(P.bw, s->swb, false, j);
   }
 }
 void solve_launch(pd_sim* s, int B) {
@@ -453,8 +401,8 @@ void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double
   const int nchunk = (int)((n3 + chunk - 1) / chunk);
   const int bd = B * std::max(1, 256 / B);
   const int np = u2 ? 2 * nv : nv;
-  k_mdot_partial<<<nchunk, bd, np * bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk, s->partial,
-                                                                      u2, V2base);
+  k_mdot_partial<<<dim3(nchunk, np), bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk,
+                                                                           s->partial, u2, V2base);
   LAUNCH_CHECK(s);
   k_dot_final<<<nblk((int64_t)(np * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, np, out);
   LAUNCH_CHECK(s);
@@ -693,46 +641,13 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.zrow = s->upload(S.zrow);
       d.out = s->upload(S.out);
       d.nvalid = s->upload(S.nvalid);
-      d.ig_ptr = s->upload(S.ig_ptr);
-      d.ig = s->upload(S.ig);
-      d.g_tptr = s->upload(S.g_tptr);
-      d.g_cnt = s->upload(S.g_cnt);
+      d.chain = s->upload(S.chain);
       d.red_row = s->upload(S.red_row);
       d.red_mode = s->upload(S.red_mode);
       d.red_ptr = s->upload(S.red_ptr);
       d.red_src = s->upload(S.red_src);
-      d.sup = s->upload(S.sup);
-      d.sig = s->upload(S.sig);
-      d.g_sig = s->upload(S.g_sig);
-      d.wl_ptr = s->upload(S.wl_ptr);
-      d.wl = s->upload(S.wl);
-      d.g_tile = s->upload(S.g_tile);
-      d.g_turn = s->upload(S.g_turn);
     };
-    // group countdown counters, one slot per column chunk, armed with the group's item count
-    auto up_cnt = [&](const HostPlan::Sweep& S) {
-      std::vector<int32_t> c(S.g_cnt.size() * kGY);
-      for (size_t g = 0; g < S.g_cnt.size(); ++g)
-        for (int y = 0; y < kGY; ++y) c[g * kGY + y] = S.g_cnt[g];
-      return s->upload(c);
-    };
-    s->grab = s->alloc<int32_t>(4 * kGY * (P.nlevels + 1));
-    s->k3_levels = std::getenv("PD_K3_DATAFLOW") ? 0 : 1;
     if (const char* e = std::getenv("PD_K3_MMA")) s->k3_mma = std::atoi(e) ? 1 : 0;
-    s->turn = s->alloc<int32_t>((int64_t)std::max(1, P.fw.ntiles) * kGY);
-    if (std::getenv("PD_K3_TRACE")) s->trace = s->alloc<int64_t>(8 * (int64_t)(P.fw.a_off.size() + P.bw.a_off.size()));
-    auto up_cd = [&](const HostPlan::Sweep& S) {
-      std::vector<int32_t> c((size_t)P.nsup * kGY);
-      for (int u = 0; u < P.nsup; ++u)
-        for (int y = 0; y < kGY; ++y) c[(size_t)u * kGY + y] = S.cd_init[u];
-      return s->upload(c);
-    };
-    s->cd_f0 = up_cd(P.fw);
-    s->cd_b0 = up_cd(P.bw);
-    s->cd_f = s->alloc<int32_t>((int64_t)P.nsup * kGY);
-    s->cd_b = s->alloc<int32_t>((int64_t)P.nsup * kGY);
-    s->cnt_f = up_cnt(P.fw);
-    s->cnt_b = up_cnt(P.bw);
     up_sweep(P.fw, s->swf);
     up_sweep(P.bw, s->swb);
     s->Spart = s->alloc<double>((std::max(P.fw.max_partial_rows, P.bw.max_partial_rows) + 32) * 3 * s->Bmax);
@@ -828,16 +743,6 @@ pd_status pd_profile(const pd_sim* s, double* ms, int64_t* count, int32_t n) {
     if (ms) ms[k] = s->prof_ms[k];
     if (count) count[k] = s->prof_cnt[k];
   }
-  return PD_OK;
-}
-
-pd_status pd_debug_k3_trace(const pd_sim* s, int64_t* out, int64_t n, int64_t* count) {
-  if (!s || !count) return PD_ERR_INVALID_ARGUMENT;
-  if (!s->trace) return PD_ERR_STATE;
-  const int64_t tot = 8 * (int64_t)(s->plan.fw.a_off.size() + s->plan.bw.a_off.size());
-  *count = tot;
-  if (out && n > 0 && cudaMemcpy(out, s->trace, sizeof(int64_t) * std::min(n, tot), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return PD_ERR_CUDA;
   return PD_OK;
 }
 

@@ -260,15 +260,30 @@ __device__ __forceinline__ double dNf(const Stencil& st, int q, int a, int j) {
   return ((a >> j) & 1) ? mag : -mag;
 }
 
+// Per-block tables of dN_a/dX_j (from dNf, so bit-identical): f[(a*3 + j)*8 + q] (load_F: lanes = q, one
+// 64-byte row per (a, j)) and b[(q*3 + j)*8 + a] (store_force: lanes = a).  One shared-memory load replaces
+// dNf's integer work per use.
+struct DNTab {
+  double f[192], b[192];
+};
+__device__ __forceinline__ void dn_fill(DNTab& t, const Stencil& st) {
+  for (int i = threadIdx.x; i < 192; i += blockDim.x) {
+    const int x = i / 24, j = (i / 8) % 3, y = i % 8;
+    t.f[i] = dNf(st, y, x, j);
+    t.b[i] = dNf(st, x, y, j);
+  }
+  __syncthreads();
+}
+
 // Deformation gradient F = G_q x_e at quad point q of element e, sim b (state layout [n][3][B]).
 __device__ __forceinline__ void load_F(const double* __restrict__ X, const int32_t* __restrict__ hex8,
-                                       const Stencil& st, int e, int b, int q, int B, double* F) {
+                                       const DNTab& dt, int e, int b, int q, int B, double* F) {
 #pragma unroll
   for (int k = 0; k < 9; ++k) F[k] = 0.0;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int node = __ldg(hex8 + 8 * (int64_t)e + a);
-    const double d0 = dNf(st, q, a, 0), d1 = dNf(st, q, a, 1), d2 = dNf(st, q, a, 2);
+    const double d0 = dt.f[(a * 3) * 8 + q], d1 = dt.f[(a * 3 + 1) * 8 + q], d2 = dt.f[(a * 3 + 2) * 8 + q];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const double xv = __ldg(X + (3 * (int64_t)node + i) * B + b);
@@ -281,21 +296,25 @@ __device__ __forceinline__ void load_F(const double* __restrict__ X, const int32
 
 // Element force sum_q G_q^T P_q of the (e, b) group (8 consecutive lanes, lane q holds P_q): the 8 P_q
 // go through shared memory (group-private, padded rows), then lane a forms the 3 components of corner
-// a in a fixed q order: EF[e][a][i][b].  Ps = this group's 73-double slot.
-__device__ __forceinline__ void store_force(const double* Pm, const Stencil& st, int e, int b, int q, int B,
+// a in a fixed q order: EF[e][a][i][b].  Ps = this group's kPsSlot-double slot: P_q at 10 q (16-byte
+// aligned, read back with 128-bit loads); slots 82 doubles apart so the 4 groups of a warp hit distinct banks.
+constexpr int kPsSlot = 82;
+__device__ __forceinline__ void store_force(const double* Pm, const DNTab& dt, int e, int b, int q, int B,
                                             double* Ps, double* __restrict__ EF) {
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Ps[9 * q + k] = Pm[k];
+  for (int k = 0; k < 9; ++k) Ps[10 * q + k] = Pm[k];
   __syncwarp();
   const int a = q;
   double o0 = 0, o1 = 0, o2 = 0;
 #pragma unroll
   for (int qq = 0; qq < 8; ++qq) {
-    const double d0 = dNf(st, qq, a, 0), d1 = dNf(st, qq, a, 1), d2 = dNf(st, qq, a, 2);
-    const double* P = Ps + 9 * qq;
-    o0 = fma(P[0], d0, fma(P[1], d1, fma(P[2], d2, o0)));
-    o1 = fma(P[3], d0, fma(P[4], d1, fma(P[5], d2, o1)));
-    o2 = fma(P[6], d0, fma(P[7], d1, fma(P[8], d2, o2)));
+    const double d0 = dt.b[(qq * 3) * 8 + a], d1 = dt.b[(qq * 3 + 1) * 8 + a], d2 = dt.b[(qq * 3 + 2) * 8 + a];
+    const double2* P2 = reinterpret_cast<const double2*>(Ps + 10 * qq);
+    const double2 p01 = P2[0], p23 = P2[1], p45 = P2[2], p67 = P2[3];
+    const double p8 = Ps[10 * qq + 8];
+    o0 = fma(p01.x, d0, fma(p01.y, d1, fma(p23.x, d2, o0)));
+    o1 = fma(p23.y, d0, fma(p45.x, d1, fma(p45.y, d2, o1)));
+    o2 = fma(p67.x, d0, fma(p67.y, d1, fma(p8, d2, o2)));
   }
   __syncwarp();
   if (EF) {
@@ -308,6 +327,8 @@ __device__ __forceinline__ void store_force(const double* Pm, const Stencil& st,
 
 __global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                        double* __restrict__ EF, double* __restrict__ EE) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
   const int64_t pair = tid >> 3;
@@ -318,7 +339,7 @@ __global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict_
   const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   const double w = ea.w_sim[b];
   double F[9];
-  load_F(X, ea.hex8, st, e, b, q, B, F);
+  load_F(X, ea.hex8, dnt, e, b, q, B, F);
   double R[9];
   polar_rotation(F, R);
   double Pm[9];
@@ -352,8 +373,8 @@ __global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict_
 #pragma unroll
       for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
   }
-  __shared__ double Psm[32][73];
-  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
+  __shared__ __align__(16) double Psm[32][kPsSlot];
+  store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
   energy = qsum8(energy);
   if (live && EE && q == 0) EE[(int64_t)e * B + b] = energy;
 }
@@ -507,6 +528,8 @@ constexpr int kJC = 19;  // cached doubles per quad point: R (9), Mi (6), n (3),
 // JC[k * nq + tid], tid = (e*B + b)*8 + q.
 __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                   double* __restrict__ JC) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nq = (int64_t)ea.m * ea.B * 8;
   if (tid >= nq) return;
@@ -515,7 +538,7 @@ __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, 
   const int q = (int)(tid & 7);
   const int e = (int)(pair / B), b = (int)(pair - (int64_t)e * B);
   double F[9], R[9], S[9], Mi[6];
-  load_F(X, ea.hex8, st, e, b, q, B, F);
+  load_F(X, ea.hex8, dnt, e, b, q, B, F);
   polar_rotation(F, R);
   sym_stretch(R, F, S);
   rot_derivative_matrix(S, st.clamp, Mi);
@@ -535,6 +558,8 @@ __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, 
 // K4 with cached Jacobian data: A_N p element term from dF = G_q p_e only (no polar per product).
 __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict__ Pv, Stencil st, ElemArgs ea,
                                                         const double* __restrict__ JC, double* __restrict__ EF) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
   const int64_t nq = (int64_t)ea.m * B * 8;
@@ -545,7 +570,7 @@ __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict
   const int64_t t = live ? tid : q;
   const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   double dF[9], R[9], Mi[6], nh[3] = {0, 0, 0}, sc = 0;
-  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
+  load_F(Pv, ea.hex8, dnt, e, b, q, B, dF);
 #pragma unroll
   for (int k = 0; k < 9; ++k) R[k] = __ldg(JC + k * nq + t);
 #pragma unroll
@@ -558,12 +583,14 @@ __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict
   }
   double Pm[9];
   an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
-  __shared__ double Psm[32][73];
-  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
+  __shared__ __align__(16) double Psm[32][kPsSlot];
+  store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
 
 __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
                                                  Stencil st, ElemArgs ea, double* __restrict__ EF) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
   const int64_t pair = tid >> 3;
@@ -572,8 +599,8 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
   const int64_t pr = live ? pair : 0;
   const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   double F[9], dF[9], R[9], S[9], Mi[6], nh[3] = {0, 0, 0}, sc = 0;
-  load_F(X, ea.hex8, st, e, b, q, B, F);
-  load_F(Pv, ea.hex8, st, e, b, q, B, dF);
+  load_F(X, ea.hex8, dnt, e, b, q, B, F);
+  load_F(Pv, ea.hex8, dnt, e, b, q, B, dF);
   polar_rotation(F, R);
   sym_stretch(R, F, S);
   rot_derivative_matrix(S, st.clamp, Mi);
@@ -581,8 +608,8 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
   if (mus) muscle_dir(F, st, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
   double Pm[9];
   an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
-  __shared__ double Psm[32][73];
-  store_force(Pm, st, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
+  __shared__ __align__(16) double Psm[32][kPsSlot];
+  store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
 
 // Parameter-gradient terms at x_{i+1} for adjoint u (chain rule):
@@ -590,6 +617,8 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
 __global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X, const double* __restrict__ U,
                                                     Stencil st, ElemArgs ea, double* __restrict__ DW,
                                                     double* __restrict__ DR) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
   const int64_t pair = tid >> 3;
@@ -598,8 +627,8 @@ __global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X
   const int64_t pr = live ? pair : 0;
   const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
   double F[9], dF[9];
-  load_F(X, ea.hex8, st, e, b, q, B, F);
-  load_F(U, ea.hex8, st, e, b, q, B, dF);
+  load_F(X, ea.hex8, dnt, e, b, q, B, F);
+  load_F(U, ea.hex8, dnt, e, b, q, B, dF);
   double R[9];
   polar_rotation(F, R);
   double acc = 0;
@@ -694,16 +723,14 @@ __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __rest
   OUT[i] = pos >= 0 ? base + a * S[(int64_t)pos * 3 * B + ax * B + b] : base;
 }
 
-// ----------------------------------------------------------------- K3: supernodal solves (v3)
-// One kernel pair per ND-tree level and sweep.  Work item = one CTA of 4 warps: lane
-// = output row (forward) or output column (backward) of a 32-wide chunk of one supernode; the item's
-// <= 256 k-steps are split into 4 warp ranges.  Each warp stages its factor block (k-major, 32
-// doubles per k, contiguous in the sweep's stream) and its right-hand-side rows (RC columns of the
-// [pos][R] solve layout) into shared memory with cp.async — everything in flight at once — then
-// accumulates RC columns per lane with broadcast shared loads; the 4 warp sums are added in warp
-// order.  Single-item chunks write their output rows directly; split chunks and every forward W
-// item write partial rows that the group's last item adds in a fixed order into y / x (assign) or into z of
-// ancestors (subtract): deterministic, no atomics.
+// ----------------------------------------------------------------- K3: supernodal solves
+// One launch per ND-tree level and sweep + one reduce launch.  Work item = <= 128 k-steps
+// of one 32-lane output (lane = output row forward, output column backward), stored in the stream in MMA
+// fragment order; a chain = consecutive items of one output, accumulated in registers by one CTA of 4
+// warps (the warps split each item's k-steps; their tiles are added in warp order at the chain's end).
+// Each item is ONE TMA round (cp.async.bulk of the factor block + its right-hand-side rows, mbarrier
+// transaction count).  Chains covering a whole output write it directly; the others write partial rows
+// summed by the level's k_sweep_reduce in a fixed order: deterministic, no float atomics.
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -753,261 +780,11 @@ constexpr int kItemK = 128;  // max k-steps per item (the planner's kc)
 // an odd number of 16-byte units (conflict-free 16-byte fragment stores)
 template <int RC>
 __host__ __device__ constexpr int tile_ld() { return ((RC + 1) / 2 % 2 == 1) ? ((RC + 1) / 2) * 2 : ((RC + 1) / 2 + 1) * 2; }
-template <int RC>
-__host__ __device__ constexpr int sweep_item_doubles() { return kItemK * (32 + RC); }
-template <int RC>
-__host__ __device__ constexpr int sweep_smem_bytes() { return sweep_item_doubles<RC>() * 8; }  // >= 4 x 32 x RC
 
-// K3 v5: ONE launch per sweep (dataflow).  Items are taken in the planned order (levels in sweep order)
-// through one integer counter; before reading its right-hand-side rows an item waits until they are
-// final: forward, the countdown of its supernode (W groups of descendants that still have to subtract
-// into z[J_s]); backward, the countdowns of the supernodes owning R_s (their 32-column chunks of x).
-// Waits only ever point at earlier items, which are held by running warps, so the schedule cannot
-// deadlock.  Within an item the warp streams its k-range through a kPS-stage cp.async ring (kKS k-steps
-// per stage: 32 factor doubles + RC right-hand-side doubles per k); lane (rg, cg) = (lane % 8, lane / 8)
-// keeps a 4-row x RC/4-column register tile.  Output: direct rows, or partial rows + countdown of each
-// reduction group fed; the warp that brings a group to zero sums its partial rows in the planned order
-// (lane = target row), re-arms the group counter and decrements the group's supernode countdown.  All
-// atomics are integer; every floating-point sum has a fixed order -> bitwise reproducible.
-constexpr int kGY = 16;  // max column chunks (gridDim.y) -> counter slots per group / supernode
+constexpr int kGY = 16;  // max column chunks (gridDim.y)
 
-__device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void red_add_release(int32_t* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int RC, bool VEC>
-__global__ void __launch_bounds__(128, 4) k_sweep_flow(SweepDev sw, int t0, int nitems, int R, int fwd,
-                                                    const double* __restrict__ zc, const double* __restrict__ zi,
-                                                    const int32_t* __restrict__ rows, double* __restrict__ direct,
-                                                    double* __restrict__ zsub, double* __restrict__ partial,
-                                                    int32_t* __restrict__ gcnt, int32_t* __restrict__ cd,
-                                                    int32_t* __restrict__ grab, int32_t* __restrict__ turn,
-                                                    int64_t* __restrict__ trace, int groups_inline, int kmax) {
-  constexpr int CW = RC / 4;
-  extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int rg = lane & 7, cg = lane >> 3;
-  const int y = blockIdx.y;
-  const int c0 = y * RC;
-  const int rcn = min(RC, R - c0);
-  // programmatic dependent launch: everything below may read what the previous kernel wrote
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  double* As = sm;                  // [kmax][32]   factor block (kmax = the level's largest item)
-  double* Zs = sm + kmax * 32;      // [kmax][RC]   right-hand-side rows
-  __shared__ __align__(8) uint64_t mb[1];
-  __shared__ int s_next, s_flag;
-  if (tid == 0) {
-    mbar_init(mb, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    s_next = atomicAdd(grab + y, 1);
-  }
-  __syncthreads();
-  unsigned phase = 0;
-  auto gtime = []() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return (int64_t)t;
-  };
-  int next = s_next;
-  while (next < nitems) {
-    const int it = t0 + next;
-    int64_t* tr = (trace && y == 0) ? trace + (int64_t)next * 8 : nullptr;  // [start, deps, data, end, smid, cta, written, counted]
-    if (tr && tid == 0) tr[0] = gtime();
-    const int nk = sw.nk[it], nkd = sw.nkd[it], nkp = (nk + 3) & ~3;
-    if (tid == 0) {
-      s_next = atomicAdd(grab + y, 1);  // prefetch the next index (never waited on before this item is done)
-      // wait until the item's right-hand-side rows are final (bounded: a schedule bug traps, never hangs)
-      const int su = sw.sup[it];
-      int64_t spins = 0;
-      auto wait0 = [&](const int32_t* c) {
-        while (ld_acquire(c) != 0) {
-          __nanosleep(64);
-          if (++spins > (int64_t)1 << 26) __trap();
-        }
-      };
-      if (!groups_inline) {
-        // per-level launches: kernel boundaries already order the levels
-      } else if (fwd) {
-        wait0(cd + (int64_t)su * kGY + y);
-      } else if (nkd < nk) {
-        for (int q = sw.wl_ptr[su]; q < sw.wl_ptr[su + 1]; ++q) wait0(cd + (int64_t)sw.wl[q] * kGY + y);
-      }
-    }
-    __syncthreads();
-    if (tr && tid == 0) tr[1] = gtime();
-    // acquired rows were written through the generic proxy; the TMA reads below use the async proxy
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    fence_proxy_async();  // generic reads of the previous item's buffer before the async-proxy refill
-    const double* Ag = sw.A + sw.a_off[it];
-    const int zr = sw.zrow[it];
-    const int32_t* idx = rows + sw.zidx[it] - nkd;
-    // ---- the whole item (<= kItemK k-steps: factor block + right-hand-side rows) in one TMA round
-    if (VEC) {
-      const bool whole = rcn == RC && RC == R && nkd == nk;  // contiguous rows, all columns: one copy
-      if (tid == 0) {
-        mbar_arrive_expect_tx(mb, (unsigned)(nkp * 256 + nk * rcn * 8));
-        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb);
-        if (whole) bulk_g2s(Zs, zc + (int64_t)zr * R, (unsigned)(nk * R * 8), mb);
-      }
-      if (!whole)
-        for (int kk = tid; kk < nk; kk += 128) {
-          const bool ct = kk < nkd;
-          const int row = ct ? zr + kk : __ldg(idx + kk);
-          bulk_g2s(Zs + kk * RC, (ct ? zc : zi) + (int64_t)row * R + c0, (unsigned)(rcn * 8), mb);
-        }
-    } else {
-      if (tid == 0) {
-        mbar_arrive_expect_tx(mb, (unsigned)(nkp * 256));
-        bulk_g2s(As, Ag, (unsigned)(nkp * 256), mb);
-      }
-      for (int i = tid; i < nk * RC; i += 128) {
-        const int k = i / RC, c = i - k * RC;
-        const bool ct = k < nkd;
-        const int row = ct ? zr + k : __ldg(idx + k);
-        if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
-        else Zs[k * RC + c] = 0.0;
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-    }
-    mbar_wait(mb, phase);
-    phase ^= 1;
-    __syncthreads();
-    if (tr && tid == 0) tr[2] = gtime();
-    // ---- 4 warps split the k-steps; lane (rg, cg) keeps a 4-row x RC/4-column register tile
-    double acc[4][CW];
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
-    const int per = (nk + 3) >> 2;
-    const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
-#pragma unroll 2
-    for (int k = k0; k < k1; ++k) {
-      // fragment layout (plan.h sweep_frag_pos): rows 4rg..4rg+3 of step k are two double2
-      const double2 a01 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2) * 32 + 4 * rg + (k & 3)) * 2);
-      const double2 a23 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2 + 1) * 32 + 4 * rg + (k & 3)) * 2);
-      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-      double zv[CW];
-      if (CW % 2 == 0) {
-#pragma unroll
-        for (int c = 0; c < CW / 2; ++c) {
-          const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
-          zv[2 * c] = t.x;
-          zv[2 * c + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
-    }
-    __syncthreads();  // everyone is done with As/Zs: reuse the buffer for the 4 warp tiles
-    double* red = sm + w * 32 * RC;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < CW; ++c) red[(4 * rg + r) * RC + cg * CW + c] = acc[r][c];
-    __syncthreads();
-    // ---- output rows: fixed-order sum of the 4 warp tiles, coalesced over columns
-    const int out = sw.out[it];
-    const int nv = sw.nvalid[it];
-    double* __restrict__ dst =
-        out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
-    for (int e = tid; e < nv * RC; e += 128) {
-      const int r = e / RC, c = e - r * RC;
-      if (c < rcn) dst[(int64_t)r * R + c] = ((sm[e] + sm[32 * RC + e]) + sm[64 * RC + e]) + sm[96 * RC + e];
-    }
-    __syncthreads();
-    if (tr && tid == 0) tr[6] = gtime();
-    if (out >= 0) {
-      if (tid == 0) {
-        if (sw.sig[it] >= 0) red_add_release(cd + (int64_t)sw.sig[it] * kGY + y, -1);
-        if (tr) tr[3] = tr[7] = gtime();
-      }
-    } else if (groups_inline) {
-      int64_t t_counted = 0;
-      for (int q = sw.ig_ptr[it]; q < sw.ig_ptr[it + 1]; ++q) {
-        const int g = sw.ig[q];
-        if (tid == 0) {
-          s_flag = atom_add_acq_rel(gcnt + (int64_t)g * kGY + y, -1) == 1;  // release ours, acquire the others'
-          if (tr && !t_counted) t_counted = gtime();
-          const int tile = sw.g_tile[g];
-          if (s_flag && tile >= 0) {  // z-row tiles apply their per-level groups in level order
-            int64_t spins = 0;
-            while (ld_acquire(turn + (int64_t)tile * kGY + y) != sw.g_turn[g]) {
-              __nanosleep(32);
-              if (++spins > (int64_t)1 << 26) __trap();
-            }
-          }
-        }
-        __syncthreads();
-        const bool last = s_flag != 0;
-        if (last) {
-          // thread (target t, column quarter cq): its RC/4 columns accumulate over the target's partial
-          // rows in the planned order
-          const int tb = sw.g_tptr[g], nt = sw.g_tptr[g + 1] - tb;
-          const int t = tid & 31, cq = tid >> 5;
-          if (t < nt) {
-            double v[CW];
-#pragma unroll
-            for (int c = 0; c < CW; ++c) v[c] = 0.0;
-            const int u0 = sw.red_ptr[tb + t], u1 = sw.red_ptr[tb + t + 1];
-#pragma unroll 4
-            for (int u = u0; u < u1; ++u) {
-              const double* pr = partial + (int64_t)sw.red_src[u] * R + c0 + cq * CW;
-#pragma unroll
-              for (int c = 0; c < CW; ++c)
-                if (cq * CW + c < rcn) v[c] += __ldcg(pr + c);
-            }
-            const bool assign = sw.red_mode[tb + t] == 0;
-            double* o = (assign ? direct : zsub) + (int64_t)sw.red_row[tb + t] * R + c0 + cq * CW;
-#pragma unroll
-            for (int c = 0; c < CW; ++c)
-              if (cq * CW + c < rcn) o[c] = assign ? v[c] : __ldcg(o + c) - v[c];
-          }
-          __syncthreads();
-          if (tid == 0) {
-            gcnt[(int64_t)g * kGY + y] = sw.g_cnt[g];  // re-arm for the next solve
-            if (sw.g_tile[g] >= 0) red_add_release(turn + (int64_t)sw.g_tile[g] * kGY + y, 1);
-            if (sw.g_sig[g] >= 0) red_add_release(cd + (int64_t)sw.g_sig[g] * kGY + y, -1);
-          }
-        }
-      }
-      if (tr && tid == 0) {
-        tr[3] = gtime();
-        tr[7] = t_counted ? t_counted : tr[3];
-      }
-    }
-    if (tr && tid == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      tr[4] = smid;
-      tr[5] = blockIdx.x;
-    }
-    __syncthreads();
-    next = s_next;
-    __syncthreads();
-  }
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-
-// Per-level mode (default): items of ONE level, no dependency waits (kernel boundaries order the levels).
-// CTA c takes items c, c + G, c + 2G, ... (G = gridDim.x) through a ring of nbuf item buffers: while item j
-// computes, the TMA rounds of items j+1 .. j+nbuf-1 are in flight.
+// CTA c takes the level's chains c, c + G, c + 2G, ... (G = gridDim.x) and walks their items through a ring
+// of nbuf item buffers: while item j computes, the TMA rounds of the next nbuf-1 items are in flight.
 //
 // MMA = true: the item product runs on the fp64 tensor cores (mma.sync m8n8k4, DMMA): warp w takes k-groups
 // of 4 steps; per group one conflict-free double2 pair of A fragments (the stream's fragment layout) and RC/8
@@ -1019,11 +796,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
       : "d"(a), "d"(b));
 }
 template <int RC, bool VEC, bool MMA>
-__global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int nitems, int R,
+__global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, int nchains, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                         double* __restrict__ partial, int kmax, int nbuf) {
   constexpr int CW = RC / 4;
+  constexpr int NT = (RC + 7) / 8;
+  constexpr int LD = tile_ld<RC>();
   extern __shared__ __align__(16) double sm[];
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -1031,6 +810,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int
   const int y = blockIdx.y;
   const int c0 = y * RC;
   const int rcn = min(RC, R - c0);
+  const int G = gridDim.x;
   const int bufd = kmax * (32 + RC);  // doubles per buffer
   __shared__ __align__(8) uint64_t mb[4];
   if (tid == 0) {
@@ -1038,8 +818,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  auto load = [&](int rel, int slot) {  // one TMA round for item t0 + rel into buffer `slot`
-    const int it = t0 + rel;
+  auto load = [&](int it, int slot) {  // one TMA round for item `it` into buffer `slot`
     double* As = sm + slot * bufd;
     double* Zs = As + kmax * 32;
     const int nk = sw.nk[it], nkd = sw.nkd[it], nkp = (nk + 3) & ~3;
@@ -1071,43 +850,55 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int
         if (c < rcn) cp_async8(Zs + k * RC + c, (ct ? zc : zi) + (int64_t)row * R + c0 + c);
         else Zs[k * RC + c] = 0.0;
       }
+      cp_async_commit();
     }
-    if (!VEC) cp_async_commit();
   };
-  const int G = gridDim.x;
-  // item ordinal j of this CTA: rel = blockIdx.x + j G, buffer j % nbuf, mbarrier parity (j / nbuf) & 1
-  for (int p = 0; p < nbuf - 1; ++p)
-    if (blockIdx.x + p * G < nitems) load(blockIdx.x + p * G, p);
-  for (int j = 0;; ++j) {
-    const int rel = blockIdx.x + j * G;
-    if (rel >= nitems) break;
+  // cursors over this CTA's item sequence: (chain, item); item -1 = exhausted
+  auto first_of = [&](int c) { return c < nchains ? sw.chain[ch0 + c] : -1; };
+  auto advance = [&](int& c, int& it) {
+    if (it + 1 < sw.chain[ch0 + c + 1]) {
+      ++it;
+    } else {
+      c += G;
+      it = first_of(c);
+    }
+  };
+  int lc = blockIdx.x, lit = first_of(lc);  // next item to load
+  for (int p = 0; p < nbuf - 1 && lit >= 0; ++p) {
+    load(lit, p);
+    advance(lc, lit);
+  }
+  // accumulators live across the items of a chain
+  double accm[2][4][NT][2];  // MMA: fragments (two sets: even / odd k-groups)
+  double accf[4][CW];        // FMA: 4 rows x CW columns
+  int cc = blockIdx.x, cit = first_of(cc);
+  for (int j = 0; cit >= 0; ++j) {
     const int slot = j % nbuf;
-    const int it = t0 + rel;
-    const int nk = sw.nk[it];
+    const int nk = sw.nk[cit];
+    const bool first = cit == sw.chain[ch0 + cc];
+    const bool last = cit + 1 == sw.chain[ch0 + cc + 1];
     if (!VEC) cp_async_wait_all();
     mbar_wait(mb + slot, (j / nbuf) & 1);
     __syncthreads();  // item j visible to all; the buffer refilled next was released at the end of item j-1
-    const int pre = blockIdx.x + (j + nbuf - 1) * G;
-    if (pre < nitems) {
+    if (lit >= 0) {
       fence_proxy_async();
-      load(pre, (j + nbuf - 1) % nbuf);
+      load(lit, (j + nbuf - 1) % nbuf);
+      advance(lc, lit);
     }
     const double* As = sm + slot * bufd;
     const double* Zs = As + kmax * 32;
     double* redb = sm + slot * bufd;
     if constexpr (MMA) {
-      constexpr int NT = (RC + 7) / 8;
       const int g = lane >> 2, t = lane & 3;
-      // two accumulator sets (even / odd k-groups) when they fit in registers: twice the independent MMA
-      // chains in flight, summed once
-      constexpr int NU = NT <= 3 ? 2 : 1;
-      double acc[2][4][NT][2];
+      constexpr int NU = NT <= 3 ? 2 : 1;  // second set only when it fits in registers
+      if (first) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+          for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int n = 0; n < NT; ++n) acc[u][m][n][0] = acc[u][m][n][1] = 0.0;
+            for (int n = 0; n < NT; ++n) accm[u][m][n][0] = accm[u][m][n][1] = 0.0;
+      }
       const int nq = (nk + 3) >> 2, per = (nq + 3) >> 2;
       const int q0 = min(nq, w * per), q1 = min(nq, q0 + per);
       const double2* A2 = reinterpret_cast<const double2*>(As);
@@ -1132,35 +923,37 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int
       int q = q0;
       if (NU == 2) {
         for (; q + 1 < q1; q += 2) {
-          kstep(q, acc[0]);
-          kstep(q + 1, acc[NU - 1]);
+          kstep(q, accm[0]);
+          kstep(q + 1, accm[NU - 1]);
         }
       } else {
 #pragma unroll 2
-        for (; q + 1 < q1; ++q) kstep(q, acc[0]);
+        for (; q + 1 < q1; ++q) kstep(q, accm[0]);
       }
-      if (q < q1) kstep(q, acc[0]);
-      __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
-      // fragment (m, n): rows 4g + m, columns 8n + 2t + {0, 1}: one 16-byte store each; rows padded to
-      // kTileLd(RC) doubles (an odd number of 16-byte units: the 8 lanes of a store phase hit 8 distinct
-      // bank groups)
-      constexpr int LD = tile_ld<RC>();
+      if (q < q1) kstep(q, accm[0]);
+      if (last) {
+        __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
+        // fragment (m, n): rows 4g + m, columns 8n + 2t + {0, 1}: one 16-byte store each; rows padded to LD
+        // doubles (an odd number of 16-byte units: the 8 lanes of a store phase hit 8 distinct bank groups)
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          const int col = 8 * n + 2 * t;
-          if (col < RC)
-            *reinterpret_cast<double2*>(redb + w * 32 * LD + (4 * g + m) * LD + col) =
-                NU == 2 ? make_double2(acc[0][m][n][0] + acc[NU - 1][m][n][0], acc[0][m][n][1] + acc[NU - 1][m][n][1])
-                        : make_double2(acc[0][m][n][0], acc[0][m][n][1]);
-        }
+          for (int n = 0; n < NT; ++n) {
+            const int col = 8 * n + 2 * t;
+            if (col < RC)
+              *reinterpret_cast<double2*>(redb + w * 32 * LD + (4 * g + m) * LD + col) =
+                  NU == 2 ? make_double2(accm[0][m][n][0] + accm[NU - 1][m][n][0],
+                                         accm[0][m][n][1] + accm[NU - 1][m][n][1])
+                          : make_double2(accm[0][m][n][0], accm[0][m][n][1]);
+          }
+      }
     } else {
-      double acc[4][CW];
+      if (first) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < CW; ++c) acc[r][c] = 0.0;
+          for (int c = 0; c < CW; ++c) accf[r][c] = 0.0;
+      }
       const int per = (nk + 3) >> 2;
       const int k0 = min(nk, w * per), k1 = min(nk, k0 + per);
 #pragma unroll 2
@@ -1170,46 +963,40 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int t0, int
         const double2 a23 = *reinterpret_cast<const double2*>(As + (((k >> 2) * 2 + 1) * 32 + 4 * rg + (k & 3)) * 2);
         const double av[4] = {a01.x, a01.y, a23.x, a23.y};
         double zv[CW];
-        if (CW % 2 == 0) {
 #pragma unroll
-          for (int c = 0; c < CW / 2; ++c) {
-            const double2 t = *reinterpret_cast<const double2*>(Zs + k * RC + cg * CW + 2 * c);
-            zv[2 * c] = t.x;
-            zv[2 * c + 1] = t.y;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
-        }
+        for (int c = 0; c < CW; ++c) zv[c] = Zs[k * RC + cg * CW + c];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < CW; ++c) acc[r][c] = fma(av[r], zv[c], acc[r][c]);
+          for (int c = 0; c < CW; ++c) accf[r][c] = fma(av[r], zv[c], accf[r][c]);
       }
-      __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
+      if (last) {
+        __syncthreads();  // all warps done with this buffer: reuse it for the 4 warp tiles
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < CW; ++c) redb[w * 32 * tile_ld<RC>() + (4 * rg + r) * tile_ld<RC>() + cg * CW + c] = acc[r][c];
+          for (int c = 0; c < CW; ++c) redb[w * 32 * LD + (4 * rg + r) * LD + cg * CW + c] = accf[r][c];
+      }
     }
-    __syncthreads();
-    const int out = sw.out[it];
-    const int nv = sw.nvalid[it];
-    double* __restrict__ dst =
-        out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
-    constexpr int LDT = tile_ld<RC>();
-    for (int e = tid; e < nv * RC; e += 128) {
-      const int r = e / RC, c = e - r * RC;
-      const double* rb = redb + r * LDT + c;
-      if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LDT]) + rb[64 * LDT]) + rb[96 * LDT];
+    if (last) {
+      __syncthreads();
+      // ---- output rows: fixed-order sum of the 4 warp tiles, coalesced over columns
+      const int out = sw.out[cit];
+      const int nv = sw.nvalid[cit];
+      double* __restrict__ dst =
+          out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
+      for (int e = tid; e < nv * RC; e += 128) {
+        const int r = e / RC, c = e - r * RC;
+        const double* rb = redb + r * LD + c;
+        if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LD]) + rb[64 * LD]) + rb[96 * LD];
+      }
     }
     __syncthreads();  // buffer released: it is refilled at the top of item j+1
+    advance(cc, cit);
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-// Per-level launches: the level's reduction targets after all its items (thread per (target, column)),
-// each target's partial rows in the planned order.  Level groups hit disjoint rows (one group per tile).
 __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
                                double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -1663,35 +1450,22 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
 //   d = -(r0 + sum_j (alpha_j - beta_j) s_j).
 
 // partial[(j*nchunk + c)*B + b] = sum over chunk c of u * V_j  (V_j = Vbase + j*vstride), j < nv; with u2:
-// pairs nv + j = u2 * V2_j as well (both families of the new curvature pair in one pass)
+// pairs nv + j = u2 * V2_j as well (both families of the new curvature pair in one launch).  Block (c, j):
+// one chunk of one pair (grid.y = pairs), so every block streams two vectors with few registers.
 __global__ void k_mdot_partial(const double* __restrict__ u, const double* __restrict__ Vbase, int64_t vstride,
                                int nv, int64_t len, int B, int64_t chunk, double* __restrict__ partial,
                                const double* __restrict__ u2 = nullptr, const double* __restrict__ V2base = nullptr) {
   extern __shared__ double red[];
   const int nb = blockDim.x;
+  const int jp = blockIdx.y;
+  const bool second = jp >= nv;
+  const double* __restrict__ uu = second ? u2 : u;
+  const double* __restrict__ V = (second ? V2base : Vbase) + (int64_t)(second ? jp - nv : jp) * vstride;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
-  double acc[8], acc2[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = acc2[j] = 0.0;
-  for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
-    const double ui = u[i];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < nv) acc[j] += ui * Vbase[j * vstride + i];
-    if (u2) {
-      const double wi = u2[i];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < nv) acc2[j] += wi * V2base[j * vstride + i];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < nv) {
-      red[j * nb + threadIdx.x] = acc[j];
-      if (u2) red[(nv + j) * nb + threadIdx.x] = acc2[j];
-    }
-  block_sim_sums(red, u2 ? 2 * nv : nv, B, partial, gridDim.x, blockIdx.x);
+  double acc = 0.0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += nb) acc += uu[i] * V[i];
+  red[threadIdx.x] = acc;
+  block_sim_sums(red, 1, B, partial + (int64_t)jp * gridDim.x * B, gridDim.x, blockIdx.x);
 }
 
 // slot of the k-th newest pair at iteration `iter` (ring of m)

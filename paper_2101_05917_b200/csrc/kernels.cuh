@@ -28,10 +28,8 @@ struct ElemArgs {
 struct SweepDev {  // device copy of HostPlan::Sweep
   const double* A;
   const int64_t *a_off, *zidx;
-  const int32_t *nk, *nkd, *zrow, *out, *nvalid;
-  const int32_t *ig_ptr, *ig, *g_tptr, *g_cnt;
+  const int32_t *nk, *nkd, *zrow, *out, *nvalid, *chain;
   const int32_t *red_row, *red_mode, *red_ptr, *red_src;
-  const int32_t *sup, *sig, *g_sig, *wl_ptr, *wl, *g_tile, *g_turn;
 };
 
 struct DotArgs {

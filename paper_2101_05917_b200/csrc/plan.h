@@ -49,44 +49,35 @@ struct HostPlan {
   std::vector<double> D, P;          // P holds W_s = L[R_s, J_s] L_ss^{-1} row-major (nr x ns)
   int64_t nnzL = 0;                  // stored entries of L_s (diag blocks packed + panels)
   double factor_flops = 0, factor_ms = 0;
-  // ---- solve schedule (K3 v4): per level and sweep, warp work items over a
-  // k-major factor stream (element (k, lane) of item t at a_off[t] + (k - k0) * 32 + lane).  Items that
-  // share an output (forward W rows of one ancestor tile, split chunks) write partial rows; the last
-  // item of each reduction group to finish (integer countdown) sums the group's partial rows in a fixed
-  // order into its targets — deterministic, one kernel per level.
+  // ---- solve schedule (K3): per level and sweep, work items over a factor stream in
+  // MMA fragment order (element (k, lane) of item t at a_off[t] + sweep_frag_pos(k, lane)).  An item is at
+  // most 128 k-steps (one TMA round); a CHAIN is a run of consecutive items accumulating into the same
+  // 32-lane output on one CTA.  A chain whose output is shared (forward W rows of several supernodes of a
+  // level, outputs split over several chains) writes partial rows; the level's reduce launch sums them in
+  // a fixed order into their targets — deterministic, no atomics.
   int nlevels = 0;
   struct Sweep {
-    std::vector<double> A;             // factor stream in item order (k-major 32-lane blocks)
+    std::vector<double> A;             // factor stream in item order
     std::vector<int32_t> lvl_item;     // [nlevels+1] items of level l: [lvl_item[l], lvl_item[l+1])
-    std::vector<int32_t> lvl_kmax;     // [nlevels] largest item (k-steps) of level l: its shared-memory size
+    std::vector<int32_t> lvl_chain;    // [nlevels+1] chains of level l
+    std::vector<int32_t> chain;        // [nchains+1] first item of each chain (chain c = [chain[c], chain[c+1]))
+    std::vector<int32_t> lvl_kmax;     // [nlevels] largest item (k-steps, padded to 4) of level l
     std::vector<int64_t> a_off;        // per item
     std::vector<int32_t> nk;           // k-steps
     std::vector<int32_t> nkd;          // k < nkd: source row zrow + k of the contiguous source
     std::vector<int32_t> zrow;         //   (z forward, y backward); k >= nkd: row rows[zidx + k - nkd]
     std::vector<int64_t> zidx;         //   of the indirect source (x backward: x[R_s])
-    std::vector<int32_t> out;          // >= 0: direct output row out + lane; < 0: partial rows (-out-1)*32 + lane
+    std::vector<int32_t> out;          // per item (same for a chain): >= 0: direct output row out + lane;
+                                       //   < 0: partial rows (-out-1)*32 + lane
     std::vector<int32_t> nvalid;       // valid lanes
-    std::vector<int32_t> ig_ptr, ig;   // CSR item -> reduction groups it contributes to
-    std::vector<int32_t> lvl_grp;      // [nlevels+1] groups of level l
-    std::vector<int32_t> g_tptr;       // [ngroups+1] targets of group g: [g_tptr[g], g_tptr[g+1])
-    std::vector<int32_t> g_cnt;        // items contributing to group g (countdown start)
+    std::vector<int32_t> lvl_red;      // [nlevels+1] reduce targets of level l
     std::vector<int32_t> red_row;      // target row (solve position)
     std::vector<int32_t> red_mode;     // 0: dst[row] = sum (y or x), 1: z[row] -= sum
     std::vector<int32_t> red_ptr;      // [ntargets+1] into red_src
     std::vector<int32_t> red_src;      // partial row indices, summed in this order
-    // dataflow (one launch per sweep): an item waits until its inputs are final
-    std::vector<int32_t> sup;          // per item: its supernode
-    std::vector<int32_t> sig;          // per item: supernode whose countdown it decrements when done (-1)
-    std::vector<int32_t> g_sig;        // per group: supernode whose countdown the group decrements (-1)
-    std::vector<int32_t> g_tile;       // per group: z-row tile it subtracts into (-1: assign groups)
-    std::vector<int32_t> g_turn;       //   and its turn among that tile's groups (level order)
-    int32_t ntiles = 0;
-    std::vector<int32_t> cd_init;      // per supernode: countdown start (fwd: W groups into it;
-                                       //   bwd: its 32-column chunks)
-    std::vector<int32_t> wl_ptr, wl;   // per supernode: supernodes whose countdown must be 0 first
-    int64_t max_partial_rows = 0;      // partial rows are unique over the whole sweep
+    int64_t max_partial_rows = 0;      // partial rows of the largest level
   } fw, bw;
-  int warps_target = 148 * 16;         // warps per level launch the item size is balanced for
+  int chain_ctas = 148 * 4;            // CTAs a level launch is balanced for (chain length cap)
   // ---- contact candidates: ordered LAST as one root supernode ----
   int nc = 0;                        // number of candidate nodes (0 = no contact)
   int csup = -1;                     // index of the candidate supernode (= nsup - 1)

@@ -20,6 +20,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <tuple>
 #include <numeric>
 #include <omp.h>
 
@@ -176,55 +177,32 @@ static void tri_inverse(const double* F, int f, int ns, double* D, bool par) {
 
 // ---------------------------------------------------------------- solve schedule
 // Forward sweep, level l (children before parents), for every level-l supernode s (z[J_s] final):
-//   D items: y[J_s rows i0..i0+32) = D_s[rows, 0..min(i0+32, ns)) z[J_s]      (k-major, lane = row)
-//   W items: partial rows = W_s[rows i0..i0+32, :] z[J_s];  group of an ancestor tile: z[R_s[i]] -= sum
+//   D outputs: y[J_s rows i0..i0+32) = D_s[rows, 0..min(i0+32, ns)) z[J_s]      (lane = row)
+//   W outputs: W_s[rows i0..i0+32 of R_s, :] z[J_s] -> partial rows; reduce: z[R_s[i]] -= sum
 // Backward sweep, level l (parents first), column chunk c0..c0+32 of s:
-//   x[J_s cols] = D_s^T y[J_s] - W_s^T x[R_s]     (D part k = c0..ns, W part k = 0..nr; lane = column)
-// Items hold <= kc_l k-steps (kc_l balances the level over warps_target warps); a chunk covered by one
-// item writes its output directly, otherwise its items write partial rows summed by the chunk's group.
-static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vector<int32_t>>& byh);
+//   x[J_s cols] = D_s^T y[J_s] - W_s^T x[R_s]     (k-sequence [D part c0..ns | W part 0..nr]; lane = column)
+// An output's k-sequence is cut into items of <= 128 k-steps (one TMA round each) grouped into chains of
+// <= CL items that accumulate on one CTA; CL balances the level's items over chain_ctas CTAs.  An output
+// covered by one chain is written directly (D, backward); otherwise each chain writes partial rows and the
+// level's reduce sums them in chain order.
 static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
-  build_solve_schedule_items(P, byh);
+  const int L = 32, KC = 128;
   for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
-    S->lvl_kmax.assign(P.nlevels, 0);
-    for (int l = 0; l < P.nlevels; ++l)
-      for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) S->lvl_kmax[l] = std::max(S->lvl_kmax[l], (S->nk[t] + 3) & ~3);
+    *S = HostPlan::Sweep();
+    S->lvl_item.assign(1, 0);
+    S->lvl_chain.assign(1, 0);
+    S->lvl_red.assign(1, 0);
+    S->red_ptr.assign(1, 0);
   }
-}
-static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
-  const int L = 32;
-  auto init = [&](HostPlan::Sweep& S) {
-    S = HostPlan::Sweep();
-    S.lvl_item.assign(1, 0);
-    S.red_ptr.assign(1, 0);
-    S.g_tptr.assign(1, 0);
-    S.ig_ptr.assign(1, 0);
-    S.lvl_grp.assign(1, 0);
-    S.cd_init.assign(P.nsup, 0);
-    S.wl_ptr.assign(1, 0);
-  };
-  init(P.fw);
-  init(P.bw);
-  std::vector<int32_t> sup_of_pos(P.nfree);
-  for (int s = 0; s < P.nsup; ++s)
-    for (int k = 0; k < P.ssize[s]; ++k) sup_of_pos[P.sfirst[s] + k] = s;
   auto Dval = [&](int s, int i, int k) -> double {  // D_s[i][k], packed lower
     return k <= i ? P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + k] : 0.0;
   };
   auto Wval = [&](int s, int i, int k) -> double {  // W_s[i][k], row-major nr x ns
     return P.P[P.poff[s] + (int64_t)i * P.ssize[s] + k];
   };
-  auto kc_for = [&](int64_t ktot) {
-    int64_t kc = (ktot + P.warps_target - 1) / P.warps_target;
-    kc = (kc + 7) / 8 * 8;
-    (void)kc;
-    return 128;  // = kItemK: one item (32 x 128 factor block + 128 rhs rows) per warp buffer, one TMA round
-  };
   // one item: the block val(k, lane), k = 0..nk, lane = output row/col 0..31, in the fragment layout of the
   // fp64 tensor-core MMA (m8n8k4; plan.h sweep_frag_pos): k padded with zeros to a multiple of 4
-  int cur_sup = -1;
-  auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, auto&& val, int nkd = -1) {
-    S.sup.push_back(cur_sup);
+  auto emit_item = [&](HostPlan::Sweep& S, int nk, int nv, int zr, int64_t zi, int nkd, int out, auto&& val) {
     const int64_t base = (int64_t)S.A.size();
     S.a_off.push_back(base);
     const int nkp = (nk + 3) & ~3;
@@ -232,194 +210,150 @@ static void build_solve_schedule_items(HostPlan& P, const std::vector<std::vecto
     for (int k = 0; k < nk; ++k)
       for (int l = 0; l < nv; ++l) S.A[base + sweep_frag_pos(k, l)] = val(k, l);
     S.nk.push_back(nk);
-    S.nkd.push_back(nkd < 0 ? nk : nkd);
+    S.nkd.push_back(nkd);
     S.zrow.push_back(zr);
     S.zidx.push_back(zi);
     S.nvalid.push_back(nv);
+    S.out.push_back(out);
   };
-  // a level's reduction groups: targets (row, mode, contributions in order), contributing items
-  struct Target { int32_t row, mode; std::vector<int32_t> src; };
-  struct Group { std::vector<Target> t; std::vector<int32_t> items; int32_t sig = -1, tile = -1, turn = 0; };
-  auto flush_groups = [&](HostPlan::Sweep& S, std::vector<Group>& groups, int item_base) {
-    const int nitem = (int)S.a_off.size() - item_base;
-    std::vector<std::vector<int32_t>> of_item(nitem);
-    for (auto& g : groups) {
-      const int gid = (int)S.g_cnt.size();
-      for (auto& t : g.t) {
-        S.red_row.push_back(t.row);
-        S.red_mode.push_back(t.mode);
-        for (int32_t r : t.src) S.red_src.push_back(r);
-        S.red_ptr.push_back((int32_t)S.red_src.size());
+  // one output (nv lanes) over a k-sequence of ktot steps; src(p0, nk) -> {zrow, zidx, nkd} of the item at
+  // p0; val(p, lane) = factor entry at sequence position p.  Direct (direct_row >= 0 and one chain) or
+  // partial rows, whose bases (one per chain) are returned in order.
+  auto emit_output = [&](HostPlan::Sweep& S, int CL, int ktot, int nv, int direct_row, int64_t& prow, auto&& src,
+                         auto&& val) {
+    std::vector<int64_t> bases;
+    const int nit = std::max(1, (ktot + KC - 1) / KC);
+    const int nch = (nit + CL - 1) / CL;
+    const int per = (nit + nch - 1) / nch;  // items per chain, balanced
+    const bool direct = direct_row >= 0 && nch == 1;
+    for (int it = 0; it < nit; ++it) {
+      int out = direct_row;
+      if (it % per == 0) {
+        S.chain.push_back((int32_t)S.a_off.size());
+        if (!direct) {
+          bases.push_back(prow);
+          prow += L;
+        }
       }
-      S.g_tptr.push_back((int32_t)S.red_row.size());
-      std::sort(g.items.begin(), g.items.end());
-      g.items.erase(std::unique(g.items.begin(), g.items.end()), g.items.end());
-      S.g_cnt.push_back((int32_t)g.items.size());
-      S.g_sig.push_back(g.sig);
-      S.g_tile.push_back(g.tile);
-      S.g_turn.push_back(g.turn);
-      for (int32_t it : g.items) of_item[it - item_base].push_back(gid);
+      if (!direct) out = -(int32_t)(bases.back() / L) - 1;
+      const int p0 = it * KC, nk = std::max(0, std::min(KC, ktot - p0));
+      const std::array<int64_t, 3> zs = src(p0, nk);
+      emit_item(S, nk, nv, (int)zs[0], zs[1], (int)zs[2], out, [&](int k, int l) { return val(p0 + k, l); });
     }
-    for (auto& v : of_item) {
-      for (int32_t g : v) S.ig.push_back(g);
-      S.ig_ptr.push_back((int32_t)S.ig.size());
-    }
-    groups.clear();
+    return bases;
   };
+  constexpr int kChainNoSplit = 4;  // outputs of <= 4 items stay on one CTA in the backward sweep
+  auto chain_cap = [&](int64_t items) { return (int)std::max<int64_t>(1, (items + P.chain_ctas - 1) / P.chain_ctas); };
+  auto close_level = [&](HostPlan::Sweep& S, int64_t prow,
+                         std::vector<std::tuple<int32_t, int32_t, std::vector<int32_t>>>& targets) {
+    // targets (row, mode, partial rows in summation order), sorted by row: the level's reduce
+    std::stable_sort(targets.begin(), targets.end(),
+                     [](const auto& x, const auto& y) { return std::get<0>(x) < std::get<0>(y); });
+    for (auto& t : targets) {
+      S.red_row.push_back(std::get<0>(t));
+      S.red_mode.push_back(std::get<1>(t));
+      for (int32_t r : std::get<2>(t)) S.red_src.push_back(r);
+      S.red_ptr.push_back((int32_t)S.red_src.size());
+    }
+    targets.clear();
+    S.lvl_red.push_back((int32_t)S.red_row.size());
+    S.lvl_item.push_back((int32_t)S.a_off.size());
+    S.lvl_chain.push_back((int32_t)S.chain.size());
+    S.max_partial_rows = std::max(S.max_partial_rows, prow);
+  };
+  std::vector<std::tuple<int32_t, int32_t, std::vector<int32_t>>> targets;
   // ---- forward
   {
     HostPlan::Sweep& S = P.fw;
-    int64_t prow = 0;  // partial rows: unique over the sweep (one launch runs all levels)
-    // z-row tiles (32 rows of one supernode) receive one W group per level that touches them; the groups
-    // of a tile take turns in level order (deterministic order of the read-modify-writes of z)
-    std::map<std::pair<int, int>, std::pair<int, int>> tiles;  // (sup, tile) -> (tile id, groups so far)
     for (int lev = 0; lev < P.nlevels; ++lev) {
-      int64_t ktot = 0;
+      int64_t items = 0;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-        for (int i0 = 0; i0 < ns; i0 += L) ktot += std::min(i0 + L, ns);
-        ktot += (int64_t)((nr + L - 1) / L) * ns;
+        for (int i0 = 0; i0 < ns; i0 += L) items += (std::min(i0 + L, ns) + KC - 1) / KC;
+        items += (int64_t)((nr + L - 1) / L) * ((ns + KC - 1) / KC);
       }
-      const int KC = kc_for(ktot);
-      const int item_base = (int)S.a_off.size();
-      std::vector<Group> groups;
-      std::vector<std::array<int32_t, 3>> contrib;  // (target row, partial row, item), emission order
+      const int CL = chain_cap(items);
+      int64_t prow = 0;  // partial rows are reused level by level (the reduce consumes them first)
+      std::map<int32_t, std::vector<int32_t>> wsum;  // target row -> partial rows (emission order)
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-        cur_sup = s;
-        for (int i0 = 0; i0 < ns; i0 += L) {  // D items
+        for (int i0 = 0; i0 < ns; i0 += L) {  // D outputs
           const int kend = std::min(i0 + L, ns), nv = std::min(L, ns - i0);
-          const int nit = (kend + KC - 1) / KC;
-          Group g;
-          if (nit > 1)
-            for (int l = 0; l < nv; ++l) g.t.push_back({f + i0 + l, 0, {}});
-          for (int k0 = 0; k0 < kend; k0 += KC) {
-            const int k1 = std::min(kend, k0 + KC);
-            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Dval(s, i0 + l, k0 + k); });
-            S.sig.push_back(-1);
-            if (nit == 1) {
-              S.out.push_back(f + i0);
-            } else {
-              S.out.push_back(-(int32_t)(prow / L) - 1);
-              for (int l = 0; l < nv; ++l) g.t[l].src.push_back((int32_t)(prow + l));
-              g.items.push_back((int32_t)S.a_off.size() - 1);
-              prow += L;
+          auto bases = emit_output(
+              S, CL, kend, nv, f + i0, prow,
+              [&](int p0, int) { return std::array<int64_t, 3>{f + p0, 0, std::min(KC, kend - p0)}; },
+              [&](int p, int l) { return Dval(s, i0 + l, p); });
+          if (!bases.empty())
+            for (int l = 0; l < nv; ++l) {
+              std::vector<int32_t> src;
+              for (int64_t b : bases) src.push_back((int32_t)(b + l));
+              targets.emplace_back(f + i0 + l, 0, std::move(src));
             }
-          }
-          if (nit > 1) groups.push_back(std::move(g));
         }
-        for (int i0 = 0; i0 < nr; i0 += L) {  // W items
+        for (int i0 = 0; i0 < nr; i0 += L) {  // W outputs (always partial: targets shared across supernodes)
           const int nv = std::min(L, nr - i0);
-          for (int k0 = 0; k0 < ns; k0 += KC) {
-            const int k1 = std::min(ns, k0 + KC);
-            emit_item(S, k1 - k0, nv, f + k0, 0, [&](int k, int l) { return Wval(s, i0 + l, k0 + k); });
-            S.sig.push_back(-1);
-            S.out.push_back(-(int32_t)(prow / L) - 1);
-            for (int l = 0; l < nv; ++l)
-              contrib.push_back({P.rows[P.rptr[s] + i0 + l], (int32_t)(prow + l), (int32_t)S.a_off.size() - 1});
-            prow += L;
-          }
+          auto bases = emit_output(
+              S, CL, ns, nv, -1, prow,
+              [&](int p0, int) { return std::array<int64_t, 3>{f + p0, 0, std::min(KC, ns - p0)}; },
+              [&](int p, int l) { return Wval(s, i0 + l, p); });
+          for (int l = 0; l < nv; ++l)
+            for (int64_t b : bases) wsum[P.rows[P.rptr[s] + i0 + l]].push_back((int32_t)(b + l));
         }
       }
-      std::stable_sort(contrib.begin(), contrib.end(),
-                       [](const std::array<int32_t, 3>& x, const std::array<int32_t, 3>& y) { return x[0] < y[0]; });
-      for (size_t i = 0; i < contrib.size();) {
-        const int row = contrib[i][0];
-        const int a = sup_of_pos[row];
-        const int tile = (row - P.sfirst[a]) / L;
-        Group g;
-        g.sig = a;
-        S.cd_init[a]++;
-        auto ins = tiles.insert({{a, tile}, {(int)tiles.size(), 0}}).first;
-        g.tile = ins->second.first;
-        g.turn = ins->second.second++;
-        size_t j = i;
-        while (j < contrib.size() && sup_of_pos[contrib[j][0]] == a && (contrib[j][0] - P.sfirst[a]) / L == tile) {
-          const int r = contrib[j][0];
-          Target t{r, 1, {}};
-          while (j < contrib.size() && contrib[j][0] == r) {
-            t.src.push_back(contrib[j][1]);
-            g.items.push_back(contrib[j][2]);
-            ++j;
-          }
-          g.t.push_back(std::move(t));
-        }
-        groups.push_back(std::move(g));
-        i = j;
-      }
-      flush_groups(S, groups, item_base);
-      S.lvl_grp.push_back((int32_t)S.g_cnt.size());
-      S.lvl_item.push_back((int32_t)S.a_off.size());
+      for (auto& kv : wsum) targets.emplace_back(kv.first, 1, std::move(kv.second));
+      close_level(S, prow, targets);
     }
-    S.ntiles = (int32_t)tiles.size();
-    S.max_partial_rows = prow;
-    for (int s2 = 0; s2 < P.nsup; ++s2) S.wl_ptr.push_back(0);  // forward waits on cd of its own supernode
   }
   // ---- backward (levels top-down; stored in that execution order: level index = H - l)
   {
     HostPlan::Sweep& S = P.bw;
-    int64_t prow = 0;
     for (int lev = P.nlevels - 1; lev >= 0; --lev) {
-      int64_t ktot = 0;
+      int64_t items = 0;
+      int lmax = 1;  // longest output (items)
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-        for (int c0 = 0; c0 < ns; c0 += L) ktot += (ns - c0) + nr;
+        for (int c0 = 0; c0 < ns; c0 += L) {
+          const int nit = ((ns - c0) + nr + KC - 1) / KC;
+          items += nit;
+          lmax = std::max(lmax, nit);
+        }
       }
-      const int KC = kc_for(ktot);
-      const int item_base = (int)S.a_off.size();
-      std::vector<Group> groups;
+      // chains long enough that no output of the level is split (no partial rows, no reduce launch) when the
+      // longest output is short; else the balance cap
+      const int CL = std::max(chain_cap(items), lmax <= kChainNoSplit ? lmax : 1);
+      int64_t prow = 0;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s];
         const int nr = (int)(P.rptr[s + 1] - P.rptr[s]);
-        cur_sup = s;
         for (int c0 = 0; c0 < ns; c0 += L) {
-          S.cd_init[s]++;
           const int nv = std::min(L, ns - c0);
-          // k-sequence = [D part: rows c0..ns of D_s | W part: rows 0..nr of W_s], cut into items of <= KC
+          // k-sequence = [D part: rows c0..ns of D_s | W part: rows 0..nr of W_s]
           const int nd = ns - c0, ktot_c = nd + nr;
-          const int nit = (ktot_c + KC - 1) / KC;
-          Group g;
-          g.sig = s;
-          if (nit > 1)
-            for (int l = 0; l < nv; ++l) g.t.push_back({f + c0 + l, 0, {}});
-          for (int p0 = 0; p0 < ktot_c; p0 += KC) {
-            const int nk = std::min(KC, ktot_c - p0);
-            const int nkd = std::max(0, std::min(nk, nd - p0));
-            emit_item(S, nk, nv, f + c0 + p0, P.rptr[s] + std::max(0, p0 - nd),
-                      [&](int k, int l) {
-                        const int q = p0 + k;
-                        return q < nd ? Dval(s, c0 + q, c0 + l) : -Wval(s, q - nd, c0 + l);
-                      },
-                      nkd);
-            S.sig.push_back(nit == 1 ? s : -1);
-            if (nit == 1) {
-              S.out.push_back(f + c0);
-            } else {
-              S.out.push_back(-(int32_t)(prow / L) - 1);
-              for (int l = 0; l < nv; ++l) g.t[l].src.push_back((int32_t)(prow + l));
-              g.items.push_back((int32_t)S.a_off.size() - 1);
-              prow += L;
+          auto bases = emit_output(
+              S, CL, ktot_c, nv, f + c0, prow,
+              [&](int p0, int nk) {
+                return std::array<int64_t, 3>{f + c0 + p0, P.rptr[s] + std::max(0, p0 - nd),
+                                              std::max(0, std::min(nk, nd - p0))};
+              },
+              [&](int q, int l) { return q < nd ? Dval(s, c0 + q, c0 + l) : -Wval(s, q - nd, c0 + l); });
+          if (!bases.empty())
+            for (int l = 0; l < nv; ++l) {
+              std::vector<int32_t> src;
+              for (int64_t b : bases) src.push_back((int32_t)(b + l));
+              targets.emplace_back(f + c0 + l, 0, std::move(src));
             }
-          }
-          if (nit > 1) groups.push_back(std::move(g));
         }
       }
-      flush_groups(S, groups, item_base);
-      S.lvl_grp.push_back((int32_t)S.g_cnt.size());
-      S.lvl_item.push_back((int32_t)S.a_off.size());
+      close_level(S, prow, targets);
     }
-    S.max_partial_rows = prow;
-    // wait list of s: the supernodes owning rows of R_s (their x must be final before W_s^T x[R_s])
-    S.wl_ptr.assign(1, 0);
-    for (int s = 0; s < P.nsup; ++s) {
-      std::vector<int32_t> a;
-      for (int64_t k = P.rptr[s]; k < P.rptr[s + 1]; ++k) a.push_back(sup_of_pos[P.rows[k]]);
-      std::sort(a.begin(), a.end());
-      a.erase(std::unique(a.begin(), a.end()), a.end());
-      for (int32_t v : a) S.wl.push_back(v);
-      S.wl_ptr.push_back((int32_t)S.wl.size());
-    }
+  }
+  for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
+    S->chain.push_back((int32_t)S->a_off.size());  // sentinel
+    S->lvl_kmax.assign(P.nlevels, 0);
+    for (int l = 0; l < P.nlevels; ++l)
+      for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t)
+        S->lvl_kmax[l] = std::max(S->lvl_kmax[l], (S->nk[t] + 3) & ~3);
   }
 }
 

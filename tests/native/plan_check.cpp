@@ -47,81 +47,66 @@ int main(int argc, char** argv) {
   std::vector<double> v(N), b(N, 0.0);
   for (auto& x : v) x = nd(rng);
   for (int p = 0; p < N; ++p) for (int64_t k = P.a_ptr[p]; k < P.a_ptr[p + 1]; ++k) b[p] += P.a_val[k] * v[P.a_col[k]];
-  // Emulate the device schedule (K3 v3) exactly: per level, items (k-major 32-lane blocks) then the
-  // level's reduce; forward writes y (D) / partial rows, backward writes x / partial rows.
+  // Emulate the device schedule exactly: per level, chains (items accumulated in order, then written to
+  // their direct rows or partial rows), then the level's reduce (targets in order, sources in order).
+  // Forward writes y (direct / assign) and subtracts into z; backward writes x.
   std::vector<double> z(b), y(N, 0.0), x(N, 0.0);
   auto run = [&](const HostPlan::Sweep& S, std::vector<double>& zsrc, std::vector<double>& direct,
                  std::vector<double>* zsub, bool fwd) {
-    // dataflow invariants of the one-launch sweep: in item order every wait is already satisfied, and
-    // every countdown ends at exactly 0
-    std::vector<int> cd(S.cd_init.begin(), S.cd_init.end()), grem(S.g_cnt.begin(), S.g_cnt.end());
-    std::vector<int> turn(S.ntiles, 0);
-    std::vector<double> part(S.max_partial_rows + 32, 0.0);
-    {  // a row is the target of at most one group (no concurrent read-modify-write of the same row)
-      // mode 0 (y/x assign): exactly one group per row; mode 1 (z subtract): every group of a row belongs
-      // to the same tile, whose groups are serialised by their turns
-      std::vector<int> hits(N, 0), tile_of(N, -1);
-      for (size_t g = 0; g < S.g_cnt.size(); ++g)
-        for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
-          const int row = S.red_row[r];
-          if (S.red_mode[r] == 0) {
-            if (++hits[row] > 1) { printf("row %d assigned by two groups\n", row); exit(10); }
-          } else {
-            if (S.g_tile[g] < 0 || (tile_of[row] >= 0 && tile_of[row] != S.g_tile[g])) {
-              printf("row %d updated by groups of different tiles\n", row);
-              exit(10);
-            }
-            tile_of[row] = S.g_tile[g];
-          }
-        }
+    std::vector<double> part((size_t)(S.max_partial_rows + 32), 0.0);
+    std::vector<int> assigned(N, 0);
+    if ((int)S.lvl_chain.size() != P.nlevels + 1 || S.chain.back() != (int)S.a_off.size()) {
+      printf("bad chain index\n");
+      exit(12);
     }
     for (int lev = 0; lev < P.nlevels; ++lev) {
-      for (int t = S.lvl_item[lev]; t < S.lvl_item[lev + 1]; ++t) {
-        const int su = S.sup[t];
-        if (fwd) {
-          if (cd[su] != 0) { printf("fwd item %d of s=%d runs before its inputs are final\n", t, su); exit(7); }
-        } else if (S.nkd[t] < S.nk[t]) {
-          for (int q = S.wl_ptr[su]; q < S.wl_ptr[su + 1]; ++q)
-            if (cd[S.wl[q]] != 0) { printf("bwd item %d waits on s=%d\n", t, S.wl[q]); exit(8); }
+      std::vector<int> pused((size_t)(S.max_partial_rows / 32 + 1), 0);
+      for (int c = S.lvl_chain[lev]; c < S.lvl_chain[lev + 1]; ++c) {
+        const int t0 = S.chain[c], t1 = S.chain[c + 1];
+        if (t0 < S.lvl_item[lev] || t1 > S.lvl_item[lev + 1] || t1 <= t0) { printf("chain outside its level\n"); exit(13); }
+        std::vector<double> acc(32, 0.0);
+        for (int t = t0; t < t1; ++t) {
+          if (S.out[t] != S.out[t0] || S.nvalid[t] != S.nvalid[t0]) { printf("chain output mismatch\n"); exit(14); }
+          for (int l = 0; l < S.nvalid[t]; ++l)
+            for (int k = 0; k < S.nk[t]; ++k) {
+              const bool contig = k < S.nkd[t];
+              const int zr = contig ? S.zrow[t] + k : P.rows[S.zidx[t] + k - S.nkd[t]];
+              acc[l] += S.A[S.a_off[t] + sweep_frag_pos(k, l)] * (fwd ? zsrc[zr] : (contig ? y[zr] : x[zr]));
+            }
         }
-        for (int l = 0; l < S.nvalid[t]; ++l) {
-          double acc = 0;
-          for (int k = 0; k < S.nk[t]; ++k) {
-            const bool contig = k < S.nkd[t];
-            const int zr = contig ? S.zrow[t] + k : P.rows[S.zidx[t] + k - S.nkd[t]];
-            acc += S.A[S.a_off[t] + sweep_frag_pos(k, l)] * (fwd ? zsrc[zr] : (contig ? y[zr] : x[zr]));
+        const int o = S.out[t0];
+        for (int l = 0; l < S.nvalid[t0]; ++l) {
+          if (o >= 0) {
+            if (assigned[o + l]++) { printf("row %d written twice\n", o + l); exit(10); }
+            direct[o + l] = acc[l];
+          } else {
+            if (l == 0 && pused[-o - 1]++) { printf("partial block %d reused in a level\n", -o - 1); exit(15); }
+            part[(size_t)(-o - 1) * 32 + l] = acc[l];
           }
-          if (S.out[t] >= 0) direct[S.out[t] + l] = acc;
-          else part[(int64_t)(-S.out[t] - 1) * 32 + l] = acc;
         }
-        if (S.sig[t] >= 0) cd[S.sig[t]]--;
-        // device semantics: the item that brings a group to zero applies the group's sums, then signals
-        for (int q = S.ig_ptr[t]; q < S.ig_ptr[t + 1]; ++q) {
-          const int g = S.ig[q];
-          if (--grem[g] != 0) continue;
-          if (S.g_tile[g] >= 0 && turn[S.g_tile[g]]++ != S.g_turn[g]) { printf("group %d out of turn\n", g); exit(11); }
-          for (int r = S.g_tptr[g]; r < S.g_tptr[g + 1]; ++r) {
-            double acc = 0;
-            for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
-            if (S.red_mode[r] == 0) direct[S.red_row[r]] = acc;
-            else (*zsub)[S.red_row[r]] -= acc;
-          }
-          if (S.g_sig[g] >= 0) cd[S.g_sig[g]]--;
+      }
+      for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) {
+        double acc = 0;
+        for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
+        if (S.red_mode[r] == 0) {
+          if (assigned[S.red_row[r]]++) { printf("row %d written twice\n", S.red_row[r]); exit(10); }
+          direct[S.red_row[r]] = acc;
+        } else {
+          (*zsub)[S.red_row[r]] -= acc;
         }
       }
     }
-    for (size_t g = 0; g < grem.size(); ++g)
-      if (grem[g] != 0) { printf("group %zu never completes (%d left)\n", g, grem[g]); exit(6); }
-    for (size_t i = 0; i < cd.size(); ++i)
-      if (cd[i] != 0) { printf("countdown of s=%zu ends at %d\n", i, cd[i]); exit(9); }
+    for (int p = 0; p < N; ++p)
+      if (assigned[p] != 1) { printf("row %d written %d times\n", p, assigned[p]); exit(11); }
   };
   run(P.fw, z, y, &z, true);
   run(P.bw, y, x, nullptr, false);
   double err = 0, mx = 0;
   for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
   int64_t nnzA = P.a_ptr[N];
-  printf("n=%d nfree=%d nsup=%d levels=%d fitems=%zu bitems=%zu fstream=%zu bstream=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
-         n, N, P.nsup, P.nlevels, P.fw.a_off.size(), P.bw.a_off.size(), P.fw.A.size(), P.bw.A.size(), (long long)nnzA,
+  printf("n=%d nfree=%d nsup=%d levels=%d fitems=%zu bitems=%zu fchains=%zu bchains=%zu fstream=%zu bstream=%zu nnzA=%lld nnzL=%lld flops=%.3g factor_ms=%.1f relerr=%.3e\n",
+         n, N, P.nsup, P.nlevels, P.fw.a_off.size(), P.bw.a_off.size(), P.fw.chain.size() - 1, P.bw.chain.size() - 1,
+         P.fw.A.size(), P.bw.A.size(), (long long)nnzA,
          (long long)P.nnzL, P.factor_flops, P.factor_ms, err / mx);
   return err / mx < 1e-10 ? 0 : 2;
 }
