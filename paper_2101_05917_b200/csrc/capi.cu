@@ -642,6 +642,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.out = s->upload(S.out);
       d.nvalid = s->upload(S.nvalid);
       d.chain = s->upload(S.chain);
+      d.rec = reinterpret_cast<const int4*>(s->upload(S.rec));
       d.red_row = s->upload(S.red_row);
       d.red_mode = s->upload(S.red_mode);
       d.red_ptr = s->upload(S.red_ptr);

@@ -818,13 +818,18 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  auto load = [&](int it, int slot) {  // one TMA round for item `it` into buffer `slot`
+  // per-buffer item metadata, written by the load phase one item ahead (the compute phase reads no global
+  // metadata): k-steps, output, valid lanes, chain flags (bit 0 first, bit 1 last)
+  __shared__ int4 meta[4];
+  // one TMA round for the item with record (ra, rb) into buffer `slot`
+  auto load = [&](const int4& ra, const int4& rb, int slot) {
     double* As = sm + slot * bufd;
     double* Zs = As + kmax * 32;
-    const int nk = sw.nk[it], nkd = sw.nkd[it], nkp = (nk + 3) & ~3;
-    const double* Ag = sw.A + sw.a_off[it];
-    const int zr = sw.zrow[it];
-    const int32_t* idx = rows + sw.zidx[it] - nkd;
+    const int nk = ra.y & 0xffff, nkd = ra.y >> 16, nkp = (nk + 3) & ~3;
+    if (tid == 0) meta[slot] = make_int4(nk, rb.x, rb.y & 0xff, (rb.y >> 8) & 3);
+    const double* Ag = sw.A + (int64_t)ra.x * 32;
+    const int zr = ra.z;
+    const int32_t* idx = rows + ra.w - nkd;
     if (VEC) {
       const bool whole = rcn == RC && RC == R && nkd == nk;
       if (tid == 0) {
@@ -854,36 +859,47 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
     }
   };
   // cursors over this CTA's item sequence: (chain, item); item -1 = exhausted
-  auto first_of = [&](int c) { return c < nchains ? sw.chain[ch0 + c] : -1; };
-  auto advance = [&](int& c, int& it) {
-    if (it + 1 < sw.chain[ch0 + c + 1]) {
-      ++it;
+  // load cursor over this CTA's items: item lit (-1 = exhausted) of chain lc, its record (ra, rb) and the first
+  // item of the CTA's next chain are always prefetched one load ahead (no dependent global load between an
+  // item's barrier and its TMA issue)
+  int lc = blockIdx.x, lit = lc < nchains ? sw.chain[ch0 + lc] : -1;
+  int nxt = lc + G < nchains ? sw.chain[ch0 + lc + G] : -1;
+  int4 ra = make_int4(0, 0, 0, 0), rb = ra;
+  if (lit >= 0) {
+    ra = __ldg(sw.rec + 2 * lit);
+    rb = __ldg(sw.rec + 2 * lit + 1);
+  }
+  int nload = 0;  // items loaded so far (uniform over the CTA)
+  auto load_next = [&](int slot) {
+    load(ra, rb, slot);
+    ++nload;
+    if (!((rb.y >> 9) & 1)) {
+      ++lit;
     } else {
-      c += G;
-      it = first_of(c);
+      lc += G;
+      lit = nxt;
+      nxt = lc + G < nchains ? sw.chain[ch0 + lc + G] : -1;
+    }
+    if (lit >= 0) {
+      ra = __ldg(sw.rec + 2 * lit);
+      rb = __ldg(sw.rec + 2 * lit + 1);
     }
   };
-  int lc = blockIdx.x, lit = first_of(lc);  // next item to load
-  for (int p = 0; p < nbuf - 1 && lit >= 0; ++p) {
-    load(lit, p);
-    advance(lc, lit);
-  }
+  for (int p = 0; p < nbuf - 1 && lit >= 0; ++p) load_next(p);
   // accumulators live across the items of a chain
   double accm[2][4][NT][2];  // MMA: fragments (two sets: even / odd k-groups)
   double accf[4][CW];        // FMA: 4 rows x CW columns
-  int cc = blockIdx.x, cit = first_of(cc);
-  for (int j = 0; cit >= 0; ++j) {
+  for (int j = 0; j < nload; ++j) {
     const int slot = j % nbuf;
-    const int nk = sw.nk[cit];
-    const bool first = cit == sw.chain[ch0 + cc];
-    const bool last = cit + 1 == sw.chain[ch0 + cc + 1];
     if (!VEC) cp_async_wait_all();
     mbar_wait(mb + slot, (j / nbuf) & 1);
-    __syncthreads();  // item j visible to all; the buffer refilled next was released at the end of item j-1
-    if (lit >= 0) {
+    __syncthreads();  // item j (data + meta) visible to all; every thread is past item j-1's epilogue
+    const int4 md = meta[slot];
+    const int nk = md.x;
+    const bool first = md.w & 1, last = md.w & 2;
+    if (lit >= 0) {  // refill the buffer of item j-1
       fence_proxy_async();
-      load(lit, (j + nbuf - 1) % nbuf);
-      advance(lc, lit);
+      load_next((j + nbuf - 1) % nbuf);
     }
     const double* As = sm + slot * bufd;
     const double* Zs = As + kmax * 32;
@@ -981,8 +997,8 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
     if (last) {
       __syncthreads();
       // ---- output rows: fixed-order sum of the 4 warp tiles, coalesced over columns
-      const int out = sw.out[cit];
-      const int nv = sw.nvalid[cit];
+      const int out = md.y;
+      const int nv = md.z;
       double* __restrict__ dst =
           out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
       for (int e = tid; e < nv * RC; e += 128) {
@@ -991,8 +1007,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
         if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LD]) + rb[64 * LD]) + rb[96 * LD];
       }
     }
-    __syncthreads();  // buffer released: it is refilled at the top of item j+1
-    advance(cc, cit);
+    // (the buffer is refilled after the next item's barrier: no barrier needed here)
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }

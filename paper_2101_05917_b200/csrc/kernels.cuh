@@ -29,6 +29,7 @@ struct SweepDev {  // device copy of HostPlan::Sweep
   const double* A;
   const int64_t *a_off, *zidx;
   const int32_t *nk, *nkd, *zrow, *out, *nvalid, *chain;
+  const int4* rec;  // packed per-item records, 2 x int4 per item (plan.h int4x2)
   const int32_t *red_row, *red_mode, *red_ptr, *red_src;
 };
 

@@ -8,6 +8,13 @@
 
 namespace pdb {
 
+// Packed per-item record of a K3 sweep (one 32-byte load on the device): v[0] = a_off / 32, v[1] = nk | nkd << 16,
+// v[2] = zrow, v[3] = zidx, v[4] = out, v[5] = nvalid | (first-of-chain) << 8 | (last-of-chain) << 9, v[6] = the
+// first item of the chain after this item's chain on the same CTA is looked up separately (unused), v[7] unused.
+struct alignas(32) int4x2 {
+  int32_t v[8];
+};
+
 // Position of factor element (k, lane) inside a sweep item's block (k padded to a multiple of 4). The block
 // is stored in the fragment order of the fp64 MMA m8n8k4 with output row/col `lane` = 4 g + m (g = lane / 4
 // is the fragment's group, m = lane % 4 its M-tile): for k-group q = k / 4 and half h = m / 2, the 32 lanes
@@ -70,6 +77,7 @@ struct HostPlan {
     std::vector<int32_t> out;          // per item (same for a chain): >= 0: direct output row out + lane;
                                        //   < 0: partial rows (-out-1)*32 + lane
     std::vector<int32_t> nvalid;       // valid lanes
+    std::vector<int4x2> rec;           // per item, packed for one 32-byte device load (see build_solve_schedule)
     std::vector<int32_t> lvl_red;      // [nlevels+1] reduce targets of level l
     std::vector<int32_t> red_row;      // target row (solve position)
     std::vector<int32_t> red_mode;     // 0: dst[row] = sum (y or x), 1: z[row] -= sum

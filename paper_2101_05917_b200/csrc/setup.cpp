@@ -350,6 +350,22 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   }
   for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
     S->chain.push_back((int32_t)S->a_off.size());  // sentinel
+    const size_t ni = S->a_off.size();
+    S->rec.assign(ni, int4x2{});
+    std::vector<uint8_t> first(ni, 0), last(ni, 0);
+    for (size_t c = 0; c + 1 < S->chain.size(); ++c) {
+      first[S->chain[c]] = 1;
+      last[S->chain[c + 1] - 1] = 1;
+    }
+    for (size_t t = 0; t < ni; ++t) {
+      int32_t* v = S->rec[t].v;
+      v[0] = (int32_t)(S->a_off[t] / 32);
+      v[1] = S->nk[t] | (S->nkd[t] << 16);
+      v[2] = S->zrow[t];
+      v[3] = (int32_t)S->zidx[t];
+      v[4] = S->out[t];
+      v[5] = S->nvalid[t] | (first[t] << 8) | (last[t] << 9);
+    }
     S->lvl_kmax.assign(P.nlevels, 0);
     for (int l = 0; l < P.nlevels; ++l)
       for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t)

@@ -99,6 +99,17 @@ int main(int argc, char** argv) {
     for (int p = 0; p < N; ++p)
       if (assigned[p] != 1) { printf("row %d written %d times\n", p, assigned[p]); exit(11); }
   };
+  if (std::getenv("PLAN_LEVELS"))  // per-level schedule statistics (developer aid)
+    for (const HostPlan::Sweep* S : {&P.fw, &P.bw})
+      for (int l = 0; l < P.nlevels; ++l) {
+        int64_t bytes = 0;
+        int lmax = 0;
+        for (int c = S->lvl_chain[l]; c < S->lvl_chain[l + 1]; ++c) lmax = std::max(lmax, S->chain[c + 1] - S->chain[c]);
+        for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) bytes += (int64_t)((S->nk[t] + 3) & ~3) * 256;
+        printf("%s level %2d: items %6d chains %6d longest %2d targets %6d factor MB %7.2f\n", S == &P.fw ? "fw" : "bw", l,
+               S->lvl_item[l + 1] - S->lvl_item[l], S->lvl_chain[l + 1] - S->lvl_chain[l], lmax,
+               S->lvl_red[l + 1] - S->lvl_red[l], bytes / 1e6);
+      }
   run(P.fw, z, y, &z, true);
   run(P.bw, y, x, nullptr, false);
   double err = 0, mx = 0;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--horizon", type=int, default=2)
     ap.add_argument("--set", action="append", default=[])
     ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("--seq", type=int, default=0, help="print the kernels of the first solve (up to N)")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -85,6 +86,14 @@ def main():
     print("| kernel | total ms | count | avg us |")
     for n, (t, c) in sorted(per.items(), key=lambda x: -x[1][0])[:a.top]:
         print(f"| {n} | {t / 1e3:.3f} | {c} | {t / c:.1f} |")
+    if a.seq:
+        first = next(i for i, k in enumerate(kern) if "k_to_solve" in k[2])
+        print("| # | kernel | us | gap before us |")
+        for i in range(first, min(len(kern), first + a.seq)):
+            print(f"| {i - first} | {kern[i][2].split('(')[0].replace('void ', '')[:40]} | {kern[i][1] - kern[i][0]:.1f} | "
+                  f"{kern[i][0] - kern[i - 1][1]:.1f} |")
+            if "k_from_solve" in kern[i][2]:
+                break
     print("| runtime call | total ms | count | avg us |")
     for n, (t, c) in sorted(rt.items(), key=lambda x: -x[1][0])[:12]:
         print(f"| {n} | {t / 1e3:.3f} | {c} | {t / c:.1f} |")
