@@ -95,6 +95,10 @@ typedef struct {
   int32_t x0_predict;     /* 1: start each step's solve from x_i + h v_i instead of x_i (converged
                              configurations only; fixed_iter keeps x^0 = x_i, reading §2.6).
                              Changes iteration counts, not the converged minimiser          */
+  int32_t lbfgs_warm;     /* accel_fwd = 1 with contact: 1 keeps the L-BFGS curvature pairs across the Alg. 1
+                             outer iterations of a time step (restricted to the new free DoFs, Gram matrix
+                             recomputed); 0 restarts the history with every corrector solve.  Changes
+                             iteration counts, not the converged minimiser   */
 } pd_options;
 
 /* Per-step statistics, caller-owned HOST arrays of length B*steps (index

@@ -51,7 +51,8 @@ class Simulator:
                  fixed_dofs=(), contact_nodes=(), muscle_w=0.0, fiber=(1.0, 0.0, 0.0),
                  tol_fwd=1e-9, tol_adj=1e-9, max_iter_fwd=20000, max_iter_adj=20000, fixed_iter=0,
                  accel_fwd=1, accel_adj=1, check_every=1, max_batch=1, max_steps=1, youngs_ref=0.0,
-                 max_outer=10, eps_phi=None, profile=0, outer_warm=1, x0_predict=0, contact_mode=1):
+                 max_outer=10, eps_phi=None, profile=0, outer_warm=1, x0_predict=0, contact_mode=1,
+                 lbfgs_warm=0):
         self.lib = _lib.load()
         rest = np.ascontiguousarray(rest, dtype=np.float64)
         hex8 = np.ascontiguousarray(hex8, dtype=np.int32)
@@ -69,7 +70,7 @@ class Simulator:
                              check_every, max_batch, max_steps, youngs_ref,
                              cand.ctypes.data_as(_lib.ip) if len(cand) else None, len(cand), max_outer,
                              float(1e-6 * dx if eps_phi is None else eps_phi), int(profile), int(outer_warm),
-                             int(contact_mode), int(x0_predict))
+                             int(contact_mode), int(x0_predict), int(lbfgs_warm))
         h_ = C.c_void_p()
         st = self.lib.pd_create(C.byref(mesh), C.byref(mat), float(h),
                                 fixed.ctypes.data_as(_lib.ip) if len(fixed) else None, len(fixed),

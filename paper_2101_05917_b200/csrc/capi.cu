@@ -49,7 +49,9 @@ struct pd_sim {
   uint8_t* d_fixed = nullptr;
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
-  int k3_mma = 1;  // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
+  int k3_mma = 1;   // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
+  int k3_nbuf = 2;  // K3 item ring depth (2..4, env PD_K3_NBUF)
+  int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
   // work
@@ -252,7 +254,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     const int ch0 = S.lvl_chain[j], nch = S.lvl_chain[j + 1] - ch0;
     if (nch > 0) {
       const int kp = kpad_of(S.lvl_kmax[j]);
-      const int nbuf = 2;  // measured: 2 buffers x several CTAs/SM beats deeper rings with 1 CTA/SM
+      const int nbuf = s->k3_nbuf;  // ring depth (default 2: 2 buffers x several CTAs/SM)
       const int smem = nbuf * kp * (32 + RC) * 8;
       const unsigned gx = (unsigned)std::min<int64_t>(nch, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
@@ -485,7 +487,7 @@ void build_Q(pd_sim* s, int B, const int32_t* sel) {
 
 // Forward quasi-Newton PD (P:79, P:254-271 applied to eq:opt): L-BFGS on g with H0 = A^{-1} (the
 // constrained prefactorised solve) and Armijo backtracking; per-sim masks; history slots shared by index.
-void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base) {
+void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base, bool warm) {
   const HostPlan& P = s->plan;
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
@@ -499,8 +501,25 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
   // on y only: constant over the solve)
   dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
   double* const gn2 = s->inert + B;  // |grad g(x_trial)|^2, from eval_f
-  int hist = 0;
-  for (int iter = 0;; ++iter) {
+  // ring position gi (slot of the next pair = gi % m) and valid pairs; kept across the Alg. 1 outer iterations
+  // of a step when warm (lbfgs_warm): the pairs are restricted to the new free DoFs and their Gram matrix and
+  // rho recomputed (pairs with s^T y <= 0 drop out through rho = 0)
+  int hist = warm ? s->lb_hist : 0;
+  const int gi0 = warm ? s->lb_gi : 0;
+  if (hist > 0) {
+    for (int j = 0; j < hist; ++j) {
+      zero_constrained(s, LSs(j), B);
+      zero_constrained(s, LYs(j), B);
+    }
+    for (int j = 0; j < hist; ++j) {
+      mdot(s, B, LSs(j), s->LY, hist, s->lb_da, LYs(j), s->LS);
+      k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)hist * B, j, m,
+                                                      hist, B, s->active, nullptr, nullptr, nullptr, nullptr);
+      LAUNCH_CHECK(s);
+    }
+  }
+  int gi = gi0;
+  for (int iter = 0;; ++iter, ++gi) {
     // convergence check; also alpha = 1 and ls_act = active for the coming line search
     k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
@@ -511,7 +530,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
-      k_lbfgs_alpha<<<B, 32, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, iter, B, s->active);
+      k_lbfgs_alpha<<<B, 32, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, gi, B, s->active);
       LAUNCH_CHECK(s);
       k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
                                                      s->active);  // q = g - sum alpha_j y_j
@@ -522,7 +541,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);  // r0 = H0 q = A^{-1} q
     if (hist > 0) {
       mdot(s, B, s->Dv, s->LY, hist, s->lb_yr);
-      k_lbfgs_beta<<<B, 32, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, iter, B,
+      k_lbfgs_beta<<<B, 32, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, gi, B,
                                                       s->active);
       LAUNCH_CHECK(s);
       k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,
@@ -545,7 +564,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     }
     // curvature pair (s, y) into slot iter % m and commit x, grad g (one pass); Gram row/column of the new
     // pair (both multi-dots in one pass); f, |grad g|^2
-    const int slot = iter % m;
+    const int slot = gi % m;
     k_lbfgs_commit<<<nblk(len), 256, 0, s->stream>>>(LSs(slot), LYs(slot), s->X, s->G, s->Xn, s->Gn, len, B, s->active);
     LAUNCH_CHECK(s);
     const int nv = std::min(hist + 1, m);  // valid slots after this store are [0, nv)
@@ -555,6 +574,8 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     LAUNCH_CHECK(s);
     hist = nv;
   }
+  s->lb_hist = hist;
+  s->lb_gi = gi;
 }
 
 }  // namespace
@@ -649,6 +670,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       d.red_src = s->upload(S.red_src);
     };
     if (const char* e = std::getenv("PD_K3_MMA")) s->k3_mma = std::atoi(e) ? 1 : 0;
+    if (const char* e = std::getenv("PD_K3_NBUF")) s->k3_nbuf = std::min(4, std::max(2, std::atoi(e)));
     up_sweep(P.fw, s->swf);
     up_sweep(P.bw, s->swb);
     s->Spart = s->alloc<double>((std::max(P.fw.max_partial_rows, P.bw.max_partial_rows) + 32) * 3 * s->Bmax);
@@ -844,7 +866,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           LAUNCH_CHECK(s);
         }
         if (s->opt.accel_fwd && s->opt.fixed_iter <= 0) {
-          inner_lbfgs(s, B, i, act_i, act_bs, contact ? s->it_base : nullptr);
+          inner_lbfgs(s, B, i, act_i, act_bs, contact ? s->it_base : nullptr, s->opt.lbfgs_warm && outer > 1);
         } else {
           for (int iter = 0;; ++iter) {
             residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);

@@ -1575,8 +1575,10 @@ __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, 
   }
   const double sy = da[sl * B + b];
   rho[sl * B + b] = sy > 0.0 ? 1.0 / sy : 0.0;
-  f[b] = fn[b];
-  gg[b] = gn2[b];
+  if (f) {
+    f[b] = fn[b];
+    gg[b] = gn2[b];
+  }
 }
 
 // commit of an accepted L-BFGS step (one pass): S_sl = Xn - X, Y_sl = Gn - G, X = Xn, G = Gn (masked)

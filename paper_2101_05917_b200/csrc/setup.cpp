@@ -243,7 +243,8 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
     return bases;
   };
   constexpr int kChainNoSplit = 4;  // outputs of <= 4 items stay on one CTA in the backward sweep
-  auto chain_cap = [&](int64_t items) { return (int)std::max<int64_t>(1, (items + P.chain_ctas - 1) / P.chain_ctas); };
+  // chains only where a level has many more items than CTAs (fewer partial rows, still >= 4 items per CTA)
+  auto chain_cap = [&](int64_t items) { return (int)std::max<int64_t>(1, items / (4 * (int64_t)P.chain_ctas)); };
   auto close_level = [&](HostPlan::Sweep& S, int64_t prow,
                          std::vector<std::tuple<int32_t, int32_t, std::vector<int32_t>>>& targets) {
     // targets (row, mode, partial rows in summation order), sorted by row: the level's reduce
@@ -350,6 +351,44 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   }
   for (HostPlan::Sweep* S : {&P.fw, &P.bw}) {
     S->chain.push_back((int32_t)S->a_off.size());  // sentinel
+    // Within a level, chains are independent: lay them out longest first, so that the static round-robin
+    // assignment (CTA c takes chains c, c + G, ...) gives every CTA one of the long chains before any gets a
+    // second chain (balance without knowing G).  Items move with their chain; outputs are unchanged.
+    {
+      HostPlan::Sweep T = *S;
+      T.A.clear();
+      T.a_off.clear();
+      T.nk.clear();
+      T.nkd.clear();
+      T.zrow.clear();
+      T.zidx.clear();
+      T.out.clear();
+      T.nvalid.clear();
+      T.chain.clear();
+      for (int l = 0; l < P.nlevels; ++l) {
+        std::vector<int32_t> order;
+        for (int c = S->lvl_chain[l]; c < S->lvl_chain[l + 1]; ++c) order.push_back(c);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+          return S->chain[x + 1] - S->chain[x] > S->chain[y + 1] - S->chain[y];
+        });
+        for (int32_t c : order) {
+          T.chain.push_back((int32_t)T.a_off.size());
+          for (int t = S->chain[c]; t < S->chain[c + 1]; ++t) {
+            const int64_t len = (int64_t)((S->nk[t] + 3) & ~3) * L;
+            T.a_off.push_back((int64_t)T.A.size());
+            T.A.insert(T.A.end(), S->A.begin() + S->a_off[t], S->A.begin() + S->a_off[t] + len);
+            T.nk.push_back(S->nk[t]);
+            T.nkd.push_back(S->nkd[t]);
+            T.zrow.push_back(S->zrow[t]);
+            T.zidx.push_back(S->zidx[t]);
+            T.out.push_back(S->out[t]);
+            T.nvalid.push_back(S->nvalid[t]);
+          }
+        }
+      }
+      T.chain.push_back((int32_t)T.a_off.size());
+      *S = std::move(T);
+    }
     const size_t ni = S->a_off.size();
     S->rec.assign(ni, int4x2{});
     std::vector<uint8_t> first(ni, 0), last(ni, 0);

@@ -106,6 +106,12 @@ int main(int argc, char** argv) {
         int lmax = 0;
         for (int c = S->lvl_chain[l]; c < S->lvl_chain[l + 1]; ++c) lmax = std::max(lmax, S->chain[c + 1] - S->chain[c]);
         for (int t = S->lvl_item[l]; t < S->lvl_item[l + 1]; ++t) bytes += (int64_t)((S->nk[t] + 3) & ~3) * 256;
+        int single = 0, srcs = 0;
+        for (int r = S->lvl_red[l]; r < S->lvl_red[l + 1]; ++r) {
+          single += S->red_ptr[r + 1] - S->red_ptr[r] == 1;
+          srcs += S->red_ptr[r + 1] - S->red_ptr[r];
+        }
+        printf("   single-source targets %d of %d, sources %d  ", single, S->lvl_red[l + 1] - S->lvl_red[l], srcs);
         printf("%s level %2d: items %6d chains %6d longest %2d targets %6d factor MB %7.2f\n", S == &P.fw ? "fw" : "bw", l,
                S->lvl_item[l + 1] - S->lvl_item[l], S->lvl_chain[l + 1] - S->lvl_chain[l], lmax,
                S->lvl_red[l + 1] - S->lvl_red[l], bytes / 1e6);

@@ -209,13 +209,13 @@ def test_bitwise_determinism(torch):
 
 
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
-def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, **over):
+def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for
     # position agreement near the fp64 floor of the residual metric (~1e-14); the forward therefore
     # runs to 2e-14 here (measured: tools/contact_diag.py).
     inp = make_inputs(get_config(name, **over))
-    sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd, outer_warm=outer_warm, tol_fwd=2e-14,
-               max_iter_fwd=4000)
+    sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd, outer_warm=outer_warm,
+               lbfgs_warm=lbfgs_warm, tol_fwd=2e-14, max_iter_fwd=4000)
     gpu = _run_gpu(torch, inp, sim)
     sets = sim.contact_sets()
     # (sticky nodes under random actuation can make Alg. 1 cycle until its outer cap; such steps are flagged on
@@ -244,17 +244,17 @@ def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, **over):
     _compare(inp, gpu, range(inp["B"]))
 
 
-@pytest.mark.parametrize("accel_fwd,outer_warm", [(0, 0), (1, 1)])
-def test_c4s_contact_drop_parity(torch, accel_fwd, outer_warm):
+@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1)])
+def test_c4s_contact_drop_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
     # BASELINE.json configs[3] recipe at oracle size: tilted plate dropped on z = 0, frictionless LCP.
-    # (0, 0) = literal Alg. 1 (plain PD corrector restarted from x_i); (1, 1) = the fast defaults.
-    _contact_parity(torch, "c4s", accel_fwd, outer_warm)
+    # (0, 0, 0) = literal Alg. 1 (plain PD corrector restarted from x_i); (1, 1, *) = the fast paths.
+    _contact_parity(torch, "c4s", accel_fwd, outer_warm, lbfgs_warm)
 
 
-@pytest.mark.parametrize("accel_fwd,outer_warm", [(0, 0), (1, 1)])
-def test_c5s_contact_muscle_parity(torch, accel_fwd, outer_warm):
+@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1)])
+def test_c5s_contact_muscle_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
     # configs[4] recipe at oracle size: muscle actuation + bottom-face contact, B = 2.
-    _contact_parity(torch, "c5s", accel_fwd, outer_warm)
+    _contact_parity(torch, "c5s", accel_fwd, outer_warm, lbfgs_warm)
 
 
 def test_contact_deterministic(torch):
