@@ -325,7 +325,7 @@ __device__ __forceinline__ void store_force(const double* Pm, const DNTab& dt, i
   }
 }
 
-__global__ void __launch_bounds__(256) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
+__global__ void __launch_bounds__(256, 4) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                        double* __restrict__ EF, double* __restrict__ EE) {
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
@@ -757,10 +757,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
       : "memory");
   return ok != 0;
 }
-// bounded: a byte-count bug becomes a trap (launch error), never a hung GPU
+// bounded: a byte-count bug becomes a trap (launch error) after ~0.5 s, never a hung GPU
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  for (int64_t i = 0; !mbar_try_wait(bar, parity); ++i)
-    if (i > ((int64_t)1 << 24)) __trap();
+  if (mbar_try_wait(bar, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try_wait(bar, parity)) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 500000000ull) __trap();
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
