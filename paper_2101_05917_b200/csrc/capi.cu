@@ -387,6 +387,16 @@ void set_w(pd_sim* s, int B, const double* youngs_per_sim) {
   CK(cudaStreamSynchronize(s->stream));
 }
 
+// the three counters in one copy: [0] the last k_*_check / k_ls_accept count, [1] the deferred convergence
+// count, [2] running sims already within 16 tol
+void read_nactive3(pd_sim* s, int* a, int* b, int* c) {
+  CK(cudaMemcpyAsync(s->h_nactive, s->nactive, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  prof_flush(s);
+  *a = s->h_nactive[0];
+  *b = s->h_nactive[1];
+  *c = s->h_nactive[2];
+}
 int read_nactive(pd_sim* s) {
   CK(cudaMemcpyAsync(s->h_nactive, s->nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -519,14 +529,24 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     }
   }
   int gi = gi0;
+  bool done = false, check_now = true;  // the first check of a solve is read immediately
   for (int iter = 0;; ++iter, ++gi) {
     // convergence check; also alpha = 1 and ls_act = active for the coming line search
+    // Far from convergence the convergence count is read together with the first line-search decision (one
+    // host sync per iteration instead of two; were every sim to converge meanwhile, the direction and trial
+    // launched after the check are fully masked and the loop ends at that sync).  Once a running sim is within
+    // 16 tol the check is read immediately, so no masked iteration is spent at the end of a solve.
     k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
-                                          s->st_flag_f + (int64_t)i * B, s->nactive, it_base, s->alpha_ls, s->ls_act);
+                                          s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
+                                          s->ls_act, s->nactive + 2);
     LAUNCH_CHECK(s);
     if (iter >= s->opt.max_iter_fwd) break;
-    if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
+    if (check_now) {
+      int a = 0, running = 0, nr = 0;
+      read_nactive3(s, &a, &running, &nr);
+      if (running == 0) break;
+    }
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
@@ -560,8 +580,18 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
       k_ls_accept<<<1, 256, 0, s->stream>>>(s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
                                             s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
       LAUNCH_CHECK(s);
-      if (read_nactive(s) == 0) break;
+      int searching = 0, running = 1, nr = 0;
+      read_nactive3(s, &searching, &running, &nr);
+      if (trial == 0) {
+        if (running == 0) {
+          done = true;
+          break;
+        }
+        check_now = nr > 0;
+      }
+      if (searching == 0) break;
     }
+    if (done) break;
     // curvature pair (s, y) into slot iter % m and commit x, grad g (one pass); Gram row/column of the new
     // pair (both multi-dots in one pass); f, |grad g|^2
     const int slot = gi % m;
@@ -694,7 +724,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
     s->partial = s->alloc<double>(16 * s->max_partial_blocks + 64);  // up to 16 dot families (mdot pairs)
     s->active = s->alloc<int32_t>(s->Bmax);
-    s->nactive = s->alloc<int32_t>(1);
+    s->nactive = s->alloc<int32_t>(3);  // [0] last check / line-search count, [1] deferred convergence count,
+                                        // [2] running sims within 16 tol (next check is immediate)
     s->it_buf = s->alloc<int32_t>(s->Bmax);
     s->flag_buf = s->alloc<int32_t>(s->Bmax);
     const int64_t TB = (int64_t)s->Tmax * s->Bmax;
@@ -707,7 +738,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->st_res_a = s->alloc<double>(TB);
     s->traj = s->alloc<double>((int64_t)(s->Tmax + 1) * n3B);
     s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
-    CK(cudaMallocHost(&s->h_nactive, sizeof(int32_t)));
+    CK(cudaMallocHost(&s->h_nactive, 3 * sizeof(int32_t)));
     CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
     if (s->opt.accel_fwd) {
       s->nhist = 8;

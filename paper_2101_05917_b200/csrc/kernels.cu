@@ -1012,6 +1012,8 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
         const double* rb = redb + r * LD + c;
         if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LD]) + rb[64 * LD]) + rb[96 * LD];
       }
+      // the tile writes (generic proxy) precede the TMA refill of this buffer (async proxy) after the next barrier
+      fence_proxy_async();
     }
     // (the buffer is refilled after the next item's barrier: no barrier needed here)
   }
@@ -1025,11 +1027,15 @@ __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const do
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= (int64_t)ntarget * R) return;
   const int t = r0 + (int)(g / R), c = (int)(g % R);
-  double acc = 0;
-  for (int q = sw.red_ptr[t]; q < sw.red_ptr[t + 1]; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  // all independent loads first (target row, mode, source range, the z value), then the fixed-order sum
+  const int q0 = sw.red_ptr[t], q1 = sw.red_ptr[t + 1], mode = sw.red_mode[t];
   const int64_t o = (int64_t)sw.red_row[t] * R + c;
-  if (sw.red_mode[t] == 0) dst_assign[o] = acc;
-  else dst_sub[o] -= acc;
+  const double zo = mode == 0 ? 0.0 : dst_sub[o];
+  double acc = 0;
+#pragma unroll 4
+  for (int q = q0; q < q1; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  if (mode == 0) dst_assign[o] = acc;
+  else dst_sub[o] = zo - acc;
 }
 
 // ----------------------------------------------------------------- K5: contact
@@ -1623,9 +1629,10 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out,
                             int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base,
-                            double* __restrict__ alpha = nullptr, int32_t* __restrict__ ls_act = nullptr) {
-  __shared__ int cnt;
-  if (threadIdx.x == 0) cnt = 0;
+                            double* __restrict__ alpha = nullptr, int32_t* __restrict__ ls_act = nullptr,
+                            int32_t* __restrict__ nnear = nullptr) {
+  __shared__ int cnt, near;
+  if (threadIdx.x == 0) cnt = near = 0;
   __syncthreads();
   for (int b = threadIdx.x; b < B; b += blockDim.x) {
     int act = active[b];
@@ -1642,6 +1649,7 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
         flag_out[b] = (fixed_iter == 0 && res > tol) ? 1 : 0;
       } else {
         atomicAdd(&cnt, 1);  // integer count only (no effect on arithmetic)
+        if (res < 16.0 * tol) atomicAdd(&near, 1);
       }
     }
     if (alpha) {
@@ -1650,7 +1658,10 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *nactive = cnt;
+  if (threadIdx.x == 0) {
+    *nactive = cnt;
+    if (nnear) *nnear = near;
+  }
 }
 
 // v = (x - xprev)/h

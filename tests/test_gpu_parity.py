@@ -208,6 +208,32 @@ def test_bitwise_determinism(torch):
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("env", [{"PD_K3_MMA": "0"}, {"PD_K3_NBUF": "3"}, {"PD_K3_NBUF": "4"}])
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+def test_k3_switches_match_direct(torch, monkeypatch, env, name):
+    # The K3 switches read at pd_create (FMA-pipe item product, deeper TMA rings) give the same A^{-1}
+    # as a direct sparse solve (c3s: odd 3B -> the non-TMA right-hand-side path; c5s: contact ordering).
+    import scipy.sparse.linalg as spla
+    from oracle import pd
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inp = make_inputs(get_config(name))
+    B = inp["B"]
+    sim = _sim(inp, youngs_ref=float(np.max(inp["youngs"])))
+    rhs = np.random.default_rng(4).standard_normal((B, 3 * inp["n_nodes"]))
+    out = torch.zeros_like(to_dev(rhs))
+    sim.apply_Ainv(to_dev(rhs), out)
+    out = out.cpu().numpy()
+    sc = pd.scene_from_inputs(inp)
+    w_ref = (np.max(inp["youngs"]) if inp["cfg"].per_sim_youngs else inp["cfg"].youngs) / (1 + sc.poisson)
+    A = sc.A(w_ref)
+    fr = sc.free
+    for b in range(B):
+        ref = np.zeros(sc.N)
+        ref[fr] = spla.spsolve(A[fr][:, fr].tocsc(), rhs[b][fr])
+        assert rel(out[b], ref) <= 1e-12
+
+
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
 def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 200 python tools/timeline.py c5 --horizon 1 > gpurun_out/tl_c5.txt 2>&1; head -4 gpurun_out/tl_c5.txt | grep -E "span"
+timeout 200 python tools/timeline.py c3 --horizon 2 > gpurun_out/tl_c3.txt 2>&1; head -4 gpurun_out/tl_c3.txt | grep -E "span"
