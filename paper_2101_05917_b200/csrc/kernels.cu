@@ -1007,10 +1007,37 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
       const int nv = md.z;
       double* __restrict__ dst =
           out >= 0 ? direct + (int64_t)out * R + c0 : partial + (int64_t)(-out - 1) * 32 * R + c0;
-      for (int e = tid; e < nv * RC; e += 128) {
-        const int r = e / RC, c = e - r * RC;
-        const double* rb = redb + r * LD + c;
-        if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LD]) + rb[64 * LD]) + rb[96 * LD];
+      if constexpr (RC % 2 == 0) {
+        // column pairs: thread = (row slot, pair); 128-bit tile loads, 128-bit stores when the row stride allows
+        constexpr int CP = RC / 2, RPP = 128 / CP;  // pairs per row, rows per pass
+        const int cp = tid % CP, rs = tid / CP, c = 2 * cp;
+        const bool st2 = (R & 1) == 0;
+        if (rs < RPP)
+          for (int r = rs; r < nv; r += RPP) {
+            const double* rb = redb + r * LD + c;
+            const double2 t0 = *reinterpret_cast<const double2*>(rb);
+            const double2 t1 = *reinterpret_cast<const double2*>(rb + 32 * LD);
+            const double2 t2 = *reinterpret_cast<const double2*>(rb + 64 * LD);
+            const double2 t3 = *reinterpret_cast<const double2*>(rb + 96 * LD);
+            const double v0 = ((t0.x + t1.x) + t2.x) + t3.x, v1 = ((t0.y + t1.y) + t2.y) + t3.y;
+            double* d = dst + (int64_t)r * R + c;
+            if (c + 1 < rcn) {
+              if (st2) {
+                *reinterpret_cast<double2*>(d) = make_double2(v0, v1);
+              } else {
+                d[0] = v0;
+                d[1] = v1;
+              }
+            } else if (c < rcn) {
+              d[0] = v0;
+            }
+          }
+      } else {
+        for (int e = tid; e < nv * RC; e += 128) {
+          const int r = e / RC, c = e - r * RC;
+          const double* rb = redb + r * LD + c;
+          if (c < rcn) dst[(int64_t)r * R + c] = ((rb[0] + rb[32 * LD]) + rb[64 * LD]) + rb[96 * LD];
+        }
       }
       // the tile writes (generic proxy) precede the TMA refill of this buffer (async proxy) after the next barrier
       fence_proxy_async();
