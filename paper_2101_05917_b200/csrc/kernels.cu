@@ -802,7 +802,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
       : "d"(a), "d"(b));
 }
 template <int RC, bool VEC, bool MMA>
-__global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, int nchains, int R,
+__global__ void __launch_bounds__(128, RC <= 24 ? 4 : 3) k_sweep_level(SweepDev sw, int ch0, int nchains, int R,
                                                         const double* __restrict__ zc, const double* __restrict__ zi,
                                                         const int32_t* __restrict__ rows, double* __restrict__ direct,
                                                         double* __restrict__ partial, int kmax, int nbuf) {
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_level(SweepDev sw, int ch0, in
     double* redb = sm + slot * bufd;
     if constexpr (MMA) {
       const int g = lane >> 2, t = lane & 3;
-      constexpr int NU = NT <= 3 ? 2 : 1;  // second set only when it fits in registers
+      constexpr int NU = 1;  // one accumulator set: fewer registers, 4 CTAs/SM for RC <= 24 (measured faster than 2 sets at 3/SM)
       if (first) {
 #pragma unroll
         for (int u = 0; u < 2; ++u)
