@@ -75,7 +75,8 @@ typedef struct {
                              1: its quasi-Newton acceleration, run as
                              A-preconditioned CG — BFGS with exact line search on a(u)   */
   int32_t check_every;    /* host polls convergence flags every k iterations (>= 1)        */
-  int32_t max_batch;      /* largest B passed to pd_forward                                */
+  int32_t max_batch;      /* largest B passed to pd_forward; at most 256 (the solve splits the 3B right-hand
+                             sides into <= 16 column chunks of 48; pd_create returns INVALID_ARGUMENT above) */
   int32_t max_steps;      /* largest `steps` passed to pd_forward (trajectory store size)  */
   double youngs_ref;      /* Young's modulus of the ONE factorised A (0 = material.youngs).
                              Sims with other E use the majorising step of DESIGN.md §2.12  */
