@@ -722,7 +722,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->dots = s->alloc<double>(3 * s->Bmax);
     for (int b = 1; b <= s->Bmax; ++b)
       s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
-    s->partial = s->alloc<double>(16 * s->max_partial_blocks + 64);  // up to 16 dot families (mdot pairs)
+    s->partial = s->alloc<double>(32 * s->max_partial_blocks + 64);  // up to 2 x 16 dot families (mdot pairs)
     s->active = s->alloc<int32_t>(s->Bmax);
     s->nactive = s->alloc<int32_t>(3);  // [0] last check / line-search count, [1] deferred convergence count,
                                         // [2] running sims within 16 tol (next check is immediate)
@@ -741,7 +741,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     CK(cudaMallocHost(&s->h_nactive, 3 * sizeof(int32_t)));
     CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
     if (s->opt.accel_fwd) {
-      s->nhist = 8;
+      s->nhist = 8;  // L-BFGS memory (env PD_LBFGS_M, 1..16)
+      if (const char* e = std::getenv("PD_LBFGS_M")) s->nhist = std::min(16, std::max(1, std::atoi(e)));
       s->LS = s->alloc<double>(s->nhist * n3B);
       s->LY = s->alloc<double>(s->nhist * n3B);
       s->Dv = s->alloc<double>(n3B);

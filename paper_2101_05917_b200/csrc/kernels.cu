@@ -1522,6 +1522,7 @@ __global__ void k_mdot_partial(const double* __restrict__ u, const double* __res
   block_sim_sums(red, 1, B, partial + (int64_t)jp * gridDim.x * B, gridDim.x, blockIdx.x);
 }
 
+constexpr int kMaxHist = 16;  // largest L-BFGS memory the two-loop kernels support
 // slot of the k-th newest pair at iteration `iter` (ring of m)
 __device__ __forceinline__ int lb_slot(int iter, int k, int m) { return ((iter - 1 - k) % m + m) % m; }
 
@@ -1529,7 +1530,7 @@ __device__ __forceinline__ int lb_slot(int iter, int k, int m) { return ((iter -
 __global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __restrict__ Gm, const double* __restrict__ rho,
                               double* __restrict__ alpha, int m, int hist, int iter, int B,
                               const int32_t* __restrict__ active) {
-  __shared__ double g[64], sv[8], rv[8], av[8];
+  __shared__ double g[kMaxHist * kMaxHist], sv[kMaxHist], rv[kMaxHist], av[kMaxHist];
   const int b = blockIdx.x, lane = threadIdx.x;
   if (!active[b]) return;
   for (int i = lane; i < m * m; i += 32) g[i] = Gm[(int64_t)i * B + b];
@@ -1558,7 +1559,7 @@ __global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __res
 __global__ void k_lbfgs_beta(const double* __restrict__ yr, const double* __restrict__ Gm, const double* __restrict__ rho,
                              const double* __restrict__ alpha, double* __restrict__ beta, int m, int hist, int iter,
                              int B, const int32_t* __restrict__ active) {
-  __shared__ double g[64], yv[8], rv[8], av[8], bv[8];
+  __shared__ double g[kMaxHist * kMaxHist], yv[kMaxHist], rv[kMaxHist], av[kMaxHist], bv[kMaxHist];
   const int b = blockIdx.x, lane = threadIdx.x;
   if (!active[b]) return;
   for (int i = lane; i < m * m; i += 32) g[i] = Gm[(int64_t)i * B + b];
