@@ -325,7 +325,7 @@ __device__ __forceinline__ void store_force(const double* Pm, const DNTab& dt, i
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
+__global__ void __launch_bounds__(256, 5) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                        double* __restrict__ EF, double* __restrict__ EE) {
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
