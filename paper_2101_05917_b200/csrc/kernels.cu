@@ -678,10 +678,27 @@ __global__ void k_gather(const double* __restrict__ X, const double* __restrict_
   const bool fx = fixed[node] != 0;
   const int pos = pos_of_node[node];
   const int cj = cand_of_node ? cand_of_node[node] : -1;
+  // the <= 8 incident (element, corner) slots of a hex-mesh node: indices first, then all 24 loads in flight,
+  // summed in element order (the order of the CSR, so the result is the same as a sequential loop)
+  const int cnt = k1 - k0;
+  int ec[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) ec[k] = k < cnt ? inc_ec[k0 + k] : 0;
+  double vv[3][8];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) vv[ax][k] = k < cnt ? EF[((int64_t)ec[k] * 3 + ax) * B + b] : 0.0;
   for (int ax = 0; ax < 3; ++ax) {
     const int64_t i = (3 * (int64_t)node + ax) * B + b;
     double s = 0;
-    for (int k = k0; k < k1; ++k) s += EF[((int64_t)inc_ec[k] * 3 + ax) * B + b];
+    if (cnt <= 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < cnt) s += vv[ax][k];
+    } else {
+      for (int k = k0; k < k1; ++k) s += EF[((int64_t)inc_ec[k] * 3 + ax) * B + b];
+    }
     double g = mode == 0 ? mh * (X[i] - Y[i]) + s : mh * X[i] + s;
     double wv = mode == 0 ? mh * Y[i] : 0.0;
     bool pinned = false;
