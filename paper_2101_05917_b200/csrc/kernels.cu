@@ -1075,9 +1075,19 @@ __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const do
   const int q0 = sw.red_ptr[t], q1 = sw.red_ptr[t + 1], mode = sw.red_mode[t];
   const int64_t o = (int64_t)sw.red_row[t] * R + c;
   const double zo = mode == 0 ? 0.0 : dst_sub[o];
+  // sources in batches of 4: indices, then the 4 partial loads in flight, then the in-order sum
   double acc = 0;
-#pragma unroll 4
-  for (int q = q0; q < q1; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  int q = q0;
+  for (; q + 4 <= q1; q += 4) {
+    const int s0 = sw.red_src[q], s1 = sw.red_src[q + 1], s2 = sw.red_src[q + 2], s3 = sw.red_src[q + 3];
+    const double p0 = partial[(int64_t)s0 * R + c], p1 = partial[(int64_t)s1 * R + c];
+    const double p2 = partial[(int64_t)s2 * R + c], p3 = partial[(int64_t)s3 * R + c];
+    acc += p0;
+    acc += p1;
+    acc += p2;
+    acc += p3;
+  }
+  for (; q < q1; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
   if (mode == 0) dst_assign[o] = acc;
   else dst_sub[o] = zo - acc;
 }
