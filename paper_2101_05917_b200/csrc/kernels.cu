@@ -1543,8 +1543,18 @@ __global__ void k_mdot_partial(const double* __restrict__ u, const double* __res
   const double* __restrict__ uu = second ? u2 : u;
   const double* __restrict__ V = (second ? V2base : Vbase) + (int64_t)(second ? jp - nv : jp) * vstride;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
+  // four elements per trip: all eight loads in flight, then the in-order accumulation
   double acc = 0.0;
-  for (int64_t i = beg + threadIdx.x; i < end; i += nb) acc += uu[i] * V[i];
+  int64_t i = beg + threadIdx.x;
+  for (; i + 3 * nb < end; i += 4 * nb) {
+    const double a0 = uu[i], a1 = uu[i + nb], a2 = uu[i + 2 * nb], a3 = uu[i + 3 * nb];
+    const double b0 = V[i], b1 = V[i + nb], b2 = V[i + 2 * nb], b3 = V[i + 3 * nb];
+    acc += a0 * b0;
+    acc += a1 * b1;
+    acc += a2 * b2;
+    acc += a3 * b3;
+  }
+  for (; i < end; i += nb) acc += uu[i] * V[i];
   red[threadIdx.x] = acc;
   block_sim_sums(red, 1, B, partial + (int64_t)jp * gridDim.x * B, gridDim.x, blockIdx.x);
 }
