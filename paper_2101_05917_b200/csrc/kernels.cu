@@ -1388,10 +1388,26 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, dou
   const int nb = blockDim.x;
   const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
   double acc[3] = {0, 0, 0};
-  for (int64_t i = beg + threadIdx.x; i < end; i += nb)
+  int64_t i = beg + threadIdx.x;
+  for (; i + nb < end; i += 2 * nb) {  // two elements per trip: loads first, then the in-order fma chain
+    double u0[3], v0[3], u1[3], v1[3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      u0[p] = p < da.npairs ? da.u[p][i] : 0.0;
+      u1[p] = p < da.npairs ? da.u[p][i + nb] : 0.0;
+      v0[p] = (p < da.npairs && da.v[p]) ? da.v[p][i] : 1.0;
+      v1[p] = (p < da.npairs && da.v[p]) ? da.v[p][i + nb] : 1.0;
+    }
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      acc[p] = fma(u0[p], v0[p], acc[p]);
+      acc[p] = fma(u1[p], v1[p], acc[p]);
+    }
+  }
+  for (; i < end; i += nb)
 #pragma unroll
     for (int p = 0; p < 3; ++p)
-      if (p < da.npairs) acc[p] += da.v[p] ? da.u[p][i] * da.v[p][i] : da.u[p][i];
+      if (p < da.npairs) acc[p] = fma(da.u[p][i], da.v[p] ? da.v[p][i] : 1.0, acc[p]);
 #pragma unroll
   for (int p = 0; p < 3; ++p)
     if (p < da.npairs) red[p * nb + threadIdx.x] = acc[p];
