@@ -210,7 +210,7 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   const int bd = B * std::max(1, 256 / B);
   k_dot_partial<<<nchunk, bd, p * bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk((int64_t)(p * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
+  k_dot_final<<<p * B, 128, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
 }
 
@@ -416,7 +416,7 @@ void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double
   k_mdot_partial<<<dim3(nchunk, np), bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk,
                                                                            s->partial, u2, V2base);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk((int64_t)(np * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, np, out);
+  k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, out);
   LAUNCH_CHECK(s);
 }
 
@@ -436,7 +436,7 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
                                                                          B, chunk, s->partial,
                                                                          with_gn2 ? Gout : nullptr);
   LAUNCH_CHECK(s);
-  k_dot_final<<<nblk((int64_t)(np * B) * 32, 256), 256, 0, s->stream>>>(s->partial, nchunk, B, np, s->inert);
+  k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, s->inert);
   LAUNCH_CHECK(s);
   dots(s, B, P.m, {{s->EE, nullptr}}, s->esum);
   if (fout) {

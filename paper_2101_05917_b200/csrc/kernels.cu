@@ -1414,26 +1414,33 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, dou
   block_sim_sums(red, da.npairs, B, partial, gridDim.x, blockIdx.x);
 }
 // one warp per (pair, sim): lane l sums chunks l, l+32, ... in order, then a fixed xor tree (deterministic)
-__global__ void k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs, double* __restrict__ out,
-                            int accumulate = 0) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// one 128-thread block per (pair, sim): thread t sums chunks t, t+128, ... with 4 independent accumulators (loads
+// in flight together), then a fixed xor tree per warp and the 4 warp sums in warp order (deterministic)
+__global__ void __launch_bounds__(128) k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs,
+                                                   double* __restrict__ out, int accumulate = 0) {
+  const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (i >= npairs * B) return;
   const int p = i / B, b = i - p * B;
-  // 4 independent accumulators (loads in flight together), combined in a fixed order
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   const double* pp = partial + (int64_t)p * nchunk * B + b;
-  int c = lane;
-  for (; c + 96 < nchunk; c += 128) {
+  int c = tid;
+  for (; c + 384 < nchunk; c += 512) {
     s0 += pp[(int64_t)c * B];
-    s1 += pp[(int64_t)(c + 32) * B];
-    s2 += pp[(int64_t)(c + 64) * B];
-    s3 += pp[(int64_t)(c + 96) * B];
+    s1 += pp[(int64_t)(c + 128) * B];
+    s2 += pp[(int64_t)(c + 256) * B];
+    s3 += pp[(int64_t)(c + 384) * B];
   }
-  for (; c < nchunk; c += 32) s0 += pp[(int64_t)c * B];
+  for (; c < nchunk; c += 128) s0 += pp[(int64_t)c * B];
   double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[i] = accumulate ? out[i] + s : s;
+  __shared__ double ws[4];
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (tid == 0) {
+    const double t = ((ws[0] + ws[1]) + ws[2]) + ws[3];
+    out[i] = accumulate ? out[i] + t : t;
+  }
 }
 // sum over elements of E[e][b] (deterministic) -> out[b] (+= if accumulate)
 __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* __restrict__ out, int accumulate) {
