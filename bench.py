@@ -7,10 +7,13 @@ K5]) followed by pd_backward (adjoint PCG with K4 + K3, parameter terms) — SUR
 metric = (sims x time steps x DoF) / second (BASELINE.json "PD sim-steps/sec (forward+backward)
 x DoF per B200"), DoF = 3 n (all nodal DoFs, as the configs quote them).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-N > 1 (torchrun): each rank runs its own B sims (weak scaling, no data-path collective;
-DESIGN.md §6); the time is the max over ranks.
+Default workload: c5 (BASELINE.json configs[4], 8 x 212k-DoF actuated robots with contact), the largest
+single-GPU configuration and the one the north star's roofline target names.
+N > 1 (torchrun): the configured batch is partitioned over the ranks (shard.shard_inputs: contiguous blocks of
+sims, the shared factor's E_ref fixed from the whole batch) with no data-path collective; the time is the max
+over ranks and `value` = the whole batch's DoF*steps / that time (total work fixed: "strong").
 """
 from __future__ import annotations
 
@@ -42,11 +45,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--horizon", type=int, default=0, help="override T (time steps per trajectory)")
     ap.add_argument("--tol", type=float, default=0.0, help="override forward/adjoint tolerance")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3, help="timed iterations of the end-to-end leg (<= --steps)")
     ap.add_argument("--set", action="append", default=[], help="config override key=value (e.g. contact=False)")
     return ap.parse_args()
 
@@ -69,27 +73,60 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- oracle (CPU)
-def oracle_sample(cfg, sample_steps, sims=1):
-    """Time the oracle as it stands (forward + backward) on a bounded sample of the workload."""
-    import resource
+# Bounded samples of each workload for the oracle timings (cpu_baseline, --impl reference): (grid override or
+# None, sims, time steps).  c5's full grid costs the oracle minutes per sim-step (Newton with PCG),
+# so its sample is the c5 recipe (contact + muscle, same h, material, seeds) on a 16x8x8 sub-grid.
+CPU_SAMPLES = {"c5": ((16, 8, 8), 8, 1), "c3": (None, 8, 2), "c4": (None, 1, 2), "c2": (None, 1, 2),
+               "c1": (None, 1, 10)}
+
+
+def _oracle_one(args):
+    """One oracle sim of a sample: forward + backward as they stand (worker process)."""
+    name, counts, sims, steps, b = args
+    import dataclasses
     from oracle import adjoint, pd
-    inp = make_inputs(cfg, batch=sims, steps=sample_steps)
-    r0 = resource.getrusage(resource.RUSAGE_SELF)
+    cfg = get_config(name)
+    if counts is not None:
+        cfg = dataclasses.replace(cfg, counts=tuple(counts))
+    inp = make_inputs(cfg, batch=sims, steps=steps)
+    sc = pd.scene_from_inputs(inp)
+    act = None if inp["act"] is None else inp["act"][b]
+    tr = pd.forward(sc, inp["q0"][b], inp["v0"][b], inp["f_ext"][b], inp["youngs"][b], act,
+                    steps=steps, tol=cfg.tol, fixed_iter=cfg.fixed_iter)
+    L, gq, gv = adjoint.loss_and_grad(inp, b, tr["q"][-1], tr["v"][-1])
+    adjoint.backward(sc, tr, inp["youngs"][b], gq, gv, act)
+    return 3 * inp["n_nodes"] * steps
+
+
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        info = dict(l.split(":", 1) for l in out.splitlines() if ":" in l)
+        return " ".join(info.get("Model name", "?").split()), int(info.get("CPU(s)", "0").strip() or 0)
+    except Exception:
+        return "unknown", os.cpu_count() or 0
+
+
+def oracle_sample(cfg, sample_steps=None):
+    """Time the oracle as it stands (forward + backward, the config's tolerance) on a bounded sample of the
+    workload, one sim per worker process on the host's cores (the oracle itself is single-threaded NumPy)."""
+    import multiprocessing as mproc
+    counts, sims, steps = CPU_SAMPLES.get(cfg.name, (None, 1, 2))
+    if sample_steps:
+        steps = sample_steps
+    model, logical = _cpu_model()
+    workers = max(1, min(sims, os.cpu_count() or 1))
+    jobs = [(cfg.name, counts, sims, steps, b) for b in range(sims)]
     t0 = time.perf_counter()
-    for b in range(sims):
-        sc = pd.scene_from_inputs(inp)
-        act = None if inp["act"] is None else inp["act"][b]
-        tr = pd.forward(sc, inp["q0"][b], inp["v0"][b], inp["f_ext"][b], inp["youngs"][b], act,
-                        steps=sample_steps, tol=cfg.tol, fixed_iter=cfg.fixed_iter)
-        L, gq, gv = adjoint.loss_and_grad(inp, b, tr["q"][-1], tr["v"][-1])
-        adjoint.backward(sc, tr, inp["youngs"][b], gq, gv, act)
+    with mproc.get_context("spawn").Pool(workers) as pool:
+        units = sum(pool.map(_oracle_one, jobs))
     wall = time.perf_counter() - t0
-    r1 = resource.getrusage(resource.RUSAGE_SELF)
-    cpu = (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
-    units = sims * sample_steps * 3 * inp["n_nodes"]
-    return dict(value=units / wall, unit=UNIT, cores=max(1, round(cpu / wall)), kind="oracle",
-                sample=f"{sims} sim x {sample_steps} time steps of {cfg.name} (forward+backward, tol {cfg.tol:g})",
-                wall_s=wall)
+    grid = "x".join(map(str, counts or cfg.counts))
+    return dict(value=units / wall, unit=UNIT, cores=workers, kind="oracle",
+                sample=f"{sims} sims x {steps} time steps of {cfg.name}"
+                       f"{' recipe on a ' + grid + ' sub-grid' if counts else ''} (forward+backward, tol {cfg.tol:g}, "
+                       f"{workers} worker processes, one sim each)",
+                host_cpu=model, host_logical_cpus=logical, wall_s=wall)
 
 
 def run_reference(args):
@@ -97,18 +134,18 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = make_cfg(args)
-    walls = []
+    vals = []
     res = None
     for _ in range(args.steps):
-        res = oracle_sample(cfg, args.cpu_sample_steps)
-        walls.append(res["wall_s"])
-    units = 3 * cfg.n_nodes * args.cpu_sample_steps
-    value = units * len(walls) / sum(walls)
+        res = oracle_sample(cfg)
+        vals.append(res["value"])
+    value = float(np.mean(vals))
     line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
-                ms_per_step=1e3 * sum(walls) / len(walls), higher_is_better=True, scaling="weak",
+                ms_per_step=1e3 * res["wall_s"], higher_is_better=True, scaling="strong",
                 vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
                 config=dict(workload=cfg.name, sample=res["sample"]),
-                cpu_baseline=dict(value=value, unit=UNIT, cores=res["cores"], kind="oracle", sample=res["sample"]),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=res["cores"], kind="oracle", sample=res["sample"],
+                                  host_cpu=res["host_cpu"], host_logical_cpus=res["host_logical_cpus"]),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
 
@@ -164,12 +201,13 @@ def main_ours(args):
     dev = torch.device("cuda", local)
     cfg = make_cfg(args)
     T = args.horizon or cfg.steps
-    # weak scaling: every rank simulates its own batch of B sims (seeded per rank)
-    if rank:
-        import dataclasses
-        cfg = dataclasses.replace(cfg, seed=cfg.seed * 1000 + rank)
-    inp = make_inputs(cfg, steps=T)
+    # the configured batch, partitioned over the ranks (E_ref of the shared factor from the whole batch)
+    from paper_2101_05917_b200 import shard
+    inp_all = make_inputs(cfg, steps=T)
+    inp = shard.shard_inputs(inp_all, ws, rank) if ws > 1 else inp_all
     B, N = inp["B"], 3 * inp["n_nodes"]
+    if B < 1:
+        raise SystemExit(f"rank {rank}: --gpus {ws} exceeds the batch of {cfg.name} ({inp_all['B']} sims)")
     t_setup = time.perf_counter()
     sim = pdb.simulator_from_inputs(inp, tol_fwd=cfg.tol, tol_adj=cfg.tol, max_steps=T, profile=1,
                                     check_every=1, accel_fwd=1, outer_warm=1)
@@ -235,10 +273,9 @@ def main_ours(args):
             prof[k] = (a + ms, b + c)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    from paper_2101_05917_b200 import shard
     total_ms = shard.max_over_ranks(total_ms, ws, dev)
     ms_per_step = total_ms / args.steps
-    units = ws * B * T * N
+    units = inp_all["B"] * T * N           # the whole batch (every rank's sims)
     value = units / (ms_per_step / 1e3)
 
     # ---------------- end to end through the public API with host buffers
@@ -257,7 +294,8 @@ def main_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
         e2e_ms = 0.0
-        for _ in range(args.steps):
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(e2e_steps):
             flush.fill_(1.0)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -272,9 +310,9 @@ def main_ours(args):
         e2e_ms = shard.max_over_ranks(e2e_ms, ws, dev)
         # the one end-of-run collective of the sharded path: per-sim losses of every rank
         all_loss = shard.gather_rows(out_loss.to(dev)[:, None], ws)
-        assert all_loss.shape[0] == ws * B
-        e2e = dict(value=units / (e2e_ms / args.steps / 1e3), unit=UNIT, h2d_bytes_per_step=h2d,
-                   d2h_bytes_per_step=d2h)
+        assert all_loss.shape[0] == inp_all["B"]
+        e2e = dict(value=units / (e2e_ms / e2e_steps / 1e3), unit=UNIT, h2d_bytes_per_step=h2d,
+                   d2h_bytes_per_step=d2h, steps=e2e_steps)
 
     # ---------------- rooflines (live CUDA events per kernel family, pd_profile)
     nfree = info["n_free_nodes"]
@@ -320,11 +358,11 @@ def main_ours(args):
     share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
 
     line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=max(3, args.warmup),
-                ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                ms_per_step=ms_per_step, higher_is_better=True, scaling="strong", vs_baseline=None, dtype="f64",
                 data="synthetic",
-                config=dict(workload=cfg.name, batch_per_gpu=B, time_steps=T, dof=N, tol=cfg.tol,
+                config=dict(workload=cfg.name, batch=inp_all["B"], batch_per_gpu=B, time_steps=T, dof=N, tol=cfg.tol,
                             grid=list(cfg.counts), l2="flushed (256 MB write) before every timed iteration",
-                            parallelism=f"batch-sharded x{ws} (weak)"),
+                            parallelism=f"batch partitioned over {ws} rank(s), no data-path collective"),
                 e2e=e2e, gpu_launches=launches, roofline=roof,
                 roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
                 kernel_share=share,
@@ -335,12 +373,11 @@ def main_ours(args):
                            supernodes=info["n_supernodes"], levels=info["n_levels"]),
                 clocks=clk)
     if rank == 0:
-        if args.cpu_sample_steps > 0:
-            line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg, args.cpu_sample_steps).items() if k != "wall_s"}
+        if args.cpu_sample_steps > 0 and ws == 1:
+            line["cpu_baseline"] = {k: v for k, v in oracle_sample(cfg).items() if k != "wall_s"}
         else:
             line["cpu_baseline"] = dict(value=None, unit=UNIT, cores=None, kind="oracle",
-                                        sample="not run (--cpu-sample-steps 0): one oracle sim-step of this "
-                                               "workload exceeds 50 min on the host")
+                                        sample="not run (--cpu-sample-steps 0, or N > 1: rank 0 at N = 1 only)")
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()

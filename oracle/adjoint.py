@@ -32,13 +32,13 @@ def hessian_blocks(scene, x, w, act=None):
     J, R = energy.polar_jacobian(F)                                 # [m,8,9,9]
     G = fem.G_matrices(scene.dx)
     I9 = np.eye(9)
-    H = w * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - J, G)
+    H = w * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - J, G, optimize=True)
     if scene.muscle:
         Fm = F @ np.asarray(scene.fiber)
         r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
         Jm, p, n_hat = energy.muscle_jacobian(Fm, r, scene.fiber)
         Gm = fem.Gm_matrices(scene.dx, scene.fiber)
-        H = H + scene.w_muscle * scene.V * np.einsum("qka,mqkl,qlb->mab", Gm, np.eye(3) - Jm, Gm)
+        H = H + scene.w_muscle * scene.V * np.einsum("qka,mqkl,qlb->mab", Gm, np.eye(3) - Jm, Gm, optimize=True)
     return H
 
 
@@ -53,9 +53,16 @@ def assemble_dA(scene, x, w, act=None):
     return (scene.A(w) - assemble_AN(scene, x, w, act)).tocsr()
 
 
-def solve_adjoint(scene, x, w, act, b, cons_mask):
+def solve_adjoint(scene, x, w, act, b, cons_mask, solver="direct", rtol=1e-13):
+    """u = A_N^{-1} b on the unconstrained DoFs (0 on cons_mask).  solver="direct": sparse LU of A_N;
+    solver="pcg": conjugate gradients preconditioned with the prefactorised A (the paper's accelerated
+    fixed point, for meshes where the LU of A_N does not fit), to ||A_N u - b|| <= rtol ||b||."""
     AN = assemble_AN(scene, x, w, act)
     fr = ~cons_mask
+    if solver == "pcg":
+        facs = scene.axis_factors(w, cons_mask)
+        u, _, _ = scene.pcg(lambda v: AN @ v, b, lambda r: scene.apply_axis_factors(facs, r), fr, rtol)
+        return u
     u = np.zeros_like(b)
     u[fr] = spla.spsolve(AN[fr][:, fr].tocsc(), b[fr])
     return u
@@ -77,7 +84,7 @@ def param_terms(scene, x, u, act=None):
     return dw, dr
 
 
-def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL_dv_steps=None):
+def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL_dv_steps=None, solver="direct"):
     """Reverse pass over a trajectory from oracle.pd.forward.
 
     Per-step losses L = sum_i l_i(q_i, v_i) (the Plant task's "loss at each time step"): optional
@@ -109,7 +116,7 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
         b_pin = b[pins].copy()
         b[cons] = 0.0
         a_i = None if act is None else act[i]
-        u = solve_adjoint(scene, x1, w, a_i, b, cons)
+        u = solve_adjoint(scene, x1, w, a_i, b, cons, solver)
         extra = None
         if sticky and len(pins):
             # x_{i+1,a} = x_{i,a}: dL/dx_{i,a} += b_a - (A_N u)_a  (u_a = 0)

@@ -16,8 +16,20 @@ The constrained global solve is the plain definition (a direct sparse solve of
 the reduced system A_{CbarCbar} x_Cbar = d_Cbar - A_{Cbar C} xbar); the paper's
 Woodbury route (Alg. 2) reaches the same x exactly and is checked against this
 in tests.  c1 is an iteration (exactly `fixed_iter` PD iterations from x^0 = x_i,
-reading §8c.6); every other config is the minimiser of g reached by plain PD to
-a relative residual ||grad g_free|| / ||(M/h^2) y_free|| <= tol (reading §8c.8).
+reading §8c.6); every other config is the minimiser of g, to a relative residual
+||grad g_free|| / ||(M/h^2) y_free|| <= tol (reading §8c.8).  The minimiser is
+reached by one of three routes that tests show agree (SURVEY §8c "plain PD, PD
+with L-BFGS, or a Newton polish"):
+  method="newton"     (default) Newton on g with A_N = M/h^2 + Hess E_int and a direct
+                      sparse LU solve per Newton step (small and mid-size meshes);
+  method="pd"         the literal local-global iteration (P:191-203);
+  method="newton_pcg" Newton on g whose step A_N d = -grad g is solved by conjugate
+                      gradients preconditioned with the prefactorised A (the
+                      BFGS-with-H0=A^{-1} of P:254-271 is the same Krylov space), for
+                      meshes where a sparse LU of A_N does not fit (config c5).  A is
+                      factored per coordinate axis: A = M/h^2 + sum w G^T G has no
+                      coupling between axes (G maps every axis identically), which
+                      `axis_factors` checks on the assembled matrix before using it.
 """
 from __future__ import annotations
 
@@ -212,9 +224,121 @@ class Scene:
             g, gg, res = gn, ggn, resn
         return x, max_iter, res
 
+    # ---- large meshes: A^{-1} per axis, A-preconditioned CG (method="newton_pcg") ----
+    def axis_factors(self, w, cons_mask):
+        """Preconditioner data for the CG routes: sparse LU of the diagonal axis blocks A[a::3, a::3] restricted
+        to the Dirichlet-free DoFs of axis a (factored once per w; axes with the same free pattern share one LU).
+        This is A^{-1} on the free DoFs only because A has no entries between different axes (checked here on
+        the assembled A: P:199-202 with G acting on each axis alike).  DoFs in cons_mask beyond the
+        Dirichlet ones (contact pins) are handled by restriction: z = (A^{-1} r_free)_free, the principal block
+        of A^{-1} on the unconstrained DoFs, which is SPD and therefore a valid CG preconditioner."""
+        base = ~self.free
+        key = ("axes", float(w))
+        if key not in self._factors:
+            A = self.A(w).tocsr()
+            Acoo = A.tocoo()
+            cross = (Acoo.row % 3) != (Acoo.col % 3)
+            if np.any(Acoo.data[cross] != 0.0):
+                raise RuntimeError("A couples different axes: the per-axis factorisation does not apply")
+            out, seen = [], {}
+            for a in range(3):
+                fr = ~base[a::3]
+                k = fr.tobytes()
+                if k not in seen:
+                    Aa = A[a::3][:, a::3].tocsr()
+                    seen[k] = spla.splu(Aa[fr][:, fr].tocsc(), permc_spec="MMD_AT_PLUS_A")
+                out.append((fr, seen[k]))
+            self._factors = {k: v for k, v in list(self._factors.items())[-4:]}
+            self._factors[key] = out
+        return self._factors[key], cons_mask.copy()
+
+    @staticmethod
+    def apply_axis_factors(facs, r):
+        """z = (A^{-1} r)_free on the unconstrained DoFs (0 on cons_mask), r a full 3n vector."""
+        axes, cons = facs
+        r = np.where(cons, 0.0, r)
+        z = np.zeros_like(r)
+        for a, (fr, lu) in enumerate(axes):
+            ra = r[a::3]
+            za = np.zeros_like(ra)
+            za[fr] = lu.solve(np.ascontiguousarray(ra[fr]))
+            z[a::3] = za
+        z[cons] = 0.0
+        return z
+
+    @staticmethod
+    def pcg(matvec, b, precond, free, rtol, max_iter=5000):
+        """Textbook preconditioned conjugate gradients for an SPD operator on the DoFs in `free` (the others stay
+        0): stops when ||b - A u|| <= rtol ||b|| (the residual is recomputed from scratch before returning)."""
+        u = np.zeros_like(b)
+        bn = np.linalg.norm(b[free])
+        if bn == 0.0:
+            return u, 0, 0.0
+        r = b.copy()
+        r[~free] = 0.0
+        z = precond(r)
+        p = z.copy()
+        rz = r @ z
+        it = 0
+        for it in range(1, max_iter + 1):
+            q = matvec(p)
+            q[~free] = 0.0
+            alpha = rz / (p @ q)
+            u += alpha * p
+            r -= alpha * q
+            if np.linalg.norm(r) <= 0.1 * rtol * bn:
+                rt = b - matvec(u)
+                rt[~free] = 0.0
+                if np.linalg.norm(rt) <= rtol * bn:
+                    break
+                r = rt
+            z = precond(r)
+            rz_new = r @ z
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        rt = b - matvec(u)
+        rt[~free] = 0.0
+        return u, it, np.linalg.norm(rt) / bn
+
+    def newton_pcg_solve(self, x0, y, w, act, cons_mask, tol, max_iter=100):
+        """Minimiser of g (eq:opt) with the DoFs in cons_mask held: Newton's method, each step A_N d = -grad g
+        (A_N assembled) solved by A-preconditioned CG to 1e-4 of ||grad g|| (an inexact Newton step:
+        the outer loop, not the inner accuracy, decides the converged point), Armijo backtracking on g (with the
+        same fp64-floor rule as newton_solve)."""
+        from . import adjoint
+        x = x0.copy()
+        fr = ~cons_mask
+        scale = np.linalg.norm((self.mass / self.h ** 2 * y)[fr])
+        facs = self.axis_factors(w, cons_mask)
+        g, gg = self.objective(x, y, w, act)
+        gg[cons_mask] = 0.0
+        res = np.linalg.norm(gg) / scale
+        for it in range(max_iter + 1):
+            if res <= tol:
+                return x, it, res
+            AN = adjoint.assemble_AN(self, x, w, act)
+            d, _, _ = self.pcg(lambda v: AN @ v, -gg, lambda r: self.apply_axis_factors(facs, r), fr, 1e-4)
+            slope = gg @ d
+            if not slope < 0:
+                d = -self.apply_axis_factors(facs, gg)
+                slope = gg @ d
+            t = 1.0
+            for _ in range(60):
+                gn, ggn = self.objective(x + t * d, y, w, act)
+                ggn[cons_mask] = 0.0
+                resn = np.linalg.norm(ggn) / scale
+                if gn <= g + 1e-4 * t * slope or (res < 1e-6 and resn < res):
+                    break
+                t *= 0.5
+            x = x + t * d
+            g, gg, res = gn, ggn, resn
+        return x, max_iter, res
+
     def solve_step(self, x0, y, w, act, cons_mask, tol, fixed_iter=0, method="newton"):
         if fixed_iter or method == "pd":
             return self.pd_solve(x0, y, w, act, cons_mask, tol, fixed_iter)
+        if method == "newton_pcg":
+            return self.newton_pcg_solve(x0, y, w, act, cons_mask, tol)
         return self.newton_solve(x0, y, w, act, cons_mask, tol)
 
     # ---- contact (Alg. 1, frictionless normal pins on z = 0) ----

@@ -28,14 +28,23 @@ class PDError(RuntimeError):
         self.status = status
 
 
-def _ptr(t):
-    """Device pointer of a contiguous fp64/int CUDA tensor (or None)."""
+def _ptr(t, shape=None, name="array", device=None):
+    """Device pointer of a contiguous fp64 CUDA tensor (or None), after checking what the C-ABI cannot:
+    dtype float64, the handle's device and the exact shape the library will read or write (a float32 tensor
+    or a short array would otherwise be read past its end)."""
     if t is None:
         return None
+    import torch
     if not t.is_cuda:
-        raise ValueError("expected a CUDA tensor (the library takes device pointers)")
+        raise ValueError(f"{name}: expected a CUDA tensor (the library takes device pointers)")
+    if t.dtype != torch.float64:
+        raise ValueError(f"{name}: expected dtype torch.float64, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: tensor on {t.device}, the simulator's device is {device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
     if not t.is_contiguous():
-        raise ValueError("expected a contiguous tensor")
+        raise ValueError(f"{name}: expected a contiguous tensor")
     return C.c_void_p(t.data_ptr())
 
 
@@ -78,6 +87,8 @@ class Simulator:
         if st != 0:
             raise PDError(st, self.lib.pd_last_error(None).decode())
         self.handle = h_
+        import torch
+        self.device = torch.device("cuda", torch.cuda.current_device())  # the handle's device (pd_create)
         self.n_contact = len(cand)
         self.max_batch, self.max_steps = max_batch, max_steps
         self.h = h
@@ -127,10 +138,17 @@ class Simulator:
         """q0, v0: CUDA fp64 [B, 3n]; f_ext [B, 3n] (constant) or [B, steps, 3n] (per step).
         Returns a stats dict (numpy [B, steps] arrays)."""
         B = q0.shape[0]
+        N, m, dev = 3 * self.n_nodes, self.n_elems, self.device
+        if not (1 <= B <= self.max_batch and 1 <= steps <= self.max_steps):
+            raise ValueError(f"B={B}, steps={steps} outside max_batch={self.max_batch}, max_steps={self.max_steps}")
         st, arrs = self._stats(B, steps)
-        stride = 0 if f_ext is None or f_ext.dim() == 2 else f_ext.shape[-1]
-        self._check(self.lib.pd_forward(self.handle, B, _ptr(q0), _ptr(v0), _ptr(f_ext), stride, _ptr(actuation),
-                                        _ptr(youngs), steps, _ptr(q_traj), _ptr(v_traj), C.byref(st), _stream()))
+        per_step = f_ext is not None and f_ext.dim() == 3
+        stride = N if per_step else 0
+        args = [_ptr(q0, (B, N), "q0", dev), _ptr(v0, (B, N), "v0", dev),
+                _ptr(f_ext, (B, steps, N) if per_step else (B, N), "f_ext", dev), stride,
+                _ptr(actuation, (B, steps, m), "actuation", dev), _ptr(youngs, (B,), "youngs", dev), steps,
+                _ptr(q_traj, (B, steps + 1, N), "q_traj", dev), _ptr(v_traj, (B, steps + 1, N), "v_traj", dev)]
+        self._check(self.lib.pd_forward(self.handle, B, *args, C.byref(st), _stream()))
         self._B, self._T = B, steps
         out = {k: v.reshape(B, steps) for k, v in arrs.items() if k in ("iters_fwd", "final_res_fwd", "contact_outer")}
         out["n_nonconverged"] = st.n_nonconverged
@@ -139,10 +157,13 @@ class Simulator:
     def backward(self, dL_dqT=None, dL_dvT=None, dL_dq0=None, dL_dv0=None, dL_dfext=None, dL_dE=None,
                  dL_dnu=None, dL_dact=None):
         B, T = self._B, self._T
+        N, m, dev = 3 * self.n_nodes, self.n_elems, self.device
         st, arrs = self._stats(B, T)
-        self._check(self.lib.pd_backward(self.handle, _ptr(dL_dqT), _ptr(dL_dvT), _ptr(dL_dq0), _ptr(dL_dv0),
-                                         _ptr(dL_dfext), _ptr(dL_dE), _ptr(dL_dnu), _ptr(dL_dact), C.byref(st),
-                                         _stream()))
+        args = [_ptr(dL_dqT, (B, N), "dL_dqT", dev), _ptr(dL_dvT, (B, N), "dL_dvT", dev),
+                _ptr(dL_dq0, (B, N), "dL_dq0", dev), _ptr(dL_dv0, (B, N), "dL_dv0", dev),
+                _ptr(dL_dfext, (B, N), "dL_dfext", dev), _ptr(dL_dE, (B,), "dL_dE", dev),
+                _ptr(dL_dnu, (B,), "dL_dnu", dev), _ptr(dL_dact, (B, T, m), "dL_dact", dev)]
+        self._check(self.lib.pd_backward(self.handle, *args, C.byref(st), _stream()))
         out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
         out["n_nonconverged"] = st.n_nonconverged
         return out
@@ -151,10 +172,13 @@ class Simulator:
                        dL_dE=None, dL_dnu=None, dL_dact=None):
         """Per-step losses: dL_dq_steps / dL_dv_steps [B, T+1, 3n]; dL_dfext_steps output [B, T, 3n]."""
         B, T = self._B, self._T
+        N, m, dev = 3 * self.n_nodes, self.n_elems, self.device
         st, arrs = self._stats(B, T)
-        self._check(self.lib.pd_backward_steps(self.handle, _ptr(dL_dq_steps), _ptr(dL_dv_steps), _ptr(dL_dq0),
-                                               _ptr(dL_dv0), _ptr(dL_dfext_steps), _ptr(dL_dE), _ptr(dL_dnu),
-                                               _ptr(dL_dact), C.byref(st), _stream()))
+        args = [_ptr(dL_dq_steps, (B, T + 1, N), "dL_dq_steps", dev), _ptr(dL_dv_steps, (B, T + 1, N), "dL_dv_steps", dev),
+                _ptr(dL_dq0, (B, N), "dL_dq0", dev), _ptr(dL_dv0, (B, N), "dL_dv0", dev),
+                _ptr(dL_dfext_steps, (B, T, N), "dL_dfext_steps", dev), _ptr(dL_dE, (B,), "dL_dE", dev),
+                _ptr(dL_dnu, (B,), "dL_dnu", dev), _ptr(dL_dact, (B, T, m), "dL_dact", dev)]
+        self._check(self.lib.pd_backward_steps(self.handle, *args, C.byref(st), _stream()))
         out = {k: v.reshape(B, T) for k, v in arrs.items() if k in ("iters_adj", "final_res_adj")}
         out["n_nonconverged"] = st.n_nonconverged
         return out
@@ -165,19 +189,33 @@ class Simulator:
         self._check(self.lib.pd_contact_sets(self.handle, out.ctypes.data_as(C.POINTER(C.c_uint8))))
         return out.astype(bool)
 
+    def _diag_B(self, x):
+        B = x.shape[0]
+        if not 1 <= B <= self.max_batch:
+            raise ValueError(f"B={B} outside [1, max_batch={self.max_batch}]")
+        return B, 3 * self.n_nodes, self.n_elems, self.device
+
     def eval_objective(self, x, y, youngs=None, act=None, grad=None, g=None):
-        self._check(self.lib.pd_eval_objective(self.handle, x.shape[0], _ptr(x), _ptr(y), _ptr(youngs), _ptr(act),
-                                               _ptr(grad), _ptr(g), _stream()))
+        B, N, m, dev = self._diag_B(x)
+        self._check(self.lib.pd_eval_objective(self.handle, B, _ptr(x, (B, N), "x", dev), _ptr(y, (B, N), "y", dev),
+                                               _ptr(youngs, (B,), "youngs", dev), _ptr(act, (B, m), "act", dev),
+                                               _ptr(grad, (B, N), "grad", dev), _ptr(g, (B,), "g", dev), _stream()))
 
     def apply_Ainv(self, rhs, out):
-        self._check(self.lib.pd_apply_Ainv(self.handle, rhs.shape[0], _ptr(rhs), _ptr(out), _stream()))
+        B, N, m, dev = self._diag_B(rhs)
+        self._check(self.lib.pd_apply_Ainv(self.handle, B, _ptr(rhs, (B, N), "rhs", dev), _ptr(out, (B, N), "out", dev),
+                                           _stream()))
 
     def apply_AN(self, x, p, out, youngs=None, act=None):
-        self._check(self.lib.pd_apply_AN(self.handle, x.shape[0], _ptr(x), _ptr(youngs), _ptr(act), _ptr(p),
-                                         _ptr(out), _stream()))
+        B, N, m, dev = self._diag_B(x)
+        self._check(self.lib.pd_apply_AN(self.handle, B, _ptr(x, (B, N), "x", dev), _ptr(youngs, (B,), "youngs", dev),
+                                         _ptr(act, (B, m), "act", dev), _ptr(p, (B, N), "p", dev),
+                                         _ptr(out, (B, N), "out", dev), _stream()))
 
     def project_rotations(self, x, R):
-        self._check(self.lib.pd_project_rotations(self.handle, x.shape[0], _ptr(x), _ptr(R), _stream()))
+        B, N, m, dev = self._diag_B(x)
+        self._check(self.lib.pd_project_rotations(self.handle, B, _ptr(x, (B, N), "x", dev),
+                                                  _ptr(R, (B, m, 8, 9), "R", dev), _stream()))
 
 
 def simulator_from_inputs(inp, **kw):
@@ -192,8 +230,9 @@ def simulator_from_inputs(inp, **kw):
     if cfg.per_sim_youngs and "youngs_ref" not in kw:
         # plain PD needs the majorising A_ref (largest E of the batch); the quasi-Newton
         # forward/adjoint only use A_ref^{-1} as a preconditioner, where the geometric mean of the batch
-        # extremes halves the worst-case condition number
-        E = np.asarray(inp["youngs"], dtype=np.float64)
+        # extremes halves the worst-case condition number.  A sharded workload (shard.shard_inputs) carries the
+        # value of the whole batch.
+        from .shard import shared_youngs_ref
         accel = args.get("accel_fwd", 1)
-        args["youngs_ref"] = float(np.max(E)) if not accel else float(np.sqrt(np.min(E) * np.max(E)))
+        args["youngs_ref"] = inp.get("youngs_ref") or shared_youngs_ref(inp["youngs"], bool(accel))
     return Simulator(inp["rest"], inp["hex8"], cfg.dx, **args)

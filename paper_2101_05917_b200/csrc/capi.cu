@@ -58,6 +58,10 @@ struct pd_sim {
   double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
   double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR, *JC;
   double *w_sim, *youngs_sim, *dots, *partial, *alpha, *beta, *rz, *bb, *dw_acc, *act;
+  // per-sim weights of the diagnostic hooks (pd_eval_objective / pd_apply_AN): kept apart from w_sim / youngs_sim,
+  // which pd_backward reuses from the last pd_forward
+  double *w_diag = nullptr, *youngs_diag = nullptr;
+  const double* w_cur = nullptr;  // the weights the element kernels read (w_sim or w_diag)
   int32_t *active, *nactive, *it_buf, *flag_buf;
   double* res_buf;
   int32_t* h_nactive = nullptr;  // pinned
@@ -126,9 +130,10 @@ struct pd_sim {
 namespace {
 
 inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
-// DoFs per reduction block: ~4096 (DoF, sim) elements per block whatever B is (fixed partition =
-// deterministic sums).
-inline int64_t dot_chunk(int B) { return std::max<int64_t>(8, 2048 / B); }
+// per-sim reductions (kernels.cu kRed*): chunks of kRedC DoFs, kRedJ threads per sim, groups of kRedS sims
+inline int red_chunks(int64_t len) { return (int)((len + kRedC - 1) / kRedC); }
+inline unsigned red_threads(int B) { return (unsigned)(kRedJ * std::min(B, kRedS)); }
+inline unsigned red_groups(int B) { return (unsigned)((B + kRedS - 1) / kRedS); }
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -188,7 +193,7 @@ ElemArgs elem_args(pd_sim* s, int B, const double* act_step, int64_t act_bstride
   ea.hex8 = s->d_hex8;
   ea.m = s->plan.m;
   ea.B = B;
-  ea.w_sim = s->w_sim;
+  ea.w_sim = s->w_cur ? s->w_cur : s->w_sim;
   ea.act = act_step;
   ea.act_bstride = act_bstride;
   return ea;
@@ -205,10 +210,8 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
     ++p;
   }
   da.npairs = p;
-  const int64_t chunk = dot_chunk(B);
-  const int nchunk = (int)((len + chunk - 1) / chunk);
-  const int bd = B * std::max(1, 256 / B);
-  k_dot_partial<<<nchunk, bd, p * bd * sizeof(double), s->stream>>>(da, len, B, chunk, s->partial);
+  const int nchunk = red_chunks(len);
+  k_dot_partial<<<dim3(nchunk, red_groups(B)), red_threads(B), 0, s->stream>>>(da, len, B, s->partial);
   LAUNCH_CHECK(s);
   k_dot_final<<<p * B, 128, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
@@ -254,7 +257,8 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     const int ch0 = S.lvl_chain[j], nch = S.lvl_chain[j + 1] - ch0;
     if (nch > 0) {
       const int kp = kpad_of(S.lvl_kmax[j]);
-      const int nbuf = s->k3_nbuf;  // ring depth (default 2: 2 buffers x several CTAs/SM)
+      // ring depth (default 2: 2 buffers x several CTAs/SM), clamped to what fits the shared-memory opt-in limit
+      const int nbuf = std::max(2, std::min(s->k3_nbuf, (232448 - 1024) / (kp * (32 + RC) * 8)));
       const int smem = nbuf * kp * (32 + RC) * 8;
       const unsigned gx = (unsigned)std::min<int64_t>(nch, std::max<int64_t>(1, resident_lvl(smem) / gy));
       cudaLaunchConfig_t c = cfg_of(dim3(gx, gy), dim3(128), smem);
@@ -374,17 +378,20 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
   LAUNCH_CHECK(s);
 }
 
-void set_w(pd_sim* s, int B, const double* youngs_per_sim) {
-  // w = E/(1+nu) per sim; youngs_sim keeps E for dL/dE, dL/dnu
+// w = E/(1+nu) per sim into the forward's w_sim / youngs_sim (diag = false: youngs_sim keeps E for
+// dL/dE, dL/dnu of the following pd_backward) or into the diagnostic hooks' own scratch (diag = true)
+void set_w(pd_sim* s, int B, const double* youngs_per_sim, bool diag = false) {
+  double* E = diag ? s->youngs_diag : s->youngs_sim;
+  double* w = diag ? s->w_diag : s->w_sim;
   std::vector<double> ones(B, s->youngs);
   if (youngs_per_sim)
-    CK(cudaMemcpyAsync(s->youngs_sim, youngs_per_sim, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(E, youngs_per_sim, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
   else
-    CK(cudaMemcpyAsync(s->youngs_sim, ones.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-  k_axpby<<<1, 256, 0, s->stream>>>(s->w_sim, s->youngs_sim, 1.0 / (1.0 + s->poisson), nullptr, nullptr, 0.0, B, B,
-                                    nullptr);
+    CK(cudaMemcpyAsync(E, ones.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  k_axpby<<<1, 256, 0, s->stream>>>(w, E, 1.0 / (1.0 + s->poisson), nullptr, nullptr, 0.0, B, B, nullptr);
   LAUNCH_CHECK(s);
   CK(cudaStreamSynchronize(s->stream));
+  s->w_cur = w;
 }
 
 // the three counters in one copy: [0] the last k_*_check / k_ls_accept count, [1] the deferred convergence
@@ -409,12 +416,10 @@ int read_nactive(pd_sim* s) {
 void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double* out, const double* u2 = nullptr,
           const double* V2base = nullptr) {
   const int64_t n3 = 3LL * s->plan.n;
-  const int64_t chunk = dot_chunk(B);
-  const int nchunk = (int)((n3 + chunk - 1) / chunk);
-  const int bd = B * std::max(1, 256 / B);
+  const int nchunk = red_chunks(n3);
   const int np = u2 ? 2 * nv : nv;
-  k_mdot_partial<<<dim3(nchunk, np), bd, bd * sizeof(double), s->stream>>>(u, Vbase, n3 * B, nv, n3, B, chunk,
-                                                                           s->partial, u2, V2base);
+  k_mdot_partial<<<dim3(nchunk, np, red_groups(B)), red_threads(B), 0, s->stream>>>(u, Vbase, n3 * B, nv, n3, B,
+                                                                                    s->partial, u2, V2base);
   LAUNCH_CHECK(s);
   k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, out);
   LAUNCH_CHECK(s);
@@ -428,13 +433,10 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
   const HostPlan& P = s->plan;
   residual(s, B, X, s->Y, act_step, act_bs, s->d_fixed, Gout);
   const int64_t n3 = 3LL * P.n;
-  const int64_t chunk = dot_chunk(B);
-  const int nchunk = (int)((n3 + chunk - 1) / chunk);
-  const int bd = B * std::max(1, 256 / B);
+  const int nchunk = red_chunks(n3);
   const int np = with_gn2 ? 2 : 1;
-  k_inertia_partial<<<nchunk, bd, np * bd * sizeof(double), s->stream>>>(X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3,
-                                                                         B, chunk, s->partial,
-                                                                         with_gn2 ? Gout : nullptr);
+  k_inertia_partial<<<dim3(nchunk, red_groups(B)), red_threads(B), 0, s->stream>>>(
+      X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B, s->partial, with_gn2 ? Gout : nullptr);
   LAUNCH_CHECK(s);
   k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, s->inert);
   LAUNCH_CHECK(s);
@@ -717,11 +719,10 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->EE = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DW = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DR = s->alloc<double>((int64_t)P.m * s->Bmax);
-    double** small[] = {&s->w_sim, &s->youngs_sim, &s->alpha, &s->beta, &s->rz, &s->bb, &s->dw_acc, &s->res_buf};
+    double** small[] = {&s->w_sim, &s->youngs_sim, &s->w_diag, &s->youngs_diag, &s->alpha, &s->beta, &s->rz, &s->bb, &s->dw_acc, &s->res_buf};
     for (double** p : small) *p = s->alloc<double>(s->Bmax);
     s->dots = s->alloc<double>(3 * s->Bmax);
-    for (int b = 1; b <= s->Bmax; ++b)
-      s->max_partial_blocks = std::max<int64_t>(s->max_partial_blocks, ((3LL * P.n + dot_chunk(b) - 1) / dot_chunk(b)) * b);
+    s->max_partial_blocks = (int64_t)red_chunks(std::max<int64_t>(3LL * P.n, P.m)) * s->Bmax;
     s->partial = s->alloc<double>(32 * s->max_partial_blocks + 64);  // up to 2 x 16 dot families (mdot pairs)
     s->active = s->alloc<int32_t>(s->Bmax);
     s->nactive = s->alloc<int32_t>(3);  // [0] last check / line-search count, [1] deferred convergence count,
@@ -835,6 +836,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   s->stream = (cudaStream_t)cuda_stream;
   s->launches = 0;
   s->pins_live = false;
+  s->have_traj = false;  // set again only when this forward completes (a failed forward leaves no trajectory)
   for (int k = 0; k < 6; ++k) { s->prof_ms[k] = 0; s->prof_cnt[k] = 0; }
   s->ev_open.clear();
   s->ev_next = 0;
@@ -1003,6 +1005,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
   if (!s) return PD_ERR_INVALID_ARGUMENT;
   if (!s->have_traj) return fail(s, PD_ERR_STATE, "pd_backward needs a preceding pd_forward");
   s->stream = (cudaStream_t)cuda_stream;
+  s->w_cur = s->w_sim;  // the forward's per-sim weights (a diagnostic hook in between used its own scratch)
   s->launches = 0;
   s->pins_live = false;
   const HostPlan& P = s->plan;
@@ -1214,7 +1217,7 @@ pd_status pd_eval_objective(pd_sim* s, int32_t B, const double* x, const double*
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
   try {
-    set_w(s, B, youngs_per_sim);
+    set_w(s, B, youngs_per_sim, true);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
     LAUNCH_CHECK(s);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(y, s->Y, n3, B);
@@ -1275,7 +1278,7 @@ pd_status pd_apply_AN(pd_sim* s, int32_t B, const double* x, const double* young
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
   try {
-    set_w(s, B, youngs_per_sim);
+    set_w(s, B, youngs_per_sim, true);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
     LAUNCH_CHECK(s);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(p, s->Pv, n3, B);

@@ -774,7 +774,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
       : "memory");
   return ok != 0;
 }
-// bounded: a byte-count bug becomes a trap (launch error) after ~0.5 s, never a hung GPU
+// bounded: a byte-count bug becomes a trap (launch error) instead of a hung GPU.  The bound is 20 s of
+// globaltimer and the barrier is re-tested after the timer read, so a CTA that was preempted or time-sliced
+// between a failed try_wait and the timer read (the timer keeps running while it is off the SM) re-checks the
+// completed barrier before giving up; only a transaction count that can never complete reaches the trap.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   if (mbar_try_wait(bar, parity)) return;
   uint64_t t0;
@@ -782,7 +785,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   while (!mbar_try_wait(bar, parity)) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 500000000ull) __trap();
+    if (t - t0 > 20000000000ull) {
+      if (mbar_try_wait(bar, parity)) return;
+      __trap();
+    }
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -1361,57 +1367,76 @@ __global__ void k_contact_outer(const int32_t* __restrict__ oact, const int32_t*
 }
 
 // ----------------------------------------------------------------- per-sim reductions
-// Block-level per-sim sums: thread t holds acc for sim t % B; red = [np][nb] staged in shared memory, then
-// thread o < np*B adds the nb/B values of (pair o / B, sim o % B) in index order (two interleaved
-// accumulators, fixed combination) -> partial[(p*nchunk + blk)*B + b].  Deterministic.
-__device__ __forceinline__ void block_sim_sums(double* red, int np, int B, double* __restrict__ partial, int nchunk,
-                                               int blk) {
-  __syncthreads();
-  const int nb = blockDim.x, J = nb / B;
-  for (int o = threadIdx.x; o < np * B; o += nb) {
-    const int p = o / B, b = o - p * B;
-    const double* r = red + p * nb + b;
-    double s0 = 0.0, s1 = 0.0;
-    int j = 0;
-    for (; j + 1 < J; j += 2) {
-      s0 += r[j * B];
-      s1 += r[(j + 1) * B];
-    }
-    if (j < J) s0 += r[j * B];
-    partial[((int64_t)p * nchunk + blk) * B + b] = s0 + s1;
-  }
+// Per-sim sums over a state-layout vector (element d*B + b): chunk c = DoFs [c*kRedC, (c+1)*kRedC); in a chunk,
+// thread j < kRedJ of sim b adds DoFs c*kRedC + j, + kRedJ, ... in ascending order, then the kRedJ thread sums are
+// added in j order -> partial[(p*nchunk + c)*B + b]; k_dot_final adds the chunks.  Every constant here is
+// independent of B, so a sim's sum — and with it every iterate — is bitwise the same whatever batch it runs in
+// (a sharded batch reproduces the single-GPU run exactly).  Blocks: kRedJ x min(B, kRedS) threads,
+// sims fastest (coalesced over b), grid.y (or .z) over groups of kRedS sims.
+constexpr int kRedC = 128;
+constexpr int kRedJ = 8;
+constexpr int kRedS = 32;
+
+struct RedLane {
+  int b, j, bl;
+  bool ok;
+};
+__device__ __forceinline__ RedLane red_lane(int B, int group) {
+  const int Bb = blockDim.x / kRedJ;
+  RedLane r;
+  r.bl = threadIdx.x % Bb;
+  r.j = threadIdx.x / Bb;
+  r.b = group * kRedS + r.bl;
+  r.ok = r.b < B;
+  return r;
 }
-// partial[c][b] = sum over chunk c of u*v (up to 3 pairs); blockDim % B == 0 so that each
-// thread keeps one sim; fixed-order sum inside the block, fixed-order sum over chunks.
-__global__ void k_dot_partial(DotArgs da, int64_t len, int B, int64_t chunk, double* __restrict__ partial) {
-  extern __shared__ double red[];
-  const int nb = blockDim.x;
-  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
-  double acc[3] = {0, 0, 0};
-  int64_t i = beg + threadIdx.x;
-  for (; i + nb < end; i += 2 * nb) {  // two elements per trip: loads first, then the in-order fma chain
-    double u0[3], v0[3], u1[3], v1[3];
+// red[p][j][bl] holds the thread sums; thread j == 0 adds them in j order and stores the chunk partial
+__device__ __forceinline__ void red_store(double (*red)[kRedJ][kRedS], int np, const RedLane& r, int B, int nchunk,
+                                          int c, double* __restrict__ partial) {
+  __syncthreads();
+  if (r.j == 0 && r.ok)
+    for (int p = 0; p < np; ++p) {
+      double t = red[p][0][r.bl];
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      u0[p] = p < da.npairs ? da.u[p][i] : 0.0;
-      u1[p] = p < da.npairs ? da.u[p][i + nb] : 0.0;
-      v0[p] = (p < da.npairs && da.v[p]) ? da.v[p][i] : 1.0;
-      v1[p] = (p < da.npairs && da.v[p]) ? da.v[p][i + nb] : 1.0;
+      for (int jj = 1; jj < kRedJ; ++jj) t += red[p][jj][r.bl];
+      partial[((int64_t)p * nchunk + c) * B + r.b] = t;
     }
+}
+// partial[c][b] = sum over chunk c of u*v (up to 3 pairs; v = null means 1)
+__global__ void k_dot_partial(DotArgs da, int64_t len, int B, double* __restrict__ partial) {
+  __shared__ double red[3][kRedJ][kRedS];
+  const RedLane r = red_lane(B, blockIdx.y);
+  const int c = blockIdx.x;
+  double acc[3] = {0, 0, 0};
+  if (r.ok) {
+    const int64_t d1 = min(len, (int64_t)(c + 1) * kRedC);
+    int64_t d = (int64_t)c * kRedC + r.j;
+    for (; d + kRedJ < d1; d += 2 * kRedJ) {  // two DoFs per trip: loads first, then the in-order fma chain
+      const int64_t i0 = d * B + r.b, i1 = (d + kRedJ) * B + r.b;
+      double u0[3], v0[3], u1[3], v1[3];
 #pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      acc[p] = fma(u0[p], v0[p], acc[p]);
-      acc[p] = fma(u1[p], v1[p], acc[p]);
+      for (int p = 0; p < 3; ++p) {
+        u0[p] = p < da.npairs ? da.u[p][i0] : 0.0;
+        u1[p] = p < da.npairs ? da.u[p][i1] : 0.0;
+        v0[p] = (p < da.npairs && da.v[p]) ? da.v[p][i0] : 1.0;
+        v1[p] = (p < da.npairs && da.v[p]) ? da.v[p][i1] : 1.0;
+      }
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        acc[p] = fma(u0[p], v0[p], acc[p]);
+        acc[p] = fma(u1[p], v1[p], acc[p]);
+      }
+    }
+    for (; d < d1; d += kRedJ) {
+      const int64_t i = d * B + r.b;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        if (p < da.npairs) acc[p] = fma(da.u[p][i], da.v[p] ? da.v[p][i] : 1.0, acc[p]);
     }
   }
-  for (; i < end; i += nb)
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
-      if (p < da.npairs) acc[p] = fma(da.u[p][i], da.v[p] ? da.v[p][i] : 1.0, acc[p]);
-#pragma unroll
-  for (int p = 0; p < 3; ++p)
-    if (p < da.npairs) red[p * nb + threadIdx.x] = acc[p];
-  block_sim_sums(red, da.npairs, B, partial, gridDim.x, blockIdx.x);
+  for (int p = 0; p < 3; ++p) red[p][r.j][r.bl] = acc[p];
+  red_store(red, da.npairs, r, B, gridDim.x, c, partial);
 }
 // one warp per (pair, sim): lane l sums chunks l, l+32, ... in order, then a fixed xor tree (deterministic)
 // one 128-thread block per (pair, sim): thread t sums chunks t, t+128, ... with 4 independent accumulators (loads
@@ -1461,23 +1486,27 @@ __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* 
 // The quasi-Newton PD of P:79/P:254 (Liu et al.): minimise g (eq:opt) with L-BFGS whose initial inverse
 // Hessian is the prefactorised A^{-1}; Armijo backtracking on g.  Same minimiser as plain PD.
 
-// partial[c][b] = sum over chunk c of (m_node/h^2) (X - Y)^2   (fixed-order, like k_dot_partial);
-// with G: a second pair, sum of G^2 (the gradient norm of the same evaluation)
+// partial[c][b] = sum over chunk c of (m_node/h^2) (X - Y)^2 (the per-sim chunking of k_dot_partial); with G: a
+// second pair, sum of G^2 (the gradient norm of the same evaluation)
 __global__ void k_inertia_partial(const double* __restrict__ X, const double* __restrict__ Y,
-                                  const double* __restrict__ mass, double inv_h2, int64_t len, int B, int64_t chunk,
+                                  const double* __restrict__ mass, double inv_h2, int64_t len, int B,
                                   double* __restrict__ partial, const double* __restrict__ G = nullptr) {
-  extern __shared__ double red[];
-  const int nb = blockDim.x;
-  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
+  __shared__ double red[2][kRedJ][kRedS];
+  const RedLane r = red_lane(B, blockIdx.y);
+  const int c = blockIdx.x;
   double acc = 0, acc2 = 0;
-  for (int64_t i = beg + threadIdx.x; i < end; i += nb) {
-    const double d = X[i] - Y[i];
-    acc += mass[i / B / 3] * inv_h2 * d * d;
-    if (G) acc2 += G[i] * G[i];
+  if (r.ok) {
+    const int64_t d1 = min(len, (int64_t)(c + 1) * kRedC);
+    for (int64_t d = (int64_t)c * kRedC + r.j; d < d1; d += kRedJ) {
+      const int64_t i = d * B + r.b;
+      const double e = X[i] - Y[i];
+      acc += mass[d / 3] * inv_h2 * e * e;
+      if (G) acc2 += G[i] * G[i];
+    }
   }
-  red[threadIdx.x] = acc;
-  if (G) red[nb + threadIdx.x] = acc2;
-  block_sim_sums(red, G ? 2 : 1, B, partial, gridDim.x, blockIdx.x);
+  red[0][r.j][r.bl] = acc;
+  red[1][r.j][r.bl] = acc2;
+  red_store(red, G ? 2 : 1, r, B, gridDim.x, c, partial);
 }
 
 // f[b] = 0.5 * inert[b] + esum[b]
@@ -1554,32 +1583,36 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
 //   d = -(r0 + sum_j (alpha_j - beta_j) s_j).
 
 // partial[(j*nchunk + c)*B + b] = sum over chunk c of u * V_j  (V_j = Vbase + j*vstride), j < nv; with u2:
-// pairs nv + j = u2 * V2_j as well (both families of the new curvature pair in one launch).  Block (c, j):
-// one chunk of one pair (grid.y = pairs), so every block streams two vectors with few registers.
+// pairs nv + j = u2 * V2_j as well (both families of the new curvature pair in one launch).  Block (c, j, group):
+// one chunk of one pair (the per-sim chunking of k_dot_partial), so every block streams two vectors.
 __global__ void k_mdot_partial(const double* __restrict__ u, const double* __restrict__ Vbase, int64_t vstride,
-                               int nv, int64_t len, int B, int64_t chunk, double* __restrict__ partial,
+                               int nv, int64_t len, int B, double* __restrict__ partial,
                                const double* __restrict__ u2 = nullptr, const double* __restrict__ V2base = nullptr) {
-  extern __shared__ double red[];
-  const int nb = blockDim.x;
+  __shared__ double red[1][kRedJ][kRedS];
+  const RedLane r = red_lane(B, blockIdx.z);
   const int jp = blockIdx.y;
   const bool second = jp >= nv;
   const double* __restrict__ uu = second ? u2 : u;
   const double* __restrict__ V = (second ? V2base : Vbase) + (int64_t)(second ? jp - nv : jp) * vstride;
-  const int64_t beg = blockIdx.x * chunk * B, end = min(beg + chunk * B, len * B);
-  // four elements per trip: all eight loads in flight, then the in-order accumulation
+  const int c = blockIdx.x;
   double acc = 0.0;
-  int64_t i = beg + threadIdx.x;
-  for (; i + 3 * nb < end; i += 4 * nb) {
-    const double a0 = uu[i], a1 = uu[i + nb], a2 = uu[i + 2 * nb], a3 = uu[i + 3 * nb];
-    const double b0 = V[i], b1 = V[i + nb], b2 = V[i + 2 * nb], b3 = V[i + 3 * nb];
-    acc += a0 * b0;
-    acc += a1 * b1;
-    acc += a2 * b2;
-    acc += a3 * b3;
+  if (r.ok) {
+    const int64_t d1 = min(len, (int64_t)(c + 1) * kRedC);
+    int64_t d = (int64_t)c * kRedC + r.j;
+    // four DoFs per trip: all eight loads in flight, then the in-order accumulation
+    for (; d + 3 * kRedJ < d1; d += 4 * kRedJ) {
+      const int64_t i = d * B + r.b, st = (int64_t)kRedJ * B;
+      const double a0 = uu[i], a1 = uu[i + st], a2 = uu[i + 2 * st], a3 = uu[i + 3 * st];
+      const double b0 = V[i], b1 = V[i + st], b2 = V[i + 2 * st], b3 = V[i + 3 * st];
+      acc += a0 * b0;
+      acc += a1 * b1;
+      acc += a2 * b2;
+      acc += a3 * b3;
+    }
+    for (; d < d1; d += kRedJ) acc += uu[d * B + r.b] * V[d * B + r.b];
   }
-  for (; i < end; i += nb) acc += uu[i] * V[i];
-  red[threadIdx.x] = acc;
-  block_sim_sums(red, 1, B, partial + (int64_t)jp * gridDim.x * B, gridDim.x, blockIdx.x);
+  red[0][r.j][r.bl] = acc;
+  red_store(red, 1, r, B, gridDim.x, c, partial + (int64_t)jp * gridDim.x * B);
 }
 
 constexpr int kMaxHist = 16;  // largest L-BFGS memory the two-loop kernels support

@@ -16,10 +16,33 @@ def shard_range(n_sims: int, world: int, rank: int):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def shared_youngs_ref(youngs_all) -> float:
-    """Young's modulus of the one factorised A for a batched run: the max over the
-    WHOLE batch, computed before sharding, so iterates do not depend on the GPU count."""
-    return float(max(youngs_all))
+def shared_youngs_ref(youngs_all, accel: bool = False) -> float:
+    """Young's modulus of the one factorised A for a batched run, computed over the WHOLE
+    batch before sharding, so iterates do not depend on the GPU count: the batch max (the majorising A_ref of
+    plain PD) or, with the quasi-Newton forward/adjoint (A_ref^{-1} only preconditions), the geometric mean of
+    the batch extremes."""
+    import math
+    E = [float(e) for e in youngs_all]
+    return math.sqrt(min(E) * max(E)) if accel else max(E)
+
+
+PER_SIM_KEYS = ("q0", "v0", "f_ext", "youngs", "act", "c_q", "c_v", "tip_target")
+
+
+def shard_inputs(inp, world: int, rank: int, accel: bool = True):
+    """The slice [lo, hi) of a pd_inputs workload owned by `rank`: per-sim arrays cut along the batch, the
+    mesh and lists shared, and `youngs_ref` fixed from the whole batch (so a sim's iterates are the same as in
+    the single-GPU run; the per-sim reductions are batch-size independent, kernels.cu kRed*)."""
+    lo, hi = shard_range(inp["B"], world, rank)
+    out = dict(inp)
+    for k in PER_SIM_KEYS:
+        if out.get(k) is not None:
+            out[k] = out[k][lo:hi]
+    out["B"] = hi - lo
+    out["shard"] = (lo, hi)
+    if inp["cfg"].per_sim_youngs:
+        out["youngs_ref"] = shared_youngs_ref(inp["youngs"], accel)
+    return out
 
 
 def gather_rows(local, world: int, group=None):

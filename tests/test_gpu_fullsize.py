@@ -135,3 +135,96 @@ def test_c5_full_properties(torch):
         Ls.append(adjoint.loss_and_grad(inp2, 0, r["q"][0, -1], r["v"][0, -1])[0])
     fd = (Ls[0] - Ls[1]) / (2 * eps * inp["youngs"][0])
     assert abs(fd - a["dE"][0]) <= 1e-4 * abs(fd) + 1e-12, (fd, a["dE"][0])
+
+
+# ----------------------------------------------------------------- full-size K3 against the oracle's A
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_size_solve_residual(torch, name):
+    # The production K3 instances (c3: 64 sims -> 192 columns in 48-wide chunks; c5: 24 columns, the 13-level
+    # contact-ordered tree with its 2145-row dense root) applied to random right-hand sides: the result must
+    # solve the oracle's assembled A (the factor's E_ref for c3) to 1e-12.
+    from oracle import pd
+    from paper_2101_05917_b200.shard import shared_youngs_ref
+    inp = make_inputs(get_config(name), steps=1)
+    B, N = inp["B"], 3 * inp["n_nodes"]
+    sim = _bench_sim(inp)
+    rng = np.random.default_rng(21)
+    rhs = rng.standard_normal((B, N))
+    out = torch.zeros((B, N), dtype=torch.float64, device="cuda")
+    sim.apply_Ainv(to_dev(rhs), out)
+    x = out.cpu().numpy()
+    sc = pd.scene_from_inputs(inp)
+    E_ref = shared_youngs_ref(inp["youngs"], True) if inp["cfg"].per_sim_youngs else inp["cfg"].youngs
+    A = sc.A(sc.w_of(E_ref))
+    fr = sc.free
+    Aff = A[fr][:, fr]
+    for b in range(B):
+        assert np.all(x[b][~fr] == 0.0)
+        r = Aff @ x[b][fr] - rhs[b][fr]
+        assert np.linalg.norm(r) <= 1e-12 * np.linalg.norm(rhs[b][fr]), (b, np.linalg.norm(r) / np.linalg.norm(rhs[b][fr]))
+
+
+# ----------------------------------------------------------------- long horizons and c5 vs committed oracle goldens
+def _golden(key):
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"oracle_{key}.npz")
+    assert os.path.exists(path), f"{path} missing: python tools/make_goldens.py {key}"
+    return dict(np.load(path, allow_pickle=False))
+
+
+def _check_golden(inp, gpu, gd, b, sets=None, vel_rel_floor=0.0):
+    """States at the stored steps, active sets and Alg. 1 outer counts of every step, gradients at the end."""
+    p = f"s{b}_"
+    for k, i in enumerate(gd["keep"]):
+        eq = rel(gpu["q"][b, i], gd[p + "q"][k])
+        assert eq <= POS_TOL, ("q", b, int(i), eq)
+        vo = gd[p + "v"][k]
+        ev = np.linalg.norm(gpu["v"][b, i] - vo) / max(np.linalg.norm(vo), vel_rel_floor)
+        assert ev <= POS_TOL, ("v", b, int(i), ev, np.linalg.norm(vo))
+    if sets is not None and gd[p + "active"].size:
+        assert np.array_equal(sets[b], gd[p + "active"]), ("active sets", b)
+        assert list(gpu["st"]["contact_outer"][b]) == list(gd[p + "outer"]), ("outer", b)
+    for k in ("dq0", "dv0", "dfext"):
+        assert rel(gpu[k][b], gd[p + k]) <= GRAD_TOL, (k, b, rel(gpu[k][b], gd[p + k]))
+    for k in ("dE", "dnu"):
+        assert abs(gpu[k][b] - gd[p + k]) <= GRAD_TOL * abs(gd[p + k]), (k, b, gpu[k][b], gd[p + k])
+    if p + "dact" in gd:
+        assert rel(gpu["dact"][b], gd[p + "dact"]) <= GRAD_TOL, ("dact", b, rel(gpu["dact"][b], gd[p + "dact"]))
+
+
+def test_c5_full_batch_vs_oracle_golden(torch):
+    # configs[4] at full size in the bench launch configuration (B = 8, 212k DoF, contact + muscle), first 2
+    # steps; sim 0 against the oracle's Newton-PCG / PCG run (tools/make_goldens.py c5): positions, velocities,
+    # bit-exact active sets and outer counts, dL/dq0, dL/dv0, dL/df_ext, dL/dE, dL/dnu, dL/dact.
+    gd = _golden("c5")
+    T = int(gd["steps"])
+    inp = make_inputs(get_config("c5"), steps=T)
+    sim = _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11)
+    gpu = _run(torch, inp, sim)
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    for b in gd["sims"]:
+        _check_golden(inp, gpu, gd, int(b), sim.contact_sets())
+
+
+def test_c3_long_horizon_vs_oracle_golden(torch):
+    # configs[2], all 64 sims in one batch, 30 steps (into the large-rotation regime of the soft beams): the
+    # stiffest and the softest sim against the oracle (direct Newton, each sim's own A_s).
+    gd = _golden("c3")
+    T = int(gd["steps"])
+    inp = make_inputs(get_config("c3"), steps=T)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    for b in gd["sims"]:
+        _check_golden(inp, gpu, gd, int(b))
+
+
+def test_c4_full_horizon_vs_oracle_golden(torch):
+    # configs[3], the whole 150-step contact drop (impact, chatter, settling): active sets bit-exact at every
+    # step, states every 10 steps, gradients of the terminal loss.
+    gd = _golden("c4")
+    T = int(gd["steps"])
+    inp = make_inputs(get_config("c4"), steps=T)
+    sim = _bench_sim(inp, tol_fwd=2e-14, tol_adj=1e-11, max_iter_fwd=6000)
+    gpu = _run(torch, inp, sim)
+    assert gpu["sb"]["n_nonconverged"] == 0
+    _check_golden(inp, gpu, gd, 0, sim.contact_sets())

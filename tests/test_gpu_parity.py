@@ -120,6 +120,51 @@ def test_AN_product_matches_assembled_hessian(torch, name):
         assert rel(out[b], AN @ p[b]) <= 1e-12
 
 
+def test_AN_product_clamp_branch(torch):
+    # The eigenvalue floor of the rotation derivative (reading §8c.5): an affine, inverted
+    # deformation F0 = diag(1.1, 0.9, -(0.9 - 1e-9)) has S = R^T F with s2 + s3 = 1e-9 < 1e-6 max sigma, so the
+    # floor binds (the Jacobi branch of rot_derivative_matrix) while R = I stays exact on both sides.
+    from oracle import adjoint, pd
+    inp = make_inputs(get_config("c2s"))
+    sim = _sim(inp)
+    F0 = np.diag([1.1, 0.9, -(0.9 - 1e-9)])
+    x = (inp["rest"] @ F0.T).ravel()[None]
+    p = np.random.default_rng(7).standard_normal(x.shape)
+    out = torch.zeros_like(to_dev(p))
+    sim.apply_AN(to_dev(x), to_dev(p), out, youngs=to_dev(inp["youngs"]))
+    sc = pd.scene_from_inputs(inp)
+    AN = adjoint.assemble_AN(sc, x[0], sc.w_of(inp["youngs"][0]))
+    from oracle import energy
+    _, _, _, sv = energy.polar_svd(F0[None])
+    assert sv[0, 1] + sv[0, 2] < energy.CLAMP * np.abs(sv).max()      # the floor binds at every quad point
+    assert rel(out.cpu().numpy()[0], AN @ p[0]) <= 1e-12
+
+
+def test_AN_product_inverted_states(torch):
+    # Random states at 2 dx (many inverted elements: SVD fallback of R, clamped or Jacobi paths of the rotation
+    # derivative) against the oracle's assembled A_N.  Elements whose rotation is ill-conditioned
+    # ((s_i + s_j) < 1e-3 max sigma: R itself is then determined only to ~1e-13 / 1e-3) are switched off by
+    # p = 0 on their nodes; every other element, inverted or not, is compared at 1e-12.
+    from oracle import adjoint, energy, fem, pd
+    inp = make_inputs(get_config("c2s"))
+    sim = _sim(inp)
+    x = _rand_states(inp, 1, 2e-2, 9)
+    F = fem.deformation_gradients(x[0], inp["hex8"], 0.01)
+    _, _, _, sv = energy.polar_svd(F)
+    pair = np.stack([sv[..., 0] + sv[..., 1], sv[..., 0] + sv[..., 2], sv[..., 1] + sv[..., 2]], -1)
+    bad = (pair.min(-1) < 1e-3 * np.abs(sv).max(-1)).any(-1)
+    inverted = (np.linalg.det(F) < 0).any(-1)
+    assert inverted[~bad].sum() > 10, "the state should invert many well-conditioned elements"
+    p = np.random.default_rng(10).standard_normal(x.shape)
+    off = np.unique(inp["hex8"][bad])
+    p.reshape(-1, 3)[off] = 0.0
+    out = torch.zeros_like(to_dev(p))
+    sim.apply_AN(to_dev(x), to_dev(p), out, youngs=to_dev(inp["youngs"]))
+    sc = pd.scene_from_inputs(inp)
+    AN = adjoint.assemble_AN(sc, x[0], sc.w_of(inp["youngs"][0]))
+    assert rel(out.cpu().numpy()[0], AN @ p[0]) <= 1e-12
+
+
 # ----------------------------------------------------------------- end to end
 def _run_gpu(torch, inp, sim):
     B, T, N = inp["B"], inp["T"], 3 * inp["n_nodes"]
@@ -209,15 +254,16 @@ def test_bitwise_determinism(torch):
 
 
 @pytest.mark.parametrize("env", [{"PD_K3_MMA": "0"}, {"PD_K3_NBUF": "3"}, {"PD_K3_NBUF": "4"}])
-@pytest.mark.parametrize("name", ["c3s", "c5s"])
-def test_k3_switches_match_direct(torch, monkeypatch, env, name):
+@pytest.mark.parametrize("name,batch", [("c3s", None), ("c5s", None), ("c3s", 10), ("c3s", 17)])
+def test_k3_switches_match_direct(torch, monkeypatch, env, name, batch):
     # The K3 switches read at pd_create (FMA-pipe item product, deeper TMA rings) give the same A^{-1}
-    # as a direct sparse solve (c3s: odd 3B -> the non-TMA right-hand-side path; c5s: contact ordering).
+    # as a direct sparse solve (c3s: odd 3B -> the non-TMA right-hand-side path; c5s: contact ordering;
+    # B = 10 / 17: 48-column chunks, where a deep ring must be clamped to the shared-memory limit).
     import scipy.sparse.linalg as spla
     from oracle import pd
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    inp = make_inputs(get_config(name))
+    inp = make_inputs(get_config(name), batch=batch)
     B = inp["B"]
     sim = _sim(inp, youngs_ref=float(np.max(inp["youngs"])))
     rhs = np.random.default_rng(4).standard_normal((B, 3 * inp["n_nodes"]))
