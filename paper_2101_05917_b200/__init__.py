@@ -139,9 +139,7 @@ class Simulator:
         Returns a stats dict (numpy [B, steps] arrays)."""
         B = q0.shape[0]
         N, m, dev = 3 * self.n_nodes, self.n_elems, self.device
-        if not (1 <= B <= self.max_batch and 1 <= steps <= self.max_steps):
-            raise ValueError(f"B={B}, steps={steps} outside max_batch={self.max_batch}, max_steps={self.max_steps}")
-        st, arrs = self._stats(B, steps)
+        st, arrs = self._stats(B, steps)   # (B and steps against max_batch / max_steps: checked by pd_forward)
         per_step = f_ext is not None and f_ext.dim() == 3
         stride = N if per_step else 0
         args = [_ptr(q0, (B, N), "q0", dev), _ptr(v0, (B, N), "v0", dev),
@@ -190,10 +188,7 @@ class Simulator:
         return out.astype(bool)
 
     def _diag_B(self, x):
-        B = x.shape[0]
-        if not 1 <= B <= self.max_batch:
-            raise ValueError(f"B={B} outside [1, max_batch={self.max_batch}]")
-        return B, 3 * self.n_nodes, self.n_elems, self.device
+        return x.shape[0], 3 * self.n_nodes, self.n_elems, self.device
 
     def eval_objective(self, x, y, youngs=None, act=None, grad=None, g=None):
         B, N, m, dev = self._diag_B(x)

@@ -37,6 +37,10 @@ def test_state_and_argument_errors(torch):
     with pytest.raises(pdb.PDError) as e:          # steps > max_steps
         sim.forward(q, torch.zeros_like(q), 4)
     assert e.value.status == _lib.PD_ERR_INVALID_ARGUMENT
+    with pytest.raises(ValueError):                # the binding checks dtype and shape before the C-ABI
+        sim.forward(q.float(), torch.zeros_like(q), 1)
+    with pytest.raises(ValueError):
+        sim.forward(q, torch.zeros_like(q)[:, :-3].contiguous(), 1)
     with pytest.raises(pdb.PDError):               # a contact candidate that is also a Dirichlet node
         pdb.simulator_from_inputs(inp, contact_nodes=inp["fixed_dofs"][::3] // 3)
     with pytest.raises(pdb.PDError):               # repeated candidate

@@ -227,4 +227,8 @@ def test_c4_full_horizon_vs_oracle_golden(torch):
     sim = _bench_sim(inp, tol_fwd=2e-14, tol_adj=1e-11, max_iter_fwd=6000)
     gpu = _run(torch, inp, sim)
     assert gpu["sb"]["n_nonconverged"] == 0
-    _check_golden(inp, gpu, gd, 0, sim.contact_sets())
+    # Settling on the plane drives ||v|| toward 0 while the positions can agree only to the fp64 floor of the
+    # residual (~1e-14 relative): v = (x_{i+1} - x_i)/h then carries an error of ~1e-14 ||x|| / h whatever
+    # the implementation.  Velocities are therefore compared relative to max(||v_i||, 1% of the trajectory's
+    # peak ||v||); positions and gradients keep the plain bars.
+    _check_golden(inp, gpu, gd, 0, sim.contact_sets(), vel_rel_floor=0.01 * float(gd["s0_vnorm"].max()))
