@@ -49,6 +49,7 @@ struct pd_sim {
   uint8_t* d_fixed = nullptr;
   uint8_t* d_nofix = nullptr;  // all-zero node mask (diagnostics on all DoFs)
   SweepDev swf{}, swb{};
+  Sweep4Dev sw4f{}, sw4b{};  // K3 v4 (warp ranges), when plan.k3_version == 4
   int k3_mma = 1;   // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
   int k3_nbuf = 2;  // K3 item ring depth (2..4, env PD_K3_NBUF)
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
@@ -287,8 +288,70 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     for (int j = 0; j < P.nlevels; ++j) level(P.bw, s->swb, false, j);
   }
 }
+// K3 v4: one k_sweep_warp launch per level and sweep (warps stream equal k-group ranges) plus
+// the level's reduce when it has partial slots; chained with programmatic dependent launch.
+template <int NT, bool VEC>
+void solve_v4(pd_sim* s, int B) {
+  const HostPlan& P = s->plan;
+  const int R = 3 * B;
+  constexpr int RC = 8 * NT;
+  const unsigned gy = (unsigned)((R + RC - 1) / RC);
+  const int smem = kWarpsK3 * kStages * stage_doubles<NT>() * 8;
+  auto* const fn = k_sweep_warp<NT, VEC>;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  auto cfg_of = [&](dim3 grid, dim3 block, size_t sm) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = grid;
+    c.blockDim = block;
+    c.dynamicSmemBytes = sm;
+    c.stream = s->stream;
+    c.attrs = pdl;
+    c.numAttrs = 1;
+    return c;
+  };
+  // forward: sources z (S0), direct y (S2), reduce: y (S2) = / z (S0) -= ; backward: sources y (S2) and x (S0),
+  // direct x (S0), reduce x (S0) =
+  // timing experiments only (wrong results): PD_K3_EXP=1 skips the reduces, 2 skips the level kernels
+  static const int exp_mode = std::getenv("PD_K3_EXP") ? std::atoi(std::getenv("PD_K3_EXP")) : 0;
+  auto level = [&](const HostPlan::Sweep4& S, const Sweep4Dev& d, bool fwd, int j) {
+    const int w0 = S.lvl_warp[j], nw = S.lvl_warp[j + 1] - w0 - 1;
+    if (exp_mode != 2) {
+    cudaLaunchConfig_t c = cfg_of(dim3((unsigned)((nw + kWarpsK3 - 1) / kWarpsK3), gy), dim3(32 * kWarpsK3), smem);
+    CK(cudaLaunchKernelEx(&c, fn, d, w0, nw, R, (const double*)(fwd ? s->S0 : s->S2), (const double*)s->S0,
+                          fwd ? s->S2 : s->S0, s->Spart));
+    LAUNCH_CHECK(s);
+    }
+    const int r0 = S.lvl_red[j], nr = S.lvl_red[j + 1] - r0;
+    if (nr > 0 && exp_mode != 1) {
+      cudaLaunchConfig_t c2 = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
+      CK(cudaLaunchKernelEx(&c2, k_sweep_reduce4, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
+      LAUNCH_CHECK(s);
+    }
+  };
+  for (int j = 0; j < P.nlevels; ++j) level(P.fw4, s->sw4f, true, j);
+  if (s->pins_live) {
+    double* root = s->S0 + (int64_t)s->csup_first * R;
+    CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
+    level(P.bw4, s->sw4b, false, 0);
+    k_contact_fix<<<dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, s->stream>>>(
+        s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos, s->Qc, root);
+    LAUNCH_CHECK(s);
+    for (int j = 1; j < P.nlevels; ++j) level(P.bw4, s->sw4b, false, j);
+  } else {
+    for (int j = 0; j < P.nlevels; ++j) level(P.bw4, s->sw4b, false, j);
+  }
+}
+
 void solve_launch(pd_sim* s, int B) {
   const int R = 3 * B;
+  if (s->plan.k3_version == 4) {
+    if (R <= 8) (R % 2 == 0) ? solve_v4<1, true>(s, B) : solve_v4<1, false>(s, B);
+    else (R % 2 == 0) ? solve_v4<3, true>(s, B) : solve_v4<3, false>(s, B);
+    return;
+  }
   if (R <= 4) solve_rc<4, false>(s, B);
   else if (R <= 8) (R % 2 == 0) ? solve_rc<8, true>(s, B) : solve_rc<8, false>(s, B);
   else if (R <= 24) (R % 2 == 0) ? solve_rc<24, true>(s, B) : solve_rc<24, false>(s, B);
@@ -660,6 +723,14 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     const double yref = opts->youngs_ref > 0 ? opts->youngs_ref : mat->youngs;
     const double w_ref = yref / (1.0 + mat->poisson);
     bool numerical = false;
+    {  // K3 schedule version (env PD_K3_V = 3 selects the round-1 chain/item schedule) and the warps a v4 level
+       // launch is split for: one CTA of kWarpsK3 warps per SM
+      s->plan.k3_version = 4;
+      if (const char* ev = std::getenv("PD_K3_V")) s->plan.k3_version = std::atoi(ev) == 3 ? 3 : 4;
+      int dev = 0, nsm = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      s->plan.k3_warps = std::max(1, nsm) * kWarpsK3;
+    }
     std::string e = build_plan(s->plan, mesh->n_nodes, mesh->n_elems, mesh->rest_xyz, mesh->hex8, mesh->dx,
                                mat->density, h, fixed_dofs, n_fixed, w_ref, mat->muscle_w, fiber, opts->contact_nodes,
                                opts->n_contact, &numerical);
@@ -703,9 +774,31 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     };
     if (const char* e = std::getenv("PD_K3_MMA")) s->k3_mma = std::atoi(e) ? 1 : 0;
     if (const char* e = std::getenv("PD_K3_NBUF")) s->k3_nbuf = std::min(4, std::max(2, std::atoi(e)));
-    up_sweep(P.fw, s->swf);
-    up_sweep(P.bw, s->swb);
-    s->Spart = s->alloc<double>((std::max(P.fw.max_partial_rows, P.bw.max_partial_rows) + 32) * 3 * s->Bmax);
+    auto up_sweep4 = [&](const HostPlan::Sweep4& S, Sweep4Dev& d) {
+      d.A = s->upload(S.A);
+      d.krow = s->upload(S.krow);
+      d.pstart = s->upload(S.pstart);
+      d.pkg = s->upload(S.pkg);
+      d.pout = s->upload(S.pout);
+      d.pnv = s->upload(S.pnv);
+      d.wg = s->upload(S.wg);
+      d.wpiece = s->upload(S.wpiece);
+      d.red_row = s->upload(S.red_row);
+      d.red_mode = s->upload(S.red_mode);
+      d.red_ptr = s->upload(S.red_ptr);
+      d.red_src = s->upload(S.red_src);
+    };
+    int64_t max_prows = 0;
+    if (P.k3_version == 4) {
+      up_sweep4(P.fw4, s->sw4f);
+      up_sweep4(P.bw4, s->sw4b);
+      max_prows = std::max(P.fw4.max_partial_rows, P.bw4.max_partial_rows);
+    } else {
+      up_sweep(P.fw, s->swf);
+      up_sweep(P.bw, s->swb);
+      max_prows = std::max(P.fw.max_partial_rows, P.bw.max_partial_rows);
+    }
+    s->Spart = s->alloc<double>((max_prows + 32) * 3 * s->Bmax);
     const int64_t n3B = 3LL * P.n * s->Bmax;
     const int64_t sB = 3LL * P.nfree * s->Bmax;
     double** st_vecs[] = {&s->X, &s->V, &s->Y, &s->Xp, &s->Fext, &s->G, &s->W, &s->U, &s->Rv, &s->Z,

@@ -1098,6 +1098,209 @@ __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const do
   else dst_sub[o] = zo - acc;
 }
 
+// ----------------------------------------------------------------- K3 v4: warp ranges
+// One launch per level and sweep.  Warp w of the level streams the contiguous k-group range [wg[w], wg[w+1]) of
+// the factor stream through its own ring of kStages stages (no CTA barrier anywhere): a stage is 4 k-groups
+// (16 k-steps): the 4 KB factor block arrives by one cp.async.bulk (TMA) on the stage's mbarrier, the 16
+// right-hand-side rows (k-step sources, krow) by cp.async into padded rows; lane 0 issues stage j + kStages - 1
+// before the warp computes stage j.  Per k-group 4 x NT DMMA (m8n8k4 fp64) into a 32 x 8NT tile held in
+// registers; at the end of each piece the tile is stored to its direct rows or to its partial slot.  The
+// level's reduce (k_sweep_reduce4) then adds partial slots into their targets in piece order.
+constexpr int kStages = 3;         // ring depth per warp
+constexpr int kWarpsK3 = 8;        // warps per CTA
+template <int NT>
+__host__ __device__ constexpr int rhs_ld() { return NT == 1 ? 8 : 28; }  // padded RHS row (doubles): conflict-free B reads
+template <int NT>
+__host__ __device__ constexpr int stage_doubles() { return 4 * 128 + 16 * rhs_ld<NT>(); }
+
+template <int NT, bool VEC>
+__global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, int w0, int nwarps, int R,
+                                                                const double* __restrict__ srcA,
+                                                                const double* __restrict__ srcB,
+                                                                double* __restrict__ direct,
+                                                                double* __restrict__ partial) {
+  constexpr int RC = 8 * NT, LD = rhs_ld<NT>(), SD = stage_doubles<NT>();
+  // the next launch (reduce / next level) may be scheduled at once; its CTAs block in griddepcontrol.wait until
+  // this grid has completed and its writes are visible, so signalling at entry only hides launch latency
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(128) double smem4[];
+  __shared__ __align__(8) uint64_t bars[kWarpsK3][kStages];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.y * RC, rcn = min(RC, R - c0);
+  double* ring = smem4 + (size_t)wl * kStages * SD;
+  // RHS areas start finite (padding k-steps multiply stale rows by an exact zero factor entry)
+  for (int i = lane; i < kStages * 16 * LD; i += 32) ring[(i / (16 * LD)) * SD + 512 + i % (16 * LD)] = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < kStages; ++i) mbar_init(&bars[wl][i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  const int w = blockIdx.x * kWarpsK3 + wl;
+  if (w >= nwarps) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    return;
+  }
+  // Everything but the right-hand side is static plan data: the warp range, its first piece, the k-step rows
+  // and the factor blocks of the first kStages - 1 stages are fetched BEFORE griddepcontrol.wait, overlapping
+  // the previous launch (its tail / the previous level's reduce); only the RHS copies wait for it.
+  const int g0 = sw.wg[w0 + w], g1 = sw.wg[w0 + w + 1];
+  const int nst = (g1 - g0 + 3) >> 2;
+  // k-step source rows of stage j (lane i < 16: k-step i)
+  auto krow_of = [&](int j) {
+    const int gs = g0 + 4 * j;
+    return (j < nst && lane < 4 * min(4, g1 - gs)) ? __ldg(sw.krow + 4 * (int64_t)gs + lane) : -1;
+  };
+  // factor block of stage j by TMA (lane 0) on the stage's mbarrier
+  auto issue_factor = [&](int j) {
+    if (j >= nst || lane != 0) return;
+    const int slot = j % kStages;
+    const int gs = g0 + 4 * j, nkg = min(4, g1 - gs);
+    mbar_arrive_expect_tx(&bars[wl][slot], (unsigned)(nkg * 1024));
+    bulk_g2s(ring + slot * SD, sw.A + (int64_t)gs * 128, (unsigned)(nkg * 1024), &bars[wl][slot]);
+  };
+  // RHS rows of stage j by cp.async (16 rows x rcn columns over the lanes), one commit group per stage
+  auto issue_rhs = [&](int j, int kr) {
+    if (j < nst) {
+      double* zs = ring + (j % kStages) * SD + 512;
+      if (VEC) {  // 16-byte copies: (row, column pair) over the lanes
+        constexpr int CP = RC / 2;  // (16 * CP and 16 * RC are multiples of 32: every lane runs the same trips)
+        for (int e = lane; e < 16 * CP; e += 32) {
+          const int j2 = e / CP, c = 2 * (e - j2 * CP);
+          const int v = __shfl_sync(0xffffffffu, kr, j2 & 15);
+          if (v != -1 && c < rcn) {
+            const double* src = v >= 0 ? srcA + (int64_t)v * R : srcB + (int64_t)(-2 - v) * R;
+            cp_async16(zs + j2 * LD + c, src + c0 + c);
+          }
+        }
+      } else {
+        for (int e = lane; e < 16 * RC; e += 32) {
+          const int j2 = e / RC, c = e - j2 * RC;
+          const int v = __shfl_sync(0xffffffffu, kr, j2 & 15);
+          if (v != -1 && c < rcn) {
+            const double* src = v >= 0 ? srcA + (int64_t)v * R : srcB + (int64_t)(-2 - v) * R;
+            cp_async8(zs + j2 * LD + c, src + c0 + c);
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  int krs[kStages - 1];
+#pragma unroll
+  for (int j = 0; j < kStages - 1; ++j) {
+    issue_factor(j);
+    krs[j] = krow_of(j);
+  }
+  int kr_next = krow_of(kStages - 1);
+  int p = sw.wpiece[w0 + w];
+  int pe = sw.pstart[p] + sw.pkg[p];  // end (global k-group) of the current piece
+  int pout = sw.pout[p], pnv = sw.pnv[p];
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < kStages - 1; ++j) issue_rhs(j, krs[j]);
+  double acc[4][NT][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int j = 0; j < nst; ++j) {
+    __syncwarp();
+    fence_proxy_async();
+    issue_factor(j + kStages - 1);  // refills the slot of stage j - 1 (every lane is past it)
+    issue_rhs(j + kStages - 1, kr_next);
+    kr_next = krow_of(j + kStages);
+    const int slot = j % kStages;
+    cp_async_wait_group<kStages - 1>();
+    mbar_wait(&bars[wl][slot], (j / kStages) & 1);
+    __syncwarp();  // every lane's RHS copies of this stage are visible to the warp
+    const double2* As = reinterpret_cast<const double2*>(ring + slot * SD);
+    const double* Zs = ring + slot * SD + 512;
+    const int gs = g0 + 4 * j, nkg = min(4, g1 - gs);
+    for (int q = 0; q < nkg; ++q) {
+      const double2 a01 = As[(q * 2) * 32 + lane], a23 = As[(q * 2 + 1) * 32 + lane];
+      double b[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = Zs[(4 * q + t) * LD + 8 * n + g];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        dmma_8x8x4(acc[0][n][0], acc[0][n][1], a01.x, b[n]);
+        dmma_8x8x4(acc[1][n][0], acc[1][n][1], a01.y, b[n]);
+        dmma_8x8x4(acc[2][n][0], acc[2][n][1], a23.x, b[n]);
+        dmma_8x8x4(acc[3][n][0], acc[3][n][1], a23.y, b[n]);
+      }
+      if (gs + q + 1 == pe) {  // end of the piece: store the tile (rows 4g + m, columns 8n + 2t + {0, 1})
+        double* dst = pout >= 0 ? direct + (int64_t)pout * R : partial + (int64_t)(-1 - pout) * 32 * R;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int row = 4 * g + m;
+          if (row < pnv) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const int c = 8 * n + 2 * t;
+              double* d = dst + (int64_t)row * R + c0 + c;
+              if (VEC && c + 1 < rcn) {
+                *reinterpret_cast<double2*>(d) = make_double2(acc[m][n][0], acc[m][n][1]);
+              } else {
+                if (c < rcn) d[0] = acc[m][n][0];
+                if (c + 1 < rcn) d[1] = acc[m][n][1];
+              }
+            }
+          }
+#pragma unroll
+          for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+        }
+        if (gs + q + 1 < g1) {
+          ++p;
+          pe = sw.pstart[p] + sw.pkg[p];
+          pout = sw.pout[p];
+          pnv = sw.pnv[p];
+        }
+      }
+    }
+  }
+  cp_async_wait_all();
+}
+
+// Level reduce of K3 v4: target t (row, mode) = fixed-order sum of its partial rows; mode 0: dst_assign[row] = sum,
+// mode 1: dst_sub[row] -= sum.
+__global__ void k_sweep_reduce4(Sweep4Dev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
+                                double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = gi < (int64_t)ntarget * R;
+  // the target's static metadata and its first source indices before griddepcontrol.wait
+  const int t = live ? r0 + (int)(gi / R) : r0, c = live ? (int)(gi % R) : 0;
+  const int q0 = sw.red_ptr[t], q1 = sw.red_ptr[t + 1], mode = sw.red_mode[t];
+  const int64_t o = (int64_t)sw.red_row[t] * R + c;
+  int sq[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) sq[k] = q0 + k < q1 ? sw.red_src[q0 + k] : 0;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (!live) return;
+  const double zo = mode == 0 ? 0.0 : dst_sub[o];
+  double acc = 0;
+  {
+    double pv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pv[k] = q0 + k < q1 ? partial[(int64_t)sq[k] * R + c] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (q0 + k < q1) acc += pv[k];
+  }
+  int q = q0 + 4;
+  for (; q + 4 <= q1; q += 4) {
+    const int s0 = sw.red_src[q], s1 = sw.red_src[q + 1], s2 = sw.red_src[q + 2], s3 = sw.red_src[q + 3];
+    const double p0 = partial[(int64_t)s0 * R + c], p1 = partial[(int64_t)s1 * R + c];
+    const double p2 = partial[(int64_t)s2 * R + c], p3 = partial[(int64_t)s3 * R + c];
+    acc += p0;
+    acc += p1;
+    acc += p2;
+    acc += p3;
+  }
+  for (; q < q1; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
+  if (mode == 0) dst_assign[o] = acc;
+  else dst_sub[o] = zo - acc;
+}
+
 // ----------------------------------------------------------------- K5: contact
 // The candidate nodes V are ordered last: their rows form the root supernode, whose assembled
 // front is the Schur complement S = S_CC of A_s onto V.  For the z-column of sim b with pinned

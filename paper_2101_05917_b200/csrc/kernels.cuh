@@ -33,6 +33,12 @@ struct SweepDev {  // device copy of HostPlan::Sweep
   const int32_t *red_row, *red_mode, *red_ptr, *red_src;
 };
 
+struct Sweep4Dev {  // device copy of HostPlan::Sweep4 (K3 v4)
+  const double* A;
+  const int32_t *krow, *pstart, *pkg, *pout, *pnv, *wg, *wpiece;
+  const int32_t *red_row, *red_mode, *red_ptr, *red_src;
+};
+
 struct DotArgs {
   const double* u[3];
   const double* v[3];

@@ -86,6 +86,31 @@ struct HostPlan {
     int64_t max_partial_rows = 0;      // partial rows of the largest level
   } fw, bw;
   int chain_ctas = 148 * 4;            // CTAs a level launch is balanced for (chain length cap)
+  // ---- K3 v4 schedule (round 2): per level and sweep, the outputs are 32-lane tiles whose
+  // k-sequences are cut into k-groups of 4 k-steps (one 1 KB block of the stream each, MMA fragment order); the
+  // level's k-groups are stored tile after tile and split into equal contiguous ranges, one per warp ("stream-K":
+  // every warp streams the same number of bytes).  A PIECE is the part of one tile inside one warp's range: a
+  // piece covering its whole (direct-eligible) tile writes its output rows directly, every other piece writes a
+  // 32-row partial slot that the level's reduce adds, in piece order, into its target rows (deterministic).
+  int k3_version = 3;                  // 3: chain/item schedule (fw, bw above); 4: warp-range schedule (fw4, bw4)
+  int k3_warps = 148 * 8;              // warps a v4 level launch is split for
+  struct Sweep4 {
+    std::vector<double> A;             // k-groups (128 doubles each) of all levels, level-major, tile-major
+    std::vector<int32_t> lvl_g;        // [nlevels+1] first global k-group of each level
+    std::vector<int32_t> krow;         // [4 per k-group] right-hand-side row of each k-step: v >= 0 row v of source
+                                       //   A (z forward, y backward); v <= -2 row -2-v of source B (x backward);
+                                       //   -1 padding (zero factor column)
+    std::vector<int32_t> lvl_piece;    // [nlevels+1] pieces of level l
+    std::vector<int32_t> pstart, pkg;  // per piece: first global k-group, k-groups
+    std::vector<int32_t> pout;         // >= 0: direct output row of lane 0; < 0: partial slot -1-pout
+    std::vector<int32_t> pnv;          // valid lanes (output rows)
+    std::vector<int32_t> lvl_warp;     // [nlevels+1] offsets into wg / wpiece; level l uses W_l = lvl_warp[l+1] -
+                                       //   lvl_warp[l] - 1 warps
+    std::vector<int32_t> wg;           // warp range starts (global k-group), W_l + 1 per level (last = level end)
+    std::vector<int32_t> wpiece;       // first piece of each warp range (same indexing as wg)
+    std::vector<int32_t> lvl_red, red_row, red_mode, red_ptr, red_src;  // reduce, as in Sweep
+    int64_t max_partial_rows = 0;
+  } fw4, bw4;
   // ---- contact candidates: ordered LAST as one root supernode ----
   int nc = 0;                        // number of candidate nodes (0 = no contact)
   int csup = -1;                     // index of the candidate supernode (= nsup - 1)

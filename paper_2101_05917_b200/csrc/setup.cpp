@@ -412,6 +412,122 @@ static void build_solve_schedule(HostPlan& P, const std::vector<std::vector<int3
   }
 }
 
+// ---------------------------------------------------------------- K3 v4 schedule (warp ranges)
+// Tiles of a level in stream order.  Forward, supernode s: D tiles (rows i0..i0+32 of D_s over columns
+// 0..min(i0+32, ns), direct into y) then W tiles (rows i0..i0+32 of W_s over all ns columns, always partial: the
+// target rows R_s are shared with other supernodes of the level; z[target] -= sum).  Backward: column tiles c0 of
+// s over [D part: rows c0..ns of D_s | W part: rows 0..nr of W_s], direct into x[J_s].
+static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32_t>>& byh) {
+  const int L = 32;
+  auto Dval = [&](int s, int i, int k) -> double {  // D_s[i][k], packed lower
+    return k <= i ? P.D[P.doff[s] + (int64_t)i * (i + 1) / 2 + k] : 0.0;
+  };
+  auto Wval = [&](int s, int i, int k) -> double { return P.P[P.poff[s] + (int64_t)i * P.ssize[s] + k]; };
+  struct Tile {
+    int s, a0, nk, nv, out, mode;  // a0: D row / W row / column start; out >= 0 direct row, -1 always partial
+    int kind;                      // 0 forward D, 1 forward W, 2 backward column tile
+  };
+  for (int fwd = 1; fwd >= 0; --fwd) {
+    HostPlan::Sweep4& S = fwd ? P.fw4 : P.bw4;
+    S = HostPlan::Sweep4();
+    S.lvl_g.assign(1, 0);
+    S.lvl_piece.assign(1, 0);
+    S.lvl_warp.assign(1, 0);
+    S.lvl_red.assign(1, 0);
+    S.red_ptr.assign(1, 0);
+    for (int li = 0; li < P.nlevels; ++li) {
+      const int lev = fwd ? li : P.nlevels - 1 - li;  // backward levels in execution order (top down)
+      std::vector<Tile> tiles;
+      for (int s : byh[lev]) {
+        const int ns = P.ssize[s], f = P.sfirst[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        if (fwd) {
+          for (int i0 = 0; i0 < ns; i0 += L) tiles.push_back({s, i0, std::min(i0 + L, ns), std::min(L, ns - i0), f + i0, 0, 0});
+          for (int i0 = 0; i0 < nr; i0 += L) tiles.push_back({s, i0, ns, std::min(L, nr - i0), -1, 1, 1});
+        } else {
+          for (int c0 = 0; c0 < ns; c0 += L) tiles.push_back({s, c0, (ns - c0) + nr, std::min(L, ns - c0), f + c0, 0, 2});
+        }
+      }
+      // emit the tiles' k-groups (factor blocks + k-step source rows)
+      const int g_lev = S.lvl_g.back();
+      std::vector<int32_t> tile_g0(tiles.size() + 1, g_lev);
+      for (size_t ti = 0; ti < tiles.size(); ++ti) {
+        const Tile& T = tiles[ti];
+        const int s = T.s, ns = P.ssize[s], f = P.sfirst[s];
+        const int nkg = (T.nk + 3) / 4;
+        const int64_t base = (int64_t)S.A.size();
+        S.A.resize(base + (int64_t)nkg * 128, 0.0);
+        for (int k = 0; k < nkg * 4; ++k) {
+          int32_t row = -1;
+          if (k < T.nk) {
+            if (T.kind == 0 || T.kind == 1) row = f + k;
+            else row = k < ns - T.a0 ? f + T.a0 + k : -2 - P.rows[P.rptr[s] + (k - (ns - T.a0))];
+          }
+          S.krow.push_back(row);
+          if (k >= T.nk) continue;
+          double* blk = S.A.data() + base + (int64_t)(k / 4) * 128;
+          for (int l = 0; l < T.nv; ++l) {
+            double v;
+            if (T.kind == 0) v = Dval(s, T.a0 + l, k);
+            else if (T.kind == 1) v = Wval(s, T.a0 + l, k);
+            else v = k < ns - T.a0 ? Dval(s, T.a0 + k, T.a0 + l) : -Wval(s, k - (ns - T.a0), T.a0 + l);
+            blk[sweep_frag_pos(k & 3, l)] = v;
+          }
+        }
+        tile_g0[ti + 1] = tile_g0[ti] + nkg;
+      }
+      const int G = tile_g0.back() - g_lev;
+      S.lvl_g.push_back(g_lev + G);
+      // equal contiguous warp ranges (>= 4 k-groups = one TMA stage per warp on average)
+      const int W = std::max(1, std::min(P.k3_warps, G / 4));
+      std::vector<int32_t> wb(W + 1);
+      for (int w = 0; w <= W; ++w) wb[w] = g_lev + (int32_t)((int64_t)G * w / W);
+      // pieces = tiles cut at the warp boundaries; partial slots numbered per level
+      std::map<std::pair<int32_t, int32_t>, std::vector<int32_t>> targets;  // (mode, row) -> partial rows
+      int64_t slot = 0;
+      size_t ti = 0;
+      const int p_lev0 = (int)S.pstart.size();
+      for (int w = 0; w < W; ++w) {
+        S.wg.push_back(wb[w]);
+        S.wpiece.push_back((int32_t)S.pstart.size());
+        int g = wb[w];
+        while (g < wb[w + 1]) {
+          while (tile_g0[ti + 1] <= g) ++ti;
+          const Tile& T = tiles[ti];
+          const int ge = std::min(wb[w + 1], tile_g0[ti + 1]);
+          const bool whole = g == tile_g0[ti] && ge == tile_g0[ti + 1];
+          S.pstart.push_back(g);
+          S.pkg.push_back(ge - g);
+          S.pnv.push_back(T.nv);
+          if (whole && T.out >= 0) {
+            S.pout.push_back(T.out);
+          } else {
+            S.pout.push_back((int32_t)(-1 - slot));
+            for (int l = 0; l < T.nv; ++l) {
+              const int32_t row = T.kind == 1 ? P.rows[P.rptr[T.s] + T.a0 + l] : T.out + l;
+              targets[{T.mode, row}].push_back((int32_t)(slot * L + l));
+            }
+            ++slot;
+          }
+          g = ge;
+        }
+      }
+      S.wg.push_back(wb[W]);
+      S.wpiece.push_back((int32_t)S.pstart.size());
+      S.lvl_warp.push_back((int32_t)S.wg.size());
+      S.lvl_piece.push_back((int32_t)S.pstart.size());
+      (void)p_lev0;
+      for (auto& kv : targets) {  // sorted by (mode, row); sources in piece order
+        S.red_row.push_back(kv.first.second);
+        S.red_mode.push_back(kv.first.first);
+        for (int32_t r : kv.second) S.red_src.push_back(r);
+        S.red_ptr.push_back((int32_t)S.red_src.size());
+      }
+      S.lvl_red.push_back((int32_t)S.red_row.size());
+      S.max_partial_rows = std::max<int64_t>(S.max_partial_rows, slot * L);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- build
 std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int32_t* hex8,
                        double dx, double density, double h, const int32_t* fixed_dofs,
@@ -761,7 +877,8 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
 
   // ---------------- solve schedule (K3 v3)
   P.nlevels = H + 1;
-  build_solve_schedule(P, byh);
+  if (P.k3_version == 4) build_warp_schedule(P, byh);
+  else build_solve_schedule(P, byh);
   return "";
 }
 

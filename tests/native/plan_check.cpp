@@ -26,6 +26,9 @@ int main(int argc, char** argv) {
   std::vector<int32_t> cand;
   if (contact) for (int j = 0; j <= ny; ++j) for (int i = 0; i <= nx; ++i) if (!fix || i > 0) cand.push_back(nid(i, j, 0));
   HostPlan P; bool num; double fib[3] = {1, 0, 0};
+  // PLAN_V=4: the K3 v4 warp-range schedule (PLAN_WARPS warps per level launch, default 148 x 8)
+  if (const char* v = std::getenv("PLAN_V")) P.k3_version = std::atoi(v);
+  if (const char* v = std::getenv("PLAN_WARPS")) P.k3_warps = std::atoi(v);
   std::string e = build_plan(P, n, m, rest.data(), hex.data(), dx, 1e3, 0.01, fixed.data(), (int)fixed.size(),
                              1e5 / 1.45, 1e5 / 1.45, fib, cand.data(), (int)cand.size(), &num);
   if (contact) {  // the candidate block is the last supernode and Scc = L_cc L_cc^T
@@ -116,6 +119,70 @@ int main(int argc, char** argv) {
                S->lvl_item[l + 1] - S->lvl_item[l], S->lvl_chain[l + 1] - S->lvl_chain[l], lmax,
                S->lvl_red[l + 1] - S->lvl_red[l], bytes / 1e6);
       }
+  // v4: per level, every warp range walked piece by piece (k-groups in order, k-steps through krow), outputs to
+  // direct rows or partial slots, then the level's reduce (targets in order, sources in order)
+  auto run4 = [&](const HostPlan::Sweep4& S, std::vector<double>& zsrc, std::vector<double>& direct,
+                  std::vector<double>* zsub, bool fwd) {
+    std::vector<double> part((size_t)(S.max_partial_rows + 32), 0.0);
+    std::vector<int> assigned(N, 0);
+    if ((int)S.lvl_g.size() != P.nlevels + 1 || (int)S.lvl_warp.size() != P.nlevels + 1) { printf("bad v4 level index\n"); exit(20); }
+    for (int lev = 0; lev < P.nlevels; ++lev) {
+      const int w0 = S.lvl_warp[lev], W = S.lvl_warp[lev + 1] - w0 - 1;
+      if (S.wg[w0] != S.lvl_g[lev] || S.wg[w0 + W] != S.lvl_g[lev + 1]) { printf("warp ranges do not cover level %d\n", lev); exit(21); }
+      std::vector<int> pused((size_t)(S.max_partial_rows / 32 + 1), 0);
+      for (int w = 0; w < W; ++w) {
+        int p = S.wpiece[w0 + w];
+        int g = S.wg[w0 + w];
+        while (g < S.wg[w0 + w + 1]) {
+          if (S.pstart[p] != g || S.pkg[p] < 1) { printf("piece %d does not start at %d\n", p, g); exit(22); }
+          std::vector<double> acc(32, 0.0);
+          for (int gg = g; gg < g + S.pkg[p]; ++gg)
+            for (int j = 0; j < 4; ++j) {
+              const int v = S.krow[4 * (int64_t)gg + j];
+              if (v == -1) continue;
+              const double src = fwd ? zsrc[v] : (v >= 0 ? y[v] : x[-2 - v]);
+              for (int l = 0; l < 32; ++l) acc[l] += S.A[(int64_t)gg * 128 + sweep_frag_pos(j, l)] * src;
+            }
+          const int o = S.pout[p];
+          for (int l = 0; l < S.pnv[p]; ++l) {
+            if (o >= 0) {
+              if (assigned[o + l]++) { printf("row %d written twice\n", o + l); exit(10); }
+              direct[o + l] = acc[l];
+            } else {
+              if (l == 0 && pused[-o - 1]++) { printf("partial slot %d reused in a level\n", -o - 1); exit(15); }
+              part[(size_t)(-o - 1) * 32 + l] = acc[l];
+            }
+          }
+          g += S.pkg[p];
+          ++p;
+        }
+        if (p != S.wpiece[w0 + w + 1]) { printf("warp %d piece count mismatch\n", w); exit(23); }
+      }
+      for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) {
+        double acc = 0;
+        for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
+        if (S.red_mode[r] == 0) {
+          if (assigned[S.red_row[r]]++) { printf("row %d written twice\n", S.red_row[r]); exit(10); }
+          direct[S.red_row[r]] = acc;
+        } else {
+          (*zsub)[S.red_row[r]] -= acc;
+        }
+      }
+    }
+    for (int p = 0; p < N; ++p)
+      if (assigned[p] != 1) { printf("row %d written %d times\n", p, assigned[p]); exit(11); }
+  };
+  if (P.k3_version == 4) {
+    run4(P.fw4, z, y, &z, true);
+    run4(P.bw4, y, x, nullptr, false);
+    double err = 0, mx = 0;
+    for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
+    int64_t pieces = (int64_t)P.fw4.pstart.size() + (int64_t)P.bw4.pstart.size();
+    printf("v4 n=%d nfree=%d nsup=%d levels=%d kgroups fw=%d bw=%d pieces=%lld partial rows fw=%lld bw=%lld nnzL=%lld relerr=%.3e\n",
+           n, N, P.nsup, P.nlevels, P.fw4.lvl_g.back(), P.bw4.lvl_g.back(), (long long)pieces,
+           (long long)P.fw4.max_partial_rows, (long long)P.bw4.max_partial_rows, (long long)P.nnzL, err / mx);
+    return err / mx < 1e-10 ? 0 : 2;
+  }
   run(P.fw, z, y, &z, true);
   run(P.bw, y, x, nullptr, false);
   double err = 0, mx = 0;

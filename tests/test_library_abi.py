@@ -55,3 +55,8 @@ def test_native_plan_factorisation():
                  ["20", "20", "4", "0", "1"], ["6", "4", "3", "0", "1"], ["8", "4", "4", "1", "1"]):
         r = subprocess.run([exe] + args, capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
+        # the K3 v4 warp-range schedule, at the GPU's warp count and at an odd one
+        for warps in ("1184", "37"):
+            r = subprocess.run([exe] + args, capture_output=True, text=True,
+                               env=dict(os.environ, PLAN_V="4", PLAN_WARPS=warps))
+            assert r.returncode == 0, r.stdout + r.stderr
