@@ -54,7 +54,8 @@ def build(force=False, verbose=False):
     log.append(_run(["g++", "-O3", "-std=c++17", "-fopenmp", "-fPIC", "-march=x86-64-v3",
                      "-c", os.path.join(CSRC, "setup.cpp"), "-o", setup_o] + inc))
     capi_o = os.path.join(BUILD, "capi.o")
-    log.append(_run([nvcc] + ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v",
+    extra = [f"-DK1_MIN_BLOCKS={int(os.environ['PD_K1_MIN_BLOCKS'])}"] if os.environ.get("PD_K1_MIN_BLOCKS") else []
+    log.append(_run([nvcc] + ARCH + extra + ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v",
                                      "-Xcompiler", "-fPIC", "-c", os.path.join(CSRC, "capi.cu"),
                                      "-o", capi_o] + inc))
     tmp = LIB + ".tmp"

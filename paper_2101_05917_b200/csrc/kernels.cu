@@ -197,6 +197,56 @@ __device__ void polar_rotation(const double* F, double* R) {
   polar_newton(F, R);
 }
 
+// 1/sqrt(x) for normal x > 0 without the libm slow-path call (whose register saves would put the caller's live
+// values in local memory): hardware approximation + two Newton steps (relative error a few ulp of fp64).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = x * y;
+  double r = fma(-h, y, 1.0);
+  y = fma(0.5 * y, r, y);
+  h = x * y;
+  r = fma(-h, y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
+// K1's polar without address-taken arrays on the common path: Newton-Schulz inline (as polar_rotation);
+// returns false when F needs the SVD or scaled-Newton fallback (det F <= 1e-6 ||F||^3, or no convergence in 14
+// iterations).  F and R stay in registers: no call frame, no local memory on the common path.
+__device__ __forceinline__ bool polar_ns(const double (&F)[9], double (&R)[9]) {
+  const double d0 = det3(F);
+  double fn2 = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) fn2 += F[i] * F[i];
+  if (!(fn2 > 1e-250)) return false;
+  const double ifn = rsqrt_nr(fn2);  // 1/||F||_F
+  if (!(d0 > 1e-6 * fn2 * fn2 * ifn)) return false;
+  const double c = 1.7320508075688772 * ifn;  // sqrt(3)/||F||_F
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = c * F[i];
+  for (int it = 0; it < 14; ++it) {
+    const double c00 = R[0] * R[0] + R[3] * R[3] + R[6] * R[6];
+    const double c11 = R[1] * R[1] + R[4] * R[4] + R[7] * R[7];
+    const double c22 = R[2] * R[2] + R[5] * R[5] + R[8] * R[8];
+    const double c01 = R[0] * R[1] + R[3] * R[4] + R[6] * R[7];
+    const double c02 = R[0] * R[2] + R[3] * R[5] + R[6] * R[8];
+    const double c12 = R[1] * R[2] + R[4] * R[5] + R[7] * R[8];
+    const double d = (c00 - 1) * (c00 - 1) + (c11 - 1) * (c11 - 1) + (c22 - 1) * (c22 - 1) +
+                     2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
+    const double y00 = 1.5 - 0.5 * c00, y11 = 1.5 - 0.5 * c11, y22 = 1.5 - 0.5 * c22;
+    const double y01 = -0.5 * c01, y02 = -0.5 * c02, y12 = -0.5 * c12;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double a0 = R[3 * i], a1 = R[3 * i + 1], a2 = R[3 * i + 2];
+      R[3 * i] = a0 * y00 + a1 * y01 + a2 * y02;
+      R[3 * i + 1] = a0 * y01 + a1 * y11 + a2 * y12;
+      R[3 * i + 2] = a0 * y02 + a1 * y12 + a2 * y22;
+    }
+    if (d < 1e-16) return true;
+  }
+  return false;
+}
+
 // ----------------------------------------------------------------- layout kernels
 __global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
                                int64_t in_bstride = -1) {
@@ -239,6 +289,9 @@ __global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
 }
 
 // ----------------------------------------------------------------- K1: local step
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 5  // resident 256-thread blocks per SM the register allocation targets
+#endif
 // One thread per (element, sim, quad point), q fastest: the 8 quadrature points of an
 // (element, sim) pair are 8 consecutive lanes; their 24 nodal force contributions are summed by a
 // 3-stage xor butterfly (identical bits in all 8 lanes: fixed pairing, commutative adds), then lane q
@@ -325,9 +378,21 @@ __device__ __forceinline__ void store_force(const double* Pm, const DNTab& dt, i
   }
 }
 
-__global__ void __launch_bounds__(256, 5) k_elem_residual(const double* __restrict__ X, Stencil st, ElemArgs ea,
-                                                       double* __restrict__ EF, double* __restrict__ EE) {
+// K1's rare fallback (SVD / scaled Newton, polar_rotation): recomputes F from x itself so that the caller's F
+// never needs an address; R goes to `out` (the thread's slot of the group's shared-memory area).
+__device__ __noinline__ void k1_polar_fallback(const double* __restrict__ X, const int32_t* __restrict__ hex8,
+                                               const DNTab* dt, int e, int b, int q, int B, double* out) {
+  double F[9], R[9];
+  load_F(X, hex8, *dt, e, b, q, B, F);
+  polar_rotation(F, R);
+  for (int k = 0; k < 9; ++k) out[k] = R[k];
+}
+
+__global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const double* __restrict__ X, Stencil st,
+                                                                    ElemArgs ea, double* __restrict__ EF,
+                                                                    double* __restrict__ EE) {
   __shared__ DNTab dnt;
+  __shared__ __align__(16) double Psm[32][kPsSlot];
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int B = ea.B;
@@ -335,13 +400,17 @@ __global__ void __launch_bounds__(256, 5) k_elem_residual(const double* __restri
   const int q = (int)(tid & 7);
   // dead lanes (past the end) compute on pair 0 and store nothing: every shuffle sees a full warp
   const bool live = pair < (int64_t)ea.m * B;
-  const int64_t pr = live ? pair : 0;
-  const int e = (int)(pr / B), b = (int)(pr - (int64_t)e * B);
+  const int pr = live ? (int)pair : 0;  // (m B < 2^31: 32-bit division, no 64-bit division call)
+  const int e = pr / B, b = pr - e * B;
   const double w = ea.w_sim[b];
-  double F[9];
+  double F[9], R[9];
   load_F(X, ea.hex8, dnt, e, b, q, B, F);
-  double R[9];
-  polar_rotation(F, R);
+  if (!polar_ns(F, R)) {  // rare: SVD (det F <= 1e-6 ||F||^3) or scaled Newton; R through this thread's slot
+    double* slot = &Psm[threadIdx.x >> 3][10 * q];
+    k1_polar_fallback(X, ea.hex8, &dnt, e, b, q, B, slot);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = slot[k];
+  }
   double Pm[9];
   double en = 0;
 #pragma unroll
@@ -353,17 +422,18 @@ __global__ void __launch_bounds__(256, 5) k_elem_residual(const double* __restri
   double energy = 0.5 * w * st.V * en;
   if (st.w_m != 0.0) {
     const double r_act = ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
-    double Fm[3], nr = 0;
+    double Fm[3], nr2 = 0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-      nr += Fm[i] * Fm[i];
+      nr2 += Fm[i] * Fm[i];
     }
-    nr = sqrt(nr);
+    const bool pos = nr2 > 1e-250;
+    const double s_act = pos ? r_act * rsqrt_nr(nr2) : 0.0;  // r / ||Fm||
     double dm[3], em = 0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double p = nr > 0 ? r_act * Fm[i] / nr : r_act * st.fiber[i];
+      const double p = pos ? s_act * Fm[i] : r_act * st.fiber[i];
       dm[i] = Fm[i] - p;
       em += dm[i] * dm[i];
     }
@@ -373,7 +443,7 @@ __global__ void __launch_bounds__(256, 5) k_elem_residual(const double* __restri
 #pragma unroll
       for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
   }
-  __shared__ __align__(16) double Psm[32][kPsSlot];
+  __syncwarp();  // (the slot may have carried a fallback R: every lane has read its own before it is reused)
   store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
   energy = qsum8(energy);
   if (live && EE && q == 0) EE[(int64_t)e * B + b] = energy;
