@@ -33,6 +33,9 @@ def hessian_blocks(scene, x, w, act=None):
     G = fem.G_matrices(scene.dx)
     I9 = np.eye(9)
     H = w * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - J, G, optimize=True)
+    if getattr(scene, "volume", False):                             # w_v G^T (I - dD/dF) G
+        Jv = energy.volume_jacobian(F)
+        H = H + w * scene.vol_ratio * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - Jv, G, optimize=True)
     if scene.muscle:
         Fm = F @ np.asarray(scene.fiber)
         r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
@@ -69,11 +72,12 @@ def solve_adjoint(scene, x, w, act, b, cons_mask, solver="direct", rtol=1e-13):
 
 
 def param_terms(scene, x, u, act=None):
-    """(dL/dw, dL/dr[m]) contributions of one step (chain rule)."""
+    """(dL/dw, dL/dr[m], dL/dw_v) contributions of one step (chain rule)."""
     F = fem.deformation_gradients(x, scene.hex8, scene.dx)
     R, S, V, s = energy.polar_svd(F)
     Gu = fem.deformation_gradients(u, scene.hex8, scene.dx)         # G_q u_e
     dw = -scene.V * np.sum(Gu * (F - R))
+    dwv = -scene.V * np.sum(Gu * (F - energy.volume_project(F)[0])) if getattr(scene, "volume", False) else 0.0
     dr = None
     if scene.muscle:
         Fm = F @ np.asarray(scene.fiber)
@@ -81,7 +85,7 @@ def param_terms(scene, x, u, act=None):
         p, n_hat, nrm = energy.muscle_project(Fm, r, scene.fiber)
         Gmu = Gu @ np.asarray(scene.fiber)
         dr = scene.w_muscle * scene.V * np.sum(n_hat * Gmu, axis=(-1, -2))
-    return dw, dr
+    return dw, dr, dwv
 
 
 def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL_dv_steps=None, solver="direct"):
@@ -106,6 +110,7 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
     dfext = np.zeros(scene.N)
     dfext_steps = np.zeros((T, scene.N))
     dw_tot = 0.0
+    dwv_tot = 0.0
     dact = np.zeros((T, scene.m)) if scene.muscle else None
     for i in range(T - 1, -1, -1):
         x1 = traj["q"][i + 1]
@@ -123,8 +128,9 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
             AN = assemble_AN(scene, x1, w, a_i)
             extra = np.zeros_like(b)
             extra[pins] = b_pin - (AN @ u)[pins]
-        dw, dr = param_terms(scene, x1, u, a_i)
+        dw, dr, dwv = param_terms(scene, x1, u, a_i)
         dw_tot += dw
+        dwv_tot += dwv
         if dr is not None:
             dact[i] = dr
         dfext += u
@@ -141,9 +147,14 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
         av[base] = 0.0
     dfext[base] = 0.0
     dfext_steps[:, base] = 0.0
+    # w = 2 mu = E/(1+nu) (reading §8c.2) and, with the volume term, w_v = lambda = E nu/((1+nu)(1-2nu))
+    # (SPEC lame_weights): dL/dE and dL/dnu by the chain rule through both weights
     nu = scene.poisson
-    return dict(dq0=ax, dv0=av, dfext=dfext, dfext_steps=dfext_steps, dw=dw_tot,
-                dE=dw_tot / (1.0 + nu), dnu=-dw_tot * youngs / (1.0 + nu) ** 2, dact=dact)
+    dE = dw_tot / (1.0 + nu) + dwv_tot * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    dnu = (-dw_tot * youngs / (1.0 + nu) ** 2
+           + dwv_tot * youngs * (1.0 + 2.0 * nu ** 2) / ((1.0 + nu) ** 2 * (1.0 - 2.0 * nu) ** 2))
+    return dict(dq0=ax, dv0=av, dfext=dfext, dfext_steps=dfext_steps, dw=dw_tot, dwv=dwv_tot,
+                dE=dE, dnu=dnu, dact=dact)
 
 
 def loss_and_grad(inp, b, q, v):

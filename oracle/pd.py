@@ -61,6 +61,7 @@ class Scene:
     muscle: bool = False
     fiber: tuple = (1.0, 0.0, 0.0)
     contact_mode: str = "frictionless"   # or "sticky": the paper's infinite-friction model
+    volume: bool = False                 # volume-preserving term of the background elasticity
 
     def __post_init__(self):
         self.n = self.rest.shape[0]
@@ -81,13 +82,19 @@ class Scene:
         return youngs / (1.0 + self.poisson)
 
     @property
+    def vol_ratio(self):
+        """w_v / w with w_v = lambda (Lame) and w = 2 mu (SPEC lame_weights):
+        lambda / (2 mu) = nu / (1 - 2 nu); 0 without the volume term."""
+        return self.poisson / (1.0 - 2.0 * self.poisson) if self.volume else 0.0
+
+    @property
     def w_muscle(self):
         """w_m = 2 mu at the nominal material, constant (reading §8c.3)."""
         return self.youngs / (1.0 + self.poisson) if self.muscle else 0.0
 
     def A(self, w):
-        """A = M/h^2 + sum w G^T G (+ w_m G_m^T G_m)."""
-        A = sp.diags(self.mass / self.h ** 2) + w * self.Kcorot
+        """A = M/h^2 + sum (w + w_v) G^T G (+ w_m G_m^T G_m)  (both elastic terms have G = F)."""
+        A = sp.diags(self.mass / self.h ** 2) + w * (1.0 + self.vol_ratio) * self.Kcorot
         if self.muscle:
             A = A + self.w_muscle * self.Kmus
         return A.tocsr()
@@ -110,10 +117,12 @@ class Scene:
         return x + self.h * v + self.h ** 2 * (g + f_ext / self.mass)
 
     def local_step(self, x, act=None):
-        """z* = Proj_M(G x) per quad point: R (SO(3)) and p (muscle sphere)."""
+        """z* = Proj_M(G x) per quad point: R (SO(3)), D (det = 1) and p (muscle sphere)."""
         F = fem.deformation_gradients(x, self.hex8, self.dx)     # [m,8,3,3]
         R, S, V, s = energy.polar_svd(F)
         out = dict(F=F, R=R)
+        if self.volume:
+            out["D"] = energy.volume_project(F)[0]
         if self.muscle:
             Fm = F @ np.asarray(self.fiber)
             r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
@@ -127,6 +136,11 @@ class Scene:
         D = F - R
         E = 0.5 * w * self.V * np.sum(D * D)
         P = w * self.V * D
+        if self.volume:
+            wv = w * self.vol_ratio
+            Dv = F - z["D"]
+            E += 0.5 * wv * self.V * np.sum(Dv * Dv)
+            P = P + wv * self.V * Dv
         if self.muscle:
             Dm = z["Fm"] - z["p"]
             E += 0.5 * self.w_muscle * self.V * np.sum(Dm * Dm)
@@ -137,6 +151,8 @@ class Scene:
     def rhs_d(self, y, z, w):
         """d = (1/h^2) M y + sum_e w_e G_e^T z_e*  (eq:pd_global, reading §8c.7)."""
         P = w * self.V * z["R"]
+        if self.volume:
+            P = P + w * self.vol_ratio * self.V * z["D"]
         if self.muscle:
             P = P + self.w_muscle * self.V * z["p"][..., :, None] * np.asarray(self.fiber)[None, None, None, :]
         return self.mass / self.h ** 2 * y + fem.scatter_element_forces(P, self.hex8, self.dx, self.n)
@@ -402,7 +418,7 @@ def scene_from_inputs(inp, youngs=None):
     return Scene(rest=inp["rest"], hex8=inp["hex8"], dx=cfg.dx, density=cfg.density, h=cfg.h,
                  youngs=cfg.youngs if youngs is None else youngs, poisson=cfg.poisson,
                  gravity=np.asarray(cfg.gravity, float), fixed_dofs=inp["fixed_dofs"],
-                 contact_nodes=inp["contact_nodes"], muscle=cfg.muscle,
+                 contact_nodes=inp["contact_nodes"], muscle=cfg.muscle, volume=getattr(cfg, "volume", False),
                  contact_mode=getattr(cfg, "contact_mode", "frictionless"))
 
 

@@ -44,6 +44,7 @@ class Config:
     contact: bool = False    # bottom-face nodes are contact candidates (plane z=0)
     contact_mode: str = "frictionless"  # or "sticky" (the paper's infinite-friction nodes)
     muscle: bool = False     # per-element fiber actuation along +x
+    volume: bool = False     # volume-preserving PD energy with w_v = lambda
     loss: str = "linear_qv"  # "linear_q" | "linear_qv" | "tip"
     v0_std: float = 0.0      # N(0, v0_std) per free node component
     per_sim_youngs: bool = False  # lognormal(ln E, 0.3) per sim (c3)
@@ -91,6 +92,10 @@ CONFIGS = {
                   lift=0.001, max_tilt_deg=10.0),
     "c5s": Config("c5s", (6, 4, 3), h=0.01, steps=6, batch=2, seed=105, contact=True,
                   muscle=True),
+    # ---- volume-preserving energy variants: the c2 / c5 recipes with the volume term ----
+    "c2v": Config("c2v", (8, 4, 4), h=0.01, steps=6, batch=2, seed=202, dirichlet="x0", v0_std=0.1,
+                  per_sim_youngs=True, volume=True),
+    "c5v": Config("c5v", (6, 4, 3), h=0.01, steps=5, batch=2, seed=205, contact=True, muscle=True, volume=True),
 }
 
 

@@ -92,3 +92,74 @@ def test_muscle_projection():
         Jfd[:, k] = (energy.muscle_project((Fm + e)[None], np.array([r]), m)[0][0]
                      - energy.muscle_project((Fm - e)[None], np.array([r]), m)[0][0]) / 2e-6
     np.testing.assert_allclose(J[0], Jfd, atol=1e-8)
+
+
+# ----------------------------------------------------------------- volume preservation
+def _rand_F(n, seed, scale=0.3):
+    rng = np.random.default_rng(seed)
+    F = np.eye(3) + scale * rng.standard_normal((n, 3, 3))
+    return F[np.linalg.det(F) > 0.05]
+
+
+def test_volume_projection_is_the_closest_det1_matrix():
+    # D = U diag(Sigma + d*) V^T has det D = 1, and no det-1 neighbour D exp(eps X), tr X = 0, is closer
+    from scipy.linalg import expm
+    F = _rand_F(200, 0)
+    D = energy.volume_project(F)[0]
+    assert np.abs(np.linalg.det(D) - 1).max() < 1e-13
+    rng = np.random.default_rng(1)
+    dist = np.linalg.norm(F - D, axis=(1, 2))
+    for _ in range(20):
+        X = rng.standard_normal(F.shape)
+        X -= np.trace(X, axis1=1, axis2=2)[:, None, None] * np.eye(3) / 3
+        for eps in (1e-2, 1e-3):
+            Dp = np.array([D[i] @ expm(eps * X[i]) for i in range(len(F))])
+            assert np.all(np.linalg.norm(F - Dp, axis=(1, 2)) >= dist - 1e-14)
+
+
+def test_volume_projection_special_cases():
+    # fixed point on the manifold; rotation invariance D(Q F) = Q D(F); uniform scaling F = a I -> D = I
+    F = _rand_F(50, 2)
+    D = energy.volume_project(F)[0]
+    np.testing.assert_allclose(energy.volume_project(D)[0], D, atol=1e-13)
+    from scipy.spatial.transform import Rotation
+    Q = Rotation.random(len(F), random_state=3).as_matrix()
+    np.testing.assert_allclose(energy.volume_project(Q @ F)[0], Q @ D, atol=1e-12)
+    for a in (0.5, 1.0, 2.0):
+        np.testing.assert_allclose(energy.volume_project(a * np.eye(3)[None])[0][0], np.eye(3), atol=1e-14)
+    # diagonal F: the KKT point in closed form, z_i (z_i - s_i) = -lam for all i
+    s = np.array([[1.2, 0.9, 0.8], [0.7, 0.7, 1.5]])
+    d, lam = energy.volume_kkt(s)
+    z = s + d
+    np.testing.assert_allclose(z * (z - s), -lam[:, None] * np.ones(3), atol=1e-13)
+    np.testing.assert_allclose(np.prod(z, 1), 1.0, atol=1e-14)
+
+
+def test_volume_kkt_jacobian_vs_finite_difference():
+    # eq:vol_kkt: d(Sigma + d*)/dSigma against central differences of the KKT solution
+    s = np.array([[1.2, 0.9, 0.8], [1.0, 1.0, 1.0], [0.6, 1.3, 1.1]])
+    d, lam = energy.volume_kkt(s)
+    J = energy.volume_dg(s, d, lam)
+    eps = 1e-6
+    for k in range(3):
+        e = np.zeros(3)
+        e[k] = eps
+        gp = s + e + energy.volume_kkt(s + e)[0]
+        gm = s - e + energy.volume_kkt(s - e)[0]
+        np.testing.assert_allclose(J[:, :, k], (gp - gm) / (2 * eps), rtol=1e-7, atol=1e-9)
+
+
+def test_volume_derivative_vs_finite_difference():
+    # full dD/dF (KKT Jacobian + SVD chain rule) against central differences, including a repeated singular
+    # value (F = diag(1.1, 0.9, 0.9) rotated) where the ratio (g_i - g_j)/(s_i - s_j) takes its limit
+    from scipy.spatial.transform import Rotation
+    F = _rand_F(100, 4)
+    Q = Rotation.random(2, random_state=5).as_matrix()
+    F = np.concatenate([F, (Q[0] @ np.diag([1.1, 0.9, 0.9]) @ Q[1])[None]], 0)
+    rng = np.random.default_rng(6)
+    dF = rng.standard_normal(F.shape)
+    eps = 1e-6
+    fd = (energy.volume_project(F + eps * dF)[0] - energy.volume_project(F - eps * dF)[0]) / (2 * eps)
+    an = energy.volume_derivative(F, dF)
+    err = np.linalg.norm(fd - an, axis=(1, 2)) / np.linalg.norm(fd, axis=(1, 2))
+    assert err.max() < 1e-6, err.max()
