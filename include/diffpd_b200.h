@@ -59,6 +59,10 @@ typedef struct {
   double muscle_w;
   double gravity[3];
   double fiber[3];
+  int32_t volume;         /* 1: add the volume-preserving PD energy (w_v/2)||F - D||^2, D the projection of F onto
+                             det D = 1, with w_v = lambda = E nu / ((1+nu)(1-2nu)) per sim (SPEC lame_weights,
+                             DESIGN.md §2.16); its Jacobian from the differentiated KKT system.
+                             pd_backward's dL_dE and dL_dnu then include the w_v terms.  0: corotated only.      */
 } pd_material;
 
 /* Solver options.  Tolerances are on the relative residual

@@ -61,7 +61,7 @@ class Simulator:
                  tol_fwd=1e-9, tol_adj=1e-9, max_iter_fwd=20000, max_iter_adj=20000, fixed_iter=0,
                  accel_fwd=1, accel_adj=1, check_every=1, max_batch=1, max_steps=1, youngs_ref=0.0,
                  max_outer=10, eps_phi=None, profile=0, outer_warm=1, x0_predict=0, contact_mode=1,
-                 lbfgs_warm=0):
+                 lbfgs_warm=0, volume=False):
         self.lib = _lib.load()
         rest = np.ascontiguousarray(rest, dtype=np.float64)
         hex8 = np.ascontiguousarray(hex8, dtype=np.int32)
@@ -71,7 +71,7 @@ class Simulator:
         mesh = _lib.PdMesh(self.n_nodes, self.n_elems, rest.ctypes.data_as(_lib.dp),
                            hex8.ctypes.data_as(_lib.ip), float(dx))
         mat = _lib.PdMaterial(float(youngs), float(poisson), float(density), float(muscle_w),
-                              (C.c_double * 3)(*gravity), (C.c_double * 3)(*fiber))
+                              (C.c_double * 3)(*gravity), (C.c_double * 3)(*fiber), int(bool(volume)))
         fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int32)
         cand = np.ascontiguousarray(contact_nodes, dtype=np.int32)
         self._keep += [fixed, cand]
@@ -218,6 +218,7 @@ def simulator_from_inputs(inp, **kw):
     cfg = inp["cfg"]
     muscle_w = cfg.youngs / (1 + cfg.poisson) if cfg.muscle else 0.0
     args = dict(contact_mode=2 if getattr(cfg, "contact_mode", "frictionless") == "sticky" else 1,
+                volume=getattr(cfg, "volume", False),
                 youngs=cfg.youngs, poisson=cfg.poisson, density=cfg.density, h=cfg.h, gravity=cfg.gravity,
                 fixed_dofs=inp["fixed_dofs"], contact_nodes=inp["contact_nodes"], muscle_w=muscle_w,
                 fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"])

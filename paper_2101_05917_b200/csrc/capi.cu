@@ -59,6 +59,7 @@ struct pd_sim {
   double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
   double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR, *JC;
   double *w_sim, *youngs_sim, *dots, *partial, *alpha, *beta, *rz, *bb, *dw_acc, *act;
+  double *DWV = nullptr, *dwv_acc = nullptr;  // volume-weight parameter terms (material.volume)
   // per-sim weights of the diagnostic hooks (pd_eval_objective / pd_apply_AN): kept apart from w_sim / youngs_sim,
   // which pd_backward reuses from the last pd_forward
   double *w_diag = nullptr, *youngs_diag = nullptr;
@@ -410,6 +411,12 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
     k_elem_residual<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
                                                                          s->EF, s->EE);
     LAUNCH_CHECK(s);
+    if (s->st.kappa != 0.0) {  // volume-preserving term added to the element forces and energies
+      k_vol<0><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, nullptr, s->st,
+                                                                      elem_args(s, B, act_step, act_bstride), nullptr,
+                                                                      s->EF, s->EE);
+      LAUNCH_CHECK(s);
+    }
   }
   ProfScope ps(s, 1);
   const bool pin = s->pins_live;
@@ -433,6 +440,17 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
     k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st,
                                                                    elem_args(s, B, act_step, act_bstride), s->EF);
   LAUNCH_CHECK(s);
+  if (s->st.kappa != 0.0) {
+    if (jc)
+      k_vol<1><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(nullptr, Pin, s->st,
+                                                                      elem_args(s, B, act_step, act_bstride),
+                                                                      const_cast<double*>(jc), s->EF, nullptr);
+    else
+      k_vol<2><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st,
+                                                                      elem_args(s, B, act_step, act_bstride), nullptr,
+                                                                      s->EF, nullptr);
+    LAUNCH_CHECK(s);
+  }
   const bool pin = s->pins_live;
   k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                           s->d_fixed, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, OUT,
@@ -721,7 +739,9 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       for (double& f : fiber) f /= fn;
     }
     const double yref = opts->youngs_ref > 0 ? opts->youngs_ref : mat->youngs;
-    const double w_ref = yref / (1.0 + mat->poisson);
+    // volume-preserving term: w_v = lambda = w nu/(1 - 2 nu) per sim; A carries w + w_v
+    const double kappa = mat->volume ? mat->poisson / (1.0 - 2.0 * mat->poisson) : 0.0;
+    const double w_ref = yref / (1.0 + mat->poisson) * (1.0 + kappa);
     bool numerical = false;
     {  // K3 schedule version (env PD_K3_V = 3 selects the round-1 chain/item schedule) and the warps a v4 level
        // launch is split for: one CTA of kWarpsK3 warps per SM
@@ -746,6 +766,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->st.V = mesh->dx * mesh->dx * mesh->dx / 8.0;
     s->st.w_m = mat->muscle_w;
     s->st.clamp = 1e-6;
+    s->st.kappa = kappa;
     // ---- device residency
     s->d_hex8 = s->upload(P.hex8);
     s->d_inc_ptr = s->upload(P.inc_ptr);
@@ -808,7 +829,11 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->S1 = s->alloc<double>(sB);
     s->S2 = s->alloc<double>(sB);
     s->EF = s->alloc<double>((int64_t)P.m * 24 * s->Bmax);
-    s->JC = s->alloc<double>((int64_t)P.m * 8 * s->Bmax * (s->w_m != 0.0 ? kJC : 15));
+    s->JC = s->alloc<double>((int64_t)P.m * 8 * s->Bmax * (kappa != 0.0 ? kJC + kJCV : (s->w_m != 0.0 ? kJC : 15)));
+    if (kappa != 0.0) {
+      s->DWV = s->alloc<double>((int64_t)P.m * s->Bmax);
+      s->dwv_acc = s->alloc<double>(s->Bmax);
+    }
     s->EE = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DW = s->alloc<double>((int64_t)P.m * s->Bmax);
     s->DR = s->alloc<double>((int64_t)P.m * s->Bmax);
@@ -1121,6 +1146,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
     }
     CK(cudaMemsetAsync(s->DF, 0, len * sizeof(double), s->stream));
     CK(cudaMemsetAsync(s->dw_acc, 0, B * sizeof(double), s->stream));
+    if (s->dwv_acc) CK(cudaMemsetAsync(s->dwv_acc, 0, B * sizeof(double), s->stream));
     const int64_t sstride = (int64_t)(T + 1) * n3;  // batch stride of [B][T+1][3n] per-step loss arrays
     if (dq_steps) {
       k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)T * n3, n3, B, sstride, s->d_fixed);
@@ -1147,6 +1173,12 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         k_elem_jac<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->st, elem_args(s, B, act_i, act_bs),
                                                                          s->JC);
         LAUNCH_CHECK(s);
+        if (s->st.kappa != 0.0) {
+          k_vol<3><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, nullptr, s->st,
+                                                                          elem_args(s, B, act_i, act_bs), s->JC,
+                                                                          nullptr, nullptr);
+          LAUNCH_CHECK(s);
+        }
       }
       k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
       LAUNCH_CHECK(s);
@@ -1198,6 +1230,12 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
                                                                       s->DW, s->has_act ? s->DR : nullptr);
       LAUNCH_CHECK(s);
       dots(s, B, P.m, {{s->DW, nullptr}}, s->dw_acc, 1);
+      if (s->DWV) {
+        k_vol<4><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
+                                                                        nullptr, s->DWV, nullptr);
+        LAUNCH_CHECK(s);
+        dots(s, B, P.m, {{s->DWV, nullptr}}, s->dwv_acc, 1);
+      }
       if (dL_dact && s->has_act) {
         k_state_to_abi<<<nblk((int64_t)P.m * B), 256, 0, s->stream>>>(s->DR, dL_dact + (int64_t)i * P.m, P.m, B,
                                                                       (int64_t)T * P.m);
@@ -1250,14 +1288,17 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
       LAUNCH_CHECK(s);
     }
     // dL/dE = dL/dw / (1+nu); dL/dnu = -dL/dw E/(1+nu)^2   (w = E/(1+nu))
-    std::vector<double> dw(B), E(B);
+    // with the volume term (w_v = lambda = E nu/((1+nu)(1-2nu))) both weights enter
+    std::vector<double> dw(B), dwv(B, 0.0), E(B);
     CK(cudaMemcpyAsync(dw.data(), s->dw_acc, B * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    if (s->dwv_acc) CK(cudaMemcpyAsync(dwv.data(), s->dwv_acc, B * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(E.data(), s->youngs_sim, B * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     std::vector<double> dE(B), dnu(B);
+    const double nu = s->poisson, p1 = 1.0 + nu, m2 = 1.0 - 2.0 * nu;
     for (int b = 0; b < B; ++b) {
-      dE[b] = dw[b] / (1.0 + s->poisson);
-      dnu[b] = -dw[b] * E[b] / ((1.0 + s->poisson) * (1.0 + s->poisson));
+      dE[b] = dw[b] / p1 + dwv[b] * nu / (p1 * m2);
+      dnu[b] = -dw[b] * E[b] / (p1 * p1) + dwv[b] * E[b] * (1.0 + 2.0 * nu * nu) / (p1 * p1 * m2 * m2);
     }
     if (dL_dE) CK(cudaMemcpyAsync(dL_dE, dE.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     if (dL_dnu) CK(cudaMemcpyAsync(dL_dnu, dnu.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -1378,6 +1419,11 @@ pd_status pd_apply_AN(pd_sim* s, int32_t B, const double* x, const double* young
     LAUNCH_CHECK(s);
     k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
     LAUNCH_CHECK(s);
+    if (s->st.kappa != 0.0) {
+      k_vol<2><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m),
+                                                                      nullptr, s->EF, nullptr);
+      LAUNCH_CHECK(s);
+    }
     k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Pv, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                             s->d_nofix, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, s->Q,
                                                             nullptr, nullptr, nullptr, nullptr, nullptr);

@@ -727,6 +727,236 @@ __global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X
   }
 }
 
+// ----------------------------------------------------------------- volume-preserving term
+// (w_v/2)||F - D||^2, D the projection of F onto det D = 1: with R = polar(F) and the symmetric
+// S = sym(R^T F) = V diag(s) V^T (s the signed singular values, U = R V), d* = argmin ||d||^2 s.t. prod(s + d) = 1
+// by Newton on the KKT system from d = 0 (same iteration and stopping rule as the oracle), g = s + d*,
+// D = R V diag(g) V^T.  Jacobian: J = dg/ds from the differentiated KKT system (eq:vol_kkt); dD[dF] =
+// U M V^T with P = U^T dF V, M_ii = (J diag P)_i, M_ij = (g_i - g_j)/(s_i - s_j) sym(P)_ij + (g_i + g_j)/(s_i +
+// s_j) skew(P)_ij (limit J_ii - J_ij for s_i = s_j; s_i + s_j floored at clamp max|s|).  These helpers run only
+// when the term is enabled and are not inlined, so the corotated-only kernels keep their registers.
+
+// x = K^{-1} rhs for a 4 x 4 K (row-major, overwritten) and nr right-hand sides rhs[4][nr]: Gaussian elimination
+// with partial pivoting
+__device__ void solve4(double* K, double* rhs, int nr) {
+  for (int c = 0; c < 4; ++c) {
+    int p = c;
+    for (int r = c + 1; r < 4; ++r)
+      if (fabs(K[4 * r + c]) > fabs(K[4 * p + c])) p = r;
+    if (p != c) {
+      for (int k = 0; k < 4; ++k) { const double t = K[4 * c + k]; K[4 * c + k] = K[4 * p + k]; K[4 * p + k] = t; }
+      for (int k = 0; k < nr; ++k) { const double t = rhs[c * nr + k]; rhs[c * nr + k] = rhs[p * nr + k]; rhs[p * nr + k] = t; }
+    }
+    const double ip = 1.0 / K[4 * c + c];
+    for (int r = c + 1; r < 4; ++r) {
+      const double f = K[4 * r + c] * ip;
+      for (int k = c; k < 4; ++k) K[4 * r + k] -= f * K[4 * c + k];
+      for (int k = 0; k < nr; ++k) rhs[r * nr + k] -= f * rhs[c * nr + k];
+    }
+  }
+  for (int c = 3; c >= 0; --c) {
+    for (int k = 0; k < nr; ++k) {
+      double v = rhs[c * nr + k];
+      for (int j = c + 1; j < 4; ++j) v -= K[4 * c + j] * rhs[j * nr + k];
+      rhs[c * nr + k] = v / K[4 * c + c];
+    }
+  }
+}
+
+// KKT matrix [I + lam Hc, gc; gc^T, 0] at z = s + d and the constraint gradient gc
+__device__ void vol_kkt_matrix(const double* z, double lam, double* K, double* gc) {
+  gc[0] = z[1] * z[2];
+  gc[1] = z[0] * z[2];
+  gc[2] = z[0] * z[1];
+  const double H01 = z[2], H02 = z[1], H12 = z[0];
+  K[0] = 1.0; K[1] = lam * H01; K[2] = lam * H02; K[3] = gc[0];
+  K[4] = lam * H01; K[5] = 1.0; K[6] = lam * H12; K[7] = gc[1];
+  K[8] = lam * H02; K[9] = lam * H12; K[10] = 1.0; K[11] = gc[2];
+  K[12] = gc[0]; K[13] = gc[1]; K[14] = gc[2]; K[15] = 0.0;
+}
+
+// d*, lam* (Newton from 0; stops after the step following the first residual <= 1e-13) and g = s + d*
+__device__ void vol_kkt(const double* s, double* g, double& lam) {
+  double d[3] = {0.0, 0.0, 0.0};
+  lam = 0.0;
+  bool last = false;
+  for (int it = 0; it < 60; ++it) {
+    const double z[3] = {s[0] + d[0], s[1] + d[1], s[2] + d[2]};
+    double K[16], gc[3];
+    vol_kkt_matrix(z, lam, K, gc);
+    double r[4] = {d[0] + lam * gc[0], d[1] + lam * gc[1], d[2] + lam * gc[2], z[0] * z[1] * z[2] - 1.0};
+    if (last) break;
+    if (fmax(fmax(fabs(r[0]), fabs(r[1])), fmax(fabs(r[2]), fabs(r[3]))) <= 1e-13) last = true;
+    for (int k = 0; k < 4; ++k) r[k] = -r[k];
+    solve4(K, r, 1);
+    d[0] += r[0]; d[1] += r[1]; d[2] += r[2];
+    lam += r[3];
+  }
+  for (int i = 0; i < 3; ++i) g[i] = s[i] + d[i];
+}
+
+// J = dg/ds (3 x 3, row-major) from eq:vol_kkt: [K] [dd; dlam] = [-lam Hc e_k; -gc_k]
+__device__ void vol_jac(const double* s, const double* g, double lam, double* J) {
+  double K[16], gc[3];
+  vol_kkt_matrix(g, lam, K, gc);
+  const double H[9] = {0.0, g[2], g[1], g[2], 0.0, g[0], g[1], g[0], 0.0};
+  double rhs[12];
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) rhs[i * 3 + k] = -lam * H[3 * i + k];
+  for (int k = 0; k < 3; ++k) rhs[9 + k] = -gc[k];
+  solve4(K, rhs, 3);
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) J[3 * i + k] = (i == k ? 1.0 : 0.0) + rhs[i * 3 + k];
+  (void)s;
+}
+
+// projection data at F: R (input, the polar rotation), V, s (signed singular values), g, J
+__device__ void vol_data(const double* F, const double* R, double* V, double* s, double* g, double* J) {
+  double S[9], lam;
+  sym_stretch(R, F, S);
+  jacobi_eig3(S, s, V);
+  vol_kkt(s, g, lam);
+  vol_jac(s, g, lam, J);
+}
+
+// dD[dF] = U M V^T, U = R V (the chain rule above)
+__device__ void vol_dD(const double* R, const double* V, const double* s, const double* g, const double* J,
+                       double clamp, const double* dF, double* dD) {
+  double U[9], P[9], T[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) U[3 * i + j] = R[3 * i] * V[j] + R[3 * i + 1] * V[3 + j] + R[3 * i + 2] * V[6 + j];
+  for (int i = 0; i < 3; ++i)  // T = dF V
+    for (int j = 0; j < 3; ++j) T[3 * i + j] = dF[3 * i] * V[j] + dF[3 * i + 1] * V[3 + j] + dF[3 * i + 2] * V[6 + j];
+  for (int i = 0; i < 3; ++i)  // P = U^T T
+    for (int j = 0; j < 3; ++j) P[3 * i + j] = U[i] * T[j] + U[3 + i] * T[3 + j] + U[6 + i] * T[6 + j];
+  const double smax = fmax(fabs(s[0]), fmax(fabs(s[1]), fabs(s[2])));
+  double M[9];
+  for (int i = 0; i < 3; ++i) M[4 * i] = J[3 * i] * P[0] + J[3 * i + 1] * P[4] + J[3 * i + 2] * P[8];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      if (i == j) continue;
+      const double sym = 0.5 * (P[3 * i + j] + P[3 * j + i]), skw = 0.5 * (P[3 * i + j] - P[3 * j + i]);
+      const double ds = s[i] - s[j];
+      const double r1 = fabs(ds) <= 1e-9 * smax ? J[3 * i + i] - J[3 * i + j] : (g[i] - g[j]) / ds;
+      const double den = fmax(s[i] + s[j], clamp * smax);
+      M[3 * i + j] = r1 * sym + (g[i] + g[j]) / den * skw;
+    }
+  for (int i = 0; i < 3; ++i)  // T = U M
+    for (int j = 0; j < 3; ++j) T[3 * i + j] = U[3 * i] * M[j] + U[3 * i + 1] * M[3 + j] + U[3 * i + 2] * M[6 + j];
+  for (int i = 0; i < 3; ++i)  // dD = T V^T
+    for (int j = 0; j < 3; ++j) dD[3 * i + j] = T[3 * i] * V[3 * j] + T[3 * i + 1] * V[3 * j + 1] + T[3 * i + 2] * V[3 * j + 2];
+}
+
+// D = R V diag(g) V^T
+__device__ void vol_D(const double* R, const double* V, const double* g, double* D) {
+  double SD[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) SD[3 * i + j] = V[3 * i] * g[0] * V[3 * j] + V[3 * i + 1] * g[1] * V[3 * j + 1] + V[3 * i + 2] * g[2] * V[3 * j + 2];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) D[3 * i + j] = R[3 * i] * SD[j] + R[3 * i + 1] * SD[3 + j] + R[3 * i + 2] * SD[6 + j];
+}
+
+// Volume-term kernels: one thread per (element, sim, quad point) like K1/K4, launched after the corotated kernel
+// of the same pass when material.volume is set; they ADD their element forces to EF (store_force_add) and their
+// energy to EE, so the tuned corotated-only kernels keep their register allocation.
+__device__ __forceinline__ void store_force_add(const double* Pm, const DNTab& dt, int e, int b, int q, int B,
+                                                double* Ps, double* __restrict__ EF) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Ps[10 * q + k] = Pm[k];
+  __syncwarp();
+  const int a = q;
+  double o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    const double d0 = dt.b[(qq * 3) * 8 + a], d1 = dt.b[(qq * 3 + 1) * 8 + a], d2 = dt.b[(qq * 3 + 2) * 8 + a];
+    const double* P = Ps + 10 * qq;
+    o0 = fma(P[0], d0, fma(P[1], d1, fma(P[2], d2, o0)));
+    o1 = fma(P[3], d0, fma(P[4], d1, fma(P[5], d2, o1)));
+    o2 = fma(P[6], d0, fma(P[7], d1, fma(P[8], d2, o2)));
+  }
+  __syncwarp();
+  if (EF) {
+    double* o = EF + ((8 * (int64_t)e + a) * 3) * B + b;
+    o[0] += o0;
+    o[B] += o1;
+    o[2 * B] += o2;
+  }
+}
+
+// mode 0 (forward): EF += w_v V G^T (F - D), EE += (w_v V/2) ||F - D||^2
+// mode 1 (A_N p, cached): EF += w_v V G^T (dF - dD[dF]) with R and the projection data from the per-step cache
+// mode 2 (A_N p, recomputed from x: the pd_apply_AN hook)
+// mode 3 (per-step cache): JC slots kJC .. kJC + kJCV of the projection data
+// mode 4 (parameter term): DWV[e][b] = -sum_q V <G_q u_e, F_q - D_q>
+template <int MODE>
+__global__ void __launch_bounds__(256) k_vol(const double* __restrict__ X, const double* __restrict__ Pv, Stencil st,
+                                             ElemArgs ea, double* __restrict__ JC, double* __restrict__ EF,
+                                             double* __restrict__ EE) {
+  __shared__ DNTab dnt;
+  __shared__ __align__(16) double Psm[32][kPsSlot];
+  dn_fill(dnt, st);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int B = ea.B;
+  const int64_t nq = (int64_t)ea.m * B * 8;
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  const bool live = pair < (int64_t)ea.m * B;
+  const int pr = live ? (int)pair : 0;
+  const int e = pr / B, b = pr - e * B;
+  const int64_t t = live ? tid : q;
+  const double wv = ea.w_sim[b] * st.kappa * st.V;
+  double F[9], R[9], V[9], sv[3], g[3], J[9], dF[9], dD[9], Pm[9];
+  if (MODE == 1) {
+    load_F(Pv, ea.hex8, dnt, e, b, q, B, dF);
+    for (int k = 0; k < 9; ++k) R[k] = JC[k * nq + t];
+    for (int k = 0; k < 9; ++k) V[k] = JC[(kJC + k) * nq + t];
+    for (int k = 0; k < 3; ++k) sv[k] = JC[(kJC + 9 + k) * nq + t];
+    for (int k = 0; k < 3; ++k) g[k] = JC[(kJC + 12 + k) * nq + t];
+    const int sy[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    for (int k = 0; k < 9; ++k) J[k] = JC[(kJC + 15 + sy[k]) * nq + t];
+  } else {
+    load_F(X, ea.hex8, dnt, e, b, q, B, F);
+    polar_rotation(F, R);
+    vol_data(F, R, V, sv, g, J);
+  }
+  if (MODE == 3) {
+    if (live) {
+      for (int k = 0; k < 9; ++k) JC[(kJC + k) * nq + tid] = V[k];
+      for (int k = 0; k < 3; ++k) JC[(kJC + 9 + k) * nq + tid] = sv[k];
+      for (int k = 0; k < 3; ++k) JC[(kJC + 12 + k) * nq + tid] = g[k];
+      const int up[6] = {0, 1, 2, 4, 5, 8};
+      for (int k = 0; k < 6; ++k) JC[(kJC + 15 + k) * nq + tid] = J[up[k]];
+    }
+    return;
+  }
+  if (MODE == 0 || MODE == 4) {
+    double D[9];
+    vol_D(R, V, g, D);
+    if (MODE == 4) {  // EF = DWV here, Pv = u
+      load_F(Pv, ea.hex8, dnt, e, b, q, B, dF);
+      double a2 = 0;
+      for (int k = 0; k < 9; ++k) a2 += dF[k] * (F[k] - D[k]);
+      const double dwv = qsum8(-st.V * a2);
+      if (live && q == 0) EF[(int64_t)e * B + b] = dwv;
+      return;
+    }
+    double en = 0;
+    for (int k = 0; k < 9; ++k) {
+      const double d = F[k] - D[k];
+      en += d * d;
+      Pm[k] = wv * d;
+    }
+    en = qsum8(0.5 * wv * en);
+    if (live && q == 0 && EE) EE[(int64_t)e * B + b] += en;
+  } else {
+    if (MODE == 2) load_F(Pv, ea.hex8, dnt, e, b, q, B, dF);
+    vol_dD(R, V, sv, g, J, st.clamp, dF, dD);
+    for (int k = 0; k < 9; ++k) Pm[k] = wv * (dF[k] - dD[k]);
+  }
+  store_force_add(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
+}
+constexpr int kJCV = 21;  // extra cached doubles per quad point with the volume term
+
 // ----------------------------------------------------------------- K2: deterministic gather
 // mode 0: G = M/h^2 (X - Y) + sum EF   (grad g)       W = M/h^2 Y  (residual normaliser)
 // mode 1: G = M/h^2 X + sum EF         (A_N p, X = p)  W unused

@@ -15,6 +15,7 @@ struct Stencil {
   double V;            // quadrature weight dx^3/8
   double w_m;          // muscle weight (0 = off)
   double clamp;        // eigenvalue floor factor of the polar derivative (1e-6)
+  double kappa;        // volume-preserving weight per corotated weight, w_v / w = nu / (1 - 2 nu); 0 = no volume term
 };
 
 struct ElemArgs {

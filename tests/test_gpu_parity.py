@@ -55,7 +55,7 @@ def test_rotations_match_oracle_polar(torch):
             assert d[ok].max() < 1e-11, (scale, d[ok].max())
 
 
-@pytest.mark.parametrize("name", ["c1", "c3s", "c5s"])
+@pytest.mark.parametrize("name", ["c1", "c3s", "c5s", "c2v", "c5v"])
 def test_objective_and_gradient(torch, name):
     from oracle import pd
     inp = make_inputs(get_config(name))
@@ -101,7 +101,7 @@ def test_global_solve_matches_direct(torch, name):
         assert np.all(out[b][~fr] == 0.0)
 
 
-@pytest.mark.parametrize("name", ["c1", "c5s"])
+@pytest.mark.parametrize("name", ["c1", "c5s", "c2v", "c5v"])
 def test_AN_product_matches_assembled_hessian(torch, name):
     # Matrix-free A_N p vs the oracle's assembled A_N = A - dA.
     from oracle import adjoint, pd
@@ -287,13 +287,13 @@ def test_k3_switches_match_direct(torch, monkeypatch, env, name, batch):
 
 
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
-def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, **over):
+def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, tol_fwd=2e-14, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for
     # position agreement near the fp64 floor of the residual metric (~1e-14); the forward therefore
     # runs to 2e-14 here (measured: tools/contact_diag.py).
     inp = make_inputs(get_config(name, **over))
     sim = _sim(inp, contact_nodes=inp["contact_nodes"], accel_fwd=accel_fwd, outer_warm=outer_warm,
-               lbfgs_warm=lbfgs_warm, tol_fwd=2e-14, max_iter_fwd=4000)
+               lbfgs_warm=lbfgs_warm, tol_fwd=tol_fwd, max_iter_fwd=4000)
     gpu = _run_gpu(torch, inp, sim)
     sets = sim.contact_sets()
     # (sticky nodes under random actuation can make Alg. 1 cycle until its outer cap; such steps are flagged on
@@ -387,3 +387,22 @@ def test_sticky_contact_parity(torch, name):
     # infinite friction: active candidates hold all three DoFs at x_i; constrained solve of all 3 columns,
     # adjoint with the pinned-value term
     _contact_parity(torch, name, 1, 1, contact_mode="sticky")
+
+
+# ----------------------------------------------------------------- volume-preserving energy (8f.2)
+def test_c2v_volume_parity(torch):
+    # corotated + volume-preserving background elasticity, per-sim E, 2 sims: forward and
+    # gradients against the oracle; dL/dnu is no longer the corotated-only multiple -E/(1+nu) of dL/dE
+    inp = make_inputs(get_config("c2v"))
+    gpu = _run_gpu(torch, inp, _sim(inp, tol_fwd=5e-14))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    _compare(inp, gpu, range(inp["B"]))
+    nu = inp["cfg"].poisson
+    for b in range(inp["B"]):
+        corot_only = -inp["youngs"][b] / (1 + nu) * gpu["dE"][b]
+        assert abs(gpu["dnu"][b] - corot_only) > 1e-3 * abs(gpu["dnu"][b])
+
+
+def test_c5v_volume_contact_muscle_parity(torch):
+    # the c5 recipe (contact + muscle) with the volume term: bit-exact active sets, states, gradients
+    _contact_parity(torch, "c5v", 1, 1, 0, tol_fwd=5e-14)   # (residual floor ~3e-14 with the volume term)
