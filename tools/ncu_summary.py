@@ -91,7 +91,8 @@ def full(path):
         if len(rr) > 2 + i:
             h, vals = rr[0], rr[2 + i]
             dv = {a: b for a, b in zip(h, vals)}
-            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"):
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                      "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"):
                 if k in dv:
                     print(f"- {k}: {dv[k]}")
             st = [(a.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""), float(b))
