@@ -366,8 +366,12 @@ def main_ours(args):
                 e2e=e2e, gpu_launches=launches, roofline=roof,
                 roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
                 kernel_share=share,
+                # per-sim means and, since the batch loop runs until its slowest sim converges, the mean over steps
+                # of the per-step maximum over sims (what the batch actually pays)
                 iters=dict(fwd_mean=float(np.mean(stats["fwd"]["iters_fwd"])),
                            adj_mean=float(np.mean(stats["bwd"]["iters_adj"])),
+                           fwd_batch=float(np.mean(np.max(stats["fwd"]["iters_fwd"], axis=0))),
+                           adj_batch=float(np.mean(np.max(stats["bwd"]["iters_adj"], axis=0))),
                            nonconverged=int(stats["fwd"]["n_nonconverged"] + stats["bwd"]["n_nonconverged"])),
                 setup=dict(seconds=setup_s, factor_ms=info["factor_ms"], nnz_L=info["nnz_L"],
                            supernodes=info["n_supernodes"], levels=info["n_levels"]),
