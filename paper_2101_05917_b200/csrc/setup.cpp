@@ -27,7 +27,10 @@
 namespace pdb {
 namespace {
 
-constexpr int kLeaf = 48;  // max nodes in an ND leaf
+int nd_leaf() {  // max nodes in an ND leaf (PD_ND_LEAF overrides; developer switch)
+  static const int v = std::getenv("PD_ND_LEAF") ? std::atoi(std::getenv("PD_ND_LEAF")) : 48;
+  return v;
+}
 
 struct NDNode {
   std::vector<int32_t> nodes;  // mesh node ids in final order
@@ -633,7 +636,7 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
     int ax = 0;
     for (int j = 1; j < 3; ++j)
       if (hi[j] - lo[j] > hi[ax] - lo[ax]) ax = j;
-    if ((int)nodes.size() <= kLeaf || hi[ax] - lo[ax] < 2) {
+    if ((int)nodes.size() <= nd_leaf() || hi[ax] - lo[ax] < 2) {
       std::sort(nodes.begin(), nodes.end(), lexless);
       supNodes.push_back(nodes);
       supParent.push_back(-1);

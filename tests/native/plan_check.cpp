@@ -158,6 +158,14 @@ int main(int argc, char** argv) {
         }
         if (p != S.wpiece[w0 + w + 1]) { printf("warp %d piece count mismatch\n", w); exit(23); }
       }
+      if (std::getenv("PLAN_STATS")) {  // per-level statistics of the v4 schedule
+        int np = S.lvl_piece[lev + 1] - S.lvl_piece[lev], nd = 0;
+        for (int q = S.lvl_piece[lev]; q < S.lvl_piece[lev + 1]; ++q) nd += S.pout[q] >= 0;
+        long long srcs = S.red_ptr[S.lvl_red[lev + 1]] - S.red_ptr[S.lvl_red[lev]];
+        printf("%s level %2d: kgroups %7d (%6.2f MB) warps %5d pieces %6d direct %6d reduce targets %7d sources %8lld\n",
+               fwd ? "fw" : "bw", lev, S.lvl_g[lev + 1] - S.lvl_g[lev], (S.lvl_g[lev + 1] - S.lvl_g[lev]) * 1024.0 / 1e6, W,
+               np, nd, S.lvl_red[lev + 1] - S.lvl_red[lev], srcs);
+      }
       for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) {
         double acc = 0;
         for (int u = S.red_ptr[r]; u < S.red_ptr[r + 1]; ++u) acc += part[S.red_src[u]];
