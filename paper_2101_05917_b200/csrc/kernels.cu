@@ -1413,6 +1413,17 @@ __host__ __device__ constexpr int rhs_ld() { return NT == 1 ? 8 : 28; }  // padd
 template <int NT>
 __host__ __device__ constexpr int stage_doubles() { return 4 * 128 + 16 * rhs_ld<NT>(); }
 
+// Piece metadata of a warp's range held one piece per lane (lane i: piece pb + i): end k-group, output, valid
+// rows.  A piece change is a shuffle instead of dependent global loads on the critical path (reloaded for the
+// next 32 pieces when a range has more).
+__device__ __forceinline__ void piece_fetch(const Sweep4Dev& sw, int pb, int pend, int lane, int& pe_l, int& po_l,
+                                            int& pn_l) {
+  const int q = pb + lane;
+  pe_l = q < pend ? sw.pstart[q] + sw.pkg[q] : 0;
+  po_l = q < pend ? sw.pout[q] : 0;
+  pn_l = q < pend ? sw.pnv[q] : 0;
+}
+
 template <int NT, bool VEC>
 __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, int w0, int nwarps, int R,
                                                                 const double* __restrict__ srcA,
@@ -1491,9 +1502,12 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
     krs[j] = krow_of(j);
   }
   int kr_next = krow_of(kStages - 1);
-  int p = sw.wpiece[w0 + w];
-  int pe = sw.pstart[p] + sw.pkg[p];  // end (global k-group) of the current piece
-  int pout = sw.pout[p], pnv = sw.pnv[p];
+  int pb = sw.wpiece[w0 + w], pi = 0;
+  const int pend = sw.wpiece[w0 + w + 1];
+  int pe_l, po_l, pn_l;
+  piece_fetch(sw, pb, pend, lane, pe_l, po_l, pn_l);
+  int pe = __shfl_sync(0xffffffffu, pe_l, 0);  // end (global k-group) of the current piece
+  int pout = __shfl_sync(0xffffffffu, po_l, 0), pnv = __shfl_sync(0xffffffffu, pn_l, 0);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #pragma unroll
   for (int j = 0; j < kStages - 1; ++j) issue_rhs(j, krs[j]);
@@ -1549,10 +1563,14 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
           for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
         }
         if (gs + q + 1 < g1) {
-          ++p;
-          pe = sw.pstart[p] + sw.pkg[p];
-          pout = sw.pout[p];
-          pnv = sw.pnv[p];
+          if (++pi == 32) {
+            pb += 32;
+            pi = 0;
+            piece_fetch(sw, pb, pend, lane, pe_l, po_l, pn_l);
+          }
+          pe = __shfl_sync(0xffffffffu, pe_l, pi);
+          pout = __shfl_sync(0xffffffffu, po_l, pi);
+          pnv = __shfl_sync(0xffffffffu, pn_l, pi);
         }
       }
     }

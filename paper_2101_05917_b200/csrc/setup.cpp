@@ -27,9 +27,13 @@
 namespace pdb {
 namespace {
 
-int nd_leaf() {  // max nodes in an ND leaf (PD_ND_LEAF overrides; developer switch)
-  static const int v = std::getenv("PD_ND_LEAF") ? std::atoi(std::getenv("PD_ND_LEAF")) : 48;
-  return v;
+// Max nodes in an ND leaf.  Every ND level costs the batched solve a fixed ~15-20 us on the B200 (one product
+// launch + one reduce), while larger leaves add fill: on large meshes (>= 32768 free nodes) leaves
+// of 128 nodes remove two levels for +7.5% nnz(L_s) (c5: 13 -> 11 levels, A^-1 519 -> 477 us measured); small
+// meshes, whose factor is L2-resident, keep 48 (c3: 48 -> 128 measured slower).  PD_ND_LEAF overrides.
+int nd_leaf(int nfree) {
+  if (const char* e = std::getenv("PD_ND_LEAF")) return std::max(2, std::atoi(e));
+  return nfree >= 32768 ? 128 : 48;
 }
 
 struct NDNode {
@@ -626,6 +630,7 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
       if (lat[3 * (int64_t)a + j] != lat[3 * (int64_t)b + j]) return lat[3 * (int64_t)a + j] < lat[3 * (int64_t)b + j];
     return a < b;
   };
+  const int leaf = nd_leaf(P.nfree);
   std::function<int(std::vector<int32_t>&)> nd = [&](std::vector<int32_t>& nodes) -> int {
     int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
     for (int v : nodes)
@@ -636,7 +641,7 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
     int ax = 0;
     for (int j = 1; j < 3; ++j)
       if (hi[j] - lo[j] > hi[ax] - lo[ax]) ax = j;
-    if ((int)nodes.size() <= nd_leaf() || hi[ax] - lo[ax] < 2) {
+    if ((int)nodes.size() <= leaf || hi[ax] - lo[ax] < 2) {
       std::sort(nodes.begin(), nodes.end(), lexless);
       supNodes.push_back(nodes);
       supParent.push_back(-1);

@@ -45,7 +45,7 @@ def main():
         torch.cuda.synchronize()
     ks = []
     for e in prof.events():
-        if e.device_type.name == "CUDA" and e.name.startswith("pdb::"):
+        if e.device_type.name == "CUDA" and "pdb::" in e.name:
             ks.append((e.time_range.start, e.time_range.end, e.name))
     ks.sort()
     # one call = from a k_to_solve to the next k_to_solve
@@ -56,7 +56,7 @@ def main():
     tot = {}
     for s, e, n in blk:
         gap = "" if prev_end is None else "%+7.2f" % (s - prev_end)
-        short = n.replace("pdb::", "").split("(")[0]
+        short = n.split("pdb::")[1].split("(")[0]
         print("%8.2f %7.2f %s  %s" % (s - t0, e - s, gap, short))
         prev_end = e
         tot.setdefault(short, [0, 0.0])
