@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=3, help="timed iterations of the end-to-end leg (<= --steps)")
     ap.add_argument("--set", action="append", default=[], help="config override key=value (e.g. contact=False)")
+    ap.add_argument("--solver", default="pd", choices=["pd", "newton"],
+                    help="forward solver: pd = quasi-Newton PD (the product); newton = the Newton-PCG baseline "
+                         "(SURVEY 8f-4, P:522-527) on the same kernels, for the on-box PD-vs-Newton comparison")
     return ap.parse_args()
 
 
@@ -210,7 +213,7 @@ def main_ours(args):
         raise SystemExit(f"rank {rank}: --gpus {ws} exceeds the batch of {cfg.name} ({inp_all['B']} sims)")
     t_setup = time.perf_counter()
     sim = pdb.simulator_from_inputs(inp, tol_fwd=cfg.tol, tol_adj=cfg.tol, max_steps=T, profile=1,
-                                    check_every=1, accel_fwd=1, outer_warm=1)
+                                    check_every=1, accel_fwd=2 if args.solver == "newton" else 1, outer_warm=1)
     setup_s = time.perf_counter() - t_setup
     info = sim.info()
     D = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=dev)
@@ -362,7 +365,9 @@ def main_ours(args):
                 data="synthetic",
                 config=dict(workload=cfg.name, batch=inp_all["B"], batch_per_gpu=B, time_steps=T, dof=N, tol=cfg.tol,
                             grid=list(cfg.counts), l2="flushed (256 MB write) before every timed iteration",
-                            parallelism=f"batch partitioned over {ws} rank(s), no data-path collective"),
+                            parallelism=f"batch partitioned over {ws} rank(s), no data-path collective",
+                            solver="quasi-Newton PD (L-BFGS, H0 = A^-1)" if args.solver == "pd"
+                            else "Newton-PCG baseline (SURVEY 8f-4)"),
                 e2e=e2e, gpu_launches=launches, roofline=roof,
                 roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
                 kernel_share=share,

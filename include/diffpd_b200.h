@@ -74,7 +74,10 @@ typedef struct {
   int32_t fixed_iter;     /* > 0: exactly this many plain local-global iterations per step
                              from x^0 = x_i, no convergence test (config c1)               */
   int32_t accel_fwd;      /* 0: plain PD x <- A^{-1} d(x); 1: L-BFGS with
-                             H0 = A^{-1} and line search (the quasi-Newton PD of P:79/P:254) */
+                             H0 = A^{-1} and line search (the quasi-Newton PD of P:79/P:254);
+                             2: the Newton baseline as Newton-PCG: truncated CG on the
+                             Hessian A_N(x) preconditioned by the prefactorised A^{-1}, forcing term
+                             1e-2, descent guard, same line search (comparison system) */
   int32_t accel_adj;      /* 0: fixed point u <- A^{-1}(b + dA u);
                              1: its quasi-Newton acceleration, run as
                              A-preconditioned CG — BFGS with exact line search on a(u)   */

@@ -55,6 +55,10 @@ struct pd_sim {
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
+  // Newton-PCG forward (accel_fwd = 2): CG mask, CG statistics, forcing term (relative CG residual)
+  int32_t *pact = nullptr, *nt_iters = nullptr, *nt_flag = nullptr;
+  double* nt_res = nullptr;
+  double newton_eta = 1e-2;
   // work
   double *X, *V, *Y, *Xp, *Fext, *G, *W, *EF, *EE, *S0, *S1, *S2;
   double *U, *Rv, *Z, *Pv, *Q, *AX, *AV, *Bv, *DF, *DW, *DR, *JC;
@@ -691,6 +695,103 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
   s->lb_gi = gi;
 }
 
+// Newton-PCG forward (accel_fwd = 2, the paper's Newton baseline of P:522-527 with an iterative
+// linear solver): per iteration the projection-derivative data at x (k_elem_jac), a truncated CG on the Hessian
+// A_N(x) D = -grad g preconditioned by the constrained A^{-1} (the adjoint's K4 + K3 machinery) to the relative
+// residual newton_eta, a descent guard (PD direction -A^{-1} grad g where CG met negative curvature first) and the
+// Armijo search of the L-BFGS path.  Same minimiser, same convergence test.
+void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base) {
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  const int max_trial = 30;
+  double* const Z0 = s->LS;  // (no curvature history in this mode)
+  CK(cudaMemcpyAsync(s->Xn, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  eval_f(s, B, s->X, s->G, s->fcur, act_i, act_bs);
+  dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+  double* const gn2 = s->inert + B;
+  for (int iter = 0;; ++iter) {
+    k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
+                                          s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
+                                          s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
+                                          s->ls_act, s->nactive + 2);
+    LAUNCH_CHECK(s);
+    if (iter >= s->opt.max_iter_fwd) break;
+    {
+      int a = 0, running = 0, nr = 0;
+      read_nactive3(s, &a, &running, &nr);
+      if (running == 0) break;
+    }
+    {  // Hessian data at x (P:228's per-step Jacobian, here per Newton iteration)
+      ProfScope ps(s, 3);
+      k_elem_jac<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->st, elem_args(s, B, act_i, act_bs),
+                                                                       s->JC);
+      LAUNCH_CHECK(s);
+      if (s->st.kappa != 0.0) {
+        k_vol<3><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, nullptr, s->st,
+                                                                        elem_args(s, B, act_i, act_bs), s->JC, nullptr,
+                                                                        nullptr);
+        LAUNCH_CHECK(s);
+      }
+    }
+    // CG: A_N D = -G on the running sims (pact), r0 = -G, z0 = A^{-1} r0 (kept: the PD direction)
+    CK(cudaMemcpyAsync(s->pact, s->active, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
+    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->G, -1.0, nullptr, nullptr, 0.0, len, B, nullptr);
+    LAUNCH_CHECK(s);
+    CK(cudaMemsetAsync(s->Dv, 0, len * sizeof(double), s->stream));
+    CK(cudaMemcpyAsync(s->bb, s->dots, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // |b|^2 = |G|^2
+    apply_Ainv(s, B, s->Rv, Z0, nullptr, 1.0, 0.0, s->pact);
+    CK(cudaMemcpyAsync(s->Pv, Z0, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    dots(s, B, n3, {{s->Rv, Z0}}, s->rz);
+    for (int it = 0;; ++it) {
+      const bool fused = it > 0;
+      if (!fused) dots(s, B, n3, {{s->Rv, s->Rv}}, s->dots + 2 * B);
+      k_adj_check<<<1, 256, 0, s->stream>>>(s->dots + 2 * B, s->bb, B, s->newton_eta, it, s->opt.max_iter_adj, s->pact,
+                                            s->nt_iters, s->nt_res, s->nt_flag, s->nactive, fused ? s->rz : nullptr,
+                                            s->dots + 3 * B);
+      LAUNCH_CHECK(s);
+      if (it >= s->opt.max_iter_adj || read_nactive(s) == 0) break;
+      apply_AN(s, B, s->X, s->Pv, s->Q, act_i, act_bs, s->JC);
+      dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + 3 * B);
+      k_negcurv<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots + 3 * B, s->pact, B);
+      LAUNCH_CHECK(s);
+      k_pcg_update<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Rv, s->Pv, s->Q, s->rz, s->dots + 3 * B, len, B, s->pact);
+      LAUNCH_CHECK(s);
+      apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->pact);
+      dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + 3 * B);  // rz_new | |r|^2
+      k_pcg_dir<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, s->dots + 3 * B, s->rz, len, B, s->pact);
+      LAUNCH_CHECK(s);
+      // (k_adj_check reads |r|^2 at dots[2B:3B): move it there)
+      CK(cudaMemcpyAsync(s->dots + 2 * B, s->dots + 4 * B, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+    }
+    dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
+    k_descent_guard<<<nblk(len), 256, 0, s->stream>>>(s->Dv, Z0, s->gtd, len, B, s->active);
+    LAUNCH_CHECK(s);
+    dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
+    bool done = false;
+    for (int trial = 0;; ++trial) {  // Armijo backtracking from alpha = 1 (as inner_lbfgs)
+      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
+      LAUNCH_CHECK(s);
+      eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
+      k_ls_accept<<<1, 256, 0, s->stream>>>(s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
+                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
+      LAUNCH_CHECK(s);
+      int searching = 0, running = 1, nr = 0;
+      read_nactive3(s, &searching, &running, &nr);
+      if (trial == 0 && running == 0) {
+        done = true;
+        break;
+      }
+      if (searching == 0) break;
+    }
+    if (done) break;
+    k_newton_commit<<<nblk(len), 256, 0, s->stream>>>(s->X, s->G, s->Xn, s->Gn, len, B, s->active);
+    LAUNCH_CHECK(s);
+    k_newton_commit_s<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->dots, gn2, B, s->active);
+    LAUNCH_CHECK(s);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -839,7 +940,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->DR = s->alloc<double>((int64_t)P.m * s->Bmax);
     double** small[] = {&s->w_sim, &s->youngs_sim, &s->w_diag, &s->youngs_diag, &s->alpha, &s->beta, &s->rz, &s->bb, &s->dw_acc, &s->res_buf};
     for (double** p : small) *p = s->alloc<double>(s->Bmax);
-    s->dots = s->alloc<double>(3 * s->Bmax);
+    s->dots = s->alloc<double>(5 * s->Bmax);  // [B] slots: pairs of the multi-dots, Newton-PCG scalars at [2B, 5B)
     s->max_partial_blocks = (int64_t)red_chunks(std::max<int64_t>(3LL * P.n, P.m)) * s->Bmax;
     s->partial = s->alloc<double>(32 * s->max_partial_blocks + 64);  // up to 2 x 16 dot families (mdot pairs)
     s->active = s->alloc<int32_t>(s->Bmax);
@@ -876,6 +977,13 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       for (double** p : lb) *p = s->alloc<double>((int64_t)2 * s->nhist * s->Bmax);  // lb_da: [da | db]
       s->lb_G = s->alloc<double>((int64_t)s->nhist * s->nhist * s->Bmax);
       s->ls_flag = s->alloc<int32_t>(s->Bmax);
+      if (s->opt.accel_fwd == 2) {  // Newton-PCG scratch: CG mask and per-sim CG statistics
+        s->pact = s->alloc<int32_t>(s->Bmax);
+        s->nt_iters = s->alloc<int32_t>(s->Bmax);
+        s->nt_flag = s->alloc<int32_t>(s->Bmax);
+        s->nt_res = s->alloc<double>(s->Bmax);
+        if (const char* e = std::getenv("PD_NEWTON_ETA")) s->newton_eta = std::atof(e);
+      }
     }
     if (P.nc > 0) {
       const int c = P.nc;
@@ -1017,7 +1125,9 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
           LAUNCH_CHECK(s);
         }
-        if (s->opt.accel_fwd && s->opt.fixed_iter <= 0) {
+        if (s->opt.accel_fwd == 2 && s->opt.fixed_iter <= 0) {
+          inner_newton(s, B, i, act_i, act_bs, contact ? s->it_base : nullptr);
+        } else if (s->opt.accel_fwd && s->opt.fixed_iter <= 0) {
           inner_lbfgs(s, B, i, act_i, act_bs, contact ? s->it_base : nullptr, s->opt.lbfgs_warm && outer > 1);
         } else {
           for (int iter = 0;; ++iter) {

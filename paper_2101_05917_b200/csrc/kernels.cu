@@ -2250,6 +2250,39 @@ __global__ void k_lbfgs_commit(double* __restrict__ S, double* __restrict__ Yv, 
   G[i] = gn;
 }
 
+// Newton-PCG forward (accel_fwd = 2): commit of an accepted trial, X <- Xn, G <- Gn (state vectors, masked)
+__global__ void k_newton_commit(double* __restrict__ X, double* __restrict__ G, const double* __restrict__ Xn,
+                                const double* __restrict__ Gn, int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (!active[b]) return;
+  X[i] = Xn[i];
+  G[i] = Gn[i];
+}
+// ... and its per-sim scalars: f <- f_new, |grad g|^2 <- that of the trial
+__global__ void k_newton_commit_s(double* __restrict__ f, const double* __restrict__ fn, double* __restrict__ g2,
+                                  const double* __restrict__ gn2, int B, const int32_t* __restrict__ active) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  f[b] = fn[b];
+  g2[b] = gn2[b];
+}
+// Truncated CG on a non-convex Hessian: a sim whose search direction has p^T A_N p <= 0 stops its CG (its
+// direction so far is kept; a zero direction falls back to the PD step below).
+__global__ void k_negcurv(const double* __restrict__ pq, int32_t* __restrict__ active, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && active[b] && !(pq[b] > 0.0)) active[b] = 0;
+}
+// Descent guard: where <grad g, D> >= 0 (not a descent direction), D = the PD direction -A^{-1} grad g (Z0)
+__global__ void k_descent_guard(double* __restrict__ D, const double* __restrict__ Z0, const double* __restrict__ gtd,
+                                int64_t len, int B, const int32_t* __restrict__ active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  const int b = (int)(i % B);
+  if (active[b] && !(gtd[b] < 0.0)) D[i] = Z0[i];
+}
+
 // v[b] = c (per-sim scalar fill)
 __global__ void k_fill_double(double* __restrict__ v, double c, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;

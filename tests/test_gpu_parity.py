@@ -223,16 +223,16 @@ def test_c1_fixed_iterations_parity(torch):
     _compare(inp, gpu, [0])
 
 
-@pytest.mark.parametrize("accel_fwd,accel_adj", [(0, 1), (0, 0), (1, 1)])
+@pytest.mark.parametrize("accel_fwd,accel_adj", [(0, 1), (0, 0), (1, 1), (2, 1)])
 def test_c2s_converged_parity(torch, accel_fwd, accel_adj):
-    # plain PD / quasi-Newton forward; PD fixed point (eq:bp_update) / accelerated adjoint
+    # plain PD / quasi-Newton / Newton-PCG forward; PD fixed point (eq:bp_update) / accelerated adjoint
     inp = make_inputs(get_config("c2s"))
     gpu = _run_gpu(torch, inp, _sim(inp, accel_fwd=accel_fwd, accel_adj=accel_adj))
     assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
     _compare(inp, gpu, [0])
 
 
-@pytest.mark.parametrize("accel_fwd", [0, 1])
+@pytest.mark.parametrize("accel_fwd", [0, 1, 2])
 def test_c3s_batched_shared_factor_parity(torch, accel_fwd):
     # Per-sim E with ONE factor of A_ref: max E (plain PD) or the geometric mean of the
     # batch extremes (quasi-Newton); the oracle uses each sim's exact A_s.
@@ -322,14 +322,14 @@ def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, tol_fw
     _compare(inp, gpu, range(inp["B"]))
 
 
-@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1)])
+@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1), (2, 1, 0)])
 def test_c4s_contact_drop_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
     # BASELINE.json configs[3] recipe at oracle size: tilted plate dropped on z = 0, frictionless LCP.
     # (0, 0, 0) = literal Alg. 1 (plain PD corrector restarted from x_i); (1, 1, *) = the fast paths.
     _contact_parity(torch, "c4s", accel_fwd, outer_warm, lbfgs_warm)
 
 
-@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1)])
+@pytest.mark.parametrize("accel_fwd,outer_warm,lbfgs_warm", [(0, 0, 0), (1, 1, 0), (1, 1, 1), (2, 1, 0)])
 def test_c5s_contact_muscle_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
     # configs[4] recipe at oracle size: muscle actuation + bottom-face contact, B = 2.
     _contact_parity(torch, "c5s", accel_fwd, outer_warm, lbfgs_warm)
