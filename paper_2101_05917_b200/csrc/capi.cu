@@ -1,6 +1,7 @@
 // C-ABI of the B200 DiffPD hot path (include/diffpd_b200.h): handle lifetime,
 // device residency and the per-step orchestration of the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: per-phase ranges for nsys / ncu --nvtx (no-ops without a tool)
 
 #include <algorithm>
 #include <chrono>
@@ -169,10 +170,17 @@ cudaEvent_t prof_event(pd_sim* s) {
   }
   return s->ev_pool[s->ev_next++];
 }
+// NVTX range for the lifetime of a scope (phases: pd_forward / pd_backward, time step, inner solve, kernel family)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+const char* const kFamilyName[6] = {"local_K1", "gather_K2", "solve_K3", "AN_K4", "contact_K5", "param"};
 struct ProfScope {
   pd_sim* s;
   int fam;
-  ProfScope(pd_sim* s_, int f) : s(s_), fam(f) {
+  Nvtx range;
+  ProfScope(pd_sim* s_, int f) : s(s_), fam(f), range(kFamilyName[f]) {
     if (!s->opt.profile) return;
     s->ev_open.push_back({fam, s->ev_next});
     CK(cudaEventRecord(prof_event(s), s->stream));
@@ -585,6 +593,7 @@ void build_Q(pd_sim* s, int B, const int32_t* sel) {
 // Forward quasi-Newton PD (P:79, P:254-271 applied to eq:opt): L-BFGS on g with H0 = A^{-1} (the
 // constrained prefactorised solve) and Armijo backtracking; per-sim masks; history slots shared by index.
 void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base, bool warm) {
+  Nvtx nv("inner_lbfgs");
   const HostPlan& P = s->plan;
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
@@ -701,6 +710,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
 // residual newton_eta, a descent guard (PD direction -A^{-1} grad g where CG met negative curvature first) and the
 // Armijo search of the L-BFGS path.  Same minimiser, same convergence test.
 void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, const int32_t* it_base) {
+  Nvtx nv("inner_newton_pcg");
   const HostPlan& P = s->plan;
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
@@ -1069,6 +1079,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   const HostPlan& P = s->plan;
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
+  Nvtx nv_fwd("pd_forward");
   try {
     set_w(s, B, youngs_per_sim);
     k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(q0, s->X, n3, B);
@@ -1087,6 +1098,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
     CK(cudaMemcpyAsync(s->traj, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
     const double tol = s->opt.tol_fwd;
     for (int i = 0; i < steps; ++i) {
+      Nvtx nv_step("forward_step");
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
       const int64_t act_bs = (int64_t)steps * P.m;
       if (f_ext && f_ext_step_stride) {  // time-varying f_ext: this step's slice of [B][steps][3n]
@@ -1267,7 +1279,9 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
       LAUNCH_CHECK(s);
     }
     const bool pcg = s->opt.accel_adj != 0;
+    Nvtx nv_bwd("pd_backward");
     for (int i = T - 1; i >= 0; --i) {
+      Nvtx nv_step("backward_step");
       const double* x1 = s->traj + (int64_t)(i + 1) * len;
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
       const int64_t act_bs = (int64_t)T * P.m;
