@@ -23,7 +23,7 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
-from . import energy, fem
+from . import energy, fem, pd
 
 
 def hessian_blocks(scene, x, w, act=None):
@@ -95,6 +95,14 @@ def backward(scene, traj, youngs, dL_dqT, dL_dvT, act=None, dL_dq_steps=None, dL
     dL_dq_steps, dL_dv_steps [T+1, 3n] are added to the adjoint of state i when the reverse pass reaches it.
     Returns dict(dq0, dv0, dfext (summed over steps), dfext_steps [T, 3n] (= u_i, dL/df_ext of step i),
     dE, dnu, dw, dact[T,m] or None)."""
+    if pd.has_plane(scene):  # general contact plane: the adjoint in plane coordinates (vectors rotate)
+        tr = dict(traj, q=pd.to_plane(scene, traj["q"], True), v=pd.to_plane(scene, traj["v"], False))
+        vec = lambda a: None if a is None else pd.to_plane(scene, np.asarray(a, float), False)
+        g = backward(pd.plane_scene(scene), tr, youngs, vec(dL_dqT), vec(dL_dvT), act, vec(dL_dq_steps),
+                     vec(dL_dv_steps), solver)
+        for k in ("dq0", "dv0", "dfext", "dfext_steps"):
+            g[k] = pd.from_plane(scene, g[k], False)
+        return g
     h = scene.h
     w = scene.w_of(youngs)
     T = traj["q"].shape[0] - 1

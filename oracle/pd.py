@@ -7,9 +7,13 @@ Implements, per simulation and per time step:
   local step  z* = Proj_M(G x)                                (P:187 eq:pd_proj)
   global step A x = (1/h^2) M y + sum_e w_e G_e^T z_e*         (P:197 eq:pd_global, with M:
                                                                reading §8c.7)
-  contact: Alg. 1 with frictionless normal pins at the plane z = 0
-           (readings §8c.10, §8c.11), constrained solve eq:dirichlet/eq:complement
-            with the coupling term kept (reading §8c.9).
+  contact: Alg. 1 with frictionless normal pins on the plane n . x = d
+           (P:278: "phi is a linear function and n ... a constant vector"; default z = 0;
+           readings §8c.10, §8c.11), constrained solve eq:dirichlet/eq:complement
+            with the coupling term kept (reading §8c.9).  A general plane is
+           solved in coordinates x' = Q x - d e_z (Q a rotation with Q n = e_z): the PD
+           energy is invariant under rigid motions (F' = Q F), gravity and forces rotate
+           as vectors, and the plane becomes z' = 0.
   v_{i+1} = (x_{i+1} - x_i)/h                                  (P:368, eq:implicit_x)
 
 The constrained global solve is the plain definition (a direct sparse solve of
@@ -62,6 +66,8 @@ class Scene:
     fiber: tuple = (1.0, 0.0, 0.0)
     contact_mode: str = "frictionless"   # or "sticky": the paper's infinite-friction model
     volume: bool = False                 # volume-preserving term of the background elasticity
+    plane_n: tuple = (0.0, 0.0, 1.0)     # contact plane n . x = plane_d, unit normal into the free side
+    plane_d: float = 0.0
 
     def __post_init__(self):
         self.n = self.rest.shape[0]
@@ -419,7 +425,54 @@ def scene_from_inputs(inp, youngs=None):
                  youngs=cfg.youngs if youngs is None else youngs, poisson=cfg.poisson,
                  gravity=np.asarray(cfg.gravity, float), fixed_dofs=inp["fixed_dofs"],
                  contact_nodes=inp["contact_nodes"], muscle=cfg.muscle, volume=getattr(cfg, "volume", False),
-                 contact_mode=getattr(cfg, "contact_mode", "frictionless"))
+                 contact_mode=getattr(cfg, "contact_mode", "frictionless"),
+                 plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0))
+
+
+# ---- general contact plane n . x = d: a rigid change of world coordinates ----
+def plane_rotation(n):
+    """Rotation Q (rows t1, t2, n) with Q n = e_z: Gram-Schmidt from the coordinate axis least aligned
+    with n; Q = I for n = e_z."""
+    n = np.asarray(n, float) / np.linalg.norm(n)
+    if np.array_equal(n, [0.0, 0.0, 1.0]):
+        return np.eye(3)
+    e = np.eye(3)[int(np.argmin(np.abs(n)))]
+    t1 = e - (e @ n) * n
+    t1 /= np.linalg.norm(t1)
+    t2 = np.cross(n, t1)
+    return np.vstack([t1, t2, n])
+
+
+def has_plane(scene):
+    return len(scene.contact_nodes) > 0 and (tuple(scene.plane_n) != (0.0, 0.0, 1.0) or scene.plane_d != 0.0)
+
+
+def plane_scene(scene):
+    """The same scene in plane coordinates x' = Q x - d e_z: gravity rotated, plane z' = 0 (cached)."""
+    if getattr(scene, "_plane_scene", None) is None:
+        Q = plane_rotation(scene.plane_n)
+        scene._plane_scene = dataclasses.replace(scene, gravity=Q @ np.asarray(scene.gravity, float),
+                                                 plane_n=(0.0, 0.0, 1.0), plane_d=0.0)
+    return scene._plane_scene
+
+
+def to_plane(scene, a, point):
+    """[..., 3n] world -> plane coordinates (point: positions, x' = Q x - d e_z; else vectors, Q v)."""
+    Q = plane_rotation(scene.plane_n)
+    d = scene.plane_d / np.linalg.norm(scene.plane_n)
+    b = np.asarray(a, float).reshape(a.shape[:-1] + (-1, 3)) @ Q.T
+    if point:
+        b[..., 2] -= d
+    return b.reshape(a.shape)
+
+
+def from_plane(scene, a, point):
+    Q = plane_rotation(scene.plane_n)
+    d = scene.plane_d / np.linalg.norm(scene.plane_n)
+    b = np.asarray(a, float).reshape(a.shape[:-1] + (-1, 3)).copy()
+    if point:
+        b[..., 2] += d
+    return (b @ Q).reshape(a.shape)
 
 
 def forward(scene, q0, v0, f_ext, youngs, act=None, steps=1, tol=1e-12, fixed_iter=0,
@@ -427,6 +480,14 @@ def forward(scene, q0, v0, f_ext, youngs, act=None, steps=1, tol=1e-12, fixed_it
     """Trajectory of one simulation: returns dict(q[T+1,3n], v[T+1,3n], active[T,|V|], stats).
 
     f_ext: [3n] constant or [T, 3n] per step."""
+    if has_plane(scene):  # general plane: solve in plane coordinates, report in world coordinates
+        fe = np.asarray(f_ext, dtype=np.float64)
+        tr = forward(plane_scene(scene), to_plane(scene, np.asarray(q0, float), True),
+                     to_plane(scene, np.asarray(v0, float), False), to_plane(scene, fe, False), youngs, act, steps,
+                     tol, fixed_iter, method)
+        tr["q"] = from_plane(scene, tr["q"], True)
+        tr["v"] = from_plane(scene, tr["v"], False)
+        return tr
     w = scene.w_of(youngs)
     q = [q0.copy()]
     vv = [v0.copy()]

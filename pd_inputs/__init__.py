@@ -51,6 +51,8 @@ class Config:
     fext_std: float = 0.0    # N(0, fext_std) N per free DoF, constant in time (c3)
     lift: float = 0.0        # min z of the plate after tilt (c4)
     max_tilt_deg: float = 0.0
+    plane_n: tuple = (0.0, 0.0, 1.0)  # contact plane n . x = plane_d; the plate is placed `lift` above it
+    plane_d: float = 0.0
 
     @property
     def n_nodes(self) -> int:
@@ -95,6 +97,9 @@ CONFIGS = {
     # ---- volume-preserving energy variants: the c2 / c5 recipes with the volume term ----
     "c2v": Config("c2v", (8, 4, 4), h=0.01, steps=6, batch=2, seed=202, dirichlet="x0", v0_std=0.1,
                   per_sim_youngs=True, volume=True),
+    # c4s on a tilted plane n . x = d (P:278 general linear phi; 20 deg slope, offset 13 mm): frictionless sliding
+    "c4p": Config("c4p", (6, 5, 2), h=0.005, steps=12, batch=1, seed=104, contact=True,
+                  lift=0.001, max_tilt_deg=10.0, plane_n=(0.296198, 0.171010, 0.939693), plane_d=0.013),
     "c5v": Config("c5v", (6, 4, 3), h=0.01, steps=5, batch=2, seed=205, contact=True, muscle=True, volume=True),
 }
 
@@ -186,6 +191,10 @@ def make_inputs(cfg: Config, batch: Optional[int] = None, steps: Optional[int] =
             c = q.mean(axis=0)
             q = (q - c) @ Rm.T + c
             q[:, 2] += cfg.lift - q[:, 2].min()
+            if tuple(cfg.plane_n) != (0.0, 0.0, 1.0) or cfg.plane_d != 0.0:  # lowest node `lift` above the plane
+                nh = np.asarray(cfg.plane_n, float) / np.linalg.norm(cfg.plane_n)
+                dh = cfg.plane_d / np.linalg.norm(cfg.plane_n)
+                q += (cfg.lift + dh - (q @ nh).min()) * nh
         q0[b] = q.ravel()
     v0 = np.zeros((B, 3 * n))
     if cfg.v0_std > 0:

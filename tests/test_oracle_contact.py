@@ -164,3 +164,102 @@ def test_sticky_gradients_vs_central_fd():
         assert abs(fd - g["dq0"][k]) <= 1e-5 * max(1.0, abs(fd)), (k, fd, g["dq0"][k])
     # v0 of a pinned node has no effect (x_1 = x_0 there): its gradient is exactly (M/h) u_a = 0
     assert g["dv0"][pinned_dof] == 0.0
+
+
+# ---- general contact plane n . x = d ("phi is a linear function and n ... a constant vector") ----
+def test_plane_offset_is_a_translation():
+    # The plane z = d is the plane z = 0 with the whole scene lifted by d: positions shift by d e_z, velocities,
+    # active sets, iteration counts and every gradient are unchanged (the PD energy depends on x only through F).
+    from oracle import adjoint
+    inp = make_inputs(get_config("c4s"))
+    sc0 = pd.scene_from_inputs(inp)
+    d = 0.013
+    sc1 = pd.scene_from_inputs(inp)
+    sc1.plane_d = d
+    q0, v0, f = inp["q0"][0], inp["v0"][0], inp["f_ext"][0]
+    lift = np.zeros_like(q0)
+    lift[2::3] = d
+    t0 = pd.forward(sc0, q0, v0, f, 1e5, steps=inp["T"], tol=1e-13)
+    t1 = pd.forward(sc1, q0 + lift, v0, f, 1e5, steps=inp["T"], tol=1e-13)
+    np.testing.assert_array_equal(t0["active"], t1["active"])
+    assert t0["active"].any()
+    for i in range(inp["T"] + 1):
+        assert np.linalg.norm(t1["q"][i] - lift - t0["q"][i]) <= 1e-11 * np.linalg.norm(t0["q"][i])
+        assert np.linalg.norm(t1["v"][i] - t0["v"][i]) <= 1e-8 * max(1e-3, np.linalg.norm(t0["v"][i]))
+    g0 = adjoint.backward(sc0, t0, 1e5, inp["c_q"][0], inp["c_v"][0])
+    g1 = adjoint.backward(sc1, t1, 1e5, inp["c_q"][0], inp["c_v"][0])
+    for k in ("dq0", "dv0", "dfext"):
+        assert np.linalg.norm(g1[k] - g0[k]) <= 1e-7 * np.linalg.norm(g0[k]), k
+    assert abs(g1["dE"] - g0["dE"]) <= 1e-7 * abs(g0["dE"])
+
+
+def test_tilted_plane_kkt_in_world_coordinates():
+    # c4p: the tilted plate falls on a 20-degree plane n . x = d.  Checked with the WORLD-frame objective (no
+    # change of coordinates): at every step x_{i+1} is the KKT point of min g s.t. n . x_j >= d (frictionless):
+    # active nodes lie exactly on the plane, carry a compressive normal force n . grad_j g >= 0 and no tangential
+    # force; every other free DoF has grad g = 0; no candidate penetrates beyond eps_phi.
+    cfg = get_config("c4p")
+    inp = make_inputs(cfg)
+    sc = pd.scene_from_inputs(inp)
+    w = sc.w_of(1e5)
+    n = np.asarray(cfg.plane_n) / np.linalg.norm(cfg.plane_n)
+    dd = cfg.plane_d / np.linalg.norm(cfg.plane_n)
+    tr = pd.forward(sc, inp["q0"][0], inp["v0"][0], inp["f_ext"][0], 1e5, steps=cfg.steps, tol=1e-13)
+    cand = np.asarray(sc.contact_nodes)
+    touched, slid = 0, 0.0
+    for i in range(cfg.steps):
+        x, xi, vi = tr["q"][i + 1], tr["q"][i], tr["v"][i]
+        y = sc.y(xi, vi, inp["f_ext"][0])
+        _, gg = sc.objective(x, y, w)
+        scale = np.linalg.norm(sc.mass / sc.h ** 2 * y)
+        X, G = x.reshape(-1, 3), gg.reshape(-1, 3)
+        act = tr["active"][i]
+        phi = X[cand] @ n - dd
+        assert np.all(np.abs(phi[act]) <= 1e-12)
+        assert np.all(phi >= -pd.EPS_PHI_REL * cfg.dx)
+        lam = G[cand] @ n
+        assert np.all(lam[act] >= -1e-9 * scale)
+        tang = G[cand] - lam[:, None] * n[None, :]
+        assert np.abs(tang[act]).max(initial=0.0) <= 1e-9 * scale
+        rest_free = np.ones(sc.n, bool)
+        rest_free[cand[act]] = False
+        assert np.abs(G[rest_free]).max() <= 1e-9 * scale
+        touched += int(act.sum())
+        both = act & tr["active"][i - 1] if i > 0 else np.zeros_like(act)
+        if both.any():  # frictionless: pinned nodes may slide along the plane
+            slid = max(slid, np.abs((X[cand[both]] - xi.reshape(-1, 3)[cand[both]]) @ (np.eye(3) - np.outer(n, n))).max())
+    assert touched > 0 and slid > 1e-6
+
+
+def test_tilted_plane_gradients_vs_central_fd():
+    # dL/dq0, dL/dv0 and dL/dE of L = c_q . q_T + c_v . v_T through contact steps on the tilted plane, against
+    # central differences of the world-frame forward (the active sets do not change under the perturbation).
+    from oracle import adjoint
+    cfg = get_config("c4p", steps=6)
+    inp = make_inputs(cfg)
+    sc = pd.scene_from_inputs(inp)
+    q0, v0, f = inp["q0"][0], inp["v0"][0], inp["f_ext"][0]
+    cq, cv = inp["c_q"][0], inp["c_v"][0]
+
+    def run(q, v, E):
+        t = pd.forward(sc, q, v, f, E, steps=cfg.steps, tol=1e-13)
+        return float(cq @ t["q"][-1] + cv @ t["v"][-1]), t
+
+    L0, tr = run(q0, v0, 1e5)
+    assert tr["active"].any()
+    g = adjoint.backward(sc, tr, 1e5, cq, cv)
+    rng = np.random.default_rng(3)
+    eps = 1e-7
+    for _ in range(2):
+        dq = rng.standard_normal(q0.size)
+        dv = rng.standard_normal(q0.size)
+        lp, tp = run(q0 + eps * dq, v0 + eps * dv, 1e5)
+        lm, tm = run(q0 - eps * dq, v0 - eps * dv, 1e5)
+        assert np.array_equal(tp["active"], tr["active"]) and np.array_equal(tm["active"], tr["active"])
+        fd = (lp - lm) / (2 * eps)
+        an = g["dq0"] @ dq + g["dv0"] @ dv
+        assert abs(fd - an) <= 1e-5 * max(1.0, abs(fd)), (fd, an)
+    lp, _ = run(q0, v0, 1e5 * (1 + 1e-6))
+    lm, _ = run(q0, v0, 1e5 * (1 - 1e-6))
+    fd = (lp - lm) / (2e-6 * 1e5)
+    assert abs(fd - g["dE"]) <= 1e-5 * max(1e-3, abs(fd)), (fd, g["dE"])
