@@ -88,7 +88,7 @@ typedef struct {
   double youngs_ref;      /* Young's modulus of the ONE factorised A (0 = material.youngs).
                              Sims with other E use the majorising step of DESIGN.md §2.12  */
   /* Frictionless node-plane contact (Alg. 1):
-   * candidate nodes V (host, node indices), plane z = 0 with normal +z.        */
+   * candidate nodes V (host, node indices); the plane is plane_n / plane_d below (default z = 0, normal +z). */
   const int32_t* contact_nodes;
   int32_t n_contact;
   int32_t max_outer;      /* Alg. 1 "maximum iteration" (default 10)                     */
@@ -107,6 +107,14 @@ typedef struct {
                              outer iterations of a time step (restricted to the new free DoFs, Gram matrix
                              recomputed); 0 restarts the history with every corrector solve.  Changes
                              iteration counts, not the converged minimiser   */
+  /* Contact plane n . x = d ("phi is a linear function and n ... a constant vector"): plane_n need not be
+   * unit (normalised; all zero = +z), the free side is n . x > d; phi_j = n . x_j - d, lambda_j = n . grad_j g.
+   * Default (zero-initialised or {0, 0, 1}, 0): the ground z = 0 of BASELINE configs[3-4].  Internally the
+   * library works in plane coordinates x' = Q x - d e_z (a rigid motion: the PD energy is invariant; gravity,
+   * f_ext and all ABI vectors are rotated at the boundary, results are returned in world coordinates).
+   * Non-finite values -> INVALID_ARGUMENT.  Ignored without contact candidates. */
+  double plane_n[3];
+  double plane_d;
 } pd_options;
 
 /* Per-step statistics, caller-owned HOST arrays of length B*steps (index

@@ -61,7 +61,7 @@ class Simulator:
                  tol_fwd=1e-9, tol_adj=1e-9, max_iter_fwd=20000, max_iter_adj=20000, fixed_iter=0,
                  accel_fwd=1, accel_adj=1, check_every=1, max_batch=1, max_steps=1, youngs_ref=0.0,
                  max_outer=10, eps_phi=None, profile=0, outer_warm=1, x0_predict=0, contact_mode=1,
-                 lbfgs_warm=0, volume=False):
+                 lbfgs_warm=0, volume=False, plane_n=(0.0, 0.0, 1.0), plane_d=0.0):
         self.lib = _lib.load()
         rest = np.ascontiguousarray(rest, dtype=np.float64)
         hex8 = np.ascontiguousarray(hex8, dtype=np.int32)
@@ -79,7 +79,8 @@ class Simulator:
                              check_every, max_batch, max_steps, youngs_ref,
                              cand.ctypes.data_as(_lib.ip) if len(cand) else None, len(cand), max_outer,
                              float(1e-6 * dx if eps_phi is None else eps_phi), int(profile), int(outer_warm),
-                             int(contact_mode), int(x0_predict), int(lbfgs_warm))
+                             int(contact_mode), int(x0_predict), int(lbfgs_warm),
+                             (C.c_double * 3)(*[float(c) for c in plane_n]), float(plane_d))
         h_ = C.c_void_p()
         st = self.lib.pd_create(C.byref(mesh), C.byref(mat), float(h),
                                 fixed.ctypes.data_as(_lib.ip) if len(fixed) else None, len(fixed),
@@ -221,7 +222,8 @@ def simulator_from_inputs(inp, **kw):
                 volume=getattr(cfg, "volume", False),
                 youngs=cfg.youngs, poisson=cfg.poisson, density=cfg.density, h=cfg.h, gravity=cfg.gravity,
                 fixed_dofs=inp["fixed_dofs"], contact_nodes=inp["contact_nodes"], muscle_w=muscle_w,
-                fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"])
+                fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"],
+                plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0))
     args.update(kw)
     if cfg.per_sim_youngs and "youngs_ref" not in kw:
         # plain PD needs the majorising A_ref (largest E of the batch); the quasi-Newton

@@ -42,7 +42,8 @@ class PdOptions(C.Structure):
                 ("max_steps", C.c_int32), ("youngs_ref", C.c_double), ("contact_nodes", ip),
                 ("n_contact", C.c_int32), ("max_outer", C.c_int32), ("eps_phi", C.c_double),
                 ("profile", C.c_int32), ("outer_warm", C.c_int32), ("contact_mode", C.c_int32),
-                ("x0_predict", C.c_int32), ("lbfgs_warm", C.c_int32)]
+                ("x0_predict", C.c_int32), ("lbfgs_warm", C.c_int32), ("plane_n", C.c_double * 3),
+                ("plane_d", C.c_double)]
 
 
 class PdStats(C.Structure):

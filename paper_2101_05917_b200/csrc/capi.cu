@@ -56,6 +56,9 @@ struct pd_sim {
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
+  // general contact plane n . x = d: plane coordinates x' = Q x - d e_z inside the library
+  bool frame = false;
+  FrameQ fq{};
   // Newton-PCG forward (accel_fwd = 2): CG mask, CG statistics, forcing term (relative CG residual)
   int32_t *pact = nullptr, *nt_iters = nullptr, *nt_flag = nullptr;
   double* nt_res = nullptr;
@@ -228,6 +231,40 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   k_dot_partial<<<dim3(nchunk, red_groups(B)), red_threads(B), 0, s->stream>>>(da, len, B, s->partial);
   LAUNCH_CHECK(s);
   k_dot_final<<<p * B, 128, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
+  LAUNCH_CHECK(s);
+}
+
+// ABI <-> state conversions at the library boundary; with a general contact plane they also change coordinates
+// (kind 1: positions, 2: vectors; kind 0: no coordinates, e.g. scalars per DoF).  Without a plane the plain
+// layout kernels run (bitwise the default path).
+void abi_in(pd_sim* s, const double* in, double* out, int B, int64_t bstride, int kind) {
+  const int n3 = 3 * s->plan.n;
+  if (s->frame && kind) {
+    k_abi_to_state_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(in, out, s->plan.n, B, bstride, s->fq,
+                                                                            kind == 1);
+  } else {
+    k_abi_to_state<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(in, out, n3, B, bstride);
+  }
+  LAUNCH_CHECK(s);
+}
+void abi_out(pd_sim* s, const double* in, double* out, int B, int64_t bstride, int kind) {
+  const int n3 = 3 * s->plan.n;
+  if (s->frame && kind) {
+    k_state_to_abi_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(in, out, s->plan.n, B, bstride, s->fq,
+                                                                            kind == 1);
+  } else {
+    k_state_to_abi<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(in, out, n3, B, bstride);
+  }
+  LAUNCH_CHECK(s);
+}
+void abi_add(pd_sim* s, double* out, const double* in, int B, int64_t bstride) {  // vectors, non-Dirichlet nodes
+  const int n3 = 3 * s->plan.n;
+  if (s->frame) {
+    k_add_abi_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(out, in, s->plan.n, B, bstride, s->d_fixed,
+                                                                       s->fq);
+  } else {
+    k_add_abi<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(out, in, n3, B, bstride, s->d_fixed);
+  }
   LAUNCH_CHECK(s);
 }
 
@@ -832,6 +869,37 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->w_m = mat->muscle_w;
     for (int j = 0; j < 3; ++j) s->gravity[j] = mat->gravity[j];
     s->opt = *opts;
+    {  // general contact plane n . x = d: plane coordinates x' = Q x - d e_z, Q the minimal rotation
+       // (Rodrigues) taking the unit normal to e_z; gravity rotates with the frame
+      double nv[3] = {opts->plane_n[0], opts->plane_n[1], opts->plane_n[2]};
+      double nn = std::sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+      if (!std::isfinite(nn) || !std::isfinite(opts->plane_d))
+        return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "contact plane must be finite");
+      if (nn == 0.0) {
+        nv[0] = nv[1] = 0.0;
+        nv[2] = nn = 1.0;
+      }
+      for (double& c : nv) c /= nn;
+      const double d = opts->plane_d / nn;
+      double* Q = s->fq.q;
+      const double vx = nv[1], vy = -nv[0], c = nv[2];  // v = n x e_z (v_z = 0), c = n . e_z
+      if (c < -1.0 + 1e-12) {  // n = -e_z: half turn about x
+        const double R[9] = {1, 0, 0, 0, -1, 0, 0, 0, -1};
+        for (int k = 0; k < 9; ++k) Q[k] = R[k];
+      } else {  // Q = I + [v]x + [v]x^2 / (1 + c)
+        const double k = 1.0 / (1.0 + c);
+        const double R[9] = {1.0 - vy * vy * k, vx * vy * k, vy, vx * vy * k, 1.0 - vx * vx * k, -vx, -vy, vx,
+                             1.0 - (vx * vx + vy * vy) * k};
+        for (int j = 0; j < 9; ++j) Q[j] = R[j];
+      }
+      s->fq.d = d;
+      s->frame = opts->n_contact > 0 && !(nv[0] == 0.0 && nv[1] == 0.0 && nv[2] == 1.0 && d == 0.0);
+      if (s->frame) {
+        double g[3];
+        for (int r = 0; r < 3; ++r) g[r] = Q[3 * r] * s->gravity[0] + Q[3 * r + 1] * s->gravity[1] + Q[3 * r + 2] * s->gravity[2];
+        for (int r = 0; r < 3; ++r) s->gravity[r] = g[r];
+      }
+    }
     if (s->opt.check_every < 1) s->opt.check_every = 1;
     if (s->opt.max_iter_fwd < 1) s->opt.max_iter_fwd = 10000;
     if (s->opt.max_iter_adj < 1) s->opt.max_iter_adj = 10000;
@@ -1082,14 +1150,9 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   Nvtx nv_fwd("pd_forward");
   try {
     set_w(s, B, youngs_per_sim);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(q0, s->X, n3, B);
-    LAUNCH_CHECK(s);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(v0, s->V, n3, B);
-    LAUNCH_CHECK(s);
-    if (f_ext && !f_ext_step_stride) {
-      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(f_ext, s->Fext, n3, B);
-      LAUNCH_CHECK(s);
-    }
+    abi_in(s, q0, s->X, B, n3, 1);
+    abi_in(s, v0, s->V, B, n3, 2);
+    if (f_ext && !f_ext_step_stride) abi_in(s, f_ext, s->Fext, B, n3, 2);
     if (actuation && s->act) {
       CK(cudaMemcpyAsync(s->act, actuation, sizeof(double) * (int64_t)B * steps * P.m, cudaMemcpyDeviceToDevice,
                          s->stream));
@@ -1101,10 +1164,8 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       Nvtx nv_step("forward_step");
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
       const int64_t act_bs = (int64_t)steps * P.m;
-      if (f_ext && f_ext_step_stride) {  // time-varying f_ext: this step's slice of [B][steps][3n]
-        k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(f_ext + (int64_t)i * n3, s->Fext, n3, B, (int64_t)steps * n3);
-        LAUNCH_CHECK(s);
-      }
+      if (f_ext && f_ext_step_stride)  // time-varying f_ext: this step's slice of [B][steps][3n]
+        abi_in(s, f_ext + (int64_t)i * n3, s->Fext, B, (int64_t)steps * n3, 2);
       k_y<<<nblk(len), 256, 0, s->stream>>>(s->X, s->V, f_ext ? s->Fext : nullptr, s->d_mass, s->Y, P.n, B, s->h,
                                             s->gravity[0], s->gravity[1], s->gravity[2]);
       LAUNCH_CHECK(s);
@@ -1191,16 +1252,8 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       LAUNCH_CHECK(s);
       CK(cudaMemcpyAsync(s->traj + (int64_t)(i + 1) * len, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice,
                          s->stream));
-      if (q_traj) {
-        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->X, q_traj + (int64_t)(i + 1) * n3, n3, B,
-                                                         (int64_t)(steps + 1) * n3);
-        LAUNCH_CHECK(s);
-      }
-      if (v_traj) {
-        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->V, v_traj + (int64_t)(i + 1) * n3, n3, B,
-                                                         (int64_t)(steps + 1) * n3);
-        LAUNCH_CHECK(s);
-      }
+      if (q_traj) abi_out(s, s->X, q_traj + (int64_t)(i + 1) * n3, B, (int64_t)(steps + 1) * n3, 1);
+      if (v_traj) abi_out(s, s->V, v_traj + (int64_t)(i + 1) * n3, B, (int64_t)(steps + 1) * n3, 2);
     }
     if (q_traj)
       CK(cudaMemcpy2DAsync(q_traj, (steps + 1) * n3 * sizeof(double), q0, n3 * sizeof(double), n3 * sizeof(double), B,
@@ -1255,14 +1308,12 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
   const double h = s->h;
   try {
     if (dL_dqT) {
-      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(dL_dqT, s->AX, n3, B);
-      LAUNCH_CHECK(s);
+      abi_in(s, dL_dqT, s->AX, B, n3, 2);
     } else {
       CK(cudaMemsetAsync(s->AX, 0, len * sizeof(double), s->stream));
     }
     if (dL_dvT) {
-      k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(dL_dvT, s->AV, n3, B);
-      LAUNCH_CHECK(s);
+      abi_in(s, dL_dvT, s->AV, B, n3, 2);
     } else {
       CK(cudaMemsetAsync(s->AV, 0, len * sizeof(double), s->stream));
     }
@@ -1270,14 +1321,8 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
     CK(cudaMemsetAsync(s->dw_acc, 0, B * sizeof(double), s->stream));
     if (s->dwv_acc) CK(cudaMemsetAsync(s->dwv_acc, 0, B * sizeof(double), s->stream));
     const int64_t sstride = (int64_t)(T + 1) * n3;  // batch stride of [B][T+1][3n] per-step loss arrays
-    if (dq_steps) {
-      k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)T * n3, n3, B, sstride, s->d_fixed);
-      LAUNCH_CHECK(s);
-    }
-    if (dv_steps) {
-      k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dv_steps + (int64_t)T * n3, n3, B, sstride, s->d_fixed);
-      LAUNCH_CHECK(s);
-    }
+    if (dq_steps) abi_add(s, s->AX, dq_steps + (int64_t)T * n3, B, sstride);
+    if (dv_steps) abi_add(s, s->AV, dv_steps + (int64_t)T * n3, B, sstride);
     const bool pcg = s->opt.accel_adj != 0;
     Nvtx nv_bwd("pd_backward");
     for (int i = T - 1; i >= 0; --i) {
@@ -1369,8 +1414,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
       LAUNCH_CHECK(s);
       if (dfext_steps) {  // dL/df_ext of step i = u_i (0 on Dirichlet DoFs)
         zero_constrained_fixed(s, s->U, B);
-        k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->U, dfext_steps + (int64_t)i * n3, n3, B, (int64_t)T * n3);
-        LAUNCH_CHECK(s);
+        abi_out(s, s->U, dfext_steps + (int64_t)i * n3, B, (int64_t)T * n3, 2);
       }
       const bool sticky_step = s->sticky && s->pins_live;
       if (sticky_step) {  // pinned values x_{i+1,a} = x_{i,a}: EX = b_a - (A_N u)_a
@@ -1387,29 +1431,16 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->AX, s->AX, 1.0, s->Pv, nullptr, 1.0, len, B, nullptr);
         LAUNCH_CHECK(s);
       }
-      if (dq_steps) {
-        k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dq_steps + (int64_t)i * n3, n3, B, sstride, s->d_fixed);
-        LAUNCH_CHECK(s);
-      }
-      if (dv_steps) {
-        k_add_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dv_steps + (int64_t)i * n3, n3, B, sstride, s->d_fixed);
-        LAUNCH_CHECK(s);
-      }
+      if (dq_steps) abi_add(s, s->AX, dq_steps + (int64_t)i * n3, B, sstride);
+      if (dv_steps) abi_add(s, s->AV, dv_steps + (int64_t)i * n3, B, sstride);
       s->pins_live = false;
     }
-    if (dL_dq0) {
-      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->AX, dL_dq0, n3, B, n3);
-      LAUNCH_CHECK(s);
-    }
-    if (dL_dv0) {
-      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->AV, dL_dv0, n3, B, n3);
-      LAUNCH_CHECK(s);
-    }
+    if (dL_dq0) abi_out(s, s->AX, dL_dq0, B, n3, 2);
+    if (dL_dv0) abi_out(s, s->AV, dL_dv0, B, n3, 2);
     if (dL_dfext) {
       k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->d_fixed, P.n, B, nullptr, nullptr);
       LAUNCH_CHECK(s);
-      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->DF, dL_dfext, n3, B, n3);
-      LAUNCH_CHECK(s);
+      abi_out(s, s->DF, dL_dfext, B, n3, 2);
     }
     // dL/dE = dL/dw / (1+nu); dL/dnu = -dL/dw E/(1+nu)^2   (w = E/(1+nu))
     // with the volume term (w_v = lambda = E nu/((1+nu)(1-2nu))) both weights enter

@@ -275,6 +275,54 @@ __global__ void k_state_to_abi(const double* __restrict__ in, double* __restrict
   out[(int64_t)b * out_bstride + d] = in[i];
 }
 
+// ---- general contact plane n . x = d: the library works in plane coordinates
+// x' = Q x - d e_z (Q n = e_z); the PD energy is invariant under this rigid motion, so only the ABI boundary changes.
+// One thread per (node, sim): the node's three components.
+struct FrameQ {
+  double q[9];  // row-major rotation, rows t1, t2, n
+  double d;     // plane offset along the unit normal
+};
+// ABI [B][bstride] (world) -> state [n][3][B] (plane): point = positions (affine), else vectors
+__global__ void k_abi_to_state_frame(const double* __restrict__ in, double* __restrict__ out, int n, int B,
+                                     int64_t bstride, FrameQ f, int point) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * B) return;
+  const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
+  const double* v = in + (int64_t)b * bstride + 3 * (int64_t)node;
+  const double v0 = v[0], v1 = v[1], v2 = v[2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    double o = f.q[3 * r] * v0 + f.q[3 * r + 1] * v1 + f.q[3 * r + 2] * v2;
+    if (point && r == 2) o -= f.d;
+    out[((int64_t)node * 3 + r) * B + b] = o;
+  }
+}
+// state [n][3][B] (plane) -> ABI [B][bstride] (world): x = Q^T (x' + d e_z)
+__global__ void k_state_to_abi_frame(const double* __restrict__ in, double* __restrict__ out, int n, int B,
+                                     int64_t bstride, FrameQ f, int point) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * B) return;
+  const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
+  const double* v = in + (int64_t)node * 3 * B + b;
+  const double v0 = v[0], v1 = v[B], v2 = v[2 * B] + (point ? f.d : 0.0);
+  double* o = out + (int64_t)b * bstride + 3 * (int64_t)node;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) o[c] = f.q[c] * v0 + f.q[3 + c] * v1 + f.q[6 + c] * v2;
+}
+// OUT += Q in (vectors, ABI -> state) on non-Dirichlet nodes (per-step loss terms in plane coordinates)
+__global__ void k_add_abi_frame(double* __restrict__ out, const double* __restrict__ in, int n, int B, int64_t bstride,
+                                const uint8_t* __restrict__ fixed, FrameQ f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * B) return;
+  const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
+  if (fixed[node]) return;
+  const double* v = in + (int64_t)b * bstride + 3 * (int64_t)node;
+  const double v0 = v[0], v1 = v[1], v2 = v[2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    out[((int64_t)node * 3 + r) * B + b] += f.q[3 * r] * v0 + f.q[3 * r + 1] * v1 + f.q[3 * r + 2] * v2;
+}
+
 // y = x + h v + h^2 (g + f_ext / m)
 __global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
                     const double* __restrict__ Fext, const double* __restrict__ mass, double* __restrict__ Y,

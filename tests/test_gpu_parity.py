@@ -314,9 +314,14 @@ def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, tol_fw
                 nodes = inp["contact_nodes"][sets[b, i]]
                 pins = (3 * nodes[:, None] + np.arange(3)).ravel()
                 assert np.array_equal(gpu["q"][b, i + 1][pins], gpu["q"][b, i][pins])
-            else:
+            elif tuple(inp["cfg"].plane_n) == (0.0, 0.0, 1.0) and inp["cfg"].plane_d == 0.0:
                 # pinned normal DoFs sit exactly on the plane z = 0 (eq:dirichlet with xbar = 0)
                 assert np.all(gpu["q"][b, i + 1][cand[sets[b, i]]] == 0.0)
+            else:
+                # general plane n . x = d: pinned nodes on it up to the rounding of the change of coordinates
+                nh = np.asarray(inp["cfg"].plane_n) / np.linalg.norm(inp["cfg"].plane_n)
+                X = gpu["q"][b, i + 1].reshape(-1, 3)[inp["contact_nodes"][sets[b, i]]]
+                assert np.all(np.abs(X @ nh - inp["cfg"].plane_d / np.linalg.norm(inp["cfg"].plane_n)) <= 1e-15)
         n_active += int(sets[b].sum())
     assert n_active > 0, "the workload never touched the plane"
     _compare(inp, gpu, range(inp["B"]))
@@ -333,6 +338,13 @@ def test_c4s_contact_drop_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
 def test_c5s_contact_muscle_parity(torch, accel_fwd, outer_warm, lbfgs_warm):
     # configs[4] recipe at oracle size: muscle actuation + bottom-face contact, B = 2.
     _contact_parity(torch, "c5s", accel_fwd, outer_warm, lbfgs_warm)
+
+
+@pytest.mark.parametrize("accel_fwd,outer_warm", [(0, 0), (1, 1)])
+def test_tilted_plane_contact_parity(torch, accel_fwd, outer_warm):
+    # general contact plane n . x = d (20-degree slope, offset 13 mm, config c4p): the plate lands and
+    # slides; bit-exact active sets and outer counts, positions / velocities / gradients in world coordinates
+    _contact_parity(torch, "c4p", accel_fwd, outer_warm, 0)
 
 
 def test_contact_deterministic(torch):
