@@ -37,11 +37,16 @@ def hessian_blocks(scene, x, w, act=None):
         Jv = energy.volume_jacobian(F)
         H = H + w * scene.vol_ratio * scene.V * np.einsum("qka,mqkl,qlb->mab", G, I9 - Jv, G, optimize=True)
     if scene.muscle:
-        Fm = F @ np.asarray(scene.fiber)
+        Fm = np.einsum("mqij,mj->mqi", F, scene.fibers)             # F m_e (per-element fibers)
         r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
-        Jm, p, n_hat = energy.muscle_jacobian(Fm, r, scene.fiber)
-        Gm = fem.Gm_matrices(scene.dx, scene.fiber)
-        H = H + scene.w_muscle * scene.V * np.einsum("qka,mqkl,qlb->mab", Gm, np.eye(3) - Jm, Gm, optimize=True)
+        Jm, p, n_hat = energy.muscle_jacobian(Fm, r, scene.fibers[:, None, :])
+        if scene.fiber_dir is None:
+            Gm = fem.Gm_matrices(scene.dx, scene.fiber)
+            H = H + scene.w_muscle * scene.V * np.einsum("qka,mqkl,qlb->mab", Gm, np.eye(3) - Jm, Gm, optimize=True)
+        else:
+            Gm = np.stack([fem.Gm_matrices(scene.dx, fe) for fe in scene.fibers])   # [m, q, 3, 24]
+            H = H + scene.w_muscle * scene.V * np.einsum("mqka,mqkl,mqlb->mab", Gm, np.eye(3) - Jm, Gm,
+                                                         optimize=True)
     return H
 
 
@@ -80,10 +85,10 @@ def param_terms(scene, x, u, act=None):
     dwv = -scene.V * np.sum(Gu * (F - energy.volume_project(F)[0])) if getattr(scene, "volume", False) else 0.0
     dr = None
     if scene.muscle:
-        Fm = F @ np.asarray(scene.fiber)
+        Fm = np.einsum("mqij,mj->mqi", F, scene.fibers)
         r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
-        p, n_hat, nrm = energy.muscle_project(Fm, r, scene.fiber)
-        Gmu = Gu @ np.asarray(scene.fiber)
+        p, n_hat, nrm = energy.muscle_project(Fm, r, scene.fibers[:, None, :])
+        Gmu = np.einsum("mqij,mj->mqi", Gu, scene.fibers)
         dr = scene.w_muscle * scene.V * np.sum(n_hat * Gmu, axis=(-1, -2))
     return dw, dr, dwv
 

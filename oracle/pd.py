@@ -68,6 +68,7 @@ class Scene:
     volume: bool = False                 # volume-preserving term of the background elasticity
     plane_n: tuple = (0.0, 0.0, 1.0)     # contact plane n . x = plane_d, unit normal into the free side
     plane_d: float = 0.0
+    fiber_dir: Optional[np.ndarray] = None  # [m, 3] per-element fiber directions (normalised); None = `fiber`
 
     def __post_init__(self):
         self.n = self.rest.shape[0]
@@ -78,8 +79,17 @@ class Scene:
         self.free = np.ones(self.N, bool)
         self.free[self.fixed_dofs] = False
         self.Kcorot = fem.assemble_blocks(fem.element_stiffness(self.dx, 1.0), self.hex8, self.n)
-        self.Kmus = (fem.assemble_blocks(fem.element_stiffness(self.dx, 0.0, 1.0, self.fiber),
-                                         self.hex8, self.n) if self.muscle else None)
+        if self.fiber_dir is not None:
+            f = np.asarray(self.fiber_dir, np.float64)
+            self.fibers = f / np.linalg.norm(f, axis=1, keepdims=True)
+            # per-element muscle blocks sum_q V G_mq^T G_mq with the element's own fiber
+            self.Kmus = (fem.assemble_blocks(np.stack([fem.element_stiffness(self.dx, 0.0, 1.0, fe)
+                                                       for fe in self.fibers]), self.hex8, self.n)
+                         if self.muscle else None)
+        else:
+            self.fibers = np.broadcast_to(np.asarray(self.fiber, np.float64), (self.m, 3))
+            self.Kmus = (fem.assemble_blocks(fem.element_stiffness(self.dx, 0.0, 1.0, self.fiber),
+                                             self.hex8, self.n) if self.muscle else None)
         self._factors = {}
 
     # ---- material (reading §8c.2 / §8c.3) ----
@@ -130,9 +140,9 @@ class Scene:
         if self.volume:
             out["D"] = energy.volume_project(F)[0]
         if self.muscle:
-            Fm = F @ np.asarray(self.fiber)
+            Fm = np.einsum("mqij,mj->mqi", F, self.fibers)           # F m_e per quad point
             r = np.broadcast_to(np.asarray(act)[:, None], Fm.shape[:-1])
-            p, n_hat, nrm = energy.muscle_project(Fm, r, self.fiber)
+            p, n_hat, nrm = energy.muscle_project(Fm, r, self.fibers[:, None, :])
             out.update(Fm=Fm, p=p)
         return out
 
@@ -150,7 +160,7 @@ class Scene:
         if self.muscle:
             Dm = z["Fm"] - z["p"]
             E += 0.5 * self.w_muscle * self.V * np.sum(Dm * Dm)
-            P = P + self.w_muscle * self.V * Dm[..., :, None] * np.asarray(self.fiber)[None, None, None, :]
+            P = P + self.w_muscle * self.V * Dm[..., :, None] * self.fibers[:, None, None, :]
         grad = fem.scatter_element_forces(P, self.hex8, self.dx, self.n)
         return E, grad
 
@@ -160,7 +170,7 @@ class Scene:
         if self.volume:
             P = P + w * self.vol_ratio * self.V * z["D"]
         if self.muscle:
-            P = P + self.w_muscle * self.V * z["p"][..., :, None] * np.asarray(self.fiber)[None, None, None, :]
+            P = P + self.w_muscle * self.V * z["p"][..., :, None] * self.fibers[:, None, None, :]
         return self.mass / self.h ** 2 * y + fem.scatter_element_forces(P, self.hex8, self.dx, self.n)
 
     def objective(self, x, y, w, act=None):
@@ -426,7 +436,8 @@ def scene_from_inputs(inp, youngs=None):
                  gravity=np.asarray(cfg.gravity, float), fixed_dofs=inp["fixed_dofs"],
                  contact_nodes=inp["contact_nodes"], muscle=cfg.muscle, volume=getattr(cfg, "volume", False),
                  contact_mode=getattr(cfg, "contact_mode", "frictionless"),
-                 plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0))
+                 plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0),
+                 fiber_dir=inp.get("fiber_dir"))
 
 
 # ---- general contact plane n . x = d: a rigid change of world coordinates ----

@@ -53,6 +53,7 @@ class Config:
     max_tilt_deg: float = 0.0
     plane_n: tuple = (0.0, 0.0, 1.0)  # contact plane n . x = plane_d; the plate is placed `lift` above it
     plane_d: float = 0.0
+    fiber_field: bool = False  # per-element fiber directions: +x perturbed by N(0, 0.4^2) per component, normalised
 
     @property
     def n_nodes(self) -> int:
@@ -100,6 +101,8 @@ CONFIGS = {
     # c4s on a tilted plane n . x = d (P:278 general linear phi; 20 deg slope, offset 13 mm): frictionless sliding
     "c4p": Config("c4p", (6, 5, 2), h=0.005, steps=12, batch=1, seed=104, contact=True,
                   lift=0.001, max_tilt_deg=10.0, plane_n=(0.296198, 0.171010, 0.939693), plane_d=0.013),
+    # c5s with a per-element fiber field (SURVEY §8(b) material.fiber_dir): muscle + contact
+    "c5f": Config("c5f", (6, 4, 3), h=0.01, steps=6, batch=2, seed=105, contact=True, muscle=True, fiber_field=True),
     "c5v": Config("c5v", (6, 4, 3), h=0.01, steps=5, batch=2, seed=205, contact=True, muscle=True, volume=True),
 }
 
@@ -155,9 +158,9 @@ def make_inputs(cfg: Config, batch: Optional[int] = None, steps: Optional[int] =
     B = cfg.batch if batch is None else int(batch)
     T = cfg.steps if steps is None else int(steps)
     ss = np.random.SeedSequence(cfg.seed)
-    ch = ss.spawn(8)
+    ch = ss.spawn(9)  # (child i depends on i only: the 9th, "fiber", leaves the first eight draws unchanged)
     rng = {name: np.random.default_rng(c) for name, c in
-           zip(["v0", "cq", "cv", "E", "target", "fext", "tilt", "act"], ch)}
+           zip(["v0", "cq", "cv", "E", "target", "fext", "tilt", "act", "fiber"], ch)}
     rest, hex8 = grid_mesh(cfg.counts, cfg.dx)
     n = rest.shape[0]
     m = hex8.shape[0]
@@ -213,6 +216,10 @@ def make_inputs(cfg: Config, batch: Optional[int] = None, steps: Optional[int] =
     act = None
     if cfg.muscle:
         act = rng["act"].uniform(0.8, 1.2, size=(B, T, m))
+    fiber_dir = None
+    if cfg.fiber_field:
+        f = np.array([1.0, 0.0, 0.0]) + rng["fiber"].normal(0.0, 0.4, size=(m, 3))
+        fiber_dir = f / np.linalg.norm(f, axis=1, keepdims=True)
     # Tip loss (c3): nodes on the x = max face; seeded targets = rest tip
     # positions displaced by N(0, 1 cm) per component ("vs seeded targets").
     tip_nodes = np.nonzero(rest[:, 0] == rest[:, 0].max())[0].astype(np.int32)
@@ -221,5 +228,5 @@ def make_inputs(cfg: Config, batch: Optional[int] = None, steps: Optional[int] =
 
     return dict(cfg=cfg, B=B, T=T, rest=rest, hex8=hex8, n_nodes=n, n_elems=m,
                 fixed_dofs=fixed_dofs, contact_nodes=contact_nodes,
-                q0=q0, v0=v0, f_ext=f_ext, youngs=youngs, act=act,
+                q0=q0, v0=v0, f_ext=f_ext, youngs=youngs, act=act, fiber_dir=fiber_dir,
                 c_q=c_q, c_v=c_v, tip_nodes=tip_nodes, tip_target=tip_target)

@@ -165,3 +165,36 @@ def test_volume_AN_is_jacobian_of_grad_g():
     eps = 1e-7
     fd = (sc.objective(x + eps * d, y, w)[1] - sc.objective(x - eps * d, y, w)[1]) / (2 * eps)
     assert np.linalg.norm(AN @ d - fd) <= 1e-6 * np.linalg.norm(fd)
+
+
+def test_gradients_vs_central_fd_fiber_field():
+    # per-element fiber directions (SURVEY §8(b) material.fiber_dir): muscle energy (w_m/2)(||F m_e|| - r)^2 with
+    # each element's own m_e; gradients wrt q0, v0, r and E against central differences (no contact)
+    _fd_check("c5f", 2, ["q0", "v0", "act", "E"], 1e-5, kw=dict(contact=False))
+
+
+def test_fiber_field_energy_closed_form_and_A():
+    # Under an affine deformation x = F X every quad point has F_q = F, so the muscle energy of element e is exactly
+    # 8 (w_m V / 2)(||F m_e|| - r_e)^2 (reading §8c.4), and x^T A_mus x = sum_e 8 w_m V ||F m_e||^2
+    # for the muscle part of A (P:199-202 with G_m x = F m_e) -- written out here per element, not through G.
+    from oracle import energy, fem, pd
+    from pd_inputs import get_config, make_inputs
+    inp = make_inputs(get_config("c5f", contact=False))
+    sc = pd.scene_from_inputs(inp)
+    F = np.array([[1.05, 0.10, -0.03], [0.02, 0.97, 0.08], [-0.04, 0.05, 1.02]])
+    x = (inp["rest"] @ F.T).ravel()
+    r = inp["act"][0, 0]
+    sc_nm = pd.scene_from_inputs(inp)
+    sc_nm.muscle = False
+    w = sc.w_of(1e5)
+    e_mus = sc.objective(x, x, w, r)[0] - sc_nm.objective(x, x, w)[0]
+    m = inp["fiber_dir"]
+    closed = sum(8 * 0.5 * sc.w_muscle * sc.V * (np.linalg.norm(F @ m[e]) - r[e]) ** 2 for e in range(sc.m))
+    assert abs(e_mus - closed) <= 1e-12 * abs(closed)
+    quad = x @ (sc.Kmus @ x)
+    closed_q = sum(8 * sc.V * np.linalg.norm(F @ m[e]) ** 2 for e in range(sc.m))
+    assert abs(quad - closed_q) <= 1e-12 * closed_q
+    # a uniform field reproduces the uniform-fiber scene
+    inp_u = dict(inp, fiber_dir=np.tile([1.0, 0.0, 0.0], (sc.m, 1)))
+    sc_u, sc_0 = pd.scene_from_inputs(inp_u), pd.scene_from_inputs(dict(inp, fiber_dir=None))
+    assert abs(sc_u.objective(x, x, w, r)[0] - sc_0.objective(x, x, w, r)[0]) <= 1e-13 * abs(sc_0.objective(x, x, w, r)[0])
