@@ -63,6 +63,9 @@ typedef struct {
                              det D = 1, with w_v = lambda = E nu / ((1+nu)(1-2nu)) per sim (SPEC lame_weights,
                              DESIGN.md §2.16); its Jacobian from the differentiated KKT system.
                              pd_backward's dL_dE and dL_dnu then include the w_v terms.  0: corotated only.      */
+  const double* fiber_dir; /* [n_elems][3] HOST per-element fiber directions (normalised by the library; zero rows
+                             -> INVALID_ARGUMENT), or NULL = the uniform `fiber`.  The muscle energy of element e
+                             is (w_m/2) ||F m_e - p||^2 with its own m_e; A stays A_s (x) I_3       */
 } pd_material;
 
 /* Solver options.  Tolerances are on the relative residual

@@ -61,7 +61,7 @@ class Simulator:
                  tol_fwd=1e-9, tol_adj=1e-9, max_iter_fwd=20000, max_iter_adj=20000, fixed_iter=0,
                  accel_fwd=1, accel_adj=1, check_every=1, max_batch=1, max_steps=1, youngs_ref=0.0,
                  max_outer=10, eps_phi=None, profile=0, outer_warm=1, x0_predict=0, contact_mode=1,
-                 lbfgs_warm=0, volume=False, plane_n=(0.0, 0.0, 1.0), plane_d=0.0):
+                 lbfgs_warm=0, volume=False, plane_n=(0.0, 0.0, 1.0), plane_d=0.0, fiber_dir=None):
         self.lib = _lib.load()
         rest = np.ascontiguousarray(rest, dtype=np.float64)
         hex8 = np.ascontiguousarray(hex8, dtype=np.int32)
@@ -70,8 +70,13 @@ class Simulator:
         self._keep = [rest, hex8]
         mesh = _lib.PdMesh(self.n_nodes, self.n_elems, rest.ctypes.data_as(_lib.dp),
                            hex8.ctypes.data_as(_lib.ip), float(dx))
+        fib = None if fiber_dir is None else np.ascontiguousarray(fiber_dir, dtype=np.float64)
+        if fib is not None and fib.shape != (self.n_elems, 3):
+            raise ValueError(f"fiber_dir: expected shape ({self.n_elems}, 3), got {fib.shape}")
+        self._keep.append(fib)
         mat = _lib.PdMaterial(float(youngs), float(poisson), float(density), float(muscle_w),
-                              (C.c_double * 3)(*gravity), (C.c_double * 3)(*fiber), int(bool(volume)))
+                              (C.c_double * 3)(*gravity), (C.c_double * 3)(*fiber), int(bool(volume)),
+                              None if fib is None else fib.ctypes.data_as(_lib.dp))
         fixed = np.ascontiguousarray(fixed_dofs, dtype=np.int32)
         cand = np.ascontiguousarray(contact_nodes, dtype=np.int32)
         self._keep += [fixed, cand]
@@ -223,7 +228,8 @@ def simulator_from_inputs(inp, **kw):
                 youngs=cfg.youngs, poisson=cfg.poisson, density=cfg.density, h=cfg.h, gravity=cfg.gravity,
                 fixed_dofs=inp["fixed_dofs"], contact_nodes=inp["contact_nodes"], muscle_w=muscle_w,
                 fixed_iter=cfg.fixed_iter, tol_fwd=cfg.tol, max_batch=inp["B"], max_steps=inp["T"],
-                plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0))
+                plane_n=tuple(getattr(cfg, "plane_n", (0.0, 0.0, 1.0))), plane_d=getattr(cfg, "plane_d", 0.0),
+                fiber_dir=inp.get("fiber_dir"))
     args.update(kw)
     if cfg.per_sim_youngs and "youngs_ref" not in kw:
         # plain PD needs the majorising A_ref (largest E of the batch); the quasi-Newton

@@ -32,7 +32,7 @@ class PdMesh(C.Structure):
 class PdMaterial(C.Structure):
     _fields_ = [("youngs", C.c_double), ("poisson", C.c_double), ("density", C.c_double),
                 ("muscle_w", C.c_double), ("gravity", C.c_double * 3), ("fiber", C.c_double * 3),
-                ("volume", C.c_int32)]
+                ("volume", C.c_int32), ("fiber_dir", dp)]
 
 
 class PdOptions(C.Structure):

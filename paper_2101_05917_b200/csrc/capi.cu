@@ -45,6 +45,7 @@ struct pd_sim {
   Stencil st{};
   std::vector<DevBuf> bufs;
   // plan on device
+  double* d_fib = nullptr;  // [m][3] per-element unit fibers (material.fiber_dir) or null
   int32_t *d_hex8 = nullptr, *d_inc_ptr = nullptr, *d_inc_ec = nullptr, *d_pos = nullptr, *d_nodepos = nullptr;
   double* d_mass = nullptr;
   uint8_t* d_fixed = nullptr;
@@ -213,6 +214,7 @@ ElemArgs elem_args(pd_sim* s, int B, const double* act_step, int64_t act_bstride
   ea.w_sim = s->w_cur ? s->w_cur : s->w_sim;
   ea.act = act_step;
   ea.act_bstride = act_bstride;
+  ea.fib = s->d_fib;
   return ea;
 }
 
@@ -457,7 +459,7 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   const HostPlan& P = s->plan;
   {
     ProfScope ps(s, 0);
-    k_elem_residual<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
+    (s->d_fib ? k_elem_residual<true> : k_elem_residual<false>)<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
                                                                          s->EF, s->EE);
     LAUNCH_CHECK(s);
     if (s->st.kappa != 0.0) {  // volume-preserving term added to the element forces and energies
@@ -917,6 +919,17 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       if (!(fn > 0)) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "fiber direction must be non-zero");
       for (double& f : fiber) f /= fn;
     }
+    if (mat->fiber_dir && mat->muscle_w != 0.0) {  // per-element fibers (normalised here, host copy for A)
+      if (mesh->n_elems < 0) return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "negative element count");
+      s->plan.fib.assign(mat->fiber_dir, mat->fiber_dir + 3 * (int64_t)mesh->n_elems);
+      for (int64_t e = 0; e < mesh->n_elems; ++e) {
+        double* f = s->plan.fib.data() + 3 * e;
+        const double nf = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+        if (!(nf > 0) || !std::isfinite(nf))
+          return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "fiber_dir of element " + std::to_string(e) + " is not a direction");
+        for (int j = 0; j < 3; ++j) f[j] /= nf;
+      }
+    }
     const double yref = opts->youngs_ref > 0 ? opts->youngs_ref : mat->youngs;
     // volume-preserving term: w_v = lambda = w nu/(1 - 2 nu) per sim; A carries w + w_v
     const double kappa = mat->volume ? mat->poisson / (1.0 - 2.0 * mat->poisson) : 0.0;
@@ -948,6 +961,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->st.kappa = kappa;
     // ---- device residency
     s->d_hex8 = s->upload(P.hex8);
+    if (!P.fib.empty()) s->d_fib = s->upload(P.fib);
     s->d_inc_ptr = s->upload(P.inc_ptr);
     s->d_inc_ec = s->upload(P.inc_ec);
     s->d_pos = s->upload(P.pos_of_node);

@@ -336,6 +336,17 @@ __global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
   Y[i] = X[i] + h * V[i] + h * h * (g + f);
 }
 
+// fiber direction of element e: the per-element field (material.fiber_dir) or the uniform Stencil fiber
+__device__ __forceinline__ void fiber_of(const Stencil& st, const ElemArgs& ea, int e, double (&mf)[3]) {
+  if (ea.fib) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) mf[j] = __ldg(ea.fib + 3 * (int64_t)e + j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) mf[j] = st.fiber[j];
+  }
+}
+
 // ----------------------------------------------------------------- K1: local step
 #ifndef K1_MIN_BLOCKS
 #define K1_MIN_BLOCKS 5  // resident 256-thread blocks per SM the register allocation targets
@@ -436,6 +447,9 @@ __device__ __noinline__ void k1_polar_fallback(const double* __restrict__ X, con
   for (int k = 0; k < 9; ++k) out[k] = R[k];
 }
 
+// FIB: per-element fiber field (material.fiber_dir); the uniform-fiber instance reads the fiber from the kernel
+// parameters (no registers held for it: the tuned corotated/muscle path keeps its allocation)
+template <bool FIB>
 __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const double* __restrict__ X, Stencil st,
                                                                     ElemArgs ea, double* __restrict__ EF,
                                                                     double* __restrict__ EE) {
@@ -470,10 +484,17 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const doub
   double energy = 0.5 * w * st.V * en;
   if (st.w_m != 0.0) {
     const double r_act = ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0;
+    double mf[3];
+    if constexpr (FIB) {
+      fiber_of(st, ea, e, mf);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) mf[j] = st.fiber[j];
+    }
     double Fm[3], nr2 = 0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+      Fm[i] = F[3 * i] * mf[0] + F[3 * i + 1] * mf[1] + F[3 * i + 2] * mf[2];
       nr2 += Fm[i] * Fm[i];
     }
     const bool pos = nr2 > 1e-250;
@@ -481,7 +502,7 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const doub
     double dm[3], em = 0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double p = pos ? s_act * Fm[i] : r_act * st.fiber[i];
+      const double p = pos ? s_act * Fm[i] : r_act * mf[i];
       dm[i] = Fm[i] - p;
       em += dm[i] * dm[i];
     }
@@ -489,7 +510,7 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const doub
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * st.fiber[j];
+      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += st.w_m * st.V * dm[i] * mf[j];
   }
   __syncwarp();  // (the slot may have carried a fallback R: every lane has read its own before it is reused)
   store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
@@ -588,7 +609,8 @@ __device__ __forceinline__ void sym_stretch(const double* R, const double* F, do
 // Pm = w V (dF - dR[dF]) (+ muscle w_m V (dFm - s (dFm - (n.dFm) n)) m^T): the projection-derivative
 // term of A_N p, dR = R [om]x, om = Mi vee(R^T dF - dF^T R).
 __device__ __forceinline__ void an_stress(const double* R, const double* Mi, const double* dF, double wv,
-                                          const Stencil& st, bool mus, const double* nh, double sc, double* Pm) {
+                                          const Stencil& st, bool mus, const double* nh, double sc, double* Pm,
+                                          const double* mf) {
   double Wm[9];  // R^T dF
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -608,24 +630,24 @@ __device__ __forceinline__ void an_stress(const double* R, const double* Mi, con
   if (mus) {
     double dFm[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+    for (int i = 0; i < 3; ++i) dFm[i] = dF[3 * i] * mf[0] + dF[3 * i + 1] * mf[1] + dF[3 * i + 2] * mf[2];
     const double nd = nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2];
     const double wm = st.w_m * st.V;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       const double jd = sc * (dFm[i] - nd * nh[i]);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += wm * (dFm[i] - jd) * st.fiber[j];
+      for (int j = 0; j < 3; ++j) Pm[3 * i + j] += wm * (dFm[i] - jd) * mf[j];
     }
   }
 }
 
 // muscle data at F: n = Fm/||Fm||, sc = r/||Fm|| (0 if ||Fm|| = 0)
-__device__ __forceinline__ void muscle_dir(const double* F, const Stencil& st, double r_act, double* nh, double& sc) {
+__device__ __forceinline__ void muscle_dir(const double* F, const double* mf, double r_act, double* nh, double& sc) {
   double Fm[3], nr = 0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
+    Fm[i] = F[3 * i] * mf[0] + F[3 * i + 1] * mf[1] + F[3 * i + 2] * mf[2];
     nr += Fm[i] * Fm[i];
   }
   nr = sqrt(nr);
@@ -635,7 +657,7 @@ __device__ __forceinline__ void muscle_dir(const double* F, const Stencil& st, d
     sc = r_act / nr;
   } else {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) nh[i] = st.fiber[i];
+    for (int i = 0; i < 3; ++i) nh[i] = mf[i];
     sc = 0.0;
   }
 }
@@ -665,8 +687,9 @@ __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, 
 #pragma unroll
   for (int k = 0; k < 6; ++k) JC[(9 + k) * nq + tid] = Mi[k];
   if (st.w_m != 0.0) {
-    double nh[3], sc;
-    muscle_dir(F, st, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
+    double nh[3], sc, mf[3];
+    fiber_of(st, ea, e, mf);
+    muscle_dir(F, mf, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
 #pragma unroll
     for (int k = 0; k < 3; ++k) JC[(15 + k) * nq + tid] = nh[k];
     JC[18 * nq + tid] = sc;
@@ -694,13 +717,15 @@ __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict
 #pragma unroll
   for (int k = 0; k < 6; ++k) Mi[k] = __ldg(JC + (9 + k) * nq + t);
   const bool mus = st.w_m != 0.0;
+  double mf[3] = {0, 0, 0};
   if (mus) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) nh[k] = __ldg(JC + (15 + k) * nq + t);
     sc = __ldg(JC + 18 * nq + t);
+    fiber_of(st, ea, e, mf);
   }
   double Pm[9];
-  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
+  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm, mf);
   __shared__ __align__(16) double Psm[32][kPsSlot];
   store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
@@ -723,9 +748,13 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
   sym_stretch(R, F, S);
   rot_derivative_matrix(S, st.clamp, Mi);
   const bool mus = st.w_m != 0.0;
-  if (mus) muscle_dir(F, st, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
+  double mf[3] = {0, 0, 0};
+  if (mus) {
+    fiber_of(st, ea, e, mf);
+    muscle_dir(F, mf, ea.act ? ea.act[(int64_t)b * ea.act_bstride + e] : 0.0, nh, sc);
+  }
   double Pm[9];
-  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm);
+  an_stress(R, Mi, dF, ea.w_sim[b] * st.V, st, mus, nh, sc, Pm, mf);
   __shared__ __align__(16) double Psm[32][kPsSlot];
   store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
 }
@@ -754,17 +783,18 @@ __global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X
   for (int k = 0; k < 9; ++k) acc += dF[k] * (F[k] - R[k]);
   double dw = -st.V * acc, dr = 0;
   if (st.w_m != 0.0 && DR) {
-    double Fm[3], dFm[3], nr = 0;
+    double Fm[3], dFm[3], nr = 0, mf[3];
+    fiber_of(st, ea, e, mf);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      Fm[i] = F[3 * i] * st.fiber[0] + F[3 * i + 1] * st.fiber[1] + F[3 * i + 2] * st.fiber[2];
-      dFm[i] = dF[3 * i] * st.fiber[0] + dF[3 * i + 1] * st.fiber[1] + dF[3 * i + 2] * st.fiber[2];
+      Fm[i] = F[3 * i] * mf[0] + F[3 * i + 1] * mf[1] + F[3 * i + 2] * mf[2];
+      dFm[i] = dF[3 * i] * mf[0] + dF[3 * i + 1] * mf[1] + dF[3 * i + 2] * mf[2];
       nr += Fm[i] * Fm[i];
     }
     nr = sqrt(nr);
     double nh[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) nh[i] = nr > 0 ? Fm[i] / nr : st.fiber[i];
+    for (int i = 0; i < 3; ++i) nh[i] = nr > 0 ? Fm[i] / nr : mf[i];
     dr = st.w_m * st.V * (nh[0] * dFm[0] + nh[1] * dFm[1] + nh[2] * dFm[2]);
   }
   dw = qsum8(dw);

@@ -24,6 +24,7 @@ struct ElemArgs {
   const double* w_sim;     // [B] corotated weight per sim
   const double* act;       // actuation base for this step: act[b*act_bstride + e], or null
   int64_t act_bstride;
+  const double* fib;       // [m][3] per-element unit fiber directions, or null = Stencil::fiber
 };
 
 struct SweepDev {  // device copy of HostPlan::Sweep

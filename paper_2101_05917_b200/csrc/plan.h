@@ -36,6 +36,8 @@ struct HostPlan {
   double dN[8][8][3];               // dN[q][a][j] = dN_a/dX_j at Gauss point q
   double Kc[8][8];                  // sum_q V dN_a . dN_b            (corotated, unit w)
   double Km[8][8];                  // sum_q V (dN_a.m)(dN_b.m)       (muscle, unit w_m)
+  double Tm[8][8][3][3];            // sum_q V dN_a dN_b^T: per-element muscle blocks m_e^T Tm[a][b] m_e
+  std::vector<double> fib;          // [m][3] unit per-element fibers (empty = the uniform fiber); set before build_plan
   double w_ref = 0, w_m = 0;        // weights of the factorised A
   // node -> incident (element, corner) CSR sorted by element (deterministic gather)
   std::vector<int32_t> inc_ptr, inc_ec;  // ec = 8*e + a

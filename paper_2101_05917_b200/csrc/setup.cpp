@@ -75,6 +75,12 @@ static void stencil(HostPlan& P, const double fiber[3]) {
       }
       P.Kc[a][b] = kc;
       P.Km[a][b] = km;
+      for (int j = 0; j < 3; ++j)
+        for (int k = 0; k < 3; ++k) {
+          double t = 0;
+          for (int q = 0; q < 8; ++q) t += V * P.dN[q][a][j] * P.dN[q][b][k];
+          P.Tm[a][b][j][k] = t;
+        }
     }
 }
 
@@ -731,7 +737,14 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
         for (int b = 0; b < 8; ++b) {
           const int pb = P.pos_of_node[c[b]];
           if (pb < 0) continue;
-          rowsA[pa].push_back({pb, w_ref * P.Kc[a][b] + w_m * P.Km[a][b]});
+          double km = P.Km[a][b];
+          if (!P.fib.empty()) {  // this element's own fiber m_e: m_e^T Tm[a][b] m_e
+            const double* me = P.fib.data() + 3 * (int64_t)e;
+            km = 0;
+            for (int j = 0; j < 3; ++j)
+              for (int k = 0; k < 3; ++k) km += me[j] * P.Tm[a][b][j][k] * me[k];
+          }
+          rowsA[pa].push_back({pb, w_ref * P.Kc[a][b] + w_m * km});
         }
       }
     }

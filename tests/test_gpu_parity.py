@@ -55,7 +55,7 @@ def test_rotations_match_oracle_polar(torch):
             assert d[ok].max() < 1e-11, (scale, d[ok].max())
 
 
-@pytest.mark.parametrize("name", ["c1", "c3s", "c5s", "c2v", "c5v"])
+@pytest.mark.parametrize("name", ["c1", "c3s", "c5s", "c2v", "c5v", "c5f"])
 def test_objective_and_gradient(torch, name):
     from oracle import pd
     inp = make_inputs(get_config(name))
@@ -77,7 +77,7 @@ def test_objective_and_gradient(torch, name):
         assert rel(grad[b], ggo) <= 1e-12
 
 
-@pytest.mark.parametrize("name", ["c2s", "c3s", "c5s"])
+@pytest.mark.parametrize("name", ["c2s", "c3s", "c5s", "c5f"])
 def test_global_solve_matches_direct(torch, name):
     # The prefactorised global step A^{-1} against a direct sparse solve of A on free DoFs.
     import scipy.sparse.linalg as spla
@@ -101,7 +101,7 @@ def test_global_solve_matches_direct(torch, name):
         assert np.all(out[b][~fr] == 0.0)
 
 
-@pytest.mark.parametrize("name", ["c1", "c5s", "c2v", "c5v"])
+@pytest.mark.parametrize("name", ["c1", "c5s", "c2v", "c5v", "c5f"])
 def test_AN_product_matches_assembled_hessian(torch, name):
     # Matrix-free A_N p vs the oracle's assembled A_N = A - dA.
     from oracle import adjoint, pd
@@ -345,6 +345,12 @@ def test_tilted_plane_contact_parity(torch, accel_fwd, outer_warm):
     # general contact plane n . x = d (20-degree slope, offset 13 mm, config c4p): the plate lands and
     # slides; bit-exact active sets and outer counts, positions / velocities / gradients in world coordinates
     _contact_parity(torch, "c4p", accel_fwd, outer_warm, 0)
+
+
+def test_fiber_field_contact_muscle_parity(torch):
+    # per-element fiber directions (material.fiber_dir): the c5 recipe at oracle size with a seeded
+    # fiber field; forward, adjoint, dL/dr and bit-exact contact sets against the oracle
+    _contact_parity(torch, "c5f", 1, 1, 0)
 
 
 def test_contact_deterministic(torch):
