@@ -198,3 +198,24 @@ def test_fiber_field_energy_closed_form_and_A():
     inp_u = dict(inp, fiber_dir=np.tile([1.0, 0.0, 0.0], (sc.m, 1)))
     sc_u, sc_0 = pd.scene_from_inputs(inp_u), pd.scene_from_inputs(dict(inp, fiber_dir=None))
     assert abs(sc_u.objective(x, x, w, r)[0] - sc_0.objective(x, x, w, r)[0]) <= 1e-13 * abs(sc_0.objective(x, x, w, r)[0])
+
+
+def test_loss_gradients_vs_central_fd():
+    # the terminal loss gradients of every loss kind (c3's squared tip error included) against
+    # central differences of the loss value itself
+    from oracle import adjoint
+    from pd_inputs import get_config, make_inputs
+    rng = np.random.default_rng(11)
+    for name in ("c1", "c2s", "c3s"):
+        inp = make_inputs(get_config(name))
+        N = 3 * inp["n_nodes"]
+        q = inp["rest"].ravel() + 0.01 * rng.standard_normal(N)
+        v = 0.1 * rng.standard_normal(N)
+        L, gq, gv = adjoint.loss_and_grad(inp, 0, q, v)
+        for _ in range(3):
+            dq, dv = rng.standard_normal(N), rng.standard_normal(N)
+            eps = 1e-6
+            fd = (adjoint.loss_and_grad(inp, 0, q + eps * dq, v + eps * dv)[0]
+                  - adjoint.loss_and_grad(inp, 0, q - eps * dq, v - eps * dv)[0]) / (2 * eps)
+            assert abs(fd - (gq @ dq + gv @ dv)) <= 1e-7 * max(1.0, abs(fd)), (name, fd)
+        assert inp["cfg"].loss != "tip" or L > 0
