@@ -9,6 +9,8 @@ tail -n 3 gpurun_out/${T}_pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"; tail -n 1 gpurun_out/${T}_smoke.log
 timeout 1500 python bench.py --steps 2 --warmup 3 > gpurun_out/${T}_bench_c5.json 2> gpurun_out/${T}_bench_c5.err; echo "bench c5 rc=$?"
 timeout 900 python bench.py --config c3 --steps 2 --warmup 3 > gpurun_out/${T}_bench_c3.json 2> gpurun_out/${T}_bench_c3.err; echo "bench c3 rc=$?"
+# the on-box Newton-PCG comparison system on the headline workload
+timeout 1500 python bench.py --solver newton --steps 1 --warmup 3 --no-e2e --cpu-sample-steps 0 > gpurun_out/${T}_bench_c5_newton.json 2> gpurun_out/${T}_bench_c5_newton.err; echo "bench c5 newton rc=$?"
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 CMD5="python bench.py --config c5 --horizon 1 --steps 1 --warmup 3 --no-e2e --cpu-sample-steps 0"
 timeout 600 $CMD5 > gpurun_out/${T}_plain_c5.log 2>&1 && \

@@ -45,7 +45,7 @@ def main():
             res["solve_K3_dram_bytes"] = sum(by(m) for m in L[start:end + 1])
             res["solve_K3_launches"] = end - start + 1
     for fam, kn in (("local_K1", "k_elem_residual"), ("AN_K4", "k_elem_AN_cached")):
-        v = [by(m) for m in L if kn + "(" in m["name"] or m["name"].endswith(kn)]
+        v = [by(m) for m in L if kn + "(" in m["name"] or kn + "<" in m["name"] or m["name"].endswith(kn)]
         if v:
             res[fam + "_dram_bytes"] = sum(v) / len(v)
     res["source"] = os.path.basename(path)
