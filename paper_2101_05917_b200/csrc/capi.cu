@@ -370,7 +370,7 @@ void solve_v4(pd_sim* s, int B) {
   static const int exp_mode = std::getenv("PD_K3_EXP") ? std::atoi(std::getenv("PD_K3_EXP")) : 0;
   auto level = [&](const HostPlan::Sweep4& S, const Sweep4Dev& d, bool fwd, int j) {
     const int w0 = S.lvl_warp[j], nw = S.lvl_warp[j + 1] - w0 - 1;
-    if (exp_mode != 2) {
+    if (exp_mode != 2 && S.lvl_g[j + 1] > S.lvl_g[j]) {  // (the forward sweep's merged root level is empty)
     cudaLaunchConfig_t c = cfg_of(dim3((unsigned)((nw + kWarpsK3 - 1) / kWarpsK3), gy), dim3(32 * kWarpsK3), smem);
     CK(cudaLaunchKernelEx(&c, fn, d, w0, nw, R, (const double*)(fwd ? s->S0 : s->S2), (const double*)s->S0,
                           fwd ? s->S2 : s->S0, s->Spart));

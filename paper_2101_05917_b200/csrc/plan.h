@@ -96,6 +96,12 @@ struct HostPlan {
   // 32-row partial slot that the level's reduce adds, in piece order, into its target rows (deterministic).
   int k3_version = 3;                  // 3: chain/item schedule (fw, bw above); 4: warp-range schedule (fw4, bw4)
   int k3_warps = 148 * 8;              // warps a v4 level launch is split for
+  // v4: the root's two dependent triangular products (forward y = D z, backward x = D^T y) replaced by ONE dense
+  // product x_root = S^{-1} z_root, S^{-1} = D_root^T D_root (the inverse Schur complement onto the root, same
+  // bytes as the two triangles): the forward sweep has no root level and the backward sweep's first level reads
+  // z_root from the x buffer (the two share it) and assigns x_root through its reduce
+  bool merge_root = true;
+  std::vector<double> Sinv;          // [ns_root][ns_root] row-major, when merge_root
   struct Sweep4 {
     std::vector<double> A;             // k-groups (128 doubles each) of all levels, level-major, tile-major
     std::vector<int32_t> lvl_g;        // [nlevels+1] first global k-group of each level

@@ -438,8 +438,26 @@ static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32
   auto Wval = [&](int s, int i, int k) -> double { return P.P[P.poff[s] + (int64_t)i * P.ssize[s] + k]; };
   struct Tile {
     int s, a0, nk, nv, out, mode;  // a0: D row / W row / column start; out >= 0 direct row, -1 always partial
-    int kind;                      // 0 forward D, 1 forward W, 2 backward column tile
+    int kind;                      // 0 forward D, 1 forward W, 2 backward column tile, 3 merged-root S^{-1} rows
   };
+  const int root_lev = P.nlevels - 1;
+  const bool merge = P.merge_root && (int)byh[root_lev].size() == 1;
+  const int root = merge ? byh[root_lev][0] : -1;
+  if (merge) {  // S^{-1} = D^T D over the root block (D = L_rr^{-1}, packed lower)
+    const int ns = P.ssize[root];
+    const double* D = P.D.data() + P.doff[root];
+    P.Sinv.assign((size_t)ns * ns, 0.0);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int i = 0; i < ns; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double acc = 0;
+        for (int k = i; k < ns; ++k) acc += D[(int64_t)k * (k + 1) / 2 + i] * D[(int64_t)k * (k + 1) / 2 + j];
+        P.Sinv[(size_t)i * ns + j] = P.Sinv[(size_t)j * ns + i] = acc;
+      }
+  } else {
+    P.merge_root = false;
+    P.Sinv.clear();
+  }
   for (int fwd = 1; fwd >= 0; --fwd) {
     HostPlan::Sweep4& S = fwd ? P.fw4 : P.bw4;
     S = HostPlan::Sweep4();
@@ -453,6 +471,11 @@ static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32
       std::vector<Tile> tiles;
       for (int s : byh[lev]) {
         const int ns = P.ssize[s], f = P.sfirst[s], nr = (int)(P.rptr[s + 1] - P.rptr[s]);
+        if (s == root) {  // merged root: nothing in the forward sweep; backward rows of S^{-1}, all partial
+          if (!fwd)
+            for (int i0 = 0; i0 < ns; i0 += L) tiles.push_back({s, i0, ns, std::min(L, ns - i0), -1, 0, 3});
+          continue;
+        }
         if (fwd) {
           for (int i0 = 0; i0 < ns; i0 += L) tiles.push_back({s, i0, std::min(i0 + L, ns), std::min(L, ns - i0), f + i0, 0, 0});
           for (int i0 = 0; i0 < nr; i0 += L) tiles.push_back({s, i0, ns, std::min(L, nr - i0), -1, 1, 1});
@@ -473,6 +496,7 @@ static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32
           int32_t row = -1;
           if (k < T.nk) {
             if (T.kind == 0 || T.kind == 1) row = f + k;
+            else if (T.kind == 3) row = -2 - (f + k);  // z_root, read from the x buffer (source B)
             else row = k < ns - T.a0 ? f + T.a0 + k : -2 - P.rows[P.rptr[s] + (k - (ns - T.a0))];
           }
           S.krow.push_back(row);
@@ -482,6 +506,7 @@ static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32
             double v;
             if (T.kind == 0) v = Dval(s, T.a0 + l, k);
             else if (T.kind == 1) v = Wval(s, T.a0 + l, k);
+            else if (T.kind == 3) v = P.Sinv[(size_t)(T.a0 + l) * ns + k];
             else v = k < ns - T.a0 ? Dval(s, T.a0 + k, T.a0 + l) : -Wval(s, k - (ns - T.a0), T.a0 + l);
             blk[sweep_frag_pos(k & 3, l)] = v;
           }
@@ -516,7 +541,9 @@ static void build_warp_schedule(HostPlan& P, const std::vector<std::vector<int32
           } else {
             S.pout.push_back((int32_t)(-1 - slot));
             for (int l = 0; l < T.nv; ++l) {
-              const int32_t row = T.kind == 1 ? P.rows[P.rptr[T.s] + T.a0 + l] : T.out + l;
+              const int32_t row = T.kind == 1   ? P.rows[P.rptr[T.s] + T.a0 + l]
+                                  : T.kind == 3 ? P.sfirst[T.s] + T.a0 + l
+                                                : T.out + l;
               targets[{T.mode, row}].push_back((int32_t)(slot * L + l));
             }
             ++slot;
@@ -898,6 +925,7 @@ std::string build_plan(HostPlan& P, int n, int m, const double* rest, const int3
 
   // ---------------- solve schedule (K3 v3)
   P.nlevels = H + 1;
+  if (const char* e = std::getenv("PD_K3_MERGE_ROOT")) P.merge_root = std::atoi(e) != 0;
   if (P.k3_version == 4) build_warp_schedule(P, byh);
   else build_solve_schedule(P, byh);
   return "";

@@ -177,11 +177,18 @@ int main(int argc, char** argv) {
         }
       }
     }
+    // (with the merged root the forward sweep leaves the root rows of y unwritten: the backward sweep's first
+    // level computes x_root = S^{-1} z_root directly)
+    const int rf = P.merge_root ? P.sfirst[P.nsup - 1] : N;
     for (int p = 0; p < N; ++p)
-      if (assigned[p] != 1) { printf("row %d written %d times\n", p, assigned[p]); exit(11); }
+      if (assigned[p] != 1 && !(fwd && p >= rf && assigned[p] == 0)) {
+        printf("row %d written %d times\n", p, assigned[p]);
+        exit(11);
+      }
   };
   if (P.k3_version == 4) {
     run4(P.fw4, z, y, &z, true);
+    x = z;  // the device's z and x share one buffer: the merged root level reads z_root from it
     run4(P.bw4, y, x, nullptr, false);
     double err = 0, mx = 0;
     for (int p = 0; p < N; ++p) { err = std::max(err, std::fabs(x[p] - v[p])); mx = std::max(mx, std::fabs(v[p])); }
