@@ -400,11 +400,21 @@ def test_per_step_loss_time_varying_fext_parity(torch, name):
 
 
 # ----------------------------------------------------------------- sticky contact (the paper's model, 8f.1)
-@pytest.mark.parametrize("name", ["c4s", "c5s"])
+@pytest.mark.parametrize("name", ["c4s", "c5s", "c4p"])
 def test_sticky_contact_parity(torch, name):
     # infinite friction: active candidates hold all three DoFs at x_i; constrained solve of all 3 columns,
-    # adjoint with the pinned-value term
+    # adjoint with the pinned-value term (c4p: on the tilted plane, where the predictor's phi is n . x - d)
     _contact_parity(torch, name, 1, 1, contact_mode="sticky")
+
+
+def test_tilted_plane_newton_pcg_parity(torch):
+    # the Newton-PCG forward through the plane coordinates
+    _contact_parity(torch, "c4p", 2, 1, 0)
+
+
+def test_fiber_field_volume_parity(torch):
+    # per-element fibers with the volume-preserving term (all three energies of the c5 family at once)
+    _contact_parity(torch, "c5f", 1, 1, 0, volume=True, tol_fwd=5e-14)
 
 
 # ----------------------------------------------------------------- volume-preserving energy (8f.2)
