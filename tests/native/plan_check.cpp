@@ -162,6 +162,9 @@ int main(int argc, char** argv) {
         int np = S.lvl_piece[lev + 1] - S.lvl_piece[lev], nd = 0;
         for (int q = S.lvl_piece[lev]; q < S.lvl_piece[lev + 1]; ++q) nd += S.pout[q] >= 0;
         long long srcs = S.red_ptr[S.lvl_red[lev + 1]] - S.red_ptr[S.lvl_red[lev]];
+        int single = 0;
+        for (int r = S.lvl_red[lev]; r < S.lvl_red[lev + 1]; ++r) single += S.red_ptr[r + 1] - S.red_ptr[r] == 1;
+        printf("  single-source %6d ", single);
         printf("%s level %2d: kgroups %7d (%6.2f MB) warps %5d pieces %6d direct %6d reduce targets %7d sources %8lld\n",
                fwd ? "fw" : "bw", lev, S.lvl_g[lev + 1] - S.lvl_g[lev], (S.lvl_g[lev + 1] - S.lvl_g[lev]) * 1024.0 / 1e6, W,
                np, nd, S.lvl_red[lev + 1] - S.lvl_red[lev], srcs);
