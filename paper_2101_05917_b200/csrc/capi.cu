@@ -908,6 +908,10 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     if (s->opt.max_outer < 1) s->opt.max_outer = 10;
     if (!(s->opt.eps_phi > 0)) s->opt.eps_phi = 1e-6 * mesh->dx;
     if (s->opt.contact_mode == 0) s->opt.contact_mode = 1;
+    if (s->opt.accel_fwd < 0 || s->opt.accel_fwd > 2)
+      return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "accel_fwd must be 0 (plain PD), 1 (L-BFGS) or 2 (Newton-PCG)");
+    if (s->opt.accel_adj < 0 || s->opt.accel_adj > 1)
+      return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "accel_adj must be 0 (fixed point) or 1 (PCG)");
     if (s->opt.contact_mode != 1 && s->opt.contact_mode != 2)
       return fail(nullptr, PD_ERR_INVALID_ARGUMENT, "contact_mode must be 1 (frictionless) or 2 (sticky)");
     s->sticky = s->opt.contact_mode == 2 ? 1 : 0;

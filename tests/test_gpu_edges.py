@@ -45,6 +45,20 @@ def test_state_and_argument_errors(torch):
         pdb.simulator_from_inputs(inp, contact_nodes=inp["fixed_dofs"][::3] // 3)
     with pytest.raises(pdb.PDError):               # repeated candidate
         pdb.simulator_from_inputs(inp, contact_nodes=np.array([5, 5], np.int32))
+    with pytest.raises(pdb.PDError) as e:          # unknown forward route
+        pdb.simulator_from_inputs(inp, accel_fwd=3)
+    assert e.value.status == _lib.PD_ERR_INVALID_ARGUMENT
+    with pytest.raises(pdb.PDError) as e:          # non-finite contact plane
+        pdb.simulator_from_inputs(inp, contact_nodes=np.array([5], np.int32), plane_n=(0.0, float("nan"), 1.0))
+    assert e.value.status == _lib.PD_ERR_INVALID_ARGUMENT
+    inp5 = make_inputs(get_config("c5f", counts=(2, 2, 1), contact=False))
+    bad = inp5["fiber_dir"].copy()
+    bad[1] = 0.0
+    with pytest.raises(pdb.PDError) as e:          # a zero fiber direction
+        pdb.simulator_from_inputs(dict(inp5, fiber_dir=bad))
+    assert e.value.status == _lib.PD_ERR_INVALID_ARGUMENT
+    with pytest.raises(ValueError):                # fiber field of the wrong shape (binding check)
+        pdb.simulator_from_inputs(dict(inp5, fiber_dir=bad[:-1]))
 
 
 def test_partial_batch_and_single_step(torch):

@@ -232,3 +232,14 @@ def test_c4_full_horizon_vs_oracle_golden(torch):
     # the implementation.  Velocities are therefore compared relative to max(||v_i||, 1% of the trajectory's
     # peak ||v||); positions and gradients keep the plain bars.
     _check_golden(inp, gpu, gd, 0, sim.contact_sets(), vel_rel_floor=0.01 * float(gd["s0_vnorm"].max()))
+
+
+def test_c2_full_horizon_vs_oracle_golden(torch):
+    # configs[1] over its whole horizon (16x8x8 cantilever, 4131 DoF, 100 steps, v0 ~ N(0, 0.1 m/s)): states every
+    # 10 steps and the gradients of the terminal loss against the oracle (tools/make_goldens.py c2)
+    gd = _golden("c2")
+    T = int(gd["steps"])
+    inp = make_inputs(get_config("c2"), steps=T)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    _check_golden(inp, gpu, gd, 0)

@@ -6,6 +6,7 @@ method's arithmetic) — nothing here imports or runs the CUDA path.  Rerun with
     python tools/make_goldens.py c5      # config c5, sim 0, first 2 steps (newton_pcg / pcg routes)
     python tools/make_goldens.py c3      # config c3, stiffest + softest sim, first 30 steps
     python tools/make_goldens.py c4      # config c4, the whole 150-step contact drop
+    python tools/make_goldens.py c2      # config c2, the whole 100-step cantilever (4131 DoF)
 
 What is stored per sim: the states of every `every`-th step and of the last step (q, v), the Alg. 1 active
 sets of every step, the per-step oracle statistics, and the gradients of the config's loss at the last
@@ -32,6 +33,7 @@ SPECS = {
     "c5": ("c5", 2, [0], 1e-13, "newton_pcg", "pcg", 1),
     "c3": ("c3", 30, None, 1e-13, "newton", "direct", 5),
     "c4": ("c4", 150, [0], 2e-14, "newton", "direct", 10),
+    "c2": ("c2", 100, [0], 1e-13, "newton", "direct", 10),
 }
 
 
