@@ -192,6 +192,13 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- ours
+# K1 operation count per quadrature point (an n-term dot product = n mul + (n-1) add): F = G_q x_e 135,
+# det F 14, ||F||^2 17, 1/||F|| (rsqrt + 2 Newton steps) 12, the fallback test and X0 = c F 13, F - R / energy /
+# stress 39, G_q^T P (24-term sums, 3 components) 141, energy butterfly 3 -> 374; muscle (Fm, ||Fm||, projection,
+# energy, stress) 76; per Newton-Schulz iteration (X^T X 30, residual 15, Y 9, X Y 45) 99
+K1_BASE_FLOPS, K1_MUSCLE_FLOPS, K1_NS_ITER_FLOPS = 374, 76, 99
+
+
 def main_ours(args):
     import torch
     import paper_2101_05917_b200 as pdb
@@ -281,6 +288,13 @@ def main_ours(args):
     units = inp_all["B"] * T * N           # the whole batch (every rank's sims)
     value = units / (ms_per_step / 1e3)
 
+    # ---------------- K1's executed operation count on this workload (outside the timed region): the local step's
+    # Newton-Schulz polar takes a data-dependent number of iterations; its mean over every quadrature point of the
+    # trajectory's final states turns the per-point operation count of DESIGN.md §5 into K1's algorithmic flops
+    k1_stats = sim.polar_stats(qt[:, T, :].contiguous())
+    ns_mean = k1_stats["ns_iters"] / max(1, k1_stats["ns_points"])
+    k1_flops_qp = K1_BASE_FLOPS + (K1_MUSCLE_FLOPS if act is not None else 0) + K1_NS_ITER_FLOPS * ns_mean
+
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -347,14 +361,20 @@ def main_ours(args):
                         peak_source="MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650")
         # element kernels: fp64 flops per quadrature point (DESIGN.md §5 operation count; ncu-measured when
         # profiles/ncu_traffic.json has it)
-        per_qp = ncu.get(fam + "_flops_per_qp", {"local_K1": 950, "AN_K4": 420, "param": 700}.get(fam))
+        per_qp = {"local_K1": k1_flops_qp, "AN_K4": 420, "param": 700}.get(fam)
         if per_qp is None:
             return None
         flops = per_qp * 8 * inp["n_elems"] * B
         ach = flops / avg_s / 1e12
-        return dict(bound="alu", achieved=ach, peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=ach / FP64_PEAK_TFLOPS,
-                    traffic=ncu.get(fam + "_dram_bytes"), kernel=fam, flops_per_qp=per_qp, avg_launch_ms=avg_s * 1e3,
-                    peak_source="derived fp64 pipe peak: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §5)")
+        r = dict(bound="alu", achieved=ach, peak=FP64_PEAK_TFLOPS, unit="TFLOP/s", frac=ach / FP64_PEAK_TFLOPS,
+                 traffic=ncu.get(fam + "_dram_bytes"), kernel=fam, flops_per_qp=per_qp, avg_launch_ms=avg_s * 1e3,
+                 peak_source="derived fp64 pipe peak: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md §5)")
+        if fam == "local_K1":
+            r.update(flop_model=f"{K1_BASE_FLOPS} + {K1_MUSCLE_FLOPS if act is not None else 0} (muscle) + "
+                                f"{K1_NS_ITER_FLOPS} x {ns_mean:.3f} Newton-Schulz iterations (measured mean over "
+                                f"{k1_stats['ns_points']} quadrature points of the final states; "
+                                f"{k1_stats['fallback_points']} fallback points counted at 0)")
+        return r
 
     fam = max(prof, key=lambda k: prof[k][0])
     roof = roof_of(fam) or roof_of("solve_K3")

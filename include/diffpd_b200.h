@@ -194,6 +194,11 @@ pd_status pd_apply_AN(pd_sim* sim, int32_t B, const double* x, const double* you
                       const double* act, const double* p, double* out, void* cuda_stream);
 /* R[B][n_elems][8][9] = rotation R(F) of every quadrature point of x (local step projection). */
 pd_status pd_project_rotations(pd_sim* sim, int32_t B, const double* x, double* R, void* cuda_stream);
+/* Local-step statistics of x (device [B][3n]): out (HOST int64[3]) = {Newton-Schulz iterations summed over every
+ * quadrature point K1's polar takes on x, quadrature points on that path, points that take the SVD / scaled-Newton
+ * fallback}.  bench.py turns the mean iteration count into K1's algorithmic flops per quadrature point
+ * (DESIGN.md §5).  Diagnostic: not on the hot path. */
+pd_status pd_polar_stats(pd_sim* sim, int32_t B, const double* x, int64_t* out, void* cuda_stream);
 
 /* Integer facts about the handle: out[0..n) = {n_nodes, n_free_nodes, n_supernodes,
  * n_levels, nnz(L_s) (stored entries of the scalar factor), n_contact,

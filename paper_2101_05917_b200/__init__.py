@@ -213,6 +213,13 @@ class Simulator:
                                          _ptr(act, (B, m), "act", dev), _ptr(p, (B, N), "p", dev),
                                          _ptr(out, (B, N), "out", dev), _stream()))
 
+    def polar_stats(self, x):
+        """{'ns_iters': total Newton-Schulz iterations, 'ns_points', 'fallback_points'} of K1's polar on x [B][3n]."""
+        B, N, m, dev = self._diag_B(x)
+        out = (C.c_int64 * 3)()
+        self._check(self.lib.pd_polar_stats(self.handle, B, _ptr(x, (B, N), "x", dev), out, _stream()))
+        return dict(ns_iters=int(out[0]), ns_points=int(out[1]), fallback_points=int(out[2]))
+
     def project_rotations(self, x, R):
         B, N, m, dev = self._diag_B(x)
         self._check(self.lib.pd_project_rotations(self.handle, B, _ptr(x, (B, N), "x", dev),

@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "PD_OK", 1: "PD_ERR_INVALID_ARGUMENT", 2: "PD_ERR_NUMERICAL",
 
 # every symbol include/diffpd_b200.h declares
 EXPORTS = ["pd_create", "pd_forward", "pd_backward", "pd_backward_steps", "pd_eval_objective", "pd_apply_Ainv", "pd_apply_AN",
-           "pd_project_rotations", "pd_info", "pd_profile", "pd_contact_sets", "pd_last_error",
+           "pd_project_rotations", "pd_polar_stats", "pd_info", "pd_profile", "pd_contact_sets", "pd_last_error",
            "pd_destroy"]
 
 dp = C.POINTER(C.c_double)
@@ -74,6 +74,7 @@ def load():
     lib.pd_apply_Ainv.argtypes = [vp, C.c_int32, vp, vp, vp]
     lib.pd_apply_AN.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
     lib.pd_project_rotations.argtypes = [vp, C.c_int32, vp, vp, vp]
+    lib.pd_polar_stats.argtypes = [vp, C.c_int32, vp, C.POINTER(C.c_int64), vp]
     lib.pd_info.argtypes = [vp, C.POINTER(C.c_int64), C.c_int32]
     lib.pd_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]
     lib.pd_contact_sets.argtypes = [vp, C.POINTER(C.c_uint8)]

@@ -57,6 +57,7 @@ struct pd_sim {
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
+  int64_t* nactive_ll = nullptr;  // 3 x 64-bit device counters (pd_polar_stats)
   // general contact plane n . x = d: plane coordinates x' = Q x - d e_z inside the library
   bool frame = false;
   FrameQ fq{};
@@ -1017,6 +1018,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       max_prows = std::max(P.fw.max_partial_rows, P.bw.max_partial_rows);
     }
     s->Spart = s->alloc<double>((max_prows + 32) * 3 * s->Bmax);
+    s->nactive_ll = s->alloc<int64_t>(4);
     const int64_t n3B = 3LL * P.n * s->Bmax;
     const int64_t sB = 3LL * P.nfree * s->Bmax;
     double** st_vecs[] = {&s->X, &s->V, &s->Y, &s->Xp, &s->Fext, &s->G, &s->W, &s->U, &s->Rv, &s->Z,
@@ -1623,6 +1625,30 @@ pd_status pd_project_rotations(pd_sim* s, int32_t B, const double* x, double* R,
     k_elem_rotations<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(s->X, s->st, s->d_hex8, P.m, B, R);
     LAUNCH_CHECK(s);
     CK(cudaStreamSynchronize(s->stream));
+  } catch (CudaError& e) {
+    return fail(s, PD_ERR_CUDA, e.what());
+  }
+  return PD_OK;
+}
+
+pd_status pd_polar_stats(pd_sim* s, int32_t B, const double* x, int64_t* out, void* cuda_stream) {
+  if (!s) return PD_ERR_INVALID_ARGUMENT;
+  if (B < 1 || B > s->Bmax || !x || !out) return fail(s, PD_ERR_INVALID_ARGUMENT, "bad arguments");
+  s->stream = (cudaStream_t)cuda_stream;
+  const HostPlan& P = s->plan;
+  const int n3 = 3 * P.n;
+  const int64_t len = (int64_t)n3 * B;
+  try {
+    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    LAUNCH_CHECK(s);
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(s->nactive_ll);
+    CK(cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s->stream));
+    k_polar_stats<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->st, s->d_hex8, P.m, B, acc);
+    LAUNCH_CHECK(s);
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    for (int k = 0; k < 3; ++k) out[k] = (int64_t)h[k];
   } catch (CudaError& e) {
     return fail(s, PD_ERR_CUDA, e.what());
   }

@@ -213,7 +213,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // K1's polar without address-taken arrays on the common path: Newton-Schulz inline (as polar_rotation);
 // returns false when F needs the SVD or scaled-Newton fallback (det F <= 1e-6 ||F||^3, or no convergence in 14
 // iterations).  F and R stay in registers: no call frame, no local memory on the common path.
-__device__ __forceinline__ bool polar_ns(const double (&F)[9], double (&R)[9]) {
+__device__ __forceinline__ bool polar_ns(const double (&F)[9], double (&R)[9], int* its = nullptr) {
   const double d0 = det3(F);
   double fn2 = 0;
 #pragma unroll
@@ -242,7 +242,10 @@ __device__ __forceinline__ bool polar_ns(const double (&F)[9], double (&R)[9]) {
       R[3 * i + 1] = a0 * y01 + a1 * y11 + a2 * y12;
       R[3 * i + 2] = a0 * y02 + a1 * y12 + a2 * y22;
     }
-    if (d < 1e-16) return true;
+    if (d < 1e-16) {
+      if (its) *its = it + 1;  // (statistics hook only; K1 passes nothing and the count is compiled out)
+      return true;
+    }
   }
   return false;
 }
@@ -516,6 +519,41 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const doub
   store_force(Pm, dnt, e, b, q, B, Psm[threadIdx.x >> 3], live ? EF : nullptr);
   energy = qsum8(energy);
   if (live && EE && q == 0) EE[(int64_t)e * B + b] = energy;
+}
+
+// Local-step statistics (diagnostic, pd_polar_stats): per quadrature point of x, the Newton-Schulz iterations K1's
+// polar takes (or the fallback); acc[0] += iterations, acc[1] += points on the Newton-Schulz path, acc[2] +=
+// fallback points.  Integer sums: exact and order-independent.
+__global__ void k_polar_stats(const double* __restrict__ X, Stencil st, const int32_t* __restrict__ hex8, int m, int B,
+                              unsigned long long* __restrict__ acc) {
+  __shared__ DNTab dnt;
+  dn_fill(dnt, st);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t pair = tid >> 3;
+  const int q = (int)(tid & 7);
+  unsigned long long it_sum = 0, ns = 0, fb = 0;
+  if (pair < (int64_t)m * B) {
+    const int e = (int)(pair / B), b = (int)(pair - (int64_t)e * B);
+    double F[9], R[9];
+    load_F(X, hex8, dnt, e, b, q, B, F);
+    int its = 0;
+    if (polar_ns(F, R, &its)) {
+      it_sum = (unsigned long long)its;
+      ns = 1;
+    } else {
+      fb = 1;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    it_sum += __shfl_down_sync(0xffffffffu, it_sum, o);
+    ns += __shfl_down_sync(0xffffffffu, ns, o);
+    fb += __shfl_down_sync(0xffffffffu, fb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, it_sum);
+    atomicAdd(acc + 1, ns);
+    atomicAdd(acc + 2, fb);
+  }
 }
 
 // Rotations of every quad point (diagnostic / parity hook).

@@ -130,3 +130,19 @@ def test_inverted_elements_project_to_rotations(torch):
     R = R.cpu().numpy().reshape(-1, 3, 3)
     assert np.allclose(np.einsum("nij,nkj->nik", R, R), np.eye(3), atol=1e-12)
     assert np.allclose(np.linalg.det(R), 1.0, atol=1e-12)
+
+
+def test_polar_stats_hook(torch):
+    # pd_polar_stats (the K1 operation count of bench.py): at rest F = I, so every quadrature point takes exactly one
+    # Newton-Schulz step (X0 = I is orthogonal); an inverted element takes the fallback path
+    import paper_2101_05917_b200 as pdb
+    inp = make_inputs(get_config("c1"))
+    sim = pdb.simulator_from_inputs(inp)
+    x = inp["rest"].ravel()[None].copy()
+    st = sim.polar_stats(to_dev(x))
+    assert st == dict(ns_iters=8 * inp["n_elems"], ns_points=8 * inp["n_elems"], fallback_points=0)
+    x2 = x.copy().reshape(-1, 3)
+    e0 = inp["hex8"][0]
+    x2[e0[4:], 2] = x2[e0[:4], 2] - 0.01      # the element's top face below its bottom face: det F < 0
+    st2 = sim.polar_stats(to_dev(x2.reshape(1, -1)))
+    assert st2["fallback_points"] > 0 and st2["ns_points"] + st2["fallback_points"] == 8 * inp["n_elems"]
