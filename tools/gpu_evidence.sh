@@ -20,5 +20,7 @@ CMD3="python bench.py --config c3 --horizon 1 --steps 1 --warmup 3 --no-e2e --cp
 timeout 300 $CMD3 > gpurun_out/${T}_plain_c3.log 2>&1 && \
 timeout 900 ncu --metrics $M --clock-control none -c 6000 --csv --log-file gpurun_out/${T}_launches_c3_h1.csv $CMD3 > gpurun_out/${T}_ncu_c3.log 2>&1
 echo "c3 launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sweep_warp|k_sweep_reduce4|k_elem_residual" -s 300 -c 6 -o gpurun_out/${T}_full_c5 $CMD5 > gpurun_out/${T}_ncu_full.log 2>&1
-echo "c5 full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sweep_warp|k_sweep_reduce4" -s 300 -c 6 -o gpurun_out/${T}_full_c5 $CMD5 > gpurun_out/${T}_ncu_full.log 2>&1
+echo "c5 full (K3) rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_elem_residual|k_elem_AN_cached|k_gather" -s 4 -c 3 -o gpurun_out/${T}_full_c5_elem $CMD5 > gpurun_out/${T}_ncu_full_elem.log 2>&1
+echo "c5 full (K1/K4/K2) rc=$?"
