@@ -53,6 +53,7 @@ struct pd_sim {
   SweepDev swf{}, swb{};
   Sweep4Dev sw4f{}, sw4b{};  // K3 v4 (warp ranges), when plan.k3_version == 4
   int k3_mma = 1;   // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
+  int nsm = 148;     // SMs of the device
   int k3_nbuf = 2;  // K3 item ring depth (2..4, env PD_K3_NBUF)
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
@@ -369,18 +370,25 @@ void solve_v4(pd_sim* s, int B) {
   // direct x (S0), reduce x (S0) =
   // timing experiments only (wrong results): PD_K3_EXP=1 skips the reduces, 2 skips the level kernels
   static const int exp_mode = std::getenv("PD_K3_EXP") ? std::atoi(std::getenv("PD_K3_EXP")) : 0;
+  // The level's nw warp ranges are fixed by the plan (independent of B, so a sim's result does not depend on the
+  // batch it runs in); with gy column chunks a physical warp streams vpw consecutive ranges (one
+  // contiguous span of the stream, same pieces and partial slots, bitwise the same result) so that the launch's
+  // gy x ceil(nw / vpw / kWarpsK3) CTAs fit one wave (c3, gy = 8: A^-1 119 -> 108 us measured)
+  const int wcap = std::max(1, s->nsm / (int)gy) * kWarpsK3;
   auto level = [&](const HostPlan::Sweep4& S, const Sweep4Dev& d, bool fwd, int j) {
     const int w0 = S.lvl_warp[j], nw = S.lvl_warp[j + 1] - w0 - 1;
     if (exp_mode != 2 && S.lvl_g[j + 1] > S.lvl_g[j]) {  // (the forward sweep's merged root level is empty)
-    cudaLaunchConfig_t c = cfg_of(dim3((unsigned)((nw + kWarpsK3 - 1) / kWarpsK3), gy), dim3(32 * kWarpsK3), smem);
-    CK(cudaLaunchKernelEx(&c, fn, d, w0, nw, R, (const double*)(fwd ? s->S0 : s->S2), (const double*)s->S0,
+    const int vpw = (nw + wcap - 1) / wcap, nphys = (nw + vpw - 1) / vpw;
+    cudaLaunchConfig_t c = cfg_of(dim3((unsigned)((nphys + kWarpsK3 - 1) / kWarpsK3), gy), dim3(32 * kWarpsK3), smem);
+    CK(cudaLaunchKernelEx(&c, fn, d, w0, nw, vpw, R, (const double*)(fwd ? s->S0 : s->S2), (const double*)s->S0,
                           fwd ? s->S2 : s->S0, s->Spart));
     LAUNCH_CHECK(s);
     }
     const int r0 = S.lvl_red[j], nr = S.lvl_red[j + 1] - r0;
     if (nr > 0 && exp_mode != 1) {
       cudaLaunchConfig_t c2 = cfg_of(dim3(nblk((int64_t)nr * R)), dim3(256), 0);
-      CK(cudaLaunchKernelEx(&c2, k_sweep_reduce4, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0, s->S0));
+      CK(cudaLaunchKernelEx(&c2, k_sweep_reduce4<8>, d, r0, nr, R, (const double*)s->Spart, fwd ? s->S2 : s->S0,
+                            s->S0));
       LAUNCH_CHECK(s);
     }
   };
@@ -946,7 +954,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       if (const char* ev = std::getenv("PD_K3_V")) s->plan.k3_version = std::atoi(ev) == 3 ? 3 : 4;
       int dev = 0, nsm = 148;
       if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      s->plan.k3_warps = std::max(1, nsm) * kWarpsK3;
+      s->nsm = std::max(1, nsm);
+      s->plan.k3_warps = s->nsm * kWarpsK3;
     }
     std::string e = build_plan(s->plan, mesh->n_nodes, mesh->n_elems, mesh->rest_xyz, mesh->hex8, mesh->dx,
                                mat->density, h, fixed_dofs, n_fixed, w_ref, mat->muscle_w, fiber, opts->contact_nodes,
@@ -1059,7 +1068,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     CK(cudaMallocHost(&s->h_nactive, 3 * sizeof(int32_t)));
     CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
     if (s->opt.accel_fwd) {
-      s->nhist = 8;  // L-BFGS memory (env PD_LBFGS_M, 1..16)
+      s->nhist = 4;  // L-BFGS memory (env PD_LBFGS_M, 1..16; 4 measured fastest)
       if (const char* e = std::getenv("PD_LBFGS_M")) s->nhist = std::min(16, std::max(1, std::atoi(e)));
       s->LS = s->alloc<double>(s->nhist * n3B);
       s->LY = s->alloc<double>(s->nhist * n3B);

@@ -1515,7 +1515,8 @@ __global__ void k_sweep_reduce(SweepDev sw, int r0, int ntarget, int R, const do
 }
 
 // ----------------------------------------------------------------- K3 v4: warp ranges
-// One launch per level and sweep.  Warp w of the level streams the contiguous k-group range [wg[w], wg[w+1]) of
+// One launch per level and sweep.  Warp w of the level streams the contiguous k-group range [wg[w], wg[w+1]) (or,
+// with vpw > 1 when several column chunks share the SMs, the vpw consecutive ranges [wg[w], wg[w+vpw])) of
 // the factor stream through its own ring of kStages stages (no CTA barrier anywhere): a stage is 4 k-groups
 // (16 k-steps): the 4 KB factor block arrives by one cp.async.bulk (TMA) on the stage's mbarrier, the 16
 // right-hand-side rows (k-step sources, krow) by cp.async into padded rows; lane 0 issues stage j + kStages - 1
@@ -1541,7 +1542,7 @@ __device__ __forceinline__ void piece_fetch(const Sweep4Dev& sw, int pb, int pen
 }
 
 template <int NT, bool VEC>
-__global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, int w0, int nwarps, int R,
+__global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, int w0, int nwarps, int vpw, int R,
                                                                 const double* __restrict__ srcA,
                                                                 const double* __restrict__ srcB,
                                                                 double* __restrict__ direct,
@@ -1561,7 +1562,7 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
     for (int i = 0; i < kStages; ++i) mbar_init(&bars[wl][i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncwarp();
-  const int w = blockIdx.x * kWarpsK3 + wl;
+  const int w = (blockIdx.x * kWarpsK3 + wl) * vpw;  // first of this warp's vpw consecutive ranges
   if (w >= nwarps) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     return;
@@ -1569,7 +1570,8 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
   // Everything but the right-hand side is static plan data: the warp range, its first piece, the k-step rows
   // and the factor blocks of the first kStages - 1 stages are fetched BEFORE griddepcontrol.wait, overlapping
   // the previous launch (its tail / the previous level's reduce); only the RHS copies wait for it.
-  const int g0 = sw.wg[w0 + w], g1 = sw.wg[w0 + w + 1];
+  const int w1 = min(w + vpw, nwarps);
+  const int g0 = sw.wg[w0 + w], g1 = sw.wg[w0 + w1];
   const int nst = (g1 - g0 + 3) >> 2;
   // k-step source rows of stage j (lane i < 16: k-step i)
   auto krow_of = [&](int j) {
@@ -1619,7 +1621,7 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
   }
   int kr_next = krow_of(kStages - 1);
   int pb = sw.wpiece[w0 + w], pi = 0;
-  const int pend = sw.wpiece[w0 + w + 1];
+  const int pend = sw.wpiece[w0 + w1];
   int pe_l, po_l, pn_l;
   piece_fetch(sw, pb, pend, lane, pe_l, po_l, pn_l);
   int pe = __shfl_sync(0xffffffffu, pe_l, 0);  // end (global k-group) of the current piece
@@ -1695,45 +1697,49 @@ __global__ void __launch_bounds__(32 * kWarpsK3, 1) k_sweep_warp(Sweep4Dev sw, i
 }
 
 // Level reduce of K3 v4: target t (row, mode) = fixed-order sum of its partial rows; mode 0: dst_assign[row] = sum,
-// mode 1: dst_sub[row] -= sum.
+// mode 1: dst_sub[row] -= sum.  NB source loads in flight per batch (8: c5 A^-1 464 -> 461 us against 4; same order,
+// bitwise-identical results).
+template <int NB>
 __global__ void k_sweep_reduce4(Sweep4Dev sw, int r0, int ntarget, int R, const double* __restrict__ partial,
                                 double* __restrict__ dst_assign, double* __restrict__ dst_sub) {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = gi < (int64_t)ntarget * R;
-  // the target's static metadata and its first source indices before griddepcontrol.wait
+  // the target's static metadata and its first NB source indices before griddepcontrol.wait
   const int t = live ? r0 + (int)(gi / R) : r0, c = live ? (int)(gi % R) : 0;
   const int q0 = sw.red_ptr[t], q1 = sw.red_ptr[t + 1], mode = sw.red_mode[t];
   const int64_t o = (int64_t)sw.red_row[t] * R + c;
-  int sq[4];
+  int sq[NB];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) sq[k] = q0 + k < q1 ? sw.red_src[q0 + k] : 0;
+  for (int k = 0; k < NB; ++k) sq[k] = q0 + k < q1 ? sw.red_src[q0 + k] : 0;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (!live) return;
   const double zo = mode == 0 ? 0.0 : dst_sub[o];
   double acc = 0;
   {
-    double pv[4];
+    double pv[NB];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) pv[k] = q0 + k < q1 ? partial[(int64_t)sq[k] * R + c] : 0.0;
+    for (int k = 0; k < NB; ++k) pv[k] = q0 + k < q1 ? partial[(int64_t)sq[k] * R + c] : 0.0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < NB; ++k)
       if (q0 + k < q1) acc += pv[k];
   }
-  int q = q0 + 4;
-  for (; q + 4 <= q1; q += 4) {
-    const int s0 = sw.red_src[q], s1 = sw.red_src[q + 1], s2 = sw.red_src[q + 2], s3 = sw.red_src[q + 3];
-    const double p0 = partial[(int64_t)s0 * R + c], p1 = partial[(int64_t)s1 * R + c];
-    const double p2 = partial[(int64_t)s2 * R + c], p3 = partial[(int64_t)s3 * R + c];
-    acc += p0;
-    acc += p1;
-    acc += p2;
-    acc += p3;
+  int q = q0 + NB;
+  for (; q + NB <= q1; q += NB) {  // NB loads in flight, then the in-order sum
+    int sk[NB];
+    double p[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) sk[k] = sw.red_src[q + k];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) p[k] = partial[(int64_t)sk[k] * R + c];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) acc += p[k];
   }
   for (; q < q1; ++q) acc += partial[(int64_t)sw.red_src[q] * R + c];
   if (mode == 0) dst_assign[o] = acc;
   else dst_sub[o] = zo - acc;
 }
+template __global__ void k_sweep_reduce4<8>(Sweep4Dev, int, int, int, const double*, double*, double*);
 
 // ----------------------------------------------------------------- K5: contact
 // The candidate nodes V are ordered last: their rows form the root supernode, whose assembled
