@@ -25,6 +25,7 @@ namespace {
 thread_local std::string g_create_error;
 
 __global__ void k_fill_int(int32_t* p, int32_t v, int n) {
+  PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
@@ -162,6 +163,29 @@ struct CudaError : std::runtime_error {
     CK(cudaGetLastError()); \
   } while (0)
 
+// Kernel launch on the handle's stream with programmatic stream serialisation (PDL; kernels.cu PDL_ENTRY): the
+// kernel's grid may be scheduled while its predecessor runs and waits in griddepcontrol.wait for it, hiding launch
+// latency and ramp between the many short dependent kernels of an iteration.  PD_PDL=0 launches
+// plainly (same results: the wait is then a no-op).
+inline bool pdl_enabled() {
+  static const bool on = !(std::getenv("PD_PDL") && std::atoi(std::getenv("PD_PDL")) == 0);
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void pdl_launch(pd_sim* s, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = grid;
+  c.blockDim = block;
+  c.dynamicSmemBytes = smem;
+  c.stream = s->stream;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  c.attrs = a;
+  c.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&c, kernel, std::forward<Args>(args)...));
+}
+
 pd_status fail(pd_sim* s, pd_status st, const std::string& msg) {
   if (s) s->err = msg;
   else g_create_error = msg;
@@ -232,9 +256,9 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
   }
   da.npairs = p;
   const int nchunk = red_chunks(len);
-  k_dot_partial<<<dim3(nchunk, red_groups(B)), red_threads(B), 0, s->stream>>>(da, len, B, s->partial);
+  pdl_launch(s, k_dot_partial, dim3(nchunk, red_groups(B)), red_threads(B), 0, da, len, B, s->partial);
   LAUNCH_CHECK(s);
-  k_dot_final<<<p * B, 128, 0, s->stream>>>(s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
+  pdl_launch(s, k_dot_final, p * B, 128, 0, s->partial, nchunk, B, p, out ? out : s->dots, accumulate);
   LAUNCH_CHECK(s);
 }
 
@@ -244,30 +268,30 @@ void dots(pd_sim* s, int B, int64_t len, std::initializer_list<std::pair<const d
 void abi_in(pd_sim* s, const double* in, double* out, int B, int64_t bstride, int kind) {
   const int n3 = 3 * s->plan.n;
   if (s->frame && kind) {
-    k_abi_to_state_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(in, out, s->plan.n, B, bstride, s->fq,
+    pdl_launch(s, k_abi_to_state_frame, nblk((int64_t)s->plan.n * B), 256, 0, in, out, s->plan.n, B, bstride, s->fq,
                                                                             kind == 1);
   } else {
-    k_abi_to_state<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(in, out, n3, B, bstride);
+    pdl_launch(s, k_abi_to_state, nblk((int64_t)n3 * B), 256, 0, in, out, n3, B, bstride);
   }
   LAUNCH_CHECK(s);
 }
 void abi_out(pd_sim* s, const double* in, double* out, int B, int64_t bstride, int kind) {
   const int n3 = 3 * s->plan.n;
   if (s->frame && kind) {
-    k_state_to_abi_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(in, out, s->plan.n, B, bstride, s->fq,
+    pdl_launch(s, k_state_to_abi_frame, nblk((int64_t)s->plan.n * B), 256, 0, in, out, s->plan.n, B, bstride, s->fq,
                                                                             kind == 1);
   } else {
-    k_state_to_abi<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(in, out, n3, B, bstride);
+    pdl_launch(s, k_state_to_abi, nblk((int64_t)n3 * B), 256, 0, in, out, n3, B, bstride);
   }
   LAUNCH_CHECK(s);
 }
 void abi_add(pd_sim* s, double* out, const double* in, int B, int64_t bstride) {  // vectors, non-Dirichlet nodes
   const int n3 = 3 * s->plan.n;
   if (s->frame) {
-    k_add_abi_frame<<<nblk((int64_t)s->plan.n * B), 256, 0, s->stream>>>(out, in, s->plan.n, B, bstride, s->d_fixed,
+    pdl_launch(s, k_add_abi_frame, nblk((int64_t)s->plan.n * B), 256, 0, out, in, s->plan.n, B, bstride, s->d_fixed,
                                                                        s->fq);
   } else {
-    k_add_abi<<<nblk((int64_t)n3 * B), 256, 0, s->stream>>>(out, in, n3, B, bstride, s->d_fixed);
+    pdl_launch(s, k_add_abi, nblk((int64_t)n3 * B), 256, 0, out, in, n3, B, bstride, s->d_fixed);
   }
   LAUNCH_CHECK(s);
 }
@@ -334,7 +358,7 @@ void solve_rc(pd_sim* s, int B) {  // (contact fixup of the root block when s->p
     double* root = s->S0 + (int64_t)s->csup_first * R;
     CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
     level(P.bw, s->swb, false, 0);
-    k_contact_fix<<<dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, s->stream>>>(
+    pdl_launch(s, k_contact_fix, dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, 
         s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos, s->Qc, root);
     LAUNCH_CHECK(s);
     for (int j = 1; j < P.nlevels; ++j) level(P.bw, s->swb, false, j);
@@ -397,7 +421,7 @@ void solve_v4(pd_sim* s, int B) {
     double* root = s->S0 + (int64_t)s->csup_first * R;
     CK(cudaMemcpyAsync(s->Rsave, root, sizeof(double) * (int64_t)s->nc * R, cudaMemcpyDeviceToDevice, s->stream));
     level(P.bw4, s->sw4b, false, 0);
-    k_contact_fix<<<dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, s->stream>>>(
+    pdl_launch(s, k_contact_fix, dim3((s->nc + 7) / 8, (s->sticky ? 3 : 1) * B), 256, 0, 
         s->Rsave, s->nc, R, B, s->kcount, s->flist, s->fpos, s->Qc, root);
     LAUNCH_CHECK(s);
     for (int j = 1; j < P.nlevels; ++j) level(P.bw4, s->sw4b, false, j);
@@ -454,10 +478,10 @@ void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* 
                 const int32_t* active) {
   const HostPlan& P = s->plan;
   ProfScope ps(s, 2);
-  k_to_solve<<<nblk((int64_t)P.nfree * 3 * B), 256, 0, s->stream>>>(Vin, s->d_nodepos, P.nfree, B, s->S0);
+  pdl_launch(s, k_to_solve, nblk((int64_t)P.nfree * 3 * B), 256, 0, Vin, s->d_nodepos, P.nfree, B, s->S0);
   LAUNCH_CHECK(s);
   solve(s, B);
-  k_from_solve<<<nblk((int64_t)3 * P.n * B), 256, 0, s->stream>>>(s->S0, s->d_pos, P.n, B, alpha, alpha_c, beta,
+  pdl_launch(s, k_from_solve, nblk((int64_t)3 * P.n * B), 256, 0, s->S0, s->d_pos, P.n, B, alpha, alpha_c, beta,
                                                                    active, OUT);
   LAUNCH_CHECK(s);
 }
@@ -468,11 +492,11 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   const HostPlan& P = s->plan;
   {
     ProfScope ps(s, 0);
-    (s->d_fib ? k_elem_residual<true> : k_elem_residual<false>)<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, s->st, elem_args(s, B, act_step, act_bstride),
+    pdl_launch(s, s->d_fib ? k_elem_residual<true> : k_elem_residual<false>, nblk((int64_t)P.m * B * 8, 256), 256, 0, X, s->st, elem_args(s, B, act_step, act_bstride),
                                                                          s->EF, s->EE);
     LAUNCH_CHECK(s);
     if (s->st.kappa != 0.0) {  // volume-preserving term added to the element forces and energies
-      k_vol<0><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, nullptr, s->st,
+      pdl_launch(s, k_vol<0>, nblk((int64_t)P.m * B * 8, 256), 256, 0, X, nullptr, s->st,
                                                                       elem_args(s, B, act_step, act_bstride), nullptr,
                                                                       s->EF, s->EE);
       LAUNCH_CHECK(s);
@@ -480,7 +504,7 @@ void residual(pd_sim* s, int B, const double* X, const double* Y, const double* 
   }
   ProfScope ps(s, 1);
   const bool pin = s->pins_live;
-  k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
+  pdl_launch(s, k_gather, nblk((int64_t)P.n * B), 256, 0, X, Y, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec, fixed_mask,
                                                           s->d_pos, P.n, B, 1.0 / (s->h * s->h), 0, Gout ? Gout : s->G,
                                                           s->W, s->S0,
                                                           pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr,
@@ -494,25 +518,25 @@ void apply_AN(pd_sim* s, int B, const double* X, const double* Pin, double* OUT,
   const HostPlan& P = s->plan;
   ProfScope ps(s, 3);
   if (jc)
-    k_elem_AN_cached<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(
+    pdl_launch(s, k_elem_AN_cached, nblk((int64_t)P.m * B * 8, 256), 256, 0, 
         Pin, s->st, elem_args(s, B, act_step, act_bstride), jc, s->EF);
   else
-    k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st,
+    pdl_launch(s, k_elem_AN, nblk((int64_t)P.m * B * 8, 256), 256, 0, X, Pin, s->st,
                                                                    elem_args(s, B, act_step, act_bstride), s->EF);
   LAUNCH_CHECK(s);
   if (s->st.kappa != 0.0) {
     if (jc)
-      k_vol<1><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(nullptr, Pin, s->st,
+      pdl_launch(s, k_vol<1>, nblk((int64_t)P.m * B * 8, 256), 256, 0, nullptr, Pin, s->st,
                                                                       elem_args(s, B, act_step, act_bstride),
                                                                       const_cast<double*>(jc), s->EF, nullptr);
     else
-      k_vol<2><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(X, Pin, s->st,
+      pdl_launch(s, k_vol<2>, nblk((int64_t)P.m * B * 8, 256), 256, 0, X, Pin, s->st,
                                                                       elem_args(s, B, act_step, act_bstride), nullptr,
                                                                       s->EF, nullptr);
     LAUNCH_CHECK(s);
   }
   const bool pin = s->pins_live;
-  k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
+  pdl_launch(s, k_gather, nblk((int64_t)P.n * B), 256, 0, Pin, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                           s->d_fixed, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, OUT,
                                                           nullptr, nullptr, pin ? s->d_cand_of_node : nullptr,
                                                           pin ? s->PIN : nullptr, nullptr, s->sticky);
@@ -529,7 +553,7 @@ void set_w(pd_sim* s, int B, const double* youngs_per_sim, bool diag = false) {
     CK(cudaMemcpyAsync(E, youngs_per_sim, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
   else
     CK(cudaMemcpyAsync(E, ones.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-  k_axpby<<<1, 256, 0, s->stream>>>(w, E, 1.0 / (1.0 + s->poisson), nullptr, nullptr, 0.0, B, B, nullptr);
+  pdl_launch(s, k_axpby, 1, 256, 0, w, E, 1.0 / (1.0 + s->poisson), nullptr, nullptr, 0.0, B, B, nullptr);
   LAUNCH_CHECK(s);
   CK(cudaStreamSynchronize(s->stream));
   s->w_cur = w;
@@ -559,10 +583,10 @@ void mdot(pd_sim* s, int B, const double* u, const double* Vbase, int nv, double
   const int64_t n3 = 3LL * s->plan.n;
   const int nchunk = red_chunks(n3);
   const int np = u2 ? 2 * nv : nv;
-  k_mdot_partial<<<dim3(nchunk, np, red_groups(B)), red_threads(B), 0, s->stream>>>(u, Vbase, n3 * B, nv, n3, B,
+  pdl_launch(s, k_mdot_partial, dim3(nchunk, np, red_groups(B)), red_threads(B), 0, u, Vbase, n3 * B, nv, n3, B,
                                                                                     s->partial, u2, V2base);
   LAUNCH_CHECK(s);
-  k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, out);
+  pdl_launch(s, k_dot_final, np * B, 128, 0, s->partial, nchunk, B, np, out, 0);
   LAUNCH_CHECK(s);
 }
 
@@ -576,14 +600,14 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
   const int64_t n3 = 3LL * P.n;
   const int nchunk = red_chunks(n3);
   const int np = with_gn2 ? 2 : 1;
-  k_inertia_partial<<<dim3(nchunk, red_groups(B)), red_threads(B), 0, s->stream>>>(
+  pdl_launch(s, k_inertia_partial, dim3(nchunk, red_groups(B)), red_threads(B), 0, 
       X, s->Y, s->d_mass, 1.0 / (s->h * s->h), n3, B, s->partial, with_gn2 ? Gout : nullptr);
   LAUNCH_CHECK(s);
-  k_dot_final<<<np * B, 128, 0, s->stream>>>(s->partial, nchunk, B, np, s->inert);
+  pdl_launch(s, k_dot_final, np * B, 128, 0, s->partial, nchunk, B, np, s->inert, 0);
   LAUNCH_CHECK(s);
   dots(s, B, P.m, {{s->EE, nullptr}}, s->esum);
   if (fout) {
-    k_obj_combine<<<nblk(B, 64), 64, 0, s->stream>>>(s->inert, s->esum, fout, B);
+    pdl_launch(s, k_obj_combine, nblk(B, 64), 64, 0, s->inert, s->esum, fout, B);
     LAUNCH_CHECK(s);
   }
 }
@@ -591,15 +615,15 @@ void eval_f(pd_sim* s, int B, const double* X, double* Gout, double* fout, const
 // zero Dirichlet nodes and (when pins are live) the pinned z DoFs of a state vector
 void zero_constrained(pd_sim* s, double* Y, int B) {
   const bool pin = s->pins_live;
-  k_zero_constrained<<<nblk((int64_t)3 * s->plan.n * B), 256, 0, s->stream>>>(
+  pdl_launch(s, k_zero_constrained, nblk((int64_t)3 * s->plan.n * B), 256, 0, 
       Y, s->d_fixed, s->plan.n, B, pin ? s->d_cand_of_node : nullptr, pin ? s->PIN : nullptr, s->sticky);
   LAUNCH_CHECK(s);
 }
 
 // zero Dirichlet nodes only
 void zero_constrained_fixed(pd_sim* s, double* Y, int B) {
-  k_zero_constrained<<<nblk((int64_t)3 * s->plan.n * B), 256, 0, s->stream>>>(Y, s->d_fixed, s->plan.n, B, nullptr,
-                                                                              nullptr);
+  pdl_launch(s, k_zero_constrained, nblk((int64_t)3 * s->plan.n * B), 256, 0, Y, s->d_fixed, s->plan.n, B, nullptr,
+                                                                              nullptr, 0);
   LAUNCH_CHECK(s);
 }
 
@@ -608,7 +632,7 @@ void zero_constrained_fixed(pd_sim* s, double* Y, int B) {
 void build_Q(pd_sim* s, int B, const int32_t* sel) {
   ProfScope ps(s, 4);
   const int c = s->nc;
-  k_contact_flist<<<B, 1024, 0, s->stream>>>(s->PIN, s->d_cand_of_loc, c, B, sel, s->flist, s->fpos, s->kcount);
+  pdl_launch(s, k_contact_flist, B, 1024, 0, s->PIN, s->d_cand_of_loc, c, B, sel, s->flist, s->fpos, s->kcount);
   LAUNCH_CHECK(s);
   std::vector<int32_t> selh(B, 1);
   if (sel) CK(cudaMemcpyAsync(s->h_small + B, sel, B * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
@@ -624,16 +648,16 @@ void build_Q(pd_sim* s, int B, const int32_t* sel) {
   if (kmax == 0) return;
   CK(cudaMemcpyAsync(s->need, selh.data(), B * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
   const int nt = (kmax + 31) / 32;
-  k_contact_gather_S<<<dim3(nt, (kmax + 7) / 8, B), dim3(32, 8), 0, s->stream>>>(s->d_S, c, s->need, s->flist,
+  pdl_launch(s, k_contact_gather_S, dim3(nt, (kmax + 7) / 8, B), dim3(32, 8), 0, s->d_S, c, s->need, s->flist,
                                                                                  s->kcount, s->Qc);
   LAUNCH_CHECK(s);
   for (int kb = 0; kb < nt; ++kb) {
-    k_gj_pivot<<<B, 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc);
+    pdl_launch(s, k_gj_pivot, B, 256, 0, s->Qc, c, kb, s->need, s->kcount, s->PIc);
     LAUNCH_CHECK(s);
-    k_gj_panel<<<dim3((kmax + 63) / 64, B), 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Cb,
+    pdl_launch(s, k_gj_panel, dim3((kmax + 63) / 64, B), 256, 0, s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Cb,
                                                                  s->Mb, s->Rb);
     LAUNCH_CHECK(s);
-    k_gj_update<<<dim3(nt, nt, B), 256, 0, s->stream>>>(s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Mb, s->Rb);
+    pdl_launch(s, k_gj_update, dim3(nt, nt, B), 256, 0, s->Qc, c, kb, s->need, s->kcount, s->PIc, s->Mb, s->Rb);
     LAUNCH_CHECK(s);
   }
 }
@@ -667,7 +691,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     }
     for (int j = 0; j < hist; ++j) {
       mdot(s, B, LSs(j), s->LY, hist, s->lb_da, LYs(j), s->LS);
-      k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)hist * B, j, m,
+      pdl_launch(s, k_gram_store, nblk(B, 64), 64, 0, s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)hist * B, j, m,
                                                       hist, B, s->active, nullptr, nullptr, nullptr, nullptr);
       LAUNCH_CHECK(s);
     }
@@ -680,7 +704,7 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // host sync per iteration instead of two; were every sim to converge meanwhile, the direction and trial
     // launched after the check are fully masked and the loop ends at that sync).  Once a running sim is within
     // 16 tol the check is read immediately, so no masked iteration is spent at the end of a solve.
-    k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
+    pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
                                           s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
                                           s->ls_act, s->nactive + 2);
@@ -694,9 +718,9 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
-      k_lbfgs_alpha<<<B, 32, 0, s->stream>>>(s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, gi, B, s->active);
+      pdl_launch(s, k_lbfgs_alpha, B, 32, 0, s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, gi, B, s->active);
       LAUNCH_CHECK(s);
-      k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
+      pdl_launch(s, k_multi_axpy, nblk(len), 256, 0, s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
                                                      s->active);  // q = g - sum alpha_j y_j
       LAUNCH_CHECK(s);
     } else {
@@ -705,23 +729,23 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);  // r0 = H0 q = A^{-1} q
     if (hist > 0) {
       mdot(s, B, s->Dv, s->LY, hist, s->lb_yr);
-      k_lbfgs_beta<<<B, 32, 0, s->stream>>>(s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, gi, B,
+      pdl_launch(s, k_lbfgs_beta, B, 32, 0, s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, gi, B,
                                                       s->active);
       LAUNCH_CHECK(s);
-      k_multi_axpy<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,
+      pdl_launch(s, k_multi_axpy, nblk(len), 256, 0, s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,
                                                      B, s->active);  // d = -(r0 + sum (alpha_j - beta_j) s_j)
       LAUNCH_CHECK(s);
     } else {
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
       LAUNCH_CHECK(s);
     }
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
     // Armijo backtracking from alpha = 1 (set by k_fwd_check); g_new and the decision in k_ls_accept
     for (int trial = 0;; ++trial) {
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
       LAUNCH_CHECK(s);
       eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
-      k_ls_accept<<<1, 256, 0, s->stream>>>(s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
+      pdl_launch(s, k_ls_accept, 1, 256, 0, s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
                                             s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
       LAUNCH_CHECK(s);
       int searching = 0, running = 1, nr = 0;
@@ -739,11 +763,11 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // curvature pair (s, y) into slot iter % m and commit x, grad g (one pass); Gram row/column of the new
     // pair (both multi-dots in one pass); f, |grad g|^2
     const int slot = gi % m;
-    k_lbfgs_commit<<<nblk(len), 256, 0, s->stream>>>(LSs(slot), LYs(slot), s->X, s->G, s->Xn, s->Gn, len, B, s->active);
+    pdl_launch(s, k_lbfgs_commit, nblk(len), 256, 0, LSs(slot), LYs(slot), s->X, s->G, s->Xn, s->Gn, len, B, s->active);
     LAUNCH_CHECK(s);
     const int nv = std::min(hist + 1, m);  // valid slots after this store are [0, nv)
     mdot(s, B, LSs(slot), s->LY, nv, s->lb_da, LYs(slot), s->LS);  // s_new^T y_j | y_new^T s_j
-    k_gram_store<<<nblk(B, 64), 64, 0, s->stream>>>(s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)nv * B, slot, m, nv,
+    pdl_launch(s, k_gram_store, nblk(B, 64), 64, 0, s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)nv * B, slot, m, nv,
                                                     B, s->active, s->fcur, s->fnew, s->dots, gn2);
     LAUNCH_CHECK(s);
     hist = nv;
@@ -769,7 +793,7 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
   dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
   double* const gn2 = s->inert + B;
   for (int iter = 0;; ++iter) {
-    k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
+    pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
                                           s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
                                           s->ls_act, s->nactive + 2);
@@ -782,11 +806,11 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
     }
     {  // Hessian data at x (P:228's per-step Jacobian, here per Newton iteration)
       ProfScope ps(s, 3);
-      k_elem_jac<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->st, elem_args(s, B, act_i, act_bs),
+      pdl_launch(s, k_elem_jac, nblk((int64_t)P.m * B * 8, 256), 256, 0, s->X, s->st, elem_args(s, B, act_i, act_bs),
                                                                        s->JC);
       LAUNCH_CHECK(s);
       if (s->st.kappa != 0.0) {
-        k_vol<3><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, nullptr, s->st,
+        pdl_launch(s, k_vol<3>, nblk((int64_t)P.m * B * 8, 256), 256, 0, s->X, nullptr, s->st,
                                                                         elem_args(s, B, act_i, act_bs), s->JC, nullptr,
                                                                         nullptr);
         LAUNCH_CHECK(s);
@@ -794,7 +818,7 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
     }
     // CG: A_N D = -G on the running sims (pact), r0 = -G, z0 = A^{-1} r0 (kept: the PD direction)
     CK(cudaMemcpyAsync(s->pact, s->active, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
-    k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->G, -1.0, nullptr, nullptr, 0.0, len, B, nullptr);
+    pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Rv, s->G, -1.0, nullptr, nullptr, 0.0, len, B, nullptr);
     LAUNCH_CHECK(s);
     CK(cudaMemsetAsync(s->Dv, 0, len * sizeof(double), s->stream));
     CK(cudaMemcpyAsync(s->bb, s->dots, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));  // |b|^2 = |G|^2
@@ -804,34 +828,34 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
     for (int it = 0;; ++it) {
       const bool fused = it > 0;
       if (!fused) dots(s, B, n3, {{s->Rv, s->Rv}}, s->dots + 2 * B);
-      k_adj_check<<<1, 256, 0, s->stream>>>(s->dots + 2 * B, s->bb, B, s->newton_eta, it, s->opt.max_iter_adj, s->pact,
+      pdl_launch(s, k_adj_check, 1, 256, 0, s->dots + 2 * B, s->bb, B, s->newton_eta, it, s->opt.max_iter_adj, s->pact,
                                             s->nt_iters, s->nt_res, s->nt_flag, s->nactive, fused ? s->rz : nullptr,
                                             s->dots + 3 * B);
       LAUNCH_CHECK(s);
       if (it >= s->opt.max_iter_adj || read_nactive(s) == 0) break;
       apply_AN(s, B, s->X, s->Pv, s->Q, act_i, act_bs, s->JC);
       dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + 3 * B);
-      k_negcurv<<<nblk(B, 64), 64, 0, s->stream>>>(s->dots + 3 * B, s->pact, B);
+      pdl_launch(s, k_negcurv, nblk(B, 64), 64, 0, s->dots + 3 * B, s->pact, B);
       LAUNCH_CHECK(s);
-      k_pcg_update<<<nblk(len), 256, 0, s->stream>>>(s->Dv, s->Rv, s->Pv, s->Q, s->rz, s->dots + 3 * B, len, B, s->pact);
+      pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->Dv, s->Rv, s->Pv, s->Q, s->rz, s->dots + 3 * B, len, B, s->pact);
       LAUNCH_CHECK(s);
       apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->pact);
       dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + 3 * B);  // rz_new | |r|^2
-      k_pcg_dir<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, s->dots + 3 * B, s->rz, len, B, s->pact);
+      pdl_launch(s, k_pcg_dir, nblk(len), 256, 0, s->Pv, s->Z, s->dots + 3 * B, s->rz, len, B, s->pact);
       LAUNCH_CHECK(s);
       // (k_adj_check reads |r|^2 at dots[2B:3B): move it there)
       CK(cudaMemcpyAsync(s->dots + 2 * B, s->dots + 4 * B, B * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
     }
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
-    k_descent_guard<<<nblk(len), 256, 0, s->stream>>>(s->Dv, Z0, s->gtd, len, B, s->active);
+    pdl_launch(s, k_descent_guard, nblk(len), 256, 0, s->Dv, Z0, s->gtd, len, B, s->active);
     LAUNCH_CHECK(s);
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
     bool done = false;
     for (int trial = 0;; ++trial) {  // Armijo backtracking from alpha = 1 (as inner_lbfgs)
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
       LAUNCH_CHECK(s);
       eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
-      k_ls_accept<<<1, 256, 0, s->stream>>>(s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
+      pdl_launch(s, k_ls_accept, 1, 256, 0, s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
                                             s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
       LAUNCH_CHECK(s);
       int searching = 0, running = 1, nr = 0;
@@ -843,9 +867,9 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
       if (searching == 0) break;
     }
     if (done) break;
-    k_newton_commit<<<nblk(len), 256, 0, s->stream>>>(s->X, s->G, s->Xn, s->Gn, len, B, s->active);
+    pdl_launch(s, k_newton_commit, nblk(len), 256, 0, s->X, s->G, s->Xn, s->Gn, len, B, s->active);
     LAUNCH_CHECK(s);
-    k_newton_commit_s<<<nblk(B, 64), 64, 0, s->stream>>>(s->fcur, s->fnew, s->dots, gn2, B, s->active);
+    pdl_launch(s, k_newton_commit_s, nblk(B, 64), 64, 0, s->fcur, s->fnew, s->dots, gn2, B, s->active);
     LAUNCH_CHECK(s);
   }
 }
@@ -1195,36 +1219,36 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       const int64_t act_bs = (int64_t)steps * P.m;
       if (f_ext && f_ext_step_stride)  // time-varying f_ext: this step's slice of [B][steps][3n]
         abi_in(s, f_ext + (int64_t)i * n3, s->Fext, B, (int64_t)steps * n3, 2);
-      k_y<<<nblk(len), 256, 0, s->stream>>>(s->X, s->V, f_ext ? s->Fext : nullptr, s->d_mass, s->Y, P.n, B, s->h,
+      pdl_launch(s, k_y, nblk(len), 256, 0, s->X, s->V, f_ext ? s->Fext : nullptr, s->d_mass, s->Y, P.n, B, s->h,
                                             s->gravity[0], s->gravity[1], s->gravity[2]);
       LAUNCH_CHECK(s);
       CK(cudaMemcpyAsync(s->Xp, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
       const bool predict = s->opt.x0_predict && s->opt.fixed_iter <= 0;
       if (predict) {  // x^0 = x_i + h v_i (Dirichlet DoFs have v = 0 and stay at rest)
-        k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, 1.0, s->V, nullptr, s->h, len, B, nullptr);
+        pdl_launch(s, k_axpby, nblk(len), 256, 0, s->X, s->Xp, 1.0, s->V, nullptr, s->h, len, B, nullptr);
         LAUNCH_CHECK(s);
       }
       const bool contact = s->nc > 0;
       const int64_t cB = (int64_t)s->nc * B;
       if (contact) {  // Alg. 1: V_i = empty
         CK(cudaMemsetAsync(s->PIN, 0, cB, s->stream));
-        k_fill_int<<<1, 256, 0, s->stream>>>(s->oact, 1, B);
+        pdl_launch(s, k_fill_int, 1, 256, 0, s->oact, 1, B);
         LAUNCH_CHECK(s);
-        k_fill_int<<<1, 256, 0, s->stream>>>(s->kcount, s->nc, B);  // no pins: unconstrained root block
+        pdl_launch(s, k_fill_int, 1, 256, 0, s->kcount, s->nc, B);  // no pins: unconstrained root block
         LAUNCH_CHECK(s);
         CK(cudaMemsetAsync(s->it_base, 0, B * sizeof(int32_t), s->stream));
         s->pins_live = true;
       }
       for (int outer = 1; outer <= (contact ? s->opt.max_outer : 1); ++outer) {
         if (contact) {
-          k_contact_restart<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact,
+          pdl_launch(s, k_contact_restart, nblk(len), 256, 0, s->X, s->Xp, P.n, B, s->d_cand_of_node, s->PIN, s->oact,
                                                               (s->opt.outer_warm && outer > 1) || (predict && outer == 1),
                                                               s->sticky);
           LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
           if (outer > 1) build_Q(s, B, s->oact);
           CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
         } else {
-          k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
+          pdl_launch(s, k_fill_int, 1, 256, 0, s->active, 1, B);
           LAUNCH_CHECK(s);
         }
         if (s->opt.accel_fwd == 2 && s->opt.fixed_iter <= 0) {
@@ -1235,10 +1259,10 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           for (int iter = 0;; ++iter) {
             residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
             dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
-            k_fwd_check<<<1, 256, 0, s->stream>>>(s->dots, B, tol, iter, s->opt.fixed_iter,
+            pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, tol, iter, s->opt.fixed_iter,
                                                            s->opt.max_iter_fwd, s->active, s->st_iters_f + (int64_t)i * B,
                                                            s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
-                                                           s->nactive, contact ? s->it_base : nullptr);
+                                                           s->nactive, contact ? s->it_base : nullptr, nullptr, nullptr, nullptr);
             LAUNCH_CHECK(s);
             if (s->opt.fixed_iter > 0) {
               if (iter >= s->opt.fixed_iter) break;
@@ -1257,10 +1281,10 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
         CK(cudaMemsetAsync(s->changed, 0, B * sizeof(int32_t), s->stream));
         {
           ProfScope ps(s, 4);
-          k_contact_predict<<<nblk(cB), 256, 0, s->stream>>>(s->X, s->LAM, s->d_cand_node, s->nc, B, s->opt.eps_phi,
+          pdl_launch(s, k_contact_predict, nblk(cB), 256, 0, s->X, s->LAM, s->d_cand_node, s->nc, B, s->opt.eps_phi,
                                                              s->PIN, s->oact, s->NEWPIN, s->changed);
           LAUNCH_CHECK(s);
-          k_contact_outer<<<nblk(cB), 256, 0, s->stream>>>(s->oact, s->changed, s->NEWPIN, s->PIN, s->nc, B, outer,
+          pdl_launch(s, k_contact_outer, nblk(cB), 256, 0, s->oact, s->changed, s->NEWPIN, s->PIN, s->nc, B, outer,
                                                            s->opt.max_outer, s->onext, s->st_outer + (int64_t)i * B,
                                                            s->st_flag_f + (int64_t)i * B);
           LAUNCH_CHECK(s);
@@ -1277,7 +1301,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
         CK(cudaMemcpyAsync(s->traj_pin + (int64_t)i * cB, s->PIN, cB, cudaMemcpyDeviceToDevice, s->stream));
         s->pins_live = false;
       }
-      k_velocity<<<nblk(len), 256, 0, s->stream>>>(s->X, s->Xp, s->V, len, 1.0 / s->h);
+      pdl_launch(s, k_velocity, nblk(len), 256, 0, s->X, s->Xp, s->V, len, 1.0 / s->h);
       LAUNCH_CHECK(s);
       CK(cudaMemcpyAsync(s->traj + (int64_t)(i + 1) * len, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice,
                          s->stream));
@@ -1368,23 +1392,23 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
       }
       {  // per-step Jacobian data of the projections at x_{i+1}, reused by every K4 product
         ProfScope ps(s, 3);
-        k_elem_jac<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->st, elem_args(s, B, act_i, act_bs),
+        pdl_launch(s, k_elem_jac, nblk((int64_t)P.m * B * 8, 256), 256, 0, x1, s->st, elem_args(s, B, act_i, act_bs),
                                                                          s->JC);
         LAUNCH_CHECK(s);
         if (s->st.kappa != 0.0) {
-          k_vol<3><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, nullptr, s->st,
+          pdl_launch(s, k_vol<3>, nblk((int64_t)P.m * B * 8, 256), 256, 0, x1, nullptr, s->st,
                                                                           elem_args(s, B, act_i, act_bs), s->JC,
                                                                           nullptr, nullptr);
           LAUNCH_CHECK(s);
         }
       }
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Bv, s->AX, 1.0, s->AV, nullptr, 1.0 / h, len, B, nullptr);
       LAUNCH_CHECK(s);
       zero_constrained(s, s->Bv, B);
       dots(s, B, n3, {{s->Bv, s->Bv}}, s->bb);
       CK(cudaMemsetAsync(s->U, 0, len * sizeof(double), s->stream));
       CK(cudaMemcpyAsync(s->Rv, s->Bv, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
-      k_fill_int<<<1, 256, 0, s->stream>>>(s->active, 1, B);
+      pdl_launch(s, k_fill_int, 1, 256, 0, s->active, 1, B);
       LAUNCH_CHECK(s);
       if (pcg) {
         apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, nullptr);
@@ -1396,7 +1420,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         // end of the previous PCG iteration (dots[2B:3B]); k_adj_check also commits rz <- rz_new there
         const bool fused_rr = pcg && iter > 0;
         if (!fused_rr) dots(s, B, n3, {{s->Rv, s->Rv}});
-        k_adj_check<<<1, 256, 0, s->stream>>>(fused_rr ? s->dots + 2 * B : s->dots, s->bb, B, s->opt.tol_adj, iter,
+        pdl_launch(s, k_adj_check, 1, 256, 0, fused_rr ? s->dots + 2 * B : s->dots, s->bb, B, s->opt.tol_adj, iter,
                                               s->opt.max_iter_adj, s->active, s->st_iters_a + (int64_t)i * B,
                                               s->st_res_a + (int64_t)i * B, s->st_flag_a + (int64_t)i * B, s->nactive,
                                               fused_rr ? s->rz : nullptr, s->dots + B);
@@ -1407,39 +1431,39 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
           apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs, s->JC);  // (k_gather zeroes the constrained rows)
           dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
           // u += alpha p, r -= alpha q, alpha = rz / pq (one pass)
-          k_pcg_update<<<nblk(len), 256, 0, s->stream>>>(s->U, s->Rv, s->Pv, s->Q, s->rz, s->dots + B, len, B, s->active);
+          pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->U, s->Rv, s->Pv, s->Q, s->rz, s->dots + B, len, B, s->active);
           LAUNCH_CHECK(s);
           apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->active);
           dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + B);  // rz_new | |r|^2
           // p = z + beta p, beta = rz_new / rz (rz itself is committed by the next k_adj_check)
-          k_pcg_dir<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->Z, s->dots + B, s->rz, len, B, s->active);
+          pdl_launch(s, k_pcg_dir, nblk(len), 256, 0, s->Pv, s->Z, s->dots + B, s->rz, len, B, s->active);
           LAUNCH_CHECK(s);
         } else {
           // fixed point u <- u + A^{-1}(b - A_N u) == A^{-1}(b + dA u)  (eq:bp_update)
           apply_Ainv(s, B, s->Rv, s->U, nullptr, 1.0, 1.0, s->active);
           apply_AN(s, B, x1, s->U, s->Q, act_i, act_bs, s->JC);  // (k_gather zeroes the constrained rows)
-          k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
+          pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Rv, s->Bv, 1.0, s->Q, nullptr, -1.0, len, B, s->active);
           LAUNCH_CHECK(s);
         }
       }
       // parameter terms, f_ext accumulation, state adjoint update
       ProfScope ps_param(s, 5);
-      k_elem_param<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
+      pdl_launch(s, k_elem_param, nblk((int64_t)P.m * B * 8, 256), 256, 0, x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
                                                                       s->DW, s->has_act ? s->DR : nullptr);
       LAUNCH_CHECK(s);
       dots(s, B, P.m, {{s->DW, nullptr}}, s->dw_acc, 1);
       if (s->DWV) {
-        k_vol<4><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
+        pdl_launch(s, k_vol<4>, nblk((int64_t)P.m * B * 8, 256), 256, 0, x1, s->U, s->st, elem_args(s, B, act_i, act_bs),
                                                                         nullptr, s->DWV, nullptr);
         LAUNCH_CHECK(s);
         dots(s, B, P.m, {{s->DWV, nullptr}}, s->dwv_acc, 1);
       }
       if (dL_dact && s->has_act) {
-        k_state_to_abi<<<nblk((int64_t)P.m * B), 256, 0, s->stream>>>(s->DR, dL_dact + (int64_t)i * P.m, P.m, B,
+        pdl_launch(s, k_state_to_abi, nblk((int64_t)P.m * B), 256, 0, s->DR, dL_dact + (int64_t)i * P.m, P.m, B,
                                                                       (int64_t)T * P.m);
         LAUNCH_CHECK(s);
       }
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->DF, 1.0, s->U, nullptr, 1.0, len, B, nullptr);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->DF, s->DF, 1.0, s->U, nullptr, 1.0, len, B, nullptr);
       LAUNCH_CHECK(s);
       if (dfext_steps) {  // dL/df_ext of step i = u_i (0 on Dirichlet DoFs)
         zero_constrained_fixed(s, s->U, B);
@@ -1450,14 +1474,14 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         s->pins_live = false;  // A_N u on every row, pinned rows included
         apply_AN(s, B, x1, s->U, s->Z, act_i, act_bs, s->JC);
         s->pins_live = true;
-        k_sticky_extra<<<nblk(len), 256, 0, s->stream>>>(s->Pv, s->AX, s->AV, s->Z, 1.0 / h, P.n, B, s->d_cand_of_node,
+        pdl_launch(s, k_sticky_extra, nblk(len), 256, 0, s->Pv, s->AX, s->AV, s->Z, 1.0 / h, P.n, B, s->d_cand_of_node,
                                                          s->PIN);
         LAUNCH_CHECK(s);
       }
-      k_adj_state<<<nblk(len), 256, 0, s->stream>>>(s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
+      pdl_launch(s, k_adj_state, nblk(len), 256, 0, s->U, s->d_mass, s->d_fixed, s->AX, s->AV, P.n, B, h);
       LAUNCH_CHECK(s);
       if (sticky_step) {
-        k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->AX, s->AX, 1.0, s->Pv, nullptr, 1.0, len, B, nullptr);
+        pdl_launch(s, k_axpby, nblk(len), 256, 0, s->AX, s->AX, 1.0, s->Pv, nullptr, 1.0, len, B, nullptr);
         LAUNCH_CHECK(s);
       }
       if (dq_steps) abi_add(s, s->AX, dq_steps + (int64_t)i * n3, B, sstride);
@@ -1467,7 +1491,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
     if (dL_dq0) abi_out(s, s->AX, dL_dq0, B, n3, 2);
     if (dL_dv0) abi_out(s, s->AV, dL_dv0, B, n3, 2);
     if (dL_dfext) {
-      k_zero_constrained<<<nblk(len), 256, 0, s->stream>>>(s->DF, s->d_fixed, P.n, B, nullptr, nullptr);
+      pdl_launch(s, k_zero_constrained, nblk(len), 256, 0, s->DF, s->d_fixed, P.n, B, nullptr, nullptr, 0);
       LAUNCH_CHECK(s);
       abi_out(s, s->DF, dL_dfext, B, n3, 2);
     }
@@ -1536,28 +1560,28 @@ pd_status pd_eval_objective(pd_sim* s, int32_t B, const double* x, const double*
   const int64_t len = (int64_t)n3 * B;
   try {
     set_w(s, B, youngs_per_sim, true);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, x, s->X, n3, B, -1);
     LAUNCH_CHECK(s);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(y, s->Y, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, y, s->Y, n3, B, -1);
     LAUNCH_CHECK(s);
     residual(s, B, s->X, s->Y, act, P.m, s->d_nofix);
     if (grad_g) {
-      k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->G, grad_g, n3, B, n3);
+      pdl_launch(s, k_state_to_abi, nblk(len), 256, 0, s->G, grad_g, n3, B, n3);
       LAUNCH_CHECK(s);
     }
     if (g) {
       // g = sum_e E_e + sum_i m_i/(2h^2) (x_i - y_i)^2   (eq:opt)
       dots(s, B, P.m, {{s->EE, nullptr}}, g);
-      k_axpby<<<nblk(len), 256, 0, s->stream>>>(s->Q, s->X, 1.0, s->Y, nullptr, -1.0, len, B, nullptr);
+      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Q, s->X, 1.0, s->Y, nullptr, -1.0, len, B, nullptr);
       LAUNCH_CHECK(s);
       CK(cudaMemsetAsync(s->EF, 0, (int64_t)P.m * 24 * B * sizeof(double), s->stream));
-      k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Q, nullptr, s->EF, s->d_mass, s->d_inc_ptr,
+      pdl_launch(s, k_gather, nblk((int64_t)P.n * B), 256, 0, s->Q, nullptr, s->EF, s->d_mass, s->d_inc_ptr,
                                                               s->d_inc_ec, s->d_nofix, s->d_pos, P.n, B,
                                                               1.0 / (s->h * s->h), 1, s->Z, nullptr, nullptr, nullptr,
-                                                              nullptr, nullptr);
+                                                              nullptr, nullptr, 0);
       LAUNCH_CHECK(s);
       dots(s, B, n3, {{s->Q, s->Z}});
-      k_axpby<<<1, 64, 0, s->stream>>>(g, g, 1.0, s->dots, nullptr, 0.5, B, B, nullptr);
+      pdl_launch(s, k_axpby, 1, 64, 0, g, g, 1.0, s->dots, nullptr, 0.5, B, B, nullptr);
       LAUNCH_CHECK(s);
     }
     CK(cudaStreamSynchronize(s->stream));
@@ -1574,10 +1598,10 @@ pd_status pd_apply_Ainv(pd_sim* s, int32_t B, const double* rhs, double* out, vo
   const int n3 = 3 * s->plan.n;
   const int64_t len = (int64_t)n3 * B;
   try {
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(rhs, s->Rv, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, rhs, s->Rv, n3, B, -1);
     LAUNCH_CHECK(s);
     apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, nullptr);
-    k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->Z, out, n3, B, n3);
+    pdl_launch(s, k_state_to_abi, nblk(len), 256, 0, s->Z, out, n3, B, n3);
     LAUNCH_CHECK(s);
     CK(cudaStreamSynchronize(s->stream));
   } catch (CudaError& e) {
@@ -1597,22 +1621,22 @@ pd_status pd_apply_AN(pd_sim* s, int32_t B, const double* x, const double* young
   const int64_t len = (int64_t)n3 * B;
   try {
     set_w(s, B, youngs_per_sim, true);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, x, s->X, n3, B, -1);
     LAUNCH_CHECK(s);
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(p, s->Pv, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, p, s->Pv, n3, B, -1);
     LAUNCH_CHECK(s);
-    k_elem_AN<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
+    pdl_launch(s, k_elem_AN, nblk((int64_t)P.m * B * 8, 256), 256, 0, s->X, s->Pv, s->st, elem_args(s, B, act, P.m), s->EF);
     LAUNCH_CHECK(s);
     if (s->st.kappa != 0.0) {
-      k_vol<2><<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->Pv, s->st, elem_args(s, B, act, P.m),
+      pdl_launch(s, k_vol<2>, nblk((int64_t)P.m * B * 8, 256), 256, 0, s->X, s->Pv, s->st, elem_args(s, B, act, P.m),
                                                                       nullptr, s->EF, nullptr);
       LAUNCH_CHECK(s);
     }
-    k_gather<<<nblk((int64_t)P.n * B), 256, 0, s->stream>>>(s->Pv, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
+    pdl_launch(s, k_gather, nblk((int64_t)P.n * B), 256, 0, s->Pv, nullptr, s->EF, s->d_mass, s->d_inc_ptr, s->d_inc_ec,
                                                             s->d_nofix, s->d_pos, P.n, B, 1.0 / (s->h * s->h), 1, s->Q,
-                                                            nullptr, nullptr, nullptr, nullptr, nullptr);
+                                                            nullptr, nullptr, nullptr, nullptr, nullptr, 0);
     LAUNCH_CHECK(s);
-    k_state_to_abi<<<nblk(len), 256, 0, s->stream>>>(s->Q, out, n3, B, n3);
+    pdl_launch(s, k_state_to_abi, nblk(len), 256, 0, s->Q, out, n3, B, n3);
     LAUNCH_CHECK(s);
     CK(cudaStreamSynchronize(s->stream));
   } catch (CudaError& e) {
@@ -1629,9 +1653,9 @@ pd_status pd_project_rotations(pd_sim* s, int32_t B, const double* x, double* R,
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
   try {
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, x, s->X, n3, B, -1);
     LAUNCH_CHECK(s);
-    k_elem_rotations<<<nblk((int64_t)P.m * B, 128), 128, 0, s->stream>>>(s->X, s->st, s->d_hex8, P.m, B, R);
+    pdl_launch(s, k_elem_rotations, nblk((int64_t)P.m * B, 128), 128, 0, s->X, s->st, s->d_hex8, P.m, B, R);
     LAUNCH_CHECK(s);
     CK(cudaStreamSynchronize(s->stream));
   } catch (CudaError& e) {
@@ -1648,11 +1672,11 @@ pd_status pd_polar_stats(pd_sim* s, int32_t B, const double* x, int64_t* out, vo
   const int n3 = 3 * P.n;
   const int64_t len = (int64_t)n3 * B;
   try {
-    k_abi_to_state<<<nblk(len), 256, 0, s->stream>>>(x, s->X, n3, B);
+    pdl_launch(s, k_abi_to_state, nblk(len), 256, 0, x, s->X, n3, B, -1);
     LAUNCH_CHECK(s);
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(s->nactive_ll);
     CK(cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s->stream));
-    k_polar_stats<<<nblk((int64_t)P.m * B * 8, 256), 256, 0, s->stream>>>(s->X, s->st, s->d_hex8, P.m, B, acc);
+    pdl_launch(s, k_polar_stats, nblk((int64_t)P.m * B * 8, 256), 256, 0, s->X, s->st, s->d_hex8, P.m, B, acc);
     LAUNCH_CHECK(s);
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s->stream));

@@ -15,6 +15,11 @@
 #include "kernels.cuh"
 
 namespace pdb {
+// Programmatic dependent launch: every hot-loop kernel is launched with programmatic stream
+// serialisation; it waits for its predecessor grid (complete, memory visible) before its first access and then lets
+// the next launch be scheduled, so launch latency and ramp overlap the running kernel.  Without the launch attribute
+// both instructions are no-ops.
+#define PDL_ENTRY() asm volatile("griddepcontrol.wait;\n" "griddepcontrol.launch_dependents;\n" ::: "memory")
 
 // ----------------------------------------------------------------- 3x3 helpers (row-major)
 __device__ __forceinline__ double det3(const double* A) {
@@ -253,6 +258,7 @@ __device__ __forceinline__ bool polar_ns(const double (&F)[9], double (&R)[9], i
 // ----------------------------------------------------------------- layout kernels
 __global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
                                int64_t in_bstride = -1) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n3 * B) return;
   const int64_t d = i / B;
@@ -262,6 +268,7 @@ __global__ void k_abi_to_state(const double* __restrict__ in, double* __restrict
 // OUT[i] += in (ABI layout, batch stride in_bstride) on non-Dirichlet DoFs (per-step loss terms)
 __global__ void k_add_abi(double* __restrict__ out, const double* __restrict__ in, int n3, int B, int64_t in_bstride,
                           const uint8_t* __restrict__ fixed) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n3 * B) return;
   const int64_t d = i / B;
@@ -271,6 +278,7 @@ __global__ void k_add_abi(double* __restrict__ out, const double* __restrict__ i
 }
 __global__ void k_state_to_abi(const double* __restrict__ in, double* __restrict__ out, int n3, int B,
                                int64_t out_bstride) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n3 * B) return;
   const int64_t d = i / B;
@@ -288,6 +296,7 @@ struct FrameQ {
 // ABI [B][bstride] (world) -> state [n][3][B] (plane): point = positions (affine), else vectors
 __global__ void k_abi_to_state_frame(const double* __restrict__ in, double* __restrict__ out, int n, int B,
                                      int64_t bstride, FrameQ f, int point) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * B) return;
   const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
@@ -303,6 +312,7 @@ __global__ void k_abi_to_state_frame(const double* __restrict__ in, double* __re
 // state [n][3][B] (plane) -> ABI [B][bstride] (world): x = Q^T (x' + d e_z)
 __global__ void k_state_to_abi_frame(const double* __restrict__ in, double* __restrict__ out, int n, int B,
                                      int64_t bstride, FrameQ f, int point) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * B) return;
   const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
@@ -315,6 +325,7 @@ __global__ void k_state_to_abi_frame(const double* __restrict__ in, double* __re
 // OUT += Q in (vectors, ABI -> state) on non-Dirichlet nodes (per-step loss terms in plane coordinates)
 __global__ void k_add_abi_frame(double* __restrict__ out, const double* __restrict__ in, int n, int B, int64_t bstride,
                                 const uint8_t* __restrict__ fixed, FrameQ f) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * B) return;
   const int node = (int)(i / B), b = (int)(i - (int64_t)node * B);
@@ -330,6 +341,7 @@ __global__ void k_add_abi_frame(double* __restrict__ out, const double* __restri
 __global__ void k_y(const double* __restrict__ X, const double* __restrict__ V,
                     const double* __restrict__ Fext, const double* __restrict__ mass, double* __restrict__ Y,
                     int n, int B, double h, double g0, double g1, double g2) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -456,6 +468,7 @@ template <bool FIB>
 __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const double* __restrict__ X, Stencil st,
                                                                     ElemArgs ea, double* __restrict__ EF,
                                                                     double* __restrict__ EE) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   __shared__ __align__(16) double Psm[32][kPsSlot];
   dn_fill(dnt, st);
@@ -526,6 +539,7 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_elem_residual(const doub
 // fallback points.  Integer sums: exact and order-independent.
 __global__ void k_polar_stats(const double* __restrict__ X, Stencil st, const int32_t* __restrict__ hex8, int m, int B,
                               unsigned long long* __restrict__ acc) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -559,6 +573,7 @@ __global__ void k_polar_stats(const double* __restrict__ X, Stencil st, const in
 // Rotations of every quad point (diagnostic / parity hook).
 __global__ void k_elem_rotations(const double* __restrict__ X, Stencil st, const int32_t* __restrict__ hex8,
                                  int m, int B, double* __restrict__ Rout) {
+  PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= (int64_t)m * B) return;
   const int e = (int)(tid / B), b = (int)(tid - (int64_t)e * B);
@@ -706,6 +721,7 @@ constexpr int kJC = 19;  // cached doubles per quad point: R (9), Mi (6), n (3),
 // JC[k * nq + tid], tid = (e*B + b)*8 + q.
 __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, Stencil st, ElemArgs ea,
                                                   double* __restrict__ JC) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -737,6 +753,7 @@ __global__ void __launch_bounds__(256) k_elem_jac(const double* __restrict__ X, 
 // K4 with cached Jacobian data: A_N p element term from dF = G_q p_e only (no polar per product).
 __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict__ Pv, Stencil st, ElemArgs ea,
                                                         const double* __restrict__ JC, double* __restrict__ EF) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -770,6 +787,7 @@ __global__ void __launch_bounds__(256) k_elem_AN_cached(const double* __restrict
 
 __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, const double* __restrict__ Pv,
                                                  Stencil st, ElemArgs ea, double* __restrict__ EF) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -802,6 +820,7 @@ __global__ void __launch_bounds__(256) k_elem_AN(const double* __restrict__ X, c
 __global__ void __launch_bounds__(256) k_elem_param(const double* __restrict__ X, const double* __restrict__ U,
                                                     Stencil st, ElemArgs ea, double* __restrict__ DW,
                                                     double* __restrict__ DR) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   dn_fill(dnt, st);
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1008,6 +1027,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_vol(const double* __restrict__ X, const double* __restrict__ Pv, Stencil st,
                                              ElemArgs ea, double* __restrict__ JC, double* __restrict__ EF,
                                              double* __restrict__ EE) {
+  PDL_ENTRY();
   __shared__ DNTab dnt;
   __shared__ __align__(16) double Psm[32][kPsSlot];
   dn_fill(dnt, st);
@@ -1085,6 +1105,7 @@ __global__ void k_gather(const double* __restrict__ X, const double* __restrict_
                          double* __restrict__ G, double* __restrict__ W, double* __restrict__ RHS,
                          const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
                          double* __restrict__ LAM, int pin_all = 0) {
+  PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= (int64_t)n * B) return;
   const int node = (int)(tid / B), b = (int)(tid - (int64_t)node * B);
@@ -1132,6 +1153,7 @@ __global__ void k_gather(const double* __restrict__ X, const double* __restrict_
 // state (free nodes) -> permuted solve vector
 __global__ void k_to_solve(const double* __restrict__ Xs, const int32_t* __restrict__ node_of_pos, int nfree, int B,
                            double* __restrict__ S) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int R = 3 * B;
   if (i >= (int64_t)nfree * R) return;
@@ -1144,6 +1166,7 @@ __global__ void k_to_solve(const double* __restrict__ Xs, const int32_t* __restr
 __global__ void k_from_solve(const double* __restrict__ S, const int32_t* __restrict__ pos_of_node, int n, int B,
                              const double* __restrict__ alpha, double alpha_c, double beta,
                              const int32_t* __restrict__ active, double* __restrict__ OUT) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -1756,6 +1779,7 @@ __global__ void __launch_bounds__(1024) k_contact_flist(const uint8_t* __restric
                                                         int c, int B, const int32_t* __restrict__ sel,
                                                         int32_t* __restrict__ flist, int32_t* __restrict__ fpos,
                                                         int32_t* __restrict__ kcount) {
+  PDL_ENTRY();
   const int b = blockIdx.x;
   if (sel && !sel[b]) return;
   __shared__ int32_t warp_tot[32];
@@ -1792,6 +1816,7 @@ __global__ void __launch_bounds__(1024) k_contact_flist(const uint8_t* __restric
 __global__ void k_contact_gather_S(const double* __restrict__ S, int c, const int32_t* __restrict__ sel,
                                    const int32_t* __restrict__ flist, const int32_t* __restrict__ kcount,
                                    double* __restrict__ Q) {
+  PDL_ENTRY();
   const int b = blockIdx.z;
   if (sel && !sel[b]) return;
   const int k = kcount[b];
@@ -1805,6 +1830,7 @@ __global__ void k_contact_gather_S(const double* __restrict__ S, int c, const in
 // C = Q[:, K] copied to Cb (k x kGJ), M = C Pinv into Mb, Rw = Q[K, :] copied to Rb (kGJ x k).
 __global__ void __launch_bounds__(256) k_gj_pivot(double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
                                                   const int32_t* __restrict__ kcount, double* __restrict__ PI) {
+  PDL_ENTRY();
   const int b = blockIdx.x;
   if (sel && !sel[b]) return;
   const int k = kcount[b];
@@ -1848,6 +1874,7 @@ __global__ void __launch_bounds__(256) k_gj_pivot(double* __restrict__ Q, int c,
 __global__ void __launch_bounds__(256) k_gj_panel(const double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
                                                   const int32_t* __restrict__ kcount, const double* __restrict__ PI,
                                                   double* __restrict__ Cb, double* __restrict__ Mb, double* __restrict__ Rb) {
+  PDL_ENTRY();
   const int b = blockIdx.y;
   if (sel && !sel[b]) return;
   const int k = kcount[b];
@@ -1882,6 +1909,7 @@ __global__ void __launch_bounds__(256) k_gj_panel(const double* __restrict__ Q, 
 __global__ void __launch_bounds__(256) k_gj_update(double* __restrict__ Q, int c, int kb, const int32_t* __restrict__ sel,
                                                    const int32_t* __restrict__ kcount, const double* __restrict__ PI,
                                                    const double* __restrict__ Mb, const double* __restrict__ Rb) {
+  PDL_ENTRY();
   const int b = blockIdx.z;
   if (sel && !sel[b]) return;
   const int k = kcount[b];
@@ -1932,6 +1960,7 @@ __global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ 
                                                      const int32_t* __restrict__ kcount, const int32_t* __restrict__ flist,
                                                      const int32_t* __restrict__ fpos, const double* __restrict__ Q,
                                                      double* __restrict__ Xroot) {
+  PDL_ENTRY();
   // blockIdx.y = a*B + b over the pinned axes (frictionless: only z; sticky: x, y, z -> gridDim.y = 3B)
   const int b = blockIdx.y % B;
   const int ax = gridDim.y == (unsigned)B ? 2 : (int)(blockIdx.y / B);
@@ -1959,6 +1988,7 @@ __global__ void __launch_bounds__(256) k_contact_fix(const double* __restrict__ 
 __global__ void k_contact_restart(double* __restrict__ X, const double* __restrict__ Xp, int n, int B,
                                   const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
                                   const int32_t* __restrict__ oact, int warm, int pin_all = 0) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -1977,6 +2007,7 @@ __global__ void k_contact_predict(const double* __restrict__ X, const double* __
                                   const int32_t* __restrict__ cand_node, int c, int B, double eps_phi,
                                   const uint8_t* __restrict__ PIN, const int32_t* __restrict__ oact,
                                   uint8_t* __restrict__ NEWPIN, int32_t* __restrict__ changed) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)c * B) return;
   const int j = (int)(i / B), b = (int)(i - (int64_t)j * B);
@@ -1993,6 +2024,7 @@ __global__ void k_contact_outer(const int32_t* __restrict__ oact, const int32_t*
                                 const uint8_t* __restrict__ NEWPIN, uint8_t* __restrict__ PIN, int c, int B,
                                 int outer, int max_outer, int32_t* __restrict__ onext,
                                 int32_t* __restrict__ outer_out, int32_t* __restrict__ flag_out) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)c * B) return;
   const int j = (int)(i / B), b = (int)(i - (int64_t)j * B);
@@ -2047,6 +2079,7 @@ __device__ __forceinline__ void red_store(double (*red)[kRedJ][kRedS], int np, c
 }
 // partial[c][b] = sum over chunk c of u*v (up to 3 pairs; v = null means 1)
 __global__ void k_dot_partial(DotArgs da, int64_t len, int B, double* __restrict__ partial) {
+  PDL_ENTRY();
   __shared__ double red[3][kRedJ][kRedS];
   const RedLane r = red_lane(B, blockIdx.y);
   const int c = blockIdx.x;
@@ -2086,6 +2119,7 @@ __global__ void k_dot_partial(DotArgs da, int64_t len, int B, double* __restrict
 // in flight together), then a fixed xor tree per warp and the 4 warp sums in warp order (deterministic)
 __global__ void __launch_bounds__(128) k_dot_final(const double* __restrict__ partial, int nchunk, int B, int npairs,
                                                    double* __restrict__ out, int accumulate = 0) {
+  PDL_ENTRY();
   const int i = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (i >= npairs * B) return;
   const int p = i / B, b = i - p * B;
@@ -2112,6 +2146,7 @@ __global__ void __launch_bounds__(128) k_dot_final(const double* __restrict__ pa
 }
 // sum over elements of E[e][b] (deterministic) -> out[b] (+= if accumulate)
 __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* __restrict__ out, int accumulate) {
+  PDL_ENTRY();
   extern __shared__ double red[];
   const int b = blockIdx.x;
   double s = 0;
@@ -2134,6 +2169,7 @@ __global__ void k_sum_elems(const double* __restrict__ E, int m, int B, double* 
 __global__ void k_inertia_partial(const double* __restrict__ X, const double* __restrict__ Y,
                                   const double* __restrict__ mass, double inv_h2, int64_t len, int B,
                                   double* __restrict__ partial, const double* __restrict__ G = nullptr) {
+  PDL_ENTRY();
   __shared__ double red[2][kRedJ][kRedS];
   const RedLane r = red_lane(B, blockIdx.y);
   const int c = blockIdx.x;
@@ -2155,6 +2191,7 @@ __global__ void k_inertia_partial(const double* __restrict__ X, const double* __
 // f[b] = 0.5 * inert[b] + esum[b]
 __global__ void k_obj_combine(const double* __restrict__ inert, const double* __restrict__ esum, double* __restrict__ f,
                               int B) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) f[b] = 0.5 * inert[b] + esum[b];
 }
@@ -2165,6 +2202,7 @@ __global__ void k_obj_combine(const double* __restrict__ inert, const double* __
 __global__ void k_lbfgs_axpy(double* __restrict__ Y, const double* __restrict__ V, const double* __restrict__ rho,
                              const double* __restrict__ dot, double* __restrict__ aj, int mode, int64_t len, int B,
                              const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2188,6 +2226,7 @@ __global__ void k_ls_accept(const double* __restrict__ f, double* __restrict__ f
                             const double* __restrict__ g2, const double* __restrict__ gn2, double* __restrict__ alpha,
                             int32_t* __restrict__ ls_active, int trial, int max_trial, int32_t* __restrict__ nactive,
                             int32_t* __restrict__ ls_flag, int B) {
+  PDL_ENTRY();
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -2213,6 +2252,7 @@ __global__ void k_ls_accept(const double* __restrict__ f, double* __restrict__ f
 // rho = 1/(s^T y) if the curvature pair is positive, else 0 (pair ignored)
 __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ rho, const int32_t* __restrict__ active,
                             int B) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
   rho[b] = sy[b] > 0.0 ? 1.0 / sy[b] : 0.0;
@@ -2231,6 +2271,7 @@ __global__ void k_lbfgs_rho(const double* __restrict__ sy, double* __restrict__ 
 __global__ void k_mdot_partial(const double* __restrict__ u, const double* __restrict__ Vbase, int64_t vstride,
                                int nv, int64_t len, int B, double* __restrict__ partial,
                                const double* __restrict__ u2 = nullptr, const double* __restrict__ V2base = nullptr) {
+  PDL_ENTRY();
   __shared__ double red[1][kRedJ][kRedS];
   const RedLane r = red_lane(B, blockIdx.z);
   const int jp = blockIdx.y;
@@ -2266,6 +2307,7 @@ __device__ __forceinline__ int lb_slot(int iter, int k, int m) { return ((iter -
 __global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __restrict__ Gm, const double* __restrict__ rho,
                               double* __restrict__ alpha, int m, int hist, int iter, int B,
                               const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   __shared__ double g[kMaxHist * kMaxHist], sv[kMaxHist], rv[kMaxHist], av[kMaxHist];
   const int b = blockIdx.x, lane = threadIdx.x;
   if (!active[b]) return;
@@ -2295,6 +2337,7 @@ __global__ void k_lbfgs_alpha(const double* __restrict__ sg, const double* __res
 __global__ void k_lbfgs_beta(const double* __restrict__ yr, const double* __restrict__ Gm, const double* __restrict__ rho,
                              const double* __restrict__ alpha, double* __restrict__ beta, int m, int hist, int iter,
                              int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   __shared__ double g[kMaxHist * kMaxHist], yv[kMaxHist], rv[kMaxHist], av[kMaxHist], bv[kMaxHist];
   const int b = blockIdx.x, lane = threadIdx.x;
   if (!active[b]) return;
@@ -2327,6 +2370,7 @@ __global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ 
                              const double* __restrict__ Vbase, int64_t vstride, const double* __restrict__ c1,
                              const double* __restrict__ c2, int nv, int64_t len, int B,
                              const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2343,6 +2387,7 @@ __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, 
                              const double* __restrict__ db, int sl, int m, int nv, int B,
                              const int32_t* __restrict__ active, double* __restrict__ f, const double* __restrict__ fn,
                              double* __restrict__ gg, const double* __restrict__ gn2) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
   for (int j = 0; j < nv; ++j) {
@@ -2361,6 +2406,7 @@ __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, 
 __global__ void k_lbfgs_commit(double* __restrict__ S, double* __restrict__ Yv, double* __restrict__ X,
                                double* __restrict__ G, const double* __restrict__ Xn, const double* __restrict__ Gn,
                                int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2375,6 +2421,7 @@ __global__ void k_lbfgs_commit(double* __restrict__ S, double* __restrict__ Yv, 
 // Newton-PCG forward (accel_fwd = 2): commit of an accepted trial, X <- Xn, G <- Gn (state vectors, masked)
 __global__ void k_newton_commit(double* __restrict__ X, double* __restrict__ G, const double* __restrict__ Xn,
                                 const double* __restrict__ Gn, int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2385,6 +2432,7 @@ __global__ void k_newton_commit(double* __restrict__ X, double* __restrict__ G, 
 // ... and its per-sim scalars: f <- f_new, |grad g|^2 <- that of the trial
 __global__ void k_newton_commit_s(double* __restrict__ f, const double* __restrict__ fn, double* __restrict__ g2,
                                   const double* __restrict__ gn2, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
   f[b] = fn[b];
@@ -2393,12 +2441,14 @@ __global__ void k_newton_commit_s(double* __restrict__ f, const double* __restri
 // Truncated CG on a non-convex Hessian: a sim whose search direction has p^T A_N p <= 0 stops its CG (its
 // direction so far is kept; a zero direction falls back to the PD step below).
 __global__ void k_negcurv(const double* __restrict__ pq, int32_t* __restrict__ active, int B) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && active[b] && !(pq[b] > 0.0)) active[b] = 0;
 }
 // Descent guard: where <grad g, D> >= 0 (not a descent direction), D = the PD direction -A^{-1} grad g (Z0)
 __global__ void k_descent_guard(double* __restrict__ D, const double* __restrict__ Z0, const double* __restrict__ gtd,
                                 int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2407,6 +2457,7 @@ __global__ void k_descent_guard(double* __restrict__ D, const double* __restrict
 
 // v[b] = c (per-sim scalar fill)
 __global__ void k_fill_double(double* __restrict__ v, double c, int B) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) v[b] = c;
 }
@@ -2414,6 +2465,7 @@ __global__ void k_fill_double(double* __restrict__ v, double c, int B) {
 // masked copy of per-sim scalars
 __global__ void k_copy_masked(double* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ active,
                               int B) {
+  PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && (!active || active[b])) dst[b] = src[b];
 }
@@ -2428,6 +2480,7 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
                             int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base,
                             double* __restrict__ alpha = nullptr, int32_t* __restrict__ ls_act = nullptr,
                             int32_t* __restrict__ nnear = nullptr) {
+  PDL_ENTRY();
   __shared__ int cnt, near;
   if (threadIdx.x == 0) cnt = near = 0;
   __syncthreads();
@@ -2464,6 +2517,7 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
 // v = (x - xprev)/h
 __global__ void k_velocity(const double* __restrict__ X, const double* __restrict__ Xp, double* __restrict__ V,
                            int64_t len, double inv_h) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < len) V[i] = (X[i] - Xp[i]) * inv_h;
 }
@@ -2471,6 +2525,7 @@ __global__ void k_velocity(const double* __restrict__ X, const double* __restric
 // generic per-sim axpy on state vectors: Y[i] = a*X[i] + c[b]*cs*Z[i] (+ masks)
 __global__ void k_axpby(double* __restrict__ Y, const double* __restrict__ X, double a, const double* __restrict__ Z,
                         const double* __restrict__ c, double cs, int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2483,6 +2538,7 @@ __global__ void k_axpby(double* __restrict__ Y, const double* __restrict__ X, do
 __global__ void k_zero_constrained(double* __restrict__ Y, const uint8_t* __restrict__ fixed, int n, int B,
                                    const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN,
                                    int pin_all = 0) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -2498,6 +2554,7 @@ __global__ void k_zero_constrained(double* __restrict__ Y, const uint8_t* __rest
 __global__ void k_sticky_extra(double* __restrict__ EX, const double* __restrict__ AX, const double* __restrict__ AV,
                                const double* __restrict__ ANu, double inv_h, int n, int B,
                                const int32_t* __restrict__ cand_of_node, const uint8_t* __restrict__ PIN) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int64_t d = i / B;
@@ -2514,6 +2571,7 @@ __global__ void k_sticky_extra(double* __restrict__ EX, const double* __restrict
 __global__ void k_pcg_update(double* __restrict__ U, double* __restrict__ Rv, const double* __restrict__ P,
                              const double* __restrict__ Q, const double* __restrict__ rz, const double* __restrict__ pq,
                              int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2525,6 +2583,7 @@ __global__ void k_pcg_update(double* __restrict__ U, double* __restrict__ Rv, co
 }
 __global__ void k_pcg_dir(double* __restrict__ P, const double* __restrict__ Z, const double* __restrict__ rz_new,
                           const double* __restrict__ rz, int64_t len, int B, const int32_t* __restrict__ active) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
@@ -2538,6 +2597,7 @@ __global__ void k_adj_check(const double* __restrict__ rr, const double* __restr
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out, int32_t* __restrict__ nactive,
                             double* __restrict__ rz = nullptr, const double* __restrict__ rz_new = nullptr) {
+  PDL_ENTRY();
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -2562,6 +2622,7 @@ __global__ void k_adj_check(const double* __restrict__ rr, const double* __restr
 // a_x = (M/h^2) u - a_v/h ; a_v = (M/h) u ; zero on fixed nodes  (eq:pre_adjoint)
 __global__ void k_adj_state(const double* __restrict__ U, const double* __restrict__ mass, const uint8_t* __restrict__ fixed,
                             double* __restrict__ AX, double* __restrict__ AV, int n, int B, double h) {
+  PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)3 * n * B) return;
   const int node = (int)(i / B / 3);
