@@ -4,6 +4,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: per-phase ranges for nsys / ncu --nvtx (no-ops without a tool)
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -56,6 +57,10 @@ struct pd_sim {
   int k3_mma = 1;   // K3 item products on the fp64 tensor cores (1) or the FMA pipe (0, env PD_K3_MMA=0)
   int nsm = 148;     // SMs of the device
   int k3_nbuf = 2;  // K3 item ring depth (2..4, env PD_K3_NBUF)
+  bool poll = true;  // iteration control by polled host flags (env PD_POLL=0: D2H copy + stream synchronisation)
+  bool lb_gamma = false;  // per-sim scaling gamma_b of H0 = gamma A^{-1} in the L-BFGS forward (env PD_LBFGS_GAMMA)
+  double* gamma = nullptr;
+  bool fuse = true;  // layout/trial passes fused into their producers (env PD_FUSE=0: separate passes, same bits)
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
   double* Spart = nullptr;  // partial rows of the K3 sweeps
@@ -78,7 +83,8 @@ struct pd_sim {
   const double* w_cur = nullptr;  // the weights the element kernels read (w_sim or w_diag)
   int32_t *active, *nactive, *it_buf, *flag_buf;
   double* res_buf;
-  int32_t* h_nactive = nullptr;  // pinned
+  int32_t* h_nactive = nullptr;  // pinned, device-mapped: [0:3) the loop counters, [3] the published sequence number
+  int flag_seq = 0;              // last sequence number handed to a check kernel (poll_flags waits for it)
   // contact K5
   int nc = 0, csup_first = 0;
   bool pins_live = false;          // the solve applies the constrained root block
@@ -222,6 +228,9 @@ struct ProfScope {
 // resolve recorded pairs (the stream must have been synchronised)
 void prof_flush(pd_sim* s) {
   if (!s->opt.profile) return;
+  // (after a poll the stream has passed the check kernel, hence every event recorded before it; the wait below
+  // returns at once and only covers the driver's bookkeeping of the last event)
+  if (!s->ev_open.empty()) CK(cudaEventSynchronize(s->ev_pool[s->ev_open.back().second + 1]));
   for (auto& pr : s->ev_open) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, s->ev_pool[pr.second], s->ev_pool[pr.second + 1]));
@@ -474,12 +483,15 @@ void solve(pd_sim* s, int B) {
 }
 
 // state vector V (free nodes) -> A^{-1} V -> OUT = beta OUT + alpha_c*alpha[b]*sol (masked)
+// (Vin = nullptr: the right-hand side is already in S0 in the solve layout)
 void apply_Ainv(pd_sim* s, int B, const double* Vin, double* OUT, const double* alpha, double alpha_c, double beta,
                 const int32_t* active) {
   const HostPlan& P = s->plan;
   ProfScope ps(s, 2);
-  pdl_launch(s, k_to_solve, nblk((int64_t)P.nfree * 3 * B), 256, 0, Vin, s->d_nodepos, P.nfree, B, s->S0);
-  LAUNCH_CHECK(s);
+  if (Vin) {
+    pdl_launch(s, k_to_solve, nblk((int64_t)P.nfree * 3 * B), 256, 0, Vin, s->d_nodepos, P.nfree, B, s->S0);
+    LAUNCH_CHECK(s);
+  }
   solve(s, B);
   pdl_launch(s, k_from_solve, nblk((int64_t)3 * P.n * B), 256, 0, s->S0, s->d_pos, P.n, B, alpha, alpha_c, beta,
                                                                    active, OUT);
@@ -559,20 +571,56 @@ void set_w(pd_sim* s, int B, const double* youngs_per_sim, bool diag = false) {
   s->w_cur = w;
 }
 
-// the three counters in one copy: [0] the last k_*_check / k_ls_accept count, [1] the deferred convergence
-// count, [2] running sims already within 16 tol
-void read_nactive3(pd_sim* s, int* a, int* b, int* c) {
-  CK(cudaMemcpyAsync(s->h_nactive, s->nactive, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaStreamSynchronize(s->stream));
+// Iteration control without a stream synchronisation: the check kernel whose result the host
+// needs next is handed a fresh sequence number (flag_args) and publishes the three loop counters
+// ([0] the last k_ls_accept / k_adj_check / plain-PD k_fwd_check count, [1] the L-BFGS / Newton running count,
+// [2] running sims already within 16 tol) into the mapped pinned triple followed by that number (kernels.cu
+// publish3); the host spins on the number (wait_flags).  The GPU is idle only for the PCIe write and the next
+// launch, not for a D2H copy operation plus the wake-up of a blocked thread.  PD_POLL=0 restores the copy + sync.
+struct FlagArgs {
+  int32_t* hflag;
+  const int32_t* nact3;
+  int seq;
+};
+// arguments for a check kernel whose counters the host reads next (want = false: nothing is published)
+FlagArgs flag_args(pd_sim* s, bool want = true) {
+  if (!want || !s->poll) return {nullptr, nullptr, 0};
+  if (++s->flag_seq == 0x7fffffff) s->flag_seq = 1;
+  return {s->h_nactive, s->nactive, s->flag_seq};
+}
+void wait_flags(pd_sim* s, int nread) {
+  if (!s->poll) {
+    CK(cudaMemcpyAsync(s->h_nactive, s->nactive, nread * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    prof_flush(s);
+    return;
+  }
+  volatile int32_t* h = s->h_nactive;
+  const int32_t seq = s->flag_seq;
+  for (uint64_t spin = 1; h[3] != seq; ++spin) {
+    if ((spin & 0x3fff) == 0) {  // a failed kernel never publishes: surface its error instead of spinning
+      const cudaError_t e = cudaStreamQuery(s->stream);
+      if (e == cudaSuccess) {
+        if (h[3] != seq) throw CudaError("iteration control: the check kernel finished without publishing");
+      } else if (e != cudaErrorNotReady) {
+        throw CudaError(std::string("iteration control: ") + cudaGetErrorString(e));
+      }
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   prof_flush(s);
+}
+void read_nactive3(pd_sim* s, int* a, int* b, int* c) {
+  wait_flags(s, 3);
   *a = s->h_nactive[0];
   *b = s->h_nactive[1];
   *c = s->h_nactive[2];
 }
 int read_nactive(pd_sim* s) {
-  CK(cudaMemcpyAsync(s->h_nactive, s->nactive, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  prof_flush(s);
+  wait_flags(s, 1);
   return *s->h_nactive;
 }
 
@@ -692,11 +740,13 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     for (int j = 0; j < hist; ++j) {
       mdot(s, B, LSs(j), s->LY, hist, s->lb_da, LYs(j), s->LS);
       pdl_launch(s, k_gram_store, nblk(B, 64), 64, 0, s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)hist * B, j, m,
-                                                      hist, B, s->active, nullptr, nullptr, nullptr, nullptr);
+                                                      hist, B, s->active, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                      nullptr, nullptr);
       LAUNCH_CHECK(s);
     }
   }
   int gi = gi0;
+  const bool fuse = s->fuse;
   bool done = false, check_now = true;  // the first check of a solve is read immediately
   for (int iter = 0;; ++iter, ++gi) {
     // convergence check; also alpha = 1 and ls_act = active for the coming line search
@@ -704,10 +754,11 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     // host sync per iteration instead of two; were every sim to converge meanwhile, the direction and trial
     // launched after the check are fully masked and the loop ends at that sync).  Once a running sim is within
     // 16 tol the check is read immediately, so no masked iteration is spent at the end of a solve.
+    const FlagArgs fc = flag_args(s, check_now && iter < s->opt.max_iter_fwd);
     pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
                                           s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
-                                          s->ls_act, s->nactive + 2);
+                                          s->ls_act, s->nactive + 2, fc.hflag, fc.nact3, fc.seq);
     LAUNCH_CHECK(s);
     if (iter >= s->opt.max_iter_fwd) break;
     if (check_now) {
@@ -716,25 +767,35 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
       if (running == 0) break;
     }
     // D = -H grad g, compact two-loop (k_lbfgs_alpha / k_lbfgs_beta): 2 multi-dots + 2 multi-axpys + A^{-1}
+    bool trial0_done = false;
     if (hist > 0) {
       mdot(s, B, s->G, s->LS, hist, s->lb_sg);
       pdl_launch(s, k_lbfgs_alpha, B, 32, 0, s->lb_sg, s->lb_G, s->rho_h, s->aj_h, m, hist, gi, B, s->active);
       LAUNCH_CHECK(s);
-      pdl_launch(s, k_multi_axpy, nblk(len), 256, 0, s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
-                                                     s->active);  // q = g - sum alpha_j y_j
+      // q = g - sum alpha_j y_j, written in the solve layout (fused k_to_solve; PD_FUSE=0: two passes)
+      if (fuse)
+        pdl_launch(s, k_multi_axpy_solve, nblk((int64_t)P.nfree * 3 * B), 256, 0, s->S0, s->G, 1.0, -1.0, s->LY, len,
+                                                             s->aj_h, nullptr, hist, P.nfree, B, s->active, s->d_nodepos);
+      else
+        pdl_launch(s, k_multi_axpy, nblk(len), 256, 0, s->Dv, s->G, 1.0, -1.0, s->LY, len, s->aj_h, nullptr, hist, len, B,
+                                                       s->active, nullptr, nullptr, nullptr);
       LAUNCH_CHECK(s);
     } else {
       CK(cudaMemcpyAsync(s->Dv, s->G, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
     }
-    apply_Ainv(s, B, s->Dv, s->Dv, nullptr, 1.0, 0.0, s->active);  // r0 = H0 q = A^{-1} q
+    // r0 = H0 q = A^{-1} q
+    apply_Ainv(s, B, (hist > 0 && fuse) ? nullptr : s->Dv, s->Dv, s->lb_gamma ? s->gamma : nullptr, 1.0, 0.0, s->active);
     if (hist > 0) {
       mdot(s, B, s->Dv, s->LY, hist, s->lb_yr);
       pdl_launch(s, k_lbfgs_beta, B, 32, 0, s->lb_yr, s->lb_G, s->rho_h, s->aj_h, s->lb_beta, m, hist, gi, B,
                                                       s->active);
       LAUNCH_CHECK(s);
+      // d = -(r0 + sum (alpha_j - beta_j) s_j); fused: also the first trial point x + alpha d (alpha = 1, ls_act =
+      // active from k_fwd_check)
       pdl_launch(s, k_multi_axpy, nblk(len), 256, 0, s->Dv, s->Dv, -1.0, 1.0, s->LS, len, s->aj_h, s->lb_beta, hist, len,
-                                                     B, s->active);  // d = -(r0 + sum (alpha_j - beta_j) s_j)
+                                                     B, s->active, fuse ? s->Xn : nullptr, s->X, s->alpha_ls);
       LAUNCH_CHECK(s);
+      trial0_done = fuse;
     } else {
       pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Dv, s->Dv, -1.0, nullptr, nullptr, 0.0, len, B, s->active);
       LAUNCH_CHECK(s);
@@ -742,11 +803,15 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     dots(s, B, n3, {{s->G, s->Dv}}, s->gtd);
     // Armijo backtracking from alpha = 1 (set by k_fwd_check); g_new and the decision in k_ls_accept
     for (int trial = 0;; ++trial) {
-      pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
-      LAUNCH_CHECK(s);
+      if (!(trial == 0 && trial0_done)) {
+        pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
+        LAUNCH_CHECK(s);
+      }
       eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
+      const FlagArgs fl = flag_args(s);
       pdl_launch(s, k_ls_accept, 1, 256, 0, s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
-                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
+                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B, fl.hflag, fl.nact3,
+                                            fl.seq);
       LAUNCH_CHECK(s);
       int searching = 0, running = 1, nr = 0;
       read_nactive3(s, &searching, &running, &nr);
@@ -767,8 +832,10 @@ void inner_lbfgs(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, c
     LAUNCH_CHECK(s);
     const int nv = std::min(hist + 1, m);  // valid slots after this store are [0, nv)
     mdot(s, B, LSs(slot), s->LY, nv, s->lb_da, LYs(slot), s->LS);  // s_new^T y_j | y_new^T s_j
+    const bool set_gamma = s->lb_gamma && hist == 0;  // (first step of a solve: d = -gamma A^{-1} grad g exactly)
     pdl_launch(s, k_gram_store, nblk(B, 64), 64, 0, s->lb_G, s->rho_h, s->lb_da, s->lb_da + (int64_t)nv * B, slot, m, nv,
-                                                    B, s->active, s->fcur, s->fnew, s->dots, gn2);
+                                                    B, s->active, s->fcur, s->fnew, s->dots, gn2,
+                                                    set_gamma ? s->gamma : nullptr, s->alpha_ls, s->gtd);
     LAUNCH_CHECK(s);
     hist = nv;
   }
@@ -793,10 +860,11 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
   dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
   double* const gn2 = s->inert + B;
   for (int iter = 0;; ++iter) {
+    const FlagArgs fc = flag_args(s, iter < s->opt.max_iter_fwd);
     pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, s->opt.tol_fwd, iter, 0, s->opt.max_iter_fwd, s->active,
                                           s->st_iters_f + (int64_t)i * B, s->st_res_f + (int64_t)i * B,
                                           s->st_flag_f + (int64_t)i * B, s->nactive + 1, it_base, s->alpha_ls,
-                                          s->ls_act, s->nactive + 2);
+                                          s->ls_act, s->nactive + 2, fc.hflag, fc.nact3, fc.seq);
     LAUNCH_CHECK(s);
     if (iter >= s->opt.max_iter_fwd) break;
     {
@@ -828,16 +896,18 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
     for (int it = 0;; ++it) {
       const bool fused = it > 0;
       if (!fused) dots(s, B, n3, {{s->Rv, s->Rv}}, s->dots + 2 * B);
+      const FlagArgs fa = flag_args(s, it < s->opt.max_iter_adj);
       pdl_launch(s, k_adj_check, 1, 256, 0, s->dots + 2 * B, s->bb, B, s->newton_eta, it, s->opt.max_iter_adj, s->pact,
                                             s->nt_iters, s->nt_res, s->nt_flag, s->nactive, fused ? s->rz : nullptr,
-                                            s->dots + 3 * B);
+                                            s->dots + 3 * B, fa.hflag, fa.nact3, fa.seq);
       LAUNCH_CHECK(s);
       if (it >= s->opt.max_iter_adj || read_nactive(s) == 0) break;
       apply_AN(s, B, s->X, s->Pv, s->Q, act_i, act_bs, s->JC);
       dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + 3 * B);
       pdl_launch(s, k_negcurv, nblk(B, 64), 64, 0, s->dots + 3 * B, s->pact, B);
       LAUNCH_CHECK(s);
-      pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->Dv, s->Rv, s->Pv, s->Q, s->rz, s->dots + 3 * B, len, B, s->pact);
+      pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->Dv, s->Rv, s->Pv, s->Q, s->rz, s->dots + 3 * B, len, B, s->pact,
+                                                     nullptr, nullptr);
       LAUNCH_CHECK(s);
       apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->pact);
       dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + 3 * B);  // rz_new | |r|^2
@@ -855,8 +925,10 @@ void inner_newton(pd_sim* s, int B, int i, const double* act_i, int64_t act_bs, 
       pdl_launch(s, k_axpby, nblk(len), 256, 0, s->Xn, s->X, 1.0, s->Dv, s->alpha_ls, 1.0, len, B, s->ls_act);
       LAUNCH_CHECK(s);
       eval_f(s, B, s->Xn, s->Gn, nullptr, act_i, act_bs, true);
+      const FlagArgs fl = flag_args(s);
       pdl_launch(s, k_ls_accept, 1, 256, 0, s->fcur, s->fnew, s->inert, s->esum, s->gtd, s->dots, gn2, s->alpha_ls,
-                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B);
+                                            s->ls_act, trial, max_trial, s->nactive, s->ls_flag, B, fl.hflag, fl.nact3,
+                                            fl.seq);
       LAUNCH_CHECK(s);
       int searching = 0, running = 1, nr = 0;
       read_nactive3(s, &searching, &running, &nr);
@@ -1026,6 +1098,9 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     };
     if (const char* e = std::getenv("PD_K3_MMA")) s->k3_mma = std::atoi(e) ? 1 : 0;
     if (const char* e = std::getenv("PD_K3_NBUF")) s->k3_nbuf = std::min(4, std::max(2, std::atoi(e)));
+    if (const char* e = std::getenv("PD_POLL")) s->poll = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PD_FUSE")) s->fuse = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PD_LBFGS_GAMMA")) s->lb_gamma = std::atoi(e) != 0;
     auto up_sweep4 = [&](const HostPlan::Sweep4& S, Sweep4Dev& d) {
       d.A = s->upload(S.A);
       d.krow = s->upload(S.krow);
@@ -1089,7 +1164,8 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     s->st_res_a = s->alloc<double>(TB);
     s->traj = s->alloc<double>((int64_t)(s->Tmax + 1) * n3B);
     s->act = s->w_m != 0.0 ? s->alloc<double>((int64_t)s->Bmax * s->Tmax * P.m) : nullptr;
-    CK(cudaMallocHost(&s->h_nactive, 3 * sizeof(int32_t)));
+    CK(cudaHostAlloc(&s->h_nactive, 4 * sizeof(int32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(s->h_nactive, 0, 4 * sizeof(int32_t));
     CK(cudaMallocHost(&s->h_small, 2 * s->Bmax * sizeof(int32_t)));
     if (s->opt.accel_fwd) {
       s->nhist = 4;  // L-BFGS memory (env PD_LBFGS_M, 1..16; 4 measured fastest)
@@ -1100,6 +1176,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
       s->Xn = s->alloc<double>(n3B);
       s->Gn = s->alloc<double>(n3B);
       s->rho_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
+      s->gamma = s->alloc<double>(s->Bmax);
       s->aj_h = s->alloc<double>((int64_t)s->nhist * s->Bmax);
       double** sc[] = {&s->fcur, &s->fnew, &s->alpha_ls, &s->gtd, &s->g2, &s->gn2, &s->inert, &s->esum, &s->dtmp};
       for (double** p : sc) *p = s->alloc<double>(2 * s->Bmax);  // inert: [inertia | |grad g|^2]
@@ -1203,6 +1280,11 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
   Nvtx nv_fwd("pd_forward");
   try {
     set_w(s, B, youngs_per_sim);
+    if (s->gamma) {  // H0 scaling of the L-BFGS forward starts at 1 (kept across the steps of this forward)
+      const std::vector<double> ones(B, 1.0);
+      CK(cudaMemcpyAsync(s->gamma, ones.data(), B * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+      CK(cudaStreamSynchronize(s->stream));
+    }
     abi_in(s, q0, s->X, B, n3, 1);
     abi_in(s, v0, s->V, B, n3, 2);
     if (f_ext && !f_ext_step_stride) abi_in(s, f_ext, s->Fext, B, n3, 2);
@@ -1259,10 +1341,13 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
           for (int iter = 0;; ++iter) {
             residual(s, B, s->X, s->Y, act_i, act_bs, s->d_fixed);
             dots(s, B, n3, {{s->G, s->G}, {s->W, s->W}});
+            const FlagArgs fc = flag_args(s, s->opt.fixed_iter <= 0 && iter < s->opt.max_iter_fwd &&
+                                                 iter % s->opt.check_every == 0);
             pdl_launch(s, k_fwd_check, 1, 256, 0, s->dots, B, tol, iter, s->opt.fixed_iter,
                                                            s->opt.max_iter_fwd, s->active, s->st_iters_f + (int64_t)i * B,
                                                            s->st_res_f + (int64_t)i * B, s->st_flag_f + (int64_t)i * B,
-                                                           s->nactive, contact ? s->it_base : nullptr, nullptr, nullptr, nullptr);
+                                                           s->nactive, contact ? s->it_base : nullptr, nullptr, nullptr, nullptr,
+                                                           fc.hflag, fc.nact3, fc.seq);
             LAUNCH_CHECK(s);
             if (s->opt.fixed_iter > 0) {
               if (iter >= s->opt.fixed_iter) break;
@@ -1377,6 +1462,7 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
     if (dq_steps) abi_add(s, s->AX, dq_steps + (int64_t)T * n3, B, sstride);
     if (dv_steps) abi_add(s, s->AV, dv_steps + (int64_t)T * n3, B, sstride);
     const bool pcg = s->opt.accel_adj != 0;
+    const bool fuse = s->fuse;
     Nvtx nv_bwd("pd_backward");
     for (int i = T - 1; i >= 0; --i) {
       Nvtx nv_step("backward_step");
@@ -1420,10 +1506,11 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
         // end of the previous PCG iteration (dots[2B:3B]); k_adj_check also commits rz <- rz_new there
         const bool fused_rr = pcg && iter > 0;
         if (!fused_rr) dots(s, B, n3, {{s->Rv, s->Rv}});
+        const FlagArgs fa = flag_args(s, iter < s->opt.max_iter_adj && iter % s->opt.check_every == 0);
         pdl_launch(s, k_adj_check, 1, 256, 0, fused_rr ? s->dots + 2 * B : s->dots, s->bb, B, s->opt.tol_adj, iter,
                                               s->opt.max_iter_adj, s->active, s->st_iters_a + (int64_t)i * B,
                                               s->st_res_a + (int64_t)i * B, s->st_flag_a + (int64_t)i * B, s->nactive,
-                                              fused_rr ? s->rz : nullptr, s->dots + B);
+                                              fused_rr ? s->rz : nullptr, s->dots + B, fa.hflag, fa.nact3, fa.seq);
         LAUNCH_CHECK(s);
         if (iter >= s->opt.max_iter_adj) break;
         if (iter % s->opt.check_every == 0 && read_nactive(s) == 0) break;
@@ -1431,9 +1518,10 @@ static pd_status backward_impl(pd_sim* s, const double* dL_dqT, const double* dL
           apply_AN(s, B, x1, s->Pv, s->Q, act_i, act_bs, s->JC);  // (k_gather zeroes the constrained rows)
           dots(s, B, n3, {{s->Pv, s->Q}}, s->dots + B);
           // u += alpha p, r -= alpha q, alpha = rz / pq (one pass)
-          pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->U, s->Rv, s->Pv, s->Q, s->rz, s->dots + B, len, B, s->active);
+          pdl_launch(s, k_pcg_update, nblk(len), 256, 0, s->U, s->Rv, s->Pv, s->Q, s->rz, s->dots + B, len, B, s->active,
+                                                         fuse ? s->S0 : nullptr, s->d_pos);
           LAUNCH_CHECK(s);
-          apply_Ainv(s, B, s->Rv, s->Z, nullptr, 1.0, 0.0, s->active);
+          apply_Ainv(s, B, fuse ? nullptr : s->Rv, s->Z, nullptr, 1.0, 0.0, s->active);
           dots(s, B, n3, {{s->Rv, s->Z}, {s->Rv, s->Rv}}, s->dots + B);  // rz_new | |r|^2
           // p = z + beta p, beta = rz_new / rz (rz itself is committed by the next k_adj_check)
           pdl_launch(s, k_pcg_dir, nblk(len), 256, 0, s->Pv, s->Z, s->dots + B, s->rz, len, B, s->active);

@@ -2216,6 +2216,23 @@ __global__ void k_lbfgs_axpy(double* __restrict__ Y, const double* __restrict__ 
   }
 }
 
+// Host-visible iteration control: the check kernels publish the three loop counters
+// ([0] sims still searching / adjoint sims running, [1] forward sims running, [2] running sims within 16 tol) to a
+// mapped pinned host word triple, then a sequence number; the host polls the sequence number instead of
+// enqueueing a copy and synchronising the stream.  own: bit k set = slot k is the value computed by this kernel
+// (v0..v2), the other slots are re-read from the device triple written by earlier kernels of the stream.
+__device__ __forceinline__ void publish3(int32_t* hflag, const int32_t* nact3, int seq, int own, int v0, int v1,
+                                         int v2) {
+  if (!hflag) return;
+  volatile int32_t* h = hflag;
+  const volatile int32_t* d = nact3;
+  h[0] = (own & 1) ? v0 : d[0];
+  h[1] = (own & 2) ? v1 : d[1];
+  h[2] = (own & 4) ? v2 : d[2];
+  __threadfence_system();
+  h[3] = seq;
+}
+
 // Armijo backtracking decision per sim.  Near the minimiser g no longer resolves the decrease in fp64;
 // there a step that leaves g unchanged to 1e-13 relative and lowers ||grad g|| is accepted (the oracle's
 // Newton uses the same rule).  After max_trial halvings the step is taken anyway and flagged.
@@ -2225,7 +2242,8 @@ __global__ void k_ls_accept(const double* __restrict__ f, double* __restrict__ f
                             const double* __restrict__ esum, const double* __restrict__ gtd,
                             const double* __restrict__ g2, const double* __restrict__ gn2, double* __restrict__ alpha,
                             int32_t* __restrict__ ls_active, int trial, int max_trial, int32_t* __restrict__ nactive,
-                            int32_t* __restrict__ ls_flag, int B) {
+                            int32_t* __restrict__ ls_flag, int B, int32_t* hflag = nullptr,
+                            const int32_t* nact3 = nullptr, int seq = 0) {
   PDL_ENTRY();
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
@@ -2246,7 +2264,10 @@ __global__ void k_ls_accept(const double* __restrict__ f, double* __restrict__ f
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *nactive = cnt;
+  if (threadIdx.x == 0) {
+    *nactive = cnt;
+    publish3(hflag, nact3, seq, 1, cnt, 0, 0);
+  }
 }
 
 // rho = 1/(s^T y) if the curvature pair is positive, else 0 (pair ignored)
@@ -2369,7 +2390,8 @@ __global__ void k_lbfgs_beta(const double* __restrict__ yr, const double* __rest
 __global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ X, double sgn, double csgn,
                              const double* __restrict__ Vbase, int64_t vstride, const double* __restrict__ c1,
                              const double* __restrict__ c2, int nv, int64_t len, int B,
-                             const int32_t* __restrict__ active) {
+                             const int32_t* __restrict__ active, double* __restrict__ Xn = nullptr,
+                             const double* __restrict__ Xc = nullptr, const double* __restrict__ alpha_ls = nullptr) {
   PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
@@ -2377,7 +2399,38 @@ __global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ 
   if (active && !active[b]) return;
   double v = X[i];
   for (int j = 0; j < nv; ++j) v += csgn * (c1[j * B + b] - (c2 ? c2[j * B + b] : 0.0)) * Vbase[j * vstride + i];
-  Y[i] = sgn * v;
+  const double d = sgn * v;
+  Y[i] = d;
+  // fused first line-search trial (k_axpby's arithmetic: x_trial = 1.0 x + (alpha 1.0) d, alpha = 1 from k_fwd_check)
+  if (Xn) {
+    double t = 1.0 * Xc[i];
+    t += (alpha_ls[b] * 1.0) * d;
+    Xn[i] = t;
+  }
+}
+
+// The first multi-axpy of the two-loop recursion written straight into the solve layout (k_multi_axpy followed by
+// k_to_solve in one pass, same arithmetic per entry): S[pos][3B] = sgn (X + csgn sum_j c1_j V_j) at the node of pos;
+// the columns of inactive sims are zero (their solution is never read: k_from_solve is masked).
+__global__ void k_multi_axpy_solve(double* __restrict__ S, const double* __restrict__ X, double sgn, double csgn,
+                                   const double* __restrict__ Vbase, int64_t vstride, const double* __restrict__ c1,
+                                   const double* __restrict__ c2, int nv, int nfree, int B,
+                                   const int32_t* __restrict__ active, const int32_t* __restrict__ node_of_pos) {
+  PDL_ENTRY();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int R = 3 * B;
+  if (i >= (int64_t)nfree * R) return;
+  const int64_t pos = i / R;
+  const int rr = (int)(i - pos * R);
+  const int b = rr % B;
+  if (active && !active[b]) {
+    S[i] = 0.0;
+    return;
+  }
+  const int64_t src = 3 * (int64_t)node_of_pos[pos] * B + rr;
+  double v = X[src];
+  for (int j = 0; j < nv; ++j) v += csgn * (c1[j * B + b] - (c2 ? c2[j * B + b] : 0.0)) * Vbase[j * vstride + src];
+  S[i] = sgn * v;
 }
 
 // new pair in slot sl: Gm[sl][j] = s_sl^T y_j (da[j]), Gm[j][sl] = s_j^T y_sl (db[j]); rho_sl.
@@ -2386,7 +2439,9 @@ __global__ void k_multi_axpy(double* __restrict__ Y, const double* __restrict__ 
 __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, const double* __restrict__ da,
                              const double* __restrict__ db, int sl, int m, int nv, int B,
                              const int32_t* __restrict__ active, double* __restrict__ f, const double* __restrict__ fn,
-                             double* __restrict__ gg, const double* __restrict__ gn2) {
+                             double* __restrict__ gg, const double* __restrict__ gn2,
+                             double* __restrict__ gamma = nullptr, const double* __restrict__ step = nullptr,
+                             const double* __restrict__ gtd = nullptr) {
   PDL_ENTRY();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || !active[b]) return;
@@ -2396,6 +2451,14 @@ __global__ void k_gram_store(double* __restrict__ Gm, double* __restrict__ rho, 
   }
   const double sy = da[sl * B + b];
   rho[sl * B + b] = sy > 0.0 ? 1.0 / sy : 0.0;
+  // Per-sim scaling of the initial inverse Hessian, H0 = gamma A^{-1}: after the first step of a
+  // solve, s = step * d with d = -gamma A^{-1} grad g, so s^T A s = -step^2 gamma (grad g . d) needs no extra solve,
+  // and gamma <- s^T A s / s^T y is the Rayleigh quotient of the prefactorised A against the sim's true Hessian
+  // along s (sims whose own E differs from the factorised E_ref; A_N below A under large rotations).
+  if (gamma) {
+    const double a = step[b], gd = gtd[b], g0 = gamma[b];
+    if (sy > 0.0 && gd < 0.0) gamma[b] = fmin(16.0, fmax(0.0625, -a * a * g0 * gd / sy));
+  }
   if (f) {
     f[b] = fn[b];
     gg[b] = gn2[b];
@@ -2479,7 +2542,8 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out,
                             int32_t* __restrict__ nactive, const int32_t* __restrict__ iter_base,
                             double* __restrict__ alpha = nullptr, int32_t* __restrict__ ls_act = nullptr,
-                            int32_t* __restrict__ nnear = nullptr) {
+                            int32_t* __restrict__ nnear = nullptr, int32_t* hflag = nullptr,
+                            const int32_t* nact3 = nullptr, int seq = 0) {
   PDL_ENTRY();
   __shared__ int cnt, near;
   if (threadIdx.x == 0) cnt = near = 0;
@@ -2511,6 +2575,9 @@ __global__ void k_fwd_check(const double* __restrict__ dots, int B, double tol, 
   if (threadIdx.x == 0) {
     *nactive = cnt;
     if (nnear) *nnear = near;
+    // (L-BFGS / Newton: nactive = nact3 + 1, nnear = nact3 + 2; plain PD: nactive = nact3)
+    if (nnear) publish3(hflag, nact3, seq, 6, 0, cnt, near);
+    else publish3(hflag, nact3, seq, 1, cnt, 0, 0);
   }
 }
 
@@ -2570,16 +2637,31 @@ __global__ void k_sticky_extra(double* __restrict__ EX, const double* __restrict
 //   k_pcg_dir:    beta = rz_new / rz; P = Z + beta P
 __global__ void k_pcg_update(double* __restrict__ U, double* __restrict__ Rv, const double* __restrict__ P,
                              const double* __restrict__ Q, const double* __restrict__ rz, const double* __restrict__ pq,
-                             int64_t len, int B, const int32_t* __restrict__ active) {
+                             int64_t len, int B, const int32_t* __restrict__ active, double* __restrict__ S = nullptr,
+                             const int32_t* __restrict__ pos_of_node = nullptr) {
   PDL_ENTRY();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= len) return;
   const int b = (int)(i % B);
-  if (!active[b]) return;
+  // the new residual also in the solve layout (fused k_to_solve of the coming z = A^{-1} r); the columns of
+  // converged sims are zero (their solution is never read: k_from_solve is masked)
+  int64_t si = -1;
+  if (S) {
+    const int64_t dof = i / B;
+    const int node = (int)(dof / 3), ax = (int)(dof - 3 * (int64_t)node);
+    const int pos = pos_of_node[node];
+    if (pos >= 0) si = (int64_t)pos * 3 * B + ax * B + b;
+  }
+  if (!active[b]) {
+    if (si >= 0) S[si] = 0.0;
+    return;
+  }
   const double d = pq[b];
   const double alpha = d != 0.0 ? rz[b] / d : 0.0;
   U[i] = U[i] + alpha * P[i];
-  Rv[i] = Rv[i] + (-alpha) * Q[i];
+  const double r = Rv[i] + (-alpha) * Q[i];
+  Rv[i] = r;
+  if (si >= 0) S[si] = r;
 }
 __global__ void k_pcg_dir(double* __restrict__ P, const double* __restrict__ Z, const double* __restrict__ rz_new,
                           const double* __restrict__ rz, int64_t len, int B, const int32_t* __restrict__ active) {
@@ -2596,7 +2678,8 @@ __global__ void k_pcg_dir(double* __restrict__ P, const double* __restrict__ Z, 
 __global__ void k_adj_check(const double* __restrict__ rr, const double* __restrict__ bb, int B, double tol, int iter,
                             int max_iter, int32_t* __restrict__ active, int32_t* __restrict__ iters_out,
                             double* __restrict__ res_out, int32_t* __restrict__ flag_out, int32_t* __restrict__ nactive,
-                            double* __restrict__ rz = nullptr, const double* __restrict__ rz_new = nullptr) {
+                            double* __restrict__ rz = nullptr, const double* __restrict__ rz_new = nullptr,
+                            int32_t* hflag = nullptr, const int32_t* nact3 = nullptr, int seq = 0) {
   PDL_ENTRY();
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
@@ -2616,7 +2699,10 @@ __global__ void k_adj_check(const double* __restrict__ rr, const double* __restr
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *nactive = cnt;
+  if (threadIdx.x == 0) {
+    *nactive = cnt;
+    publish3(hflag, nact3, seq, 1, cnt, 0, 0);
+  }
 }
 
 // a_x = (M/h^2) u - a_v/h ; a_v = (M/h) u ; zero on fixed nodes  (eq:pre_adjoint)

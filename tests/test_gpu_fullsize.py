@@ -218,6 +218,20 @@ def test_c3_long_horizon_vs_oracle_golden(torch):
         _check_golden(inp, gpu, gd, int(b))
 
 
+def test_c3_full_horizon_vs_oracle_golden(torch):
+    # configs[2] over its WHOLE 200-step horizon, all 64 sims in one batch (the bench launch configuration): the
+    # stiffest and the softest sim against the oracle (tools/make_goldens.py c3full) — states every 20 steps through
+    # the soft beam's full swing, gradients of the terminal tip loss back through all 200 steps.
+    gd = _golden("c3full")
+    T = int(gd["steps"])
+    assert T == 200
+    inp = make_inputs(get_config("c3"), steps=T)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    for b in gd["sims"]:
+        _check_golden(inp, gpu, gd, int(b))
+
+
 def test_c4_full_horizon_vs_oracle_golden(torch):
     # configs[3], the whole 150-step contact drop (impact, chatter, settling): active sets bit-exact at every
     # step, states every 10 steps, gradients of the terminal loss.

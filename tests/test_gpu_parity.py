@@ -286,6 +286,30 @@ def test_k3_switches_match_direct(torch, monkeypatch, env, name, batch):
         assert rel(out[b], ref) <= 1e-12
 
 
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+@pytest.mark.parametrize("env", [{"PD_POLL": "0"}, {"PD_FUSE": "0"}, {"PD_POLL": "0", "PD_FUSE": "0"}])
+def test_orchestration_switches_bitwise(torch, monkeypatch, env, name):
+    # Iteration control by polled host flags (PD_POLL) and the fused layout / first-trial passes
+    # (PD_FUSE) change how the same kernels' results are produced and read, not a single bit of them: trajectory,
+    # iteration counts, active sets and every gradient equal the copy + synchronise / separate-pass path exactly
+    # (c3s: per-sim E, sims converge at different iterations; c5s: contact + muscle).  Switches are read at pd_create.
+    inp = make_inputs(get_config(name))
+    kw = dict(contact_nodes=inp["contact_nodes"]) if name == "c5s" else {}
+    kw.update(accel_fwd=1, outer_warm=1)
+    ref = _run_gpu(torch, inp, _sim(inp, **kw))
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    alt_sim = _sim(inp, **kw)
+    alt = _run_gpu(torch, inp, alt_sim)
+    for k in ("q", "v", "dq0", "dv0", "dfext", "dE", "dnu"):
+        assert np.array_equal(ref[k], alt[k]), k
+    if ref["dact"] is not None:
+        assert np.array_equal(ref["dact"], alt["dact"])
+    for k in ("iters_fwd", "iters_adj"):
+        a, b = ref["st" if k == "iters_fwd" else "sb"][k], alt["st" if k == "iters_fwd" else "sb"][k]
+        assert np.array_equal(np.asarray(a), np.asarray(b)), k
+
+
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
 def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, tol_fwd=2e-14, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for

@@ -7,6 +7,8 @@ method's arithmetic) — nothing here imports or runs the CUDA path.  Rerun with
     python tools/make_goldens.py c3      # config c3, stiffest + softest sim, first 30 steps
     python tools/make_goldens.py c4      # config c4, the whole 150-step contact drop
     python tools/make_goldens.py c2      # config c2, the whole 100-step cantilever (4131 DoF)
+    python tools/make_goldens.py c3full  # config c3, stiffest + softest sim, the whole 200-step horizon
+    python tools/make_goldens.py c5long  # config c5, sim 0, first 4 steps (about 40 min on 8 host cores)
 
 What is stored per sim: the states of every `every`-th step and of the last step (q, v), the Alg. 1 active
 sets of every step, the per-step oracle statistics, and the gradients of the config's loss at the last
@@ -34,6 +36,10 @@ SPECS = {
     "c3": ("c3", 30, None, 1e-13, "newton", "direct", 5),
     "c4": ("c4", 150, [0], 2e-14, "newton", "direct", 10),
     "c2": ("c2", 100, [0], 1e-13, "newton", "direct", 10),
+    # the whole 200-step horizon of configs[2] (stiffest + softest sim): the soft beam's full swing
+    "c3full": ("c3", 200, None, 1e-13, "newton", "direct", 20),
+    # a longer c5 prefix (sim 0, 4 steps: the contact set changes again after the first impact steps)
+    "c5long": ("c5", 4, [0], 1e-13, "newton_pcg", "pcg", 1),
 }
 
 
