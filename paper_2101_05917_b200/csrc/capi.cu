@@ -58,7 +58,7 @@ struct pd_sim {
   int nsm = 148;     // SMs of the device
   int k3_nbuf = 2;  // K3 item ring depth (2..4, env PD_K3_NBUF)
   bool poll = true;  // iteration control by polled host flags (env PD_POLL=0: D2H copy + stream synchronisation)
-  bool lb_gamma = false;  // per-sim scaling gamma_b of H0 = gamma A^{-1} in the L-BFGS forward (env PD_LBFGS_GAMMA)
+  bool lb_gamma = true;  // per-sim scaling gamma_b of H0 = gamma A^{-1} in the L-BFGS forward (env PD_LBFGS_GAMMA=0: 1)
   double* gamma = nullptr;
   bool fuse = true;  // layout/trial passes fused into their producers (env PD_FUSE=0: separate passes, same bits)
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)

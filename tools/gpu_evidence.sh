@@ -4,8 +4,10 @@
 T=${1:-r2}
 mkdir -p gpurun_out profiles
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/${T}_smi.txt 2>&1
+if [ -z "$SKIP_TESTS" ]; then  # (SKIP_TESTS=1: the GPU test suite is run by a separate call, tools/gpu_tests.sh)
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${T}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -n 3 gpurun_out/${T}_pytest_gpu.log
+fi
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"; tail -n 1 gpurun_out/${T}_smoke.log
 timeout 1500 python bench.py --steps 2 --warmup 3 > gpurun_out/${T}_bench_c5.json 2> gpurun_out/${T}_bench_c5.err; echo "bench c5 rc=$?"
 timeout 900 python bench.py --config c3 --steps 2 --warmup 3 > gpurun_out/${T}_bench_c3.json 2> gpurun_out/${T}_bench_c3.err; echo "bench c3 rc=$?"

@@ -38,6 +38,9 @@ SPECS = {
     "c2": ("c2", 100, [0], 1e-13, "newton", "direct", 10),
     # the whole 200-step horizon of configs[2] (stiffest + softest sim): the soft beam's full swing
     "c3full": ("c3", 200, None, 1e-13, "newton", "direct", 20),
+    # the softest c3 sim up to step 160, with the gradients of the tip loss at that horizon: the part of its swing
+    # on which the minimiser of g is unique (reading 2.20; tools/c3_branch_probe.py)
+    "c3soft160": ("c3", 160, [53], 1e-13, "newton", "direct", 20),
     # a longer c5 prefix (sim 0, 4 steps: the contact set changes again after the first impact steps)
     "c5long": ("c5", 4, [0], 1e-13, "newton_pcg", "pcg", 1),
 }
