@@ -172,10 +172,13 @@ def _golden(key):
     return dict(np.load(path, allow_pickle=False))
 
 
-def _check_golden(inp, gpu, gd, b, sets=None, vel_rel_floor=0.0):
-    """States at the stored steps, active sets and Alg. 1 outer counts of every step, gradients at the end."""
+def _check_golden(inp, gpu, gd, b, sets=None, vel_rel_floor=0.0, last_step=None):
+    """States at the stored steps, active sets and Alg. 1 outer counts of every step, gradients at the end.
+    last_step: compare the states up to that step only, and no gradients (the trajectory's unique part)."""
     p = f"s{b}_"
     for k, i in enumerate(gd["keep"]):
+        if last_step is not None and i > last_step:
+            break
         eq = rel(gpu["q"][b, i], gd[p + "q"][k])
         assert eq <= POS_TOL, ("q", b, int(i), eq)
         vo = gd[p + "v"][k]
@@ -184,6 +187,8 @@ def _check_golden(inp, gpu, gd, b, sets=None, vel_rel_floor=0.0):
     if sets is not None and gd[p + "active"].size:
         assert np.array_equal(sets[b], gd[p + "active"]), ("active sets", b)
         assert list(gpu["st"]["contact_outer"][b]) == list(gd[p + "outer"]), ("outer", b)
+    if last_step is not None:
+        return
     for k in ("dq0", "dv0", "dfext"):
         assert rel(gpu[k][b], gd[p + k]) <= GRAD_TOL, (k, b, rel(gpu[k][b], gd[p + k]))
     for k in ("dE", "dnu"):
@@ -192,11 +197,12 @@ def _check_golden(inp, gpu, gd, b, sets=None, vel_rel_floor=0.0):
         assert rel(gpu["dact"][b], gd[p + "dact"]) <= GRAD_TOL, ("dact", b, rel(gpu["dact"][b], gd[p + "dact"]))
 
 
-def test_c5_full_batch_vs_oracle_golden(torch):
+@pytest.mark.parametrize("key", ["c5", "c5long"])
+def test_c5_full_batch_vs_oracle_golden(torch, key):
     # configs[4] at full size in the bench launch configuration (B = 8, 212k DoF, contact + muscle), first 2
-    # steps; sim 0 against the oracle's Newton-PCG / PCG run (tools/make_goldens.py c5): positions, velocities,
-    # bit-exact active sets and outer counts, dL/dq0, dL/dv0, dL/df_ext, dL/dE, dL/dnu, dL/dact.
-    gd = _golden("c5")
+    # (c5) / 4 (c5long) steps; sim 0 against the oracle's Newton-PCG / PCG run (tools/make_goldens.py): positions,
+    # velocities, bit-exact active sets and outer counts, dL/dq0, dL/dv0, dL/df_ext, dL/dE, dL/dnu, dL/dact.
+    gd = _golden(key)
     T = int(gd["steps"])
     inp = make_inputs(get_config("c5"), steps=T)
     sim = _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11)
@@ -219,14 +225,42 @@ def test_c3_long_horizon_vs_oracle_golden(torch):
 
 
 def test_c3_full_horizon_vs_oracle_golden(torch):
-    # configs[2] over its WHOLE 200-step horizon, all 64 sims in one batch (the bench launch configuration): the
-    # stiffest and the softest sim against the oracle (tools/make_goldens.py c3full) — states every 20 steps through
-    # the soft beam's full swing, gradients of the terminal tip loss back through all 200 steps.
+    # configs[2] over its WHOLE 200-step horizon, all 64 sims in one batch (the bench launch configuration), against
+    # the oracle (tools/make_goldens.py c3full): states every 20 steps, gradients of the terminal tip loss back
+    # through all 200 steps.
+    # * Each step is solved to 1e-13 here (the golden's own tolerance; 1e-12 elsewhere): the per-step solver error is
+    #   carried and added up by the barely damped swing, and at 1e-12 the soft beam's velocities reach 2.4e-9 relative
+    #   by step 120 (positions stay within the bar), measured on the B200.
+    # * The stiffest sim is compared in full.  The softest sim's objective g has TWO local minimisers at step 177
+    #   (reading 2.20): the oracle's Newton route (the golden) and its literal local-global PD route agree to
+    #   1e-12 up to step 176 and then separate by 6e-4 (tools/c3_branch_probe.py, oracle only).  All three GPU routes
+    #   follow the PD route's branch.  So what is unique is compared — the golden up to step 160 here, and with
+    #   gradients at a 160-step horizon in the next test — and beyond it the GPU must reproduce the oracle's PD route
+    #   (oracle_c3full_pdbranch.npz) at step 180.  (The oracle's literal PD route stops converging at step 186 — its
+    #   stagnation exit, residual 7e-6 — so there is no reference for the soft sim's last 15 steps.)
     gd = _golden("c3full")
+    br = _golden("c3full_pdbranch")
     T = int(gd["steps"])
     assert T == 200
     inp = make_inputs(get_config("c3"), steps=T)
-    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-12, tol_adj=1e-11))
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-13, tol_adj=1e-12))
+    assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
+    soft = int(br["sim"])
+    assert soft in [int(b) for b in gd["sims"]] and int(br["first_separated_step"]) > int(br["start"])
+    for b in gd["sims"]:
+        _check_golden(inp, gpu, gd, int(b), last_step=int(br["start"]) if int(b) == soft else None)
+    for k, i in enumerate(br["steps"]):
+        assert rel(gpu["q"][soft, i], br["q"][k]) <= POS_TOL, ("q", soft, int(i), rel(gpu["q"][soft, i], br["q"][k]))
+        assert rel(gpu["v"][soft, i], br["v"][k]) <= POS_TOL, ("v", soft, int(i), rel(gpu["v"][soft, i], br["v"][k]))
+
+
+def test_c3_soft_sim_160_steps_vs_oracle_golden(torch):
+    # The softest c3 sim (full 64-sim batch) over the 160 steps on which its minimiser is unique, with the gradients
+    # of the tip loss at that horizon (tools/make_goldens.py c3soft160); per-step tolerance as in the test above.
+    gd = _golden("c3soft160")
+    T = int(gd["steps"])
+    inp = make_inputs(get_config("c3"), steps=T)
+    gpu = _run(torch, inp, _bench_sim(inp, tol_fwd=1e-13, tol_adj=1e-12))
     assert gpu["st"]["n_nonconverged"] == 0 and gpu["sb"]["n_nonconverged"] == 0
     for b in gd["sims"]:
         _check_golden(inp, gpu, gd, int(b))
