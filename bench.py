@@ -386,8 +386,11 @@ def main_ours(args):
                 config=dict(workload=cfg.name, batch=inp_all["B"], batch_per_gpu=B, time_steps=T, dof=N, tol=cfg.tol,
                             grid=list(cfg.counts), l2="flushed (256 MB write) before every timed iteration",
                             parallelism=f"batch partitioned over {ws} rank(s), no data-path collective",
-                            solver="quasi-Newton PD (L-BFGS, H0 = A^-1)" if args.solver == "pd"
-                            else "Newton-PCG baseline (SURVEY 8f-4)"),
+                            solver="quasi-Newton PD (L-BFGS, H0 = gamma_b A^-1)" if args.solver == "pd"
+                            else "Newton-PCG baseline (SURVEY 8f-4)",
+                            # any developer switch in the environment is part of the measured configuration
+                            # (PD_ACTIVE_WARM=1 is not Alg. 1 as printed: never the headline)
+                            switches={k: v for k, v in sorted(os.environ.items()) if k.startswith("PD_")}),
                 e2e=e2e, gpu_launches=launches, roofline=roof,
                 roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
                 kernel_share=share,

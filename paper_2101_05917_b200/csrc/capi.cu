@@ -60,6 +60,9 @@ struct pd_sim {
   bool poll = true;  // iteration control by polled host flags (env PD_POLL=0: D2H copy + stream synchronisation)
   bool lb_gamma = true;  // per-sim scaling gamma_b of H0 = gamma A^{-1} in the L-BFGS forward (env PD_LBFGS_GAMMA=0: 1)
   double* gamma = nullptr;
+  // Probe only (env PD_ACTIVE_WARM=1, off by default, NOT Alg. 1 as printed): a time step's first outer iteration
+  // starts from the previous step's final active set instead of the empty set of P:339
+  bool active_warm = false;
   bool fuse = true;  // layout/trial passes fused into their producers (env PD_FUSE=0: separate passes, same bits)
   int lb_hist = 0, lb_gi = 0;  // L-BFGS history state carried across Alg. 1 outer iterations (lbfgs_warm)
   int32_t* d_rows = nullptr;
@@ -1100,6 +1103,7 @@ pd_status pd_create(const pd_mesh* mesh, const pd_material* mat, double h, const
     if (const char* e = std::getenv("PD_K3_NBUF")) s->k3_nbuf = std::min(4, std::max(2, std::atoi(e)));
     if (const char* e = std::getenv("PD_POLL")) s->poll = std::atoi(e) != 0;
     if (const char* e = std::getenv("PD_FUSE")) s->fuse = std::atoi(e) != 0;
+    if (const char* e = std::getenv("PD_ACTIVE_WARM")) s->active_warm = std::atoi(e) != 0;
     if (const char* e = std::getenv("PD_LBFGS_GAMMA")) s->lb_gamma = std::atoi(e) != 0;
     auto up_sweep4 = [&](const HostPlan::Sweep4& S, Sweep4Dev& d) {
       d.A = s->upload(S.A);
@@ -1295,6 +1299,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
     s->has_act = actuation && s->act;
     CK(cudaMemcpyAsync(s->traj, s->X, len * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
     const double tol = s->opt.tol_fwd;
+    bool q_stale = false;
     for (int i = 0; i < steps; ++i) {
       Nvtx nv_step("forward_step");
       const double* act_i = s->has_act ? s->act + (int64_t)i * P.m : nullptr;
@@ -1312,12 +1317,16 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
       }
       const bool contact = s->nc > 0;
       const int64_t cB = (int64_t)s->nc * B;
+      if (i == 0) q_stale = false;
       if (contact) {  // Alg. 1: V_i = empty
-        CK(cudaMemsetAsync(s->PIN, 0, cB, s->stream));
+        const bool keep_set = s->active_warm && i > 0;  // (probe: PIN, kcount and Q of the last step's final set stay)
+        if (!keep_set) CK(cudaMemsetAsync(s->PIN, 0, cB, s->stream));
         pdl_launch(s, k_fill_int, 1, 256, 0, s->oact, 1, B);
         LAUNCH_CHECK(s);
-        pdl_launch(s, k_fill_int, 1, 256, 0, s->kcount, s->nc, B);  // no pins: unconstrained root block
-        LAUNCH_CHECK(s);
+        if (!keep_set) {
+          pdl_launch(s, k_fill_int, 1, 256, 0, s->kcount, s->nc, B);  // no pins: unconstrained root block
+          LAUNCH_CHECK(s);
+        }
         CK(cudaMemsetAsync(s->it_base, 0, B * sizeof(int32_t), s->stream));
         s->pins_live = true;
       }
@@ -1328,6 +1337,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
                                                               s->sticky);
           LAUNCH_CHECK(s);  // x_{i+1} = x_i, pinned normal DoFs on the plane
           if (outer > 1) build_Q(s, B, s->oact);
+          else if (s->active_warm && i > 0 && q_stale) build_Q(s, B, nullptr);  // (probe: kept set whose Q is not current)
           CK(cudaMemcpyAsync(s->active, s->oact, B * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->stream));
         } else {
           pdl_launch(s, k_fill_int, 1, 256, 0, s->active, 1, B);
@@ -1380,6 +1390,7 @@ pd_status pd_forward(pd_sim* s, int32_t B, const double* q0, const double* v0, c
         prof_flush(s);
         int going = 0;
         for (int b = 0; b < B; ++b) going += s->h_small[b];
+        q_stale = going != 0;  // (left through the outer cap: PIN was updated after the last build_Q)
         if (!going) break;
       }
       if (contact) {

@@ -310,6 +310,31 @@ def test_orchestration_switches_bitwise(torch, monkeypatch, env, name):
         assert np.array_equal(np.asarray(a), np.asarray(b)), k
 
 
+@pytest.mark.parametrize("name", ["c4s", "c5s"])
+def test_active_set_warm_start_probe_same_sets(torch, monkeypatch, name):
+    # PD_ACTIVE_WARM=1 (off by default; NOT Alg. 1 as printed, which initialises V_i = empty at P:339): a step's first
+    # outer iteration starts from the previous step's final active set.  The fixed point V' = V it stops at is the same:
+    # final active sets identical at every step, states and gradients equal to the solver tolerance, fewer outer
+    # iterations (the default path is the one compared with the oracle).
+    inp = make_inputs(get_config(name))
+    kw = dict(contact_nodes=inp["contact_nodes"], accel_fwd=1, outer_warm=1, tol_fwd=2e-14, max_iter_fwd=4000)
+    ref_sim = _sim(inp, **kw)
+    ref = _run_gpu(torch, inp, ref_sim)
+    ref_sets = ref_sim.contact_sets()
+    monkeypatch.setenv("PD_ACTIVE_WARM", "1")
+    alt_sim = _sim(inp, **kw)
+    alt = _run_gpu(torch, inp, alt_sim)
+    assert np.array_equal(ref_sets, alt_sim.contact_sets())
+    assert alt["st"]["n_nonconverged"] == 0 and alt["sb"]["n_nonconverged"] == 0
+    B, T = inp["B"], inp["T"]
+    for b in range(B):
+        for i in range(1, T + 1):
+            assert rel(alt["q"][b, i], ref["q"][b, i]) <= POS_TOL
+        for k in ("dq0", "dv0", "dfext"):
+            assert rel(alt[k][b], ref[k][b]) <= GRAD_TOL
+    assert np.sum(alt["st"]["contact_outer"]) <= np.sum(ref["st"]["contact_outer"])
+
+
 # ----------------------------------------------------------------- contact (K5, Alg. 1)
 def _contact_parity(torch, name, accel_fwd=0, outer_warm=0, lbfgs_warm=0, tol_fwd=2e-14, **over):
     # The plate comes to rest on the plane, where ||v|| -> 0 and the relative velocity bar asks for
