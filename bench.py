@@ -393,6 +393,9 @@ def main_ours(args):
                             switches={k: v for k, v in sorted(os.environ.items()) if k.startswith("PD_")}),
                 e2e=e2e, gpu_launches=launches, roofline=roof,
                 roofline_k3=roof_of("solve_K3"), roofline_k1=roof_of("local_K1"),
+                # the launch durations are CUDA-event times of a 1-in-N sample of each family's launches inside the
+                # timed region (N = PD_PROF_EVERY, default 4; an event boundary interrupts the PDL chain)
+                profile_sampling=f"1 in {os.environ.get('PD_PROF_EVERY', '4')} launches per kernel family",
                 kernel_share=share,
                 # per-sim means and, since the batch loop runs until its slowest sim converges, the mean over steps
                 # of the per-step maximum over sims (what the batch actually pays)
